@@ -1,0 +1,388 @@
+"""Plan-search benchmark: candidate plans evaluated / s and wall-time to the best plan.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1|3|4|5] [--impl ours|reference]
+
+A step = one complete solve of the configured workload (config 1: the exhaustive
+search of all 3.25e10 candidates of the paper workload; sampled configs: a fixed
+candidate budget), sharded over the ranks, combined with an NCCL all-reduce MIN.
+Rank 0 prints one JSON line.  `--impl reference` times the CPU oracle port
+(oracle/oracle.c, OpenMP on every host thread) on a bounded sample of the same
+workload -- the reference's own solver does not exist.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+L2_FLUSH_BYTES = 256 << 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=1, choices=[1, 3, 4, 5])
+    ap.add_argument("--budget", type=int, default=0, help="sampled configs: candidates per step")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=8.0, help="CPU baseline sample length")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 4 + i and "Active" in s[4 + i]
+                          and "Not" not in s[4 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- workload
+def workload(cfg: int, budget: int):
+    from paper_2311_02840_b200.problem import SolveOptions
+    from paper_2311_02840_b200.workloads import CONFIGS, config_workload
+
+    w, t, c = config_workload(cfg)
+    if cfg == 1:
+        opts = SolveOptions()                                   # exhaustive, tree kernel
+    else:
+        default = {3: 1 << 27, 4: 1 << 26, 5: 1 << 26}[cfg]
+        opts = SolveOptions(search="sampled", budget=budget or default, seed=7)
+    return w, t, c, opts
+
+
+def dist_setup(n_gpus: int):
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ----------------------------------------------------------------------------- CPU baseline
+def cpu_baseline(cfg: int, seconds: float, w, t, opts):
+    """C oracle port on every host thread over a bounded prefix (or sample) of the workload."""
+    from oracle import coracle, saturn_oracle
+
+    op = saturn_oracle.build(t.entries, w)
+    cp = coracle.CProblem(op)
+    threads = os.cpu_count() or 1
+    src = "index" if cfg == 1 else "substream"
+    n = 20000
+    while True:
+        t0 = time.perf_counter()
+        cp.search(src, opts.seed, 0, n, threads)
+        dt = time.perf_counter() - t0
+        if dt > 0.5 or n > 1 << 34:
+            break
+        n *= 4
+    rate = n / dt
+    n2 = max(n, int(rate * seconds))
+    t0 = time.perf_counter()
+    cp.search(src, opts.seed, 0, n2, threads)
+    dt2 = time.perf_counter() - t0
+    return {"value": n2 / dt2, "unit": "plans/s", "cores": threads, "kind": "port",
+            "sample": f"{'first' if cfg == 1 else 'substream(7, i) for i <'} {n2} candidates of config {cfg} "
+                      f"({dt2:.1f} s, oracle/oracle.c literal per-GPU list scheduler, OpenMP)"}
+
+
+def python_baseline(cfg: int, w, t, opts, seconds: float = 3.0):
+    """Pure-Python oracle (the reference's language), 1 core, for context."""
+    from oracle import saturn_oracle
+
+    op = saturn_oracle.build(t.entries, w)
+    src = "index" if cfg == 1 else "substream"
+    n, t0 = 0, time.perf_counter()
+    step = 500
+    while time.perf_counter() - t0 < seconds:
+        saturn_oracle.search(op, src, opts.seed, n, n + step)
+        n += step
+    return {"value": n / (time.perf_counter() - t0), "unit": "plans/s", "cores": 1, "kind": "port",
+            "sample": f"first {n} candidates, oracle/saturn_oracle.py"}
+
+
+def run_reference(args):
+    rank, world, _ = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), 0
+    if rank != 0:
+        return
+    w, t, c, opts = workload(args.config, args.budget)
+    from oracle import coracle, saturn_oracle
+
+    op = saturn_oracle.build(t.entries, w)
+    cp = coracle.CProblem(op)
+    threads = os.cpu_count() or 1
+    src = "index" if args.config == 1 else "substream"
+    # calibrate a per-step sample of ~`per_step` seconds so K+W steps finish in minutes
+    per_step = min(15.0, 150.0 / max(1, args.steps + args.warmup))
+    n = 20000
+    while True:
+        t0 = time.perf_counter()
+        cp.search(src, opts.seed, 0, n, threads)
+        dt = time.perf_counter() - t0
+        if dt > 0.3 or n > 1 << 34:
+            break
+        n *= 4
+    n_step = max(n, int(n / dt * per_step))
+    for i in range(args.warmup):
+        cp.search(src, opts.seed, 0, max(1, n_step // 10), threads)
+    times = []
+    for i in range(args.steps):
+        t0 = time.perf_counter()
+        cp.search(src, opts.seed, i * n_step, (i + 1) * n_step, threads)
+        times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    value = n_step * args.steps / tot
+    line = {
+        "impl": "reference", "metric": "candidate plans evaluated/sec", "value": value, "unit": "plans/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "int32" if opts.time_mode == "grid" else "f64", "data": "synthetic",
+        "config": {"workload": c["name"], "sample_per_step": n_step},
+        "cpu_baseline": {"value": value, "unit": "plans/s", "cores": threads, "kind": "port",
+                         "sample": f"{n_step} candidates per step ({src} order) of {c['name']}, oracle/oracle.c, "
+                                   f"OpenMP {threads} threads"},
+        "e2e": {"value": value, "unit": "plans/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "time_to_best_s_extrapolated": (op.space / value) if args.config == 1 else None,
+    }
+    print(json.dumps(line))
+
+
+# ----------------------------------------------------------------------------- ours
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    from paper_2311_02840_b200 import engine as EN
+    from paper_2311_02840_b200 import planners
+    from paper_2311_02840_b200.problem import build_problem
+
+    rank, world, local = dist_setup(args.gpus)
+    group = None
+    w, t, c, opts = workload(args.config, args.budget)
+    eng = planners.get_engine(local)
+    prob = build_problem(t, w, opts)
+    mode, n_idx = eng.plan_search(prob, opts)
+    idx_bits, _ = prob.key_bits(n_idx)
+    nprob = EN.NativeProblem(prob, idx_bits)
+    use_tree = mode == "exhaustive" and eng._tree_ok(prob)
+    if use_tree:
+        info = eng.tree_plan(nprob)
+        a, b = EN._shard(info.n_tasks, rank, world)
+        n_cand = info.n_candidates
+        leaves = info.n_candidates
+        merges = info.n_job_steps - info.n_candidates
+        kernel_name = "k_tree"
+    else:
+        a, b = EN._shard(n_idx, rank, world)
+        n_cand = n_idx
+        kernel_name = "k_generic"
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device="cuda")
+    best = eng.reset_best()
+
+    def device_step():
+        eng.reset_best(best)
+        if use_tree:
+            eng.search_tree(nprob, info.prefix_len, a, b, best)
+        elif mode == "exhaustive":
+            eng.search_index(nprob, a, b, best)
+        else:
+            eng.search_sampled(nprob, EN.SRC_SUBSTREAM, opts.seed, a, b, best)
+
+    for _ in range(args.warmup):
+        device_step()
+        EN._combine(best, nprob.grid, group, world)
+    torch.cuda.synchronize()
+
+    # ---- device-resident timed region: K steps, L2 flushed between steps ----
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = eng.launches
+    keys = []
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()
+            e0, e1, e2 = ev[i]
+            e0.record(stream)
+            device_step()
+            e1.record(stream)
+            keys.append(EN._combine(best, nprob.grid, group, world))
+            e2.record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    launches = eng.launches - launches0
+    step_s = [e0.elapsed_time(e2) / 1e3 for e0, _, e2 in ev]
+    kern_s = [e0.elapsed_time(e1) / 1e3 for e0, e1, _ in ev]
+    t_local = sum(step_s)
+    t_max = max_over_ranks(t_local, world)
+    kern_avg = max_over_ranks(sum(kern_s) / len(kern_s), world)
+    value = n_cand * args.steps / t_max
+    key = keys[-1]
+    assert all(k == key for k in keys), "non-deterministic search result"
+    ms = key[0] >> idx_bits if nprob.grid else None
+
+    # ---- e2e: the public API with host inputs (marshal, launch, NCCL, decode, check) ----
+    e2e_times = []
+    barrier(world)
+    for i in range(max(2, min(args.steps, 5))):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        sol = planners.solve(t, w, None, opts, group=group)
+        torch.cuda.synchronize()
+        e2e_times.append(time.perf_counter() - t0)
+    e2e_s = max_over_ranks(statistics.median(e2e_times[1:]), world)
+    h2d = nprob.param_bytes + 8                    # tables packed into the launch + decode id
+    d2h = 16 + 3 * 4 * prob.J + 8                  # best key + winner schedule (option, node, start) + makespan
+
+    # ---- roofline: INT32 min/max issue rate measured on this GPU ----
+    ops = torch.zeros(1, dtype=torch.int64, device="cuda")
+    sink = torch.zeros(1, dtype=torch.int32, device="cuda")
+    blocks, iters = eng.sm_count * 8, 4096
+    eng.lib.sat_alu_probe(blocks, 256, iters, EN._vp(ops.data_ptr()), EN._vp(sink.data_ptr()),
+                          EN._vp(stream.cuda_stream))
+    torch.cuda.synchronize()
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    p0.record(stream)
+    eng.lib.sat_alu_probe(blocks, 256, iters, EN._vp(ops.data_ptr()), EN._vp(sink.data_ptr()),
+                          EN._vp(stream.cuda_stream))
+    p1.record(stream)
+    torch.cuda.synchronize()
+    peak_ops = int(ops.item()) / (p0.elapsed_time(p1) / 1e3)
+    G, N = prob.G, prob.N
+    if use_tree:
+        # algorithmic INT32 work of the prefix-shared walk:
+        #   internal placement: node pick (N) + 2G slot min/max + add + makespan max = N + 2G + 2
+        #   leaf placement (last job, no state update): node pick + add + max = N + 2
+        per_launch_ops = (merges // world) * (N + 2 * G + 2) + (leaves // world) * (N + 2)
+    else:
+        per_launch_ops = (n_cand // world) * prob.J * (N + 2 * G + 2)
+    achieved = per_launch_ops / kern_avg
+
+    line = {
+        "metric": "candidate plans evaluated/sec", "value": value, "unit": "plans/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps,
+        "higher_is_better": True, "scaling": "strong" if args.config == 1 else "strong",
+        "vs_baseline": None, "dtype": "int32" if nprob.grid else "f64", "data": "synthetic",
+        "config": {"workload": c["name"], "jobs": prob.J, "nodes": prob.N, "gpus_per_node": int(prob.node_gpus[0]),
+                   "search": mode, "candidates_per_step": n_cand, "kernel": kernel_name,
+                   "radix": [int(r) for r in prob.radix], "delta_s": prob.delta,
+                   "l2": "256 MiB flush between steps, outside step events; working set = launch params",
+                   "parallelism": f"candidate-space shards x{world}, NCCL all-reduce MIN"},
+        "best": {"makespan_intervals": ms, "index": key[0] & ((1 << idx_bits) - 1) if nprob.grid else key[1],
+                 "predicted_makespan_s": (ms * prob.delta) if ms is not None else None},
+        "time_to_best_s": t_max / args.steps,
+        "e2e": {"value": n_cand / e2e_s, "unit": "plans/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "solve_wall_s": e2e_s, "api": "paper_2311_02840_b200.planners.solve (plan_saturn)"},
+        "gpu_launches": launches,
+        "kernel_ms": 1e3 * kern_avg,
+        "roofline": {"bound": "int32-alu", "achieved": achieved / 1e12, "peak": peak_ops / 1e12, "unit": "TOP/s",
+                     "frac": achieved / peak_ops, "traffic": None,
+                     "peak_source": "measured: sat_alu_probe IMNMX chains on this GPU (MEASURED_PEAKS.json has "
+                                    "no INT32 figure)",
+                     "algorithmic_ops_per_launch": per_launch_ops},
+        "clocks": clk.summary(),
+    }
+    if use_tree:
+        line["config"]["prefix_len"] = info.prefix_len
+        line["config"]["walk_placements"] = info.n_job_steps
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args.config, args.cpu_seconds, w, t, opts)
+        line["cpu_baseline_python"] = python_baseline(args.config, w, t, opts)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,148 @@
+/*
+ * saturn_engine.h -- C ABI of the B200 plan-search engine (libsaturn_b200.so).
+ *
+ * The engine replaces the Solver's plan search of the reference
+ * (arXiv 2311.02840 "Saturn"; reference package /root/reference/pkg/src/jointsched):
+ *
+ *   sat_search_tree / sat_search_index
+ *       replace branch_and_bound + solve_lp_relaxation (milp/__init__.py:6,
+ *       SPEC.md:201-214) and brute_force_schedule (milp/__init__.py:3,
+ *       SPEC.md:219-227): exhaustive search of (option per job) x (submission
+ *       order), each candidate list-scheduled to its makespan (the SPEC.md:213
+ *       "list-schedule earliest-fit"), best = lowest (makespan, index).
+ *   sat_search_sampled
+ *       replaces plan_random's draws (rng.py:20-56): candidate
+ *       i is decoded from SplitMix64 substream(seed, i) or SplitMix64(seed + i).
+ *   sat_schedule
+ *       replaces decode_plan (milp/__init__.py:4) and the
+ *       evaluation of fixed plans (plan_optimus / plan_current_practice,
+ *       SPEC.md:285-320): per-job option, node and start of given candidates.
+ *
+ * Conventions
+ *   - Problem tables (sat_problem_t) are HOST pointers, read during the call
+ *     and packed into the launch; nothing is retained after return.
+ *   - Outputs and workspaces are DEVICE pointers owned by the caller.
+ *   - Every call is asynchronous on `stream` (a cudaStream_t, NULL = legacy
+ *     default stream) and reentrant: no globals, one call per stream.
+ *   - Returns SAT_OK or an error code; sat_error_string() explains it.
+ *   - Results accumulate: *d_best is min-combined with what it already holds,
+ *     so shards of one search can be issued back to back; sat_best_reset()
+ *     initialises it.  Grid mode: d_best->hi = (makespan << idx_bits) | index.
+ *     Float mode: d_best->hi = bit pattern of the fp64 makespan (positive
+ *     doubles order like unsigned integers), d_best->lo = index.
+ */
+#ifndef SATURN_ENGINE_H
+#define SATURN_ENGINE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SAT_ABI_VERSION 1
+
+/* status codes (mapped to reference errors.py classes by the host layer) */
+#define SAT_OK              0
+#define SAT_ERR_INVALID     1  /* bad shapes / arguments        -> InvariantViolation (errors.py:8) */
+#define SAT_ERR_NO_OPTIONS  2  /* a job with zero options       -> NoFeasibleConfig   (errors.py:23) */
+#define SAT_ERR_TOO_LARGE   3  /* index / key / table overflow  -> TooLarge           (errors.py:84) */
+#define SAT_ERR_UNSUPPORTED 4  /* shape outside this kernel     -> TooLarge                       */
+#define SAT_ERR_CUDA        5  /* CUDA launch / runtime failure -> PlanFailure / ReplanFailure     */
+
+/* time modes */
+#define SAT_TIME_GRID_I32 0    /* int32 interval durations d = ceil(T / delta) */
+#define SAT_TIME_F64      1    /* float64 seconds, adds and max only: bit-exact vs CPU      */
+
+/* candidate sources */
+#define SAT_SRC_INDEX     0    /* index = c * J! + p             */
+#define SAT_SRC_SUBSTREAM 1    /* candidate i <- SplitMix64 substream(seed, i) (rng.py:51) */
+#define SAT_SRC_SEED      2    /* candidate i <- SplitMix64(seed + i): plan_random(seed+i) */
+#define SAT_SRC_EXPLICIT  3    /* candidate i <- caller arrays options[i][J], order[i][J]  */
+
+#define SAT_MAX_JOBS   64
+#define SAT_MAX_LANES  32      /* N nodes x G padded GPUs per node must fit one warp */
+
+typedef struct sat_problem {
+    int32_t J;              /* jobs (job axis = jobs sorted by id)                         */
+    int32_t N;              /* nodes                                                       */
+    int32_t G;              /* padded GPU slots per node: power of two >= max gpu_count   */
+    int32_t Cmax;           /* row stride of the option tables                             */
+    int32_t time_mode;      /* SAT_TIME_*                                                   */
+    int32_t idx_bits;       /* grid mode: bits of the key holding the candidate index      */
+    const int32_t  *radix;        /* [J]            options per job (>= 1)                 */
+    const int32_t  *gpus;         /* [J*Cmax]       gang size g of option (j, o)           */
+    const uint32_t *node_mask;    /* [J*Cmax]       bit n: option runnable on node n       */
+    const int32_t  *dur_i32;      /* [J*Cmax*N]     grid durations (grid mode)             */
+    const double   *dur_f64;      /* [J*Cmax*N]     seconds (float mode)                   */
+    const int32_t  *node_gpus;    /* [N]            GPUs per node (<= G)                   */
+    const int32_t  *release_i32;  /* [J] or NULL    earliest start per job                 */
+    const double   *release_f64;  /* [J] or NULL                                           */
+    const int32_t  *init_free_i32;/* [N*G] or NULL  ascending per-node GPU free times      */
+    const double   *init_free_f64;/* [N*G] or NULL                                         */
+} sat_problem_t;
+
+typedef struct sat_best {
+    uint64_t hi;
+    uint64_t lo;
+} sat_best_t;
+
+typedef struct sat_tree_info {
+    int32_t  prefix_len;    /* P: jobs fixed per lane; the other J-P are enumerated per warp */
+    int32_t  n_sets;        /* C(J, P) prefix job sets                                       */
+    uint64_t n_tasks;       /* warp tasks (32 prefixes of one set each)                      */
+    uint64_t n_candidates;  /* = prod(radix) * J!                                            */
+    uint64_t n_job_steps;   /* list-scheduling placements the prefix-shared walk performs    */
+} sat_tree_info_t;
+
+int         sat_abi_version(void);
+const char *sat_error_string(int status);
+
+/* device facts (sm count, compute capability) for launch sizing and reporting */
+int sat_device_info(int device, int32_t *sm_count, int32_t *cc_major, int32_t *cc_minor);
+
+/* *d_best <- "empty" (all ones) */
+int sat_best_reset(sat_best_t *d_best, void *stream);
+
+/* Workspace bytes needed by sat_search_index / sat_search_sampled / sat_schedule. */
+int sat_workspace_bytes(const sat_problem_t *p, size_t *bytes);
+
+/* Exhaustive search, per-candidate decode, candidates [lo, hi) of the index space. */
+int sat_search_index(const sat_problem_t *p, uint64_t lo, uint64_t hi,
+                     sat_best_t *d_best, void *d_ws, size_t ws_bytes, void *stream);
+
+/* Sampled search: candidates [lo, hi) of source SAT_SRC_SUBSTREAM / SAT_SRC_SEED. */
+int sat_search_sampled(const sat_problem_t *p, int32_t source, uint64_t seed,
+                       uint64_t lo, uint64_t hi,
+                       sat_best_t *d_best, void *d_ws, size_t ws_bytes, void *stream);
+
+/* Prefix-shared exhaustive search (single node, grid mode, no release times).
+ * sat_tree_plan fills *info for a prefix length (0 = engine's choice);
+ * sat_search_tree walks warp tasks [task_lo, task_hi) of that layout. */
+int sat_tree_plan(const sat_problem_t *p, int32_t prefix_len, sat_tree_info_t *info);
+int sat_search_tree(const sat_problem_t *p, int32_t prefix_len,
+                    uint64_t task_lo, uint64_t task_hi,
+                    sat_best_t *d_best, void *stream);
+
+/* Schedule n candidates and record the plan of each.
+ *   source SAT_SRC_INDEX/SUBSTREAM/SEED: d_ids[n] candidate ids (seed used by streams)
+ *   source SAT_SRC_EXPLICIT: d_explicit[n][2*J] = option digit per job, then order
+ * Outputs (device, [n*J] each, any may be NULL): option, node, start (i32 or f64);
+ * d_makespan_i64 / d_makespan_f64 [n]. */
+int sat_schedule(const sat_problem_t *p, int32_t source, uint64_t seed,
+                 const uint64_t *d_ids, const uint8_t *d_explicit, int32_t n,
+                 int32_t *d_option, int32_t *d_node,
+                 int32_t *d_start_i32, double *d_start_f64,
+                 int64_t *d_makespan_i64, double *d_makespan_f64,
+                 void *d_ws, size_t ws_bytes, void *stream);
+
+/* INT32 min/max issue-rate probe for the roofline denominator: runs `iters`
+ * dependent-chain IMNMX iterations on every SM; *d_ops_out = lane-ops done. */
+int sat_alu_probe(int32_t blocks, int32_t threads, int32_t iters,
+                  uint64_t *d_ops_out, int32_t *d_sink, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SATURN_ENGINE_H */

@@ -1,0 +1,211 @@
+/*
+ * oracle.c -- CPU ORACLE for the plan-search hot path.  TEST INFRASTRUCTURE ONLY:
+ * used by tests/ as the checker and by bench.py as the CPU baseline (cpu_baseline,
+ * --impl reference).  Never linked into or called by the product engine.
+ *
+ * C restatement of the same semantics as oracle/saturn_oracle.py (which it is
+ * checked against in tests/test_oracle_c.py):
+ *   - candidate space of SURVEY.md Appendix A1 (index = c * J! + p), SplitMix64
+ *     draws of plan_random (rng.py:20-56),
+ *   - list scheduling "earliest-fit" over explicit per-GPU free
+ *     times with GPU ids: node = the one finishing the job earliest (start = g-th
+ *     smallest free time max release, + duration on that node), lowest node on ties; the g earliest-free GPUs (lowest id on ties) run the job,
+ *   - best = lowest (makespan, id).
+ * Times are doubles in both modes (grid intervals are small integers, exact).
+ * OpenMP splits the id range into contiguous chunks, one per thread.
+ */
+#include <math.h>
+#include <omp.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define OMAX_J 64
+#define OMAX_N 32
+#define OMAX_G 32
+
+typedef struct {
+    int J, N, Cmax;
+    const int *radix;        /* [J]            */
+    const int *gpus;         /* [J*Cmax]       */
+    const unsigned *mask;    /* [J*Cmax]       */
+    const double *dur;       /* [J*Cmax*N]     */
+    const int *node_gpus;    /* [N]            */
+    const double *release;   /* [J] or NULL    */
+    const double *init_free; /* [N*OMAX_G] or NULL, per GPU id */
+} oproblem;
+
+static const uint64_t GOLD = 0x9E3779B97F4A7C15ull;
+
+static uint64_t mix(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+static uint32_t below(uint64_t *state, uint32_t n) {
+    /* limit = 2^64 - (2^64 mod n); accept r < limit */
+    uint64_t rem = (uint64_t)(((unsigned __int128)1 << 64) % n);
+    for (;;) {
+        *state += GOLD;
+        uint64_t r = mix(*state);
+        if (rem == 0 || r < (uint64_t)0 - rem) return (uint32_t)(r % n);
+    }
+}
+
+static void decode_stream(const oproblem *p, uint64_t state, int *opt, int *ord) {
+    for (int j = 0; j < p->J; ++j) opt[j] = (int)below(&state, (uint32_t)p->radix[j]);
+    for (int k = 0; k < p->J; ++k) ord[k] = k;
+    for (int i = p->J - 1; i >= 1; --i) {
+        int k = (int)below(&state, (uint32_t)(i + 1));
+        int t = ord[i]; ord[i] = ord[k]; ord[k] = t;
+    }
+}
+
+static void decode_index(const oproblem *p, uint64_t id, int *opt, int *ord) {
+    int J = p->J;
+    uint64_t f = 1;
+    for (int k = 2; k <= J; ++k) f *= (uint64_t)k;
+    uint64_t conf = id / f, perm = id % f;
+    for (int j = J - 1; j >= 0; --j) { opt[j] = (int)(conf % (uint64_t)p->radix[j]); conf /= (uint64_t)p->radix[j]; }
+    int pool[OMAX_J];
+    for (int k = 0; k < J; ++k) pool[k] = k;
+    int left = J;
+    for (int k = 0; k < J; ++k) {
+        f /= (uint64_t)(J - k);
+        int d = (int)(perm / f);
+        perm %= f;
+        ord[k] = pool[d];
+        memmove(pool + d, pool + d + 1, sizeof(int) * (size_t)(left - d - 1));
+        --left;
+    }
+}
+
+/* next candidate in index order (next lexicographic permutation, then options) */
+static void next_index(const oproblem *p, int *opt, int *ord) {
+    int J = p->J, i = J - 2;
+    while (i >= 0 && ord[i] > ord[i + 1]) --i;
+    if (i >= 0) {
+        int k = J - 1;
+        while (ord[k] < ord[i]) --k;
+        int t = ord[i]; ord[i] = ord[k]; ord[k] = t;
+        for (int a = i + 1, b = J - 1; a < b; ++a, --b) { t = ord[a]; ord[a] = ord[b]; ord[b] = t; }
+        return;
+    }
+    for (int k = 0; k < J; ++k) ord[k] = k;
+    for (int j = J - 1; j >= 0; --j) {
+        if (opt[j] + 1 < p->radix[j]) { opt[j]++; return; }
+        opt[j] = 0;
+    }
+}
+
+/* list schedule one candidate; optional per-job start / node outputs */
+double oracle_eval(const oproblem *p, const int *opt, const int *ord, double *start, int *node_out) {
+    double free_t[OMAX_N][OMAX_G];
+    for (int n = 0; n < p->N; ++n)
+        for (int k = 0; k < p->node_gpus[n]; ++k)
+            free_t[n][k] = p->init_free ? p->init_free[n * OMAX_G + k] : 0.0;
+    for (int kk = 0; kk < p->J; ++kk) {
+        int j = ord[kk], o = opt[j];
+        int q = j * p->Cmax + o;
+        int g = p->gpus[q];
+        double best_t = INFINITY, best_e = INFINITY;
+        int best_n = -1;
+        for (int n = 0; n < p->N; ++n) {
+            if (!((p->mask[q] >> n) & 1u) || p->node_gpus[n] < g) continue;
+            /* g-th smallest free time on node n (selection by counting) */
+            double t = INFINITY;
+            for (int a = 0; a < p->node_gpus[n]; ++a) {
+                int less = 0, lesseq = 0;
+                for (int b = 0; b < p->node_gpus[n]; ++b) {
+                    less += free_t[n][b] < free_t[n][a];
+                    lesseq += free_t[n][b] <= free_t[n][a];
+                }
+                if (less < g && g <= lesseq) { t = free_t[n][a]; break; }
+            }
+            if (p->release && p->release[j] > t) t = p->release[j];
+            double e = t + p->dur[q * p->N + n];          /* earliest finish, lowest node on ties */
+            if (best_n < 0 || e < best_e) { best_e = e; best_t = t; best_n = n; }
+        }
+        double e = best_e;
+        /* the g earliest-free GPUs, lowest id on ties */
+        int taken[OMAX_G] = {0};
+        for (int c = 0; c < g; ++c) {
+            int pick = -1;
+            for (int a = 0; a < p->node_gpus[best_n]; ++a)
+                if (!taken[a] && (pick < 0 || free_t[best_n][a] < free_t[best_n][pick])) pick = a;
+            taken[pick] = 1;
+        }
+        for (int a = 0; a < p->node_gpus[best_n]; ++a)
+            if (taken[a]) free_t[best_n][a] = e;
+        if (start) start[j] = best_t;
+        if (node_out) node_out[j] = best_n;
+    }
+    double ms = 0.0;
+    for (int n = 0; n < p->N; ++n)
+        for (int k = 0; k < p->node_gpus[n]; ++k)
+            if (free_t[n][k] > ms) ms = free_t[n][k];
+    return ms;
+}
+
+/* source: 0 index, 1 substream(seed, id), 2 SplitMix64(seed + id) */
+int oracle_search(const oproblem *p, int source, uint64_t seed, uint64_t lo, uint64_t hi, int threads,
+                  double *best_ms, uint64_t *best_id) {
+    if (p->J < 1 || p->J > OMAX_J || p->N < 1 || p->N > OMAX_N) return 1;
+    double gms = INFINITY;
+    uint64_t gid = UINT64_MAX;
+    if (threads < 1) threads = omp_get_max_threads();
+#pragma omp parallel num_threads(threads)
+    {
+        int nt = omp_get_num_threads(), t = omp_get_thread_num();
+        uint64_t n = hi - lo;
+        uint64_t a = lo + (uint64_t)((unsigned __int128)n * (unsigned)t / (unsigned)nt);
+        uint64_t b = lo + (uint64_t)((unsigned __int128)n * (unsigned)(t + 1) / (unsigned)nt);
+        int opt[OMAX_J], ord[OMAX_J];
+        double ms_l = INFINITY;
+        uint64_t id_l = UINT64_MAX;
+        for (uint64_t id = a; id < b; ++id) {
+            if (source == 0) {
+                if (id == a) decode_index(p, id, opt, ord);
+                else next_index(p, opt, ord);
+            } else if (source == 1) {
+                decode_stream(p, mix((seed ^ id) + GOLD), opt, ord);
+            } else {
+                decode_stream(p, seed + id, opt, ord);
+            }
+            double ms = oracle_eval(p, opt, ord, NULL, NULL);
+            if (ms < ms_l) { ms_l = ms; id_l = id; }   /* ids ascend: first wins ties */
+        }
+#pragma omp critical
+        {
+            if (ms_l < gms || (ms_l == gms && id_l < gid)) { gms = ms_l; gid = id_l; }
+        }
+    }
+    *best_ms = gms;
+    *best_id = gid;
+    return 0;
+}
+
+/* evaluate makespans of ids [lo, hi) into out[hi-lo] (window checks) */
+int oracle_makespans(const oproblem *p, int source, uint64_t seed, uint64_t lo, uint64_t hi, double *out) {
+    int opt[OMAX_J], ord[OMAX_J];
+    for (uint64_t id = lo; id < hi; ++id) {
+        if (source == 0) {
+            if (id == lo) decode_index(p, id, opt, ord);
+            else next_index(p, opt, ord);
+        } else if (source == 1) {
+            decode_stream(p, mix((seed ^ id) + GOLD), opt, ord);
+        } else {
+            decode_stream(p, seed + id, opt, ord);
+        }
+        out[id - lo] = oracle_eval(p, opt, ord, NULL, NULL);
+    }
+    return 0;
+}
+
+int oracle_decode(const oproblem *p, int source, uint64_t seed, uint64_t id, int *opt, int *ord) {
+    if (source == 0) decode_index(p, id, opt, ord);
+    else if (source == 1) decode_stream(p, mix((seed ^ id) + GOLD), opt, ord);
+    else decode_stream(p, seed + id, opt, ord);
+    return 0;
+}

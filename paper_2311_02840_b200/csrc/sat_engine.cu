@@ -1,0 +1,1118 @@
+// sat_engine.cu -- B200 (sm_100a) plan-search engine behind include/saturn_engine.h.
+//
+// What one candidate is: an option digit
+// per job plus a submission order.  Its makespan comes from per-GPU free-time list
+// scheduling: in order, each job can start on a node at that node's g-th smallest
+// GPU free time (max'd with the job's release); it goes to the node where it
+// FINISHES earliest (lowest node on ties; with node-independent durations this is
+// the earliest-starting node); its g earliest-free GPUs then become free at
+// start + duration; the makespan is the largest free time at the end.
+//
+// Representation used on the device: per node, the free times are kept SORTED.
+// Placing a (g, d) job that starts at s (= max(release, a[g-1])) with end e = s+d
+// turns the sorted vector a into
+//        b[i] = max(a[i], min(a[i+g], e))         (a[i+g] = +inf past the end)
+// which is the sorted merge of a[g..] with g copies of e (proof in DESIGN.md).
+// Every slot update is one min and one max, with no data-dependent branches.
+//
+// Two kernel families:
+//   k_generic<T, SRC, RECORD>  one candidate per W-lane warp segment (lane = GPU slot,
+//       W = nodes x padded GPUs in {8,16,32}); candidates decoded on the device from
+//       an index (mixed radix + Lehmer, odometer-advanced), a SplitMix64 stream, or
+//       explicit arrays.  Multi-node, releases, int32 grid or fp64 time.
+//   k_tree<G>  prefix-shared exhaustive walk for one node in grid time: each lane
+//       owns a distinct prefix (first P jobs of the order + their options) and the
+//       warp walks the remaining J-P jobs' orders x options in lock step, so the
+//       job sequence and gang sizes are warp-uniform and only free times differ per
+//       lane.  The last job of every candidate costs one smem load, one add and one
+//       min; every candidate still gets its full makespan computed.
+//
+// Best-plan selection: key = (makespan, index) lexicographic, lowest index wins on
+// equal makespans.  Grid mode packs it into one u64 and uses
+// atomicMin; float mode reduces per block and merges in a second tiny kernel.
+
+#include "../../include/saturn_engine.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#define SAT_INF_I32 0x3FFFFFFF
+
+namespace {
+
+constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;
+constexpr uint64_t kMix1 = 0xBF58476D1CE4E5B9ull;
+constexpr uint64_t kMix2 = 0x94D049BB133111EBull;
+constexpr int kGenThreads = 256;
+constexpr int kGenWarps = kGenThreads / 32;
+constexpr int kTreeThreads = 128;
+constexpr int kTreeWarps = kTreeThreads / 32;
+
+// ---------------------------------------------------------------------------
+// small helpers
+// ---------------------------------------------------------------------------
+__host__ __device__ inline uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * kMix1;
+    z = (z ^ (z >> 27)) * kMix2;
+    return z ^ (z >> 31);
+}
+
+template <typename T> struct TimeTraits;
+template <> struct TimeTraits<int32_t> {
+    __device__ static int32_t inf() { return SAT_INF_I32; }
+};
+template <> struct TimeTraits<double> {
+    __device__ static double inf() { return __longlong_as_double(0x7ff0000000000000ll); }
+};
+
+__device__ inline int32_t tmin(int32_t a, int32_t b) { return min(a, b); }
+__device__ inline int32_t tmax(int32_t a, int32_t b) { return max(a, b); }
+__device__ inline double tmin(double a, double b) { return fmin(a, b); }
+__device__ inline double tmax(double a, double b) { return fmax(a, b); }
+
+__device__ inline uint64_t shfl_u64(uint64_t v, int src) {
+    return __shfl_sync(0xffffffffu, v, src);
+}
+
+// ---------------------------------------------------------------------------
+// Generic problem blob (host-packed, copied to the workspace, staged to smem)
+// ---------------------------------------------------------------------------
+struct BlobHeader {
+    int32_t J, N, G, W;
+    int32_t time_mode, idx_bits, n_opt, has_release;
+    int32_t max_n;            // largest n that below(n) is asked for (sampled decode)
+    int32_t bytes;            // total blob bytes
+    int32_t off_radix, off_optbase, off_g, off_mask, off_dur, off_release, off_lane_init, off_modn;
+    int32_t pad[2];
+    int64_t init_max_i32;
+    double init_max_f64;
+};
+static_assert(sizeof(BlobHeader) % 16 == 0, "blob header alignment");
+
+// per-n constants for SplitMix64 below(n): rejection threshold and a reciprocal
+struct ModN {
+    uint64_t reject_rem;  // (2^64 mod n): accept r iff r <= ~0 - reject_rem   (rng.py:37-41)
+    uint64_t magic;       // floor((2^64 - 1) / n)
+};
+
+__device__ inline uint64_t mod_small(uint64_t r, uint32_t n, uint64_t magic) {
+    uint64_t q = __umul64hi(r, magic);
+    uint64_t rem = r - q * (uint64_t)n;
+    while (rem >= n) rem -= n;
+    return rem;
+}
+
+// SplitMix64 stream with a draw counter: k-th output = mix64(state0 + k*GOLDEN)
+struct Stream {
+    uint64_t state;
+    __device__ inline uint64_t next() {
+        state += kGolden;
+        return mix64(state);
+    }
+    __device__ inline uint32_t below(uint32_t n, const ModN *mods) {
+        const ModN m = mods[n];
+        uint64_t r = next();
+        while (r > ~0ull - m.reject_rem) r = next();   // rejection (practically never taken)
+        return (uint32_t)mod_small(r, n, m.magic);
+    }
+};
+
+// ---------------------------------------------------------------------------
+// k_generic: candidate decode (one lane per candidate) + W-lane list scheduling
+// ---------------------------------------------------------------------------
+struct GenArgs {
+    const uint8_t *blob;
+    uint64_t lo, hi;            // candidate ids [lo, hi)
+    uint64_t seed;
+    int32_t per_lane;           // consecutive candidates per lane per batch (index source)
+    const uint64_t *ids;        // RECORD: explicit candidate ids (index/stream sources)
+    const uint8_t *expl;        // EXPLICIT source: [n][2J]
+    sat_best_t *best;           // grid mode result
+    sat_best_t *partials;       // float mode per-block partials
+    int32_t *rec_opt, *rec_node;
+    int32_t *rec_start_i32;
+    double *rec_start_f64;
+    int64_t *rec_ms_i64;
+    double *rec_ms_f64;
+};
+
+template <typename T>
+__device__ inline bool key_less(T ms_a, uint64_t ix_a, T ms_b, uint64_t ix_b) {
+    return ms_a < ms_b || (ms_a == ms_b && ix_a < ix_b);
+}
+
+// Decode candidate `id` from mixed radix (job 0 most significant) x Lehmer rank.
+__device__ inline void decode_index(uint64_t id, int J, const int32_t *radix, uint8_t *opt,
+                                    uint8_t *ord) {
+    uint64_t f = 1;
+    for (int k = 2; k <= J; ++k) f *= (uint64_t)k;
+    uint64_t conf = id / f;
+    uint64_t perm = id - conf * f;
+    for (int j = J - 1; j >= 0; --j) {
+        uint64_t r = (uint64_t)radix[j];
+        uint64_t qd = conf / r;
+        opt[j] = (uint8_t)(conf - qd * r);
+        conf = qd;
+    }
+    uint64_t unused = (J == 64) ? ~0ull : ((1ull << J) - 1ull);
+    for (int k = 0; k < J; ++k) {
+        f /= (uint64_t)(J - k);                       // (J-1-k)!
+        uint64_t digit = perm / f;
+        perm -= digit * f;
+        // digit-th set bit of `unused`
+        uint64_t m = unused;
+        for (uint64_t t = 0; t < digit; ++t) m &= m - 1;
+        int job = __ffsll((long long)m) - 1;
+        ord[k] = (uint8_t)job;
+        unused &= ~(1ull << job);
+    }
+}
+
+// Advance to index + 1: next lexicographic permutation; on wrap, odometer the options.
+__device__ inline void advance_index(int J, const int32_t *radix, uint8_t *opt, uint8_t *ord) {
+    int i = J - 2;
+    while (i >= 0 && ord[i] >= ord[i + 1]) --i;
+    if (i >= 0) {
+        int k = J - 1;
+        while (ord[k] <= ord[i]) --k;
+        uint8_t t = ord[i]; ord[i] = ord[k]; ord[k] = t;
+        for (int a = i + 1, b = J - 1; a < b; ++a, --b) { t = ord[a]; ord[a] = ord[b]; ord[b] = t; }
+        return;
+    }
+    for (int k = 0; k < J; ++k) ord[k] = (uint8_t)k;
+    for (int j = J - 1; j >= 0; --j) {
+        if ((int)opt[j] + 1 < radix[j]) { opt[j] += 1; return; }
+        opt[j] = 0;
+    }
+}
+
+__device__ inline void decode_stream(uint64_t state0, int J, const int32_t *radix,
+                                     const ModN *mods, uint8_t *opt, uint8_t *ord) {
+    Stream s{state0};
+    for (int j = 0; j < J; ++j) opt[j] = (uint8_t)s.below((uint32_t)radix[j], mods);
+    for (int k = 0; k < J; ++k) ord[k] = (uint8_t)k;
+    for (int i = J - 1; i >= 1; --i) {                // Fisher-Yates, rng.py:44-48
+        uint32_t k = s.below((uint32_t)(i + 1), mods);
+        uint8_t t = ord[i]; ord[i] = ord[k]; ord[k] = t;
+    }
+}
+
+template <typename T, int SRC, bool RECORD>
+__global__ void __launch_bounds__(kGenThreads)
+k_generic(GenArgs a) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const BlobHeader &h = *reinterpret_cast<const BlobHeader *>(smem);
+    // stage the blob
+    {
+        const int nwords = (*reinterpret_cast<const BlobHeader *>(a.blob)).bytes / 16;
+        const int4 *src = reinterpret_cast<const int4 *>(a.blob);
+        int4 *dst = reinterpret_cast<int4 *>(smem);
+        for (int i = threadIdx.x; i < nwords; i += blockDim.x) dst[i] = src[i];
+    }
+    __syncthreads();
+    const int J = h.J, N = h.N, G = h.G, W = h.W;
+    const int32_t *radix = reinterpret_cast<const int32_t *>(smem + h.off_radix);
+    const int32_t *optbase = reinterpret_cast<const int32_t *>(smem + h.off_optbase);
+    const int32_t *optg = reinterpret_cast<const int32_t *>(smem + h.off_g);
+    const uint32_t *optmask = reinterpret_cast<const uint32_t *>(smem + h.off_mask);
+    const T *dur = reinterpret_cast<const T *>(smem + h.off_dur);
+    const T *release = reinterpret_cast<const T *>(smem + h.off_release);
+    const T *lane_init = reinterpret_cast<const T *>(smem + h.off_lane_init);
+    const ModN *mods = reinterpret_cast<const ModN *>(smem + h.off_modn);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint8_t *rows = smem + h.bytes + warp * (2 * 32 * SAT_MAX_JOBS);
+    uint8_t *my_opt = rows + lane * (2 * SAT_MAX_JOBS);
+    uint8_t *my_ord = my_opt + SAT_MAX_JOBS;
+
+    const int sl = lane & (W - 1), seg = lane / W, node = sl / G, slot = sl - node * G;
+    const int seg_base = seg * W;
+    const int segs = 32 / W;
+    const T INF = TimeTraits<T>::inf();
+    const T init_max = sizeof(T) == 4 ? (T)h.init_max_i32 : (T)h.init_max_f64;
+
+    T best_ms = INF;
+    uint64_t best_ix = ~0ull;
+
+    const uint64_t total = a.hi - a.lo;
+    const int per_lane = (SRC == SAT_SRC_INDEX && !RECORD) ? a.per_lane : 1;
+    const uint64_t per_batch = 32ull * (uint64_t)per_lane;
+    const uint64_t nbatches = (total + per_batch - 1) / per_batch;
+    const uint64_t gwarp = (uint64_t)blockIdx.x * kGenWarps + warp;
+    const uint64_t nwarps = (uint64_t)gridDim.x * kGenWarps;
+
+    for (uint64_t b = gwarp; b < nbatches; b += nwarps) {
+        const uint64_t first = b * per_batch + (uint64_t)lane * per_lane;   // offset from lo
+        for (int k = 0; k < per_lane; ++k) {
+            const uint64_t off = first + k;
+            const bool valid = off < total;
+            uint64_t id = a.lo + off;
+            if (RECORD) id = a.ids ? a.ids[off < total ? off : 0] : a.lo + off;
+            // ---- decode (thread per candidate) ----
+            if (valid) {
+                if (SRC == SAT_SRC_INDEX) {
+                    if (k == 0 || RECORD) decode_index(id, J, radix, my_opt, my_ord);
+                    else advance_index(J, radix, my_opt, my_ord);
+                } else if (SRC == SAT_SRC_SUBSTREAM) {
+                    decode_stream(mix64((a.seed ^ id) + kGolden), J, radix, mods, my_opt, my_ord);
+                } else if (SRC == SAT_SRC_SEED) {
+                    decode_stream(a.seed + id, J, radix, mods, my_opt, my_ord);
+                } else {
+                    const uint8_t *e = a.expl + (size_t)(RECORD ? off : id) * (2 * J);
+                    for (int j = 0; j < J; ++j) { my_opt[j] = e[j]; my_ord[j] = e[J + j]; }
+                }
+            }
+            const uint64_t my_id = id;
+            const bool my_valid = valid;
+            __syncwarp();
+            // ---- schedule: segment `seg` handles slot (pass * segs + seg) ----
+            for (int pass = 0; pass < W; ++pass) {
+                const int c = pass * segs + seg;                // candidate slot (= lane that decoded it)
+                const uint8_t *c_opt = rows + c * (2 * SAT_MAX_JOBS);
+                const uint8_t *c_ord = c_opt + SAT_MAX_JOBS;
+                const uint64_t c_off = __shfl_sync(0xffffffffu, first + k, c);
+                const bool c_valid = __shfl_sync(0xffffffffu, (int)my_valid, c) != 0;
+                const uint64_t c_id = shfl_u64(my_id, c);
+                T av = lane_init[sl];
+                T mx = init_max;
+                for (int kk = 0; kk < J; ++kk) {
+                    const int job = c_ord[kk];
+                    const int o = c_opt[job];
+                    const int q = optbase[job] + o;
+                    const int g = optg[q];
+                    T t = __shfl_sync(0xffffffffu, av, seg_base + node * G + g - 1);
+                    if (!((optmask[q] >> node) & 1u)) t = INF;
+                    if (h.has_release) t = tmax(t, release[job]);
+                    // node finishing the job earliest, lowest node on ties
+                    T bt = t;
+                    T be = t + (node < N ? dur[q * N + node] : (T)0);
+                    int bn = node;
+                    for (int x = G; x < W; x <<= 1) {
+                        T oe = __shfl_xor_sync(0xffffffffu, be, x);
+                        T ot = __shfl_xor_sync(0xffffffffu, bt, x);
+                        int on = __shfl_xor_sync(0xffffffffu, bn, x);
+                        if (oe < be || (oe == be && on < bn)) { be = oe; bt = ot; bn = on; }
+                    }
+                    const T e = be;
+                    int src = lane + g;
+                    src = src > 31 ? 31 : src;
+                    T up = __shfl_sync(0xffffffffu, av, src);
+                    if (slot + g >= G) up = INF;
+                    if (node == bn) av = tmax(av, tmin(up, e));
+                    mx = tmax(mx, e);
+                    if (RECORD && sl == 0 && c_valid) {
+                        const size_t r = (size_t)c_off * J + job;
+                        if (a.rec_opt) a.rec_opt[r] = o;
+                        if (a.rec_node) a.rec_node[r] = bn;
+                        if (sizeof(T) == 4) { if (a.rec_start_i32) a.rec_start_i32[r] = (int32_t)bt; }
+                        else { if (a.rec_start_f64) a.rec_start_f64[r] = (double)bt; }
+                    }
+                }
+                if (sl == 0 && c_valid) {
+                    if (RECORD) {
+                        if (sizeof(T) == 4) { if (a.rec_ms_i64) a.rec_ms_i64[c_off] = (int64_t)mx; }
+                        else { if (a.rec_ms_f64) a.rec_ms_f64[c_off] = (double)mx; }
+                    } else if (key_less(mx, c_id, best_ms, best_ix)) {
+                        best_ms = mx;
+                        best_ix = c_id;
+                    }
+                }
+            }
+            __syncwarp();
+        }
+    }
+    if (RECORD) return;
+
+    // ---- warp -> block -> grid argmin ----
+    for (int x = 16; x >= 1; x >>= 1) {
+        T oms = __shfl_xor_sync(0xffffffffu, best_ms, x);
+        uint64_t oix = shfl_u64(best_ix, lane ^ x);
+        if (key_less(oms, oix, best_ms, best_ix)) { best_ms = oms; best_ix = oix; }
+    }
+    __shared__ T s_ms[kGenWarps];
+    __shared__ uint64_t s_ix[kGenWarps];
+    if (lane == 0) { s_ms[warp] = best_ms; s_ix[warp] = best_ix; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < kGenWarps; ++w)
+            if (key_less(s_ms[w], s_ix[w], best_ms, best_ix)) { best_ms = s_ms[w]; best_ix = s_ix[w]; }
+        if (sizeof(T) == 4) {
+            if (best_ms < INF) {
+                const uint64_t key = ((uint64_t)(uint32_t)best_ms << h.idx_bits) | best_ix;
+                atomicMin(reinterpret_cast<unsigned long long *>(&a.best->hi), (unsigned long long)key);
+            }
+        } else {
+            double d = (double)best_ms;
+            a.partials[blockIdx.x].hi = (uint64_t)__double_as_longlong(d);
+            a.partials[blockIdx.x].lo = best_ix;
+        }
+    }
+}
+
+// float mode: fold per-block partials into *best (lexicographic on (ms bits, index))
+__global__ void k_fold_partials(const sat_best_t *partials, int n, sat_best_t *best) {
+    uint64_t hi = best->hi, lo = best->lo;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < n; ++i) {
+            const uint64_t ph = partials[i].hi, pl = partials[i].lo;
+            if (ph < hi || (ph == hi && pl < lo)) { hi = ph; lo = pl; }
+        }
+        best->hi = hi;
+        best->lo = lo;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// k_tree: prefix-shared exhaustive walk, one node, grid int32 time
+// ---------------------------------------------------------------------------
+constexpr int kTreeMaxJ = 20;
+constexpr int kTreeMaxOpt = 384;
+constexpr int kTreeMaxSets = 768;
+
+struct TreeParams {
+    int32_t J, P, Q, Gr, n_sets, idx_bits, init_max, pad;
+    int32_t radix[kTreeMaxJ];
+    int32_t optbase[kTreeMaxJ];
+    uint64_t wJ[kTreeMaxJ];           // option-digit weight in the index: W_j * J!
+    uint64_t fact[kTreeMaxJ + 1];     // k!
+    int32_t init_free[32];            // ascending, INF past Gr
+    int32_t optg[kTreeMaxOpt];
+    int32_t optoff[kTreeMaxOpt];      // (g - 1) * 32: smem word offset of slot g-1
+    int32_t optd[kTreeMaxOpt];
+    uint32_t set_mask[kTreeMaxSets];
+    uint64_t set_cum[kTreeMaxSets + 1];  // cumulative warp tasks
+    uint64_t set_prod[kTreeMaxSets];     // prod of radix over the set
+    uint64_t task_lo, task_hi;
+    sat_best_t *best;
+};
+
+// Merge of a register-resident sorted vector A with a compile-time gang size g;
+// result goes to the lane's column of smem (stride 32 words).
+template <int G, int g>
+__device__ __forceinline__ void merge_store(const int32_t (&A)[G], int32_t d, int32_t *out) {
+    const int32_t e = A[g - 1] + d;
+#pragma unroll
+    for (int i = 0; i < G; ++i) {
+        int32_t v;
+        if (i + g < G) v = min(A[(i + g < G) ? i + g : 0], e);
+        else v = e;
+        if (i >= g) v = max(A[i], v);
+        out[i * 32] = v;
+    }
+}
+
+template <int G>
+__device__ __forceinline__ void merge_dispatch(int g, const int32_t (&A)[G], int32_t d, int32_t *out) {
+    switch (g) {
+#define SAT_CASE(K) case K: if constexpr (K <= G) merge_store<G, (K <= G ? K : 1)>(A, d, out); break;
+        SAT_CASE(1) SAT_CASE(2) SAT_CASE(3) SAT_CASE(4) SAT_CASE(5) SAT_CASE(6) SAT_CASE(7) SAT_CASE(8)
+        SAT_CASE(9) SAT_CASE(10) SAT_CASE(11) SAT_CASE(12) SAT_CASE(13) SAT_CASE(14) SAT_CASE(15) SAT_CASE(16)
+        SAT_CASE(17) SAT_CASE(18) SAT_CASE(19) SAT_CASE(20) SAT_CASE(21) SAT_CASE(22) SAT_CASE(23) SAT_CASE(24)
+        SAT_CASE(25) SAT_CASE(26) SAT_CASE(27) SAT_CASE(28) SAT_CASE(29) SAT_CASE(30) SAT_CASE(31) SAT_CASE(32)
+#undef SAT_CASE
+        default: break;
+    }
+}
+
+// Per-lane running best (makespan, index).
+struct LaneBest {
+    int32_t ms;
+    uint64_t ix;
+};
+
+// Two jobs left (a < b): both orders x all options of the first (a merge each) x all
+// options of the second (a leaf each).
+template <int G>
+__device__ __forceinline__ void tree_pair(const TreeParams &p, const int32_t *U, int32_t *B,
+                                          uint32_t rem, uint64_t base, bool valid, LaneBest &lb) {
+    int32_t A[G];
+#pragma unroll
+    for (int i = 0; i < G; ++i) A[i] = U[i * 32];
+    const int ja = __ffs(rem) - 1;
+    const int jb = 31 - __clz(rem);
+    const int last = p.Gr - 1;
+#pragma unroll 1
+    for (int side = 0; side < 2; ++side) {
+        const int j1 = side ? jb : ja;
+        const int j2 = side ? ja : jb;
+        const uint64_t base1 = base + (uint64_t)side;     // Lehmer digit of position J-2
+        const int r1 = p.radix[j1], ob1 = p.optbase[j1];
+        const int r2 = p.radix[j2], ob2 = p.optbase[j2];
+        const uint64_t w1 = p.wJ[j1], w2 = p.wJ[j2];
+#pragma unroll 1
+        for (int o1 = 0; o1 < r1; ++o1) {
+            merge_dispatch<G>(p.optg[ob1 + o1], A, p.optd[ob1 + o1], B);
+            const int32_t blast = B[last * 32];
+            int32_t m = SAT_INF_I32;
+#pragma unroll 4
+            for (int o2 = 0; o2 < r2; ++o2) m = min(m, B[p.optoff[ob2 + o2]] + p.optd[ob2 + o2]);
+            const int32_t ms = max(m, blast);
+            if (valid && ms <= lb.ms) {
+                // lowest option of the second job reaching ms
+                int o2 = 0;
+                for (; o2 < r2; ++o2)
+                    if (max(B[p.optoff[ob2 + o2]] + p.optd[ob2 + o2], blast) == ms) break;
+                const uint64_t ix = base1 + (uint64_t)o1 * w1 + (uint64_t)o2 * w2;
+                if (ms < lb.ms || ix < lb.ix) { lb.ms = ms; lb.ix = ix; }
+            }
+        }
+    }
+}
+
+// Upper-level merge with a warp-uniform runtime gang size, smem column to smem column.
+template <int G>
+__device__ __forceinline__ void merge_cols(const int32_t *src, int32_t *dst, int g, int32_t d) {
+    const int32_t e = src[(g - 1) * 32] + d;
+#pragma unroll
+    for (int i = 0; i < G; ++i) {
+        const int32_t v = max(src[i * 32], min(src[(i + g) * 32], e));   // src rows G..2G-1 = INF
+        dst[i * 32] = v;
+    }
+}
+
+template <int G>
+__global__ void __launch_bounds__(kTreeThreads)
+k_tree(const __grid_constant__ TreeParams p) {
+    extern __shared__ __align__(16) int32_t tsm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int Q = p.Q, P = p.P, J = p.J;
+    const int upper = Q - 1;                         // level buffers 0..Q-2 (padded)
+    const int col_words = 2 * G * 32;
+    int32_t *wbase = tsm + warp * (upper * col_words + G * 32);
+    int32_t *Bbuf = wbase + upper * col_words + lane;
+    // padding rows of every level buffer = INF (never rewritten)
+    for (int L = 0; L < upper; ++L)
+        for (int i = G; i < 2 * G; ++i) wbase[L * col_words + i * 32 + lane] = SAT_INF_I32;
+
+    LaneBest lb{SAT_INF_I32, ~0ull};
+    const uint64_t gwarp = (uint64_t)blockIdx.x * kTreeWarps + warp;
+    const uint64_t nwarps = (uint64_t)gridDim.x * kTreeWarps;
+    const uint32_t all = (J >= 32) ? 0xffffffffu : ((1u << J) - 1u);
+
+    for (uint64_t t = p.task_lo + gwarp; t < p.task_hi; t += nwarps) {
+        // ---- which prefix set (warp-uniform binary search) ----
+        int lo = 0, hi = p.n_sets - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (p.set_cum[mid] <= t) lo = mid; else hi = mid - 1;
+        }
+        const int s = lo;
+        const uint32_t S = p.set_mask[s];
+        uint64_t fP = p.fact[P];
+        const uint64_t npref = fP * p.set_prod[s];
+        const uint64_t q = (t - p.set_cum[s]) * 32ull + (uint64_t)lane;
+        const bool valid = q < npref;
+        const uint64_t qq = valid ? q : 0;
+
+        // ---- decode this lane's prefix: order of S (Lehmer) and options of S ----
+        uint64_t code = qq / fP;
+        uint64_t prank = qq - code * fP;
+        int32_t *L0 = wbase + lane;
+        for (int i = 0; i < G; ++i) L0[i * 32] = p.init_free[i];
+        uint8_t popt[kTreeMaxJ];
+        {
+            // options: mixed radix over S's jobs, highest job id least significant
+            uint32_t m = S;
+            while (m) {
+                const int j = 31 - __clz(m);
+                m &= ~(1u << j);
+                const uint64_t r = (uint64_t)p.radix[j];
+                const uint64_t qd = code / r;
+                popt[j] = (uint8_t)(code - qd * r);
+                code = qd;
+            }
+        }
+        uint64_t base = 0;
+        uint32_t unplaced = all, avail = S;
+        for (int k = 0; k < P; ++k) {
+            fP /= (uint64_t)(P - k);
+            const uint64_t digit = prank / fP;
+            prank -= digit * fP;
+            uint32_t m = avail;
+            for (uint64_t x = 0; x < digit; ++x) m &= m - 1;
+            const int j = __ffs(m) - 1;
+            avail &= ~(1u << j);
+            const int o = popt[j];
+            base += (uint64_t)__popc(unplaced & ((1u << j) - 1u)) * p.fact[J - 1 - k] + (uint64_t)o * p.wJ[j];
+            unplaced &= ~(1u << j);
+            // per-lane gang size: in-place merge on the lane's column
+            const int q2 = p.optbase[j] + o;
+            const int g = p.optg[q2];
+            const int32_t e = L0[(g - 1) * 32] + p.optd[q2];
+            for (int i = 0; i < G; ++i) L0[i * 32] = max(L0[i * 32], min(L0[(i + g) * 32], e));
+        }
+        __syncwarp();
+
+        // ---- warp-uniform walk over the suffix (jobs in `unplaced`) ----
+        if (Q == 2) {
+            tree_pair<G>(p, L0, Bbuf, unplaced, base, valid, lb);
+        } else {
+            uint32_t rem_st[kTreeMaxJ];
+            uint64_t acc_st[kTreeMaxJ];
+            int cj[kTreeMaxJ], co[kTreeMaxJ];
+            int L = 0;
+            rem_st[0] = unplaced;
+            acc_st[0] = base;
+            cj[0] = -1;
+            co[0] = 0;
+            while (L >= 0) {
+                // advance the cursor of level L to its next (job, option)
+                int j = cj[L], o = co[L] + 1;
+                if (j < 0 || o >= p.radix[j]) {
+                    const uint32_t later = (j < 0) ? rem_st[L] : (rem_st[L] & ~((2u << j) - 1u));
+                    if (!later) { --L; continue; }
+                    j = __ffs(later) - 1;
+                    o = 0;
+                }
+                cj[L] = j;
+                co[L] = o;
+                const int32_t *src = wbase + L * col_words + lane;
+                int32_t *dst = wbase + (L + 1) * col_words + lane;
+                const int q2 = p.optbase[j] + o;
+                merge_cols<G>(src, dst, p.optg[q2], p.optd[q2]);
+                const uint32_t rem = rem_st[L];
+                const uint64_t acc = acc_st[L] +
+                    (uint64_t)__popc(rem & ((1u << j) - 1u)) * p.fact[Q - 1 - L] + (uint64_t)o * p.wJ[j];
+                const uint32_t rem2 = rem & ~(1u << j);
+                if (L + 1 == Q - 2) {
+                    tree_pair<G>(p, dst, Bbuf, rem2, acc, valid, lb);
+                } else {
+                    ++L;
+                    rem_st[L] = rem2;
+                    acc_st[L] = acc;
+                    cj[L] = -1;
+                    co[L] = 0;
+                }
+            }
+        }
+        __syncwarp();
+    }
+
+    // ---- warp argmin, one atomic per warp ----
+    uint64_t key = (lb.ms < SAT_INF_I32) ? (((uint64_t)(uint32_t)lb.ms << p.idx_bits) | lb.ix) : ~0ull;
+    for (int x = 16; x >= 1; x >>= 1) {
+        const uint64_t o = shfl_u64(key, lane ^ x);
+        key = o < key ? o : key;
+    }
+    if (lane == 0 && key != ~0ull)
+        atomicMin(reinterpret_cast<unsigned long long *>(&p.best->hi), (unsigned long long)key);
+}
+
+// ---------------------------------------------------------------------------
+// ALU probe: independent IMNMX chains (8 per thread) for the INT32 roofline
+// ---------------------------------------------------------------------------
+__global__ void k_alu_probe(int iters, unsigned long long *ops, int32_t *sink) {
+    // 16 independent min/max chains; asm volatile keeps every IMNMX
+    int32_t v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = (int32_t)threadIdx.x + i;
+    const int32_t lo = (int32_t)(blockIdx.x & 7), hi = (int32_t)(blockIdx.x | 1024);
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            asm volatile("min.s32 %0, %0, %1;" : "+r"(v[i]) : "r"(hi));
+            asm volatile("max.s32 %0, %0, %1;" : "+r"(v[i]) : "r"(lo));
+        }
+    }
+    int32_t r = 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) r ^= v[i];
+    if (r == 0x7fffffff) sink[0] = r;
+    if (threadIdx.x == 0 && blockIdx.x == 0)
+        *ops = (unsigned long long)gridDim.x * blockDim.x * (unsigned long long)iters * 32ull;
+}
+
+// ---------------------------------------------------------------------------
+// host side: validation, packing, launch sizing
+// ---------------------------------------------------------------------------
+inline int check_cuda(cudaError_t e) { return e == cudaSuccess ? SAT_OK : SAT_ERR_CUDA; }
+
+int validate(const sat_problem_t *p) {
+    if (!p) return SAT_ERR_INVALID;
+    if (p->J < 1 || p->J > SAT_MAX_JOBS || p->N < 1 || p->G < 1 || p->Cmax < 1) return SAT_ERR_INVALID;
+    if ((p->G & (p->G - 1)) != 0) return SAT_ERR_INVALID;
+    if ((int64_t)p->N * p->G > SAT_MAX_LANES) return SAT_ERR_UNSUPPORTED;
+    if (p->time_mode != SAT_TIME_GRID_I32 && p->time_mode != SAT_TIME_F64) return SAT_ERR_INVALID;
+    if (!p->radix || !p->gpus || !p->node_gpus) return SAT_ERR_INVALID;
+    if (p->time_mode == SAT_TIME_GRID_I32 && !p->dur_i32) return SAT_ERR_INVALID;
+    if (p->time_mode == SAT_TIME_F64 && !p->dur_f64) return SAT_ERR_INVALID;
+    for (int n = 0; n < p->N; ++n)
+        if (p->node_gpus[n] < 1 || p->node_gpus[n] > p->G) return SAT_ERR_INVALID;
+    for (int j = 0; j < p->J; ++j) {
+        if (p->radix[j] < 1) return SAT_ERR_NO_OPTIONS;
+        if (p->radix[j] > p->Cmax || p->radix[j] > 255) return SAT_ERR_INVALID;
+        for (int o = 0; o < p->radix[j]; ++o) {
+            const int g = p->gpus[j * p->Cmax + o];
+            if (g < 1 || g > p->G) return SAT_ERR_INVALID;
+            const uint32_t m = p->node_mask ? p->node_mask[j * p->Cmax + o] : ~0u;
+            bool any = false;
+            for (int n = 0; n < p->N; ++n)
+                if (((m >> n) & 1u) && p->node_gpus[n] >= g) any = true;
+            if (!any) return SAT_ERR_INVALID;
+        }
+    }
+    if (p->time_mode == SAT_TIME_GRID_I32 && (p->idx_bits < 1 || p->idx_bits > 62)) return SAT_ERR_INVALID;
+    return SAT_OK;
+}
+
+inline int align16(int x) { return (x + 15) & ~15; }
+
+int device_sms() {
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 148;
+    return sms > 0 ? sms : 148;
+}
+
+// Build the generic blob.  Lane init: for W lanes, node = lane / G, slot = lane % G.
+int pack_blob(const sat_problem_t *p, std::vector<uint8_t> &blob) {
+    const int J = p->J, N = p->N, G = p->G;
+    int W = 8;
+    while (W < N * G) W <<= 1;
+    const bool f64 = p->time_mode == SAT_TIME_F64;
+    const int tsz = f64 ? 8 : 4;
+    int n_opt = 0, max_n = J;
+    for (int j = 0; j < J; ++j) { n_opt += p->radix[j]; max_n = std::max(max_n, (int)p->radix[j]); }
+    BlobHeader h{};
+    h.J = J; h.N = N; h.G = G; h.W = W;
+    h.time_mode = p->time_mode; h.idx_bits = p->idx_bits; h.n_opt = n_opt;
+    h.max_n = max_n;
+    int off = sizeof(BlobHeader);
+    h.off_radix = off; off = align16(off + 4 * J);
+    h.off_optbase = off; off = align16(off + 4 * J);
+    h.off_g = off; off = align16(off + 4 * n_opt);
+    h.off_mask = off; off = align16(off + 4 * n_opt);
+    h.off_dur = off; off = align16(off + tsz * n_opt * N);
+    h.off_release = off; off = align16(off + tsz * J);
+    h.off_lane_init = off; off = align16(off + tsz * W);
+    h.off_modn = off; off = align16(off + (int)sizeof(ModN) * (max_n + 1));
+    h.bytes = off;
+    blob.assign(off, 0);
+    int32_t *radix = reinterpret_cast<int32_t *>(&blob[h.off_radix]);
+    int32_t *optbase = reinterpret_cast<int32_t *>(&blob[h.off_optbase]);
+    int32_t *og = reinterpret_cast<int32_t *>(&blob[h.off_g]);
+    uint32_t *om = reinterpret_cast<uint32_t *>(&blob[h.off_mask]);
+    int q = 0;
+    bool has_release = false;
+    for (int j = 0; j < J; ++j) {
+        radix[j] = p->radix[j];
+        optbase[j] = q;
+        for (int o = 0; o < p->radix[j]; ++o, ++q) {
+            const int src = j * p->Cmax + o;
+            og[q] = p->gpus[src];
+            uint32_t m = p->node_mask ? p->node_mask[src] : ((N >= 32) ? ~0u : ((1u << N) - 1u));
+            if (N < 32) m &= (1u << N) - 1u;
+            om[q] = m;
+            for (int n = 0; n < N; ++n) {
+                if (f64) reinterpret_cast<double *>(&blob[h.off_dur])[q * N + n] = p->dur_f64[src * N + n];
+                else reinterpret_cast<int32_t *>(&blob[h.off_dur])[q * N + n] = p->dur_i32[src * N + n];
+            }
+        }
+        if (f64) {
+            const double r = p->release_f64 ? p->release_f64[j] : 0.0;
+            reinterpret_cast<double *>(&blob[h.off_release])[j] = r;
+            has_release |= r != 0.0;
+        } else {
+            const int32_t r = p->release_i32 ? p->release_i32[j] : 0;
+            reinterpret_cast<int32_t *>(&blob[h.off_release])[j] = r;
+            has_release |= r != 0;
+        }
+    }
+    h.has_release = has_release ? 1 : 0;
+    int64_t imax_i = 0;
+    double imax_f = 0.0;
+    for (int l = 0; l < W; ++l) {
+        const int n = l / G, s = l % G;
+        const bool real = n < N && s < p->node_gpus[n];
+        if (f64) {
+            double v = real ? (p->init_free_f64 ? p->init_free_f64[n * G + s] : 0.0)
+                            : __builtin_inf();
+            reinterpret_cast<double *>(&blob[h.off_lane_init])[l] = v;
+            if (real) imax_f = std::max(imax_f, v);
+        } else {
+            int32_t v = real ? (p->init_free_i32 ? p->init_free_i32[n * G + s] : 0) : SAT_INF_I32;
+            reinterpret_cast<int32_t *>(&blob[h.off_lane_init])[l] = v;
+            if (real) imax_i = std::max<int64_t>(imax_i, v);
+        }
+    }
+    h.init_max_i32 = imax_i;
+    h.init_max_f64 = imax_f;
+    ModN *mods = reinterpret_cast<ModN *>(&blob[h.off_modn]);
+    for (int n = 1; n <= max_n; ++n) {
+        const unsigned __int128 two64 = (unsigned __int128)1 << 64;
+        mods[n].reject_rem = (uint64_t)(two64 % (unsigned)n);
+        mods[n].magic = ~0ull / (uint64_t)n;
+    }
+    std::memcpy(blob.data(), &h, sizeof(h));
+    return SAT_OK;
+}
+
+constexpr int kRowsBytesPerBlock = kGenWarps * 2 * 32 * SAT_MAX_JOBS;
+
+int gen_blocks(const void *kernel, int smem_bytes) {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kGenThreads, smem_bytes) != cudaSuccess ||
+        per_sm < 1)
+        per_sm = 1;
+    return device_sms() * per_sm;
+}
+
+template <typename T, int SRC, bool RECORD>
+int launch_generic(const sat_problem_t *p, GenArgs a, uint64_t n_cand, void *d_ws, size_t ws_bytes,
+                   cudaStream_t stream) {
+    std::vector<uint8_t> blob;
+    int st = pack_blob(p, blob);
+    if (st) return st;
+    const size_t blob_bytes = blob.size();
+    const int smem = (int)blob_bytes + kRowsBytesPerBlock;
+    if (smem > 200 * 1024) return SAT_ERR_TOO_LARGE;
+    auto kern = k_generic<T, SRC, RECORD>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+        return SAT_ERR_CUDA;
+    int blocks = gen_blocks((const void *)kern, smem);
+    const uint64_t per_batch = 32ull * (uint64_t)std::max(1, a.per_lane);
+    const uint64_t batches = (n_cand + per_batch - 1) / per_batch;
+    const uint64_t need = (batches + kGenWarps - 1) / kGenWarps;
+    if ((uint64_t)blocks > need) blocks = (int)std::max<uint64_t>(1, need);
+    const size_t part_off = (blob_bytes + 255) & ~(size_t)255;
+    const size_t need_ws = part_off + (size_t)blocks * sizeof(sat_best_t);
+    if (!d_ws || ws_bytes < need_ws) return SAT_ERR_INVALID;
+    uint8_t *ws = static_cast<uint8_t *>(d_ws);
+    if (cudaMemcpyAsync(ws, blob.data(), blob_bytes, cudaMemcpyHostToDevice, stream) != cudaSuccess)
+        return SAT_ERR_CUDA;
+    a.blob = ws;
+    a.partials = reinterpret_cast<sat_best_t *>(ws + part_off);
+    kern<<<blocks, kGenThreads, smem, stream>>>(a);
+    if (cudaGetLastError() != cudaSuccess) return SAT_ERR_CUDA;
+    if (!RECORD && sizeof(T) == 8) {
+        k_fold_partials<<<1, 32, 0, stream>>>(a.partials, blocks, a.best);
+        if (cudaGetLastError() != cudaSuccess) return SAT_ERR_CUDA;
+    }
+    return SAT_OK;
+}
+
+uint64_t factorial_u64(int n) {
+    uint64_t f = 1;
+    for (int k = 2; k <= n; ++k) f *= (uint64_t)k;
+    return f;
+}
+
+// n! * prod(radix) without overflow?  Returns false if > 2^63.
+bool space_size(const sat_problem_t *p, uint64_t *out) {
+    unsigned __int128 s = 1;
+    for (int k = 2; k <= p->J; ++k) { s *= (unsigned)k; if (s > ((unsigned __int128)1 << 63)) return false; }
+    for (int j = 0; j < p->J; ++j) { s *= (unsigned)p->radix[j]; if (s > ((unsigned __int128)1 << 63)) return false; }
+    *out = (uint64_t)s;
+    return true;
+}
+
+// ---- tree layout ----
+struct TreeLayout {
+    int P = 0;
+    std::vector<uint32_t> sets;
+    std::vector<uint64_t> cum, prod;
+    uint64_t n_tasks = 0, n_cand = 0, n_steps = 0;
+};
+
+// number of placements in the full walk below a remaining-set (memoised by mask)
+uint64_t walk_nodes(const int32_t *radix, uint32_t rem, std::vector<int64_t> &memo, uint32_t full) {
+    if (!rem) return 0;
+    // memo indexed by rem (sub-mask of `full`): compress via the mask itself when small
+    if (memo[rem] >= 0) return (uint64_t)memo[rem];
+    uint64_t tot = 0;
+    for (uint32_t m = rem; m; m &= m - 1) {
+        const int j = __builtin_ctz(m);
+        tot += (uint64_t)radix[j] * (1 + walk_nodes(radix, rem & ~(1u << j), memo, full));
+    }
+    memo[rem] = (int64_t)tot;
+    return tot;
+}
+
+int tree_layout(const sat_problem_t *p, int prefix_len, TreeLayout &lay) {
+    const int J = p->J;
+    if (p->N != 1 || p->time_mode != SAT_TIME_GRID_I32) return SAT_ERR_UNSUPPORTED;
+    if (J < 3 || J > kTreeMaxJ) return SAT_ERR_UNSUPPORTED;
+    if (p->release_i32)
+        for (int j = 0; j < J; ++j) if (p->release_i32[j] != 0) return SAT_ERR_UNSUPPORTED;
+    int n_opt = 0;
+    for (int j = 0; j < J; ++j) n_opt += p->radix[j];
+    if (n_opt > kTreeMaxOpt) return SAT_ERR_UNSUPPORTED;
+    uint64_t space;
+    if (!space_size(p, &space)) return SAT_ERR_TOO_LARGE;
+    auto build = [&](int P, TreeLayout &L) -> bool {
+        L = TreeLayout();
+        L.P = P;
+        const uint64_t fP = factorial_u64(P);
+        for (uint32_t S = 0; S < (1u << J); ++S) {
+            if (__builtin_popcount(S) != P) continue;
+            unsigned __int128 pr = 1;
+            for (int j = 0; j < J; ++j) if (S >> j & 1u) pr *= (unsigned)p->radix[j];
+            L.sets.push_back(S);
+            L.prod.push_back((uint64_t)pr);
+            L.cum.push_back(L.n_tasks);
+            L.n_tasks += ((uint64_t)pr * fP + 31) / 32;
+            if (L.sets.size() > (size_t)kTreeMaxSets) return false;
+        }
+        L.cum.push_back(L.n_tasks);
+        L.n_cand = space;
+        return true;
+    };
+    int P = prefix_len;
+    if (P <= 0) {
+        // smallest prefix giving enough warp tasks to fill 8 GPUs several times over
+        P = J - 2;
+        for (int cand = 1; cand <= J - 2; ++cand) {
+            TreeLayout t;
+            if (!build(cand, t)) break;
+            if (t.n_tasks >= (1ull << 17)) { P = cand; break; }
+        }
+    }
+    if (P < 1 || P > J - 2) return SAT_ERR_INVALID;
+    if (!build(P, lay)) return SAT_ERR_UNSUPPORTED;
+    // placements: P per lane prefix + the suffix walk
+    std::vector<int64_t> memo((size_t)1 << J, -1);
+    const uint32_t full = (1u << J) - 1u;
+    const uint64_t fP = factorial_u64(P);
+    lay.n_steps = 0;
+    for (size_t s = 0; s < lay.sets.size(); ++s) {
+        const uint64_t npref = fP * lay.prod[s];
+        lay.n_steps += npref * ((uint64_t)P + walk_nodes(p->radix, full & ~lay.sets[s], memo, full));
+    }
+    return SAT_OK;
+}
+
+template <int G>
+int launch_tree_g(const TreeParams &tp, int Q, cudaStream_t stream) {
+    const int upper = Q - 1;
+    const int smem = kTreeWarps * (upper * 2 * G * 32 + G * 32) * 4;
+    if (smem > 200 * 1024) return SAT_ERR_UNSUPPORTED;
+    auto kern = k_tree<G>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+        return SAT_ERR_CUDA;
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kTreeThreads, smem) != cudaSuccess ||
+        per_sm < 1)
+        per_sm = 1;
+    uint64_t blocks = (uint64_t)device_sms() * per_sm;
+    const uint64_t tasks = tp.task_hi - tp.task_lo;
+    const uint64_t need = (tasks + kTreeWarps - 1) / kTreeWarps;
+    if (blocks > need) blocks = std::max<uint64_t>(1, need);
+    kern<<<(unsigned)blocks, kTreeThreads, smem, stream>>>(tp);
+    return cudaGetLastError() == cudaSuccess ? SAT_OK : SAT_ERR_CUDA;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+int sat_abi_version(void) { return SAT_ABI_VERSION; }
+
+const char *sat_error_string(int status) {
+    switch (status) {
+        case SAT_OK: return "ok";
+        case SAT_ERR_INVALID: return "invalid problem or arguments";
+        case SAT_ERR_NO_OPTIONS: return "a job has no feasible option";
+        case SAT_ERR_TOO_LARGE: return "search space, key or tables exceed the engine encoding";
+        case SAT_ERR_UNSUPPORTED: return "problem shape not supported by this kernel";
+        case SAT_ERR_CUDA: return "CUDA launch or runtime failure";
+        default: return "unknown status";
+    }
+}
+
+int sat_device_info(int device, int32_t *sm_count, int32_t *cc_major, int32_t *cc_minor) {
+    int v = 0;
+    if (sm_count) {
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return SAT_ERR_CUDA;
+        *sm_count = v;
+    }
+    if (cc_major) {
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrComputeCapabilityMajor, device) != cudaSuccess) return SAT_ERR_CUDA;
+        *cc_major = v;
+    }
+    if (cc_minor) {
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrComputeCapabilityMinor, device) != cudaSuccess) return SAT_ERR_CUDA;
+        *cc_minor = v;
+    }
+    return SAT_OK;
+}
+
+int sat_best_reset(sat_best_t *d_best, void *stream) {
+    if (!d_best) return SAT_ERR_INVALID;
+    return check_cuda(cudaMemsetAsync(d_best, 0xFF, sizeof(sat_best_t), (cudaStream_t)stream));
+}
+
+int sat_workspace_bytes(const sat_problem_t *p, size_t *bytes) {
+    int st = validate(p);
+    if (st) return st;
+    std::vector<uint8_t> blob;
+    st = pack_blob(p, blob);
+    if (st) return st;
+    const size_t part_off = (blob.size() + 255) & ~(size_t)255;
+    *bytes = part_off + (size_t)device_sms() * 32 * sizeof(sat_best_t);
+    return SAT_OK;
+}
+
+int sat_search_index(const sat_problem_t *p, uint64_t lo, uint64_t hi, sat_best_t *d_best, void *d_ws,
+                     size_t ws_bytes, void *stream) {
+    int st = validate(p);
+    if (st) return st;
+    if (!d_best || hi < lo) return SAT_ERR_INVALID;
+    uint64_t space;
+    if (!space_size(p, &space)) return SAT_ERR_TOO_LARGE;
+    if (hi > space) return SAT_ERR_INVALID;
+    if (p->time_mode == SAT_TIME_GRID_I32 && p->idx_bits < 64 && (space - 1) >> p->idx_bits) return SAT_ERR_TOO_LARGE;
+    if (hi == lo) return SAT_OK;
+    GenArgs a{};
+    a.lo = lo; a.hi = hi; a.best = d_best;
+    a.per_lane = 16;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (p->time_mode == SAT_TIME_F64)
+        return launch_generic<double, SAT_SRC_INDEX, false>(p, a, hi - lo, d_ws, ws_bytes, s);
+    return launch_generic<int32_t, SAT_SRC_INDEX, false>(p, a, hi - lo, d_ws, ws_bytes, s);
+}
+
+int sat_search_sampled(const sat_problem_t *p, int32_t source, uint64_t seed, uint64_t lo, uint64_t hi,
+                       sat_best_t *d_best, void *d_ws, size_t ws_bytes, void *stream) {
+    int st = validate(p);
+    if (st) return st;
+    if (!d_best || hi < lo) return SAT_ERR_INVALID;
+    if (source != SAT_SRC_SUBSTREAM && source != SAT_SRC_SEED) return SAT_ERR_INVALID;
+    if (p->time_mode == SAT_TIME_GRID_I32 && hi > 0 && ((hi - 1) >> p->idx_bits)) return SAT_ERR_TOO_LARGE;
+    if (hi == lo) return SAT_OK;
+    GenArgs a{};
+    a.lo = lo; a.hi = hi; a.best = d_best; a.seed = seed; a.per_lane = 1;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (p->time_mode == SAT_TIME_F64) {
+        if (source == SAT_SRC_SUBSTREAM)
+            return launch_generic<double, SAT_SRC_SUBSTREAM, false>(p, a, hi - lo, d_ws, ws_bytes, s);
+        return launch_generic<double, SAT_SRC_SEED, false>(p, a, hi - lo, d_ws, ws_bytes, s);
+    }
+    if (source == SAT_SRC_SUBSTREAM)
+        return launch_generic<int32_t, SAT_SRC_SUBSTREAM, false>(p, a, hi - lo, d_ws, ws_bytes, s);
+    return launch_generic<int32_t, SAT_SRC_SEED, false>(p, a, hi - lo, d_ws, ws_bytes, s);
+}
+
+int sat_schedule(const sat_problem_t *p, int32_t source, uint64_t seed, const uint64_t *d_ids,
+                 const uint8_t *d_explicit, int32_t n, int32_t *d_option, int32_t *d_node,
+                 int32_t *d_start_i32, double *d_start_f64, int64_t *d_makespan_i64,
+                 double *d_makespan_f64, void *d_ws, size_t ws_bytes, void *stream) {
+    int st = validate(p);
+    if (st) return st;
+    if (n < 0) return SAT_ERR_INVALID;
+    if (n == 0) return SAT_OK;
+    if (source == SAT_SRC_EXPLICIT ? !d_explicit : !d_ids) return SAT_ERR_INVALID;
+    GenArgs a{};
+    a.lo = 0; a.hi = (uint64_t)n; a.seed = seed; a.per_lane = 1;
+    a.ids = d_ids; a.expl = d_explicit;
+    a.rec_opt = d_option; a.rec_node = d_node;
+    a.rec_start_i32 = d_start_i32; a.rec_start_f64 = d_start_f64;
+    a.rec_ms_i64 = d_makespan_i64; a.rec_ms_f64 = d_makespan_f64;
+    cudaStream_t s = (cudaStream_t)stream;
+    const uint64_t nn = (uint64_t)n;
+    if (p->time_mode == SAT_TIME_F64) {
+        switch (source) {
+            case SAT_SRC_INDEX: return launch_generic<double, SAT_SRC_INDEX, true>(p, a, nn, d_ws, ws_bytes, s);
+            case SAT_SRC_SUBSTREAM: return launch_generic<double, SAT_SRC_SUBSTREAM, true>(p, a, nn, d_ws, ws_bytes, s);
+            case SAT_SRC_SEED: return launch_generic<double, SAT_SRC_SEED, true>(p, a, nn, d_ws, ws_bytes, s);
+            case SAT_SRC_EXPLICIT: return launch_generic<double, SAT_SRC_EXPLICIT, true>(p, a, nn, d_ws, ws_bytes, s);
+            default: return SAT_ERR_INVALID;
+        }
+    }
+    switch (source) {
+        case SAT_SRC_INDEX: return launch_generic<int32_t, SAT_SRC_INDEX, true>(p, a, nn, d_ws, ws_bytes, s);
+        case SAT_SRC_SUBSTREAM: return launch_generic<int32_t, SAT_SRC_SUBSTREAM, true>(p, a, nn, d_ws, ws_bytes, s);
+        case SAT_SRC_SEED: return launch_generic<int32_t, SAT_SRC_SEED, true>(p, a, nn, d_ws, ws_bytes, s);
+        case SAT_SRC_EXPLICIT: return launch_generic<int32_t, SAT_SRC_EXPLICIT, true>(p, a, nn, d_ws, ws_bytes, s);
+        default: return SAT_ERR_INVALID;
+    }
+}
+
+int sat_tree_plan(const sat_problem_t *p, int32_t prefix_len, sat_tree_info_t *info) {
+    int st = validate(p);
+    if (st) return st;
+    if (!info) return SAT_ERR_INVALID;
+    TreeLayout lay;
+    st = tree_layout(p, prefix_len, lay);
+    if (st) return st;
+    info->prefix_len = lay.P;
+    info->n_sets = (int32_t)lay.sets.size();
+    info->n_tasks = lay.n_tasks;
+    info->n_candidates = lay.n_cand;
+    info->n_job_steps = lay.n_steps;
+    return SAT_OK;
+}
+
+int sat_search_tree(const sat_problem_t *p, int32_t prefix_len, uint64_t task_lo, uint64_t task_hi,
+                    sat_best_t *d_best, void *stream) {
+    int st = validate(p);
+    if (st) return st;
+    if (!d_best || task_hi < task_lo) return SAT_ERR_INVALID;
+    TreeLayout lay;
+    st = tree_layout(p, prefix_len, lay);
+    if (st) return st;
+    if (task_hi > lay.n_tasks) return SAT_ERR_INVALID;
+    if ((lay.n_cand - 1) >> p->idx_bits) return SAT_ERR_TOO_LARGE;
+    if (task_hi == task_lo) return SAT_OK;
+    TreeParams tp;
+    std::memset(&tp, 0, sizeof(tp));
+    const int J = p->J;
+    tp.J = J; tp.P = lay.P; tp.Q = J - lay.P; tp.Gr = p->node_gpus[0];
+    tp.n_sets = (int32_t)lay.sets.size(); tp.idx_bits = p->idx_bits;
+    tp.fact[0] = 1;
+    for (int k = 1; k <= J; ++k) tp.fact[k] = tp.fact[k - 1] * (uint64_t)k;
+    uint64_t w = 1;
+    for (int j = J - 1; j >= 0; --j) { tp.wJ[j] = w * tp.fact[J]; w *= (uint64_t)p->radix[j]; }
+    int q = 0;
+    for (int j = 0; j < J; ++j) {
+        tp.radix[j] = p->radix[j];
+        tp.optbase[j] = q;
+        for (int o = 0; o < p->radix[j]; ++o, ++q) {
+            const int g = p->gpus[j * p->Cmax + o];
+            tp.optg[q] = g;
+            tp.optoff[q] = (g - 1) * 32;
+            tp.optd[q] = p->dur_i32[j * p->Cmax + o];
+        }
+    }
+    int32_t imax = 0;
+    for (int i = 0; i < 32; ++i) {
+        const bool real = i < tp.Gr;
+        const int32_t v = real ? (p->init_free_i32 ? p->init_free_i32[i] : 0) : SAT_INF_I32;
+        tp.init_free[i] = v;
+        if (real) imax = std::max(imax, v);
+    }
+    tp.init_max = imax;
+    for (size_t s = 0; s < lay.sets.size(); ++s) {
+        tp.set_mask[s] = lay.sets[s];
+        tp.set_cum[s] = lay.cum[s];
+        tp.set_prod[s] = lay.prod[s];
+    }
+    tp.set_cum[lay.sets.size()] = lay.cum.back();
+    tp.task_lo = task_lo; tp.task_hi = task_hi;
+    tp.best = d_best;
+    cudaStream_t s = (cudaStream_t)stream;
+    switch (p->G) {
+        case 1: return launch_tree_g<1>(tp, tp.Q, s);
+        case 2: return launch_tree_g<2>(tp, tp.Q, s);
+        case 4: return launch_tree_g<4>(tp, tp.Q, s);
+        case 8: return launch_tree_g<8>(tp, tp.Q, s);
+        case 16: return launch_tree_g<16>(tp, tp.Q, s);
+        case 32: return launch_tree_g<32>(tp, tp.Q, s);
+        default: return SAT_ERR_UNSUPPORTED;
+    }
+}
+
+int sat_alu_probe(int32_t blocks, int32_t threads, int32_t iters, uint64_t *d_ops_out, int32_t *d_sink,
+                  void *stream) {
+    if (blocks < 1 || threads < 32 || iters < 1 || !d_ops_out || !d_sink) return SAT_ERR_INVALID;
+    k_alu_probe<<<blocks, threads, 0, (cudaStream_t)stream>>>(iters, (unsigned long long *)d_ops_out, d_sink);
+    return cudaGetLastError() == cudaSuccess ? SAT_OK : SAT_ERR_CUDA;
+}
+
+}  // extern "C"

@@ -1,0 +1,368 @@
+"""ctypes binding of the CUDA engine (include/saturn_engine.h) plus search orchestration.
+
+PyTorch is plumbing here: device buffers, the current stream, and
+``torch.distributed`` (NCCL) for the one cross-GPU exchange -- an all-reduce MIN
+of each rank's packed (makespan, index) key.  There is
+no CPU path: if the extension or a GPU is missing, every entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import errors as E
+from .problem import TIME_FLOAT, TIME_GRID, SearchProblem, SolveOptions
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libsaturn_b200.so")
+
+SAT_OK, SAT_ERR_INVALID, SAT_ERR_NO_OPTIONS, SAT_ERR_TOO_LARGE, SAT_ERR_UNSUPPORTED, SAT_ERR_CUDA = range(6)
+SAT_TIME_GRID_I32, SAT_TIME_F64 = 0, 1
+SRC_INDEX, SRC_SUBSTREAM, SRC_SEED, SRC_EXPLICIT = 0, 1, 2, 3
+INT64_MAX = (1 << 63) - 1
+
+_vp = ctypes.c_void_p
+_i32 = ctypes.c_int32
+_u64 = ctypes.c_uint64
+
+
+class SatProblem(ctypes.Structure):
+    _fields_ = [
+        ("J", _i32), ("N", _i32), ("G", _i32), ("Cmax", _i32), ("time_mode", _i32), ("idx_bits", _i32),
+        ("radix", _vp), ("gpus", _vp), ("node_mask", _vp), ("dur_i32", _vp), ("dur_f64", _vp),
+        ("node_gpus", _vp), ("release_i32", _vp), ("release_f64", _vp),
+        ("init_free_i32", _vp), ("init_free_f64", _vp),
+    ]
+
+
+class SatTreeInfo(ctypes.Structure):
+    _fields_ = [("prefix_len", _i32), ("n_sets", _i32), ("n_tasks", _u64),
+                ("n_candidates", _u64), ("n_job_steps", _u64)]
+
+
+# exported symbols and their signatures (the header is the source of truth;
+# tests/test_abi.py checks that every declared function is exported)
+_SIGS = {
+    "sat_abi_version": ([], _i32),
+    "sat_error_string": ([_i32], ctypes.c_char_p),
+    "sat_device_info": ([ctypes.c_int, _vp, _vp, _vp], _i32),
+    "sat_best_reset": ([_vp, _vp], _i32),
+    "sat_workspace_bytes": ([_vp, _vp], _i32),
+    "sat_search_index": ([_vp, _u64, _u64, _vp, _vp, ctypes.c_size_t, _vp], _i32),
+    "sat_search_sampled": ([_vp, _i32, _u64, _u64, _u64, _vp, _vp, ctypes.c_size_t, _vp], _i32),
+    "sat_tree_plan": ([_vp, _i32, _vp], _i32),
+    "sat_search_tree": ([_vp, _i32, _u64, _u64, _vp, _vp], _i32),
+    "sat_schedule": ([_vp, _i32, _u64, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                      ctypes.c_size_t, _vp], _i32),
+    "sat_alu_probe": ([_i32, _i32, _i32, _vp, _vp, _vp], _i32),
+}
+
+_LIB = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libsaturn_b200.so; fails loudly (no fallback) when it is not built."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(path):
+        raise E.PlanFailure(
+            f"CUDA engine not built ({path} missing); run `python -m paper_2311_02840_b200.build`")
+    lib = ctypes.CDLL(path)
+    for name, (args, res) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    if lib.sat_abi_version() != 1:
+        raise E.PlanFailure("libsaturn_b200.so ABI version mismatch")
+    _LIB = lib
+    return lib
+
+
+def _ptr(a) -> int | None:
+    return None if a is None else a.ctypes.data
+
+
+class NativeProblem:
+    """sat_problem_t over host numpy arrays (kept alive by this object)."""
+
+    def __init__(self, prob: SearchProblem, idx_bits: int):
+        grid = prob.time_mode == TIME_GRID
+        J, Cmax, N = prob.J, prob.Cmax, prob.N
+        self.radix = np.ascontiguousarray(prob.radix, dtype=np.int32)
+        self.gpus = np.ascontiguousarray(prob.gpus, dtype=np.int32)
+        self.mask = np.ascontiguousarray(prob.node_mask, dtype=np.uint32)
+        self.node_gpus = np.ascontiguousarray(prob.node_gpus, dtype=np.int32)
+        if grid:
+            self.dur = np.ascontiguousarray(prob.dur_i32, dtype=np.int32)
+            self.release = np.ascontiguousarray(prob.release_i32, dtype=np.int32)
+            self.init = np.ascontiguousarray(prob.init_free_i32, dtype=np.int32)
+        else:
+            self.dur = np.ascontiguousarray(prob.runtime, dtype=np.float64)
+            self.release = np.ascontiguousarray(prob.release_f64, dtype=np.float64)
+            self.init = np.ascontiguousarray(prob.init_free_f64, dtype=np.float64)
+        s = SatProblem()
+        s.J, s.N, s.G, s.Cmax = J, N, prob.G, Cmax
+        s.time_mode = SAT_TIME_GRID_I32 if grid else SAT_TIME_F64
+        s.idx_bits = idx_bits
+        s.radix, s.gpus, s.node_mask = _ptr(self.radix), _ptr(self.gpus), _ptr(self.mask)
+        s.node_gpus = _ptr(self.node_gpus)
+        if grid:
+            s.dur_i32, s.release_i32, s.init_free_i32 = _ptr(self.dur), _ptr(self.release), _ptr(self.init)
+        else:
+            s.dur_f64, s.release_f64, s.init_free_f64 = _ptr(self.dur), _ptr(self.release), _ptr(self.init)
+        self.struct = s
+        self.idx_bits = idx_bits
+        self.grid = grid
+
+    @property
+    def ref(self):
+        return ctypes.byref(self.struct)
+
+    @property
+    def param_bytes(self) -> int:
+        """Bytes of problem tables that cross to the device per launch."""
+        return sum(a.nbytes for a in (self.radix, self.gpus, self.mask, self.node_gpus, self.dur,
+                                      self.release, self.init))
+
+
+@dataclass
+class SearchResult:
+    makespan: float            # grid intervals (grid mode) or seconds (float mode)
+    index: int                 # winning candidate id (index / sample counter)
+    source: int                # SRC_INDEX, SRC_SUBSTREAM, SRC_SEED
+    seed: int
+    evaluated: int             # candidates evaluated by all ranks
+    kernel: str                # "tree", "index", "sampled"
+    exhaustive: bool
+    launches: int              # engine kernel launches on this rank
+    job_steps: int = 0         # list-scheduling placements (tree walk) on all ranks
+    device_seconds: float = 0.0
+    wall_seconds: float = 0.0
+
+
+class Engine:
+    """One engine per process / CUDA device."""
+
+    def __init__(self, device=None):
+        import torch
+
+        if not torch.cuda.is_available():
+            raise E.PlanFailure("no CUDA device: the plan-search engine has no CPU fallback")
+        self.torch = torch
+        self.lib = load_library()
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None
+                                   else torch.device(device).index or 0)
+        sm = ctypes.c_int32()
+        self._check(self.lib.sat_device_info(self.device.index, ctypes.byref(sm), None, None))
+        self.sm_count = sm.value
+        self._best = torch.empty(2, dtype=torch.int64, device=self.device)
+        self._ws = None
+        self.launches = 0
+
+    # ---- plumbing ----------------------------------------------------------
+    def _check(self, st: int, err=E, what: str = "engine call"):
+        if st == SAT_OK:
+            return
+        msg = f"{what}: {self.lib.sat_error_string(st).decode()}" if hasattr(self, "lib") else what
+        if st == SAT_ERR_NO_OPTIONS:
+            raise err.NoFeasibleConfig("<job>")
+        if st == SAT_ERR_INVALID:
+            raise err.InvariantViolation("problem", msg)
+        if st in (SAT_ERR_TOO_LARGE, SAT_ERR_UNSUPPORTED):
+            raise err.TooLarge(msg)
+        raise err.PlanFailure(msg)
+
+    def stream(self) -> int:
+        return self.torch.cuda.current_stream(self.device).cuda_stream
+
+    def workspace(self, nprob: NativeProblem):
+        nbytes = ctypes.c_size_t()
+        self._check(self.lib.sat_workspace_bytes(nprob.ref, ctypes.byref(nbytes)))
+        need = int(nbytes.value)
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = self.torch.empty(max(need, 1 << 16), dtype=self.torch.uint8, device=self.device)
+        return self._ws.data_ptr(), self._ws.numel()
+
+    def reset_best(self, best=None):
+        best = self._best if best is None else best
+        self._check(self.lib.sat_best_reset(_vp(best.data_ptr()), _vp(self.stream())))
+        return best
+
+    # ---- kernels -------------------------------------------------------------
+    def tree_plan(self, nprob: NativeProblem, prefix_len: int = 0) -> SatTreeInfo:
+        info = SatTreeInfo()
+        self._check(self.lib.sat_tree_plan(nprob.ref, prefix_len, ctypes.byref(info)), what="sat_tree_plan")
+        return info
+
+    def search_tree(self, nprob, prefix_len, task_lo, task_hi, best=None):
+        best = self._best if best is None else best
+        self._check(self.lib.sat_search_tree(nprob.ref, prefix_len, task_lo, task_hi,
+                                             _vp(best.data_ptr()), _vp(self.stream())), what="sat_search_tree")
+        self.launches += 1
+
+    def search_index(self, nprob, lo, hi, best=None):
+        best = self._best if best is None else best
+        ws, wsb = self.workspace(nprob)
+        self._check(self.lib.sat_search_index(nprob.ref, lo, hi, _vp(best.data_ptr()), _vp(ws), wsb,
+                                              _vp(self.stream())), what="sat_search_index")
+        self.launches += 1 if nprob.grid else 2
+
+    def search_sampled(self, nprob, source, seed, lo, hi, best=None):
+        best = self._best if best is None else best
+        ws, wsb = self.workspace(nprob)
+        self._check(self.lib.sat_search_sampled(nprob.ref, source, seed & ((1 << 64) - 1), lo, hi,
+                                                _vp(best.data_ptr()), _vp(ws), wsb, _vp(self.stream())),
+                    what="sat_search_sampled")
+        self.launches += 1 if nprob.grid else 2
+
+    def schedule(self, nprob: NativeProblem, source: int, seed: int = 0, ids=None, explicit=None):
+        """Per-candidate (option, node, start) [n, J] and makespan [n], as numpy arrays."""
+        torch = self.torch
+        J = nprob.struct.J
+        if source == SRC_EXPLICIT:
+            ex = torch.as_tensor(np.ascontiguousarray(explicit, dtype=np.uint8)).to(self.device)
+            n = ex.shape[0]
+            ids_t = None
+        else:
+            ids_t = torch.as_tensor(np.asarray(ids, dtype=np.uint64).view(np.int64)).to(self.device)
+            n = ids_t.numel()
+            ex = None
+        opt = torch.empty((n, J), dtype=torch.int32, device=self.device)
+        node = torch.empty((n, J), dtype=torch.int32, device=self.device)
+        if nprob.grid:
+            start = torch.empty((n, J), dtype=torch.int32, device=self.device)
+            ms = torch.empty(n, dtype=torch.int64, device=self.device)
+        else:
+            start = torch.empty((n, J), dtype=torch.float64, device=self.device)
+            ms = torch.empty(n, dtype=torch.float64, device=self.device)
+        ws, wsb = self.workspace(nprob)
+        g = nprob.grid
+        self._check(self.lib.sat_schedule(
+            nprob.ref, source, seed & ((1 << 64) - 1),
+            _vp(ids_t.data_ptr()) if ids_t is not None else None,
+            _vp(ex.data_ptr()) if ex is not None else None, n,
+            _vp(opt.data_ptr()), _vp(node.data_ptr()),
+            _vp(start.data_ptr()) if g else None, None if g else _vp(start.data_ptr()),
+            _vp(ms.data_ptr()) if g else None, None if g else _vp(ms.data_ptr()),
+            _vp(ws), wsb, _vp(self.stream())), what="sat_schedule")
+        self.launches += 1
+        return opt.cpu().numpy(), node.cpu().numpy(), start.cpu().numpy(), ms.cpu().numpy()
+
+    # ---- orchestration ---------------------------------------------------------
+    def plan_search(self, prob: SearchProblem, opts: SolveOptions, group=None) -> tuple:
+        """Choose kernel + index encoding for a problem: returns (mode, n_indices, prefix)."""
+        space = prob.space
+        mode = opts.search
+        if mode == "auto":
+            mode = "exhaustive" if space <= opts.max_exhaustive else "sampled"
+        if mode == "exhaustive":
+            if space > (1 << 62):
+                raise E.errors_for(prob.jobs[0]).TooLarge(f"exhaustive space {space} exceeds 2^62")
+            return mode, space
+        return mode, int(opts.budget)
+
+    def search(self, prob: SearchProblem, opts: SolveOptions, group=None, source: int | None = None,
+               seed: int | None = None, lo: int | None = None, hi: int | None = None) -> SearchResult:
+        """Run one solve's search on this rank's shard and combine across ranks (NCCL MIN)."""
+        torch = self.torch
+        err = E.errors_for(prob.jobs[0]) if prob.jobs else E
+        t0 = time.perf_counter()
+        mode, n_idx = self.plan_search(prob, opts)
+        rank, world = _rank_world(group)
+        idx_bits, _ = prob.key_bits(n_idx)
+        nprob = NativeProblem(prob, idx_bits)
+        launches0 = self.launches
+        best = self.reset_best()
+        job_steps = 0
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        if mode == "exhaustive":
+            src = SRC_INDEX
+            use_tree = opts.kernel in ("auto", "tree") and self._tree_ok(prob)
+            if opts.kernel == "tree" and not use_tree:
+                raise err.TooLarge("tree kernel needs one node, grid time, 3..20 jobs")
+            if use_tree:
+                info = self.tree_plan(nprob)
+                a, b = _shard(info.n_tasks, rank, world)
+                self.search_tree(nprob, info.prefix_len, a, b, best)
+                kernel, evaluated, job_steps = "tree", info.n_candidates, info.n_job_steps
+            else:
+                a, b = _shard(n_idx, rank, world)
+                self.search_index(nprob, a, b, best)
+                kernel, evaluated = "index", n_idx
+            seed_used = 0
+        else:
+            src = SRC_SUBSTREAM if source is None else source
+            seed_used = opts.seed if seed is None else seed
+            base_lo = 0 if lo is None else lo
+            base_hi = n_idx if hi is None else hi
+            a, b = _shard(base_hi - base_lo, rank, world)
+            self.search_sampled(nprob, src, seed_used, base_lo + a, base_lo + b, best)
+            kernel, evaluated = "sampled", base_hi - base_lo
+        ev1.record()
+        key = _combine(best, nprob.grid, group, world)
+        ev1.synchronize()
+        dev_s = ev0.elapsed_time(ev1) / 1e3
+        if nprob.grid:
+            k = int(key[0])
+            if k == INT64_MAX:
+                raise err.PlanFailure("search produced no candidate")
+            makespan = float(k >> idx_bits)
+            index = k & ((1 << idx_bits) - 1)
+        else:
+            hi_bits, index = int(key[0]), int(key[1])
+            if hi_bits == INT64_MAX:
+                raise err.PlanFailure("search produced no candidate")
+            makespan = float(np.array([hi_bits], dtype=np.int64).view(np.float64)[0])
+        return SearchResult(makespan=makespan, index=index, source=src, seed=seed_used, evaluated=evaluated,
+                            kernel=kernel, exhaustive=mode == "exhaustive",
+                            launches=self.launches - launches0, job_steps=job_steps,
+                            device_seconds=dev_s, wall_seconds=time.perf_counter() - t0)
+
+    @staticmethod
+    def _tree_ok(prob: SearchProblem) -> bool:
+        return (prob.N == 1 and prob.time_mode == TIME_GRID and 3 <= prob.J <= 20
+                and not prob.release_i32.any() and int(prob.radix.sum()) <= 384)
+
+
+def _rank_world(group):
+    try:
+        import torch.distributed as dist
+    except Exception:  # pragma: no cover
+        return 0, 1
+    if not (dist.is_available() and dist.is_initialized()):
+        return 0, 1
+    return dist.get_rank(group), dist.get_world_size(group)
+
+
+def _shard(n: int, rank: int, world: int) -> tuple:
+    """Contiguous block partition of [0, n)."""
+    return (n * rank) // world, (n * (rank + 1)) // world
+
+
+def _combine(best, grid: bool, group, world: int):
+    """All-reduce MIN of the packed key (grid) or of (makespan bits, then index) (float)."""
+    import torch
+
+    key = best.clone()
+    empty = key == -1                                   # all-ones = nothing found on this rank
+    key = torch.where(empty, torch.full_like(key, INT64_MAX), key)
+    if world > 1:
+        import torch.distributed as dist
+
+        if grid:
+            dist.all_reduce(key[:1], op=dist.ReduceOp.MIN, group=group)
+        else:
+            ms = key[:1].clone()
+            dist.all_reduce(ms, op=dist.ReduceOp.MIN, group=group)
+            idx = torch.where(key[:1] == ms, key[1:], torch.full_like(key[1:], INT64_MAX))
+            dist.all_reduce(idx, op=dist.ReduceOp.MIN, group=group)
+            key = torch.cat([ms, idx])
+    return key.cpu().tolist()

@@ -1,0 +1,337 @@
+"""Planners on the B200 engine -- the reference's Solver / baseline API.
+
+  plan_saturn(table, jobs, cluster, delta_opts, running_context)
+  resolve(...)          = plan_saturn with a RunningContext
+  plan_random(table, jobs, cluster, seed)
+  plan_random_best(...) best of a batch of seeds (Random over >=1e9 seeds)
+  optimus_marginal_gain / plan_optimus
+  plan_current_practice
+
+``jobs`` may be a workload (anything with ``jobs``, ``cluster`` and
+``techniques``) or a job list with ``cluster`` and ``techniques=`` given.  The
+objects may be this package's dataclasses or the reference's pydantic models;
+the returned Plan is of the caller's type family.
+
+Every candidate plan is list-scheduled on the GPU; the host only marshals the
+table (problem.py), runs the O(J x G) Optimus allocator, and turns the
+engine's winner into a Plan.
+"""
+
+from __future__ import annotations
+
+import sys
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import domain as D
+from . import errors as E
+from .engine import SRC_EXPLICIT, SRC_INDEX, SRC_SEED, SRC_SUBSTREAM, Engine, NativeProblem, SearchResult
+from .problem import TIME_GRID, SearchProblem, SolveOptions, build_problem
+
+_ENGINES: dict = {}
+
+
+def get_engine(device=None) -> Engine:
+    import torch
+
+    idx = torch.cuda.current_device() if device is None else (torch.device(device).index or 0)
+    eng = _ENGINES.get(idx)
+    if eng is None:
+        eng = _ENGINES[idx] = Engine(idx)
+    return eng
+
+
+@dataclass
+class _WorkloadView:
+    jobs: tuple
+    cluster: object
+    techniques: tuple
+
+
+def _as_workload(jobs, cluster=None, techniques=None):
+    if hasattr(jobs, "jobs") and hasattr(jobs, "cluster"):
+        return jobs
+    if cluster is None or techniques is None:
+        raise E.InvariantViolation("workload", "pass a workload, or jobs with cluster and techniques")
+    return _WorkloadView(tuple(jobs), cluster, tuple(techniques))
+
+
+def _types_for(workload):
+    """(Plan, PlanEntry, RunConfig) classes of the caller's domain family."""
+    probe = workload.jobs[0] if workload.jobs else workload
+    mod = sys.modules.get(type(probe).__module__)
+    if mod is not None and all(hasattr(mod, n) for n in ("Plan", "PlanEntry", "RunConfig")):
+        return mod.Plan, mod.PlanEntry, mod.RunConfig
+    return D.Plan, D.PlanEntry, D.RunConfig
+
+
+def _opts(delta_opts) -> SolveOptions:
+    if delta_opts is None:
+        return SolveOptions()
+    if isinstance(delta_opts, SolveOptions):
+        return delta_opts
+    if isinstance(delta_opts, dict):
+        return SolveOptions(**delta_opts)
+    if isinstance(delta_opts, (int, float)):
+        return SolveOptions(delta=float(delta_opts))
+    raise E.InvariantViolation("delta_opts", f"unsupported {type(delta_opts).__name__}")
+
+
+@dataclass
+class Solution:
+    """A plan plus how it was found (the reference's MilpSolution analogue)."""
+
+    plan: object
+    status: str                 # "Optimal" (whole space scanned) or "Sampled"
+    makespan: float             # grid intervals or seconds
+    objective: float            # seconds (= plan.predicted_makespan)
+    problem: SearchProblem
+    search: SearchResult | None
+    options: list               # option digit per job (problem's job axis)
+    order: list                 # submission order (job axis indices)
+    runtimes: dict = field(default_factory=dict)   # job id -> seconds of the chosen option/node
+
+
+def _decode(engine: Engine, prob: SearchProblem, nprob: NativeProblem, workload, source: int, seed: int,
+            ident=None, explicit=None):
+    """Replay one candidate on the device; build the Plan."""
+    opt, node, start, ms = engine.schedule(nprob, source, seed,
+                                           ids=None if ident is None else [ident],
+                                           explicit=None if explicit is None else explicit[None, :])
+    Plan, PlanEntry, RunConfig = _types_for(workload)
+    grid = prob.time_mode == TIME_GRID
+    scale = prob.delta if grid else 1.0
+    entries, runtimes = {}, {}
+    for j, job_id in enumerate(prob.job_ids):
+        o, n = int(opt[0, j]), int(node[0, j])
+        cfg = prob.options[j][o][0]
+        s = float(start[0, j]) * scale
+        entries[job_id] = PlanEntry(config=RunConfig(technique=cfg.technique, gpus=cfg.gpus),
+                                    node=prob.node_ids[n], start_time=s)
+        runtimes[job_id] = float(prob.runtime[j, o, n])
+    predicted = float(ms[0]) * scale
+    plan = Plan(entries=entries, predicted_makespan=predicted)
+    return plan, [int(x) for x in opt[0]], float(ms[0]), runtimes
+
+
+def solve(table, jobs, cluster=None, delta_opts=None, running_context=None, *, techniques=None,
+          group=None, device=None, validate: bool = True) -> Solution:
+    """Solver.solve / re-solve on the engine (build -> search -> decode -> check)."""
+    workload = _as_workload(jobs, cluster, techniques)
+    err = E.errors_for(workload.jobs[0] if workload.jobs else workload)
+    opts = _opts(delta_opts)
+    prob = build_problem(table, workload, opts, running_context)
+    eng = get_engine(device)
+    try:
+        res = eng.search(prob, opts, group=group)
+        idx_bits, _ = prob.key_bits(res.evaluated if not res.exhaustive else prob.space)
+        nprob = NativeProblem(prob, idx_bits)
+        src = SRC_INDEX if res.exhaustive else res.source
+        plan, options, ms, runtimes = _decode(eng, prob, nprob, workload, src, res.seed, ident=res.index)
+    except E.SchedulerError:
+        raise
+    except Exception as exc:  # CUDA / NCCL trouble -> PlanFailure (ReplanFailure on re-solve)
+        cls = err.ReplanFailure if running_context is not None else err.PlanFailure
+        raise cls(f"engine failure: {exc}") from exc
+    if ms != res.makespan:
+        raise err.PlanFailure(f"winner replay makespan {ms} != search makespan {res.makespan}")
+    if res.exhaustive:
+        order = prob.decode_index(res.index)[1]
+    else:
+        order = sorted(range(prob.J), key=lambda j: (plan.entries[prob.job_ids[j]].start_time, j))
+    if validate and running_context is None:
+        D.check_plan(plan, workload, runtimes)
+    return Solution(plan=plan, status="Optimal" if res.exhaustive else "Sampled", makespan=res.makespan,
+                    objective=plan.predicted_makespan, problem=prob, search=res, options=options,
+                    order=order, runtimes=runtimes)
+
+
+def plan_saturn(table, jobs, cluster=None, delta_opts=None, running_context=None, *, techniques=None,
+                group=None, device=None):
+    """the joint (technique, GPU count, order) optimum as a Plan."""
+    return solve(table, jobs, cluster, delta_opts, running_context, techniques=techniques,
+                 group=group, device=device).plan
+
+
+def resolve(table, workload, running_context, delta_opts=None, *, group=None, device=None):
+    """Introspection re-solve: all unfinished jobs re-planned from now
+    (start times relative to the tick); a running job pays rho on any option whose
+    (technique, g, node) differs from what it holds."""
+    return solve(table, workload, None, delta_opts, running_context, group=group, device=device)
+
+
+# --------------------------------------------------------------------------
+# Random baseline on the same engine
+# --------------------------------------------------------------------------
+
+def _baseline_problem(table, workload, opts, running_context=None) -> SearchProblem:
+    """Baselines choose among ALL feasible entries (no dominance prune)."""
+    o = SolveOptions(**{**opts.__dict__, "prune": False})
+    return build_problem(table, workload, o, running_context)
+
+
+def plan_random(table, jobs, cluster=None, seed: int = 0, delta_opts=None, running_context=None, *,
+                techniques=None, device=None):
+    """SplitMix64(seed): one below(|C_j|) per job in id order, then shuffle(order); list-scheduled."""
+    workload = _as_workload(jobs, cluster, techniques)
+    opts = _opts(delta_opts)
+    prob = _baseline_problem(table, workload, opts, running_context)
+    eng = get_engine(device)
+    nprob = NativeProblem(prob, 62)
+    plan, _, _, _ = _decode(eng, prob, nprob, workload, SRC_SEED, seed, ident=0)
+    return plan
+
+
+def plan_random_best(table, jobs, cluster=None, seed0: int = 0, n_seeds: int = 1 << 20, delta_opts=None, *,
+                     techniques=None, group=None, device=None) -> Solution:
+    """Best Random plan over seeds seed0 .. seed0+n_seeds-1 (lowest seed on ties)."""
+    workload = _as_workload(jobs, cluster, techniques)
+    opts = _opts(delta_opts)
+    prob = _baseline_problem(table, workload, opts)
+    eng = get_engine(device)
+    sopts = SolveOptions(**{**opts.__dict__, "search": "sampled", "budget": n_seeds})
+    res = eng.search(prob, sopts, group=group, source=SRC_SEED, seed=seed0)
+    idx_bits, _ = prob.key_bits(n_seeds)
+    nprob = NativeProblem(prob, idx_bits)
+    plan, options, ms, runtimes = _decode(eng, prob, nprob, workload, SRC_SEED, seed0, ident=res.index)
+    return Solution(plan=plan, status="Sampled", makespan=ms, objective=plan.predicted_makespan, problem=prob,
+                    search=res, options=options, order=[], runtimes=runtimes)
+
+
+# --------------------------------------------------------------------------
+# Optimus -- host allocator, device schedule
+# --------------------------------------------------------------------------
+
+def _best_runtime_by_g(prob: SearchProblem, j: int) -> dict:
+    """g -> (runtime seconds, option) minimising runtime over techniques at that g
+    (earliest option on ties); runtime on the job's fastest eligible node."""
+    out: dict = {}
+    for o in range(int(prob.radix[j])):
+        g = int(prob.gpus[j, o])
+        rts = [prob.runtime[j, o, n] for n in range(prob.N) if (int(prob.node_mask[j, o]) >> n) & 1]
+        rt = min(rts)
+        if g not in out or rt < out[g][0]:
+            out[g] = (rt, o)
+    return out
+
+
+def optimus_marginal_gain(prob: SearchProblem, j: int, g: int, best=None) -> float:
+    """best_runtime(g) - best_runtime(g+1), clamped at 0; 0 if g+1 is infeasible."""
+    best = best if best is not None else _best_runtime_by_g(prob, j)
+    if g not in best or (g + 1) not in best:
+        return 0.0
+    return max(0.0, best[g][0] - best[g + 1][0])
+
+
+def optimus_allocation(prob: SearchProblem) -> tuple:
+    """(option per job, submission order) of the Optimus baseline.
+
+    Waves: jobs FIFO (id order) while the sum of their minimum feasible g fits the
+    cluster's GPUs; each gets its min g, then free GPUs go one at a time to the job
+    with the largest marginal gain (lower job first on ties) while the gain is > 0.
+    Order: wave, then descending g, then job id."""
+    J = prob.J
+    total = int(prob.node_gpus.sum())
+    node_max = int(prob.node_gpus.max())
+    best = [_best_runtime_by_g(prob, j) for j in range(J)]
+    gmin = [min(b) for b in best]
+    alloc = [0] * J
+    waves = []
+    j = 0
+    while j < J:
+        wave = [j]
+        used = gmin[j]
+        j += 1
+        while j < J and used + gmin[j] <= total:
+            used += gmin[j]
+            wave.append(j)
+            j += 1
+        for k in wave:
+            alloc[k] = gmin[k]
+        free = total - used
+        while free > 0:
+            pick, pick_gain = -1, 0.0
+            for k in wave:
+                if alloc[k] + 1 > node_max:
+                    continue
+                gain = optimus_marginal_gain(prob, k, alloc[k], best[k])
+                if gain > pick_gain:
+                    pick, pick_gain = k, gain
+            if pick < 0:
+                break
+            alloc[pick] += 1
+            free -= 1
+        waves.append(wave)
+    options = [best[k][alloc[k]][1] for k in range(J)]
+    order = []
+    for wave in waves:
+        order.extend(sorted(wave, key=lambda k: (-alloc[k], k)))
+    return options, order
+
+
+def _explicit_solution(table, workload, opts, running_context, builder, device) -> Solution:
+    prob = _baseline_problem(table, workload, opts, running_context)
+    options, order = builder(prob)
+    eng = get_engine(device)
+    nprob = NativeProblem(prob, 62)
+    explicit = np.array(list(options) + list(order), dtype=np.uint8)
+    plan, opts_out, ms, runtimes = _decode(eng, prob, nprob, workload, SRC_EXPLICIT, 0, explicit=explicit)
+    return Solution(plan=plan, status="Fixed", makespan=ms, objective=plan.predicted_makespan, problem=prob,
+                    search=None, options=opts_out, order=list(order), runtimes=runtimes)
+
+
+def plan_optimus(table, jobs, cluster=None, delta_opts=None, running_context=None, *, techniques=None,
+                 device=None):
+    workload = _as_workload(jobs, cluster, techniques)
+    return _explicit_solution(table, workload, _opts(delta_opts), running_context, optimus_allocation,
+                              device).plan
+
+
+def current_practice_allocation(prob: SearchProblem) -> tuple:
+    """Each job alone on a full node (largest feasible g if a full node does not fit), fastest
+    technique at that g; jobs in id order, each on the earliest-free node."""
+    node_max = int(prob.node_gpus.max())
+    options = []
+    for j in range(prob.J):
+        best = _best_runtime_by_g(prob, j)
+        g = node_max if node_max in best else max(best)
+        options.append(best[g][1])
+    return options, list(range(prob.J))
+
+
+def plan_current_practice(table, jobs, cluster=None, delta_opts=None, *, techniques=None, device=None):
+    workload = _as_workload(jobs, cluster, techniques)
+    return _explicit_solution(table, workload, _opts(delta_opts), None, current_practice_allocation,
+                              device).plan
+
+
+def evaluate_fixed(table, workload, options, order, delta_opts=None, running_context=None, device=None,
+                   prune: bool = False) -> Solution:
+    """Schedule one explicit (options, order) candidate on the engine."""
+    opts = _opts(delta_opts)
+    if prune:
+        prob = build_problem(table, workload, opts, running_context)
+        builder_prob = prob
+    else:
+        builder_prob = None
+
+    def builder(_prob):
+        return list(options), list(order)
+
+    if builder_prob is None:
+        return _explicit_solution(table, workload, opts, running_context, builder, device)
+    eng = get_engine(device)
+    nprob = NativeProblem(builder_prob, 62)
+    explicit = np.array(list(options) + list(order), dtype=np.uint8)
+    plan, opts_out, ms, runtimes = _decode(eng, builder_prob, nprob, workload, SRC_EXPLICIT, 0,
+                                           explicit=explicit)
+    return Solution(plan=plan, status="Fixed", makespan=ms, objective=plan.predicted_makespan,
+                    problem=builder_prob, search=None, options=opts_out, order=list(order), runtimes=runtimes)
+
+
+__all__ = [
+    "Solution", "solve", "plan_saturn", "resolve", "plan_random", "plan_random_best",
+    "optimus_marginal_gain", "optimus_allocation", "plan_optimus", "current_practice_allocation",
+    "plan_current_practice", "evaluate_fixed", "get_engine",
+]

@@ -1,0 +1,314 @@
+"""Marshal (profile table, workload, re-solve context) into the engine's dense problem.
+
+This is the host half of the Solver's ``build_milp`` step (SPEC.md:192-196,
+244-249) restricted to what the list-scheduling search needs:
+
+* option lists per job: ``feasible_entries`` order (profiling.py:154-161),
+  optionally reduced by an exact dominance prune (single node only);
+* runtimes ``T = remaining x latency`` (profiling.py:147-151) plus the
+  checkpoint cost rho for a running job whose (technique, g, node) changes
+  (core.py:211-223);
+* the time grid ``delta = max(sum_j min T / K_max, min_j min T / 4)``
+   and grid durations ``d = ceil(T / delta)``,
+  computed once here in float64 and shipped as integers -- the device never
+  recomputes them;
+* the candidate index space of SURVEY.md Appendix A1:
+  ``index = c * J! + p`` with ``c`` the mixed-radix option code (job 0 most
+  significant) and ``p`` the lexicographic (Lehmer) rank of the order.
+
+Everything here runs once per solve; the per-candidate work is on the device.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import errors as E
+from .domain import RunConfig, node_eligible
+from .profiling import INFEASIBLE
+
+TIME_GRID = "grid"
+TIME_FLOAT = "float"
+K_MAX_DEFAULT = 48
+INF_I32 = 0x3FFFFFFF        # device "never free" sentinel (ghost slots)
+MAX_LANES = 32              # nodes x padded GPUs must fit one warp
+
+
+@dataclass
+class SolveOptions:
+    """The reference's delta_opts plus the engine's search knobs."""
+
+    time_mode: str = TIME_GRID
+    k_max: int = K_MAX_DEFAULT
+    delta: float | None = None          # explicit interval length (seconds)
+    prune: bool | None = None           # None: on for single-node clusters
+    search: str = "auto"                # auto | exhaustive | sampled
+    max_exhaustive: int = 1 << 42       # auto -> exhaustive when the space is <= this
+    budget: int = 1 << 28               # sampled candidates when not exhaustive
+    seed: int = 7                       # sampled stream: candidate i = substream(seed, i)
+    kernel: str = "auto"                # auto | tree | index (exhaustive kernel family)
+
+
+@dataclass
+class SearchProblem:
+    job_ids: list
+    jobs: list
+    node_ids: list
+    node_gpus: np.ndarray          # int32 [N]
+    G: int                         # padded slots per node (power of two)
+    W: int                         # lanes per candidate segment (8, 16 or 32)
+    options: list                  # per job: [(RunConfig, latency)] after prune
+    option_src: list               # per job: index of each kept option in feasible_entries
+    radix: np.ndarray              # int32 [J]
+    gpus: np.ndarray               # int32 [J, Cmax]
+    node_mask: np.ndarray          # uint32 [J, Cmax]  bit n = option runnable on node n
+    runtime: np.ndarray            # float64 [J, Cmax, N] seconds (0 where not runnable)
+    dur_i32: np.ndarray            # int32 [J, Cmax, N] grid intervals
+    release_i32: np.ndarray        # int32 [J]
+    release_f64: np.ndarray        # float64 [J]
+    init_free_i32: np.ndarray      # int32 [N, G] ascending per node, INF on ghost slots
+    init_free_f64: np.ndarray      # float64 [N, G]
+    time_mode: str
+    delta: float
+    pruned: bool
+    resolve: bool = False
+    extra: dict = field(default_factory=dict)
+
+    # ---- derived sizes -------------------------------------------------
+    @property
+    def J(self) -> int:
+        return len(self.job_ids)
+
+    @property
+    def N(self) -> int:
+        return len(self.node_ids)
+
+    @property
+    def Cmax(self) -> int:
+        return int(self.gpus.shape[1])
+
+    @property
+    def space(self) -> int:
+        """Number of exhaustive candidates: prod(radix) * J!."""
+        return math.prod(int(r) for r in self.radix) * math.factorial(self.J)
+
+    def weights(self) -> list:
+        """Mixed-radix weight of each job's option digit (job 0 most significant)."""
+        w, out = 1, [0] * self.J
+        for j in range(self.J - 1, -1, -1):
+            out[j] = w
+            w *= int(self.radix[j])
+        return out
+
+    def makespan_bound(self) -> int:
+        """Upper bound on any grid makespan (sum of worst durations + offsets)."""
+        worst = int(self.dur_i32.reshape(self.J, -1).max(axis=1).sum()) if self.J else 0
+        real = self.init_free_i32[self.init_free_i32 < INF_I32]
+        return worst + int(real.max() if real.size else 0) + int(self.release_i32.max() if self.J else 0)
+
+    def key_bits(self, n_indices: int) -> tuple:
+        """(idx_bits, ms_bits) for packing (makespan << idx_bits) | index into 63 bits."""
+        idx_bits = max(1, (max(n_indices, 1) - 1).bit_length())
+        ms_bits = max(1, self.makespan_bound().bit_length())
+        if self.time_mode == TIME_GRID and idx_bits + ms_bits > 63:
+            raise E.TooLarge(f"key needs {idx_bits}+{ms_bits} bits > 63")
+        return idx_bits, ms_bits
+
+    # ---- candidate codec (host side, used only to explain results) ------
+    def decode_index(self, index: int) -> tuple:
+        """index -> (option digit per job, submission order); inverse of encode_index."""
+        J = self.J
+        conf, perm = divmod(int(index), math.factorial(J))
+        opts = [0] * J
+        for j in range(J - 1, -1, -1):
+            conf, opts[j] = divmod(conf, int(self.radix[j]))
+        pool = list(range(J))
+        order = []
+        for k in range(J):
+            f = math.factorial(J - 1 - k)
+            digit, perm = divmod(perm, f)
+            order.append(pool.pop(digit))
+        return opts, order
+
+    def encode_index(self, opts, order) -> int:
+        J = self.J
+        conf = 0
+        for j in range(J):
+            conf = conf * int(self.radix[j]) + int(opts[j])
+        pool = list(range(J))
+        rank = 0
+        for k, job in enumerate(order):
+            digit = pool.index(job)
+            pool.pop(digit)
+            rank += digit * math.factorial(J - 1 - k)
+        return conf * math.factorial(J) + rank
+
+
+def _pow2_at_least(x: int) -> int:
+    p = 1
+    while p < x:
+        p <<= 1
+    return p
+
+
+def _techniques_of(workload, table):
+    techs = getattr(workload, "techniques", None)
+    if techs:
+        return techs
+    raise E.InvariantViolation("techniques", "workload must carry its registered techniques")
+
+
+def _dominance_prune(cost_rows: list) -> list:
+    """Exact single-node prune: per g keep the cheapest option (earliest on ties), then keep
+    g only while the cost strictly decreases with g.  Returns kept option indices in their
+    original (canonical) order.  cost_rows: [(option_index, g, cost)] in canonical order."""
+    best_per_g: dict = {}
+    for idx, g, cost in cost_rows:
+        cur = best_per_g.get(g)
+        if cur is None or cost < cur[1]:
+            best_per_g[g] = (idx, cost)
+    kept, last = [], None
+    for g in sorted(best_per_g):
+        idx, cost = best_per_g[g]
+        if last is None or cost < last:
+            kept.append(idx)
+            last = cost
+    return sorted(kept)
+
+
+def choose_delta(min_runtimes: list, k_max: int = K_MAX_DEFAULT) -> float:
+    """delta = max(sequential-best total / K_max, shortest job / 4).
+    Summation is left to right in job-id order (fixed so oracle and engine agree)."""
+    total = 0.0
+    for t in min_runtimes:
+        total += t
+    return max(total / k_max, min(min_runtimes) / 4.0)
+
+
+def build_problem(table, workload, opts: SolveOptions | None = None, running_context=None,
+                  jobs=None) -> SearchProblem:
+    """Marshal one solve.  ``jobs`` restricts/reorders nothing: the job axis is always the
+    selected jobs sorted by id (SPEC.md:249 tie-break key 1)."""
+    opts = opts or SolveOptions()
+    err = E.errors_for(workload)
+    if opts.time_mode not in (TIME_GRID, TIME_FLOAT):
+        raise err.InvariantViolation("time_mode", f"unknown {opts.time_mode!r}")
+    cluster = workload.cluster
+    techniques = _techniques_of(workload, table)
+    tech_by_name = {t.name: t for t in techniques}
+    pool = list(jobs) if jobs is not None else list(workload.jobs)
+
+    if running_context is not None:
+        remaining = {k: int(v) for k, v in running_context.remaining.items() if int(v) > 0}
+        pool = [j for j in pool if j.id in remaining]
+        current = dict(running_context.current)
+        rho = float(running_context.checkpoint_cost)
+    else:
+        remaining = {j.id: int(j.total_batches) for j in pool}
+        current, rho = {}, 0.0
+    pool.sort(key=lambda j: j.id)
+    nodes = list(cluster.nodes)
+    N = len(nodes)
+    max_g = max(n.gpu_count for n in nodes)
+    G = _pow2_at_least(max_g)
+    W = max(8, _pow2_at_least(N * G))
+    if N * G > MAX_LANES:
+        raise err.TooLarge(f"{N} nodes x {G} padded GPUs exceed one warp ({MAX_LANES} lanes)")
+
+    # per job: canonical option list with per-node runtimes
+    rows = []
+    for job in pool:
+        from .profiling import feasible_entries  # local: avoid a cycle at import time
+        entries = feasible_entries(table, job, workload)
+        if not entries:
+            raise err.NoFeasibleConfig(job.id)
+        rem = remaining[job.id]
+        cur = current.get(job.id)
+        row = []
+        for cfg, lat in entries:
+            tech = tech_by_name[cfg.technique]
+            per_node = []
+            for n in nodes:
+                if not node_eligible(job, tech, cfg.gpus, n):
+                    per_node.append(INFEASIBLE)
+                    continue
+                t = rem * lat                                     # profiling.py:151
+                if cur is not None and (cfg.technique, cfg.gpus, n.id) != tuple(cur):
+                    t = t + rho
+                per_node.append(t)
+            row.append((cfg, lat, per_node))
+        if all(math.isinf(t) for _, _, pn in row for t in pn):
+            raise err.NoFeasibleConfig(job.id)
+        rows.append(row)
+
+    J = len(pool)
+    if J == 0:
+        raise err.InvariantViolation("jobs", "nothing to plan")
+    min_rt = [min(t for _, _, pn in row for t in pn) for row in rows]
+    if opts.delta is not None:
+        delta = float(opts.delta)
+        if not delta > 0:
+            raise err.InvariantViolation("delta", "must be > 0")
+        horizon = math.ceil(sum(min_rt) / delta)
+        if horizon > opts.k_max:
+            raise err.HorizonOverflow(horizon, opts.k_max)
+    else:
+        delta = choose_delta(min_rt, opts.k_max)
+
+    grid = opts.time_mode == TIME_GRID
+    prune = (N == 1) if opts.prune is None else bool(opts.prune)
+    if prune and N != 1:
+        raise err.InvariantViolation("prune", "the dominance prune is exact only on one node")
+
+    kept_rows, kept_src = [], []
+    for row in rows:
+        if prune:
+            def cost(t):
+                return math.ceil(t / delta) if grid else t
+            keep = _dominance_prune([(i, cfg.gpus, cost(pn[0])) for i, (cfg, _, pn) in enumerate(row)])
+        else:
+            keep = list(range(len(row)))
+        kept_rows.append([row[i] for i in keep])
+        kept_src.append(keep)
+
+    Cmax = max(len(r) for r in kept_rows)
+    radix = np.array([len(r) for r in kept_rows], dtype=np.int32)
+    gpus = np.zeros((J, Cmax), dtype=np.int32)
+    mask = np.zeros((J, Cmax), dtype=np.uint32)
+    runtime = np.zeros((J, Cmax, N), dtype=np.float64)
+    dur = np.zeros((J, Cmax, N), dtype=np.int32)
+    for j, row in enumerate(kept_rows):
+        for o, (cfg, _lat, per_node) in enumerate(row):
+            gpus[j, o] = cfg.gpus
+            for n, t in enumerate(per_node):
+                if math.isinf(t):
+                    continue
+                mask[j, o] |= np.uint32(1 << n)
+                runtime[j, o, n] = t
+                d = math.ceil(t / delta)
+                if d >= INF_I32 // 4:
+                    raise err.TooLarge(f"duration {d} intervals overflows the device time type")
+                dur[j, o, n] = d
+
+    init_i = np.full((N, G), INF_I32, dtype=np.int32)
+    init_f = np.full((N, G), np.inf, dtype=np.float64)
+    for n, node in enumerate(nodes):
+        init_i[n, : node.gpu_count] = 0
+        init_f[n, : node.gpu_count] = 0.0
+
+    return SearchProblem(
+        job_ids=[j.id for j in pool], jobs=pool, node_ids=[n.id for n in nodes],
+        node_gpus=np.array([n.gpu_count for n in nodes], dtype=np.int32), G=G, W=W,
+        options=[[(cfg, lat) for cfg, lat, _ in r] for r in kept_rows], option_src=kept_src,
+        radix=radix, gpus=gpus, node_mask=mask, runtime=runtime, dur_i32=dur,
+        release_i32=np.zeros(J, dtype=np.int32), release_f64=np.zeros(J, dtype=np.float64),
+        init_free_i32=init_i, init_free_f64=init_f, time_mode=opts.time_mode, delta=delta,
+        pruned=prune, resolve=running_context is not None,
+    )
+
+
+def option_config(problem: SearchProblem, j: int, o: int) -> RunConfig:
+    return problem.options[j][o][0]

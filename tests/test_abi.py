@@ -1,0 +1,84 @@
+"""The C-ABI library builds for sm_100a, loads, and exports every symbol include/ declares.
+
+No compute call needs a GPU here: only the pure-host entry points are exercised."""
+
+import ctypes
+import math
+import os
+import re
+
+import pytest
+
+from helpers import golden_workload
+
+from paper_2311_02840_b200 import build as B
+from paper_2311_02840_b200 import engine as EN
+from paper_2311_02840_b200.problem import build_problem
+from paper_2311_02840_b200.profiling import SyntheticExecutor, build_profile_table
+
+HEADER = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "saturn_engine.h")
+
+
+def declared():
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:int|const char \*)\s*(sat_\w+)\s*\(", txt, re.M)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    B.build()
+    return EN.load_library()
+
+
+def test_header_declarations_bound(lib):
+    names = declared()
+    assert len(names) >= 10
+    for n in names:
+        assert hasattr(lib, n), n
+        assert n in EN._SIGS, f"{n} not bound in engine._SIGS"
+
+
+def test_host_only_entry_points(lib):
+    assert lib.sat_abi_version() == 1
+    for st in range(6):
+        assert lib.sat_error_string(st)
+
+
+def test_sass_is_sm100a():
+    out = os.popen(f"cuobjdump --list-elf {B.OUT} 2>&1").read()
+    assert "sm_100a" in out
+
+
+def test_tree_plan_layout_host_only(lib):
+    w, _ = golden_workload("cfg1")
+    t = build_profile_table(w, SyntheticExecutor(w.cluster))
+    prob = build_problem(t, w)
+    nprob = EN.NativeProblem(prob, 35)
+    info = EN.SatTreeInfo()
+    assert lib.sat_tree_plan(nprob.ref, 0, ctypes.byref(info)) == 0
+    assert info.n_candidates == prob.space == 32514048000
+    assert info.prefix_len == 5 and info.n_sets == math.comb(8, 5)
+    assert info.n_tasks >= 1 << 17
+    # placements of the prefix-shared walk are far fewer than J per candidate
+    assert prob.space < info.n_job_steps < 2 * prob.space
+    for P in (1, 3, 6):
+        assert lib.sat_tree_plan(nprob.ref, P, ctypes.byref(info)) == 0
+        assert info.prefix_len == P and info.n_candidates == prob.space
+    assert lib.sat_tree_plan(nprob.ref, 7, ctypes.byref(info)) == EN.SAT_ERR_INVALID
+
+
+def test_validation_codes(lib):
+    w, _ = golden_workload("small5_1x4")
+    t = build_profile_table(w, SyntheticExecutor(w.cluster))
+    prob = build_problem(t, w)
+    nprob = EN.NativeProblem(prob, 20)
+    info = EN.SatTreeInfo()
+    nprob.radix[2] = 0
+    assert lib.sat_tree_plan(nprob.ref, 0, ctypes.byref(info)) == EN.SAT_ERR_NO_OPTIONS
+    nprob.radix[2] = prob.radix[2]
+    nprob.struct.G = 3
+    assert lib.sat_tree_plan(nprob.ref, 0, ctypes.byref(info)) == EN.SAT_ERR_INVALID
+    w4, _ = golden_workload("small4_2x2")
+    t4 = build_profile_table(w4, SyntheticExecutor(w4.cluster))
+    p4 = EN.NativeProblem(build_problem(t4, w4), 20)
+    assert lib.sat_tree_plan(p4.ref, 0, ctypes.byref(info)) == EN.SAT_ERR_UNSUPPORTED

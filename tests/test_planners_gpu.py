@@ -1,0 +1,137 @@
+"""End-to-end planners on the GPU engine: reference-facing API, plan validity, SPEC examples."""
+
+import math
+
+import numpy as np
+import pytest
+
+from helpers import golden, golden_workload, import_reference, reference_available
+
+from oracle import coracle as C
+from oracle import saturn_oracle as O
+import paper_2311_02840_b200 as S
+from paper_2311_02840_b200 import domain as D
+from paper_2311_02840_b200 import planners as PL
+from paper_2311_02840_b200.problem import SolveOptions
+from paper_2311_02840_b200.profiling import ProfileTable, SyntheticExecutor, build_profile_table
+
+pytestmark = pytest.mark.gpu
+
+
+def setup(name):
+    w, _ = golden_workload(name)
+    return w, build_profile_table(w, SyntheticExecutor(w.cluster))
+
+
+def test_plan_saturn_cfg1_optimal_and_valid():
+    w, t = setup("cfg1")
+    sol = PL.solve(t, w)
+    assert sol.status == "Optimal"
+    assert sol.makespan == 30 == golden()["milp"]["cfg1"]["optimum_intervals"]
+    assert sol.search.kernel == "tree" and sol.search.evaluated == 32514048000
+    D.check_plan(sol.plan, w, sol.runtimes)
+    assert math.isclose(sol.plan.predicted_makespan, 30 * sol.problem.delta)
+    # the decoded plan is exactly the oracle's replay of the winning index
+    op = O.build(t.entries, w)
+    opts, order = O.decode_index(op, sol.search.index)
+    ms, starts, nodes = C.CProblem(op).eval(opts, order)
+    for j, jid in enumerate(op.job_ids):
+        e = sol.plan.entries[jid]
+        assert (e.config.technique, e.config.gpus) == op.options[j][opts[j]]
+        assert e.start_time == starts[j] * op.delta
+
+
+def test_spec_two_job_example():
+    """SPEC.md:199/283/292/373: Saturn makespan 10, Current Practice 12, Optimus 10."""
+    techs = (D.TechniqueSpec(name="t", archetype="sharded", serial_fraction=0.0, comm_overhead=0.0),)
+    jobs = (D.JobSpec("a", 1, 1.0, 1.0), D.JobSpec("b", 1, 1.0, 1.0))
+    cl = D.ClusterSpec((D.NodeSpec("n", 2, 80.0),))
+    w = D.Workload(jobs, cl, techs)
+    t = ProfileTable({("a", "t", 1): 10.0, ("a", "t", 2): 6.0, ("b", "t", 1): 10.0, ("b", "t", 2): 6.0}, "ingested")
+    opts = SolveOptions(delta=1.0, k_max=1000)
+    sat = S.plan_saturn(t, w, None, opts)
+    assert sat.predicted_makespan == 10.0
+    assert all(e.config.gpus == 1 and e.start_time == 0 for e in sat.entries.values())
+    cp = S.plan_current_practice(t, w, None, opts)
+    assert cp.predicted_makespan == 12.0
+    opt = S.plan_optimus(t, w, None, opts)
+    assert opt.predicted_makespan == 10.0
+    # one job -> its best config at t=0
+    w1 = D.Workload(jobs[:1], cl, techs)
+    p1 = S.plan_saturn(t, w1, None, opts)
+    assert p1.entries["a"].config.gpus == 2 and p1.entries["a"].start_time == 0.0
+
+
+@pytest.mark.parametrize("name", ["cfg3", "cfg4", "cfg5"])
+def test_sampled_saturn_and_baselines(name):
+    w, t = setup(name)
+    sol = PL.solve(t, w, None, SolveOptions(search="sampled", budget=200000))
+    assert sol.status == "Sampled"
+    D.check_plan(sol.plan, w, sol.runtimes)
+    opt = PL._explicit_solution(t, w, SolveOptions(), None, PL.optimus_allocation, None)
+    cp = PL._explicit_solution(t, w, SolveOptions(), None, PL.current_practice_allocation, None)
+    for s in (opt, cp):
+        D.check_plan(s.plan, w, s.runtimes)
+    rnd = S.plan_random(t, w, None, seed=7)
+    assert set(rnd.entries) == {j.id for j in w.jobs}
+    # the baselines' allocations equal the oracle's restatement
+    op = O.build(t.entries, w, prune=False)
+    assert PL.optimus_allocation(opt.problem) == tuple(O.optimus(op))
+    assert PL.current_practice_allocation(cp.problem) == tuple(O.current_practice(op))
+    # and their engine makespans equal the oracle's list schedule
+    cpo = C.CProblem(op)
+    assert opt.makespan == cpo.eval(*O.optimus(op))[0]
+    assert cp.makespan == cpo.eval(*O.current_practice(op))[0]
+
+
+def test_plan_random_matches_oracle_draws():
+    w, t = setup("cfg3")
+    op = O.build(t.entries, w, prune=False)
+    for seed in (0, 7, 2**63 + 1):
+        plan = S.plan_random(t, w, None, seed=seed)
+        opts, order = O.candidate(op, "seed", seed, 0)
+        ms, starts, nodes = C.CProblem(op).eval(opts, order)
+        assert math.isclose(plan.predicted_makespan, ms * op.delta)
+        for j, jid in enumerate(op.job_ids):
+            assert (plan.entries[jid].config.technique, plan.entries[jid].config.gpus) == op.options[j][opts[j]]
+    best = PL.plan_random_best(t, w, None, seed0=100, n_seeds=50000)
+    want = C.CProblem(op).search("seed", 100, 0, 50000)
+    assert (best.makespan, best.search.index) == want
+
+
+def test_resolve_runs_and_keeps_running_job_cheaper():
+    w, t = setup("cfg1")
+    first = PL.solve(t, w)
+    remaining = {j.id: j.total_batches // 2 for j in w.jobs}
+    running = {jid: (e.config.technique, e.config.gpus, e.node)
+               for jid, e in first.plan.entries.items() if e.start_time == 0.0}
+    ctx = D.RunningContext(remaining=remaining, current=running, checkpoint_cost=30.0)
+    sol = PL.solve(t, w, None, None, ctx)
+    assert sol.status == "Optimal" and set(sol.plan.entries) == set(remaining)
+    op = O.build(t.entries, w, context=(remaining, running, 30.0))
+    assert sol.makespan == C.CProblem(op).search()[0]
+
+
+def test_distinct_time_modes_agree_on_valid_plans():
+    w, t = setup("small5_1x4")
+    g = PL.solve(t, w, None, SolveOptions(time_mode="grid"))
+    f = PL.solve(t, w, None, SolveOptions(time_mode="float"))
+    D.check_plan(f.plan, w, f.runtimes)
+    # float optimum never exceeds the grid optimum (grid rounds durations up)
+    assert f.plan.predicted_makespan <= g.plan.predicted_makespan + 1e-9
+
+
+@pytest.mark.skipif(not reference_available(), reason="reference package not present (GPU box)")
+def test_drop_in_with_reference_objects():
+    core, profiling, rng = import_reference()
+    w, _ = golden_workload("small5_1x4")
+    rw = core.Workload.model_validate({"jobs": [j.__dict__ for j in w.jobs],
+                                       "cluster": {"nodes": [n.__dict__ for n in w.cluster.nodes]},
+                                       "techniques": [t.__dict__ for t in w.techniques]})
+    rt = profiling.build_profile_table(rw, profiling.SyntheticExecutor(rw.cluster))
+    plan = S.plan_saturn(rt, rw)
+    assert type(plan) is core.Plan
+    runtimes = {}
+    for jid, e in plan.entries.items():
+        runtimes[jid] = profiling.estimate_runtime(rt, rw.job(jid), e.config, rw.job(jid).total_batches)
+    core.check_plan(plan, rw, runtimes)

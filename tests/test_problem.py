@@ -1,0 +1,126 @@
+"""Host marshalling (problem.py) == the oracle's independent restatement, bit for bit."""
+
+import math
+
+import numpy as np
+import pytest
+
+from helpers import golden, golden_workload, unhex
+
+from oracle import saturn_oracle as O
+from paper_2311_02840_b200 import domain as D
+from paper_2311_02840_b200 import errors as E
+from paper_2311_02840_b200.problem import SolveOptions, build_problem
+from paper_2311_02840_b200.profiling import SyntheticExecutor, build_profile_table
+
+NAMES = ["cfg1", "cfg3", "cfg4", "cfg5", "small5_1x4", "small4_2x2", "hetero6", "tiny3_1x3"]
+
+
+def compare(prob, oprob):
+    assert prob.job_ids == oprob.job_ids
+    assert prob.node_ids == oprob.node_ids
+    assert prob.delta.hex() == float(oprob.delta).hex()
+    assert list(prob.radix) == oprob.radix
+    grid = prob.time_mode == "grid"
+    for j in range(prob.J):
+        for o in range(int(prob.radix[j])):
+            cfg = prob.options[j][o][0]
+            assert (cfg.technique, cfg.gpus) == oprob.options[j][o]
+            assert int(prob.gpus[j, o]) == oprob.gpus[j][o]
+            for n in range(prob.N):
+                el = bool((int(prob.node_mask[j, o]) >> n) & 1)
+                assert el == oprob.eligible[j][o][n]
+                if el:
+                    assert prob.runtime[j, o, n].hex() == float(oprob.runtime[j][o][n]).hex()
+                    if grid:
+                        assert int(prob.dur_i32[j, o, n]) == oprob.dur[j][o][n]
+
+
+@pytest.mark.parametrize("name", NAMES)
+@pytest.mark.parametrize("mode", ["grid", "float"])
+def test_build_problem_matches_oracle(name, mode):
+    w, _ = golden_workload(name)
+    t = build_profile_table(w, SyntheticExecutor(w.cluster))
+    prob = build_problem(t, w, SolveOptions(time_mode=mode))
+    oprob = O.build(t.entries, w, grid=mode == "grid")
+    compare(prob, oprob)
+    assert prob.pruned == (len(w.cluster.nodes) == 1)
+
+
+@pytest.mark.parametrize("name", ["cfg1", "small5_1x4", "tiny3_1x3"])
+def test_build_problem_unpruned_matches_oracle(name):
+    w, _ = golden_workload(name)
+    t = build_profile_table(w, SyntheticExecutor(w.cluster))
+    prob = build_problem(t, w, SolveOptions(prune=False))
+    compare(prob, O.build(t.entries, w, prune=False))
+    assert not prob.pruned
+
+
+def test_cfg1_shape_and_delta():
+    """cfg1 radices 4,7,5,6,5,8,4,6, space 3.25e10, delta 2255.40625668252 s."""
+    w, _ = golden_workload("cfg1")
+    t = build_profile_table(w, SyntheticExecutor(w.cluster))
+    prob = build_problem(t, w)
+    assert list(prob.radix) == [4, 7, 5, 6, 5, 8, 4, 6]
+    assert prob.space == 32514048000
+    assert prob.delta.hex() == golden()["milp"]["cfg1"]["delta"]
+    assert prob.key_bits(prob.space) == (35, 9)
+
+
+@pytest.mark.parametrize("rho", [0.0, 30.0, 5000.0])
+def test_resolve_transform_matches_oracle(rho):
+    """Re-solve: remaining batches, finished jobs dropped, +rho on changed assignments."""
+    w, _ = golden_workload("hetero6")
+    t = build_profile_table(w, SyntheticExecutor(w.cluster))
+    remaining = {"j00": 1234, "j01": 0, "j02": 20000, "j03": 7, "j05": 15000}
+    current = {"j00": ("ddp", 2, "n0"), "j03": ("fsdp", 4, "n1")}
+    ctx = D.RunningContext(remaining=remaining, current=current, checkpoint_cost=rho)
+    for mode in ("grid", "float"):
+        prob = build_problem(t, w, SolveOptions(time_mode=mode), running_context=ctx)
+        oprob = O.build(t.entries, w, grid=mode == "grid", context=(remaining, current, rho))
+        compare(prob, oprob)
+        assert prob.job_ids == ["j00", "j02", "j03", "j05"]
+
+
+def test_resolve_single_node_prune_with_rho():
+    w, _ = golden_workload("cfg1")
+    t = build_profile_table(w, SyntheticExecutor(w.cluster))
+    remaining = {j.id: j.total_batches // 3 for j in w.jobs}
+    current = {"j01": ("gpipe", 5, "n0"), "j04": ("ddp", 3, "n0")}
+    ctx = D.RunningContext(remaining=remaining, current=current, checkpoint_cost=30.0)
+    prob = build_problem(t, w, running_context=ctx)
+    compare(prob, O.build(t.entries, w, context=(remaining, current, 30.0)))
+
+
+def test_index_codec_roundtrip():
+    w, _ = golden_workload("small5_1x4")
+    t = build_profile_table(w, SyntheticExecutor(w.cluster))
+    prob = build_problem(t, w)
+    oprob = O.build(t.entries, w)
+    rng = np.random.default_rng(0)
+    for ident in list(rng.integers(0, prob.space, 200)) + [0, prob.space - 1]:
+        ident = int(ident)
+        opts, order = prob.decode_index(ident)
+        assert (opts, order) == O.decode_index(oprob, ident)
+        assert prob.encode_index(opts, order) == ident
+
+
+def test_errors():
+    w, _ = golden_workload("cfg1")
+    t = build_profile_table(w, SyntheticExecutor(w.cluster))
+    with pytest.raises(E.HorizonOverflow):
+        build_problem(t, w, SolveOptions(delta=10.0))
+    with pytest.raises(E.InvariantViolation):
+        build_problem(t, w, SolveOptions(time_mode="bogus"))
+    empty = type(t)({k: v for k, v in t.entries.items() if k[0] != "j03"}, "synthetic")
+    with pytest.raises(E.NoFeasibleConfig):
+        build_problem(empty, w)
+    w4, _ = golden_workload("cfg4")
+    t4 = build_profile_table(w4, SyntheticExecutor(w4.cluster))
+    with pytest.raises(E.InvariantViolation):
+        build_problem(t4, w4, SolveOptions(prune=True))
+    big = D.Workload(jobs=w4.jobs, cluster=D.ClusterSpec(nodes=tuple(
+        D.NodeSpec(f"n{i}", 8, 40.0) for i in range(5))), techniques=w4.techniques)
+    tb = build_profile_table(big, SyntheticExecutor(big.cluster))
+    with pytest.raises(E.TooLarge):
+        build_problem(tb, big)
