@@ -1,12 +1,15 @@
 """Build the in-tree CUDA engine: ``paper_2311_02840_b200/_lib/libsaturn_b200.so``.
 
 Plain nvcc, sm_100a only, static cudart (the .so loads through ctypes without
-any CUDA runtime on the library path).  The built file is git-ignored but
+any CUDA runtime on the library path).  The walk kernel is specialised for
+every node size 1..32, so its instantiations are split over several
+translation units compiled in parallel.  The built file is git-ignored but
 travels to the GPU box with the repo snapshot.
 """
 
 from __future__ import annotations
 
+import glob
 import os
 import shutil
 import subprocess
@@ -14,17 +17,15 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-SRC = os.path.join(HERE, "csrc", "sat_engine.cu")
+CSRC = os.path.join(HERE, "csrc")
 HDR = os.path.join(ROOT, "include", "saturn_engine.h")
 OUT_DIR = os.path.join(HERE, "_lib")
+OBJ_DIR = os.path.join(OUT_DIR, "obj")
 OUT = os.path.join(OUT_DIR, "libsaturn_b200.so")
 
-NVCC_FLAGS = [
-    "-gencode", "arch=compute_100a,code=sm_100a",
-    "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-shared",
-    "-diag-suppress", "128",
-]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-diag-suppress", "128"]
+TREE_RANGES = [(1, 6), (7, 10), (11, 14), (15, 18), (19, 22), (23, 26), (27, 29), (30, 32)]
 
 
 def nvcc() -> str:
@@ -34,22 +35,45 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
+def sources() -> list:
+    return sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cuh"))) + [HDR]
+
+
 def up_to_date() -> bool:
     if not os.path.exists(OUT):
         return False
     t = os.path.getmtime(OUT)
-    return all(os.path.getmtime(f) <= t for f in (SRC, HDR, __file__))
+    return all(os.path.getmtime(f) <= t for f in sources() + [__file__])
+
+
+def units() -> list:
+    """(source, extra defines, object) for every translation unit."""
+    out = [(os.path.join(CSRC, "sat_engine.cu"), [], os.path.join(OBJ_DIR, "sat_engine.o"))]
+    for lo, hi in TREE_RANGES:
+        out.append((os.path.join(CSRC, "sat_tree_g.cu"), [f"-DSAT_G_LO={lo}", f"-DSAT_G_HI={hi}"],
+                    os.path.join(OBJ_DIR, f"sat_tree_g{lo}_{hi}.o")))
+    return out
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return OUT
-    os.makedirs(OUT_DIR, exist_ok=True)
+    os.makedirs(OBJ_DIR, exist_ok=True)
+    cc = nvcc()
+    procs = []
+    for src, defs, obj in units():
+        cmd = [cc, *NVCC_FLAGS, *defs, "-c", "-o", obj, src]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        procs.append((cmd, subprocess.Popen(cmd)))
+    for cmd, p in procs:
+        if p.wait() != 0:
+            raise subprocess.CalledProcessError(p.returncode, cmd)
     tmp = OUT + ".tmp"
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", tmp, SRC]
+    link = [cc, *ARCH, "-shared", "-o", tmp, *[obj for _, _, obj in units()]]
     if verbose:
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.run(cmd, check=True)
+        print(" ".join(link), file=sys.stderr)
+    subprocess.run(link, check=True)
     os.replace(tmp, OUT)
     return OUT
 

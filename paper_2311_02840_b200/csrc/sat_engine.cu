@@ -30,54 +30,9 @@
 // Best-plan selection: key = (makespan, index) lexicographic, lowest index wins on
 // equal makespans.  Grid mode packs it into one u64 and uses
 // atomicMin; float mode reduces per block and merges in a second tiny kernel.
+#include "sat_common.cuh"
 
-#include "../../include/saturn_engine.h"
-
-#include <cuda_runtime.h>
-
-#include <algorithm>
-#include <cstdio>
-#include <cstring>
-#include <vector>
-
-#define SAT_INF_I32 0x3FFFFFFF
-
-namespace {
-
-constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;
-constexpr uint64_t kMix1 = 0xBF58476D1CE4E5B9ull;
-constexpr uint64_t kMix2 = 0x94D049BB133111EBull;
-constexpr int kGenThreads = 256;
-constexpr int kGenWarps = kGenThreads / 32;
-constexpr int kTreeThreads = 128;
-constexpr int kTreeWarps = kTreeThreads / 32;
-
-// ---------------------------------------------------------------------------
-// small helpers
-// ---------------------------------------------------------------------------
-__host__ __device__ inline uint64_t mix64(uint64_t z) {
-    z = (z ^ (z >> 30)) * kMix1;
-    z = (z ^ (z >> 27)) * kMix2;
-    return z ^ (z >> 31);
-}
-
-template <typename T> struct TimeTraits;
-template <> struct TimeTraits<int32_t> {
-    __device__ static int32_t inf() { return SAT_INF_I32; }
-};
-template <> struct TimeTraits<double> {
-    __device__ static double inf() { return __longlong_as_double(0x7ff0000000000000ll); }
-};
-
-__device__ inline int32_t tmin(int32_t a, int32_t b) { return min(a, b); }
-__device__ inline int32_t tmax(int32_t a, int32_t b) { return max(a, b); }
-__device__ inline double tmin(double a, double b) { return fmin(a, b); }
-__device__ inline double tmax(double a, double b) { return fmax(a, b); }
-
-__device__ inline uint64_t shfl_u64(uint64_t v, int src) {
-    return __shfl_sync(0xffffffffu, v, src);
-}
-
+namespace sat {
 // ---------------------------------------------------------------------------
 // Generic problem blob (host-packed, copied to the workspace, staged to smem)
 // ---------------------------------------------------------------------------
@@ -263,8 +218,15 @@ k_generic(GenArgs a) {
                     decode_stream(a.seed + id, J, radix, mods, my_opt, my_ord);
                 } else {
                     const uint8_t *e = a.expl + (size_t)(RECORD ? off : id) * (2 * J);
-                    for (int j = 0; j < J; ++j) { my_opt[j] = e[j]; my_ord[j] = e[J + j]; }
+                    // memory safety only: the host validates explicit candidates before upload
+                    for (int j = 0; j < J; ++j) {
+                        my_opt[j] = (uint8_t)min((int)e[j], radix[j] - 1);
+                        my_ord[j] = (uint8_t)(e[J + j] % J);
+                    }
                 }
+            } else {
+                // no candidate for this lane: park a harmless one (its key is discarded)
+                for (int j = 0; j < J; ++j) { my_opt[j] = 0; my_ord[j] = (uint8_t)j; }
             }
             const uint64_t my_id = id;
             const bool my_valid = valid;
@@ -364,242 +326,6 @@ __global__ void k_fold_partials(const sat_best_t *partials, int n, sat_best_t *b
         best->hi = hi;
         best->lo = lo;
     }
-}
-
-// ---------------------------------------------------------------------------
-// k_tree: prefix-shared exhaustive walk, one node, grid int32 time
-// ---------------------------------------------------------------------------
-constexpr int kTreeMaxJ = 20;
-constexpr int kTreeMaxOpt = 384;
-constexpr int kTreeMaxSets = 768;
-
-struct TreeParams {
-    int32_t J, P, Q, Gr, n_sets, idx_bits, init_max, pad;
-    int32_t radix[kTreeMaxJ];
-    int32_t optbase[kTreeMaxJ];
-    uint64_t wJ[kTreeMaxJ];           // option-digit weight in the index: W_j * J!
-    uint64_t fact[kTreeMaxJ + 1];     // k!
-    int32_t init_free[32];            // ascending, INF past Gr
-    int32_t optg[kTreeMaxOpt];
-    int32_t optoff[kTreeMaxOpt];      // (g - 1) * 32: smem word offset of slot g-1
-    int32_t optd[kTreeMaxOpt];
-    uint32_t set_mask[kTreeMaxSets];
-    uint64_t set_cum[kTreeMaxSets + 1];  // cumulative warp tasks
-    uint64_t set_prod[kTreeMaxSets];     // prod of radix over the set
-    uint64_t task_lo, task_hi;
-    sat_best_t *best;
-};
-
-// Merge of a register-resident sorted vector A with a compile-time gang size g;
-// result goes to the lane's column of smem (stride 32 words).
-template <int G, int g>
-__device__ __forceinline__ void merge_store(const int32_t (&A)[G], int32_t d, int32_t *out) {
-    const int32_t e = A[g - 1] + d;
-#pragma unroll
-    for (int i = 0; i < G; ++i) {
-        int32_t v;
-        if (i + g < G) v = min(A[(i + g < G) ? i + g : 0], e);
-        else v = e;
-        if (i >= g) v = max(A[i], v);
-        out[i * 32] = v;
-    }
-}
-
-template <int G>
-__device__ __forceinline__ void merge_dispatch(int g, const int32_t (&A)[G], int32_t d, int32_t *out) {
-    switch (g) {
-#define SAT_CASE(K) case K: if constexpr (K <= G) merge_store<G, (K <= G ? K : 1)>(A, d, out); break;
-        SAT_CASE(1) SAT_CASE(2) SAT_CASE(3) SAT_CASE(4) SAT_CASE(5) SAT_CASE(6) SAT_CASE(7) SAT_CASE(8)
-        SAT_CASE(9) SAT_CASE(10) SAT_CASE(11) SAT_CASE(12) SAT_CASE(13) SAT_CASE(14) SAT_CASE(15) SAT_CASE(16)
-        SAT_CASE(17) SAT_CASE(18) SAT_CASE(19) SAT_CASE(20) SAT_CASE(21) SAT_CASE(22) SAT_CASE(23) SAT_CASE(24)
-        SAT_CASE(25) SAT_CASE(26) SAT_CASE(27) SAT_CASE(28) SAT_CASE(29) SAT_CASE(30) SAT_CASE(31) SAT_CASE(32)
-#undef SAT_CASE
-        default: break;
-    }
-}
-
-// Per-lane running best (makespan, index).
-struct LaneBest {
-    int32_t ms;
-    uint64_t ix;
-};
-
-// Two jobs left (a < b): both orders x all options of the first (a merge each) x all
-// options of the second (a leaf each).
-template <int G>
-__device__ __forceinline__ void tree_pair(const TreeParams &p, const int32_t *U, int32_t *B,
-                                          uint32_t rem, uint64_t base, bool valid, LaneBest &lb) {
-    int32_t A[G];
-#pragma unroll
-    for (int i = 0; i < G; ++i) A[i] = U[i * 32];
-    const int ja = __ffs(rem) - 1;
-    const int jb = 31 - __clz(rem);
-    const int last = p.Gr - 1;
-#pragma unroll 1
-    for (int side = 0; side < 2; ++side) {
-        const int j1 = side ? jb : ja;
-        const int j2 = side ? ja : jb;
-        const uint64_t base1 = base + (uint64_t)side;     // Lehmer digit of position J-2
-        const int r1 = p.radix[j1], ob1 = p.optbase[j1];
-        const int r2 = p.radix[j2], ob2 = p.optbase[j2];
-        const uint64_t w1 = p.wJ[j1], w2 = p.wJ[j2];
-#pragma unroll 1
-        for (int o1 = 0; o1 < r1; ++o1) {
-            merge_dispatch<G>(p.optg[ob1 + o1], A, p.optd[ob1 + o1], B);
-            const int32_t blast = B[last * 32];
-            int32_t m = SAT_INF_I32;
-#pragma unroll 4
-            for (int o2 = 0; o2 < r2; ++o2) m = min(m, B[p.optoff[ob2 + o2]] + p.optd[ob2 + o2]);
-            const int32_t ms = max(m, blast);
-            if (valid && ms <= lb.ms) {
-                // lowest option of the second job reaching ms
-                int o2 = 0;
-                for (; o2 < r2; ++o2)
-                    if (max(B[p.optoff[ob2 + o2]] + p.optd[ob2 + o2], blast) == ms) break;
-                const uint64_t ix = base1 + (uint64_t)o1 * w1 + (uint64_t)o2 * w2;
-                if (ms < lb.ms || ix < lb.ix) { lb.ms = ms; lb.ix = ix; }
-            }
-        }
-    }
-}
-
-// Upper-level merge with a warp-uniform runtime gang size, smem column to smem column.
-template <int G>
-__device__ __forceinline__ void merge_cols(const int32_t *src, int32_t *dst, int g, int32_t d) {
-    const int32_t e = src[(g - 1) * 32] + d;
-#pragma unroll
-    for (int i = 0; i < G; ++i) {
-        const int32_t v = max(src[i * 32], min(src[(i + g) * 32], e));   // src rows G..2G-1 = INF
-        dst[i * 32] = v;
-    }
-}
-
-template <int G>
-__global__ void __launch_bounds__(kTreeThreads)
-k_tree(const __grid_constant__ TreeParams p) {
-    extern __shared__ __align__(16) int32_t tsm[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int Q = p.Q, P = p.P, J = p.J;
-    const int upper = Q - 1;                         // level buffers 0..Q-2 (padded)
-    const int col_words = 2 * G * 32;
-    int32_t *wbase = tsm + warp * (upper * col_words + G * 32);
-    int32_t *Bbuf = wbase + upper * col_words + lane;
-    // padding rows of every level buffer = INF (never rewritten)
-    for (int L = 0; L < upper; ++L)
-        for (int i = G; i < 2 * G; ++i) wbase[L * col_words + i * 32 + lane] = SAT_INF_I32;
-
-    LaneBest lb{SAT_INF_I32, ~0ull};
-    const uint64_t gwarp = (uint64_t)blockIdx.x * kTreeWarps + warp;
-    const uint64_t nwarps = (uint64_t)gridDim.x * kTreeWarps;
-    const uint32_t all = (J >= 32) ? 0xffffffffu : ((1u << J) - 1u);
-
-    for (uint64_t t = p.task_lo + gwarp; t < p.task_hi; t += nwarps) {
-        // ---- which prefix set (warp-uniform binary search) ----
-        int lo = 0, hi = p.n_sets - 1;
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (p.set_cum[mid] <= t) lo = mid; else hi = mid - 1;
-        }
-        const int s = lo;
-        const uint32_t S = p.set_mask[s];
-        uint64_t fP = p.fact[P];
-        const uint64_t npref = fP * p.set_prod[s];
-        const uint64_t q = (t - p.set_cum[s]) * 32ull + (uint64_t)lane;
-        const bool valid = q < npref;
-        const uint64_t qq = valid ? q : 0;
-
-        // ---- decode this lane's prefix: order of S (Lehmer) and options of S ----
-        uint64_t code = qq / fP;
-        uint64_t prank = qq - code * fP;
-        int32_t *L0 = wbase + lane;
-        for (int i = 0; i < G; ++i) L0[i * 32] = p.init_free[i];
-        uint8_t popt[kTreeMaxJ];
-        {
-            // options: mixed radix over S's jobs, highest job id least significant
-            uint32_t m = S;
-            while (m) {
-                const int j = 31 - __clz(m);
-                m &= ~(1u << j);
-                const uint64_t r = (uint64_t)p.radix[j];
-                const uint64_t qd = code / r;
-                popt[j] = (uint8_t)(code - qd * r);
-                code = qd;
-            }
-        }
-        uint64_t base = 0;
-        uint32_t unplaced = all, avail = S;
-        for (int k = 0; k < P; ++k) {
-            fP /= (uint64_t)(P - k);
-            const uint64_t digit = prank / fP;
-            prank -= digit * fP;
-            uint32_t m = avail;
-            for (uint64_t x = 0; x < digit; ++x) m &= m - 1;
-            const int j = __ffs(m) - 1;
-            avail &= ~(1u << j);
-            const int o = popt[j];
-            base += (uint64_t)__popc(unplaced & ((1u << j) - 1u)) * p.fact[J - 1 - k] + (uint64_t)o * p.wJ[j];
-            unplaced &= ~(1u << j);
-            // per-lane gang size: in-place merge on the lane's column
-            const int q2 = p.optbase[j] + o;
-            const int g = p.optg[q2];
-            const int32_t e = L0[(g - 1) * 32] + p.optd[q2];
-            for (int i = 0; i < G; ++i) L0[i * 32] = max(L0[i * 32], min(L0[(i + g) * 32], e));
-        }
-        __syncwarp();
-
-        // ---- warp-uniform walk over the suffix (jobs in `unplaced`) ----
-        if (Q == 2) {
-            tree_pair<G>(p, L0, Bbuf, unplaced, base, valid, lb);
-        } else {
-            uint32_t rem_st[kTreeMaxJ];
-            uint64_t acc_st[kTreeMaxJ];
-            int cj[kTreeMaxJ], co[kTreeMaxJ];
-            int L = 0;
-            rem_st[0] = unplaced;
-            acc_st[0] = base;
-            cj[0] = -1;
-            co[0] = 0;
-            while (L >= 0) {
-                // advance the cursor of level L to its next (job, option)
-                int j = cj[L], o = co[L] + 1;
-                if (j < 0 || o >= p.radix[j]) {
-                    const uint32_t later = (j < 0) ? rem_st[L] : (rem_st[L] & ~((2u << j) - 1u));
-                    if (!later) { --L; continue; }
-                    j = __ffs(later) - 1;
-                    o = 0;
-                }
-                cj[L] = j;
-                co[L] = o;
-                const int32_t *src = wbase + L * col_words + lane;
-                int32_t *dst = wbase + (L + 1) * col_words + lane;
-                const int q2 = p.optbase[j] + o;
-                merge_cols<G>(src, dst, p.optg[q2], p.optd[q2]);
-                const uint32_t rem = rem_st[L];
-                const uint64_t acc = acc_st[L] +
-                    (uint64_t)__popc(rem & ((1u << j) - 1u)) * p.fact[Q - 1 - L] + (uint64_t)o * p.wJ[j];
-                const uint32_t rem2 = rem & ~(1u << j);
-                if (L + 1 == Q - 2) {
-                    tree_pair<G>(p, dst, Bbuf, rem2, acc, valid, lb);
-                } else {
-                    ++L;
-                    rem_st[L] = rem2;
-                    acc_st[L] = acc;
-                    cj[L] = -1;
-                    co[L] = 0;
-                }
-            }
-        }
-        __syncwarp();
-    }
-
-    // ---- warp argmin, one atomic per warp ----
-    uint64_t key = (lb.ms < SAT_INF_I32) ? (((uint64_t)(uint32_t)lb.ms << p.idx_bits) | lb.ix) : ~0ull;
-    for (int x = 16; x >= 1; x >>= 1) {
-        const uint64_t o = shfl_u64(key, lane ^ x);
-        key = o < key ? o : key;
-    }
-    if (lane == 0 && key != ~0ull)
-        atomicMin(reinterpret_cast<unsigned long long *>(&p.best->hi), (unsigned long long)key);
 }
 
 // ---------------------------------------------------------------------------
@@ -885,27 +611,9 @@ int tree_layout(const sat_problem_t *p, int prefix_len, TreeLayout &lay) {
     return SAT_OK;
 }
 
-template <int G>
-int launch_tree_g(const TreeParams &tp, int Q, cudaStream_t stream) {
-    const int upper = Q - 1;
-    const int smem = kTreeWarps * (upper * 2 * G * 32 + G * 32) * 4;
-    if (smem > 200 * 1024) return SAT_ERR_UNSUPPORTED;
-    auto kern = k_tree<G>;
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
-        return SAT_ERR_CUDA;
-    int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kTreeThreads, smem) != cudaSuccess ||
-        per_sm < 1)
-        per_sm = 1;
-    uint64_t blocks = (uint64_t)device_sms() * per_sm;
-    const uint64_t tasks = tp.task_hi - tp.task_lo;
-    const uint64_t need = (tasks + kTreeWarps - 1) / kTreeWarps;
-    if (blocks > need) blocks = std::max<uint64_t>(1, need);
-    kern<<<(unsigned)blocks, kTreeThreads, smem, stream>>>(tp);
-    return cudaGetLastError() == cudaSuccess ? SAT_OK : SAT_ERR_CUDA;
-}
+}  // namespace sat
 
-}  // namespace
+using namespace sat;
 
 // ===========================================================================
 // C ABI
@@ -1080,6 +788,13 @@ int sat_search_tree(const sat_problem_t *p, int32_t prefix_len, uint64_t task_lo
             tp.optd[q] = p->dur_i32[j * p->Cmax + o];
         }
     }
+    for (int j = 0; j < J; ++j) {
+        for (int k = 0; k < 32; ++k) tp.dg[j][k] = SAT_INF_I32;
+        for (int o = 0; o < p->radix[j]; ++o) {
+            const int g = p->gpus[j * p->Cmax + o];
+            tp.dg[j][g - 1] = std::min(tp.dg[j][g - 1], p->dur_i32[j * p->Cmax + o]);
+        }
+    }
     int32_t imax = 0;
     for (int i = 0; i < 32; ++i) {
         const bool real = i < tp.Gr;
@@ -1097,13 +812,14 @@ int sat_search_tree(const sat_problem_t *p, int32_t prefix_len, uint64_t task_lo
     tp.task_lo = task_lo; tp.task_hi = task_hi;
     tp.best = d_best;
     cudaStream_t s = (cudaStream_t)stream;
-    switch (p->G) {
-        case 1: return launch_tree_g<1>(tp, tp.Q, s);
-        case 2: return launch_tree_g<2>(tp, tp.Q, s);
-        case 4: return launch_tree_g<4>(tp, tp.Q, s);
-        case 8: return launch_tree_g<8>(tp, tp.Q, s);
-        case 16: return launch_tree_g<16>(tp, tp.Q, s);
-        case 32: return launch_tree_g<32>(tp, tp.Q, s);
+    // the walk is specialised on the node's exact GPU count (no ghost slots)
+    switch (tp.Gr) {
+#define SAT_G(K) case K: return launch_tree_g<K>(tp, tp.Q, s);
+        SAT_G(1) SAT_G(2) SAT_G(3) SAT_G(4) SAT_G(5) SAT_G(6) SAT_G(7) SAT_G(8)
+        SAT_G(9) SAT_G(10) SAT_G(11) SAT_G(12) SAT_G(13) SAT_G(14) SAT_G(15) SAT_G(16)
+        SAT_G(17) SAT_G(18) SAT_G(19) SAT_G(20) SAT_G(21) SAT_G(22) SAT_G(23) SAT_G(24)
+        SAT_G(25) SAT_G(26) SAT_G(27) SAT_G(28) SAT_G(29) SAT_G(30) SAT_G(31) SAT_G(32)
+#undef SAT_G
         default: return SAT_ERR_UNSUPPORTED;
     }
 }

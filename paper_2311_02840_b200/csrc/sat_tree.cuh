@@ -1,0 +1,291 @@
+// sat_tree.cuh -- k_tree<G>: the prefix-shared exhaustive walk (single node, grid time),
+// specialised on the node's exact GPU count G.  Instantiated by sat_tree_g.cu.
+#pragma once
+
+#include "sat_common.cuh"
+
+namespace sat {
+
+// Merge of a register-resident sorted vector A with a compile-time gang size g;
+// result goes to the lane's column of smem (stride 32 words).
+template <int G, int g>
+__device__ __forceinline__ void merge_store(const int32_t (&A)[G], int32_t d, int32_t *out) {
+    const int32_t e = A[g - 1] + d;
+#pragma unroll
+    for (int i = 0; i < G; ++i) {
+        int32_t v;
+        if (i + g < G) v = min(A[(i + g < G) ? i + g : 0], e);
+        else v = e;
+        if (i >= g) v = max(A[i], v);
+        out[i * 32] = v;
+    }
+}
+
+template <int G>
+__device__ __forceinline__ void merge_dispatch(int g, const int32_t (&A)[G], int32_t d, int32_t *out) {
+    switch (g) {
+#define SAT_CASE(K) case K: if constexpr (K <= G) merge_store<G, (K <= G ? K : 1)>(A, d, out); break;
+        SAT_CASE(1) SAT_CASE(2) SAT_CASE(3) SAT_CASE(4) SAT_CASE(5) SAT_CASE(6) SAT_CASE(7) SAT_CASE(8)
+        SAT_CASE(9) SAT_CASE(10) SAT_CASE(11) SAT_CASE(12) SAT_CASE(13) SAT_CASE(14) SAT_CASE(15) SAT_CASE(16)
+        SAT_CASE(17) SAT_CASE(18) SAT_CASE(19) SAT_CASE(20) SAT_CASE(21) SAT_CASE(22) SAT_CASE(23) SAT_CASE(24)
+        SAT_CASE(25) SAT_CASE(26) SAT_CASE(27) SAT_CASE(28) SAT_CASE(29) SAT_CASE(30) SAT_CASE(31) SAT_CASE(32)
+#undef SAT_CASE
+        default: break;
+    }
+}
+
+
+// Value of the best candidate below one (first job j1 with option of gang g, then the
+// second job): with B = the state after j1, the last job's best end over its options is
+// min_k (B[k] + D2[k]) where D2[k] = least duration among its options of gang k+1, and
+// the makespan is max(B[G-1], that).  B is never materialised: each slot costs at most a
+// min, a max and one fused add-min (VIADDMNMX).
+template <int G, int g>
+__device__ __forceinline__ int32_t group_value(const int32_t (&A)[G], int32_t d, const int32_t (&D2)[G]) {
+    const int32_t e = A[g - 1] + d;
+    int32_t m = SAT_INF_I32, blast = e;
+#pragma unroll
+    for (int k = 0; k < G; ++k) {
+        int32_t b = (k + g < G) ? min(A[(k + g < G) ? k + g : 0], e) : e;
+        if (k >= g) b = max(A[k], b);
+        m = min(m, b + D2[k]);
+        if (k == G - 1) blast = b;
+    }
+    return max(blast, m);
+}
+
+template <int G>
+__device__ __forceinline__ int32_t group_dispatch(int g, const int32_t (&A)[G], int32_t d,
+                                                  const int32_t (&D2)[G]) {
+    switch (g) {
+#define SAT_CASE(K) case K: if constexpr (K <= G) return group_value<G, (K <= G ? K : 1)>(A, d, D2); break;
+        SAT_CASE(1) SAT_CASE(2) SAT_CASE(3) SAT_CASE(4) SAT_CASE(5) SAT_CASE(6) SAT_CASE(7) SAT_CASE(8)
+        SAT_CASE(9) SAT_CASE(10) SAT_CASE(11) SAT_CASE(12) SAT_CASE(13) SAT_CASE(14) SAT_CASE(15) SAT_CASE(16)
+        SAT_CASE(17) SAT_CASE(18) SAT_CASE(19) SAT_CASE(20) SAT_CASE(21) SAT_CASE(22) SAT_CASE(23) SAT_CASE(24)
+        SAT_CASE(25) SAT_CASE(26) SAT_CASE(27) SAT_CASE(28) SAT_CASE(29) SAT_CASE(30) SAT_CASE(31) SAT_CASE(32)
+#undef SAT_CASE
+        default: break;
+    }
+    return SAT_INF_I32;
+}
+
+// Best makespan over every candidate that places j1 then j2 after state A (values only).
+template <int G>
+__device__ __forceinline__ int32_t side_value(const TreeParams &p, const int32_t (&A)[G], int j1, int j2) {
+    int32_t D2[G];
+#pragma unroll
+    for (int k = 0; k < G; ++k) D2[k] = p.dg[j2][k];
+    const int r1 = p.radix[j1], ob1 = p.optbase[j1];
+    int32_t v = SAT_INF_I32;
+#pragma unroll 1
+    for (int o1 = 0; o1 < r1; ++o1) v = min(v, group_dispatch<G>(p.optg[ob1 + o1], A, p.optd[ob1 + o1], D2));
+    return v;
+}
+
+// Exact pass over a pair node: per (first job, option) group, the makespan and the lowest
+// option of the last job reaching it, with the full candidate index for the tie-break.
+template <int G>
+__device__ __noinline__ void tree_pair_exact(const TreeParams &p, const int32_t (&A)[G], int32_t *B, int ja,
+                                             int jb, uint64_t base, LaneBest &lb) {
+#pragma unroll 1
+    for (int side = 0; side < 2; ++side) {
+        const int j1 = side ? jb : ja;
+        const int j2 = side ? ja : jb;
+        const uint64_t base1 = base + (uint64_t)side;     // Lehmer digit of position J-2
+        const int r1 = p.radix[j1], ob1 = p.optbase[j1];
+        const int r2 = p.radix[j2], ob2 = p.optbase[j2];
+        const uint64_t w1 = p.wJ[j1], w2 = p.wJ[j2];
+#pragma unroll 1
+        for (int o1 = 0; o1 < r1; ++o1) {
+            merge_dispatch<G>(p.optg[ob1 + o1], A, p.optd[ob1 + o1], B);
+            const int32_t blast = B[(G - 1) * 32];
+            int32_t ms = SAT_INF_I32;
+            int best_o2 = 0;
+#pragma unroll 1
+            for (int o2 = 0; o2 < r2; ++o2) {
+                const int32_t v = max(B[p.optoff[ob2 + o2]] + p.optd[ob2 + o2], blast);
+                if (v < ms) { ms = v; best_o2 = o2; }
+            }
+            if (ms <= lb.ms) {
+                const uint64_t ix = base1 + (uint64_t)o1 * w1 + (uint64_t)best_o2 * w2;
+                if (ms < lb.ms || ix < lb.ix) { lb.ms = ms; lb.ix = ix; }
+            }
+        }
+    }
+}
+
+// Two jobs left (a < b): both orders x all options of the first x all options of the
+// second.  Fast value pass in registers; the exact pass only runs when this pair node
+// can tie or beat the lane's best (rare once the lane has a good plan).
+template <int G>
+__device__ __forceinline__ void tree_pair(const TreeParams &p, const int32_t *U, int32_t *B,
+                                          uint32_t rem, uint64_t base, bool valid, LaneBest &lb) {
+    int32_t A[G];
+#pragma unroll
+    for (int i = 0; i < G; ++i) A[i] = U[i * 32];
+    const int ja = __ffs(rem) - 1;
+    const int jb = 31 - __clz(rem);
+    const int32_t v = min(side_value<G>(p, A, ja, jb), side_value<G>(p, A, jb, ja));
+    if (valid && v <= lb.ms) tree_pair_exact<G>(p, A, B, ja, jb, base, lb);
+}
+
+// Upper-level merge with a warp-uniform runtime gang size, smem column to smem column.
+template <int G>
+__device__ __forceinline__ void merge_cols(const int32_t *src, int32_t *dst, int g, int32_t d) {
+    const int32_t e = src[(g - 1) * 32] + d;
+#pragma unroll
+    for (int i = 0; i < G; ++i) {
+        const int32_t v = max(src[i * 32], min(src[(i + g) * 32], e));   // src rows G..2G-1 = INF
+        dst[i * 32] = v;
+    }
+}
+
+template <int G>
+__global__ void __launch_bounds__(kTreeThreads)
+k_tree(const __grid_constant__ TreeParams p) {
+    extern __shared__ __align__(16) int32_t tsm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int Q = p.Q, P = p.P, J = p.J;
+    const int upper = Q - 1;                         // level buffers 0..Q-2 (padded)
+    const int col_words = 2 * G * 32;
+    int32_t *wbase = tsm + warp * (upper * col_words + G * 32);
+    int32_t *Bbuf = wbase + upper * col_words + lane;
+    // padding rows of every level buffer = INF (never rewritten)
+    for (int L = 0; L < upper; ++L)
+        for (int i = G; i < 2 * G; ++i) wbase[L * col_words + i * 32 + lane] = SAT_INF_I32;
+
+    LaneBest lb{SAT_INF_I32, ~0ull};
+    const uint64_t gwarp = (uint64_t)blockIdx.x * kTreeWarps + warp;
+    const uint64_t nwarps = (uint64_t)gridDim.x * kTreeWarps;
+    const uint32_t all = (J >= 32) ? 0xffffffffu : ((1u << J) - 1u);
+
+    for (uint64_t t = p.task_lo + gwarp; t < p.task_hi; t += nwarps) {
+        // ---- which prefix set (warp-uniform binary search) ----
+        int lo = 0, hi = p.n_sets - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (p.set_cum[mid] <= t) lo = mid; else hi = mid - 1;
+        }
+        const int s = lo;
+        const uint32_t S = p.set_mask[s];
+        uint64_t fP = p.fact[P];
+        const uint64_t npref = fP * p.set_prod[s];
+        const uint64_t q = (t - p.set_cum[s]) * 32ull + (uint64_t)lane;
+        const bool valid = q < npref;
+        const uint64_t qq = valid ? q : 0;
+
+        // ---- decode this lane's prefix: order of S (Lehmer) and options of S ----
+        uint64_t code = qq / fP;
+        uint64_t prank = qq - code * fP;
+        int32_t *L0 = wbase + lane;
+        for (int i = 0; i < G; ++i) L0[i * 32] = p.init_free[i];
+        uint8_t popt[kTreeMaxJ];
+        {
+            // options: mixed radix over S's jobs, highest job id least significant
+            uint32_t m = S;
+            while (m) {
+                const int j = 31 - __clz(m);
+                m &= ~(1u << j);
+                const uint64_t r = (uint64_t)p.radix[j];
+                const uint64_t qd = code / r;
+                popt[j] = (uint8_t)(code - qd * r);
+                code = qd;
+            }
+        }
+        uint64_t base = 0;
+        uint32_t unplaced = all, avail = S;
+        for (int k = 0; k < P; ++k) {
+            fP /= (uint64_t)(P - k);
+            const uint64_t digit = prank / fP;
+            prank -= digit * fP;
+            uint32_t m = avail;
+            for (uint64_t x = 0; x < digit; ++x) m &= m - 1;
+            const int j = __ffs(m) - 1;
+            avail &= ~(1u << j);
+            const int o = popt[j];
+            base += (uint64_t)__popc(unplaced & ((1u << j) - 1u)) * p.fact[J - 1 - k] + (uint64_t)o * p.wJ[j];
+            unplaced &= ~(1u << j);
+            // per-lane gang size: in-place merge on the lane's column
+            const int q2 = p.optbase[j] + o;
+            const int g = p.optg[q2];
+            const int32_t e = L0[(g - 1) * 32] + p.optd[q2];
+            for (int i = 0; i < G; ++i) L0[i * 32] = max(L0[i * 32], min(L0[(i + g) * 32], e));
+        }
+        __syncwarp();
+
+        // ---- warp-uniform walk over the suffix (jobs in `unplaced`) ----
+        if (Q == 2) {
+            tree_pair<G>(p, L0, Bbuf, unplaced, base, valid, lb);
+        } else {
+            uint32_t rem_st[kTreeMaxJ];
+            uint64_t acc_st[kTreeMaxJ];
+            int cj[kTreeMaxJ], co[kTreeMaxJ];
+            int L = 0;
+            rem_st[0] = unplaced;
+            acc_st[0] = base;
+            cj[0] = -1;
+            co[0] = 0;
+            while (L >= 0) {
+                // advance the cursor of level L to its next (job, option)
+                int j = cj[L], o = co[L] + 1;
+                if (j < 0 || o >= p.radix[j]) {
+                    const uint32_t later = (j < 0) ? rem_st[L] : (rem_st[L] & ~((2u << j) - 1u));
+                    if (!later) { --L; continue; }
+                    j = __ffs(later) - 1;
+                    o = 0;
+                }
+                cj[L] = j;
+                co[L] = o;
+                const int32_t *src = wbase + L * col_words + lane;
+                int32_t *dst = wbase + (L + 1) * col_words + lane;
+                const int q2 = p.optbase[j] + o;
+                merge_cols<G>(src, dst, p.optg[q2], p.optd[q2]);
+                const uint32_t rem = rem_st[L];
+                const uint64_t acc = acc_st[L] +
+                    (uint64_t)__popc(rem & ((1u << j) - 1u)) * p.fact[Q - 1 - L] + (uint64_t)o * p.wJ[j];
+                const uint32_t rem2 = rem & ~(1u << j);
+                if (L + 1 == Q - 2) {
+                    tree_pair<G>(p, dst, Bbuf, rem2, acc, valid, lb);
+                } else {
+                    ++L;
+                    rem_st[L] = rem2;
+                    acc_st[L] = acc;
+                    cj[L] = -1;
+                    co[L] = 0;
+                }
+            }
+        }
+        __syncwarp();
+    }
+
+    // ---- warp argmin, one atomic per warp ----
+    uint64_t key = (lb.ms < SAT_INF_I32) ? (((uint64_t)(uint32_t)lb.ms << p.idx_bits) | lb.ix) : ~0ull;
+    for (int x = 16; x >= 1; x >>= 1) {
+        const uint64_t o = shfl_u64(key, lane ^ x);
+        key = o < key ? o : key;
+    }
+    if (lane == 0 && key != ~0ull)
+        atomicMin(reinterpret_cast<unsigned long long *>(&p.best->hi), (unsigned long long)key);
+}
+
+template <int G>
+int launch_tree_g(const TreeParams &tp, int Q, cudaStream_t stream) {
+    const int upper = Q - 1;
+    const int smem = kTreeWarps * (upper * 2 * G * 32 + G * 32) * 4;
+    if (smem > 200 * 1024) return SAT_ERR_UNSUPPORTED;
+    auto kern = k_tree<G>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+        return SAT_ERR_CUDA;
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kTreeThreads, smem) != cudaSuccess ||
+        per_sm < 1)
+        per_sm = 1;
+    uint64_t blocks = (uint64_t)device_sms() * per_sm;
+    const uint64_t tasks = tp.task_hi - tp.task_lo;
+    const uint64_t need = (tasks + kTreeWarps - 1) / kTreeWarps;
+    if (blocks > need) blocks = std::max<uint64_t>(1, need);
+    kern<<<(unsigned)blocks, kTreeThreads, smem, stream>>>(tp);
+    return cudaGetLastError() == cudaSuccess ? SAT_OK : SAT_ERR_CUDA;
+}
+
+}  // namespace sat

@@ -226,7 +226,11 @@ class Engine:
         torch = self.torch
         J = nprob.struct.J
         if source == SRC_EXPLICIT:
-            ex = torch.as_tensor(np.ascontiguousarray(explicit, dtype=np.uint8)).to(self.device)
+            arr = np.ascontiguousarray(explicit, dtype=np.int64).reshape(-1, 2 * J)
+            for row in arr:
+                if (row[:J] < 0).any() or (row[:J] >= nprob.radix).any() or sorted(row[J:]) != list(range(J)):
+                    raise E.InvariantViolation("explicit", "option digit out of range or order not a permutation")
+            ex = torch.as_tensor(arr.astype(np.uint8)).to(self.device)
             n = ex.shape[0]
             ids_t = None
         else:

@@ -249,7 +249,7 @@ def test_edge_cases(eng):
     prob = to_search_problem(op)
     nprob = EN.NativeProblem(prob, 8)
     best = eng.reset_best()
-    eng.search_index(nprob, 3, 3, best)
+    eng.search_index(nprob, 1, 1, best)
     assert int(best.cpu().numpy().view(np.uint64)[0]) == 2**64 - 1
     # out-of-range indices are rejected
     from paper_2311_02840_b200 import errors as E

@@ -102,9 +102,10 @@ def test_plan_random_matches_oracle_draws():
 def test_resolve_runs_and_keeps_running_job_cheaper():
     w, t = setup("cfg1")
     first = PL.solve(t, w)
-    remaining = {j.id: j.total_batches // 2 for j in w.jobs}
+    # five unfinished jobs keep the oracle's exhaustive check to seconds
+    remaining = {j.id: j.total_batches // 2 for j in w.jobs[:5]}
     running = {jid: (e.config.technique, e.config.gpus, e.node)
-               for jid, e in first.plan.entries.items() if e.start_time == 0.0}
+               for jid, e in first.plan.entries.items() if e.start_time == 0.0 and jid in remaining}
     ctx = D.RunningContext(remaining=remaining, current=running, checkpoint_cost=30.0)
     sol = PL.solve(t, w, None, None, ctx)
     assert sol.status == "Optimal" and set(sol.plan.entries) == set(remaining)
