@@ -54,32 +54,15 @@ __device__ __forceinline__ int32_t group_value(const int32_t (&A)[G], int32_t d,
     return max(blast, m);
 }
 
-template <int G>
-__device__ __forceinline__ int32_t group_dispatch(int g, const int32_t (&A)[G], int32_t d,
-                                                  const int32_t (&D2)[G]) {
-    switch (g) {
-#define SAT_CASE(K) case K: if constexpr (K <= G) return group_value<G, (K <= G ? K : 1)>(A, d, D2); break;
-        SAT_CASE(1) SAT_CASE(2) SAT_CASE(3) SAT_CASE(4) SAT_CASE(5) SAT_CASE(6) SAT_CASE(7) SAT_CASE(8)
-        SAT_CASE(9) SAT_CASE(10) SAT_CASE(11) SAT_CASE(12) SAT_CASE(13) SAT_CASE(14) SAT_CASE(15) SAT_CASE(16)
-        SAT_CASE(17) SAT_CASE(18) SAT_CASE(19) SAT_CASE(20) SAT_CASE(21) SAT_CASE(22) SAT_CASE(23) SAT_CASE(24)
-        SAT_CASE(25) SAT_CASE(26) SAT_CASE(27) SAT_CASE(28) SAT_CASE(29) SAT_CASE(30) SAT_CASE(31) SAT_CASE(32)
-#undef SAT_CASE
-        default: break;
+// All gang sizes of the first job at compile time: D1[g-1] = least duration of its options
+// with gang g (INF: none), so only existing gangs cost work (one uniform branch each).
+template <int G, int g>
+__device__ __forceinline__ void side_fold(const int32_t (&A)[G], const int32_t (&D1)[G], const int32_t (&D2)[G],
+                                          int32_t &v) {
+    if constexpr (g <= G) {
+        if (D1[g - 1] < SAT_INF_I32) v = min(v, group_value<G, g>(A, D1[g - 1], D2));
+        side_fold<G, g + 1>(A, D1, D2, v);
     }
-    return SAT_INF_I32;
-}
-
-// Best makespan over every candidate that places j1 then j2 after state A (values only).
-template <int G>
-__device__ __forceinline__ int32_t side_value(const TreeParams &p, const int32_t (&A)[G], int j1, int j2) {
-    int32_t D2[G];
-#pragma unroll
-    for (int k = 0; k < G; ++k) D2[k] = p.dg[j2][k];
-    const int r1 = p.radix[j1], ob1 = p.optbase[j1];
-    int32_t v = SAT_INF_I32;
-#pragma unroll 1
-    for (int o1 = 0; o1 < r1; ++o1) v = min(v, group_dispatch<G>(p.optg[ob1 + o1], A, p.optd[ob1 + o1], D2));
-    return v;
 }
 
 // Exact pass over a pair node: per (first job, option) group, the makespan and the lowest
@@ -115,17 +98,25 @@ __device__ __noinline__ void tree_pair_exact(const TreeParams &p, const int32_t 
 }
 
 // Two jobs left (a < b): both orders x all options of the first x all options of the
-// second.  Fast value pass in registers; the exact pass only runs when this pair node
-// can tie or beat the lane's best (rare once the lane has a good plan).
+// second.  Fast value pass in registers (per-gang minimum durations are exact for the
+// value: a shorter first job never hurts, a shorter last job never hurts); the exact pass
+// only runs when this pair node can tie or beat the lane's best.
 template <int G>
 __device__ __forceinline__ void tree_pair(const TreeParams &p, const int32_t *U, int32_t *B,
-                                          uint32_t rem, uint64_t base, bool valid, LaneBest &lb) {
-    int32_t A[G];
-#pragma unroll
-    for (int i = 0; i < G; ++i) A[i] = U[i * 32];
+                                          const int32_t *sdg, uint32_t rem, uint64_t base, bool valid,
+                                          LaneBest &lb) {
+    int32_t A[G], Da[G], Db[G];
     const int ja = __ffs(rem) - 1;
     const int jb = 31 - __clz(rem);
-    const int32_t v = min(side_value<G>(p, A, ja, jb), side_value<G>(p, A, jb, ja));
+#pragma unroll
+    for (int i = 0; i < G; ++i) {
+        A[i] = U[i * 32];
+        Da[i] = sdg[ja * 32 + i];
+        Db[i] = sdg[jb * 32 + i];
+    }
+    int32_t v = SAT_INF_I32;
+    side_fold<G, 1>(A, Da, Db, v);
+    side_fold<G, 1>(A, Db, Da, v);
     if (valid && v <= lb.ms) tree_pair_exact<G>(p, A, B, ja, jb, base, lb);
 }
 
@@ -140,8 +131,9 @@ __device__ __forceinline__ void merge_cols(const int32_t *src, int32_t *dst, int
     }
 }
 
+// occupancy target per node size: 12 blocks (40 regs) up to 8 GPUs, fewer for larger nodes
 template <int G>
-__global__ void __launch_bounds__(kTreeThreads)
+__global__ void __launch_bounds__(kTreeThreads, G <= 8 ? 12 : (G <= 16 ? 8 : 4))
 k_tree(const __grid_constant__ TreeParams p) {
     extern __shared__ __align__(16) int32_t tsm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -150,6 +142,10 @@ k_tree(const __grid_constant__ TreeParams p) {
     const int col_words = 2 * G * 32;
     int32_t *wbase = tsm + warp * (upper * col_words + G * 32);
     int32_t *Bbuf = wbase + upper * col_words + lane;
+    // per (job, gang) least durations, shared by the block (broadcast loads in the pair pass)
+    int32_t *sdg = tsm + kTreeWarps * (upper * col_words + G * 32);
+    for (int i = threadIdx.x; i < p.J * 32; i += blockDim.x) sdg[i] = p.dg[i >> 5][i & 31];
+    __syncthreads();
     // padding rows of every level buffer = INF (never rewritten)
     for (int L = 0; L < upper; ++L)
         for (int i = G; i < 2 * G; ++i) wbase[L * col_words + i * 32 + lane] = SAT_INF_I32;
@@ -215,7 +211,7 @@ k_tree(const __grid_constant__ TreeParams p) {
 
         // ---- warp-uniform walk over the suffix (jobs in `unplaced`) ----
         if (Q == 2) {
-            tree_pair<G>(p, L0, Bbuf, unplaced, base, valid, lb);
+            tree_pair<G>(p, L0, Bbuf, sdg, unplaced, base, valid, lb);
         } else {
             uint32_t rem_st[kTreeMaxJ];
             uint64_t acc_st[kTreeMaxJ];
@@ -245,7 +241,7 @@ k_tree(const __grid_constant__ TreeParams p) {
                     (uint64_t)__popc(rem & ((1u << j) - 1u)) * p.fact[Q - 1 - L] + (uint64_t)o * p.wJ[j];
                 const uint32_t rem2 = rem & ~(1u << j);
                 if (L + 1 == Q - 2) {
-                    tree_pair<G>(p, dst, Bbuf, rem2, acc, valid, lb);
+                    tree_pair<G>(p, dst, Bbuf, sdg, rem2, acc, valid, lb);
                 } else {
                     ++L;
                     rem_st[L] = rem2;
@@ -271,7 +267,7 @@ k_tree(const __grid_constant__ TreeParams p) {
 template <int G>
 int launch_tree_g(const TreeParams &tp, int Q, cudaStream_t stream) {
     const int upper = Q - 1;
-    const int smem = kTreeWarps * (upper * 2 * G * 32 + G * 32) * 4;
+    const int smem = (kTreeWarps * (upper * 2 * G * 32 + G * 32) + tp.J * 32) * 4;
     if (smem > 200 * 1024) return SAT_ERR_UNSUPPORTED;
     auto kern = k_tree<G>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
