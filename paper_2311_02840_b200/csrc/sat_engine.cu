@@ -84,6 +84,7 @@ struct GenArgs {
     uint64_t lo, hi;            // candidate ids [lo, hi)
     uint64_t seed;
     int32_t per_lane;           // consecutive candidates per lane per batch (index source)
+    int32_t rec_d;              // step records carry the duration itself (one node, grid, search)
     const uint64_t *ids;        // RECORD: explicit candidate ids (index/stream sources)
     const uint8_t *expl;        // EXPLICIT source: [n][2J]
     sat_best_t *best;           // grid mode result
@@ -100,59 +101,87 @@ __device__ inline bool key_less(T ms_a, uint64_t ix_a, T ms_b, uint64_t ix_b) {
     return ms_a < ms_b || (ms_a == ms_b && ix_a < ix_b);
 }
 
-// Decode candidate `id` from mixed radix (job 0 most significant) x Lehmer rank.
-__device__ inline void decode_index(uint64_t id, int J, const int32_t *radix, uint8_t *opt,
-                                    uint8_t *ord) {
+// A candidate is decoded into J step records, one per position of the submission order:
+//   bits 0-5  gang size - 1      bits 6-11  job      bits 12-31  duration or global option q
+// stored lane-interleaved (record k of lane l at word k*32 + l): decode writes are
+// conflict-free and a W-lane segment reads its candidate's record as one broadcast.
+__device__ inline uint32_t step_rec(int g, int job, uint32_t payload) {
+    return (uint32_t)(g - 1) | ((uint32_t)job << 6) | (payload << 12);
+}
+
+struct GenTables {
+    const int32_t *radix, *optbase, *optg;
+    const uint32_t *optmask;
+    const ModN *mods;
+    int J, N;
+};
+
+template <typename T>
+__device__ inline uint32_t rec_for(const GenTables &t, const T *dur, bool rec_d, int job, int o) {
+    const int q = t.optbase[job] + o;
+    const uint32_t pay = rec_d ? (uint32_t)(int32_t)dur[q] : (uint32_t)q;
+    return step_rec(t.optg[q], job, pay);
+}
+
+// index -> option digits (job 0 most significant) and Lehmer-ranked order, into the
+// lane's interleaved u8 scratch
+__device__ inline void decode_index(uint64_t id, int J, const int32_t *radix, uint8_t *opt, uint8_t *ord) {
     uint64_t f = 1;
     for (int k = 2; k <= J; ++k) f *= (uint64_t)k;
     uint64_t conf = id / f;
     uint64_t perm = id - conf * f;
     for (int j = J - 1; j >= 0; --j) {
-        uint64_t r = (uint64_t)radix[j];
-        uint64_t qd = conf / r;
-        opt[j] = (uint8_t)(conf - qd * r);
+        const uint64_t r = (uint64_t)radix[j];
+        const uint64_t qd = conf / r;
+        opt[j * 32] = (uint8_t)(conf - qd * r);
         conf = qd;
     }
     uint64_t unused = (J == 64) ? ~0ull : ((1ull << J) - 1ull);
     for (int k = 0; k < J; ++k) {
         f /= (uint64_t)(J - k);                       // (J-1-k)!
-        uint64_t digit = perm / f;
+        const uint64_t digit = perm / f;
         perm -= digit * f;
-        // digit-th set bit of `unused`
         uint64_t m = unused;
-        for (uint64_t t = 0; t < digit; ++t) m &= m - 1;
-        int job = __ffsll((long long)m) - 1;
-        ord[k] = (uint8_t)job;
+        for (uint64_t x = 0; x < digit; ++x) m &= m - 1;
+        const int job = __ffsll((long long)m) - 1;
+        ord[k * 32] = (uint8_t)job;
         unused &= ~(1ull << job);
     }
 }
 
-// Advance to index + 1: next lexicographic permutation; on wrap, odometer the options.
+// index + 1: next lexicographic permutation; on wrap, odometer the option digits
 __device__ inline void advance_index(int J, const int32_t *radix, uint8_t *opt, uint8_t *ord) {
     int i = J - 2;
-    while (i >= 0 && ord[i] >= ord[i + 1]) --i;
+    while (i >= 0 && ord[i * 32] >= ord[(i + 1) * 32]) --i;
     if (i >= 0) {
         int k = J - 1;
-        while (ord[k] <= ord[i]) --k;
-        uint8_t t = ord[i]; ord[i] = ord[k]; ord[k] = t;
-        for (int a = i + 1, b = J - 1; a < b; ++a, --b) { t = ord[a]; ord[a] = ord[b]; ord[b] = t; }
+        while (ord[k * 32] <= ord[i * 32]) --k;
+        uint8_t t = ord[i * 32]; ord[i * 32] = ord[k * 32]; ord[k * 32] = t;
+        for (int a = i + 1, b = J - 1; a < b; ++a, --b) { t = ord[a * 32]; ord[a * 32] = ord[b * 32]; ord[b * 32] = t; }
         return;
     }
-    for (int k = 0; k < J; ++k) ord[k] = (uint8_t)k;
+    for (int k = 0; k < J; ++k) ord[k * 32] = (uint8_t)k;
     for (int j = J - 1; j >= 0; --j) {
-        if ((int)opt[j] + 1 < radix[j]) { opt[j] += 1; return; }
-        opt[j] = 0;
+        if ((int)opt[j * 32] + 1 < radix[j]) { opt[j * 32] += 1; return; }
+        opt[j * 32] = 0;
     }
 }
 
-__device__ inline void decode_stream(uint64_t state0, int J, const int32_t *radix,
-                                     const ModN *mods, uint8_t *opt, uint8_t *ord) {
+// plan_random draw order: below(radix_j) per job in id order, then a
+// Fisher-Yates shuffle of the order -- applied directly to the step records.
+template <typename T>
+__device__ inline void decode_stream(uint64_t state0, const GenTables &t, const T *dur, bool rec_d,
+                                     uint32_t *steps) {
     Stream s{state0};
-    for (int j = 0; j < J; ++j) opt[j] = (uint8_t)s.below((uint32_t)radix[j], mods);
-    for (int k = 0; k < J; ++k) ord[k] = (uint8_t)k;
-    for (int i = J - 1; i >= 1; --i) {                // Fisher-Yates, rng.py:44-48
-        uint32_t k = s.below((uint32_t)(i + 1), mods);
-        uint8_t t = ord[i]; ord[i] = ord[k]; ord[k] = t;
+    for (int j = 0; j < t.J; ++j) {
+        const int o = (int)s.below((uint32_t)t.radix[j], t.mods);
+        steps[j * 32] = rec_for(t, dur, rec_d, j, o);
+    }
+    for (int i = t.J - 1; i >= 1; --i) {                 // rng.py:44-48
+        const int k = (int)s.below((uint32_t)(i + 1), t.mods);
+        const uint32_t x = steps[i * 32];
+        steps[i * 32] = steps[k * 32];
+        steps[k * 32] = x;
     }
 }
 
@@ -161,7 +190,6 @@ __global__ void __launch_bounds__(kGenThreads)
 k_generic(GenArgs a) {
     extern __shared__ __align__(16) uint8_t smem[];
     const BlobHeader &h = *reinterpret_cast<const BlobHeader *>(smem);
-    // stage the blob
     {
         const int nwords = (*reinterpret_cast<const BlobHeader *>(a.blob)).bytes / 16;
         const int4 *src = reinterpret_cast<const int4 *>(a.blob);
@@ -170,25 +198,34 @@ k_generic(GenArgs a) {
     }
     __syncthreads();
     const int J = h.J, N = h.N, G = h.G, W = h.W;
-    const int32_t *radix = reinterpret_cast<const int32_t *>(smem + h.off_radix);
-    const int32_t *optbase = reinterpret_cast<const int32_t *>(smem + h.off_optbase);
-    const int32_t *optg = reinterpret_cast<const int32_t *>(smem + h.off_g);
-    const uint32_t *optmask = reinterpret_cast<const uint32_t *>(smem + h.off_mask);
+    GenTables tb;
+    tb.radix = reinterpret_cast<const int32_t *>(smem + h.off_radix);
+    tb.optbase = reinterpret_cast<const int32_t *>(smem + h.off_optbase);
+    tb.optg = reinterpret_cast<const int32_t *>(smem + h.off_g);
+    tb.optmask = reinterpret_cast<const uint32_t *>(smem + h.off_mask);
+    tb.mods = reinterpret_cast<const ModN *>(smem + h.off_modn);
+    tb.J = J;
+    tb.N = N;
     const T *dur = reinterpret_cast<const T *>(smem + h.off_dur);
     const T *release = reinterpret_cast<const T *>(smem + h.off_release);
     const T *lane_init = reinterpret_cast<const T *>(smem + h.off_lane_init);
-    const ModN *mods = reinterpret_cast<const ModN *>(smem + h.off_modn);
+    const bool rec_d = a.rec_d != 0;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint8_t *rows = smem + h.bytes + warp * (2 * 32 * SAT_MAX_JOBS);
-    uint8_t *my_opt = rows + lane * (2 * SAT_MAX_JOBS);
-    uint8_t *my_ord = my_opt + SAT_MAX_JOBS;
+    const int warp_bytes = J * 32 * (4 + (SRC == SAT_SRC_INDEX ? 2 : 0));
+    uint8_t *wscr = smem + h.bytes + warp * warp_bytes;
+    uint32_t *steps = reinterpret_cast<uint32_t *>(wscr);            // [J][32]
+    uint32_t *my_steps = steps + lane;
+    uint8_t *my_opt = wscr + J * 128 + lane;                         // [J][32] (index source)
+    uint8_t *my_ord = my_opt + J * 32;
 
     const int sl = lane & (W - 1), seg = lane / W, node = sl / G, slot = sl - node * G;
     const int seg_base = seg * W;
     const int segs = 32 / W;
     const T INF = TimeTraits<T>::inf();
     const T init_max = sizeof(T) == 4 ? (T)h.init_max_i32 : (T)h.init_max_f64;
+    const T my_init = lane_init[sl];
+    const bool multi = N > 1;
 
     T best_ms = INF;
     uint64_t best_ix = ~0ull;
@@ -206,72 +243,77 @@ k_generic(GenArgs a) {
             const uint64_t off = first + k;
             const bool valid = off < total;
             uint64_t id = a.lo + off;
-            if (RECORD) id = a.ids ? a.ids[off < total ? off : 0] : a.lo + off;
+            if (RECORD && a.ids) id = a.ids[valid ? off : 0];
             // ---- decode (thread per candidate) ----
             if (valid) {
                 if (SRC == SAT_SRC_INDEX) {
-                    if (k == 0 || RECORD) decode_index(id, J, radix, my_opt, my_ord);
-                    else advance_index(J, radix, my_opt, my_ord);
+                    if (k == 0 || RECORD) decode_index(id, J, tb.radix, my_opt, my_ord);
+                    else advance_index(J, tb.radix, my_opt, my_ord);
+                    for (int kk = 0; kk < J; ++kk) {
+                        const int job = my_ord[kk * 32];
+                        my_steps[kk * 32] = rec_for(tb, dur, rec_d, job, my_opt[job * 32]);
+                    }
                 } else if (SRC == SAT_SRC_SUBSTREAM) {
-                    decode_stream(mix64((a.seed ^ id) + kGolden), J, radix, mods, my_opt, my_ord);
+                    decode_stream(mix64((a.seed ^ id) + kGolden), tb, dur, rec_d, my_steps);
                 } else if (SRC == SAT_SRC_SEED) {
-                    decode_stream(a.seed + id, J, radix, mods, my_opt, my_ord);
+                    decode_stream(a.seed + id, tb, dur, rec_d, my_steps);
                 } else {
-                    const uint8_t *e = a.expl + (size_t)(RECORD ? off : id) * (2 * J);
                     // memory safety only: the host validates explicit candidates before upload
-                    for (int j = 0; j < J; ++j) {
-                        my_opt[j] = (uint8_t)min((int)e[j], radix[j] - 1);
-                        my_ord[j] = (uint8_t)(e[J + j] % J);
+                    const uint8_t *e = a.expl + (size_t)(RECORD ? off : id) * (2 * J);
+                    for (int kk = 0; kk < J; ++kk) {
+                        const int job = e[J + kk] % J;
+                        my_steps[kk * 32] = rec_for(tb, dur, rec_d, job, min((int)e[job], tb.radix[job] - 1));
                     }
                 }
             } else {
                 // no candidate for this lane: park a harmless one (its key is discarded)
-                for (int j = 0; j < J; ++j) { my_opt[j] = 0; my_ord[j] = (uint8_t)j; }
+                for (int kk = 0; kk < J; ++kk) my_steps[kk * 32] = rec_for(tb, dur, rec_d, kk, 0);
             }
-            const uint64_t my_id = id;
-            const bool my_valid = valid;
             __syncwarp();
-            // ---- schedule: segment `seg` handles slot (pass * segs + seg) ----
+            // ---- schedule: segment `seg` handles candidate slot pass * segs + seg ----
             for (int pass = 0; pass < W; ++pass) {
-                const int c = pass * segs + seg;                // candidate slot (= lane that decoded it)
-                const uint8_t *c_opt = rows + c * (2 * SAT_MAX_JOBS);
-                const uint8_t *c_ord = c_opt + SAT_MAX_JOBS;
-                const uint64_t c_off = __shfl_sync(0xffffffffu, first + k, c);
-                const bool c_valid = __shfl_sync(0xffffffffu, (int)my_valid, c) != 0;
-                const uint64_t c_id = shfl_u64(my_id, c);
-                T av = lane_init[sl];
+                const int c = pass * segs + seg;
+                const uint64_t c_off = __shfl_sync(0xffffffffu, off, c);
+                const bool c_valid = __shfl_sync(0xffffffffu, (int)valid, c) != 0;
+                const uint64_t c_id = shfl_u64(id, c);
+                const uint32_t *c_steps = steps + c;
+                T av = my_init;
                 T mx = init_max;
                 for (int kk = 0; kk < J; ++kk) {
-                    const int job = c_ord[kk];
-                    const int o = c_opt[job];
-                    const int q = optbase[job] + o;
-                    const int g = optg[q];
+                    const uint32_t r = c_steps[kk * 32];
+                    const int g = (int)(r & 63u) + 1;
+                    const uint32_t pay = r >> 12;
                     T t = __shfl_sync(0xffffffffu, av, seg_base + node * G + g - 1);
-                    if (!((optmask[q] >> node) & 1u)) t = INF;
-                    if (h.has_release) t = tmax(t, release[job]);
+                    T d;
+                    if (rec_d) {
+                        d = (T)(int32_t)pay;
+                    } else {
+                        if (multi && !((tb.optmask[pay] >> node) & 1u)) t = INF;
+                        d = node < N ? dur[pay * N + node] : (T)0;
+                    }
+                    if (h.has_release) t = tmax(t, release[(r >> 6) & 63u]);
                     // node finishing the job earliest, lowest node on ties
-                    T bt = t;
-                    T be = t + (node < N ? dur[q * N + node] : (T)0);
+                    T bt = t, be = t + d;
                     int bn = node;
                     for (int x = G; x < W; x <<= 1) {
-                        T oe = __shfl_xor_sync(0xffffffffu, be, x);
-                        T ot = __shfl_xor_sync(0xffffffffu, bt, x);
-                        int on = __shfl_xor_sync(0xffffffffu, bn, x);
+                        const T oe = __shfl_xor_sync(0xffffffffu, be, x);
+                        const T ot = __shfl_xor_sync(0xffffffffu, bt, x);
+                        const int on = __shfl_xor_sync(0xffffffffu, bn, x);
                         if (oe < be || (oe == be && on < bn)) { be = oe; bt = ot; bn = on; }
                     }
-                    const T e = be;
                     int src = lane + g;
                     src = src > 31 ? 31 : src;
                     T up = __shfl_sync(0xffffffffu, av, src);
                     if (slot + g >= G) up = INF;
-                    if (node == bn) av = tmax(av, tmin(up, e));
-                    mx = tmax(mx, e);
+                    if (node == bn) av = tmax(av, tmin(up, be));
+                    mx = tmax(mx, be);
                     if (RECORD && sl == 0 && c_valid) {
-                        const size_t r = (size_t)c_off * J + job;
-                        if (a.rec_opt) a.rec_opt[r] = o;
-                        if (a.rec_node) a.rec_node[r] = bn;
-                        if (sizeof(T) == 4) { if (a.rec_start_i32) a.rec_start_i32[r] = (int32_t)bt; }
-                        else { if (a.rec_start_f64) a.rec_start_f64[r] = (double)bt; }
+                        const int job = (int)((r >> 6) & 63u);
+                        const size_t o = (size_t)c_off * J + job;
+                        if (a.rec_opt) a.rec_opt[o] = (int32_t)pay - tb.optbase[job];
+                        if (a.rec_node) a.rec_node[o] = bn;
+                        if (sizeof(T) == 4) { if (a.rec_start_i32) a.rec_start_i32[o] = (int32_t)bt; }
+                        else { if (a.rec_start_f64) a.rec_start_f64[o] = (double)bt; }
                     }
                 }
                 if (sl == 0 && c_valid) {
@@ -287,30 +329,29 @@ k_generic(GenArgs a) {
             __syncwarp();
         }
     }
-    if (RECORD) return;
-
-    // ---- warp -> block -> grid argmin ----
-    for (int x = 16; x >= 1; x >>= 1) {
-        T oms = __shfl_xor_sync(0xffffffffu, best_ms, x);
-        uint64_t oix = shfl_u64(best_ix, lane ^ x);
-        if (key_less(oms, oix, best_ms, best_ix)) { best_ms = oms; best_ix = oix; }
-    }
-    __shared__ T s_ms[kGenWarps];
-    __shared__ uint64_t s_ix[kGenWarps];
-    if (lane == 0) { s_ms[warp] = best_ms; s_ix[warp] = best_ix; }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int w = 1; w < kGenWarps; ++w)
-            if (key_less(s_ms[w], s_ix[w], best_ms, best_ix)) { best_ms = s_ms[w]; best_ix = s_ix[w]; }
-        if (sizeof(T) == 4) {
-            if (best_ms < INF) {
-                const uint64_t key = ((uint64_t)(uint32_t)best_ms << h.idx_bits) | best_ix;
-                atomicMin(reinterpret_cast<unsigned long long *>(&a.best->hi), (unsigned long long)key);
+    if constexpr (!RECORD) {
+        // ---- warp -> block -> grid argmin ----
+        for (int x = 16; x >= 1; x >>= 1) {
+            T oms = __shfl_xor_sync(0xffffffffu, best_ms, x);
+            uint64_t oix = shfl_u64(best_ix, lane ^ x);
+            if (key_less(oms, oix, best_ms, best_ix)) { best_ms = oms; best_ix = oix; }
+        }
+        __shared__ T s_ms[kGenWarps];
+        __shared__ uint64_t s_ix[kGenWarps];
+        if (lane == 0) { s_ms[warp] = best_ms; s_ix[warp] = best_ix; }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int w = 1; w < kGenWarps; ++w)
+                if (key_less(s_ms[w], s_ix[w], best_ms, best_ix)) { best_ms = s_ms[w]; best_ix = s_ix[w]; }
+            if (sizeof(T) == 4) {
+                if (best_ms < INF) {
+                    const uint64_t key = ((uint64_t)(uint32_t)best_ms << h.idx_bits) | best_ix;
+                    atomicMin(reinterpret_cast<unsigned long long *>(&a.best->hi), (unsigned long long)key);
+                }
+            } else {
+                a.partials[blockIdx.x].hi = (uint64_t)__double_as_longlong((double)best_ms);
+                a.partials[blockIdx.x].lo = best_ix;
             }
-        } else {
-            double d = (double)best_ms;
-            a.partials[blockIdx.x].hi = (uint64_t)__double_as_longlong(d);
-            a.partials[blockIdx.x].lo = best_ix;
         }
     }
 }
@@ -477,7 +518,6 @@ int pack_blob(const sat_problem_t *p, std::vector<uint8_t> &blob) {
     return SAT_OK;
 }
 
-constexpr int kRowsBytesPerBlock = kGenWarps * 2 * 32 * SAT_MAX_JOBS;
 
 int gen_blocks(const void *kernel, int smem_bytes) {
     int per_sm = 0;
@@ -494,7 +534,16 @@ int launch_generic(const sat_problem_t *p, GenArgs a, uint64_t n_cand, void *d_w
     int st = pack_blob(p, blob);
     if (st) return st;
     const size_t blob_bytes = blob.size();
-    const int smem = (int)blob_bytes + kRowsBytesPerBlock;
+    const int smem = (int)blob_bytes + kGenWarps * p->J * 32 * (4 + (SRC == SAT_SRC_INDEX ? 2 : 0));
+    // one node + grid time: step records carry the duration itself (no table lookup per step)
+    a.rec_d = 0;
+    if (!RECORD && sizeof(T) == 4 && p->N == 1) {
+        a.rec_d = 1;
+        for (int j = 0; j < p->J; ++j)
+            for (int o = 0; o < p->radix[j]; ++o)
+                if (p->dur_i32[(j * p->Cmax + o) * p->N] >= (1 << 20) || p->dur_i32[(j * p->Cmax + o) * p->N] < 0)
+                    a.rec_d = 0;
+    }
     if (smem > 200 * 1024) return SAT_ERR_TOO_LARGE;
     auto kern = k_generic<T, SRC, RECORD>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
