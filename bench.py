@@ -224,6 +224,22 @@ def run_reference(args):
     print(json.dumps(line))
 
 
+def ncu_traffic(kernel: str, cfg: int):
+    """DRAM bytes per launch of the dominant kernel from the newest committed ncu --set full
+    capture of this kernel and config (profiles/rNN_ncu_full_<kernel>_cfg<k>.json), else None."""
+    import glob
+
+    hits = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_ncu_full_{kernel}_cfg{cfg}.json")))
+    if not hits:
+        return None, None
+    with open(hits[-1]) as f:
+        rep = json.load(f)
+    for k in rep.get("kernels", []):
+        if kernel in k.get("kernel", "") and "traffic_bytes" in k:
+            return k["traffic_bytes"], os.path.relpath(hits[-1], ROOT)
+    return None, None
+
+
 # ----------------------------------------------------------------------------- ours
 def run_ours(args):
     import numpy as np
@@ -336,6 +352,7 @@ def run_ours(args):
     else:
         per_launch_ops = (n_cand // world) * prob.J * (N + 2 * G + 2)
     achieved = per_launch_ops / kern_avg
+    traffic, traffic_src = ncu_traffic(kernel_name, args.config)
 
     line = {
         "metric": "candidate plans evaluated/sec", "value": value, "unit": "plans/s", "n_gpus": world,
@@ -355,7 +372,7 @@ def run_ours(args):
         "gpu_launches": launches,
         "kernel_ms": 1e3 * kern_avg,
         "roofline": {"bound": "int32-alu", "achieved": achieved / 1e12, "peak": peak_ops / 1e12, "unit": "TOP/s",
-                     "frac": achieved / peak_ops, "traffic": None,
+                     "frac": achieved / peak_ops, "traffic": traffic, "traffic_source": traffic_src,
                      "peak_source": "measured: sat_alu_probe IMNMX chains on this GPU (MEASURED_PEAKS.json has "
                                     "no INT32 figure)",
                      "algorithmic_ops_per_launch": per_launch_ops},
