@@ -49,6 +49,10 @@ def up_to_date() -> bool:
 def units() -> list:
     """(source, extra defines, object) for every translation unit."""
     out = [(os.path.join(CSRC, "sat_engine.cu"), [], os.path.join(OBJ_DIR, "sat_engine.o"))]
+    for t in ("int32_t", "double"):
+        for s in ("SAT_SRC_INDEX", "SAT_SRC_SUBSTREAM", "SAT_SRC_SEED"):
+            out.append((os.path.join(CSRC, "sat_cand.cu"), [f"-DSAT_CAND_T={t}", f"-DSAT_CAND_SRC={s}"],
+                        os.path.join(OBJ_DIR, f"sat_cand_{t}_{s.split('_')[-1].lower()}.o")))
     for lo, hi in TREE_RANGES:
         out.append((os.path.join(CSRC, "sat_tree_g.cu"), [f"-DSAT_G_LO={lo}", f"-DSAT_G_HI={hi}"],
                     os.path.join(OBJ_DIR, f"sat_tree_g{lo}_{hi}.o")))

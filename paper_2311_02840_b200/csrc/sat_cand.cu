@@ -1,0 +1,86 @@
+// sat_cand.cu -- launch_cand<T, SRC> for one (time type, candidate source) pair; compiled once
+// per pair (SAT_CAND_T / SAT_CAND_SRC) so the node-size specialisations build in parallel.
+#include "sat_cand.cuh"
+
+#ifndef SAT_CAND_T
+#define SAT_CAND_T int32_t
+#define SAT_CAND_SRC SAT_SRC_SUBSTREAM
+#endif
+
+namespace sat {
+
+template <typename T, int SRC, int G, bool MULTI>
+static int launch_cand_g(const sat_problem_t *p, CandArgs a, uint64_t n_cand, const std::vector<uint8_t> &blob,
+                         void *d_ws, size_t ws_bytes, cudaStream_t stream) {
+    const size_t blob_bytes = blob.size();
+    const int N = MULTI ? p->N : 1;
+    const int smem = (int)blob_bytes +
+                     kCandWarps * cand_warp_bytes(p->J, N, G, (int)sizeof(T), SRC == SAT_SRC_INDEX);
+    if (smem > 220 * 1024) return SAT_ERR_TOO_LARGE;
+    auto kern = k_cand<T, SRC, G, MULTI>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+        return SAT_ERR_CUDA;
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kCandThreads, smem) != cudaSuccess ||
+        per_sm < 1)
+        per_sm = 1;
+    uint64_t blocks = (uint64_t)device_sms() * (uint64_t)per_sm;
+    const uint64_t chunks = (n_cand + (uint64_t)a.per_lane - 1) / (uint64_t)a.per_lane;
+    const uint64_t need = (chunks + kCandThreads - 1) / kCandThreads;
+    if (blocks > need) blocks = std::max<uint64_t>(1, need);
+    const size_t part_off = (blob_bytes + 255) & ~(size_t)255;
+    const size_t need_ws = part_off + (size_t)blocks * sizeof(sat_best_t);
+    if (!d_ws || ws_bytes < need_ws) return SAT_ERR_INVALID;
+    uint8_t *ws = static_cast<uint8_t *>(d_ws);
+    if (cudaMemcpyAsync(ws, blob.data(), blob_bytes, cudaMemcpyHostToDevice, stream) != cudaSuccess)
+        return SAT_ERR_CUDA;
+    a.blob = ws;
+    a.partials = reinterpret_cast<sat_best_t *>(ws + part_off);
+    kern<<<(unsigned)blocks, kCandThreads, smem, stream>>>(a);
+    if (cudaGetLastError() != cudaSuccess) return SAT_ERR_CUDA;
+    if (sizeof(T) == 8) {
+        k_fold_partials<<<1, 32, 0, stream>>>(a.partials, (int)blocks, a.best);
+        if (cudaGetLastError() != cudaSuccess) return SAT_ERR_CUDA;
+    }
+    return SAT_OK;
+}
+
+template <typename T, int SRC>
+int launch_cand(const sat_problem_t *p, CandArgs a, uint64_t n_cand, void *d_ws, size_t ws_bytes,
+                cudaStream_t stream) {
+    std::vector<uint8_t> blob;
+    int st = pack_blob(p, blob);
+    if (st) return st;
+    // durations ride in the step records when they do not depend on the node and every
+    // option may run on every node (grid time, fits the 20-bit payload)
+    a.rec_d = 0;
+    if (sizeof(T) == 4) {
+        bool ok = true;
+        const uint32_t all = p->N >= 32 ? ~0u : ((1u << p->N) - 1u);
+        for (int j = 0; j < p->J && ok; ++j)
+            for (int o = 0; o < p->radix[j] && ok; ++o) {
+                const int q = j * p->Cmax + o;
+                const int32_t d0 = p->dur_i32[q * p->N];
+                if (d0 < 0 || d0 >= (1 << 20)) ok = false;
+                if (p->node_mask && (p->node_mask[q] & all) != all) ok = false;
+                for (int n = 1; n < p->N && ok; ++n)
+                    if (p->dur_i32[q * p->N + n] != d0) ok = false;
+            }
+        a.rec_d = ok ? 1 : 0;
+    }
+    const bool multi = p->N > 1;
+    switch (p->G) {
+#define SAT_CASE(K)                                                                                  \
+    case K:                                                                                          \
+        return multi ? launch_cand_g<T, SRC, (K <= 16 ? K : 16), true>(p, a, n_cand, blob, d_ws, ws_bytes, stream) \
+                     : launch_cand_g<T, SRC, K, false>(p, a, n_cand, blob, d_ws, ws_bytes, stream);
+        SAT_CASE(1) SAT_CASE(2) SAT_CASE(4) SAT_CASE(8) SAT_CASE(16) SAT_CASE(32)
+#undef SAT_CASE
+        default: return SAT_ERR_UNSUPPORTED;
+    }
+}
+
+template int launch_cand<SAT_CAND_T, SAT_CAND_SRC>(const sat_problem_t *, CandArgs, uint64_t, void *, size_t,
+                                                   cudaStream_t);
+
+}  // namespace sat

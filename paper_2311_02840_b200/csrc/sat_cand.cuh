@@ -1,0 +1,215 @@
+// sat_cand.cuh -- k_cand<T, SRC, G, MULTI>: one candidate per THREAD.
+//
+// The search kernel for everything the prefix-shared walk (k_tree) does not cover:
+// sampled candidate streams (plan_random draws, configs 3-5), multi-node clusters,
+// float64 time, release times and initial free times (re-solve), and exhaustive
+// index ranges of such problems.
+//
+// Each thread decodes its candidate into J step records (g-1 | job<<6 | payload<<12)
+// in its own shared-memory column, then list-schedules it.  Per node the GPU free
+// times are kept sorted ascending; placing a (g, d) job that can start at
+// s = max(a[g-1], release) with end e = s + d turns the vector into
+//        b[i] = max(a[i], min(a[i+g], e))          (a[k] = +inf for k >= G)
+// (DESIGN.md section 4.1).  The shift by the thread's own g is a read of its own
+// shared-memory column at rows i+g: every lane stays in its own bank (row stride 32
+// words), so a warp's 32 different g values cost one wavefront per row, and the
+// thread's vector itself stays in registers (one node) or in the column (several
+// nodes: the node is chosen at run time).  Rows G..2G-1 of a node hold +inf.
+//
+// Per placement: 1 + G shared loads, G shared stores, G min + G max, 1 add, 1 max
+// (one node); multi-node adds N loads + the earliest-finish node pick.
+#pragma once
+
+#include "sat_decode.cuh"
+
+namespace sat {
+
+constexpr int kCandThreads = 128;
+constexpr int kCandWarps = kCandThreads / 32;
+
+struct CandArgs {
+    const uint8_t *blob;
+    uint64_t lo, hi;            // candidate ids [lo, hi)
+    uint64_t seed;
+    int32_t per_lane;           // consecutive ids per thread per chunk (index source)
+    int32_t rec_d;              // records carry the duration (node-independent, all nodes eligible)
+    sat_best_t *best;           // grid mode result
+    sat_best_t *partials;       // float mode per-block partials
+};
+
+// bytes of one warp's private region: records, index scratch, free-time columns
+__host__ __device__ inline int cand_warp_bytes(int J, int N, int G, int tsz, bool index_src) {
+    return J * 128 + (index_src ? J * 64 : 0) + N * 2 * G * 32 * tsz;
+}
+
+template <typename T, int SRC, int G, bool MULTI>
+__global__ void __launch_bounds__(kCandThreads)
+k_cand(CandArgs a) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    {
+        const int nwords = (*reinterpret_cast<const BlobHeader *>(a.blob)).bytes / 16;
+        const int4 *src = reinterpret_cast<const int4 *>(a.blob);
+        int4 *dst = reinterpret_cast<int4 *>(smem);
+        for (int i = threadIdx.x; i < nwords; i += blockDim.x) dst[i] = src[i];
+    }
+    __syncthreads();
+    const BlobHeader &h = *reinterpret_cast<const BlobHeader *>(smem);
+    const int J = h.J;
+    const int N = MULTI ? h.N : 1;
+    GenTables tb;
+    tb.radix = reinterpret_cast<const int32_t *>(smem + h.off_radix);
+    tb.optbase = reinterpret_cast<const int32_t *>(smem + h.off_optbase);
+    tb.optg = reinterpret_cast<const int32_t *>(smem + h.off_g);
+    tb.optmask = reinterpret_cast<const uint32_t *>(smem + h.off_mask);
+    tb.mods = reinterpret_cast<const ModN *>(smem + h.off_modn);
+    tb.J = J;
+    tb.N = h.N;
+    const T *dur = reinterpret_cast<const T *>(smem + h.off_dur);
+    const T *release = reinterpret_cast<const T *>(smem + h.off_release);
+    const T *lane_init = reinterpret_cast<const T *>(smem + h.off_lane_init);   // [N][G] (blob G == G)
+    const bool rec_d = a.rec_d != 0;
+    const bool has_release = h.has_release != 0;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr bool kIndex = SRC == SAT_SRC_INDEX;
+    uint8_t *wbase = smem + h.bytes + warp * cand_warp_bytes(J, N, G, (int)sizeof(T), kIndex);
+    uint32_t *rec = reinterpret_cast<uint32_t *>(wbase) + lane;          // [J][32]
+    uint8_t *opt = wbase + J * 128 + lane;                               // [J][32] (index source)
+    uint8_t *ord = opt + J * 32;                                         // [J][32]
+    T *st = reinterpret_cast<T *>(wbase + J * 128 + (kIndex ? J * 64 : 0)) + lane;   // [N][2G][32]
+
+    const T INF = TimeTraits<T>::inf();
+    for (int n = 0; n < N; ++n)
+#pragma unroll
+        for (int i = G; i < 2 * G; ++i) st[(n * 2 * G + i) * 32] = INF;
+    const T init_max = sizeof(T) == 4 ? (T)h.init_max_i32 : (T)h.init_max_f64;
+
+    T best_ms = INF;
+    uint64_t best_ix = ~0ull;
+
+    const uint64_t total = a.hi - a.lo;
+    const int per_lane = kIndex ? a.per_lane : 1;
+    const uint64_t nthreads = (uint64_t)gridDim.x * kCandThreads;
+    const uint64_t gthread = (uint64_t)blockIdx.x * kCandThreads + threadIdx.x;
+    const uint64_t nchunks = (total + per_lane - 1) / per_lane;
+
+    for (uint64_t c = gthread; c < nchunks; c += nthreads) {
+        for (int k = 0; k < per_lane; ++k) {
+            const uint64_t off = c * (uint64_t)per_lane + k;
+            if (off >= total) break;
+            const uint64_t id = a.lo + off;
+            // ---- decode into this thread's record column ----
+            if (kIndex) {
+                if (k == 0) decode_index(id, J, tb.radix, opt, ord);
+                else advance_index(J, tb.radix, opt, ord);
+                for (int kk = 0; kk < J; ++kk) {
+                    const int job = ord[kk * 32];
+                    rec[kk * 32] = rec_for(tb, dur, rec_d, job, opt[job * 32]);
+                }
+            } else if (SRC == SAT_SRC_SUBSTREAM) {
+                decode_stream(mix64((a.seed ^ id) + kGolden), tb, dur, rec_d, rec);
+            } else {
+                decode_stream(a.seed + id, tb, dur, rec_d, rec);
+            }
+            // ---- list schedule ----
+            T mx = init_max;
+            if constexpr (!MULTI) {
+                T av[G];
+#pragma unroll
+                for (int i = 0; i < G; ++i) {
+                    av[i] = lane_init[i];
+                    st[i * 32] = av[i];
+                }
+                for (int kk = 0; kk < J; ++kk) {
+                    const uint32_t r = rec[kk * 32];
+                    const int g = (int)(r & 63u) + 1;
+                    const T d = rec_d ? (T)(int32_t)(r >> 12) : dur[r >> 12];
+                    T t = st[(g - 1) * 32];
+                    if (has_release) t = tmax(t, release[(r >> 6) & 63u]);
+                    const T e = t + d;
+                    T s[G];
+#pragma unroll
+                    for (int i = 0; i < G; ++i) s[i] = st[(i + g) * 32];
+#pragma unroll
+                    for (int i = 0; i < G; ++i) {
+                        av[i] = tmax(av[i], tmin(s[i], e));
+                        st[i * 32] = av[i];
+                    }
+                    mx = tmax(mx, e);
+                }
+            } else {
+                for (int n = 0; n < N; ++n)
+#pragma unroll
+                    for (int i = 0; i < G; ++i) st[(n * 2 * G + i) * 32] = lane_init[n * G + i];
+                for (int kk = 0; kk < J; ++kk) {
+                    const uint32_t r = rec[kk * 32];
+                    const int g = (int)(r & 63u) + 1;
+                    const uint32_t pay = r >> 12;
+                    const T rel = has_release ? release[(r >> 6) & 63u] : (T)0;
+                    // node finishing the job earliest, lowest node on ties
+                    T be = INF, bt = INF;
+                    int bn = 0;
+                    for (int n = 0; n < N; ++n) {
+                        T t = st[(n * 2 * G + g - 1) * 32];
+                        T d;
+                        if (rec_d) {
+                            d = (T)(int32_t)pay;
+                        } else {
+                            if (!((tb.optmask[pay] >> n) & 1u)) t = INF;
+                            d = dur[pay * N + n];
+                        }
+                        t = tmax(t, rel);
+                        const T e = t + d;
+                        if (n == 0 || e < be) { be = e; bt = t; bn = n; }
+                    }
+                    (void)bt;
+                    T *sb = st + bn * 2 * G * 32;
+                    T cur[G], s[G];
+#pragma unroll
+                    for (int i = 0; i < G; ++i) {
+                        cur[i] = sb[i * 32];
+                        s[i] = sb[(i + g) * 32];
+                    }
+#pragma unroll
+                    for (int i = 0; i < G; ++i) sb[i * 32] = tmax(cur[i], tmin(s[i], be));
+                    mx = tmax(mx, be);
+                }
+            }
+            if (key_less(mx, id, best_ms, best_ix)) {
+                best_ms = mx;
+                best_ix = id;
+            }
+        }
+    }
+
+    // ---- warp -> block -> grid argmin ----
+    for (int x = 16; x >= 1; x >>= 1) {
+        const T oms = __shfl_xor_sync(0xffffffffu, best_ms, x);
+        const uint64_t oix = shfl_u64(best_ix, lane ^ x);
+        if (key_less(oms, oix, best_ms, best_ix)) { best_ms = oms; best_ix = oix; }
+    }
+    __shared__ T s_ms[kCandWarps];
+    __shared__ uint64_t s_ix[kCandWarps];
+    if (lane == 0) { s_ms[warp] = best_ms; s_ix[warp] = best_ix; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < kCandWarps; ++w)
+            if (key_less(s_ms[w], s_ix[w], best_ms, best_ix)) { best_ms = s_ms[w]; best_ix = s_ix[w]; }
+        if (sizeof(T) == 4) {
+            if (best_ms < INF) {
+                const uint64_t key = ((uint64_t)(uint32_t)best_ms << h.idx_bits) | best_ix;
+                atomicMin(reinterpret_cast<unsigned long long *>(&a.best->hi), (unsigned long long)key);
+            }
+        } else {
+            a.partials[blockIdx.x].hi = (uint64_t)__double_as_longlong((double)best_ms);
+            a.partials[blockIdx.x].lo = best_ix;
+        }
+    }
+}
+
+// host launcher for one (T, SRC) pair; dispatches on the padded node size and N > 1
+template <typename T, int SRC>
+int launch_cand(const sat_problem_t *p, CandArgs a, uint64_t n_cand, void *d_ws, size_t ws_bytes,
+                cudaStream_t stream);
+
+}  // namespace sat

@@ -1,0 +1,178 @@
+// sat_decode.cuh -- the problem blob and the candidate decoders shared by the
+// per-candidate kernels (k_generic in sat_engine.cu, k_cand in sat_cand.cu).
+#pragma once
+
+#include "sat_common.cuh"
+
+namespace sat {
+// ---------------------------------------------------------------------------
+// Generic problem blob (host-packed, copied to the workspace, staged to smem)
+// ---------------------------------------------------------------------------
+struct BlobHeader {
+    int32_t J, N, G, W;
+    int32_t time_mode, idx_bits, n_opt, has_release;
+    int32_t max_n;            // largest n that below(n) is asked for (sampled decode)
+    int32_t bytes;            // total blob bytes
+    int32_t off_radix, off_optbase, off_g, off_mask, off_dur, off_release, off_lane_init, off_modn;
+    int32_t pad[2];
+    int64_t init_max_i32;
+    double init_max_f64;
+};
+static_assert(sizeof(BlobHeader) % 16 == 0, "blob header alignment");
+
+// per-n constants for SplitMix64 below(n): rejection threshold and a reciprocal
+struct ModN {
+    uint64_t reject_rem;  // (2^64 mod n): accept r iff r <= ~0 - reject_rem   (rng.py:37-41)
+    uint64_t magic;       // floor((2^64 - 1) / n)
+};
+
+__device__ inline uint64_t mod_small(uint64_t r, uint32_t n, uint64_t magic) {
+    uint64_t q = __umul64hi(r, magic);
+    uint64_t rem = r - q * (uint64_t)n;
+    while (rem >= n) rem -= n;
+    return rem;
+}
+
+// SplitMix64 stream with a draw counter: k-th output = mix64(state0 + k*GOLDEN)
+struct Stream {
+    uint64_t state;
+    __device__ inline uint64_t next() {
+        state += kGolden;
+        return mix64(state);
+    }
+    __device__ inline uint32_t below(uint32_t n, const ModN *mods) {
+        const ModN m = mods[n];
+        uint64_t r = next();
+        while (r > ~0ull - m.reject_rem) r = next();   // rejection (practically never taken)
+        return (uint32_t)mod_small(r, n, m.magic);
+    }
+};
+
+// ---------------------------------------------------------------------------
+// k_generic: candidate decode (one lane per candidate) + W-lane list scheduling
+// ---------------------------------------------------------------------------
+struct GenArgs {
+    const uint8_t *blob;
+    uint64_t lo, hi;            // candidate ids [lo, hi)
+    uint64_t seed;
+    int32_t per_lane;           // consecutive candidates per lane per batch (index source)
+    int32_t rec_d;              // step records carry the duration itself (one node, grid, search)
+    const uint64_t *ids;        // RECORD: explicit candidate ids (index/stream sources)
+    const uint8_t *expl;        // EXPLICIT source: [n][2J]
+    sat_best_t *best;           // grid mode result
+    sat_best_t *partials;       // float mode per-block partials
+    int32_t *rec_opt, *rec_node;
+    int32_t *rec_start_i32;
+    double *rec_start_f64;
+    int64_t *rec_ms_i64;
+    double *rec_ms_f64;
+};
+
+template <typename T>
+__device__ inline bool key_less(T ms_a, uint64_t ix_a, T ms_b, uint64_t ix_b) {
+    return ms_a < ms_b || (ms_a == ms_b && ix_a < ix_b);
+}
+
+// A candidate is decoded into J step records, one per position of the submission order:
+//   bits 0-5  gang size - 1      bits 6-11  job      bits 12-31  duration or global option q
+// stored lane-interleaved (record k of lane l at word k*32 + l): decode writes are
+// conflict-free and a W-lane segment reads its candidate's record as one broadcast.
+__device__ inline uint32_t step_rec(int g, int job, uint32_t payload) {
+    return (uint32_t)(g - 1) | ((uint32_t)job << 6) | (payload << 12);
+}
+
+struct GenTables {
+    const int32_t *radix, *optbase, *optg;
+    const uint32_t *optmask;
+    const ModN *mods;
+    int J, N;
+};
+
+template <typename T>
+__device__ inline uint32_t rec_for(const GenTables &t, const T *dur, bool rec_d, int job, int o) {
+    const int q = t.optbase[job] + o;
+    const uint32_t pay = rec_d ? (uint32_t)(int32_t)dur[q * t.N] : (uint32_t)q;
+    return step_rec(t.optg[q], job, pay);
+}
+
+// index -> option digits (job 0 most significant) and Lehmer-ranked order, into the
+// lane's interleaved u8 scratch
+__device__ inline void decode_index(uint64_t id, int J, const int32_t *radix, uint8_t *opt, uint8_t *ord) {
+    uint64_t f = 1;
+    for (int k = 2; k <= J; ++k) f *= (uint64_t)k;
+    uint64_t conf = id / f;
+    uint64_t perm = id - conf * f;
+    for (int j = J - 1; j >= 0; --j) {
+        const uint64_t r = (uint64_t)radix[j];
+        const uint64_t qd = conf / r;
+        opt[j * 32] = (uint8_t)(conf - qd * r);
+        conf = qd;
+    }
+    uint64_t unused = (J == 64) ? ~0ull : ((1ull << J) - 1ull);
+    for (int k = 0; k < J; ++k) {
+        f /= (uint64_t)(J - k);                       // (J-1-k)!
+        const uint64_t digit = perm / f;
+        perm -= digit * f;
+        uint64_t m = unused;
+        for (uint64_t x = 0; x < digit; ++x) m &= m - 1;
+        const int job = __ffsll((long long)m) - 1;
+        ord[k * 32] = (uint8_t)job;
+        unused &= ~(1ull << job);
+    }
+}
+
+// index + 1: next lexicographic permutation; on wrap, odometer the option digits
+__device__ inline void advance_index(int J, const int32_t *radix, uint8_t *opt, uint8_t *ord) {
+    int i = J - 2;
+    while (i >= 0 && ord[i * 32] >= ord[(i + 1) * 32]) --i;
+    if (i >= 0) {
+        int k = J - 1;
+        while (ord[k * 32] <= ord[i * 32]) --k;
+        uint8_t t = ord[i * 32]; ord[i * 32] = ord[k * 32]; ord[k * 32] = t;
+        for (int a = i + 1, b = J - 1; a < b; ++a, --b) { t = ord[a * 32]; ord[a * 32] = ord[b * 32]; ord[b * 32] = t; }
+        return;
+    }
+    for (int k = 0; k < J; ++k) ord[k * 32] = (uint8_t)k;
+    for (int j = J - 1; j >= 0; --j) {
+        if ((int)opt[j * 32] + 1 < radix[j]) { opt[j * 32] += 1; return; }
+        opt[j * 32] = 0;
+    }
+}
+
+// plan_random draw order: below(radix_j) per job in id order, then a
+// Fisher-Yates shuffle of the order -- applied directly to the step records.
+template <typename T>
+__device__ inline void decode_stream(uint64_t state0, const GenTables &t, const T *dur, bool rec_d,
+                                     uint32_t *steps) {
+    Stream s{state0};
+    for (int j = 0; j < t.J; ++j) {
+        const int o = (int)s.below((uint32_t)t.radix[j], t.mods);
+        steps[j * 32] = rec_for(t, dur, rec_d, j, o);
+    }
+    for (int i = t.J - 1; i >= 1; --i) {                 // rng.py:44-48
+        const int k = (int)s.below((uint32_t)(i + 1), t.mods);
+        const uint32_t x = steps[i * 32];
+        steps[i * 32] = steps[k * 32];
+        steps[k * 32] = x;
+    }
+}
+
+
+// float mode: fold per-block partials into *best (lexicographic on (ms bits, index))
+static __global__ void k_fold_partials(const sat_best_t *partials, int n, sat_best_t *best) {
+    uint64_t hi = best->hi, lo = best->lo;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < n; ++i) {
+            const uint64_t ph = partials[i].hi, pl = partials[i].lo;
+            if (ph < hi || (ph == hi && pl < lo)) { hi = ph; lo = pl; }
+        }
+        best->hi = hi;
+        best->lo = lo;
+    }
+}
+
+
+// host: pack the problem into the blob staged to shared memory (sat_engine.cu)
+int pack_blob(const sat_problem_t *p, std::vector<uint8_t> &blob);
+
+}  // namespace sat
