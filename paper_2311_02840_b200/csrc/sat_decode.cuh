@@ -33,6 +33,16 @@ __device__ inline uint64_t mod_small(uint64_t r, uint32_t n, uint64_t magic) {
     return rem;
 }
 
+// r mod n for n <= 255 without a loop: q = umulhi(r, floor((2^64-1)/n)) is floor(r/n) or
+// one less (r*magic/2^64 lies in (r/n - 1, r/n]), so r - q*n < 2n < 2^32 is exact in the
+// low word and needs at most one conditional subtract.
+__device__ __forceinline__ uint32_t mod_small_fast(uint64_t r, uint32_t n, uint64_t magic) {
+    const uint64_t q = __umul64hi(r, magic);
+    uint32_t rem = (uint32_t)r - (uint32_t)q * n;
+    rem = rem >= n ? rem - n : rem;
+    return rem;
+}
+
 // SplitMix64 stream with a draw counter: k-th output = mix64(state0 + k*GOLDEN)
 struct Stream {
     uint64_t state;
@@ -40,11 +50,20 @@ struct Stream {
         state += kGolden;
         return mix64(state);
     }
+    // exact below(n) (rng.py:34-42), rejection loop included
     __device__ inline uint32_t below(uint32_t n, const ModN *mods) {
         const ModN m = mods[n];
         uint64_t r = next();
         while (r > ~0ull - m.reject_rem) r = next();   // rejection (practically never taken)
         return (uint32_t)mod_small(r, n, m.magic);
+    }
+    // below(n) assuming no rejection; `hi_max` accumulates the draws' high words.  A draw
+    // can only be rejected when r >= 2^64 - (2^64 mod n) > 2^64 - 2^32, i.e. its high word
+    // is all ones, so hi_max != 0xffffffff proves every fast draw equals the exact one.
+    __device__ __forceinline__ uint32_t below_fast(uint32_t n, uint64_t magic, uint32_t &hi_max) {
+        const uint64_t r = next();
+        hi_max = max(hi_max, (uint32_t)(r >> 32));
+        return mod_small_fast(r, n, magic);
     }
 };
 
@@ -140,20 +159,37 @@ __device__ inline void advance_index(int J, const int32_t *radix, uint8_t *opt, 
 }
 
 // plan_random draw order: below(radix_j) per job in id order, then a
-// Fisher-Yates shuffle of the order -- applied directly to the step records.
+// Fisher-Yates shuffle of the order -- applied directly to the step records.  The
+// common path skips the rejection tests; in the (p ~ 1e-17 per draw) case a draw could
+// have been rejected, the candidate is decoded again with the exact loops.
 template <typename T>
 __device__ inline void decode_stream(uint64_t state0, const GenTables &t, const T *dur, bool rec_d,
                                      uint32_t *steps) {
     Stream s{state0};
+    uint32_t hi_max = 0;
     for (int j = 0; j < t.J; ++j) {
-        const int o = (int)s.below((uint32_t)t.radix[j], t.mods);
+        const uint32_t n = (uint32_t)t.radix[j];
+        const int o = (int)s.below_fast(n, t.mods[n].magic, hi_max);
         steps[j * 32] = rec_for(t, dur, rec_d, j, o);
     }
     for (int i = t.J - 1; i >= 1; --i) {                 // rng.py:44-48
-        const int k = (int)s.below((uint32_t)(i + 1), t.mods);
+        const int k = (int)s.below_fast((uint32_t)(i + 1), t.mods[i + 1].magic, hi_max);
         const uint32_t x = steps[i * 32];
         steps[i * 32] = steps[k * 32];
         steps[k * 32] = x;
+    }
+    if (hi_max == 0xffffffffu) {
+        s.state = state0;
+        for (int j = 0; j < t.J; ++j) {
+            const int o = (int)s.below((uint32_t)t.radix[j], t.mods);
+            steps[j * 32] = rec_for(t, dur, rec_d, j, o);
+        }
+        for (int i = t.J - 1; i >= 1; --i) {
+            const int k = (int)s.below((uint32_t)(i + 1), t.mods);
+            const uint32_t x = steps[i * 32];
+            steps[i * 32] = steps[k * 32];
+            steps[k * 32] = x;
+        }
     }
 }
 
