@@ -17,7 +17,9 @@
 // nodes: the node is chosen at run time).  Rows G..2G-1 of a node hold +inf.
 //
 // Per placement: 1 + G shared loads, G shared stores, G min + G max, 1 add, 1 max
-// (one node); multi-node adds N loads + the earliest-finish node pick.
+// (one node); multi-node adds N loads + the earliest-finish node pick.  When no free
+// time can reach 2^16 (grid time, one node) two slots share a word: G/2 + 2 loads,
+// G/2 stores, G/2 PRMT + G/2 VIMNMX.U16x2 min + G/2 max per placement.
 #pragma once
 
 #include "sat_decode.cuh"
@@ -42,9 +44,16 @@ __host__ __device__ inline int cand_warp_bytes(int J, int N, int G, int tsz, boo
     return J * 128 + (index_src ? J * 64 : 0) + N * 2 * G * 32 * tsz;
 }
 
-template <typename T, int SRC, int G, bool MULTI>
+// Layouts of the free-time state (template parameter L)
+constexpr int kLayoutOne = 0;     // one node, 32-bit (or fp64) slots
+constexpr int kLayoutMulti = 1;   // several nodes, node chosen per placement
+constexpr int kLayoutOne16 = 2;   // one node, two 16-bit slots per word (grid time < 2^16)
+
+template <typename T, int SRC, int G, int L>
 __global__ void __launch_bounds__(kCandThreads)
 k_cand(CandArgs a) {
+    constexpr bool MULTI = L == kLayoutMulti;
+    constexpr bool P16 = L == kLayoutOne16;
     extern __shared__ __align__(16) uint8_t smem[];
     {
         const int nwords = (*reinterpret_cast<const BlobHeader *>(a.blob)).bytes / 16;
@@ -77,11 +86,17 @@ k_cand(CandArgs a) {
     uint8_t *opt = wbase + J * 128 + lane;                               // [J][32] (index source)
     uint8_t *ord = opt + J * 32;                                         // [J][32]
     T *st = reinterpret_cast<T *>(wbase + J * 128 + (kIndex ? J * 64 : 0)) + lane;   // [N][2G][32]
+    uint32_t *st16 = reinterpret_cast<uint32_t *>(st);                               // [G][32] words
 
     const T INF = TimeTraits<T>::inf();
-    for (int n = 0; n < N; ++n)
+    if constexpr (P16) {
 #pragma unroll
-        for (int i = G; i < 2 * G; ++i) st[(n * 2 * G + i) * 32] = INF;
+        for (int w = G / 2; w < G; ++w) st16[w * 32] = 0xffffffffu;
+    } else {
+        for (int n = 0; n < N; ++n)
+#pragma unroll
+            for (int i = G; i < 2 * G; ++i) st[(n * 2 * G + i) * 32] = INF;
+    }
     const T init_max = sizeof(T) == 4 ? (T)h.init_max_i32 : (T)h.init_max_f64;
 
     T best_ms = INF;
@@ -113,7 +128,40 @@ k_cand(CandArgs a) {
             }
             // ---- list schedule ----
             T mx = init_max;
-            if constexpr (!MULTI) {
+            if constexpr (P16) {
+                // slots 2w (low half) and 2w+1 (high half) of word w; rows G/2..G-1 = +inf.
+                // Shift by the thread's g: word k of the shifted vector is word g/2 + k (g even)
+                // or the high half of word g/2 + k joined to the low half of the next (g odd):
+                // one PRMT with a per-thread selector either way.
+                const uint16_t *st_h = reinterpret_cast<const uint16_t *>(st16);
+                uint32_t av[G / 2];
+#pragma unroll
+                for (int w = 0; w < G / 2; ++w) {
+                    av[w] = (uint32_t)(uint16_t)lane_init[2 * w] | ((uint32_t)(uint16_t)lane_init[2 * w + 1] << 16);
+                    st16[w * 32] = av[w];
+                }
+                for (int kk = 0; kk < J; ++kk) {
+                    const uint32_t r = rec[kk * 32];
+                    const int g = (int)(r & 63u) + 1;
+                    const int gm = g - 1;
+                    int32_t t = (int32_t)st_h[((gm >> 1) * 32) * 2 + (gm & 1)];
+                    if (has_release) t = max(t, (int32_t)release[(r >> 6) & 63u]);
+                    const int32_t e = t + (int32_t)(r >> 12);
+                    const uint32_t e2 = (uint32_t)e * 0x10001u;
+                    const uint32_t sel = (g & 1) ? 0x5432u : 0x3210u;
+                    const uint32_t *src = st16 + (g >> 1) * 32;
+                    uint32_t w[G / 2 + 1];
+#pragma unroll
+                    for (int k = 0; k <= G / 2; ++k) w[k] = src[k * 32];
+#pragma unroll
+                    for (int k = 0; k < G / 2; ++k) {
+                        const uint32_t s = __byte_perm(w[k], w[k + 1], sel);
+                        av[k] = __vmaxu2(av[k], __vminu2(s, e2));
+                        st16[k * 32] = av[k];
+                    }
+                    mx = tmax(mx, (T)e);
+                }
+            } else if constexpr (!MULTI) {
                 T av[G];
 #pragma unroll
                 for (int i = 0; i < G; ++i) {
@@ -207,7 +255,7 @@ k_cand(CandArgs a) {
     }
 }
 
-// host launcher for one (T, SRC) pair; dispatches on the padded node size and N > 1
+// host launcher for one (T, SRC) pair; dispatches on the padded node size and layout
 template <typename T, int SRC>
 int launch_cand(const sat_problem_t *p, CandArgs a, uint64_t n_cand, void *d_ws, size_t ws_bytes,
                 cudaStream_t stream);

@@ -165,6 +165,25 @@ def test_float_mode_full_space(eng):
         assert float(got[0]).hex() == float(want[0]).hex()       # bit-exact, stricter than 1e-6
 
 
+def test_wide_times_use_32bit_slots(eng):
+    """One node with free times past 2^16 (the packed 16-bit layout must not be used) and
+    right at its boundary: index and sampled searches still equal the oracle."""
+    rng = random.Random(77)
+    for trial in range(16):
+        nodes = [[rng.randint(2, 8)], [rng.randint(9, 16)], [rng.randint(17, 32)], [1]][trial % 4]
+        op = random_problem(rng, rng.randint(2, 5), nodes, max_opts=3, max_d=9)
+        scale = [40000, 9000, 13107, 21845][trial % 4]          # bounds on both sides of 65535
+        op.dur = [[[d * scale for d in row] for row in job] for job in op.dur]
+        op.runtime = [[list(r) for r in job] for job in op.dur]
+        if trial % 2:
+            op.release = [rng.randint(0, 3) * scale for _ in range(op.J)]
+            op.init_free = [[rng.randint(0, 2) * scale for _ in range(n)] for n in nodes]
+        prob = to_search_problem(op)
+        assert gpu_key(eng, prob, "index") == C.CProblem(op).search(), trial
+        got = gpu_key(eng, prob, "sampled", 0, 3000, source=EN.SRC_SUBSTREAM, seed=trial, n_idx=3000)
+        assert got == C.CProblem(op).search("substream", trial, 0, 3000), trial
+
+
 # --------------------------------------------------------------------------- sampled
 @pytest.mark.parametrize("name", ["cfg3", "cfg4", "cfg5", "hetero6"])
 @pytest.mark.parametrize("source", [EN.SRC_SUBSTREAM, EN.SRC_SEED])
