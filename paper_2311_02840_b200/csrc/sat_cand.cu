@@ -52,26 +52,12 @@ static int launch_cand_g(const sat_problem_t *p, CandArgs a, uint64_t n_cand, co
 template <typename T, int SRC>
 int launch_cand(const sat_problem_t *p, CandArgs a, uint64_t n_cand, void *d_ws, size_t ws_bytes,
                 cudaStream_t stream) {
-    std::vector<uint8_t> blob;
-    int st = pack_blob(p, blob);
-    if (st) return st;
     // durations ride in the step records when they do not depend on the node and every
     // option may run on every node (grid time, fits the 20-bit payload)
-    a.rec_d = 0;
-    if (sizeof(T) == 4) {
-        bool ok = true;
-        const uint32_t all = p->N >= 32 ? ~0u : ((1u << p->N) - 1u);
-        for (int j = 0; j < p->J && ok; ++j)
-            for (int o = 0; o < p->radix[j] && ok; ++o) {
-                const int q = j * p->Cmax + o;
-                const int32_t d0 = p->dur_i32[q * p->N];
-                if (d0 < 0 || d0 >= (1 << 20)) ok = false;
-                if (p->node_mask && (p->node_mask[q] & all) != all) ok = false;
-                for (int n = 1; n < p->N && ok; ++n)
-                    if (p->dur_i32[q * p->N + n] != d0) ok = false;
-            }
-        a.rec_d = ok ? 1 : 0;
-    }
+    a.rec_d = records_carry_duration(p) ? 1 : 0;
+    std::vector<uint8_t> blob;
+    int st = pack_blob(p, blob, a.rec_d != 0);
+    if (st) return st;
     const bool multi = p->N > 1;
     // 16-bit packed slots when no free time can reach 2^16 - 1 (one node, grid time, records
     // carry the durations): bound = latest initial free time + latest release + sum of the

@@ -66,13 +66,7 @@ k_cand(CandArgs a) {
     const int J = h.J;
     const int N = MULTI ? h.N : 1;
     GenTables tb;
-    tb.radix = reinterpret_cast<const int32_t *>(smem + h.off_radix);
-    tb.optbase = reinterpret_cast<const int32_t *>(smem + h.off_optbase);
-    tb.optg = reinterpret_cast<const int32_t *>(smem + h.off_g);
-    tb.optmask = reinterpret_cast<const uint32_t *>(smem + h.off_mask);
-    tb.mods = reinterpret_cast<const ModN *>(smem + h.off_modn);
-    tb.J = J;
-    tb.N = h.N;
+    load_tables(tb, smem, h);
     const T *dur = reinterpret_cast<const T *>(smem + h.off_dur);
     const T *release = reinterpret_cast<const T *>(smem + h.off_release);
     const T *lane_init = reinterpret_cast<const T *>(smem + h.off_lane_init);   // [N][G] (blob G == G)
@@ -119,12 +113,12 @@ k_cand(CandArgs a) {
                 else advance_index(J, tb.radix, opt, ord);
                 for (int kk = 0; kk < J; ++kk) {
                     const int job = ord[kk * 32];
-                    rec[kk * 32] = rec_for(tb, dur, rec_d, job, opt[job * 32]);
+                    rec[kk * 32] = rec_for(tb, job, opt[job * 32]);
                 }
             } else if (SRC == SAT_SRC_SUBSTREAM) {
-                decode_stream(mix64((a.seed ^ id) + kGolden), tb, dur, rec_d, rec);
+                decode_stream(mix64((a.seed ^ id) + kGolden), tb, rec);
             } else {
-                decode_stream(a.seed + id, tb, dur, rec_d, rec);
+                decode_stream(a.seed + id, tb, rec);
             }
             // ---- list schedule ----
             T mx = init_max;

@@ -14,7 +14,7 @@ struct BlobHeader {
     int32_t max_n;            // largest n that below(n) is asked for (sampled decode)
     int32_t bytes;            // total blob bytes
     int32_t off_radix, off_optbase, off_g, off_mask, off_dur, off_release, off_lane_init, off_modn;
-    int32_t pad[2];
+    int32_t off_prerec, off_jobinfo;   // per-option step records, per-job draw constants
     int64_t init_max_i32;
     double init_max_f64;
 };
@@ -100,18 +100,37 @@ __device__ inline uint32_t step_rec(int g, int job, uint32_t payload) {
     return (uint32_t)(g - 1) | ((uint32_t)job << 6) | (payload << 12);
 }
 
+// per-job constants of the option draw below(radix_j): one 16-byte broadcast load
+struct JobInfo {
+    int32_t radix;
+    int32_t optbase;     // global id of option 0 of the job
+    uint64_t magic;      // floor((2^64 - 1) / radix)
+};
+
 struct GenTables {
-    const int32_t *radix, *optbase, *optg;
+    const int32_t *radix, *optbase;
     const uint32_t *optmask;
+    const uint32_t *prerec;    // [n_opt] step record of every option (host-built)
+    const JobInfo *jobinfo;    // [J]
     const ModN *mods;
     int J, N;
 };
 
-template <typename T>
-__device__ inline uint32_t rec_for(const GenTables &t, const T *dur, bool rec_d, int job, int o) {
-    const int q = t.optbase[job] + o;
-    const uint32_t pay = rec_d ? (uint32_t)(int32_t)dur[q * t.N] : (uint32_t)q;
-    return step_rec(t.optg[q], job, pay);
+// step record of job `job` running option `o` (payload = duration or global option id,
+// fixed per problem on the host)
+__device__ __forceinline__ uint32_t rec_for(const GenTables &t, int job, int o) {
+    return t.prerec[t.optbase[job] + o];
+}
+
+__device__ inline void load_tables(GenTables &tb, const uint8_t *smem, const BlobHeader &h) {
+    tb.radix = reinterpret_cast<const int32_t *>(smem + h.off_radix);
+    tb.optbase = reinterpret_cast<const int32_t *>(smem + h.off_optbase);
+    tb.optmask = reinterpret_cast<const uint32_t *>(smem + h.off_mask);
+    tb.prerec = reinterpret_cast<const uint32_t *>(smem + h.off_prerec);
+    tb.jobinfo = reinterpret_cast<const JobInfo *>(smem + h.off_jobinfo);
+    tb.mods = reinterpret_cast<const ModN *>(smem + h.off_modn);
+    tb.J = h.J;
+    tb.N = h.N;
 }
 
 // index -> option digits (job 0 most significant) and Lehmer-ranked order, into the
@@ -162,15 +181,13 @@ __device__ inline void advance_index(int J, const int32_t *radix, uint8_t *opt, 
 // Fisher-Yates shuffle of the order -- applied directly to the step records.  The
 // common path skips the rejection tests; in the (p ~ 1e-17 per draw) case a draw could
 // have been rejected, the candidate is decoded again with the exact loops.
-template <typename T>
-__device__ inline void decode_stream(uint64_t state0, const GenTables &t, const T *dur, bool rec_d,
-                                     uint32_t *steps) {
+__device__ inline void decode_stream(uint64_t state0, const GenTables &t, uint32_t *steps) {
     Stream s{state0};
     uint32_t hi_max = 0;
     for (int j = 0; j < t.J; ++j) {
-        const uint32_t n = (uint32_t)t.radix[j];
-        const int o = (int)s.below_fast(n, t.mods[n].magic, hi_max);
-        steps[j * 32] = rec_for(t, dur, rec_d, j, o);
+        const JobInfo ji = t.jobinfo[j];
+        const int o = (int)s.below_fast((uint32_t)ji.radix, ji.magic, hi_max);
+        steps[j * 32] = t.prerec[ji.optbase + o];
     }
     for (int i = t.J - 1; i >= 1; --i) {                 // rng.py:44-48
         const int k = (int)s.below_fast((uint32_t)(i + 1), t.mods[i + 1].magic, hi_max);
@@ -182,7 +199,7 @@ __device__ inline void decode_stream(uint64_t state0, const GenTables &t, const 
         s.state = state0;
         for (int j = 0; j < t.J; ++j) {
             const int o = (int)s.below((uint32_t)t.radix[j], t.mods);
-            steps[j * 32] = rec_for(t, dur, rec_d, j, o);
+            steps[j * 32] = rec_for(t, j, o);
         }
         for (int i = t.J - 1; i >= 1; --i) {
             const int k = (int)s.below((uint32_t)(i + 1), t.mods);
@@ -208,7 +225,10 @@ static __global__ void k_fold_partials(const sat_best_t *partials, int n, sat_be
 }
 
 
-// host: pack the problem into the blob staged to shared memory (sat_engine.cu)
-int pack_blob(const sat_problem_t *p, std::vector<uint8_t> &blob);
+// host (sat_engine.cu): whether step records can carry the duration itself (grid time,
+// node-independent durations < 2^20, every option runnable on every node), and the blob
+// staged to shared memory (records carry durations iff rec_d)
+bool records_carry_duration(const sat_problem_t *p);
+int pack_blob(const sat_problem_t *p, std::vector<uint8_t> &blob, bool rec_d);
 
 }  // namespace sat

@@ -50,13 +50,7 @@ k_generic(GenArgs a) {
     __syncthreads();
     const int J = h.J, N = h.N, G = h.G, W = h.W;
     GenTables tb;
-    tb.radix = reinterpret_cast<const int32_t *>(smem + h.off_radix);
-    tb.optbase = reinterpret_cast<const int32_t *>(smem + h.off_optbase);
-    tb.optg = reinterpret_cast<const int32_t *>(smem + h.off_g);
-    tb.optmask = reinterpret_cast<const uint32_t *>(smem + h.off_mask);
-    tb.mods = reinterpret_cast<const ModN *>(smem + h.off_modn);
-    tb.J = J;
-    tb.N = N;
+    load_tables(tb, smem, h);
     const T *dur = reinterpret_cast<const T *>(smem + h.off_dur);
     const T *release = reinterpret_cast<const T *>(smem + h.off_release);
     const T *lane_init = reinterpret_cast<const T *>(smem + h.off_lane_init);
@@ -102,23 +96,23 @@ k_generic(GenArgs a) {
                     else advance_index(J, tb.radix, my_opt, my_ord);
                     for (int kk = 0; kk < J; ++kk) {
                         const int job = my_ord[kk * 32];
-                        my_steps[kk * 32] = rec_for(tb, dur, rec_d, job, my_opt[job * 32]);
+                        my_steps[kk * 32] = rec_for(tb, job, my_opt[job * 32]);
                     }
                 } else if (SRC == SAT_SRC_SUBSTREAM) {
-                    decode_stream(mix64((a.seed ^ id) + kGolden), tb, dur, rec_d, my_steps);
+                    decode_stream(mix64((a.seed ^ id) + kGolden), tb, my_steps);
                 } else if (SRC == SAT_SRC_SEED) {
-                    decode_stream(a.seed + id, tb, dur, rec_d, my_steps);
+                    decode_stream(a.seed + id, tb, my_steps);
                 } else {
                     // memory safety only: the host validates explicit candidates before upload
                     const uint8_t *e = a.expl + (size_t)(RECORD ? off : id) * (2 * J);
                     for (int kk = 0; kk < J; ++kk) {
                         const int job = e[J + kk] % J;
-                        my_steps[kk * 32] = rec_for(tb, dur, rec_d, job, min((int)e[job], tb.radix[job] - 1));
+                        my_steps[kk * 32] = rec_for(tb, job, min((int)e[job], tb.radix[job] - 1));
                     }
                 }
             } else {
                 // no candidate for this lane: park a harmless one (its key is discarded)
-                for (int kk = 0; kk < J; ++kk) my_steps[kk * 32] = rec_for(tb, dur, rec_d, kk, 0);
+                for (int kk = 0; kk < J; ++kk) my_steps[kk * 32] = rec_for(tb, kk, 0);
             }
             __syncwarp();
             // ---- schedule: segment `seg` handles candidate slot pass * segs + seg ----
@@ -273,8 +267,23 @@ int device_sms() {
     return sms > 0 ? sms : 148;
 }
 
+bool records_carry_duration(const sat_problem_t *p) {
+    if (p->time_mode != SAT_TIME_GRID_I32) return false;
+    const uint32_t all = p->N >= 32 ? ~0u : ((1u << p->N) - 1u);
+    for (int j = 0; j < p->J; ++j)
+        for (int o = 0; o < p->radix[j]; ++o) {
+            const int q = j * p->Cmax + o;
+            const int32_t d0 = p->dur_i32[q * p->N];
+            if (d0 < 0 || d0 >= (1 << 20)) return false;
+            if (p->node_mask && (p->node_mask[q] & all) != all) return false;
+            for (int n = 1; n < p->N; ++n)
+                if (p->dur_i32[q * p->N + n] != d0) return false;
+        }
+    return true;
+}
+
 // Build the generic blob.  Lane init: for W lanes, node = lane / G, slot = lane % G.
-int pack_blob(const sat_problem_t *p, std::vector<uint8_t> &blob) {
+int pack_blob(const sat_problem_t *p, std::vector<uint8_t> &blob, bool rec_d) {
     const int J = p->J, N = p->N, G = p->G;
     int W = 8;
     while (W < N * G) W <<= 1;
@@ -289,17 +298,21 @@ int pack_blob(const sat_problem_t *p, std::vector<uint8_t> &blob) {
     int off = sizeof(BlobHeader);
     h.off_radix = off; off = align16(off + 4 * J);
     h.off_optbase = off; off = align16(off + 4 * J);
-    h.off_g = off; off = align16(off + 4 * n_opt);
-    h.off_mask = off; off = align16(off + 4 * n_opt);
-    h.off_dur = off; off = align16(off + tsz * n_opt * N);
+    // tables only the paths that read them get: node masks with several nodes, the
+    // duration table unless every record carries its duration
+    const bool need_mask = N > 1, need_dur = !rec_d;
+    h.off_g = off;                                     // (gang sizes ride in the records)
+    h.off_mask = off; off = align16(off + (need_mask ? 4 * n_opt : 0));
+    h.off_dur = off; off = align16(off + (need_dur ? tsz * n_opt * N : 0));
     h.off_release = off; off = align16(off + tsz * J);
     h.off_lane_init = off; off = align16(off + tsz * W);
     h.off_modn = off; off = align16(off + (int)sizeof(ModN) * (max_n + 1));
+    h.off_prerec = off; off = align16(off + 4 * n_opt);
+    h.off_jobinfo = off; off = align16(off + (int)sizeof(JobInfo) * J);
     h.bytes = off;
     blob.assign(off, 0);
     int32_t *radix = reinterpret_cast<int32_t *>(&blob[h.off_radix]);
     int32_t *optbase = reinterpret_cast<int32_t *>(&blob[h.off_optbase]);
-    int32_t *og = reinterpret_cast<int32_t *>(&blob[h.off_g]);
     uint32_t *om = reinterpret_cast<uint32_t *>(&blob[h.off_mask]);
     int q = 0;
     bool has_release = false;
@@ -308,11 +321,10 @@ int pack_blob(const sat_problem_t *p, std::vector<uint8_t> &blob) {
         optbase[j] = q;
         for (int o = 0; o < p->radix[j]; ++o, ++q) {
             const int src = j * p->Cmax + o;
-            og[q] = p->gpus[src];
             uint32_t m = p->node_mask ? p->node_mask[src] : ((N >= 32) ? ~0u : ((1u << N) - 1u));
             if (N < 32) m &= (1u << N) - 1u;
-            om[q] = m;
-            for (int n = 0; n < N; ++n) {
+            if (need_mask) om[q] = m;
+            for (int n = 0; n < N && need_dur; ++n) {
                 if (f64) reinterpret_cast<double *>(&blob[h.off_dur])[q * N + n] = p->dur_f64[src * N + n];
                 else reinterpret_cast<int32_t *>(&blob[h.off_dur])[q * N + n] = p->dur_i32[src * N + n];
             }
@@ -352,6 +364,18 @@ int pack_blob(const sat_problem_t *p, std::vector<uint8_t> &blob) {
         mods[n].reject_rem = (uint64_t)(two64 % (unsigned)n);
         mods[n].magic = ~0ull / (uint64_t)n;
     }
+    uint32_t *prerec = reinterpret_cast<uint32_t *>(&blob[h.off_prerec]);
+    JobInfo *ji = reinterpret_cast<JobInfo *>(&blob[h.off_jobinfo]);
+    for (int j = 0, qq = 0; j < J; ++j) {
+        ji[j].radix = p->radix[j];
+        ji[j].optbase = qq;
+        ji[j].magic = ~0ull / (uint64_t)p->radix[j];
+        for (int o = 0; o < p->radix[j]; ++o, ++qq) {
+            const int src = j * p->Cmax + o;
+            const uint32_t pay = rec_d ? (uint32_t)p->dur_i32[src * N] : (uint32_t)qq;
+            prerec[qq] = (uint32_t)(p->gpus[src] - 1) | ((uint32_t)j << 6) | (pay << 12);
+        }
+    }
     std::memcpy(blob.data(), &h, sizeof(h));
     return SAT_OK;
 }
@@ -369,19 +393,11 @@ template <typename T, int SRC, bool RECORD>
 int launch_generic(const sat_problem_t *p, GenArgs a, uint64_t n_cand, void *d_ws, size_t ws_bytes,
                    cudaStream_t stream) {
     std::vector<uint8_t> blob;
-    int st = pack_blob(p, blob);
+    a.rec_d = 0;                 // recorded plans need the option id in every record
+    int st = pack_blob(p, blob, false);
     if (st) return st;
     const size_t blob_bytes = blob.size();
     const int smem = (int)blob_bytes + kGenWarps * p->J * 32 * (4 + (SRC == SAT_SRC_INDEX ? 2 : 0));
-    // one node + grid time: step records carry the duration itself (no table lookup per step)
-    a.rec_d = 0;
-    if (!RECORD && sizeof(T) == 4 && p->N == 1) {
-        a.rec_d = 1;
-        for (int j = 0; j < p->J; ++j)
-            for (int o = 0; o < p->radix[j]; ++o)
-                if (p->dur_i32[(j * p->Cmax + o) * p->N] >= (1 << 20) || p->dur_i32[(j * p->Cmax + o) * p->N] < 0)
-                    a.rec_d = 0;
-    }
     if (smem > 200 * 1024) return SAT_ERR_TOO_LARGE;
     auto kern = k_generic<T, SRC, RECORD>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
@@ -547,7 +563,7 @@ int sat_workspace_bytes(const sat_problem_t *p, size_t *bytes) {
     int st = validate(p);
     if (st) return st;
     std::vector<uint8_t> blob;
-    st = pack_blob(p, blob);
+    st = pack_blob(p, blob, records_carry_duration(p));
     if (st) return st;
     const size_t part_off = (blob.size() + 255) & ~(size_t)255;
     *bytes = part_off + (size_t)device_sms() * 32 * sizeof(sat_best_t);
