@@ -12,13 +12,13 @@ namespace sat {
 template <typename T, int SRC, int G, int L>
 static int launch_cand_g(const sat_problem_t *p, CandArgs a, uint64_t n_cand, const std::vector<uint8_t> &blob,
                          void *d_ws, size_t ws_bytes, cudaStream_t stream) {
-    if constexpr (L == kLayoutOne16 && sizeof(T) != 4) {
+    if constexpr ((L == kLayoutOne16 || L == kLayoutMulti16) && sizeof(T) != 4) {
         return SAT_ERR_UNSUPPORTED;      // packed slots are grid-time only
     } else {
     const size_t blob_bytes = blob.size();
-    const int N = L == kLayoutMulti ? p->N : 1;
+    const int N = (L == kLayoutMulti || L == kLayoutMulti16) ? p->N : 1;
     const int smem = (int)blob_bytes +
-                     kCandWarps * cand_warp_bytes(p->J, N, G, (int)sizeof(T), SRC == SAT_SRC_INDEX);
+                     kCandWarps * cand_warp_bytes(p->J, N, G, cand_slot_bytes<T, L>(), SRC == SAT_SRC_INDEX);
     if (smem > 220 * 1024) return SAT_ERR_TOO_LARGE;
     auto kern = k_cand<T, SRC, G, L>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
@@ -63,21 +63,24 @@ int launch_cand(const sat_problem_t *p, CandArgs a, uint64_t n_cand, void *d_ws,
     // carry the durations): bound = latest initial free time + latest release + sum of the
     // longest option of every job
     bool p16 = false;
-    if (sizeof(T) == 4 && !multi && a.rec_d && p->G >= 2) {
+    if (sizeof(T) == 4 && a.rec_d && p->G >= 2) {
         int64_t bound = 0, rel = 0, init = 0;
         for (int j = 0; j < p->J; ++j) {
             int32_t dm = 0;
-            for (int o = 0; o < p->radix[j]; ++o) dm = std::max(dm, p->dur_i32[j * p->Cmax + o]);
+            for (int o = 0; o < p->radix[j]; ++o) dm = std::max(dm, p->dur_i32[(j * p->Cmax + o) * p->N]);
             bound += dm;
             if (p->release_i32) rel = std::max<int64_t>(rel, p->release_i32[j]);
         }
-        for (int i = 0; i < p->node_gpus[0]; ++i)
-            if (p->init_free_i32) init = std::max<int64_t>(init, p->init_free_i32[i]);
+        for (int n = 0; n < p->N; ++n)
+            for (int i = 0; i < p->node_gpus[n]; ++i)
+                if (p->init_free_i32) init = std::max<int64_t>(init, p->init_free_i32[n * p->G + i]);
         p16 = bound + rel + init < 0xffff;
     }
     switch (p->G) {
 #define SAT_CASE(K)                                                                                      \
     case K:                                                                                              \
+        if (multi && K >= 2 && p16)                                                                      \
+            return launch_cand_g<T, SRC, (K <= 16 ? (K >= 2 ? K : 2) : 16), kLayoutMulti16>(p, a, n_cand, blob, d_ws, ws_bytes, stream); \
         if (multi)                                                                                       \
             return launch_cand_g<T, SRC, (K <= 16 ? K : 16), kLayoutMulti>(p, a, n_cand, blob, d_ws, ws_bytes, stream); \
         if (K >= 2 && p16)                                                                               \

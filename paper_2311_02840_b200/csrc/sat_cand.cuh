@@ -1,4 +1,4 @@
-// sat_cand.cuh -- k_cand<T, SRC, G, MULTI>: one candidate per THREAD.
+// sat_cand.cuh -- k_cand<T, SRC, G, L>: one candidate per THREAD.
 //
 // The search kernel for everything the prefix-shared walk (k_tree) does not cover:
 // sampled candidate streams (plan_random draws, configs 3-5), multi-node clusters,
@@ -40,20 +40,31 @@ struct CandArgs {
 };
 
 // bytes of one warp's private region: records, index scratch, free-time columns
-__host__ __device__ inline int cand_warp_bytes(int J, int N, int G, int tsz, bool index_src) {
-    return J * 128 + (index_src ? J * 64 : 0) + N * 2 * G * 32 * tsz;
+// (slot_bytes: 4 int32, 8 fp64, 2 packed 16-bit -- every node has 2G slots, G of them +inf)
+// Packed layouts read one row past a node's slots (the unused partner word when g is even):
+// a trailing pad row keeps the last node's read inside the warp's region.
+__host__ __device__ inline int cand_warp_bytes(int J, int N, int G, int slot_bytes, bool index_src) {
+    return J * 128 + (index_src ? J * 64 : 0) + N * 2 * G * 32 * slot_bytes + (slot_bytes == 2 ? 128 : 0);
 }
 
 // Layouts of the free-time state (template parameter L)
 constexpr int kLayoutOne = 0;     // one node, 32-bit (or fp64) slots
 constexpr int kLayoutMulti = 1;   // several nodes, node chosen per placement
 constexpr int kLayoutOne16 = 2;   // one node, two 16-bit slots per word (grid time < 2^16)
+constexpr int kLayoutMulti16 = 3; // several nodes, 16-bit slots, records carry durations
+
+template <typename T, int L>
+__host__ __device__ constexpr int cand_slot_bytes() {
+    return (L == kLayoutOne16 || L == kLayoutMulti16) ? 2 : (int)sizeof(T);
+}
 
 template <typename T, int SRC, int G, int L>
 __global__ void __launch_bounds__(kCandThreads)
 k_cand(CandArgs a) {
     constexpr bool MULTI = L == kLayoutMulti;
     constexpr bool P16 = L == kLayoutOne16;
+    constexpr bool M16 = L == kLayoutMulti16;
+    constexpr int NMAX = (MULTI || M16) ? (32 / G) : 1;     // nodes x padded GPUs fit a warp
     extern __shared__ __align__(16) uint8_t smem[];
     {
         const int nwords = (*reinterpret_cast<const BlobHeader *>(a.blob)).bytes / 16;
@@ -64,7 +75,7 @@ k_cand(CandArgs a) {
     __syncthreads();
     const BlobHeader &h = *reinterpret_cast<const BlobHeader *>(smem);
     const int J = h.J;
-    const int N = MULTI ? h.N : 1;
+    const int N = (MULTI || M16) ? h.N : 1;
     GenTables tb;
     load_tables(tb, smem, h);
     const T *dur = reinterpret_cast<const T *>(smem + h.off_dur);
@@ -75,7 +86,7 @@ k_cand(CandArgs a) {
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr bool kIndex = SRC == SAT_SRC_INDEX;
-    uint8_t *wbase = smem + h.bytes + warp * cand_warp_bytes(J, N, G, (int)sizeof(T), kIndex);
+    uint8_t *wbase = smem + h.bytes + warp * cand_warp_bytes(J, N, G, cand_slot_bytes<T, L>(), kIndex);
     uint32_t *rec = reinterpret_cast<uint32_t *>(wbase) + lane;          // [J][32]
     uint8_t *opt = wbase + J * 128 + lane;                               // [J][32] (index source)
     uint8_t *ord = opt + J * 32;                                         // [J][32]
@@ -83,9 +94,10 @@ k_cand(CandArgs a) {
     uint32_t *st16 = reinterpret_cast<uint32_t *>(st);                               // [G][32] words
 
     const T INF = TimeTraits<T>::inf();
-    if constexpr (P16) {
+    if constexpr (P16 || M16) {
+        for (int n = 0; n < N; ++n)
 #pragma unroll
-        for (int w = G / 2; w < G; ++w) st16[w * 32] = 0xffffffffu;
+            for (int w = G / 2; w < G; ++w) st16[(n * G + w) * 32] = 0xffffffffu;
     } else {
         for (int n = 0; n < N; ++n)
 #pragma unroll
@@ -127,7 +139,6 @@ k_cand(CandArgs a) {
                 // Shift by the thread's g: word k of the shifted vector is word g/2 + k (g even)
                 // or the high half of word g/2 + k joined to the low half of the next (g odd):
                 // one PRMT with a per-thread selector either way.
-                const uint16_t *st_h = reinterpret_cast<const uint16_t *>(st16);
                 uint32_t av[G / 2];
 #pragma unroll
                 for (int w = 0; w < G / 2; ++w) {
@@ -138,7 +149,9 @@ k_cand(CandArgs a) {
                     const uint32_t r = rec[kk * 32];
                     const int g = (int)(r & 63u) + 1;
                     const int gm = g - 1;
-                    int32_t t = (int32_t)st_h[((gm >> 1) * 32) * 2 + (gm & 1)];
+                    // slot g-1 = one half of word (g-1)/2 (read as the word: no type-punned loads)
+                    const uint32_t selt = 0x4410u + (uint32_t)(gm & 1) * 0x22u;
+                    int32_t t = (int32_t)__byte_perm(st16[(gm >> 1) * 32], 0u, selt);
                     if (has_release) t = max(t, (int32_t)release[(r >> 6) & 63u]);
                     const int32_t e = t + (int32_t)(r >> 12);
                     const uint32_t e2 = (uint32_t)e * 0x10001u;
@@ -155,7 +168,7 @@ k_cand(CandArgs a) {
                     }
                     mx = tmax(mx, (T)e);
                 }
-            } else if constexpr (!MULTI) {
+            } else if constexpr (L == kLayoutOne) {
                 T av[G];
 #pragma unroll
                 for (int i = 0; i < G; ++i) {
@@ -179,32 +192,78 @@ k_cand(CandArgs a) {
                     }
                     mx = tmax(mx, e);
                 }
-            } else {
-                for (int n = 0; n < N; ++n)
+            } else if constexpr (M16) {
+                // per node n: words n*G .. n*G+G/2-1 = slots, n*G+G/2 .. n*G+G-1 = +inf.  Node pick:
+                // min over nodes of (start << 5 | n) = earliest start, lowest node on ties
+                // (durations are node-independent in this layout, so earliest start = earliest end).
 #pragma unroll
-                    for (int i = 0; i < G; ++i) st[(n * 2 * G + i) * 32] = lane_init[n * G + i];
+                for (int n = 0; n < NMAX; ++n)
+                    if (n < N)
+#pragma unroll
+                        for (int w = 0; w < G / 2; ++w)
+                            st16[(n * G + w) * 32] = (uint32_t)(uint16_t)lane_init[n * G + 2 * w] |
+                                                     ((uint32_t)(uint16_t)lane_init[n * G + 2 * w + 1] << 16);
+                for (int kk = 0; kk < J; ++kk) {
+                    const uint32_t r = rec[kk * 32];
+                    const int g = (int)(r & 63u) + 1;
+                    const int gm = g - 1;
+                    const int32_t rel = has_release ? (int32_t)release[(r >> 6) & 63u] : 0;
+                    const uint32_t selt = 0x4410u + (uint32_t)(gm & 1) * 0x22u;
+                    uint32_t kb = 0xffffffffu;
+#pragma unroll
+                    for (int n = 0; n < NMAX; ++n) {
+                        if (n < N) {
+                            int32_t t = (int32_t)__byte_perm(st16[(n * G + (gm >> 1)) * 32], 0u, selt);
+                            t = max(t, rel);
+                            kb = min(kb, (uint32_t)t * 32u + (uint32_t)n);
+                        }
+                    }
+                    const int bn = (int)(kb & 31u);
+                    const int32_t e = (int32_t)(kb >> 5) + (int32_t)(r >> 12);
+                    const uint32_t e2 = (uint32_t)e * 0x10001u;
+                    const uint32_t sel = (g & 1) ? 0x5432u : 0x3210u;
+                    uint32_t *nb = st16 + bn * G * 32;
+                    const uint32_t *src = nb + (g >> 1) * 32;
+                    uint32_t w[G / 2 + 1], cur[G / 2];
+#pragma unroll
+                    for (int k = 0; k <= G / 2; ++k) w[k] = src[k * 32];
+#pragma unroll
+                    for (int k = 0; k < G / 2; ++k) cur[k] = nb[k * 32];
+#pragma unroll
+                    for (int k = 0; k < G / 2; ++k)
+                        nb[k * 32] = __vmaxu2(cur[k], __vminu2(__byte_perm(w[k], w[k + 1], sel), e2));
+                    mx = tmax(mx, (T)e);
+                }
+            } else {
+#pragma unroll
+                for (int n = 0; n < NMAX; ++n)
+                    if (n < N)
+#pragma unroll
+                        for (int i = 0; i < G; ++i) st[(n * 2 * G + i) * 32] = lane_init[n * G + i];
                 for (int kk = 0; kk < J; ++kk) {
                     const uint32_t r = rec[kk * 32];
                     const int g = (int)(r & 63u) + 1;
                     const uint32_t pay = r >> 12;
                     const T rel = has_release ? release[(r >> 6) & 63u] : (T)0;
                     // node finishing the job earliest, lowest node on ties
-                    T be = INF, bt = INF;
+                    T be = INF;
                     int bn = 0;
-                    for (int n = 0; n < N; ++n) {
-                        T t = st[(n * 2 * G + g - 1) * 32];
-                        T d;
-                        if (rec_d) {
-                            d = (T)(int32_t)pay;
-                        } else {
-                            if (!((tb.optmask[pay] >> n) & 1u)) t = INF;
-                            d = dur[pay * N + n];
+#pragma unroll
+                    for (int n = 0; n < NMAX; ++n) {
+                        if (n < N) {
+                            T t = st[(n * 2 * G + g - 1) * 32];
+                            T d;
+                            if (rec_d) {
+                                d = (T)(int32_t)pay;
+                            } else {
+                                if (!((tb.optmask[pay] >> n) & 1u)) t = INF;
+                                d = dur[pay * N + n];
+                            }
+                            t = tmax(t, rel);
+                            const T e = t + d;
+                            if (n == 0 || e < be) { be = e; bn = n; }
                         }
-                        t = tmax(t, rel);
-                        const T e = t + d;
-                        if (n == 0 || e < be) { be = e; bt = t; bn = n; }
                     }
-                    (void)bt;
                     T *sb = st + bn * 2 * G * 32;
                     T cur[G], s[G];
 #pragma unroll
