@@ -1,10 +1,12 @@
 """Plan-search benchmark: candidate plans evaluated / s and wall-time to the best plan.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1|3|4|5] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1|2|3|4|5] [--impl ours|reference]
 
 A step = one complete solve of the configured workload (config 1: the exhaustive
-search of all 3.25e10 candidates of the paper workload; sampled configs: a fixed
-candidate budget), sharded over the ranks, combined with an NCCL all-reduce MIN.
+search of all 3.25e10 candidates of the paper workload; config 2: every solve of
+one introspection run of it -- the initial solve plus the re-solve at each tick;
+sampled configs: a fixed candidate budget), sharded over the ranks, combined with
+an NCCL all-reduce MIN.
 Rank 0 prints one JSON line.  `--impl reference` times the CPU oracle port
 (oracle/oracle.c, OpenMP on every host thread) on a bounded sample of the same
 workload -- the reference's own solver does not exist.
@@ -33,7 +35,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=1, choices=[1, 3, 4, 5])
+    ap.add_argument("--config", type=int, default=1, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--budget", type=int, default=0, help="sampled configs: candidates per step")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=8.0, help="CPU baseline sample length")
@@ -94,7 +96,7 @@ def workload(cfg: int, budget: int):
     from paper_2311_02840_b200.workloads import CONFIGS, config_workload
 
     w, t, c = config_workload(cfg)
-    if cfg == 1:
+    if cfg in (1, 2):
         opts = SolveOptions()                                   # exhaustive, tree kernel
     else:
         default = {3: 1 << 27, 4: 1 << 26, 5: 1 << 26}[cfg]
@@ -188,7 +190,7 @@ def run_reference(args):
     op = saturn_oracle.build(t.entries, w)
     cp = coracle.CProblem(op)
     threads = os.cpu_count() or 1
-    src = "index" if args.config == 1 else "substream"
+    src = "index" if args.config in (1, 2) else "substream"
     # calibrate a per-step sample of ~`per_step` seconds so K+W steps finish in minutes
     per_step = min(15.0, 150.0 / max(1, args.steps + args.warmup))
     n = 20000
@@ -241,8 +243,72 @@ def ncu_traffic(kernel: str, cfg: int):
 
 
 # ----------------------------------------------------------------------------- ours
+class DeviceSolve:
+    """One search of a step, marshalled once (launch parameters resident), sharded over ranks."""
+
+    def __init__(self, eng, prob, opts, rank, world):
+        from paper_2311_02840_b200 import engine as EN
+
+        self.EN, self.eng, self.prob, self.opts, self.world = EN, eng, prob, opts, world
+        self.mode, n_idx = eng.plan_search(prob, opts)
+        self.idx_bits, _ = prob.key_bits(n_idx)
+        self.nprob = EN.NativeProblem(prob, self.idx_bits)
+        self.use_tree = self.mode == "exhaustive" and eng._tree_ok(prob)
+        G, N, J = prob.G, prob.N, prob.J
+        if self.use_tree:
+            self.info = eng.tree_plan(self.nprob)
+            self.a, self.b = EN._shard(self.info.n_tasks, rank, world)
+            self.n_cand = self.info.n_candidates
+            merges = self.info.n_job_steps - self.info.n_candidates
+            # algorithmic INT32 work of the prefix-shared walk (DESIGN.md section 4):
+            #   internal placement: node pick (N) + 2G slot min/max + add + makespan max = N + 2G + 2
+            #   leaf placement (last job, no state update): node pick + add + max = N + 2
+            self.ops = (merges // world) * (N + 2 * G + 2) + (self.n_cand // world) * (N + 2)
+            self.kernel = "k_tree"
+        else:
+            self.a, self.b = EN._shard(n_idx, rank, world)
+            self.n_cand = n_idx
+            self.ops = (n_idx // world) * J * (N + 2 * G + 2)
+            self.kernel = "k_cand"
+        self.best = eng.reset_best(eng.torch.empty(2, dtype=eng.torch.int64, device=eng.device))
+
+    def launch(self):
+        EN, eng = self.EN, self.eng
+        eng.reset_best(self.best)
+        if self.use_tree:
+            eng.search_tree(self.nprob, self.info.prefix_len, self.a, self.b, self.best)
+        elif self.mode == "exhaustive":
+            eng.search_index(self.nprob, self.a, self.b, self.best)
+        else:
+            eng.search_sampled(self.nprob, EN.SRC_SUBSTREAM, self.opts.seed, self.a, self.b, self.best)
+
+    def combine(self, group):
+        return self.EN._combine(self.best, self.nprob.grid, group, self.world)
+
+
+def introspection_run(t, w, opts, group=None, record=None):
+    """Config 2: plan_saturn, then execute with a re-solve every R = predicted/10 and rho = 30 s
+     -- the public API end to end.  Returns (report, candidates evaluated)."""
+    from paper_2311_02840_b200 import planners
+    from paper_2311_02840_b200 import simulator as SIM
+
+    evaluated = [0]
+
+    def replan(table, workload, ctx):
+        sol = planners.solve(table, workload, None, opts, ctx, group=group)
+        evaluated[0] += sol.search.evaluated
+        if record is not None:
+            record.append(ctx)
+        return sol.plan
+
+    sol0 = planners.solve(t, w, None, opts, group=group)
+    evaluated[0] += sol0.search.evaluated
+    rep = SIM.simulate(w, t, sol0.plan, SIM.SimOptions(introspection_interval=sol0.plan.predicted_makespan / 10,
+                                                       checkpoint_overhead=30.0, replanner=replan))
+    return rep, evaluated[0]
+
+
 def run_ours(args):
-    import numpy as np
     import torch
 
     from paper_2311_02840_b200 import engine as EN
@@ -253,38 +319,24 @@ def run_ours(args):
     group = None
     w, t, c, opts = workload(args.config, args.budget)
     eng = planners.get_engine(local)
-    prob = build_problem(t, w, opts)
-    mode, n_idx = eng.plan_search(prob, opts)
-    idx_bits, _ = prob.key_bits(n_idx)
-    nprob = EN.NativeProblem(prob, idx_bits)
-    use_tree = mode == "exhaustive" and eng._tree_ok(prob)
-    if use_tree:
-        info = eng.tree_plan(nprob)
-        a, b = EN._shard(info.n_tasks, rank, world)
-        n_cand = info.n_candidates
-        leaves = info.n_candidates
-        merges = info.n_job_steps - info.n_candidates
-        kernel_name = "k_tree"
+    report = None
+    if args.config == 2:
+        ctxs = []
+        report, _ = introspection_run(t, w, opts, group, record=ctxs)
+        problems = [build_problem(t, w, opts)] + [build_problem(t, w, opts, ctx) for ctx in ctxs]
     else:
-        a, b = EN._shard(n_idx, rank, world)
-        n_cand = n_idx
-        kernel_name = "k_generic"
+        problems = [build_problem(t, w, opts)]
+    solves = [DeviceSolve(eng, p, opts, rank, world) for p in problems]
+    head = solves[0]
+    n_cand = sum(s.n_cand for s in solves)
     stream = torch.cuda.current_stream()
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device="cuda")
-    best = eng.reset_best()
-
-    def device_step():
-        eng.reset_best(best)
-        if use_tree:
-            eng.search_tree(nprob, info.prefix_len, a, b, best)
-        elif mode == "exhaustive":
-            eng.search_index(nprob, a, b, best)
-        else:
-            eng.search_sampled(nprob, EN.SRC_SUBSTREAM, opts.seed, a, b, best)
 
     for _ in range(args.warmup):
-        device_step()
-        EN._combine(best, nprob.grid, group, world)
+        for s in solves:
+            s.launch()
+        for s in solves:
+            s.combine(group)
     torch.cuda.synchronize()
 
     # ---- device-resident timed region: K steps, L2 flushed between steps ----
@@ -299,35 +351,44 @@ def run_ours(args):
             flush.zero_()
             e0, e1, e2 = ev[i]
             e0.record(stream)
-            device_step()
+            for s in solves:
+                s.launch()
             e1.record(stream)
-            keys.append(EN._combine(best, nprob.grid, group, world))
+            keys.append([s.combine(group) for s in solves])
             e2.record(stream)
         torch.cuda.synchronize()
     barrier(world)
     launches = eng.launches - launches0
     step_s = [e0.elapsed_time(e2) / 1e3 for e0, _, e2 in ev]
     kern_s = [e0.elapsed_time(e1) / 1e3 for e0, e1, _ in ev]
-    t_local = sum(step_s)
-    t_max = max_over_ranks(t_local, world)
+    t_max = max_over_ranks(sum(step_s), world)
     kern_avg = max_over_ranks(sum(kern_s) / len(kern_s), world)
     value = n_cand * args.steps / t_max
-    key = keys[-1]
-    assert all(k == key for k in keys), "non-deterministic search result"
-    ms = key[0] >> idx_bits if nprob.grid else None
+    key = keys[-1][0]
+    assert all(k == keys[-1] for k in keys), "non-deterministic search result"
+    idx_bits = head.idx_bits
+    ms = key[0] >> idx_bits if head.nprob.grid else None
 
     # ---- e2e: the public API with host inputs (marshal, launch, NCCL, decode, check) ----
     e2e_times = []
+    e2e_cand = n_cand
     barrier(world)
     for i in range(max(2, min(args.steps, 5))):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        sol = planners.solve(t, w, None, opts, group=group)
+        if args.config == 2:
+            _, e2e_cand = introspection_run(t, w, opts, group)
+            api = "planners.solve (plan_saturn) + simulator.simulate with engine re-solves (resolve)"
+        else:
+            planners.solve(t, w, None, opts, group=group)
+            api = "paper_2311_02840_b200.planners.solve (plan_saturn)"
         torch.cuda.synchronize()
         e2e_times.append(time.perf_counter() - t0)
     e2e_s = max_over_ranks(statistics.median(e2e_times[1:]), world)
-    h2d = nprob.param_bytes + 8                    # tables packed into the launch + decode id
-    d2h = 16 + 3 * 4 * prob.J + 8                  # best key + winner schedule (option, node, start) + makespan
+    # per solve: tables packed into the launch + decode id in; best key + winner schedule
+    # (option, node, start per job) + makespan out
+    h2d = sum(s.nprob.param_bytes + 8 for s in solves)
+    d2h = sum(16 + 3 * 4 * s.prob.J + 8 for s in solves)
 
     # ---- roofline: INT32 min/max issue rate measured on this GPU ----
     ops = torch.zeros(1, dtype=torch.int64, device="cuda")
@@ -343,32 +404,27 @@ def run_ours(args):
     p1.record(stream)
     torch.cuda.synchronize()
     peak_ops = int(ops.item()) / (p0.elapsed_time(p1) / 1e3)
-    G, N = prob.G, prob.N
-    if use_tree:
-        # algorithmic INT32 work of the prefix-shared walk:
-        #   internal placement: node pick (N) + 2G slot min/max + add + makespan max = N + 2G + 2
-        #   leaf placement (last job, no state update): node pick + add + max = N + 2
-        per_launch_ops = (merges // world) * (N + 2 * G + 2) + (leaves // world) * (N + 2)
-    else:
-        per_launch_ops = (n_cand // world) * prob.J * (N + 2 * G + 2)
+    per_launch_ops = sum(s.ops for s in solves)
     achieved = per_launch_ops / kern_avg
-    traffic, traffic_src = ncu_traffic(kernel_name, args.config)
+    kernel_name = head.kernel
+    traffic, traffic_src = ncu_traffic(kernel_name, 1 if args.config == 2 else args.config)
+    prob = head.prob
 
     line = {
         "metric": "candidate plans evaluated/sec", "value": value, "unit": "plans/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps,
-        "higher_is_better": True, "scaling": "strong" if args.config == 1 else "strong",
-        "vs_baseline": None, "dtype": "int32" if nprob.grid else "f64", "data": "synthetic",
+        "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "int32" if head.nprob.grid else "f64", "data": "synthetic",
         "config": {"workload": c["name"], "jobs": prob.J, "nodes": prob.N, "gpus_per_node": int(prob.node_gpus[0]),
-                   "search": mode, "candidates_per_step": n_cand, "kernel": kernel_name,
-                   "radix": [int(r) for r in prob.radix], "delta_s": prob.delta,
+                   "search": head.mode, "candidates_per_step": n_cand, "solves_per_step": len(solves),
+                   "kernel": kernel_name, "radix": [int(r) for r in prob.radix], "delta_s": prob.delta,
                    "l2": "256 MiB flush between steps, outside step events; working set = launch params",
                    "parallelism": f"candidate-space shards x{world}, NCCL all-reduce MIN"},
-        "best": {"makespan_intervals": ms, "index": key[0] & ((1 << idx_bits) - 1) if nprob.grid else key[1],
+        "best": {"makespan_intervals": ms, "index": key[0] & ((1 << idx_bits) - 1) if head.nprob.grid else key[1],
                  "predicted_makespan_s": (ms * prob.delta) if ms is not None else None},
-        "time_to_best_s": t_max / args.steps,
-        "e2e": {"value": n_cand / e2e_s, "unit": "plans/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "solve_wall_s": e2e_s, "api": "paper_2311_02840_b200.planners.solve (plan_saturn)"},
+        "time_to_best_s": t_max / args.steps / len(solves),
+        "e2e": {"value": e2e_cand / e2e_s, "unit": "plans/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "solve_wall_s": e2e_s, "api": api},
         "gpu_launches": launches,
         "kernel_ms": 1e3 * kern_avg,
         "roofline": {"bound": "int32-alu", "achieved": achieved / 1e12, "peak": peak_ops / 1e12, "unit": "TOP/s",
@@ -378,12 +434,16 @@ def run_ours(args):
                      "algorithmic_ops_per_launch": per_launch_ops},
         "clocks": clk.summary(),
     }
-    if use_tree:
-        line["config"]["prefix_len"] = info.prefix_len
-        line["config"]["walk_placements"] = info.n_job_steps
+    if head.use_tree:
+        line["config"]["prefix_len"] = head.info.prefix_len
+        line["config"]["walk_placements"] = head.info.n_job_steps
+    if report is not None:
+        line["introspection"] = {"makespan_s": report.makespan, "replans": report.replan_count,
+                                 "checkpoints": report.checkpoint_count,
+                                 "candidates_per_solve": [s.n_cand for s in solves]}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(args.config, args.cpu_seconds, w, t, opts)
-        line["cpu_baseline_python"] = python_baseline(args.config, w, t, opts)
+        line["cpu_baseline"] = cpu_baseline(1 if args.config == 2 else args.config, args.cpu_seconds, w, t, opts)
+        line["cpu_baseline_python"] = python_baseline(1 if args.config == 2 else args.config, w, t, opts)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

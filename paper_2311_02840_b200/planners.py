@@ -157,8 +157,9 @@ def plan_saturn(table, jobs, cluster=None, delta_opts=None, running_context=None
 def resolve(table, workload, running_context, delta_opts=None, *, group=None, device=None):
     """Introspection re-solve: all unfinished jobs re-planned from now
     (start times relative to the tick); a running job pays rho on any option whose
-    (technique, g, node) differs from what it holds."""
-    return solve(table, workload, None, delta_opts, running_context, group=group, device=device)
+    (technique, g, node) differs from what it holds.  Returns the Plan (use ``solve`` for the
+    full Solution)."""
+    return solve(table, workload, None, delta_opts, running_context, group=group, device=device).plan
 
 
 # --------------------------------------------------------------------------
