@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define SAT_ABI_VERSION 1
+#define SAT_ABI_VERSION 2
 
 /* status codes (mapped to reference errors.py classes by the host layer) */
 #define SAT_OK              0
@@ -119,11 +119,14 @@ int sat_search_sampled(const sat_problem_t *p, int32_t source, uint64_t seed,
 
 /* Prefix-shared exhaustive search (single node, grid mode, no release times).
  * sat_tree_plan fills *info for a prefix length (0 = engine's choice);
- * sat_search_tree walks warp tasks [task_lo, task_hi) of that layout. */
+ * sat_search_tree walks warp tasks [task_lo, task_hi) of that layout; warps take
+ * tasks from a cursor kept in the workspace (>= SAT_TREE_WS_BYTES, device memory;
+ * the same workspace as the other searches is fine). */
+#define SAT_TREE_WS_BYTES 256
 int sat_tree_plan(const sat_problem_t *p, int32_t prefix_len, sat_tree_info_t *info);
 int sat_search_tree(const sat_problem_t *p, int32_t prefix_len,
                     uint64_t task_lo, uint64_t task_hi,
-                    sat_best_t *d_best, void *stream);
+                    sat_best_t *d_best, void *d_ws, size_t ws_bytes, void *stream);
 
 /* Schedule n candidates and record the plan of each.
  *   source SAT_SRC_INDEX/SUBSTREAM/SEED: d_ids[n] candidate ids (seed used by streams)

@@ -76,6 +76,7 @@ struct TreeParams {
     uint64_t set_prod[kTreeMaxSets];     // prod of radix over the set
     uint64_t task_lo, task_hi;
     sat_best_t *best;
+    unsigned long long *cursor;       // tasks handed out so far (zeroed before the launch)
 };
 
 // Per-lane running best (makespan, index).

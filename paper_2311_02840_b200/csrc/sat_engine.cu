@@ -661,10 +661,11 @@ int sat_tree_plan(const sat_problem_t *p, int32_t prefix_len, sat_tree_info_t *i
 }
 
 int sat_search_tree(const sat_problem_t *p, int32_t prefix_len, uint64_t task_lo, uint64_t task_hi,
-                    sat_best_t *d_best, void *stream) {
+                    sat_best_t *d_best, void *d_ws, size_t ws_bytes, void *stream) {
     int st = validate(p);
     if (st) return st;
     if (!d_best || task_hi < task_lo) return SAT_ERR_INVALID;
+    if (!d_ws || ws_bytes < SAT_TREE_WS_BYTES) return SAT_ERR_INVALID;
     TreeLayout lay;
     st = tree_layout(p, prefix_len, lay);
     if (st) return st;
@@ -714,7 +715,9 @@ int sat_search_tree(const sat_problem_t *p, int32_t prefix_len, uint64_t task_lo
     tp.set_cum[lay.sets.size()] = lay.cum.back();
     tp.task_lo = task_lo; tp.task_hi = task_hi;
     tp.best = d_best;
+    tp.cursor = static_cast<unsigned long long *>(d_ws);
     cudaStream_t s = (cudaStream_t)stream;
+    if (cudaMemsetAsync(d_ws, 0, sizeof(unsigned long long), s) != cudaSuccess) return SAT_ERR_CUDA;
     // the walk is specialised on the node's exact GPU count (no ghost slots)
     switch (tp.Gr) {
 #define SAT_G(K) case K: return launch_tree_g<K>(tp, tp.Q, s);

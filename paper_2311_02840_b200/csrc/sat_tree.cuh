@@ -151,11 +151,16 @@ k_tree(const __grid_constant__ TreeParams p) {
         for (int i = G; i < 2 * G; ++i) wbase[L * col_words + i * 32 + lane] = SAT_INF_I32;
 
     LaneBest lb{SAT_INF_I32, ~0ull};
-    const uint64_t gwarp = (uint64_t)blockIdx.x * kTreeWarps + warp;
-    const uint64_t nwarps = (uint64_t)gridDim.x * kTreeWarps;
     const uint32_t all = (J >= 32) ? 0xffffffffu : ((1u << J) - 1u);
 
-    for (uint64_t t = p.task_lo + gwarp; t < p.task_hi; t += nwarps) {
+    // dynamic task cursor: a warp takes the next task when it finishes one (task costs
+    // differ by the remaining jobs' radices; a static split leaves a long tail)
+    auto next_task = [&]() -> uint64_t {
+        unsigned long long v = 0;
+        if (lane == 0) v = atomicAdd(p.cursor, 1ull);
+        return p.task_lo + __shfl_sync(0xffffffffu, v, 0);
+    };
+    for (uint64_t t = next_task(); t < p.task_hi; t = next_task()) {
         // ---- which prefix set (warp-uniform binary search) ----
         int lo = 0, hi = p.n_sets - 1;
         while (lo < hi) {

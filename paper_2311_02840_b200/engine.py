@@ -56,7 +56,7 @@ _SIGS = {
     "sat_search_index": ([_vp, _u64, _u64, _vp, _vp, ctypes.c_size_t, _vp], _i32),
     "sat_search_sampled": ([_vp, _i32, _u64, _u64, _u64, _vp, _vp, ctypes.c_size_t, _vp], _i32),
     "sat_tree_plan": ([_vp, _i32, _vp], _i32),
-    "sat_search_tree": ([_vp, _i32, _u64, _u64, _vp, _vp], _i32),
+    "sat_search_tree": ([_vp, _i32, _u64, _u64, _vp, _vp, ctypes.c_size_t, _vp], _i32),
     "sat_schedule": ([_vp, _i32, _u64, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                       ctypes.c_size_t, _vp], _i32),
     "sat_alu_probe": ([_i32, _i32, _i32, _vp, _vp, _vp], _i32),
@@ -78,7 +78,7 @@ def load_library(path: str = LIB_PATH):
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res
-    if lib.sat_abi_version() != 1:
+    if lib.sat_abi_version() != 2:
         raise E.PlanFailure("libsaturn_b200.so ABI version mismatch")
     _LIB = lib
     return lib
@@ -202,8 +202,9 @@ class Engine:
 
     def search_tree(self, nprob, prefix_len, task_lo, task_hi, best=None):
         best = self._best if best is None else best
-        self._check(self.lib.sat_search_tree(nprob.ref, prefix_len, task_lo, task_hi,
-                                             _vp(best.data_ptr()), _vp(self.stream())), what="sat_search_tree")
+        ws, wsb = self.workspace(nprob)
+        self._check(self.lib.sat_search_tree(nprob.ref, prefix_len, task_lo, task_hi, _vp(best.data_ptr()),
+                                             _vp(ws), wsb, _vp(self.stream())), what="sat_search_tree")
         self.launches += 1
 
     def search_index(self, nprob, lo, hi, best=None):
