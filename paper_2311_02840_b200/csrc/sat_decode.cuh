@@ -38,9 +38,8 @@ __device__ inline uint64_t mod_small(uint64_t r, uint32_t n, uint64_t magic) {
 // low word and needs at most one conditional subtract.
 __device__ __forceinline__ uint32_t mod_small_fast(uint64_t r, uint32_t n, uint64_t magic) {
     const uint64_t q = __umul64hi(r, magic);
-    uint32_t rem = (uint32_t)r - (uint32_t)q * n;
-    rem = rem >= n ? rem - n : rem;
-    return rem;
+    const uint32_t rem = (uint32_t)r - (uint32_t)q * n;
+    return min(rem, rem - n);          // rem - n wraps above rem exactly when rem < n
 }
 
 // SplitMix64 stream with a draw counter: k-th output = mix64(state0 + k*GOLDEN)
