@@ -128,6 +128,18 @@ int sat_search_tree(const sat_problem_t *p, int32_t prefix_len,
                     uint64_t task_lo, uint64_t task_hi,
                     sat_best_t *d_best, void *d_ws, size_t ws_bytes, void *stream);
 
+/* Bound-and-prune over the same layout (replaces branch_and_bound):
+ * subtrees whose makespan lower bound exceeds the best makespan found so far are
+ * skipped; every candidate that could tie or beat the best is still scheduled, so the
+ * key equals sat_search_tree's.  *d_best may be seeded with an upper bound key
+ * (makespan << idx_bits | (2^idx_bits - 1)) from any known candidate.  Counters are
+ * left in the workspace as uint64 words after the task cursor (index 1 + SAT_BNB_STAT_*). */
+#define SAT_BNB_STAT_PRUNED_TASKS 0   /* warp tasks cut at the prefix          */
+#define SAT_BNB_STAT_PAIR_NODES   1   /* two-job subtrees scheduled (per warp)  */
+int sat_search_bnb(const sat_problem_t *p, int32_t prefix_len,
+                   uint64_t task_lo, uint64_t task_hi,
+                   sat_best_t *d_best, void *d_ws, size_t ws_bytes, void *stream);
+
 /* Schedule n candidates and record the plan of each.
  *   source SAT_SRC_INDEX/SUBSTREAM/SEED: d_ids[n] candidate ids (seed used by streams)
  *   source SAT_SRC_EXPLICIT: d_explicit[n][2*J] = option digit per job, then order

@@ -74,9 +74,11 @@ struct TreeParams {
     uint32_t set_mask[kTreeMaxSets];
     uint64_t set_cum[kTreeMaxSets + 1];  // cumulative warp tasks
     uint64_t set_prod[kTreeMaxSets];     // prod of radix over the set
+    int32_t minarea[kTreeMaxJ];       // per job: least g * d over its options (bound-and-prune)
     uint64_t task_lo, task_hi;
     sat_best_t *best;
     unsigned long long *cursor;       // tasks handed out so far (zeroed before the launch)
+    unsigned long long *stats;        // bound-and-prune counters (SAT_BNB_STAT_*), or null
 };
 
 // Per-lane running best (makespan, index).
@@ -86,6 +88,6 @@ struct LaneBest {
 };
 
 template <int G>
-int launch_tree_g(const TreeParams &tp, int Q, cudaStream_t stream);   // sat_tree.cuh
+int launch_tree_g(const TreeParams &tp, int Q, bool bnb, cudaStream_t stream);   // sat_tree.cuh
 
 }  // namespace sat

@@ -660,8 +660,8 @@ int sat_tree_plan(const sat_problem_t *p, int32_t prefix_len, sat_tree_info_t *i
     return SAT_OK;
 }
 
-int sat_search_tree(const sat_problem_t *p, int32_t prefix_len, uint64_t task_lo, uint64_t task_hi,
-                    sat_best_t *d_best, void *d_ws, size_t ws_bytes, void *stream) {
+static int search_tree_impl(const sat_problem_t *p, int32_t prefix_len, uint64_t task_lo, uint64_t task_hi,
+                            sat_best_t *d_best, void *d_ws, size_t ws_bytes, void *stream, bool bnb) {
     int st = validate(p);
     if (st) return st;
     if (!d_best || task_hi < task_lo) return SAT_ERR_INVALID;
@@ -716,11 +716,18 @@ int sat_search_tree(const sat_problem_t *p, int32_t prefix_len, uint64_t task_lo
     tp.task_lo = task_lo; tp.task_hi = task_hi;
     tp.best = d_best;
     tp.cursor = static_cast<unsigned long long *>(d_ws);
+    tp.stats = tp.cursor + 1;
+    for (int j = 0; j < J; ++j) {
+        int32_t a = SAT_INF_I32;
+        for (int o = 0; o < p->radix[j]; ++o)
+            a = std::min<int64_t>(a, (int64_t)p->gpus[j * p->Cmax + o] * p->dur_i32[j * p->Cmax + o]);
+        tp.minarea[j] = a;
+    }
     cudaStream_t s = (cudaStream_t)stream;
-    if (cudaMemsetAsync(d_ws, 0, sizeof(unsigned long long), s) != cudaSuccess) return SAT_ERR_CUDA;
+    if (cudaMemsetAsync(d_ws, 0, 3 * sizeof(unsigned long long), s) != cudaSuccess) return SAT_ERR_CUDA;
     // the walk is specialised on the node's exact GPU count (no ghost slots)
     switch (tp.Gr) {
-#define SAT_G(K) case K: return launch_tree_g<K>(tp, tp.Q, s);
+#define SAT_G(K) case K: return launch_tree_g<K>(tp, tp.Q, bnb, s);
         SAT_G(1) SAT_G(2) SAT_G(3) SAT_G(4) SAT_G(5) SAT_G(6) SAT_G(7) SAT_G(8)
         SAT_G(9) SAT_G(10) SAT_G(11) SAT_G(12) SAT_G(13) SAT_G(14) SAT_G(15) SAT_G(16)
         SAT_G(17) SAT_G(18) SAT_G(19) SAT_G(20) SAT_G(21) SAT_G(22) SAT_G(23) SAT_G(24)
@@ -728,6 +735,16 @@ int sat_search_tree(const sat_problem_t *p, int32_t prefix_len, uint64_t task_lo
 #undef SAT_G
         default: return SAT_ERR_UNSUPPORTED;
     }
+}
+
+int sat_search_tree(const sat_problem_t *p, int32_t prefix_len, uint64_t task_lo, uint64_t task_hi,
+                    sat_best_t *d_best, void *d_ws, size_t ws_bytes, void *stream) {
+    return search_tree_impl(p, prefix_len, task_lo, task_hi, d_best, d_ws, ws_bytes, stream, false);
+}
+
+int sat_search_bnb(const sat_problem_t *p, int32_t prefix_len, uint64_t task_lo, uint64_t task_hi,
+                   sat_best_t *d_best, void *d_ws, size_t ws_bytes, void *stream) {
+    return search_tree_impl(p, prefix_len, task_lo, task_hi, d_best, d_ws, ws_bytes, stream, true);
 }
 
 int sat_alu_probe(int32_t blocks, int32_t threads, int32_t iters, uint64_t *d_ops_out, int32_t *d_sink,

@@ -131,8 +131,47 @@ __device__ __forceinline__ void merge_cols(const int32_t *src, int32_t *dst, int
     }
 }
 
-// occupancy target per node size: 12 blocks (40 regs) up to 8 GPUs, fewer for larger nodes
+// Lower bound on the makespan of every completion of a partial schedule (bound-and-prune):
+// the lane's sorted free times `col` (stride 32) after the placed jobs, `rem` unplaced.
+//   - the largest free time already committed;
+//   - each unplaced job j ends no earlier than min over its gangs k of (col[k] + dg[j][k])
+//     (free times only grow, and a g-gang cannot start before the g-th free time);
+//   - area: the GPU time from the free times to the makespan must hold every unplaced
+//     job's least g * d:  M * G >= sum(col) + sum_j minarea_j.
+// Every completion of the prefix has makespan >= the bound, so pruning on bound > best
+// keeps every candidate that could tie or beat the best (the result equals exhaustive).
 template <int G>
+__device__ __forceinline__ int32_t lane_bound(const TreeParams &p, const int32_t *col, const int32_t *sdg,
+                                              uint32_t rem) {
+    int32_t A[G];
+    int32_t area = 0;
+#pragma unroll
+    for (int i = 0; i < G; ++i) {
+        A[i] = col[i * 32];
+        area += A[i];
+    }
+    int32_t lb = A[G - 1];
+    for (uint32_t m = rem; m; m &= m - 1) {
+        const int j = __ffs(m) - 1;
+        area += p.minarea[j];
+        int32_t e = SAT_INF_I32;
+#pragma unroll
+        for (int k = 0; k < G; ++k) e = min(e, A[k] + sdg[j * 32 + k]);
+        lb = max(lb, e);
+    }
+    return max(lb, (area + G - 1) / G);
+}
+
+// best makespan published so far (makespan part of the packed key), +inf if none
+__device__ __forceinline__ int32_t published_ms(const TreeParams &p) {
+    const unsigned long long hi = *reinterpret_cast<volatile unsigned long long *>(&p.best->hi);
+    return hi == ~0ull ? SAT_INF_I32 : (int32_t)(hi >> p.idx_bits);
+}
+
+// occupancy target per node size: 12 blocks (40 regs) up to 8 GPUs, fewer for larger nodes.
+// BNB = bound-and-prune: subtrees whose bound exceeds the best makespan found so far (by
+// any warp: published after every task) are skipped; the key found is the exhaustive one.
+template <int G, bool BNB>
 __global__ void __launch_bounds__(kTreeThreads, G <= 8 ? 12 : (G <= 16 ? 8 : 4))
 k_tree(const __grid_constant__ TreeParams p) {
     extern __shared__ __align__(16) int32_t tsm[];
@@ -152,6 +191,8 @@ k_tree(const __grid_constant__ TreeParams p) {
 
     LaneBest lb{SAT_INF_I32, ~0ull};
     const uint32_t all = (J >= 32) ? 0xffffffffu : ((1u << J) - 1u);
+    unsigned long long published = ~0ull;          // BNB: last key this warp published
+    unsigned long long n_pruned = 0, n_pairs = 0;   // BNB counters (lane 0)
 
     // dynamic task cursor: a warp takes the next task when it finishes one (task costs
     // differ by the remaining jobs' radices; a static split leaves a long tail)
@@ -213,14 +254,26 @@ k_tree(const __grid_constant__ TreeParams p) {
             for (int i = 0; i < G; ++i) L0[i * 32] = max(L0[i * 32], min(L0[(i + g) * 32], e));
         }
         __syncwarp();
+        bool lane_ok = valid;
+        int32_t U = SAT_INF_I32;
+        if constexpr (BNB) {
+            U = min(published_ms(p), lb.ms);
+            lane_ok = valid && lane_bound<G>(p, L0, sdg, unplaced) <= U;
+            if (!__any_sync(0xffffffffu, lane_ok)) {
+                if (lane == 0) ++n_pruned;
+                continue;
+            }
+        }
 
         // ---- warp-uniform walk over the suffix (jobs in `unplaced`) ----
         if (Q == 2) {
-            tree_pair<G>(p, L0, Bbuf, sdg, unplaced, base, valid, lb);
+            if (BNB && lane == 0) ++n_pairs;
+            tree_pair<G>(p, L0, Bbuf, sdg, unplaced, base, lane_ok, lb);
         } else {
             uint32_t rem_st[kTreeMaxJ];
             uint64_t acc_st[kTreeMaxJ];
             int cj[kTreeMaxJ], co[kTreeMaxJ];
+            uint32_t okbits = lane_ok ? 1u : 0u;    // bit L: this lane's level-L node is live
             int L = 0;
             rem_st[0] = unplaced;
             acc_st[0] = base;
@@ -245,18 +298,40 @@ k_tree(const __grid_constant__ TreeParams p) {
                 const uint64_t acc = acc_st[L] +
                     (uint64_t)__popc(rem & ((1u << j) - 1u)) * p.fact[Q - 1 - L] + (uint64_t)o * p.wJ[j];
                 const uint32_t rem2 = rem & ~(1u << j);
+                bool child_ok = (okbits >> L) & 1u;
+                if constexpr (BNB) {
+                    if (__any_sync(0xffffffffu, child_ok)) {
+                        U = min(U, lb.ms);
+                        child_ok = child_ok && lane_bound<G>(p, dst, sdg, rem2) <= U;
+                    }
+                    if (!__any_sync(0xffffffffu, child_ok)) continue;
+                }
                 if (L + 1 == Q - 2) {
-                    tree_pair<G>(p, dst, Bbuf, sdg, rem2, acc, valid, lb);
+                    if (BNB && lane == 0) ++n_pairs;
+                    tree_pair<G>(p, dst, Bbuf, sdg, rem2, acc, child_ok, lb);
                 } else {
                     ++L;
                     rem_st[L] = rem2;
                     acc_st[L] = acc;
                     cj[L] = -1;
                     co[L] = 0;
+                    okbits = (okbits & ((1u << L) - 1u)) | ((child_ok ? 1u : 0u) << L);
                 }
             }
         }
         __syncwarp();
+        if constexpr (BNB) {
+            // publish an improvement right away so every warp prunes against it
+            uint64_t key = (lb.ms < SAT_INF_I32) ? (((uint64_t)(uint32_t)lb.ms << p.idx_bits) | lb.ix) : ~0ull;
+            for (int x = 16; x >= 1; x >>= 1) {
+                const uint64_t o = shfl_u64(key, lane ^ x);
+                key = o < key ? o : key;
+            }
+            if (key < published) {
+                published = key;
+                if (lane == 0) atomicMin(reinterpret_cast<unsigned long long *>(&p.best->hi), (unsigned long long)key);
+            }
+        }
     }
 
     // ---- warp argmin, one atomic per warp ----
@@ -267,14 +342,18 @@ k_tree(const __grid_constant__ TreeParams p) {
     }
     if (lane == 0 && key != ~0ull)
         atomicMin(reinterpret_cast<unsigned long long *>(&p.best->hi), (unsigned long long)key);
+    if (BNB && lane == 0 && p.stats) {
+        atomicAdd(&p.stats[SAT_BNB_STAT_PRUNED_TASKS], n_pruned);
+        atomicAdd(&p.stats[SAT_BNB_STAT_PAIR_NODES], n_pairs);
+    }
 }
 
-template <int G>
-int launch_tree_g(const TreeParams &tp, int Q, cudaStream_t stream) {
+template <int G, bool BNB>
+int launch_tree_k(const TreeParams &tp, int Q, cudaStream_t stream) {
     const int upper = Q - 1;
     const int smem = (kTreeWarps * (upper * 2 * G * 32 + G * 32) + tp.J * 32) * 4;
     if (smem > 200 * 1024) return SAT_ERR_UNSUPPORTED;
-    auto kern = k_tree<G>;
+    auto kern = k_tree<G, BNB>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
         return SAT_ERR_CUDA;
     int per_sm = 0;
@@ -287,6 +366,11 @@ int launch_tree_g(const TreeParams &tp, int Q, cudaStream_t stream) {
     if (blocks > need) blocks = std::max<uint64_t>(1, need);
     kern<<<(unsigned)blocks, kTreeThreads, smem, stream>>>(tp);
     return cudaGetLastError() == cudaSuccess ? SAT_OK : SAT_ERR_CUDA;
+}
+
+template <int G>
+int launch_tree_g(const TreeParams &tp, int Q, bool bnb, cudaStream_t stream) {
+    return bnb ? launch_tree_k<G, true>(tp, Q, stream) : launch_tree_k<G, false>(tp, Q, stream);
 }
 
 }  // namespace sat

@@ -57,6 +57,7 @@ _SIGS = {
     "sat_search_sampled": ([_vp, _i32, _u64, _u64, _u64, _vp, _vp, ctypes.c_size_t, _vp], _i32),
     "sat_tree_plan": ([_vp, _i32, _vp], _i32),
     "sat_search_tree": ([_vp, _i32, _u64, _u64, _vp, _vp, ctypes.c_size_t, _vp], _i32),
+    "sat_search_bnb": ([_vp, _i32, _u64, _u64, _vp, _vp, ctypes.c_size_t, _vp], _i32),
     "sat_schedule": ([_vp, _i32, _u64, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                       ctypes.c_size_t, _vp], _i32),
     "sat_alu_probe": ([_i32, _i32, _i32, _vp, _vp, _vp], _i32),
@@ -144,6 +145,7 @@ class SearchResult:
     job_steps: int = 0         # list-scheduling placements (tree walk) on all ranks
     device_seconds: float = 0.0
     wall_seconds: float = 0.0
+    stats: dict | None = None  # bound-and-prune counters (this rank)
 
 
 class Engine:
@@ -206,6 +208,41 @@ class Engine:
         self._check(self.lib.sat_search_tree(nprob.ref, prefix_len, task_lo, task_hi, _vp(best.data_ptr()),
                                              _vp(ws), wsb, _vp(self.stream())), what="sat_search_tree")
         self.launches += 1
+
+    def search_bnb(self, nprob, prefix_len, task_lo, task_hi, best=None):
+        """Bound-and-prune over the tree layout; returns the workspace (counters after the cursor)."""
+        best = self._best if best is None else best
+        ws, wsb = self.workspace(nprob)
+        self._check(self.lib.sat_search_bnb(nprob.ref, prefix_len, task_lo, task_hi, _vp(best.data_ptr()),
+                                            _vp(ws), wsb, _vp(self.stream())), what="sat_search_bnb")
+        self.launches += 1
+        return self._ws
+
+    def bnb_prefix(self, nprob, min_tasks: int = 1 << 15) -> int:
+        """Shortest lane prefix giving enough warp tasks to spread the pruned search over the GPU."""
+        J = nprob.struct.J
+        for P in range(1, J - 1):
+            info = SatTreeInfo()
+            if self.lib.sat_tree_plan(nprob.ref, P, ctypes.byref(info)) != SAT_OK:
+                break
+            if info.n_tasks >= min_tasks:
+                return P
+        return 0
+
+    def seed_upper_bound(self, prob: SearchProblem, nprob: NativeProblem, best, budget: int = 1 << 16,
+                         seed: int = 7):
+        """Seed *best with (U << idx_bits | max index), U = best makespan of a quick sampled search:
+        any real candidate with makespan <= U replaces it, and the bound prunes from the start."""
+        torch = self.torch
+        s_bits, _ = prob.key_bits(budget)
+        sprob = NativeProblem(prob, s_bits)
+        tmp = self.reset_best(torch.empty(2, dtype=torch.int64, device=self.device))
+        self.search_sampled(sprob, SRC_SUBSTREAM, seed, 0, budget, tmp)
+        hi = tmp[0:1].view(torch.int64)
+        ms = torch.bitwise_right_shift(hi, s_bits)
+        key = torch.bitwise_or(torch.bitwise_left_shift(ms, nprob.idx_bits), (1 << nprob.idx_bits) - 1)
+        best[0:1].copy_(torch.minimum(key, torch.where(best[0:1] == -1, torch.full_like(key, INT64_MAX),
+                                                       best[0:1])))
 
     def search_index(self, nprob, lo, hi, best=None):
         best = self._best if best is None else best
@@ -285,15 +322,24 @@ class Engine:
         launches0 = self.launches
         best = self.reset_best()
         job_steps = 0
+        stats, bnb_ws = None, None
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
         ev0.record()
         if mode == "exhaustive":
             src = SRC_INDEX
-            use_tree = opts.kernel in ("auto", "tree") and self._tree_ok(prob)
-            if opts.kernel == "tree" and not use_tree:
-                raise err.TooLarge("tree kernel needs one node, grid time, 3..20 jobs")
-            if use_tree:
+            use_tree = opts.kernel in ("auto", "tree", "bnb") and self._tree_ok(prob)
+            if opts.kernel in ("tree", "bnb") and not use_tree:
+                raise err.TooLarge("tree / bnb kernels need one node, grid time, 3..20 jobs")
+            if use_tree and opts.kernel == "bnb":
+                P = self.bnb_prefix(nprob)
+                info = self.tree_plan(nprob, P)
+                a, b = _shard(info.n_tasks, rank, world)
+                self.seed_upper_bound(prob, nprob, best)
+                bnb_ws = self.search_bnb(nprob, info.prefix_len, a, b, best)
+                stats = {"prefix_len": info.prefix_len, "tasks": b - a}
+                kernel, evaluated = "bnb", info.n_candidates
+            elif use_tree:
                 info = self.tree_plan(nprob)
                 a, b = _shard(info.n_tasks, rank, world)
                 self.search_tree(nprob, info.prefix_len, a, b, best)
@@ -315,6 +361,9 @@ class Engine:
         key = _combine(best, nprob.grid, group, world)
         ev1.synchronize()
         dev_s = ev0.elapsed_time(ev1) / 1e3
+        if bnb_ws is not None:
+            cnt = bnb_ws[:24].view(torch.int64).cpu().tolist()
+            stats.update(pruned_tasks=cnt[1], pair_nodes=cnt[2])
         if nprob.grid:
             k = int(key[0])
             if k == INT64_MAX:
@@ -329,7 +378,8 @@ class Engine:
         return SearchResult(makespan=makespan, index=index, source=src, seed=seed_used, evaluated=evaluated,
                             kernel=kernel, exhaustive=mode == "exhaustive",
                             launches=self.launches - launches0, job_steps=job_steps,
-                            device_seconds=dev_s, wall_seconds=time.perf_counter() - t0)
+                            device_seconds=dev_s, wall_seconds=time.perf_counter() - t0,
+                            stats=stats if mode == "exhaustive" else None)
 
     @staticmethod
     def _tree_ok(prob: SearchProblem) -> bool:

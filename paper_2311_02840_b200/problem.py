@@ -49,7 +49,7 @@ class SolveOptions:
     max_exhaustive: int = 1 << 42       # auto -> exhaustive when the space is <= this
     budget: int = 1 << 28               # sampled candidates when not exhaustive
     seed: int = 7                       # sampled stream: candidate i = substream(seed, i)
-    kernel: str = "auto"                # auto | tree | index (exhaustive kernel family)
+    kernel: str = "auto"                # auto | tree | index | bnb (exhaustive kernel family)
 
 
 @dataclass

@@ -184,6 +184,51 @@ def test_wide_times_use_32bit_slots(eng):
         assert got == C.CProblem(op).search("substream", trial, 0, 3000), trial
 
 
+# --------------------------------------------------------------------------- bound-and-prune
+def bnb_key(eng, prob, prefix=None, seed_bound=True, shards=1):
+    idx_bits, _ = prob.key_bits(prob.space)
+    nprob = EN.NativeProblem(prob, idx_bits)
+    P = eng.bnb_prefix(nprob) if prefix is None else prefix
+    info = eng.tree_plan(nprob, P)
+    keys = []
+    for r in range(shards):
+        best = eng.reset_best()
+        if seed_bound:
+            eng.seed_upper_bound(prob, nprob, best)
+        a, b = EN._shard(info.n_tasks, r, shards)
+        eng.search_bnb(nprob, info.prefix_len, a, b, best)
+        keys.append(int(best.cpu().numpy().view(np.uint64)[0]))
+    k = min(keys)
+    return (float(k >> idx_bits), k & ((1 << idx_bits) - 1))
+
+
+def test_bnb_equals_exhaustive_random(eng):
+    """Pruning on bound > best keeps every tie: same (makespan, lowest index) as the full scan."""
+    rng = random.Random(303)
+    for trial in range(40):
+        nodes = [rng.choice([2, 3, 4, 5, 8])]
+        op = random_problem(rng, rng.randint(3, 6), nodes, max_opts=4, max_d=9)
+        if trial % 3 == 0:
+            op.init_free = [sorted(rng.randint(0, 5) for _ in range(nodes[0]))]
+        prob = to_search_problem(op)
+        want = C.CProblem(op).search()
+        assert gpu_key(eng, prob, "tree") == want, trial
+        assert bnb_key(eng, prob, seed_bound=trial % 2 == 0) == want, trial
+        assert bnb_key(eng, prob, prefix=1, shards=3) == want, trial
+
+
+@pytest.mark.parametrize("name", ["small5_1x4", "tiny3_1x3", "cfg1"])
+def test_bnb_workloads(eng, name):
+    w, t, prob, op = workload_problem(name)
+    want = gpu_key(eng, prob, "tree")
+    assert bnb_key(eng, prob) == want
+    assert bnb_key(eng, prob, seed_bound=False) == want
+    if name != "cfg1":
+        assert want == C.CProblem(op).search()
+    else:
+        assert want[0] == golden()["milp"]["cfg1"]["optimum_intervals"]
+
+
 # --------------------------------------------------------------------------- sampled
 @pytest.mark.parametrize("name", ["cfg3", "cfg4", "cfg5", "hetero6"])
 @pytest.mark.parametrize("source", [EN.SRC_SUBSTREAM, EN.SRC_SEED])

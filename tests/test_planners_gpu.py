@@ -136,3 +136,14 @@ def test_drop_in_with_reference_objects():
     for jid, e in plan.entries.items():
         runtimes[jid] = profiling.estimate_runtime(rt, rw.job(jid), e.config, rw.job(jid).total_batches)
     core.check_plan(plan, rw, runtimes)
+
+
+def test_plan_saturn_bnb_equals_exhaustive():
+    for name in ("cfg1", "small5_1x4"):
+        w, t = setup(name)
+        ex = PL.solve(t, w)
+        bb = PL.solve(t, w, None, SolveOptions(kernel="bnb"))
+        assert bb.search.kernel == "bnb" and bb.status == "Optimal"
+        assert (bb.makespan, bb.search.index) == (ex.makespan, ex.search.index)
+        assert bb.plan == ex.plan
+        assert bb.search.stats["pair_nodes"] > 0
