@@ -302,7 +302,16 @@ class Engine:
         space = prob.space
         mode = opts.search
         if mode == "auto":
-            mode = "exhaustive" if space <= opts.max_exhaustive else "sampled"
+            # exact when the full scan is affordable, or when bound-and-prune applies (one
+            # node, grid time) and the packed key still holds the index
+            exact = space <= opts.max_exhaustive
+            if not exact and opts.kernel in ("auto", "bnb") and self._tree_ok(prob) and space <= opts.max_bnb:
+                try:
+                    prob.key_bits(space)
+                    exact = True
+                except E.SchedulerError:
+                    exact = False
+            mode = "exhaustive" if exact else "sampled"
         if mode == "exhaustive":
             if space > (1 << 62):
                 raise E.errors_for(prob.jobs[0]).TooLarge(f"exhaustive space {space} exceeds 2^62")
@@ -331,7 +340,7 @@ class Engine:
             use_tree = opts.kernel in ("auto", "tree", "bnb") and self._tree_ok(prob)
             if opts.kernel in ("tree", "bnb") and not use_tree:
                 raise err.TooLarge("tree / bnb kernels need one node, grid time, 3..20 jobs")
-            if use_tree and opts.kernel == "bnb":
+            if use_tree and opts.kernel in ("auto", "bnb"):
                 P = self.bnb_prefix(nprob)
                 info = self.tree_plan(nprob, P)
                 a, b = _shard(info.n_tasks, rank, world)

@@ -47,9 +47,10 @@ class SolveOptions:
     prune: bool | None = None           # None: on for single-node clusters
     search: str = "auto"                # auto | exhaustive | sampled
     max_exhaustive: int = 1 << 42       # auto -> exhaustive when the space is <= this
+    max_bnb: int = 1 << 52              # auto -> exact bound-and-prune (one node, grid) up to this
     budget: int = 1 << 28               # sampled candidates when not exhaustive
     seed: int = 7                       # sampled stream: candidate i = substream(seed, i)
-    kernel: str = "auto"                # auto | tree | index | bnb (exhaustive kernel family)
+    kernel: str = "auto"                # auto (bnb when it applies) | tree | index | bnb
 
 
 @dataclass

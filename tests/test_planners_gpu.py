@@ -25,10 +25,12 @@ def setup(name):
 
 def test_plan_saturn_cfg1_optimal_and_valid():
     w, t = setup("cfg1")
-    sol = PL.solve(t, w)
+    sol = PL.solve(t, w, None, SolveOptions(kernel="tree"))
     assert sol.status == "Optimal"
     assert sol.makespan == 30 == golden()["milp"]["cfg1"]["optimum_intervals"]
     assert sol.search.kernel == "tree" and sol.search.evaluated == 32514048000
+    default = PL.solve(t, w)                                   # auto = bound-and-prune
+    assert default.search.kernel == "bnb" and default.plan == sol.plan
     D.check_plan(sol.plan, w, sol.runtimes)
     assert math.isclose(sol.plan.predicted_makespan, 30 * sol.problem.delta)
     # the decoded plan is exactly the oracle's replay of the winning index
