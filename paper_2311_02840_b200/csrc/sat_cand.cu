@@ -28,17 +28,20 @@ static int launch_cand_g(const sat_problem_t *p, CandArgs a, uint64_t n_cand, co
         per_sm < 1)
         per_sm = 1;
     uint64_t blocks = (uint64_t)device_sms() * (uint64_t)per_sm;
-    const uint64_t chunks = (n_cand + (uint64_t)a.per_lane - 1) / (uint64_t)a.per_lane;
-    const uint64_t need = (chunks + kCandThreads - 1) / kCandThreads;
+    const uint64_t chunks = (n_cand + 32ull * a.per_lane - 1) / (32ull * a.per_lane);   // warp chunks
+    const uint64_t need = (chunks + kCandWarps - 1) / kCandWarps;
     if (blocks > need) blocks = std::max<uint64_t>(1, need);
     const size_t part_off = (blob_bytes + 255) & ~(size_t)255;
-    const size_t need_ws = part_off + (size_t)blocks * sizeof(sat_best_t);
+    const size_t cur_off = part_off + (size_t)blocks * sizeof(sat_best_t);
+    const size_t need_ws = cur_off + sizeof(unsigned long long);
     if (!d_ws || ws_bytes < need_ws) return SAT_ERR_INVALID;
     uint8_t *ws = static_cast<uint8_t *>(d_ws);
     if (cudaMemcpyAsync(ws, blob.data(), blob_bytes, cudaMemcpyHostToDevice, stream) != cudaSuccess)
         return SAT_ERR_CUDA;
+    if (cudaMemsetAsync(ws + cur_off, 0, sizeof(unsigned long long), stream) != cudaSuccess) return SAT_ERR_CUDA;
     a.blob = ws;
     a.partials = reinterpret_cast<sat_best_t *>(ws + part_off);
+    a.cursor = reinterpret_cast<unsigned long long *>(ws + cur_off);
     kern<<<(unsigned)blocks, kCandThreads, smem, stream>>>(a);
     if (cudaGetLastError() != cudaSuccess) return SAT_ERR_CUDA;
     if (sizeof(T) == 8) {

@@ -33,7 +33,8 @@ struct CandArgs {
     const uint8_t *blob;
     uint64_t lo, hi;            // candidate ids [lo, hi)
     uint64_t seed;
-    int32_t per_lane;           // consecutive ids per thread per chunk (index source)
+    int32_t per_lane;           // consecutive ids per thread per warp chunk
+    unsigned long long *cursor; // warp chunks handed out so far (zeroed before the launch)
     int32_t rec_d;              // records carry the duration (node-independent, all nodes eligible)
     sat_best_t *best;           // grid mode result
     sat_best_t *partials;       // float mode per-block partials
@@ -109,14 +110,19 @@ k_cand(CandArgs a) {
     uint64_t best_ix = ~0ull;
 
     const uint64_t total = a.hi - a.lo;
-    const int per_lane = kIndex ? a.per_lane : 1;
-    const uint64_t nthreads = (uint64_t)gridDim.x * kCandThreads;
-    const uint64_t gthread = (uint64_t)blockIdx.x * kCandThreads + threadIdx.x;
-    const uint64_t nchunks = (total + per_lane - 1) / per_lane;
-
-    for (uint64_t c = gthread; c < nchunks; c += nthreads) {
+    // warps take chunks of 32 x per_lane candidates from a cursor (thread: per_lane
+    // consecutive ids, so the index source can advance instead of re-decoding)
+    const int per_lane = a.per_lane;
+    const uint64_t chunk = 32ull * (uint64_t)per_lane;
+    const uint64_t nchunks = (total + chunk - 1) / chunk;
+    auto next_chunk = [&]() -> uint64_t {
+        unsigned long long v = 0;
+        if (lane == 0) v = atomicAdd(a.cursor, 1ull);
+        return __shfl_sync(0xffffffffu, v, 0);
+    };
+    for (uint64_t c = next_chunk(); c < nchunks; c = next_chunk()) {
         for (int k = 0; k < per_lane; ++k) {
-            const uint64_t off = c * (uint64_t)per_lane + k;
+            const uint64_t off = c * chunk + (uint64_t)lane * per_lane + k;
             if (off >= total) break;
             const uint64_t id = a.lo + off;
             // ---- decode into this thread's record column ----

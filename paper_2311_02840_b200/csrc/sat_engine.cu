@@ -566,7 +566,7 @@ int sat_workspace_bytes(const sat_problem_t *p, size_t *bytes) {
     st = pack_blob(p, blob, records_carry_duration(p));
     if (st) return st;
     const size_t part_off = (blob.size() + 255) & ~(size_t)255;
-    *bytes = part_off + (size_t)device_sms() * 32 * sizeof(sat_best_t);
+    *bytes = part_off + (size_t)device_sms() * 32 * sizeof(sat_best_t) + 256;   // + k_cand chunk cursor
     return SAT_OK;
 }
 
@@ -598,7 +598,7 @@ int sat_search_sampled(const sat_problem_t *p, int32_t source, uint64_t seed, ui
     if (p->time_mode == SAT_TIME_GRID_I32 && hi > 0 && ((hi - 1) >> p->idx_bits)) return SAT_ERR_TOO_LARGE;
     if (hi == lo) return SAT_OK;
     CandArgs a{};
-    a.lo = lo; a.hi = hi; a.best = d_best; a.seed = seed; a.per_lane = 1;
+    a.lo = lo; a.hi = hi; a.best = d_best; a.seed = seed; a.per_lane = 8;
     cudaStream_t s = (cudaStream_t)stream;
     if (p->time_mode == SAT_TIME_F64) {
         if (source == SAT_SRC_SUBSTREAM)
