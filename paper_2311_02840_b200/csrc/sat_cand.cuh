@@ -60,7 +60,7 @@ __host__ __device__ constexpr int cand_slot_bytes() {
 }
 
 template <typename T, int SRC, int G, int L>
-__global__ void __launch_bounds__(kCandThreads, SRC == SAT_SRC_INDEX ? 1 : (G <= 8 ? 12 : (G <= 16 ? 10 : 8)))
+__global__ void __launch_bounds__(kCandThreads, SRC == SAT_SRC_INDEX ? 8 : (G <= 8 ? 12 : (G <= 16 ? 10 : 8)))
 k_cand(CandArgs a) {
     constexpr bool MULTI = L == kLayoutMulti;
     constexpr bool P16 = L == kLayoutOne16;

@@ -119,9 +119,15 @@ def solve(table, jobs, cluster=None, delta_opts=None, running_context=None, *, t
           group=None, device=None, validate: bool = True) -> Solution:
     """Solver.solve / re-solve on the engine (build -> search -> decode -> check)."""
     workload = _as_workload(jobs, cluster, techniques)
-    err = E.errors_for(workload.jobs[0] if workload.jobs else workload)
     opts = _opts(delta_opts)
     prob = build_problem(table, workload, opts, running_context)
+    return solve_problem(prob, workload, opts, running_context, group=group, device=device, validate=validate)
+
+
+def solve_problem(prob: SearchProblem, workload, opts: SolveOptions, running_context=None, *, group=None,
+                  device=None, validate: bool = True) -> Solution:
+    """Search -> decode -> check for an already marshalled problem (the milp facade's entry)."""
+    err = E.errors_for(workload.jobs[0] if workload.jobs else workload)
     eng = get_engine(device)
     try:
         res = eng.search(prob, opts, group=group)
@@ -332,7 +338,7 @@ def evaluate_fixed(table, workload, options, order, delta_opts=None, running_con
 
 
 __all__ = [
-    "Solution", "solve", "plan_saturn", "resolve", "plan_random", "plan_random_best",
+    "Solution", "solve", "solve_problem", "plan_saturn", "resolve", "plan_random", "plan_random_best",
     "optimus_marginal_gain", "optimus_allocation", "plan_optimus", "current_practice_allocation",
     "plan_current_practice", "evaluate_fixed", "get_engine",
 ]
