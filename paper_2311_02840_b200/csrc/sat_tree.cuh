@@ -168,6 +168,46 @@ __device__ __forceinline__ int32_t published_ms(const TreeParams &p) {
     return hi == ~0ull ? SAT_INF_I32 : (int32_t)(hi >> p.idx_bits);
 }
 
+// Suffix walk with a compile-time number D of upper levels (Q = D + 2 jobs left): the
+// level state (remaining set, index accumulator, cursor) stays in registers instead of the
+// local-memory stack of the generic walk.  Level L's free times are the lane's column in
+// level buffer L; children go to buffer L + 1; the last two jobs are the pair pass.
+template <int G, bool BNB, int D>
+__device__ __forceinline__ void walk_fixed(const TreeParams &p, int32_t *wbase, int lane, int L, int Q,
+                                           uint32_t rem, uint64_t acc_in, bool ok, int32_t *Bbuf,
+                                           const int32_t *sdg, LaneBest &lb, int32_t &U,
+                                           unsigned long long &n_pairs) {
+    constexpr int col_words = 2 * G * 32;
+    const int32_t *src = wbase + L * col_words + lane;
+    int32_t *dst = wbase + (L + 1) * col_words + lane;
+    const uint64_t fq = p.fact[Q - 1 - L];
+    for (uint32_t m = rem; m; m &= m - 1) {
+        const int j = __ffs(m) - 1;
+        const uint32_t rem2 = rem & ~(1u << j);
+        const uint64_t acc_j = acc_in + (uint64_t)__popc(rem & ((1u << j) - 1u)) * fq;
+        const int r = p.radix[j], ob = p.optbase[j];
+        const uint64_t wj = p.wJ[j];
+        for (int o = 0; o < r; ++o) {
+            merge_cols<G>(src, dst, p.optg[ob + o], p.optd[ob + o]);
+            const uint64_t acc = acc_j + (uint64_t)o * wj;
+            bool child_ok = ok;
+            if constexpr (BNB) {
+                if (__any_sync(0xffffffffu, child_ok)) {
+                    U = min(U, lb.ms);
+                    child_ok = child_ok && lane_bound<G>(p, dst, sdg, rem2) <= U;
+                }
+                if (!__any_sync(0xffffffffu, child_ok)) continue;
+            }
+            if constexpr (D == 1) {
+                if (BNB && lane == 0) ++n_pairs;
+                tree_pair<G>(p, dst, Bbuf, sdg, rem2, acc, child_ok, lb);
+            } else {
+                walk_fixed<G, BNB, D - 1>(p, wbase, lane, L + 1, Q, rem2, acc, child_ok, Bbuf, sdg, lb, U, n_pairs);
+            }
+        }
+    }
+}
+
 // occupancy target per node size: 12 blocks (40 regs) up to 8 GPUs, fewer for larger nodes.
 // BNB = bound-and-prune: subtrees whose bound exceeds the best makespan found so far (by
 // any warp: published after every task) are skipped; the key found is the exhaustive one.
@@ -221,16 +261,22 @@ k_tree(const __grid_constant__ TreeParams p) {
         uint64_t prank = qq - code * fP;
         int32_t *L0 = wbase + lane;
         for (int i = 0; i < G; ++i) L0[i * 32] = p.init_free[i];
-        uint8_t popt[kTreeMaxJ];
+        // options of S's jobs: mixed radix, highest job id least significant; kept as 8-bit
+        // fields indexed by the job's rank within S (P <= 8: one u64 register; else local)
+        uint64_t popt_lo = 0;
+        uint8_t popt_hi[kTreeMaxJ];
         {
-            // options: mixed radix over S's jobs, highest job id least significant
             uint32_t m = S;
+            int rank = P;
             while (m) {
                 const int j = 31 - __clz(m);
                 m &= ~(1u << j);
+                --rank;
                 const uint64_t r = (uint64_t)p.radix[j];
                 const uint64_t qd = code / r;
-                popt[j] = (uint8_t)(code - qd * r);
+                const uint64_t dig = code - qd * r;
+                if (rank < 8) popt_lo |= dig << (8 * rank);
+                else popt_hi[rank] = (uint8_t)dig;
                 code = qd;
             }
         }
@@ -244,7 +290,8 @@ k_tree(const __grid_constant__ TreeParams p) {
             for (uint64_t x = 0; x < digit; ++x) m &= m - 1;
             const int j = __ffs(m) - 1;
             avail &= ~(1u << j);
-            const int o = popt[j];
+            const int rk = __popc(S & ((1u << j) - 1u));
+            const int o = rk < 8 ? (int)((popt_lo >> (8 * rk)) & 0xffu) : (int)popt_hi[rk];
             base += (uint64_t)__popc(unplaced & ((1u << j) - 1u)) * p.fact[J - 1 - k] + (uint64_t)o * p.wJ[j];
             unplaced &= ~(1u << j);
             // per-lane gang size: in-place merge on the lane's column
@@ -269,6 +316,10 @@ k_tree(const __grid_constant__ TreeParams p) {
         if (Q == 2) {
             if (BNB && lane == 0) ++n_pairs;
             tree_pair<G>(p, L0, Bbuf, sdg, unplaced, base, lane_ok, lb);
+        } else if (Q == 3) {
+            walk_fixed<G, BNB, 1>(p, wbase, lane, 0, Q, unplaced, base, lane_ok, Bbuf, sdg, lb, U, n_pairs);
+        } else if (Q == 4) {
+            walk_fixed<G, BNB, 2>(p, wbase, lane, 0, Q, unplaced, base, lane_ok, Bbuf, sdg, lb, U, n_pairs);
         } else {
             uint32_t rem_st[kTreeMaxJ];
             uint64_t acc_st[kTreeMaxJ];
