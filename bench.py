@@ -113,8 +113,17 @@ def dist_setup(n_gpus: int):
     if world > 1:
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # SATURN_BENCH_GPU_OVERRIDE=k maps every rank onto cuda:k with the gloo backend: a
+        # functional check of the sharded path on a one-GPU box (ranks never wait on each
+        # other inside a kernel; only the host-side collectives meet).  Never a bench number.
+        override = os.environ.get("SATURN_BENCH_GPU_OVERRIDE")
+        if override is not None:
+            local = int(override)
+            torch.cuda.set_device(local)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     elif torch.cuda.is_available():
         torch.cuda.set_device(0)
     return rank, world, local
