@@ -265,7 +265,8 @@ class DeviceSolve:
         self.use_tree = self.mode == "exhaustive" and eng._tree_ok(prob)
         G, N, J = prob.G, prob.N, prob.J
         if self.use_tree:
-            self.info = eng.tree_plan(self.nprob)
+            # per rank ~22 warp tasks per resident warp at least (dynamic cursor balance)
+            self.info = eng.tree_plan(self.nprob, eng.tree_prefix(self.nprob, (1 << 17) * world) if world > 1 else 0)
             self.a, self.b = EN._shard(self.info.n_tasks, rank, world)
             self.n_cand = self.info.n_candidates
             merges = self.info.n_job_steps - self.info.n_candidates

@@ -218,6 +218,10 @@ class Engine:
         self.launches += 1
         return self._ws
 
+    def tree_prefix(self, nprob, min_tasks: int) -> int:
+        """Shortest lane prefix with at least `min_tasks` warp tasks (0 = the library's choice)."""
+        return self.bnb_prefix(nprob, min_tasks)
+
     def bnb_prefix(self, nprob, min_tasks: int = 1 << 15) -> int:
         """Shortest lane prefix giving enough warp tasks to spread the pruned search over the GPU."""
         J = nprob.struct.J
@@ -341,7 +345,7 @@ class Engine:
             if opts.kernel in ("tree", "bnb") and not use_tree:
                 raise err.TooLarge("tree / bnb kernels need one node, grid time, 3..20 jobs")
             if use_tree and opts.kernel in ("auto", "bnb"):
-                P = self.bnb_prefix(nprob)
+                P = self.bnb_prefix(nprob, (1 << 15) * world)       # enough tasks on every rank
                 info = self.tree_plan(nprob, P)
                 a, b = _shard(info.n_tasks, rank, world)
                 self.seed_upper_bound(prob, nprob, best)
@@ -349,7 +353,7 @@ class Engine:
                 stats = {"prefix_len": info.prefix_len, "tasks": b - a}
                 kernel, evaluated = "bnb", info.n_candidates
             elif use_tree:
-                info = self.tree_plan(nprob)
+                info = self.tree_plan(nprob, self.tree_prefix(nprob, (1 << 17) * world) if world > 1 else 0)
                 a, b = _shard(info.n_tasks, rank, world)
                 self.search_tree(nprob, info.prefix_len, a, b, best)
                 kernel, evaluated, job_steps = "tree", info.n_candidates, info.n_job_steps
