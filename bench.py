@@ -419,9 +419,11 @@ def run_ours(args):
                "stats": stats,
                "api": api.replace("(plan_saturn)", "(plan_saturn, default options)")}
 
-    # per solve: tables packed into the launch + decode id in; best key + winner schedule
-    # (option, node, start per job) + makespan out
-    h2d = sum(s.nprob.param_bytes + 8 for s in solves)
+    # per solve in: the problem tables (host arrays), the tree kernel's by-value parameter block
+    # and cursor reset, the decode id; out: best key + winner schedule (option, node, start per
+    # job) + makespan
+    tree_param = int(eng.lib.sat_tree_param_bytes())
+    h2d = sum(s.nprob.param_bytes + 8 + (tree_param + 24 if s.use_tree else 0) for s in solves)
     d2h = sum(16 + 3 * 4 * s.prob.J + 8 for s in solves)
 
     # ---- roofline: INT32 min/max issue rate measured on this GPU ----

@@ -152,6 +152,10 @@ int sat_schedule(const sat_problem_t *p, int32_t source, uint64_t seed,
                  int64_t *d_makespan_i64, double *d_makespan_f64,
                  void *d_ws, size_t ws_bytes, void *stream);
 
+/* Bytes of the launch-parameter block the tree / bnb searches pass by value (their
+ * host-to-device traffic per launch, besides the 24-byte cursor reset). */
+size_t sat_tree_param_bytes(void);
+
 /* INT32 min/max issue-rate probe for the roofline denominator: runs `iters`
  * dependent-chain IMNMX iterations on every SM; *d_ops_out = lane-ops done. */
 int sat_alu_probe(int32_t blocks, int32_t threads, int32_t iters,

@@ -737,6 +737,8 @@ static int search_tree_impl(const sat_problem_t *p, int32_t prefix_len, uint64_t
     }
 }
 
+size_t sat_tree_param_bytes(void) { return sizeof(TreeParams); }
+
 int sat_search_tree(const sat_problem_t *p, int32_t prefix_len, uint64_t task_lo, uint64_t task_hi,
                     sat_best_t *d_best, void *d_ws, size_t ws_bytes, void *stream) {
     return search_tree_impl(p, prefix_len, task_lo, task_hi, d_best, d_ws, ws_bytes, stream, false);

@@ -61,6 +61,7 @@ _SIGS = {
     "sat_schedule": ([_vp, _i32, _u64, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                       ctypes.c_size_t, _vp], _i32),
     "sat_alu_probe": ([_i32, _i32, _i32, _vp, _vp, _vp], _i32),
+    "sat_tree_param_bytes": ([], ctypes.c_size_t),
 }
 
 _LIB = None
