@@ -22,6 +22,9 @@ HDR = os.path.join(ROOT, "include", "saturn_engine.h")
 OUT_DIR = os.path.join(HERE, "_lib")
 OBJ_DIR = os.path.join(OUT_DIR, "obj")
 OUT = os.path.join(OUT_DIR, "libsaturn_b200.so")
+# debug variant: device-side bounds checks on every shared-memory region index (SAT_ASSERT)
+DEBUG_OBJ_DIR = os.path.join(OUT_DIR, "obj_debug")
+DEBUG_OUT = os.path.join(OUT_DIR, "libsaturn_b200_debug.so")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-diag-suppress", "128"]
@@ -39,15 +42,16 @@ def sources() -> list:
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cuh"))) + [HDR]
 
 
-def up_to_date() -> bool:
-    if not os.path.exists(OUT):
+def up_to_date(out_path: str = OUT) -> bool:
+    if not os.path.exists(out_path):
         return False
-    t = os.path.getmtime(OUT)
+    t = os.path.getmtime(out_path)
     return all(os.path.getmtime(f) <= t for f in sources() + [__file__])
 
 
-def units() -> list:
+def units(obj_dir: str = OBJ_DIR) -> list:
     """(source, extra defines, object) for every translation unit."""
+    OBJ_DIR = obj_dir  # noqa: N806 (local rebinding keeps the table below readable)
     out = [(os.path.join(CSRC, "sat_engine.cu"), [], os.path.join(OBJ_DIR, "sat_engine.o"))]
     for t in ("int32_t", "double"):
         for s in ("SAT_SRC_INDEX", "SAT_SRC_SUBSTREAM", "SAT_SRC_SEED"):
@@ -59,28 +63,30 @@ def units() -> list:
     return out
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
-        return OUT
-    os.makedirs(OBJ_DIR, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, debug: bool = False) -> str:
+    out_path, obj_dir = (DEBUG_OUT, DEBUG_OBJ_DIR) if debug else (OUT, OBJ_DIR)
+    extra = ["-DSAT_DEBUG_BOUNDS"] if debug else []
+    if not force and up_to_date(out_path):
+        return out_path
+    os.makedirs(obj_dir, exist_ok=True)
     cc = nvcc()
     procs = []
-    for src, defs, obj in units():
-        cmd = [cc, *NVCC_FLAGS, *defs, "-c", "-o", obj, src]
+    for src, defs, obj in units(obj_dir):
+        cmd = [cc, *NVCC_FLAGS, *extra, *defs, "-c", "-o", obj, src]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         procs.append((cmd, subprocess.Popen(cmd)))
     for cmd, p in procs:
         if p.wait() != 0:
             raise subprocess.CalledProcessError(p.returncode, cmd)
-    tmp = OUT + ".tmp"
-    link = [cc, *ARCH, "-shared", "-o", tmp, *[obj for _, _, obj in units()]]
+    tmp = out_path + ".tmp"
+    link = [cc, *ARCH, "-shared", "-o", tmp, *[obj for _, _, obj in units(obj_dir)]]
     if verbose:
         print(" ".join(link), file=sys.stderr)
     subprocess.run(link, check=True)
-    os.replace(tmp, OUT)
-    return OUT
+    os.replace(tmp, out_path)
+    return out_path
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    print(build(force="--force" in sys.argv, verbose=True, debug="--debug" in sys.argv))

@@ -88,6 +88,7 @@ k_cand(CandArgs a) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr bool kIndex = SRC == SAT_SRC_INDEX;
     uint8_t *wbase = smem + h.bytes + warp * cand_warp_bytes(J, N, G, cand_slot_bytes<T, L>(), kIndex);
+    SAT_ASSERT(N >= 1 && N * G <= 32 && J >= 1 && J <= SAT_MAX_JOBS);
     uint32_t *rec = reinterpret_cast<uint32_t *>(wbase) + lane;          // [J][32]
     uint8_t *opt = wbase + J * 128 + lane;                               // [J][32] (index source)
     uint8_t *ord = opt + J * 32;                                         // [J][32]
@@ -154,6 +155,8 @@ k_cand(CandArgs a) {
                 for (int kk = 0; kk < J; ++kk) {
                     const uint32_t r = rec[kk * 32];
                     const int g = (int)(r & 63u) + 1;
+                    SAT_ASSERT(g >= 1 && g <= G && (int)((r >> 6) & 63u) < J);
+                    SAT_ASSERT(rec_d || (int)(r >> 12) < h.n_opt);
                     const int gm = g - 1;
                     // slot g-1 = one half of word (g-1)/2 (read as the word: no type-punned loads)
                     const uint32_t selt = 0x4410u + (uint32_t)(gm & 1) * 0x22u;
@@ -184,6 +187,8 @@ k_cand(CandArgs a) {
                 for (int kk = 0; kk < J; ++kk) {
                     const uint32_t r = rec[kk * 32];
                     const int g = (int)(r & 63u) + 1;
+                    SAT_ASSERT(g >= 1 && g <= G && (int)((r >> 6) & 63u) < J);
+                    SAT_ASSERT(rec_d || (int)(r >> 12) < h.n_opt);
                     const T d = rec_d ? (T)(int32_t)(r >> 12) : dur[r >> 12];
                     T t = st[(g - 1) * 32];
                     if (has_release) t = tmax(t, release[(r >> 6) & 63u]);
@@ -212,6 +217,8 @@ k_cand(CandArgs a) {
                 for (int kk = 0; kk < J; ++kk) {
                     const uint32_t r = rec[kk * 32];
                     const int g = (int)(r & 63u) + 1;
+                    SAT_ASSERT(g >= 1 && g <= G && (int)((r >> 6) & 63u) < J);
+                    SAT_ASSERT(rec_d || (int)(r >> 12) < h.n_opt);
                     const int gm = g - 1;
                     const int32_t rel = has_release ? (int32_t)release[(r >> 6) & 63u] : 0;
                     const uint32_t selt = 0x4410u + (uint32_t)(gm & 1) * 0x22u;
@@ -225,6 +232,7 @@ k_cand(CandArgs a) {
                         }
                     }
                     const int bn = (int)(kb & 31u);
+                    SAT_ASSERT(bn < N);
                     const int32_t e = (int32_t)(kb >> 5) + (int32_t)(r >> 12);
                     const uint32_t e2 = (uint32_t)e * 0x10001u;
                     const uint32_t sel = (g & 1) ? 0x5432u : 0x3210u;
@@ -249,6 +257,8 @@ k_cand(CandArgs a) {
                 for (int kk = 0; kk < J; ++kk) {
                     const uint32_t r = rec[kk * 32];
                     const int g = (int)(r & 63u) + 1;
+                    SAT_ASSERT(g >= 1 && g <= G && (int)((r >> 6) & 63u) < J);
+                    SAT_ASSERT(rec_d || (int)(r >> 12) < h.n_opt);
                     const uint32_t pay = r >> 12;
                     const T rel = has_release ? release[(r >> 6) & 63u] : (T)0;
                     // node finishing the job earliest, lowest node on ties
@@ -270,6 +280,7 @@ k_cand(CandArgs a) {
                             if (n == 0 || e < be) { be = e; bn = n; }
                         }
                     }
+                    SAT_ASSERT(bn >= 0 && bn < N);
                     T *sb = st + bn * 2 * G * 32;
                     T cur[G], s[G];
 #pragma unroll

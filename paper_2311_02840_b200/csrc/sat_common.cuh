@@ -14,6 +14,22 @@
 
 #define SAT_INF_I32 0x3FFFFFFF
 
+// Device-side bounds checks for the debug build of the library (build.py --debug ->
+// libsaturn_b200_debug.so, -DSAT_DEBUG_BOUNDS): every index that addresses a thread's or
+// warp's shared-memory region is checked against the region; a violation traps.  The
+// release build compiles them out.  (compute-sanitizer is not available on this pool.)
+#ifdef SAT_DEBUG_BOUNDS
+#define SAT_ASSERT(c)                                                                  \
+    do {                                                                               \
+        if (!(c)) {                                                                    \
+            printf("SAT_ASSERT failed %s:%d: %s\n", __FILE__, __LINE__, #c);           \
+            __trap();                                                                  \
+        }                                                                              \
+    } while (0)
+#else
+#define SAT_ASSERT(c) do { } while (0)
+#endif
+
 namespace sat {
 
 constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;

@@ -186,10 +186,12 @@ __device__ inline void decode_stream(uint64_t state0, const GenTables &t, uint32
     for (int j = 0; j < t.J; ++j) {
         const JobInfo ji = t.jobinfo[j];
         const int o = (int)s.below_fast((uint32_t)ji.radix, ji.magic, hi_max);
+        SAT_ASSERT(o >= 0 && o < ji.radix);
         steps[j * 32] = t.prerec[ji.optbase + o];
     }
     for (int i = t.J - 1; i >= 1; --i) {                 // rng.py:44-48
         const int k = (int)s.below_fast((uint32_t)(i + 1), t.mods[i + 1].magic, hi_max);
+        SAT_ASSERT(k >= 0 && k <= i);
         const uint32_t x = steps[i * 32];
         steps[i * 32] = steps[k * 32];
         steps[k * 32] = x;

@@ -123,6 +123,7 @@ __device__ __forceinline__ void tree_pair(const TreeParams &p, const int32_t *U,
 // Upper-level merge with a warp-uniform runtime gang size, smem column to smem column.
 template <int G>
 __device__ __forceinline__ void merge_cols(const int32_t *src, int32_t *dst, int g, int32_t d) {
+    SAT_ASSERT(g >= 1 && g <= G);
     const int32_t e = src[(g - 1) * 32] + d;
 #pragma unroll
     for (int i = 0; i < G; ++i) {
@@ -297,6 +298,7 @@ k_tree(const __grid_constant__ TreeParams p) {
             // per-lane gang size: in-place merge on the lane's column
             const int q2 = p.optbase[j] + o;
             const int g = p.optg[q2];
+            SAT_ASSERT(j >= 0 && j < J && o < p.radix[j] && g >= 1 && g <= G);
             const int32_t e = L0[(g - 1) * 32] + p.optd[q2];
             for (int i = 0; i < G; ++i) L0[i * 32] = max(L0[i * 32], min(L0[(i + g) * 32], e));
         }

@@ -19,7 +19,8 @@ import numpy as np
 from . import errors as E
 from .problem import TIME_FLOAT, TIME_GRID, SearchProblem, SolveOptions
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libsaturn_b200.so")
+LIB_PATH = os.environ.get("SATURN_ENGINE_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib",
+                                                                  "libsaturn_b200.so")
 
 SAT_OK, SAT_ERR_INVALID, SAT_ERR_NO_OPTIONS, SAT_ERR_TOO_LARGE, SAT_ERR_UNSUPPORTED, SAT_ERR_CUDA = range(6)
 SAT_TIME_GRID_I32, SAT_TIME_F64 = 0, 1
