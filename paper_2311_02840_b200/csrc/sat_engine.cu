@@ -670,6 +670,7 @@ static int search_tree_impl(const sat_problem_t *p, int32_t prefix_len, uint64_t
     st = tree_layout(p, prefix_len, lay);
     if (st) return st;
     if (task_hi > lay.n_tasks) return SAT_ERR_INVALID;
+    if (task_hi - task_lo >= (1ull << 32)) return SAT_ERR_TOO_LARGE;   // task ids travel as 32-bit
     if ((lay.n_cand - 1) >> p->idx_bits) return SAT_ERR_TOO_LARGE;
     if (task_hi == task_lo) return SAT_OK;
     TreeParams tp;

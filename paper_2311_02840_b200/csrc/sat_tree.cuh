@@ -223,9 +223,9 @@ k_tree(const __grid_constant__ TreeParams p) {
     int32_t *wbase = tsm + warp * (upper * col_words + G * 32);
     int32_t *Bbuf = wbase + upper * col_words + lane;
     // per (job, gang) least durations, shared by the block (broadcast loads in the pair pass)
-    int32_t *sdg = tsm + kTreeWarps * (upper * col_words + G * 32);
-    for (int i = threadIdx.x; i < p.J * 32; i += blockDim.x) sdg[i] = p.dg[i >> 5][i & 31];
-    __syncthreads();
+    // per (job, gang) least durations, read straight from the parameter block: the job index
+    // is warp-uniform, so these are uniform constant loads and the gang branches uniform
+    const int32_t *sdg = &p.dg[0][0];
     // padding rows of every level buffer = INF (never rewritten)
     for (int L = 0; L < upper; ++L)
         for (int i = G; i < 2 * G; ++i) wbase[L * col_words + i * 32 + lane] = SAT_INF_I32;
@@ -237,10 +237,12 @@ k_tree(const __grid_constant__ TreeParams p) {
 
     // dynamic task cursor: a warp takes the next task when it finishes one (task costs
     // differ by the remaining jobs' radices; a static split leaves a long tail)
+    // (the host keeps a launch below 2^32 tasks, so the id travels as a 32-bit warp reduction,
+    // which the compiler knows to be warp-uniform)
     auto next_task = [&]() -> uint64_t {
-        unsigned long long v = 0;
-        if (lane == 0) v = atomicAdd(p.cursor, 1ull);
-        return p.task_lo + __shfl_sync(0xffffffffu, v, 0);
+        unsigned v = 0xffffffffu;
+        if (lane == 0) v = (unsigned)atomicAdd(p.cursor, 1ull);
+        return p.task_lo + (uint64_t)__reduce_min_sync(0xffffffffu, v);
     };
     for (uint64_t t = next_task(); t < p.task_hi; t = next_task()) {
         // ---- which prefix set (warp-uniform binary search) ----
@@ -282,7 +284,8 @@ k_tree(const __grid_constant__ TreeParams p) {
             }
         }
         uint64_t base = 0;
-        uint32_t unplaced = all, avail = S;
+        const uint32_t unplaced = all & ~S;          // warp-uniform: the suffix jobs
+        uint32_t unpl = all, avail = S;
         for (int k = 0; k < P; ++k) {
             fP /= (uint64_t)(P - k);
             const uint64_t digit = prank / fP;
@@ -293,8 +296,8 @@ k_tree(const __grid_constant__ TreeParams p) {
             avail &= ~(1u << j);
             const int rk = __popc(S & ((1u << j) - 1u));
             const int o = rk < 8 ? (int)((popt_lo >> (8 * rk)) & 0xffu) : (int)popt_hi[rk];
-            base += (uint64_t)__popc(unplaced & ((1u << j) - 1u)) * p.fact[J - 1 - k] + (uint64_t)o * p.wJ[j];
-            unplaced &= ~(1u << j);
+            base += (uint64_t)__popc(unpl & ((1u << j) - 1u)) * p.fact[J - 1 - k] + (uint64_t)o * p.wJ[j];
+            unpl &= ~(1u << j);
             // per-lane gang size: in-place merge on the lane's column
             const int q2 = p.optbase[j] + o;
             const int g = p.optg[q2];
@@ -404,7 +407,7 @@ k_tree(const __grid_constant__ TreeParams p) {
 template <int G, bool BNB>
 int launch_tree_k(const TreeParams &tp, int Q, cudaStream_t stream) {
     const int upper = Q - 1;
-    const int smem = (kTreeWarps * (upper * 2 * G * 32 + G * 32) + tp.J * 32) * 4;
+    const int smem = kTreeWarps * (upper * 2 * G * 32 + G * 32) * 4;
     if (smem > 200 * 1024) return SAT_ERR_UNSUPPORTED;
     auto kern = k_tree<G, BNB>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
