@@ -59,13 +59,198 @@ __host__ __device__ constexpr int cand_slot_bytes() {
     return (L == kLayoutOne16 || L == kLayoutMulti16) ? 2 : (int)sizeof(T);
 }
 
+// Everything the list scheduler reads, resolved once per kernel (pointers are per lane).
+template <typename T>
+struct SchedCtx {
+    T *st;                   // the lane's free-time column: [N][2G][32] (T) or [N][G][32] words (packed)
+    uint32_t *st16;
+    const T *lane_init;      // [N][G] initial free times (+inf on ghost slots)
+    const T *release;        // [J]
+    const T *dur;            // [n_opt][N] (when records carry option ids)
+    const uint32_t *optmask; // [n_opt] node eligibility (several nodes)
+    int J, N, n_opt;
+    bool rec_d, has_release;
+    T init_max, INF;
+};
+
+// List-schedule the J step records in the lane's record column (stride 32) and return the
+// makespan.  Layout L as in the file comment; G = padded GPUs per node.
+template <typename T, int G, int L>
+__device__ __forceinline__ T schedule_records(const SchedCtx<T> &c, const uint32_t *rec) {
+    constexpr bool P16 = L == kLayoutOne16;
+    constexpr bool M16 = L == kLayoutMulti16;
+    constexpr int NMAX = (L == kLayoutMulti || M16) ? (32 / G) : 1;
+    T *st = c.st;
+    uint32_t *st16 = c.st16;
+    const T *lane_init = c.lane_init;
+    const T *release = c.release;
+    const T *dur = c.dur;
+    const int J = c.J, N = c.N;
+    const bool rec_d = c.rec_d, has_release = c.has_release;
+    const T INF = c.INF;
+    (void)INF; (void)dur; (void)N;
+    T mx = c.init_max;
+    if constexpr (P16) {
+        // slots 2w (low half) and 2w+1 (high half) of word w; rows G/2..G-1 = +inf.
+        // Shift by the thread's g: word k of the shifted vector is word g/2 + k (g even)
+        // or the high half of word g/2 + k joined to the low half of the next (g odd):
+        // one PRMT with a per-thread selector either way.
+        uint32_t av[G / 2];
+#pragma unroll
+        for (int w = 0; w < G / 2; ++w) {
+            av[w] = (uint32_t)(uint16_t)lane_init[2 * w] | ((uint32_t)(uint16_t)lane_init[2 * w + 1] << 16);
+            st16[w * 32] = av[w];
+        }
+        for (int kk = 0; kk < J; ++kk) {
+            const uint32_t r = rec[kk * 32];
+            const int g = (int)(r & 63u) + 1;
+            SAT_ASSERT(g >= 1 && g <= G && (int)((r >> 6) & 63u) < J);
+            SAT_ASSERT(rec_d || (int)(r >> 12) < c.n_opt);
+            const int gm = g - 1;
+            // slot g-1 = one half of word (g-1)/2 (read as the word: no type-punned loads)
+            const uint32_t selt = 0x4410u + (uint32_t)(gm & 1) * 0x22u;
+            int32_t t = (int32_t)__byte_perm(st16[(gm >> 1) * 32], 0u, selt);
+            if (has_release) t = max(t, (int32_t)release[(r >> 6) & 63u]);
+            const int32_t e = t + (int32_t)(r >> 12);
+            const uint32_t e2 = (uint32_t)e * 0x10001u;
+            const uint32_t sel = (g & 1) ? 0x5432u : 0x3210u;
+            const uint32_t *src = st16 + (g >> 1) * 32;
+            uint32_t w[G / 2 + 1];
+#pragma unroll
+            for (int k = 0; k <= G / 2; ++k) w[k] = src[k * 32];
+#pragma unroll
+            for (int k = 0; k < G / 2; ++k) {
+                const uint32_t s = __byte_perm(w[k], w[k + 1], sel);
+                av[k] = __vmaxu2(av[k], __vminu2(s, e2));
+                st16[k * 32] = av[k];
+            }
+            mx = tmax(mx, (T)e);
+        }
+    } else if constexpr (L == kLayoutOne) {
+        T av[G];
+#pragma unroll
+        for (int i = 0; i < G; ++i) {
+            av[i] = lane_init[i];
+            st[i * 32] = av[i];
+        }
+        for (int kk = 0; kk < J; ++kk) {
+            const uint32_t r = rec[kk * 32];
+            const int g = (int)(r & 63u) + 1;
+            SAT_ASSERT(g >= 1 && g <= G && (int)((r >> 6) & 63u) < J);
+            SAT_ASSERT(rec_d || (int)(r >> 12) < c.n_opt);
+            const T d = rec_d ? (T)(int32_t)(r >> 12) : dur[r >> 12];
+            T t = st[(g - 1) * 32];
+            if (has_release) t = tmax(t, release[(r >> 6) & 63u]);
+            const T e = t + d;
+            T s[G];
+#pragma unroll
+            for (int i = 0; i < G; ++i) s[i] = st[(i + g) * 32];
+#pragma unroll
+            for (int i = 0; i < G; ++i) {
+                av[i] = tmax(av[i], tmin(s[i], e));
+                st[i * 32] = av[i];
+            }
+            mx = tmax(mx, e);
+        }
+    } else if constexpr (M16) {
+        // per node n: words n*G .. n*G+G/2-1 = slots, n*G+G/2 .. n*G+G-1 = +inf.  Node pick:
+        // min over nodes of (start << 5 | n) = earliest start, lowest node on ties
+        // (durations are node-independent in this layout, so earliest start = earliest end).
+#pragma unroll
+        for (int n = 0; n < NMAX; ++n)
+            if (n < N)
+#pragma unroll
+                for (int w = 0; w < G / 2; ++w)
+                    st16[(n * G + w) * 32] = (uint32_t)(uint16_t)lane_init[n * G + 2 * w] |
+                                             ((uint32_t)(uint16_t)lane_init[n * G + 2 * w + 1] << 16);
+        for (int kk = 0; kk < J; ++kk) {
+            const uint32_t r = rec[kk * 32];
+            const int g = (int)(r & 63u) + 1;
+            SAT_ASSERT(g >= 1 && g <= G && (int)((r >> 6) & 63u) < J);
+            SAT_ASSERT(rec_d || (int)(r >> 12) < c.n_opt);
+            const int gm = g - 1;
+            const int32_t rel = has_release ? (int32_t)release[(r >> 6) & 63u] : 0;
+            const uint32_t selt = 0x4410u + (uint32_t)(gm & 1) * 0x22u;
+            uint32_t kb = 0xffffffffu;
+#pragma unroll
+            for (int n = 0; n < NMAX; ++n) {
+                if (n < N) {
+                    int32_t t = (int32_t)__byte_perm(st16[(n * G + (gm >> 1)) * 32], 0u, selt);
+                    t = max(t, rel);
+                    kb = min(kb, (uint32_t)t * 32u + (uint32_t)n);
+                }
+            }
+            const int bn = (int)(kb & 31u);
+            SAT_ASSERT(bn < N);
+            const int32_t e = (int32_t)(kb >> 5) + (int32_t)(r >> 12);
+            const uint32_t e2 = (uint32_t)e * 0x10001u;
+            const uint32_t sel = (g & 1) ? 0x5432u : 0x3210u;
+            uint32_t *nb = st16 + bn * G * 32;
+            const uint32_t *src = nb + (g >> 1) * 32;
+            uint32_t w[G / 2 + 1], cur[G / 2];
+#pragma unroll
+            for (int k = 0; k <= G / 2; ++k) w[k] = src[k * 32];
+#pragma unroll
+            for (int k = 0; k < G / 2; ++k) cur[k] = nb[k * 32];
+#pragma unroll
+            for (int k = 0; k < G / 2; ++k)
+                nb[k * 32] = __vmaxu2(cur[k], __vminu2(__byte_perm(w[k], w[k + 1], sel), e2));
+            mx = tmax(mx, (T)e);
+        }
+    } else {
+#pragma unroll
+        for (int n = 0; n < NMAX; ++n)
+            if (n < N)
+#pragma unroll
+                for (int i = 0; i < G; ++i) st[(n * 2 * G + i) * 32] = lane_init[n * G + i];
+        for (int kk = 0; kk < J; ++kk) {
+            const uint32_t r = rec[kk * 32];
+            const int g = (int)(r & 63u) + 1;
+            SAT_ASSERT(g >= 1 && g <= G && (int)((r >> 6) & 63u) < J);
+            SAT_ASSERT(rec_d || (int)(r >> 12) < c.n_opt);
+            const uint32_t pay = r >> 12;
+            const T rel = has_release ? release[(r >> 6) & 63u] : (T)0;
+            // node finishing the job earliest, lowest node on ties
+            T be = INF;
+            int bn = 0;
+#pragma unroll
+            for (int n = 0; n < NMAX; ++n) {
+                if (n < N) {
+                    T t = st[(n * 2 * G + g - 1) * 32];
+                    T d;
+                    if (rec_d) {
+                        d = (T)(int32_t)pay;
+                    } else {
+                        if (!((c.optmask[pay] >> n) & 1u)) t = INF;
+                        d = dur[pay * N + n];
+                    }
+                    t = tmax(t, rel);
+                    const T e = t + d;
+                    if (n == 0 || e < be) { be = e; bn = n; }
+                }
+            }
+            SAT_ASSERT(bn >= 0 && bn < N);
+            T *sb = st + bn * 2 * G * 32;
+            T cur[G], s[G];
+#pragma unroll
+            for (int i = 0; i < G; ++i) {
+                cur[i] = sb[i * 32];
+                s[i] = sb[(i + g) * 32];
+            }
+#pragma unroll
+            for (int i = 0; i < G; ++i) sb[i * 32] = tmax(cur[i], tmin(s[i], be));
+            mx = tmax(mx, be);
+        }
+    }
+    return mx;
+}
+
 template <typename T, int SRC, int G, int L>
 __global__ void __launch_bounds__(kCandThreads, SRC == SAT_SRC_INDEX ? 8 : (G <= 8 ? 12 : (G <= 16 ? 10 : 8)))
 k_cand(CandArgs a) {
     constexpr bool MULTI = L == kLayoutMulti;
     constexpr bool P16 = L == kLayoutOne16;
     constexpr bool M16 = L == kLayoutMulti16;
-    constexpr int NMAX = (MULTI || M16) ? (32 / G) : 1;     // nodes x padded GPUs fit a warp
     extern __shared__ __align__(16) uint8_t smem[];
     {
         const int nwords = (*reinterpret_cast<const BlobHeader *>(a.blob)).bytes / 16;
@@ -106,6 +291,7 @@ k_cand(CandArgs a) {
             for (int i = G; i < 2 * G; ++i) st[(n * 2 * G + i) * 32] = INF;
     }
     const T init_max = sizeof(T) == 4 ? (T)h.init_max_i32 : (T)h.init_max_f64;
+    SchedCtx<T> sc{st, st16, lane_init, release, dur, tb.optmask, J, N, h.n_opt, rec_d, has_release, init_max, INF};
 
     T best_ms = INF;
     uint64_t best_ix = ~0ull;
@@ -139,160 +325,7 @@ k_cand(CandArgs a) {
             } else {
                 decode_stream(a.seed + id, tb, rec);
             }
-            // ---- list schedule ----
-            T mx = init_max;
-            if constexpr (P16) {
-                // slots 2w (low half) and 2w+1 (high half) of word w; rows G/2..G-1 = +inf.
-                // Shift by the thread's g: word k of the shifted vector is word g/2 + k (g even)
-                // or the high half of word g/2 + k joined to the low half of the next (g odd):
-                // one PRMT with a per-thread selector either way.
-                uint32_t av[G / 2];
-#pragma unroll
-                for (int w = 0; w < G / 2; ++w) {
-                    av[w] = (uint32_t)(uint16_t)lane_init[2 * w] | ((uint32_t)(uint16_t)lane_init[2 * w + 1] << 16);
-                    st16[w * 32] = av[w];
-                }
-                for (int kk = 0; kk < J; ++kk) {
-                    const uint32_t r = rec[kk * 32];
-                    const int g = (int)(r & 63u) + 1;
-                    SAT_ASSERT(g >= 1 && g <= G && (int)((r >> 6) & 63u) < J);
-                    SAT_ASSERT(rec_d || (int)(r >> 12) < h.n_opt);
-                    const int gm = g - 1;
-                    // slot g-1 = one half of word (g-1)/2 (read as the word: no type-punned loads)
-                    const uint32_t selt = 0x4410u + (uint32_t)(gm & 1) * 0x22u;
-                    int32_t t = (int32_t)__byte_perm(st16[(gm >> 1) * 32], 0u, selt);
-                    if (has_release) t = max(t, (int32_t)release[(r >> 6) & 63u]);
-                    const int32_t e = t + (int32_t)(r >> 12);
-                    const uint32_t e2 = (uint32_t)e * 0x10001u;
-                    const uint32_t sel = (g & 1) ? 0x5432u : 0x3210u;
-                    const uint32_t *src = st16 + (g >> 1) * 32;
-                    uint32_t w[G / 2 + 1];
-#pragma unroll
-                    for (int k = 0; k <= G / 2; ++k) w[k] = src[k * 32];
-#pragma unroll
-                    for (int k = 0; k < G / 2; ++k) {
-                        const uint32_t s = __byte_perm(w[k], w[k + 1], sel);
-                        av[k] = __vmaxu2(av[k], __vminu2(s, e2));
-                        st16[k * 32] = av[k];
-                    }
-                    mx = tmax(mx, (T)e);
-                }
-            } else if constexpr (L == kLayoutOne) {
-                T av[G];
-#pragma unroll
-                for (int i = 0; i < G; ++i) {
-                    av[i] = lane_init[i];
-                    st[i * 32] = av[i];
-                }
-                for (int kk = 0; kk < J; ++kk) {
-                    const uint32_t r = rec[kk * 32];
-                    const int g = (int)(r & 63u) + 1;
-                    SAT_ASSERT(g >= 1 && g <= G && (int)((r >> 6) & 63u) < J);
-                    SAT_ASSERT(rec_d || (int)(r >> 12) < h.n_opt);
-                    const T d = rec_d ? (T)(int32_t)(r >> 12) : dur[r >> 12];
-                    T t = st[(g - 1) * 32];
-                    if (has_release) t = tmax(t, release[(r >> 6) & 63u]);
-                    const T e = t + d;
-                    T s[G];
-#pragma unroll
-                    for (int i = 0; i < G; ++i) s[i] = st[(i + g) * 32];
-#pragma unroll
-                    for (int i = 0; i < G; ++i) {
-                        av[i] = tmax(av[i], tmin(s[i], e));
-                        st[i * 32] = av[i];
-                    }
-                    mx = tmax(mx, e);
-                }
-            } else if constexpr (M16) {
-                // per node n: words n*G .. n*G+G/2-1 = slots, n*G+G/2 .. n*G+G-1 = +inf.  Node pick:
-                // min over nodes of (start << 5 | n) = earliest start, lowest node on ties
-                // (durations are node-independent in this layout, so earliest start = earliest end).
-#pragma unroll
-                for (int n = 0; n < NMAX; ++n)
-                    if (n < N)
-#pragma unroll
-                        for (int w = 0; w < G / 2; ++w)
-                            st16[(n * G + w) * 32] = (uint32_t)(uint16_t)lane_init[n * G + 2 * w] |
-                                                     ((uint32_t)(uint16_t)lane_init[n * G + 2 * w + 1] << 16);
-                for (int kk = 0; kk < J; ++kk) {
-                    const uint32_t r = rec[kk * 32];
-                    const int g = (int)(r & 63u) + 1;
-                    SAT_ASSERT(g >= 1 && g <= G && (int)((r >> 6) & 63u) < J);
-                    SAT_ASSERT(rec_d || (int)(r >> 12) < h.n_opt);
-                    const int gm = g - 1;
-                    const int32_t rel = has_release ? (int32_t)release[(r >> 6) & 63u] : 0;
-                    const uint32_t selt = 0x4410u + (uint32_t)(gm & 1) * 0x22u;
-                    uint32_t kb = 0xffffffffu;
-#pragma unroll
-                    for (int n = 0; n < NMAX; ++n) {
-                        if (n < N) {
-                            int32_t t = (int32_t)__byte_perm(st16[(n * G + (gm >> 1)) * 32], 0u, selt);
-                            t = max(t, rel);
-                            kb = min(kb, (uint32_t)t * 32u + (uint32_t)n);
-                        }
-                    }
-                    const int bn = (int)(kb & 31u);
-                    SAT_ASSERT(bn < N);
-                    const int32_t e = (int32_t)(kb >> 5) + (int32_t)(r >> 12);
-                    const uint32_t e2 = (uint32_t)e * 0x10001u;
-                    const uint32_t sel = (g & 1) ? 0x5432u : 0x3210u;
-                    uint32_t *nb = st16 + bn * G * 32;
-                    const uint32_t *src = nb + (g >> 1) * 32;
-                    uint32_t w[G / 2 + 1], cur[G / 2];
-#pragma unroll
-                    for (int k = 0; k <= G / 2; ++k) w[k] = src[k * 32];
-#pragma unroll
-                    for (int k = 0; k < G / 2; ++k) cur[k] = nb[k * 32];
-#pragma unroll
-                    for (int k = 0; k < G / 2; ++k)
-                        nb[k * 32] = __vmaxu2(cur[k], __vminu2(__byte_perm(w[k], w[k + 1], sel), e2));
-                    mx = tmax(mx, (T)e);
-                }
-            } else {
-#pragma unroll
-                for (int n = 0; n < NMAX; ++n)
-                    if (n < N)
-#pragma unroll
-                        for (int i = 0; i < G; ++i) st[(n * 2 * G + i) * 32] = lane_init[n * G + i];
-                for (int kk = 0; kk < J; ++kk) {
-                    const uint32_t r = rec[kk * 32];
-                    const int g = (int)(r & 63u) + 1;
-                    SAT_ASSERT(g >= 1 && g <= G && (int)((r >> 6) & 63u) < J);
-                    SAT_ASSERT(rec_d || (int)(r >> 12) < h.n_opt);
-                    const uint32_t pay = r >> 12;
-                    const T rel = has_release ? release[(r >> 6) & 63u] : (T)0;
-                    // node finishing the job earliest, lowest node on ties
-                    T be = INF;
-                    int bn = 0;
-#pragma unroll
-                    for (int n = 0; n < NMAX; ++n) {
-                        if (n < N) {
-                            T t = st[(n * 2 * G + g - 1) * 32];
-                            T d;
-                            if (rec_d) {
-                                d = (T)(int32_t)pay;
-                            } else {
-                                if (!((tb.optmask[pay] >> n) & 1u)) t = INF;
-                                d = dur[pay * N + n];
-                            }
-                            t = tmax(t, rel);
-                            const T e = t + d;
-                            if (n == 0 || e < be) { be = e; bn = n; }
-                        }
-                    }
-                    SAT_ASSERT(bn >= 0 && bn < N);
-                    T *sb = st + bn * 2 * G * 32;
-                    T cur[G], s[G];
-#pragma unroll
-                    for (int i = 0; i < G; ++i) {
-                        cur[i] = sb[i * 32];
-                        s[i] = sb[(i + g) * 32];
-                    }
-#pragma unroll
-                    for (int i = 0; i < G; ++i) sb[i * 32] = tmax(cur[i], tmin(s[i], be));
-                    mx = tmax(mx, be);
-                }
-            }
+            const T mx = schedule_records<T, G, L>(sc, rec);
             if (key_less(mx, id, best_ms, best_ix)) {
                 best_ms = mx;
                 best_ix = id;
