@@ -140,6 +140,16 @@ int sat_search_bnb(const sat_problem_t *p, int32_t prefix_len,
                    uint64_t task_lo, uint64_t task_hi,
                    sat_best_t *d_best, void *d_ws, size_t ws_bytes, void *stream);
 
+/* Local search from sampled starting points (grid time): walker w starts at candidate w of
+ * `source` (SAT_SRC_SUBSTREAM / SAT_SRC_SEED) and descends over swap / option / insertion
+ * moves on (makespan, total GPU load) until no move improves or max_rounds rounds of 32
+ * moves were scanned.  Result: (makespan << idx_bits) | walker.
+ * d_state_out (device, 2J bytes: options then order) receives the final candidate of walker
+ * lo when hi == lo + 1 -- the replay that decodes a winning walker. */
+int sat_local_search(const sat_problem_t *p, int32_t source, uint64_t seed, uint64_t lo, uint64_t hi,
+                     int32_t max_rounds, sat_best_t *d_best, uint8_t *d_state_out,
+                     void *d_ws, size_t ws_bytes, void *stream);
+
 /* Schedule n candidates and record the plan of each.
  *   source SAT_SRC_INDEX/SUBSTREAM/SEED: d_ids[n] candidate ids (seed used by streams)
  *   source SAT_SRC_EXPLICIT: d_explicit[n][2*J] = option digit per job, then order

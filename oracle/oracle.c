@@ -99,8 +99,10 @@ static void next_index(const oproblem *p, int *opt, int *ord) {
     }
 }
 
-/* list schedule one candidate; optional per-job start / node outputs */
-double oracle_eval(const oproblem *p, const int *opt, const int *ord, double *start, int *node_out) {
+/* list schedule one candidate; optional per-job start / node outputs; *load_out (optional) =
+ * sum of the final free times of every GPU (the local search's tie-breaking objective) */
+static double eval_full(const oproblem *p, const int *opt, const int *ord, double *start, int *node_out,
+                        double *load_out) {
     double free_t[OMAX_N][OMAX_G];
     for (int n = 0; n < p->N; ++n)
         for (int k = 0; k < p->node_gpus[n]; ++k)
@@ -141,11 +143,18 @@ double oracle_eval(const oproblem *p, const int *opt, const int *ord, double *st
         if (start) start[j] = best_t;
         if (node_out) node_out[j] = best_n;
     }
-    double ms = 0.0;
+    double ms = 0.0, load = 0.0;
     for (int n = 0; n < p->N; ++n)
-        for (int k = 0; k < p->node_gpus[n]; ++k)
+        for (int k = 0; k < p->node_gpus[n]; ++k) {
             if (free_t[n][k] > ms) ms = free_t[n][k];
+            load += free_t[n][k];
+        }
+    if (load_out) *load_out = load;
     return ms;
+}
+
+double oracle_eval(const oproblem *p, const int *opt, const int *ord, double *start, int *node_out) {
+    return eval_full(p, opt, ord, start, node_out, NULL);
 }
 
 /* source: 0 index, 1 substream(seed, id), 2 SplitMix64(seed + id) */
@@ -207,5 +216,108 @@ int oracle_decode(const oproblem *p, int source, uint64_t seed, uint64_t id, int
     if (source == 0) decode_index(p, id, opt, ord);
     else if (source == 1) decode_stream(p, mix((seed ^ id) + GOLD), opt, ord);
     else decode_stream(p, seed + id, opt, ord);
+    return 0;
+}
+
+/* ---------------------------------------------------------------- local search
+ * Same semantics as the engine's sat_local_search, restated with the
+ * literal per-GPU list scheduler above:
+ *   start: candidate `walker` of the stream (source 1 substream / 2 seed)
+ *   moves, in this order:  [0, M1)       swap positions (a, b), a < b, lexicographic
+ *                          [M1, M1+M2)   job j takes option o' != opt[j] (j, then o' ascending)
+ *                          [M1+M2, M)    the job at position a moves to position b != a
+ *                                        (a ascending, then b ascending)
+ *   objective: (makespan, load) lexicographic, load = sum of the final free times of every
+ *   GPU (it breaks the plateaus where several jobs pin the makespan)
+ *   a round = 32 consecutive move ids; rounds are scanned from move 0; the first round
+ *   holding a move with objective < current applies its best move (lowest objective, then
+ *   lowest id) and the scan restarts at 0; a scan without improvement, or max_rounds
+ *   rounds in total, ends the walk. */
+static int ls_counts(const oproblem *p, int *M1, int *M2) {
+    int J = p->J, m2 = 0;
+    for (int j = 0; j < J; ++j) m2 += p->radix[j] - 1;
+    *M1 = J * (J - 1) / 2;
+    *M2 = m2;
+    return *M1 + m2 + J * (J - 1);
+}
+
+static void ls_neighbor(const oproblem *p, int m, int M1, int M2, const int *opt, const int *ord, int *nopt,
+                        int *nord) {
+    int J = p->J;
+    memcpy(nopt, opt, sizeof(int) * (size_t)J);
+    memcpy(nord, ord, sizeof(int) * (size_t)J);
+    if (m < M1) {
+        int a = 0, rest = m;
+        while (rest >= J - 1 - a) { rest -= J - 1 - a; ++a; }
+        int b = a + 1 + rest;
+        int t = nord[a]; nord[a] = nord[b]; nord[b] = t;
+    } else if (m < M1 + M2) {
+        int rest = m - M1, j = 0;
+        while (rest >= p->radix[j] - 1) { rest -= p->radix[j] - 1; ++j; }
+        nopt[j] = rest < opt[j] ? rest : rest + 1;
+    } else {
+        int rest = m - M1 - M2;
+        int a = rest / (J - 1), bi = rest % (J - 1);
+        int b = bi < a ? bi : bi + 1;
+        int x = nord[a];
+        if (a < b) memmove(nord + a, nord + a + 1, sizeof(int) * (size_t)(b - a));
+        else memmove(nord + b + 1, nord + b, sizeof(int) * (size_t)(a - b));
+        nord[b] = x;
+    }
+}
+
+double oracle_local_search(const oproblem *p, int source, uint64_t seed, uint64_t walker, int max_rounds,
+                           int *opt, int *ord, int *rounds_out) {
+    int M1, M2;
+    int M = ls_counts(p, &M1, &M2);
+    if (source == 1) decode_stream(p, mix((seed ^ walker) + GOLD), opt, ord);
+    else decode_stream(p, seed + walker, opt, ord);
+    double cur_load;
+    double cur = eval_full(p, opt, ord, NULL, NULL, &cur_load);
+    int rounds = 0, nopt[OMAX_J], nord[OMAX_J];
+    for (;;) {
+        int improved = 0;
+        for (int r0 = 0; r0 < M && rounds < max_rounds; r0 += 32, ++rounds) {
+            double bms = INFINITY, bload = INFINITY;
+            int bm = -1;
+            for (int m = r0; m < r0 + 32 && m < M; ++m) {
+                ls_neighbor(p, m, M1, M2, opt, ord, nopt, nord);
+                double load;
+                double ms = eval_full(p, nopt, nord, NULL, NULL, &load);
+                if (ms < bms || (ms == bms && load < bload)) { bms = ms; bload = load; bm = m; }
+            }
+            if (bms < cur || (bms == cur && bload < cur_load)) {
+                ls_neighbor(p, bm, M1, M2, opt, ord, nopt, nord);
+                memcpy(opt, nopt, sizeof(int) * (size_t)p->J);
+                memcpy(ord, nord, sizeof(int) * (size_t)p->J);
+                cur = bms;
+                cur_load = bload;
+                improved = 1;
+                ++rounds;
+                break;
+            }
+        }
+        if (!improved || rounds >= max_rounds) break;
+    }
+    if (rounds_out) *rounds_out = rounds;
+    return cur;
+}
+
+int oracle_ls_search(const oproblem *p, int source, uint64_t seed, uint64_t lo, uint64_t hi, int max_rounds,
+                     int threads, double *best_ms, uint64_t *best_id) {
+    double gms = INFINITY;
+    uint64_t gid = UINT64_MAX;
+    if (threads < 1) threads = omp_get_max_threads();
+#pragma omp parallel for schedule(dynamic, 1) num_threads(threads)
+    for (long long w = (long long)lo; w < (long long)hi; ++w) {
+        int opt[OMAX_J], ord[OMAX_J];
+        double ms = oracle_local_search(p, source, seed, (uint64_t)w, max_rounds, opt, ord, NULL);
+#pragma omp critical
+        {
+            if (ms < gms || (ms == gms && (uint64_t)w < gid)) { gms = ms; gid = (uint64_t)w; }
+        }
+    }
+    *best_ms = gms;
+    *best_id = gid;
     return 0;
 }

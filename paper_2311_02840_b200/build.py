@@ -55,7 +55,8 @@ def units(obj_dir: str = OBJ_DIR) -> list:
     out = [(os.path.join(CSRC, "sat_engine.cu"), [], os.path.join(OBJ_DIR, "sat_engine.o"))]
     for t in ("int32_t", "double"):
         for s in ("SAT_SRC_INDEX", "SAT_SRC_SUBSTREAM", "SAT_SRC_SEED"):
-            out.append((os.path.join(CSRC, "sat_cand.cu"), [f"-DSAT_CAND_T={t}", f"-DSAT_CAND_SRC={s}"],
+            ls = ["-DSAT_LS_INSTANTIATE"] if t == "int32_t" and s != "SAT_SRC_INDEX" else []
+            out.append((os.path.join(CSRC, "sat_cand.cu"), [f"-DSAT_CAND_T={t}", f"-DSAT_CAND_SRC={s}", *ls],
                         os.path.join(OBJ_DIR, f"sat_cand_{t}_{s.split('_')[-1].lower()}.o")))
     for lo, hi in TREE_RANGES:
         out.append((os.path.join(CSRC, "sat_tree_g.cu"), [f"-DSAT_G_LO={lo}", f"-DSAT_G_HI={hi}"],

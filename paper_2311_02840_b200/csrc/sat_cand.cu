@@ -98,4 +98,81 @@ int launch_cand(const sat_problem_t *p, CandArgs a, uint64_t n_cand, void *d_ws,
 template int launch_cand<SAT_CAND_T, SAT_CAND_SRC>(const sat_problem_t *, CandArgs, uint64_t, void *, size_t,
                                                    cudaStream_t);
 
+// ---------------------------------------------------------------- local search
+template <int SRC, int G, int L>
+static int launch_ls_g(const sat_problem_t *p, LsArgs a, const std::vector<uint8_t> &blob, void *d_ws,
+                       size_t ws_bytes, cudaStream_t stream) {
+    const size_t blob_bytes = blob.size();
+    const int N = (L == kLayoutMulti || L == kLayoutMulti16) ? p->N : 1;
+    const int smem = (int)blob_bytes + kCandWarps * ls_warp_bytes(p->J, N, G, cand_slot_bytes<int32_t, L>());
+    if (smem > 220 * 1024) return SAT_ERR_TOO_LARGE;
+    auto kern = k_ls<SRC, G, L>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+        return SAT_ERR_CUDA;
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kCandThreads, smem) != cudaSuccess ||
+        per_sm < 1)
+        per_sm = 1;
+    uint64_t blocks = (uint64_t)device_sms() * (uint64_t)per_sm;
+    const uint64_t need = (a.hi - a.lo + kCandWarps - 1) / kCandWarps;
+    if (blocks > need) blocks = std::max<uint64_t>(1, need);
+    const size_t cur_off = (blob_bytes + 255) & ~(size_t)255;
+    if (!d_ws || ws_bytes < cur_off + sizeof(unsigned long long)) return SAT_ERR_INVALID;
+    uint8_t *ws = static_cast<uint8_t *>(d_ws);
+    if (cudaMemcpyAsync(ws, blob.data(), blob_bytes, cudaMemcpyHostToDevice, stream) != cudaSuccess)
+        return SAT_ERR_CUDA;
+    if (cudaMemsetAsync(ws + cur_off, 0, sizeof(unsigned long long), stream) != cudaSuccess) return SAT_ERR_CUDA;
+    a.blob = ws;
+    a.cursor = reinterpret_cast<unsigned long long *>(ws + cur_off);
+    kern<<<(unsigned)blocks, kCandThreads, smem, stream>>>(a);
+    return cudaGetLastError() == cudaSuccess ? SAT_OK : SAT_ERR_CUDA;
+}
+
+template <int SRC>
+int launch_ls(const sat_problem_t *p, LsArgs a, void *d_ws, size_t ws_bytes, cudaStream_t stream) {
+    if (p->time_mode != SAT_TIME_GRID_I32) return SAT_ERR_UNSUPPORTED;
+    a.rec_d = records_carry_duration(p) ? 1 : 0;
+    std::vector<uint8_t> blob;
+    int st = pack_blob(p, blob, a.rec_d != 0);
+    if (st) return st;
+    const bool multi = p->N > 1;
+    bool p16 = false;
+    if (a.rec_d && p->G >= 2) {
+        int64_t bound = 0, rel = 0, init = 0;
+        for (int j = 0; j < p->J; ++j) {
+            int32_t dm = 0;
+            for (int o = 0; o < p->radix[j]; ++o) dm = std::max(dm, p->dur_i32[(j * p->Cmax + o) * p->N]);
+            bound += dm;
+            if (p->release_i32) rel = std::max<int64_t>(rel, p->release_i32[j]);
+        }
+        for (int n = 0; n < p->N; ++n)
+            for (int i = 0; i < p->node_gpus[n]; ++i)
+                if (p->init_free_i32) init = std::max<int64_t>(init, p->init_free_i32[n * p->G + i]);
+        p16 = bound + rel + init < 0xffff;
+    }
+    switch (p->G) {
+#define SAT_LCASE(K)                                                                                   \
+    case K:                                                                                            \
+        if (multi && K >= 2 && p16)                                                                    \
+            return launch_ls_g<SRC, (K <= 16 ? (K >= 2 ? K : 2) : 16), kLayoutMulti16>(p, a, blob, d_ws, ws_bytes, stream); \
+        if (multi)                                                                                     \
+            return launch_ls_g<SRC, (K <= 16 ? K : 16), kLayoutMulti>(p, a, blob, d_ws, ws_bytes, stream); \
+        if (K >= 2 && p16)                                                                             \
+            return launch_ls_g<SRC, (K >= 2 ? K : 2), kLayoutOne16>(p, a, blob, d_ws, ws_bytes, stream); \
+        return launch_ls_g<SRC, K, kLayoutOne>(p, a, blob, d_ws, ws_bytes, stream);
+        SAT_LCASE(1) SAT_LCASE(2) SAT_LCASE(4) SAT_LCASE(8) SAT_LCASE(16) SAT_LCASE(32)
+#undef SAT_LCASE
+        default: return SAT_ERR_UNSUPPORTED;
+    }
+}
+
+
+
 }  // namespace sat
+
+// the local search runs in grid time only: instantiate it in the int32 translation units
+#if defined(SAT_LS_INSTANTIATE)
+namespace sat {
+template int launch_ls<SAT_CAND_SRC>(const sat_problem_t *, LsArgs, void *, size_t, cudaStream_t);
+}
+#endif

@@ -75,8 +75,9 @@ struct SchedCtx {
 
 // List-schedule the J step records in the lane's record column (stride 32) and return the
 // makespan.  Layout L as in the file comment; G = padded GPUs per node.
-template <typename T, int G, int L>
-__device__ __forceinline__ T schedule_records(const SchedCtx<T> &c, const uint32_t *rec) {
+template <typename T, int G, int L, bool LOAD = false>
+__device__ __forceinline__ T schedule_records(const SchedCtx<T> &c, const uint32_t *rec,
+                                             uint64_t *load = nullptr) {
     constexpr bool P16 = L == kLayoutOne16;
     constexpr bool M16 = L == kLayoutMulti16;
     constexpr int NMAX = (L == kLayoutMulti || M16) ? (32 / G) : 1;
@@ -126,6 +127,15 @@ __device__ __forceinline__ T schedule_records(const SchedCtx<T> &c, const uint32
             }
             mx = tmax(mx, (T)e);
         }
+        if constexpr (LOAD) {
+            uint64_t sum = 0;
+#pragma unroll
+            for (int w = 0; w < G / 2; ++w) {
+                const uint32_t lo = av[w] & 0xffffu, hi = av[w] >> 16;
+                sum += (lo != 0xffffu ? lo : 0u) + (hi != 0xffffu ? hi : 0u);
+            }
+            *load = sum;
+        }
     } else if constexpr (L == kLayoutOne) {
         T av[G];
 #pragma unroll
@@ -151,6 +161,12 @@ __device__ __forceinline__ T schedule_records(const SchedCtx<T> &c, const uint32
                 st[i * 32] = av[i];
             }
             mx = tmax(mx, e);
+        }
+        if constexpr (LOAD) {
+            uint64_t sum = 0;
+#pragma unroll
+            for (int i = 0; i < G; ++i) sum += (av[i] != INF) ? (uint64_t)(int64_t)av[i] : 0ull;
+            *load = sum;
         }
     } else if constexpr (M16) {
         // per node n: words n*G .. n*G+G/2-1 = slots, n*G+G/2 .. n*G+G-1 = +inf.  Node pick:
@@ -197,6 +213,19 @@ __device__ __forceinline__ T schedule_records(const SchedCtx<T> &c, const uint32
                 nb[k * 32] = __vmaxu2(cur[k], __vminu2(__byte_perm(w[k], w[k + 1], sel), e2));
             mx = tmax(mx, (T)e);
         }
+        if constexpr (LOAD) {
+            uint64_t sum = 0;
+#pragma unroll
+            for (int n = 0; n < NMAX; ++n)
+                if (n < N)
+#pragma unroll
+                    for (int w = 0; w < G / 2; ++w) {
+                        const uint32_t v = st16[(n * G + w) * 32];
+                        const uint32_t lo = v & 0xffffu, hi = v >> 16;
+                        sum += (lo != 0xffffu ? lo : 0u) + (hi != 0xffffu ? hi : 0u);
+                    }
+            *load = sum;
+        }
     } else {
 #pragma unroll
         for (int n = 0; n < NMAX; ++n)
@@ -240,6 +269,18 @@ __device__ __forceinline__ T schedule_records(const SchedCtx<T> &c, const uint32
 #pragma unroll
             for (int i = 0; i < G; ++i) sb[i * 32] = tmax(cur[i], tmin(s[i], be));
             mx = tmax(mx, be);
+        }
+        if constexpr (LOAD) {
+            uint64_t sum = 0;
+#pragma unroll
+            for (int n = 0; n < NMAX; ++n)
+                if (n < N)
+#pragma unroll
+                    for (int i = 0; i < G; ++i) {
+                        const T v = st[(n * 2 * G + i) * 32];
+                        sum += (v != INF) ? (uint64_t)(int64_t)v : 0ull;
+                    }
+            *load = sum;
         }
     }
     return mx;
@@ -357,6 +398,204 @@ k_cand(CandArgs a) {
         }
     }
 }
+
+// ---------------------------------------------------------------------------
+// k_ls: local search from sampled starting points (one walker per warp, one move per lane)
+// ---------------------------------------------------------------------------
+// Walker w starts at candidate w of the stream (the sampled search's candidate w) and
+// descends: moves in a fixed order -- [0, M1) swap positions a < b; [M1, M1+M2) job j takes
+// option o' != its own; [M1+M2, M) the job at position a moves to position b -- are scanned
+// 32 at a time (a lane per move, each scheduled to its makespan and load = sum of the final
+// GPU free times); the first round holding an improvement of (makespan, load) applies its
+// best move (lowest objective, then lowest move id) and the scan restarts at move 0.  A
+// full scan without improvement, or max_rounds rounds, ends the walk; the walker's result
+// is (makespan, w).  oracle/oracle.c restates the same walk with its per-GPU scheduler.
+struct LsArgs {
+    const uint8_t *blob;
+    uint64_t lo, hi;            // walkers [lo, hi)
+    uint64_t seed;
+    int32_t max_rounds;
+    int32_t rec_d;
+    sat_best_t *best;
+    unsigned long long *cursor;
+    uint8_t *state_out;         // [2J] final options then order of walker lo (hi == lo + 1), or null
+};
+
+__host__ __device__ inline int ls_warp_bytes(int J, int N, int G, int slot_bytes) {
+    return cand_warp_bytes(J, N, G, slot_bytes, false) + 128;        // + the walker's options / order
+}
+
+// neighbour of (opt, ord) under move m: source position of position k, and the option override
+struct LsMove {
+    int kind;      // 0 swap, 1 option, 2 insertion
+    int a, b;      // positions (swap / insertion) or (job, option) for kind 1
+};
+
+__device__ __forceinline__ LsMove ls_decode_move(int m, int J, int M1, int M2, const int32_t *radix,
+                                                 const uint8_t *wopt) {
+    LsMove mv;
+    if (m < M1) {
+        int a = 0, rest = m;
+        while (rest >= J - 1 - a) { rest -= J - 1 - a; ++a; }
+        mv.kind = 0; mv.a = a; mv.b = a + 1 + rest;
+    } else if (m < M1 + M2) {
+        int rest = m - M1, j = 0;
+        while (rest >= radix[j] - 1) { rest -= radix[j] - 1; ++j; }
+        mv.kind = 1; mv.a = j; mv.b = rest < (int)wopt[j] ? rest : rest + 1;
+    } else {
+        const int rest = m - M1 - M2;
+        const int a = rest / (J - 1), bi = rest - a * (J - 1);
+        mv.kind = 2; mv.a = a; mv.b = bi < a ? bi : bi + 1;
+    }
+    return mv;
+}
+
+__device__ __forceinline__ int ls_src(const LsMove &mv, int k) {
+    if (mv.kind == 0) return k == mv.a ? mv.b : (k == mv.b ? mv.a : k);
+    if (mv.kind == 1) return k;
+    if (mv.a < mv.b) return (k < mv.a || k > mv.b) ? k : (k == mv.b ? mv.a : k + 1);
+    return (k < mv.b || k > mv.a) ? k : (k == mv.b ? mv.a : k - 1);
+}
+
+template <int SRC, int G, int L>
+__global__ void __launch_bounds__(kCandThreads)
+k_ls(LsArgs a) {
+    using T = int32_t;
+    extern __shared__ __align__(16) uint8_t smem[];
+    {
+        const int nwords = (*reinterpret_cast<const BlobHeader *>(a.blob)).bytes / 16;
+        const int4 *src = reinterpret_cast<const int4 *>(a.blob);
+        int4 *dst = reinterpret_cast<int4 *>(smem);
+        for (int i = threadIdx.x; i < nwords; i += blockDim.x) dst[i] = src[i];
+    }
+    __syncthreads();
+    const BlobHeader &h = *reinterpret_cast<const BlobHeader *>(smem);
+    const int J = h.J;
+    const int N = (L == kLayoutMulti || L == kLayoutMulti16) ? h.N : 1;
+    GenTables tb;
+    load_tables(tb, smem, h);
+    const T *dur = reinterpret_cast<const T *>(smem + h.off_dur);
+    const T *release = reinterpret_cast<const T *>(smem + h.off_release);
+    const T *lane_init = reinterpret_cast<const T *>(smem + h.off_lane_init);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint8_t *wbase = smem + h.bytes + warp * ls_warp_bytes(J, N, G, cand_slot_bytes<T, L>());
+    uint32_t *rec = reinterpret_cast<uint32_t *>(wbase) + lane;
+    T *st = reinterpret_cast<T *>(wbase + J * 128) + lane;
+    uint32_t *st16 = reinterpret_cast<uint32_t *>(st);
+    uint8_t *wopt = wbase + cand_warp_bytes(J, N, G, cand_slot_bytes<T, L>(), false);   // [64]
+    uint8_t *word = wopt + 64;                                                           // [64]
+    const T INF = SAT_INF_I32;
+    if constexpr (L == kLayoutOne16 || L == kLayoutMulti16) {
+        for (int n = 0; n < N; ++n)
+            for (int w = G / 2; w < G; ++w) st16[(n * G + w) * 32] = 0xffffffffu;
+    } else {
+        for (int n = 0; n < N; ++n)
+            for (int i = G; i < 2 * G; ++i) st[(n * 2 * G + i) * 32] = INF;
+    }
+    SchedCtx<T> sc{st, st16, lane_init, release, dur, tb.optmask, J, N, h.n_opt, a.rec_d != 0,
+                   h.has_release != 0, (T)h.init_max_i32, INF};
+    int M2 = 0;
+    for (int j = 0; j < J; ++j) M2 += tb.radix[j] - 1;
+    const int M1 = J * (J - 1) / 2, M = M1 + M2 + J * (J - 1);
+
+    T best_ms = INF;
+    uint64_t best_ix = ~0ull;
+    const uint64_t total = a.hi - a.lo;
+    auto next_walker = [&]() -> uint64_t {
+        unsigned long long v = 0;
+        if (lane == 0) v = atomicAdd(a.cursor, 1ull);
+        return __shfl_sync(0xffffffffu, v, 0);
+    };
+    for (uint64_t wk = next_walker(); wk < total; wk = next_walker()) {
+        const uint64_t id = a.lo + wk;
+        if (lane == 0) {       // the walker's start: candidate id of the stream (plan_random's draw order)
+            Stream s{SRC == SAT_SRC_SUBSTREAM ? mix64((a.seed ^ id) + kGolden) : a.seed + id};
+            for (int j = 0; j < J; ++j) wopt[j] = (uint8_t)s.below((uint32_t)tb.radix[j], tb.mods);
+            for (int k = 0; k < J; ++k) word[k] = (uint8_t)k;
+            for (int i = J - 1; i >= 1; --i) {
+                const int k = (int)s.below((uint32_t)(i + 1), tb.mods);
+                const uint8_t t = word[i]; word[i] = word[k]; word[k] = t;
+            }
+        }
+        __syncwarp();
+        // objective of the start (every lane, identical)
+        for (int k = 0; k < J; ++k) { const int job = word[k]; rec[k * 32] = rec_for(tb, job, wopt[job]); }
+        uint64_t load = 0;
+        T cur = schedule_records<T, G, L, true>(sc, rec, &load);
+        uint64_t cur_key = ((uint64_t)(uint32_t)cur << 34) | load;
+        int rounds = 0;
+        for (;;) {
+            bool improved = false;
+            for (int r0 = 0; r0 < M && rounds < a.max_rounds; r0 += 32, ++rounds) {
+                const int m = r0 + lane;
+                uint64_t key = ~0ull;
+                if (m < M) {
+                    const LsMove mv = ls_decode_move(m, J, M1, M2, tb.radix, wopt);
+                    for (int k = 0; k < J; ++k) {
+                        const int job = word[ls_src(mv, k)];
+                        const int o = (mv.kind == 1 && job == mv.a) ? mv.b : (int)wopt[job];
+                        rec[k * 32] = rec_for(tb, job, o);
+                    }
+                    uint64_t ld = 0;
+                    const T ms = schedule_records<T, G, L, true>(sc, rec, &ld);
+                    key = ((uint64_t)(uint32_t)ms << 34) | ld;
+                }
+                // warp argmin of (objective, move id)
+                uint64_t bk = key;
+                int bm = m;
+                for (int x = 16; x >= 1; x >>= 1) {
+                    const uint64_t ok = shfl_u64(bk, lane ^ x);
+                    const int om = __shfl_xor_sync(0xffffffffu, bm, x);
+                    if (ok < bk || (ok == bk && om < bm)) { bk = ok; bm = om; }
+                }
+                if (bk < cur_key) {
+                    if (lane == 0) {
+                        const LsMove mv = ls_decode_move(bm, J, M1, M2, tb.radix, wopt);
+                        if (mv.kind == 0) {
+                            const uint8_t t = word[mv.a]; word[mv.a] = word[mv.b]; word[mv.b] = t;
+                        } else if (mv.kind == 1) {
+                            wopt[mv.a] = (uint8_t)mv.b;
+                        } else {
+                            const uint8_t x = word[mv.a];
+                            if (mv.a < mv.b) for (int k = mv.a; k < mv.b; ++k) word[k] = word[k + 1];
+                            else for (int k = mv.a; k > mv.b; --k) word[k] = word[k - 1];
+                            word[mv.b] = x;
+                        }
+                    }
+                    __syncwarp();
+                    cur_key = bk;
+                    cur = (T)(bk >> 34);
+                    improved = true;
+                    ++rounds;
+                    break;
+                }
+            }
+            if (!improved || rounds >= a.max_rounds) break;
+        }
+        if (lane == 0 && key_less(cur, id, best_ms, best_ix)) { best_ms = cur; best_ix = id; }
+        if (a.state_out && total == 1 && lane == 0) {
+            for (int j = 0; j < J; ++j) a.state_out[j] = wopt[j];
+            for (int k = 0; k < J; ++k) a.state_out[J + k] = word[k];
+        }
+        __syncwarp();
+    }
+    // ---- warp -> block -> grid argmin (lane 0 holds each warp's best) ----
+    __shared__ T s_ms[kCandWarps];
+    __shared__ uint64_t s_ix[kCandWarps];
+    if (lane == 0) { s_ms[warp] = best_ms; s_ix[warp] = best_ix; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < kCandWarps; ++w)
+            if (key_less(s_ms[w], s_ix[w], best_ms, best_ix)) { best_ms = s_ms[w]; best_ix = s_ix[w]; }
+        if (best_ms < INF) {
+            const uint64_t key = ((uint64_t)(uint32_t)best_ms << h.idx_bits) | best_ix;
+            atomicMin(reinterpret_cast<unsigned long long *>(&a.best->hi), (unsigned long long)key);
+        }
+    }
+}
+
+template <int SRC>
+int launch_ls(const sat_problem_t *p, LsArgs a, void *d_ws, size_t ws_bytes, cudaStream_t stream);
 
 // host launcher for one (T, SRC) pair; dispatches on the padded node size and layout
 template <typename T, int SRC>

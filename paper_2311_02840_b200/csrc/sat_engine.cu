@@ -740,6 +740,25 @@ static int search_tree_impl(const sat_problem_t *p, int32_t prefix_len, uint64_t
 
 size_t sat_tree_param_bytes(void) { return sizeof(TreeParams); }
 
+int sat_local_search(const sat_problem_t *p, int32_t source, uint64_t seed, uint64_t lo, uint64_t hi,
+                     int32_t max_rounds, sat_best_t *d_best, uint8_t *d_state_out, void *d_ws, size_t ws_bytes,
+                     void *stream) {
+    int st = validate(p);
+    if (st) return st;
+    if (!d_best || hi < lo || max_rounds < 0) return SAT_ERR_INVALID;
+    if (source != SAT_SRC_SUBSTREAM && source != SAT_SRC_SEED) return SAT_ERR_INVALID;
+    if (p->time_mode != SAT_TIME_GRID_I32) return SAT_ERR_UNSUPPORTED;
+    if (p->J < 2) return SAT_ERR_UNSUPPORTED;
+    if (hi > 0 && ((hi - 1) >> p->idx_bits)) return SAT_ERR_TOO_LARGE;
+    if (d_state_out && hi - lo != 1) return SAT_ERR_INVALID;
+    if (hi == lo) return SAT_OK;
+    LsArgs a{};
+    a.lo = lo; a.hi = hi; a.seed = seed; a.max_rounds = max_rounds; a.best = d_best; a.state_out = d_state_out;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (source == SAT_SRC_SUBSTREAM) return launch_ls<SAT_SRC_SUBSTREAM>(p, a, d_ws, ws_bytes, s);
+    return launch_ls<SAT_SRC_SEED>(p, a, d_ws, ws_bytes, s);
+}
+
 int sat_search_tree(const sat_problem_t *p, int32_t prefix_len, uint64_t task_lo, uint64_t task_hi,
                     sat_best_t *d_best, void *d_ws, size_t ws_bytes, void *stream) {
     return search_tree_impl(p, prefix_len, task_lo, task_hi, d_best, d_ws, ws_bytes, stream, false);

@@ -63,6 +63,7 @@ _SIGS = {
                       ctypes.c_size_t, _vp], _i32),
     "sat_alu_probe": ([_i32, _i32, _i32, _vp, _vp, _vp], _i32),
     "sat_tree_param_bytes": ([], ctypes.c_size_t),
+    "sat_local_search": ([_vp, _i32, _u64, _u64, _u64, _i32, _vp, _vp, _vp, ctypes.c_size_t, _vp], _i32),
 }
 
 _LIB = None
@@ -250,6 +251,27 @@ class Engine:
         best[0:1].copy_(torch.minimum(key, torch.where(best[0:1] == -1, torch.full_like(key, INT64_MAX),
                                                        best[0:1])))
 
+    def local_search(self, nprob, source, seed, lo, hi, max_rounds: int = 4096, best=None, state_out=None):
+        """Walkers [lo, hi) of the local search; state_out (uint8 device tensor, 2J) receives the
+        final (options, order) of walker lo when hi == lo + 1."""
+        best = self._best if best is None else best
+        ws, wsb = self.workspace(nprob)
+        self._check(self.lib.sat_local_search(nprob.ref, source, seed & ((1 << 64) - 1), lo, hi, max_rounds,
+                                              _vp(best.data_ptr()),
+                                              _vp(state_out.data_ptr()) if state_out is not None else None,
+                                              _vp(ws), wsb, _vp(self.stream())), what="sat_local_search")
+        self.launches += 1
+
+    def local_search_state(self, nprob, source, seed, walker, max_rounds: int = 4096):
+        """Replay one walker: its final (options, order) as lists."""
+        torch = self.torch
+        J = nprob.struct.J
+        out = torch.zeros(2 * J, dtype=torch.uint8, device=self.device)
+        tmp = self.reset_best(torch.empty(2, dtype=torch.int64, device=self.device))
+        self.local_search(nprob, source, seed, walker, walker + 1, max_rounds, tmp, out)
+        v = out.cpu().tolist()
+        return v[:J], v[J:]
+
     def search_index(self, nprob, lo, hi, best=None):
         best = self._best if best is None else best
         ws, wsb = self.workspace(nprob)
@@ -322,6 +344,8 @@ class Engine:
             if space > (1 << 62):
                 raise E.errors_for(prob.jobs[0]).TooLarge(f"exhaustive space {space} exceeds 2^62")
             return mode, space
+        if mode == "local":
+            return mode, int(opts.walkers)
         return mode, int(opts.budget)
 
     def search(self, prob: SearchProblem, opts: SolveOptions, group=None, source: int | None = None,
@@ -364,6 +388,12 @@ class Engine:
                 self.search_index(nprob, a, b, best)
                 kernel, evaluated = "index", n_idx
             seed_used = 0
+        elif mode == "local":
+            src = SRC_SUBSTREAM if source is None else source
+            seed_used = opts.seed if seed is None else seed
+            a, b = _shard(n_idx, rank, world)
+            self.local_search(nprob, src, seed_used, a, b, opts.max_rounds, best)
+            kernel, evaluated = "local", n_idx
         else:
             src = SRC_SUBSTREAM if source is None else source
             seed_used = opts.seed if seed is None else seed

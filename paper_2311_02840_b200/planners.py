@@ -83,7 +83,7 @@ class Solution:
     """A plan plus how it was found (the reference's MilpSolution analogue)."""
 
     plan: object
-    status: str                 # "Optimal" (whole space scanned) or "Sampled"
+    status: str                 # "Optimal" (space exhausted or proven), "Sampled" or "Local" (heuristic)
     makespan: float             # grid intervals or seconds
     objective: float            # seconds (= plan.predicted_makespan)
     problem: SearchProblem
@@ -133,8 +133,15 @@ def solve_problem(prob: SearchProblem, workload, opts: SolveOptions, running_con
         res = eng.search(prob, opts, group=group)
         idx_bits, _ = prob.key_bits(res.evaluated if not res.exhaustive else prob.space)
         nprob = NativeProblem(prob, idx_bits)
-        src = SRC_INDEX if res.exhaustive else res.source
-        plan, options, ms, runtimes = _decode(eng, prob, nprob, workload, src, res.seed, ident=res.index)
+        if res.kernel == "local":
+            # replay the winning walker to get its final candidate, then schedule it explicitly
+            o_, r_ = eng.local_search_state(nprob, res.source, res.seed, res.index, opts.max_rounds)
+            explicit = np.array(list(o_) + list(r_), dtype=np.uint8)
+            plan, options, ms, runtimes = _decode(eng, prob, NativeProblem(prob, 62), workload, SRC_EXPLICIT, 0,
+                                                  explicit=explicit)
+        else:
+            src = SRC_INDEX if res.exhaustive else res.source
+            plan, options, ms, runtimes = _decode(eng, prob, nprob, workload, src, res.seed, ident=res.index)
     except E.SchedulerError:
         raise
     except Exception as exc:  # CUDA / NCCL trouble -> PlanFailure (ReplanFailure on re-solve)
@@ -144,11 +151,14 @@ def solve_problem(prob: SearchProblem, workload, opts: SolveOptions, running_con
         raise err.PlanFailure(f"winner replay makespan {ms} != search makespan {res.makespan}")
     if res.exhaustive:
         order = prob.decode_index(res.index)[1]
+    elif res.kernel == "local":
+        order = [int(x) for x in explicit[prob.J:]]
     else:
         order = sorted(range(prob.J), key=lambda j: (plan.entries[prob.job_ids[j]].start_time, j))
     if validate and running_context is None:
         D.check_plan(plan, workload, runtimes)
-    return Solution(plan=plan, status="Optimal" if res.exhaustive else "Sampled", makespan=res.makespan,
+    status = "Optimal" if res.exhaustive else ("Local" if res.kernel == "local" else "Sampled")
+    return Solution(plan=plan, status=status, makespan=res.makespan,
                     objective=plan.predicted_makespan, problem=prob, search=res, options=options,
                     order=order, runtimes=runtimes)
 

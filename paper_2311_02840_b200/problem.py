@@ -45,11 +45,13 @@ class SolveOptions:
     k_max: int = K_MAX_DEFAULT
     delta: float | None = None          # explicit interval length (seconds)
     prune: bool | None = None           # None: on for single-node clusters
-    search: str = "auto"                # auto | exhaustive | sampled
+    search: str = "auto"                # auto | exhaustive | sampled | local
     max_exhaustive: int = 1 << 38       # auto -> full scan when the space is <= this (~10 s worst case)
     max_bnb: int = 1 << 52              # auto -> exact bound-and-prune (one node, grid) up to this
     budget: int = 1 << 28               # sampled candidates when not exhaustive
     seed: int = 7                       # sampled stream: candidate i = substream(seed, i)
+    walkers: int = 1 << 14              # local search: walkers (walker w starts at candidate w)
+    max_rounds: int = 4096              # local search: rounds of 32 moves per walker
     kernel: str = "auto"                # auto (bnb when it applies) | tree | index | bnb
 
 

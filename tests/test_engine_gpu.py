@@ -319,3 +319,43 @@ def test_edge_cases(eng):
     from paper_2311_02840_b200 import errors as E
     with pytest.raises(E.InvariantViolation):
         eng.search_index(nprob, 0, prob.space + 1, best)
+
+
+# --------------------------------------------------------------------------- local search
+@pytest.mark.parametrize("name", ["cfg1", "cfg3", "small4_2x2", "cfg4", "hetero6", "cfg5"])
+def test_local_search_walkers_match_oracle(eng, name):
+    """Every walker's whole descent (start = stream candidate, moves, tie-breaks, stop rule)
+    equals the oracle's restatement: same final candidate and makespan; and the search key
+    over a walker range equals the oracle's."""
+    w, t, prob, op = workload_problem(name)
+    cp = C.CProblem(op)
+    rounds = 64 if name == "cfg5" else 4096
+    W = 4 if name == "cfg5" else 48
+    bits, _ = prob.key_bits(1 << 20)
+    nprob = EN.NativeProblem(prob, bits)
+    for walker in range(0, W, max(1, W // 6)):
+        ms, o, r, _ = cp.local_search(walker, "substream", 7, rounds)
+        go, gr = eng.local_search_state(nprob, EN.SRC_SUBSTREAM, 7, walker, rounds)
+        assert (go, gr) == (o, r), (name, walker)
+        assert cp.eval(go, gr)[0] == ms
+    best = eng.reset_best()
+    eng.local_search(nprob, EN.SRC_SUBSTREAM, 7, 0, W, rounds, best)
+    k = int(best.cpu().numpy().view(np.uint64)[0])
+    assert (float(k >> bits), k & ((1 << bits) - 1)) == cp.ls_search("substream", 7, 0, W, rounds)
+
+
+def test_local_search_seed_source_and_release(eng):
+    rng = random.Random(9)
+    for trial in range(6):
+        nodes = [[6], [4, 4], [8]][trial % 3]
+        op = random_problem(rng, rng.randint(3, 7), nodes, max_opts=4, max_d=9, hetero=trial == 4)
+        if trial % 2:
+            op.release = [rng.randint(0, 4) for _ in range(op.J)]
+            op.init_free = [[rng.randint(0, 3) for _ in range(n)] for n in nodes]
+        prob = to_search_problem(op)
+        bits, _ = prob.key_bits(1 << 10)
+        nprob = EN.NativeProblem(prob, bits)
+        cp = C.CProblem(op)
+        for walker in (0, 3, 11):
+            ms, o, r, _ = cp.local_search(walker, "seed", 5, 4096)
+            assert eng.local_search_state(nprob, EN.SRC_SEED, 5, walker, 4096) == (o, r), (trial, walker)

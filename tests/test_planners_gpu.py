@@ -149,3 +149,15 @@ def test_plan_saturn_bnb_equals_exhaustive():
         assert (bb.makespan, bb.search.index) == (ex.makespan, ex.search.index)
         assert bb.plan == ex.plan
         assert bb.search.stats["pair_nodes"] > 0
+
+
+@pytest.mark.parametrize("name", ["cfg3", "cfg4"])
+def test_local_search_plan_beats_its_own_starts(name):
+    """search="local": each walker ends at or below its start, so the best walker is at least as
+    good as sampling the same candidates; the decoded plan is valid and replays to the key."""
+    w, t = setup(name)
+    n = 2048
+    loc = PL.solve(t, w, None, SolveOptions(search="local", walkers=n))
+    smp = PL.solve(t, w, None, SolveOptions(search="sampled", budget=n))
+    assert loc.status == "Local" and loc.makespan <= smp.makespan
+    D.check_plan(loc.plan, w, loc.runtimes)
