@@ -145,7 +145,11 @@ int sat_search_bnb(const sat_problem_t *p, int32_t prefix_len,
  * moves on (makespan, total GPU load) until no move improves or max_rounds rounds of 32
  * moves were scanned.  Result: (makespan << idx_bits) | walker.
  * d_state_out (device, 2J bytes: options then order) receives the final candidate of walker
- * lo when hi == lo + 1 -- the replay that decodes a winning walker. */
+ * lo when hi == lo + 1 -- the replay that decodes a winning walker.  The number of rounds
+ * scanned (each = up to 32 candidates scheduled) is left in the workspace as the uint64 word
+ * after the walker cursor, which follows the problem blob at offset
+ * sat_ls_counter_offset(p). */
+int sat_ls_counter_offset(const sat_problem_t *p, size_t *offset);
 int sat_local_search(const sat_problem_t *p, int32_t source, uint64_t seed, uint64_t lo, uint64_t hi,
                      int32_t max_rounds, sat_best_t *d_best, uint8_t *d_state_out,
                      void *d_ws, size_t ws_bytes, void *stream);

@@ -117,13 +117,14 @@ static int launch_ls_g(const sat_problem_t *p, LsArgs a, const std::vector<uint8
     const uint64_t need = (a.hi - a.lo + kCandWarps - 1) / kCandWarps;
     if (blocks > need) blocks = std::max<uint64_t>(1, need);
     const size_t cur_off = (blob_bytes + 255) & ~(size_t)255;
-    if (!d_ws || ws_bytes < cur_off + sizeof(unsigned long long)) return SAT_ERR_INVALID;
+    if (!d_ws || ws_bytes < cur_off + 2 * sizeof(unsigned long long)) return SAT_ERR_INVALID;
     uint8_t *ws = static_cast<uint8_t *>(d_ws);
     if (cudaMemcpyAsync(ws, blob.data(), blob_bytes, cudaMemcpyHostToDevice, stream) != cudaSuccess)
         return SAT_ERR_CUDA;
-    if (cudaMemsetAsync(ws + cur_off, 0, sizeof(unsigned long long), stream) != cudaSuccess) return SAT_ERR_CUDA;
+    if (cudaMemsetAsync(ws + cur_off, 0, 2 * sizeof(unsigned long long), stream) != cudaSuccess) return SAT_ERR_CUDA;
     a.blob = ws;
     a.cursor = reinterpret_cast<unsigned long long *>(ws + cur_off);
+    a.rounds = a.cursor + 1;
     kern<<<(unsigned)blocks, kCandThreads, smem, stream>>>(a);
     return cudaGetLastError() == cudaSuccess ? SAT_OK : SAT_ERR_CUDA;
 }

@@ -418,6 +418,7 @@ struct LsArgs {
     int32_t rec_d;
     sat_best_t *best;
     unsigned long long *cursor;
+    unsigned long long *rounds; // rounds of 32 moves executed, summed over walkers (zeroed before)
     uint8_t *state_out;         // [2J] final options then order of walker lo (hi == lo + 1), or null
 };
 
@@ -573,6 +574,7 @@ k_ls(LsArgs a) {
             if (!improved || rounds >= a.max_rounds) break;
         }
         if (lane == 0 && key_less(cur, id, best_ms, best_ix)) { best_ms = cur; best_ix = id; }
+        if (lane == 0) atomicAdd(a.rounds, (unsigned long long)rounds + 1ull);   // + the start's round
         if (a.state_out && total == 1 && lane == 0) {
             for (int j = 0; j < J; ++j) a.state_out[j] = wopt[j];
             for (int k = 0; k < J; ++k) a.state_out[J + k] = word[k];

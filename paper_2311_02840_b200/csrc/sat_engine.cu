@@ -740,6 +740,17 @@ static int search_tree_impl(const sat_problem_t *p, int32_t prefix_len, uint64_t
 
 size_t sat_tree_param_bytes(void) { return sizeof(TreeParams); }
 
+int sat_ls_counter_offset(const sat_problem_t *p, size_t *offset) {
+    int st = validate(p);
+    if (st) return st;
+    if (!offset) return SAT_ERR_INVALID;
+    std::vector<uint8_t> blob;
+    st = pack_blob(p, blob, records_carry_duration(p));
+    if (st) return st;
+    *offset = ((blob.size() + 255) & ~(size_t)255) + sizeof(unsigned long long);
+    return SAT_OK;
+}
+
 int sat_local_search(const sat_problem_t *p, int32_t source, uint64_t seed, uint64_t lo, uint64_t hi,
                      int32_t max_rounds, sat_best_t *d_best, uint8_t *d_state_out, void *d_ws, size_t ws_bytes,
                      void *stream) {

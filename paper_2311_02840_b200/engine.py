@@ -64,6 +64,7 @@ _SIGS = {
     "sat_alu_probe": ([_i32, _i32, _i32, _vp, _vp, _vp], _i32),
     "sat_tree_param_bytes": ([], ctypes.c_size_t),
     "sat_local_search": ([_vp, _i32, _u64, _u64, _u64, _i32, _vp, _vp, _vp, ctypes.c_size_t, _vp], _i32),
+    "sat_ls_counter_offset": ([_vp, _vp], _i32),
 }
 
 _LIB = None
@@ -339,7 +340,8 @@ class Engine:
                     exact = True
                 except E.SchedulerError:
                     exact = False
-            mode = "exhaustive" if exact else "sampled"
+            # otherwise local search from sampled starts (grid time), else plain sampling
+            mode = "exhaustive" if exact else ("local" if prob.time_mode == TIME_GRID and prob.J >= 2 else "sampled")
         if mode == "exhaustive":
             if space > (1 << 62):
                 raise E.errors_for(prob.jobs[0]).TooLarge(f"exhaustive space {space} exceeds 2^62")
@@ -389,11 +391,28 @@ class Engine:
                 kernel, evaluated = "index", n_idx
             seed_used = 0
         elif mode == "local":
+            # waves of walkers in walker order; stop after the first wave whose best meets the
+            # lower bound (proven optimal).  The stop depends only on completed waves, so the
+            # result is deterministic.
             src = SRC_SUBSTREAM if source is None else source
             seed_used = opts.seed if seed is None else seed
-            a, b = _shard(n_idx, rank, world)
-            self.local_search(nprob, src, seed_used, a, b, opts.max_rounds, best)
-            kernel, evaluated = "local", n_idx
+            target = prob.lower_bound() if nprob.grid else -1.0
+            off = ctypes.c_size_t()
+            self._check(self.lib.sat_ls_counter_offset(nprob.ref, ctypes.byref(off)))
+            wave = max(1, min(int(opts.wave), n_idx))
+            rounds_total, walkers_done = 0, 0
+            for w0 in range(0, n_idx, wave):
+                w1 = min(n_idx, w0 + wave)
+                a, b = _shard(w1 - w0, rank, world)
+                self.local_search(nprob, src, seed_used, w0 + a, w0 + b, opts.max_rounds, best)
+                rounds_total += int(self._ws[off.value:off.value + 8].view(torch.int64).item())
+                walkers_done = w1
+                k = int(_combine(best, True, group, world)[0])
+                if k != INT64_MAX and (k >> idx_bits) <= target:
+                    break
+            stats = {"walkers": walkers_done, "waves": (walkers_done + wave - 1) // wave, "rounds": rounds_total,
+                     "moves_scheduled_max": rounds_total * 32, "lower_bound": target}
+            kernel, evaluated = "local", walkers_done
         else:
             src = SRC_SUBSTREAM if source is None else source
             seed_used = opts.seed if seed is None else seed
@@ -424,7 +443,7 @@ class Engine:
                             kernel=kernel, exhaustive=mode == "exhaustive",
                             launches=self.launches - launches0, job_steps=job_steps,
                             device_seconds=dev_s, wall_seconds=time.perf_counter() - t0,
-                            stats=stats if mode == "exhaustive" else None)
+                            stats=stats)
 
     @staticmethod
     def _tree_ok(prob: SearchProblem) -> bool:

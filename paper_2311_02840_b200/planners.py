@@ -83,7 +83,8 @@ class Solution:
     """A plan plus how it was found (the reference's MilpSolution analogue)."""
 
     plan: object
-    status: str                 # "Optimal" (space exhausted or proven), "Sampled" or "Local" (heuristic)
+    status: str                 # "Optimal" (space exhausted, or makespan == lower bound), "Sampled" or
+                                # "Local" (heuristic, see `gap`)
     makespan: float             # grid intervals or seconds
     objective: float            # seconds (= plan.predicted_makespan)
     problem: SearchProblem
@@ -91,6 +92,14 @@ class Solution:
     options: list               # option digit per job (problem's job axis)
     order: list                 # submission order (job axis indices)
     runtimes: dict = field(default_factory=dict)   # job id -> seconds of the chosen option/node
+    lower_bound: float | None = None               # makespan lower bound (same unit as makespan)
+
+    @property
+    def gap(self) -> float:
+        """Relative optimality gap (0 when proven optimal)."""
+        if self.status == "Optimal" or not self.lower_bound:
+            return 0.0
+        return max(0.0, (self.makespan - self.lower_bound) / self.lower_bound)
 
 
 def _decode(engine: Engine, prob: SearchProblem, nprob: NativeProblem, workload, source: int, seed: int,
@@ -158,7 +167,10 @@ def solve_problem(prob: SearchProblem, workload, opts: SolveOptions, running_con
     if validate and running_context is None:
         D.check_plan(plan, workload, runtimes)
     status = "Optimal" if res.exhaustive else ("Local" if res.kernel == "local" else "Sampled")
-    return Solution(plan=plan, status=status, makespan=res.makespan,
+    lb = res.makespan if res.exhaustive else prob.lower_bound()
+    if not res.exhaustive and res.makespan <= lb:
+        status = "Optimal"          # a heuristic plan meeting the lower bound is optimal (bound proof)
+    return Solution(plan=plan, status=status, makespan=res.makespan, lower_bound=lb,
                     objective=plan.predicted_makespan, problem=prob, search=res, options=options,
                     order=order, runtimes=runtimes)
 

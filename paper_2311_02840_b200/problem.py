@@ -50,7 +50,8 @@ class SolveOptions:
     max_bnb: int = 1 << 52              # auto -> exact bound-and-prune (one node, grid) up to this
     budget: int = 1 << 28               # sampled candidates when not exhaustive
     seed: int = 7                       # sampled stream: candidate i = substream(seed, i)
-    walkers: int = 1 << 14              # local search: walkers (walker w starts at candidate w)
+    walkers: int = 1 << 16              # local search: walkers at most (walker w starts at candidate w)
+    wave: int = 1 << 12                 # local search: walkers per launch; stops once the bound is met
     max_rounds: int = 4096              # local search: rounds of 32 moves per walker
     kernel: str = "auto"                # auto (bnb when it applies) | tree | index | bnb
 
@@ -111,6 +112,32 @@ class SearchProblem:
         worst = int(self.dur_i32.reshape(self.J, -1).max(axis=1).sum()) if self.J else 0
         real = self.init_free_i32[self.init_free_i32 < INF_I32]
         return worst + int(real.max() if real.size else 0) + int(self.release_i32.max() if self.J else 0)
+
+    def lower_bound(self) -> float:
+        """A makespan lower bound of every candidate (grid intervals or seconds): the latest
+        committed free time, each job's earliest possible end, and the area bound
+        (total GPU time >= initial commitments + every job's least g * d)."""
+        grid = self.time_mode == TIME_GRID
+        d = self.dur_i32 if grid else self.runtime
+        init = self.init_free_i32 if grid else self.init_free_f64
+        rel = self.release_i32 if grid else self.release_f64
+        real = [float(init[n, i]) for n in range(self.N) for i in range(int(self.node_gpus[n]))]
+        lb = max(real) if real else 0.0
+        area = sum(real)
+        for j in range(self.J):
+            ends, areas = [], []
+            for o in range(int(self.radix[j])):
+                g = int(self.gpus[j, o])
+                for n in range(self.N):
+                    if (int(self.node_mask[j, o]) >> n) & 1:
+                        start = max(float(rel[j]), sorted(float(init[n, i]) for i in range(int(self.node_gpus[n])))[g - 1])
+                        ends.append(start + float(d[j, o, n]))
+                        areas.append(g * float(d[j, o, n]))
+            lb = max(lb, min(ends))
+            area += min(areas)
+        total = float(sum(int(x) for x in self.node_gpus))
+        lb = max(lb, area / total)
+        return float(math.ceil(lb - 1e-9)) if grid else lb
 
     def key_bits(self, n_indices: int) -> tuple:
         """(idx_bits, ms_bits) for packing (makespan << idx_bits) | index into 63 bits."""

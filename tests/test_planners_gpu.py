@@ -159,5 +159,21 @@ def test_local_search_plan_beats_its_own_starts(name):
     n = 2048
     loc = PL.solve(t, w, None, SolveOptions(search="local", walkers=n))
     smp = PL.solve(t, w, None, SolveOptions(search="sampled", budget=n))
-    assert loc.status == "Local" and loc.makespan <= smp.makespan
+    assert loc.status in ("Local", "Optimal") and loc.makespan <= smp.makespan
+    assert loc.lower_bound <= loc.makespan
+    assert (loc.status == "Optimal") == (loc.makespan == loc.lower_bound)
     D.check_plan(loc.plan, w, loc.runtimes)
+
+
+def test_default_solve_of_large_configs_is_local_and_bounded():
+    """auto on spaces beyond exact search = local search; cfg4 / cfg5 meet the lower bound
+    (proven optimal), cfg3 stays within one interval of it."""
+    for name, proven in (("cfg3", False), ("cfg4", True), ("cfg5", True)):
+        w, t = setup(name)
+        sol = PL.solve(t, w)
+        assert sol.search.kernel == "local"
+        D.check_plan(sol.plan, w, sol.runtimes)
+        if proven:
+            assert sol.status == "Optimal" and sol.makespan == sol.lower_bound
+        else:
+            assert sol.makespan - sol.lower_bound <= 1

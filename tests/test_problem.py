@@ -124,3 +124,22 @@ def test_errors():
     tb = build_profile_table(big, SyntheticExecutor(big.cluster))
     with pytest.raises(E.TooLarge):
         build_problem(tb, big)
+
+
+def test_lower_bound_never_exceeds_the_optimum():
+    """problem.lower_bound() <= the exhaustive optimum (oracle) on random 1- and 2-node problems."""
+    import random
+
+    from oracle import coracle as C
+    from test_engine_gpu import to_search_problem
+    from test_oracle import random_problem
+
+    rng = random.Random(41)
+    for trial in range(40):
+        nodes = [[rng.randint(1, 6)], [rng.randint(1, 4), rng.randint(1, 4)]][trial % 2]
+        op = random_problem(rng, rng.randint(1, 4), nodes, max_opts=3, max_d=8, hetero=trial % 3 == 0)
+        if trial % 4 == 1:
+            op.release = [rng.randint(0, 4) for _ in range(op.J)]
+            op.init_free = [[rng.randint(0, 3) for _ in range(n)] for n in nodes]
+        ms, _ = C.CProblem(op).search()
+        assert to_search_problem(op).lower_bound() <= ms, trial
