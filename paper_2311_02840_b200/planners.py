@@ -337,26 +337,19 @@ def plan_current_practice(table, jobs, cluster=None, delta_opts=None, *, techniq
 
 def evaluate_fixed(table, workload, options, order, delta_opts=None, running_context=None, device=None,
                    prune: bool = False) -> Solution:
-    """Schedule one explicit (options, order) candidate on the engine."""
+    """Schedule one explicit candidate -- option digit per job (problem job axis, option order of
+    the pruned lists when prune=True, of feasible_entries otherwise) and a submission order."""
     opts = _opts(delta_opts)
     if prune:
         prob = build_problem(table, workload, opts, running_context)
-        builder_prob = prob
     else:
-        builder_prob = None
-
-    def builder(_prob):
-        return list(options), list(order)
-
-    if builder_prob is None:
-        return _explicit_solution(table, workload, opts, running_context, builder, device)
+        prob = _baseline_problem(table, workload, opts, running_context)
     eng = get_engine(device)
-    nprob = NativeProblem(builder_prob, 62)
     explicit = np.array(list(options) + list(order), dtype=np.uint8)
-    plan, opts_out, ms, runtimes = _decode(eng, builder_prob, nprob, workload, SRC_EXPLICIT, 0,
+    plan, opts_out, ms, runtimes = _decode(eng, prob, NativeProblem(prob, 62), workload, SRC_EXPLICIT, 0,
                                            explicit=explicit)
-    return Solution(plan=plan, status="Fixed", makespan=ms, objective=plan.predicted_makespan,
-                    problem=builder_prob, search=None, options=opts_out, order=list(order), runtimes=runtimes)
+    return Solution(plan=plan, status="Fixed", makespan=ms, objective=plan.predicted_makespan, problem=prob,
+                    search=None, options=opts_out, order=list(order), runtimes=runtimes)
 
 
 __all__ = [

@@ -177,3 +177,13 @@ def test_default_solve_of_large_configs_is_local_and_bounded():
             assert sol.status == "Optimal" and sol.makespan == sol.lower_bound
         else:
             assert sol.makespan - sol.lower_bound <= 1
+
+
+def test_evaluate_fixed_reproduces_planner_plans():
+    w, t = setup("cfg1")
+    sol = PL.solve(t, w)
+    fixed = PL.evaluate_fixed(t, w, sol.options, sol.order, prune=True)
+    assert fixed.plan == sol.plan and fixed.makespan == sol.makespan
+    prob = PL._baseline_problem(t, w, SolveOptions())
+    options, order = PL.optimus_allocation(prob)
+    assert PL.evaluate_fixed(t, w, options, order).plan == PL.plan_optimus(t, w)
