@@ -151,6 +151,17 @@ def solve_problem(prob: SearchProblem, workload, opts: SolveOptions, running_con
         else:
             src = SRC_INDEX if res.exhaustive else res.source
             plan, options, ms, runtimes = _decode(eng, prob, nprob, workload, src, res.seed, ident=res.index)
+        incumbent = None
+        if not res.exhaustive:
+            # heuristic searches also weigh the greedy baselines as incumbents (the B&B's
+            # "initial incumbent from rounding"): the plan is never worse than them
+            nexp = NativeProblem(prob, 62)
+            for builder in (optimus_allocation, current_practice_allocation):
+                b_opts, b_order = builder(prob)
+                ex = np.array(list(b_opts) + list(b_order), dtype=np.uint8)
+                cand = _decode(eng, prob, nexp, workload, SRC_EXPLICIT, 0, explicit=ex)
+                if cand[2] < ms and (incumbent is None or cand[2] < incumbent[0][2]):
+                    incumbent = (cand, list(b_order), builder.__name__)
     except E.SchedulerError:
         raise
     except Exception as exc:  # CUDA / NCCL trouble -> PlanFailure (ReplanFailure on re-solve)
@@ -164,13 +175,17 @@ def solve_problem(prob: SearchProblem, workload, opts: SolveOptions, running_con
         order = [int(x) for x in explicit[prob.J:]]
     else:
         order = sorted(range(prob.J), key=lambda j: (plan.entries[prob.job_ids[j]].start_time, j))
+    if incumbent is not None:
+        (plan, options, ms, runtimes), order, source_name = incumbent
+        res.stats = {**(res.stats or {}), "incumbent": source_name}
+    makespan = ms
     if validate and running_context is None:
         D.check_plan(plan, workload, runtimes)
     status = "Optimal" if res.exhaustive else ("Local" if res.kernel == "local" else "Sampled")
-    lb = res.makespan if res.exhaustive else prob.lower_bound()
-    if not res.exhaustive and res.makespan <= lb:
+    lb = makespan if res.exhaustive else prob.lower_bound()
+    if not res.exhaustive and makespan <= lb:
         status = "Optimal"          # a heuristic plan meeting the lower bound is optimal (bound proof)
-    return Solution(plan=plan, status=status, makespan=res.makespan, lower_bound=lb,
+    return Solution(plan=plan, status=status, makespan=makespan, lower_bound=lb,
                     objective=plan.predicted_makespan, problem=prob, search=res, options=options,
                     order=order, runtimes=runtimes)
 

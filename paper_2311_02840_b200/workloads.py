@@ -62,3 +62,52 @@ def config_workload(k: int):
     c = CONFIGS[k]
     w = synthetic_workload(c["jobs"], c["nodes"], c["gpus"], c["techs"])
     return w, build_profile_table(w, SyntheticExecutor(w.cluster)), c
+
+
+# ---------------------------------------------------------------- SPEC.md:428-436 mirror presets
+# Table 1 grid shape: 2 models x 3 learning rates x 2 batch sizes = 12 jobs on `nodes` x 8
+# GPUs; one model tier fits a GPU under replication, the other needs sharding / pipelining /
+# offloading; +-10 % seeded jitter on the per-batch time.  Numeric job parameters are
+# synthetic (the SPEC's own design decision); epochs fold into total_batches.
+PRESETS = {
+    #                 (model id, model GiB, activation GiB, base s/batch, batches per epoch x 10 epochs)
+    "wikitext_mirror": (("gpt2", 20.0, 6.0, 1.0, 2_000), ("gptj", 96.0, 8.0, 4.0, 2_000)),
+    "imagenet_mirror": (("resnet200", 12.0, 10.0, 0.8, 2_500), ("vitg", 72.0, 12.0, 3.0, 2_500)),
+}
+
+
+def generate_workload(preset: str, nodes: int = 1, seed: int = 7, gpus_per_node: int = 8) -> Workload:
+    """SPEC.md:428-436 generate_workload: 12 jobs (model x lr x batch size) on nodes x 8 GPUs."""
+    from . import errors as E
+
+    if preset not in PRESETS:
+        raise E.InvariantViolation("preset", f"unknown preset {preset!r}")
+    stream = substream(seed, 2)
+    jobs = []
+    for model, mem, act, base, batches in PRESETS[preset]:
+        for lr in range(3):
+            for bs, (scale, bfac) in enumerate(((1.0, 1.0), (1.8, 0.5))):   # batch x2: ~1.8x time, half the batches
+                jitter = 0.9 + 0.2 * stream.uniform()
+                jobs.append(JobSpec(id=f"{model}-lr{lr}-bs{bs}", total_batches=int(batches * 10 * bfac),
+                                    base_batch_time=base * scale * jitter, model_memory=mem,
+                                    activation_memory=act * scale))
+    cluster = ClusterSpec(nodes=tuple(NodeSpec(id=f"n{i}", gpu_count=gpus_per_node, gpu_memory=40.0)
+                                      for i in range(nodes)))
+    return Workload(jobs=tuple(jobs), cluster=cluster, techniques=TECHNIQUES_4)
+
+
+def random_workload(seed: int, n_jobs=None, n_nodes=None, gpus_per_node: int = 4) -> Workload:
+    """SPEC.md:481 criterion 3 workloads: 4-8 jobs, 1-2 nodes of 4 GPUs, synthetic profiles."""
+    s = substream(seed, 3)
+    J = n_jobs or 4 + s.below(5)
+    N = n_nodes or 1 + s.below(2)
+    jobs = []
+    for j in range(J):
+        large = s.below(3) == 0
+        jobs.append(JobSpec(id=f"j{j:02d}", total_batches=1000 * (1 + s.below(10)),
+                            base_batch_time=(3.0 if large else 1.0) * (0.5 + s.uniform()),
+                            model_memory=60.0 if large else 10.0 + 20.0 * s.uniform(),
+                            activation_memory=4.0 + 4.0 * s.uniform()))
+    cluster = ClusterSpec(nodes=tuple(NodeSpec(id=f"n{i}", gpu_count=gpus_per_node, gpu_memory=40.0)
+                                      for i in range(N)))
+    return Workload(jobs=tuple(jobs), cluster=cluster, techniques=TECHNIQUES_4)

@@ -68,7 +68,7 @@ def test_spec_two_job_example():
 def test_sampled_saturn_and_baselines(name):
     w, t = setup(name)
     sol = PL.solve(t, w, None, SolveOptions(search="sampled", budget=200000))
-    assert sol.status == "Sampled"
+    assert sol.status in ("Sampled", "Optimal") and sol.makespan <= sol.search.makespan
     D.check_plan(sol.plan, w, sol.runtimes)
     opt = PL._explicit_solution(t, w, SolveOptions(), None, PL.optimus_allocation, None)
     cp = PL._explicit_solution(t, w, SolveOptions(), None, PL.current_practice_allocation, None)
