@@ -230,7 +230,9 @@ k_tree(const __grid_constant__ TreeParams p) {
     for (int L = 0; L < upper; ++L)
         for (int i = G; i < 2 * G; ++i) wbase[L * col_words + i * 32 + lane] = SAT_INF_I32;
 
-    LaneBest lb{SAT_INF_I32, ~0ull};
+    // bound-and-prune records only candidates at or below the seed bound (the key's makespan
+    // field is sized for it); the full scan records everything
+    LaneBest lb{BNB ? min(published_ms(p), (int32_t)SAT_INF_I32) : (int32_t)SAT_INF_I32, ~0ull};
     const uint32_t all = (J >= 32) ? 0xffffffffu : ((1u << J) - 1u);
     unsigned long long published = ~0ull;          // BNB: last key this warp published
     unsigned long long n_pruned = 0, n_pairs = 0;   // BNB counters (lane 0)
@@ -378,7 +380,7 @@ k_tree(const __grid_constant__ TreeParams p) {
         __syncwarp();
         if constexpr (BNB) {
             // publish an improvement right away so every warp prunes against it
-            uint64_t key = (lb.ms < SAT_INF_I32) ? (((uint64_t)(uint32_t)lb.ms << p.idx_bits) | lb.ix) : ~0ull;
+            uint64_t key = (lb.ix != ~0ull) ? (((uint64_t)(uint32_t)lb.ms << p.idx_bits) | lb.ix) : ~0ull;
             for (int x = 16; x >= 1; x >>= 1) {
                 const uint64_t o = shfl_u64(key, lane ^ x);
                 key = o < key ? o : key;
@@ -391,7 +393,7 @@ k_tree(const __grid_constant__ TreeParams p) {
     }
 
     // ---- warp argmin, one atomic per warp ----
-    uint64_t key = (lb.ms < SAT_INF_I32) ? (((uint64_t)(uint32_t)lb.ms << p.idx_bits) | lb.ix) : ~0ull;
+    uint64_t key = (lb.ix != ~0ull) ? (((uint64_t)(uint32_t)lb.ms << p.idx_bits) | lb.ix) : ~0ull;
     for (int x = 16; x >= 1; x >>= 1) {
         const uint64_t o = shfl_u64(key, lane ^ x);
         key = o < key ? o : key;

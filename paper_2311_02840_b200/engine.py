@@ -149,7 +149,8 @@ class SearchResult:
     job_steps: int = 0         # list-scheduling placements (tree walk) on all ranks
     device_seconds: float = 0.0
     wall_seconds: float = 0.0
-    stats: dict | None = None  # bound-and-prune counters (this rank)
+    stats: dict | None = None  # bound-and-prune / local-search counters (this rank)
+    idx_bits: int = 0          # bits of the packed key holding the candidate id
 
 
 class Engine:
@@ -237,20 +238,26 @@ class Engine:
                 return P
         return 0
 
-    def seed_upper_bound(self, prob: SearchProblem, nprob: NativeProblem, best, budget: int = 1 << 16,
-                         seed: int = 7):
-        """Seed *best with (U << idx_bits | max index), U = best makespan of a quick sampled search:
-        any real candidate with makespan <= U replaces it, and the bound prunes from the start."""
+    def seed_bound(self, prob: SearchProblem, budget: int = 1 << 16, seed: int = 7) -> int:
+        """Best makespan of a quick sampled search: an achievable upper bound (grid intervals).
+        Seeding *best with (U << idx_bits | max index) lets any real candidate with makespan <= U
+        replace it while the bound prunes from the start."""
         torch = self.torch
-        s_bits, _ = prob.key_bits(budget)
+        s_bits = max(1, (budget - 1).bit_length())
         sprob = NativeProblem(prob, s_bits)
         tmp = self.reset_best(torch.empty(2, dtype=torch.int64, device=self.device))
         self.search_sampled(sprob, SRC_SUBSTREAM, seed, 0, budget, tmp)
-        hi = tmp[0:1].view(torch.int64)
-        ms = torch.bitwise_right_shift(hi, s_bits)
-        key = torch.bitwise_or(torch.bitwise_left_shift(ms, nprob.idx_bits), (1 << nprob.idx_bits) - 1)
-        best[0:1].copy_(torch.minimum(key, torch.where(best[0:1] == -1, torch.full_like(key, INT64_MAX),
-                                                       best[0:1])))
+        k = int(tmp[0].item()) & ((1 << 64) - 1)
+        return k >> s_bits
+
+    def seed_upper_bound(self, prob: SearchProblem, nprob: NativeProblem, best, budget: int = 1 << 16,
+                         seed: int = 7):
+        """Seed *best (device) from seed_bound()."""
+        U = self.seed_bound(prob, budget, seed)
+        key = (U << nprob.idx_bits) | ((1 << nprob.idx_bits) - 1)
+        cur = int(best[0].item())
+        if cur == -1 or key < cur:
+            best[0:1].fill_(key)
 
     def local_search(self, nprob, source, seed, lo, hi, max_rounds: int = 4096, best=None, state_out=None):
         """Walkers [lo, hi) of the local search; state_out (uint8 device tensor, 2J) receives the
@@ -335,11 +342,9 @@ class Engine:
             # node, grid time) and the packed key still holds the index
             exact = space <= opts.max_exhaustive
             if not exact and opts.kernel in ("auto", "bnb") and self._tree_ok(prob) and space <= opts.max_bnb:
-                try:
-                    prob.key_bits(space)
-                    exact = True
-                except E.SchedulerError:
-                    exact = False
+                # the bound-and-prune key holds (makespan <= seed bound) << idx_bits | index:
+                # leave at least 7 bits for the makespan (grids of <= 127 intervals)
+                exact = (space - 1).bit_length() <= 56
             # otherwise local search from sampled starts (grid time), else plain sampling
             mode = "exhaustive" if exact else ("local" if prob.time_mode == TIME_GRID and prob.J >= 2 else "sampled")
         if mode == "exhaustive":
@@ -358,7 +363,18 @@ class Engine:
         t0 = time.perf_counter()
         mode, n_idx = self.plan_search(prob, opts)
         rank, world = _rank_world(group)
-        idx_bits, _ = prob.key_bits(n_idx)
+        use_bnb = (mode == "exhaustive" and opts.kernel in ("auto", "bnb") and self._tree_ok(prob))
+        seed_ms = None
+        if use_bnb:
+            # bound-and-prune: keys only ever hold makespans <= the seed bound
+            seed_ms = self.seed_bound(prob)
+            idx_bits = max(1, (n_idx - 1).bit_length())
+            if idx_bits + max(1, seed_ms.bit_length()) > 63:
+                if opts.kernel == "bnb":
+                    raise err.TooLarge(f"key needs {idx_bits}+{seed_ms.bit_length()} bits > 63")
+                mode, n_idx, use_bnb = "local", int(opts.walkers), False
+        if not use_bnb:
+            idx_bits, _ = prob.key_bits(n_idx)
         nprob = NativeProblem(prob, idx_bits)
         launches0 = self.launches
         best = self.reset_best()
@@ -372,11 +388,11 @@ class Engine:
             use_tree = opts.kernel in ("auto", "tree", "bnb") and self._tree_ok(prob)
             if opts.kernel in ("tree", "bnb") and not use_tree:
                 raise err.TooLarge("tree / bnb kernels need one node, grid time, 3..20 jobs")
-            if use_tree and opts.kernel in ("auto", "bnb"):
+            if use_bnb:
                 P = self.bnb_prefix(nprob, (1 << 15) * world)       # enough tasks on every rank
                 info = self.tree_plan(nprob, P)
                 a, b = _shard(info.n_tasks, rank, world)
-                self.seed_upper_bound(prob, nprob, best)
+                best[0:1].fill_((seed_ms << idx_bits) | ((1 << idx_bits) - 1))
                 bnb_ws = self.search_bnb(nprob, info.prefix_len, a, b, best)
                 stats = {"prefix_len": info.prefix_len, "tasks": b - a}
                 kernel, evaluated = "bnb", info.n_candidates
@@ -443,7 +459,7 @@ class Engine:
                             kernel=kernel, exhaustive=mode == "exhaustive",
                             launches=self.launches - launches0, job_steps=job_steps,
                             device_seconds=dev_s, wall_seconds=time.perf_counter() - t0,
-                            stats=stats)
+                            stats=stats, idx_bits=idx_bits)
 
     @staticmethod
     def _tree_ok(prob: SearchProblem) -> bool:

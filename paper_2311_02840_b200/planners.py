@@ -140,8 +140,7 @@ def solve_problem(prob: SearchProblem, workload, opts: SolveOptions, running_con
     eng = get_engine(device)
     try:
         res = eng.search(prob, opts, group=group)
-        idx_bits, _ = prob.key_bits(res.evaluated if not res.exhaustive else prob.space)
-        nprob = NativeProblem(prob, idx_bits)
+        nprob = NativeProblem(prob, res.idx_bits)
         if res.kernel == "local":
             # replay the winning walker to get its final candidate, then schedule it explicitly
             o_, r_ = eng.local_search_state(nprob, res.source, res.seed, res.index, opts.max_rounds)

@@ -187,3 +187,17 @@ def test_evaluate_fixed_reproduces_planner_plans():
     prob = PL._baseline_problem(t, w, SolveOptions())
     options, order = PL.optimus_allocation(prob)
     assert PL.evaluate_fixed(t, w, options, order).plan == PL.plan_optimus(t, w)
+
+
+def test_bnb_beyond_the_worst_case_key_width():
+    """A 12-job one-node mirror (space 3.9e16): the worst-case makespan bound would not fit the
+    packed key next to the index, the seed bound does -- exact bound-and-prune when asked for."""
+    from paper_2311_02840_b200.workloads import generate_workload
+
+    w = generate_workload("wikitext_mirror", 1, 7)
+    t = build_profile_table(w, SyntheticExecutor(w.cluster))
+    exact = PL.solve(t, w, None, SolveOptions(kernel="bnb", max_bnb=1 << 60))
+    assert exact.search.kernel == "bnb" and exact.status == "Optimal"
+    local = PL.solve(t, w)                                  # default: local search for this size
+    assert exact.makespan <= local.makespan
+    assert exact.lower_bound == exact.makespan
