@@ -1,4 +1,5 @@
 # Bounds-checked library (SAT_ASSERT on every shared-memory region index) through the small
+python -m paper_2311_02840_b200.build --debug > gpurun_out/debug_build.log 2>&1 || exit 1
 # all-kernel script and the whole GPU parity suite; compute-sanitizer is closed on this pool.
 export SATURN_ENGINE_LIB=$PWD/paper_2311_02840_b200/_lib/libsaturn_b200_debug.so
 timeout 300 python tools/sanitize_small.py > gpurun_out/debug_small.log 2>&1; echo rc=$? >> gpurun_out/debug_small.log
