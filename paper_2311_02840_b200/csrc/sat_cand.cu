@@ -104,7 +104,8 @@ static int launch_ls_g(const sat_problem_t *p, LsArgs a, const std::vector<uint8
                        size_t ws_bytes, cudaStream_t stream) {
     const size_t blob_bytes = blob.size();
     const int N = (L == kLayoutMulti || L == kLayoutMulti16) ? p->N : 1;
-    const int smem = (int)blob_bytes + kCandWarps * ls_warp_bytes(p->J, N, G, cand_slot_bytes<int32_t, L>());
+    const int smem = (int)blob_bytes +
+                     kCandWarps * ls_warp_bytes(p->J, N, G, cand_slot_bytes<int32_t, L>(), cache_state_words<G, L>(N));
     if (smem > 220 * 1024) return SAT_ERR_TOO_LARGE;
     auto kern = k_ls<SRC, G, L>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)

@@ -75,9 +75,20 @@ struct SchedCtx {
 
 // List-schedule the J step records in the lane's record column (stride 32) and return the
 // makespan.  Layout L as in the file comment; G = padded GPUs per node.
+// Prefix cache (local search): cin / cout point at a warp-shared array of J + 1 entries of
+// cache_words<G, L>(N) words -- the free-time state before position k, then the makespan
+// so far.  With cin the schedule resumes at position k0 from entry k0 (records before k0 are
+// not read); with cout (written by `writer` only) every entry of this candidate is stored.
+template <int G, int L>
+__host__ __device__ constexpr int cache_state_words(int N) {
+    return (L == kLayoutOne16 || L == kLayoutMulti16) ? N * (G / 2) : N * G;
+}
+
 template <typename T, int G, int L, bool LOAD = false>
 __device__ __forceinline__ T schedule_records(const SchedCtx<T> &c, const uint32_t *rec,
-                                             uint64_t *load = nullptr) {
+                                             uint64_t *load = nullptr, int k0 = 0,
+                                             const uint32_t *cin = nullptr, uint32_t *cout = nullptr,
+                                             bool writer = false) {
     constexpr bool P16 = L == kLayoutOne16;
     constexpr bool M16 = L == kLayoutMulti16;
     constexpr int NMAX = (L == kLayoutMulti || M16) ? (32 / G) : 1;
@@ -90,7 +101,10 @@ __device__ __forceinline__ T schedule_records(const SchedCtx<T> &c, const uint32
     const bool rec_d = c.rec_d, has_release = c.has_release;
     const T INF = c.INF;
     (void)INF; (void)dur; (void)N;
-    T mx = c.init_max;
+    const int SW = cache_state_words<G, L>(N), CW = SW + 1;
+    T mx = cin ? (T)(int32_t)cin[k0 * CW + SW] : c.init_max;
+    const bool wr = cout != nullptr && writer;
+    (void)SW; (void)CW; (void)wr;
     if constexpr (P16) {
         // slots 2w (low half) and 2w+1 (high half) of word w; rows G/2..G-1 = +inf.
         // Shift by the thread's g: word k of the shifted vector is word g/2 + k (g even)
@@ -99,10 +113,13 @@ __device__ __forceinline__ T schedule_records(const SchedCtx<T> &c, const uint32
         uint32_t av[G / 2];
 #pragma unroll
         for (int w = 0; w < G / 2; ++w) {
-            av[w] = (uint32_t)(uint16_t)lane_init[2 * w] | ((uint32_t)(uint16_t)lane_init[2 * w + 1] << 16);
+            av[w] = cin ? cin[k0 * CW + w]
+                        : (uint32_t)(uint16_t)lane_init[2 * w] | ((uint32_t)(uint16_t)lane_init[2 * w + 1] << 16);
             st16[w * 32] = av[w];
+            if (wr) cout[w] = av[w];
         }
-        for (int kk = 0; kk < J; ++kk) {
+        if (wr) cout[SW] = (uint32_t)(int32_t)mx;
+        for (int kk = k0; kk < J; ++kk) {
             const uint32_t r = rec[kk * 32];
             const int g = (int)(r & 63u) + 1;
             SAT_ASSERT(g >= 1 && g <= G && (int)((r >> 6) & 63u) < J);
@@ -126,6 +143,11 @@ __device__ __forceinline__ T schedule_records(const SchedCtx<T> &c, const uint32
                 st16[k * 32] = av[k];
             }
             mx = tmax(mx, (T)e);
+            if (wr) {
+#pragma unroll
+                for (int w = 0; w < G / 2; ++w) cout[(kk + 1) * CW + w] = av[w];
+                cout[(kk + 1) * CW + SW] = (uint32_t)(int32_t)mx;
+            }
         }
         if constexpr (LOAD) {
             uint64_t sum = 0;
@@ -140,10 +162,12 @@ __device__ __forceinline__ T schedule_records(const SchedCtx<T> &c, const uint32
         T av[G];
 #pragma unroll
         for (int i = 0; i < G; ++i) {
-            av[i] = lane_init[i];
+            av[i] = cin ? (T)(int32_t)cin[k0 * CW + i] : lane_init[i];
             st[i * 32] = av[i];
+            if (wr) cout[i] = (uint32_t)(int32_t)av[i];
         }
-        for (int kk = 0; kk < J; ++kk) {
+        if (wr) cout[SW] = (uint32_t)(int32_t)mx;
+        for (int kk = k0; kk < J; ++kk) {
             const uint32_t r = rec[kk * 32];
             const int g = (int)(r & 63u) + 1;
             SAT_ASSERT(g >= 1 && g <= G && (int)((r >> 6) & 63u) < J);
@@ -161,6 +185,11 @@ __device__ __forceinline__ T schedule_records(const SchedCtx<T> &c, const uint32
                 st[i * 32] = av[i];
             }
             mx = tmax(mx, e);
+            if (wr) {
+#pragma unroll
+                for (int i = 0; i < G; ++i) cout[(kk + 1) * CW + i] = (uint32_t)(int32_t)av[i];
+                cout[(kk + 1) * CW + SW] = (uint32_t)(int32_t)mx;
+            }
         }
         if constexpr (LOAD) {
             uint64_t sum = 0;
@@ -176,10 +205,15 @@ __device__ __forceinline__ T schedule_records(const SchedCtx<T> &c, const uint32
         for (int n = 0; n < NMAX; ++n)
             if (n < N)
 #pragma unroll
-                for (int w = 0; w < G / 2; ++w)
-                    st16[(n * G + w) * 32] = (uint32_t)(uint16_t)lane_init[n * G + 2 * w] |
-                                             ((uint32_t)(uint16_t)lane_init[n * G + 2 * w + 1] << 16);
-        for (int kk = 0; kk < J; ++kk) {
+                for (int w = 0; w < G / 2; ++w) {
+                    const uint32_t v = cin ? cin[k0 * CW + n * (G / 2) + w]
+                                           : (uint32_t)(uint16_t)lane_init[n * G + 2 * w] |
+                                                 ((uint32_t)(uint16_t)lane_init[n * G + 2 * w + 1] << 16);
+                    st16[(n * G + w) * 32] = v;
+                    if (wr) cout[n * (G / 2) + w] = v;
+                }
+        if (wr) cout[SW] = (uint32_t)(int32_t)mx;
+        for (int kk = k0; kk < J; ++kk) {
             const uint32_t r = rec[kk * 32];
             const int g = (int)(r & 63u) + 1;
             SAT_ASSERT(g >= 1 && g <= G && (int)((r >> 6) & 63u) < J);
@@ -212,6 +246,14 @@ __device__ __forceinline__ T schedule_records(const SchedCtx<T> &c, const uint32
             for (int k = 0; k < G / 2; ++k)
                 nb[k * 32] = __vmaxu2(cur[k], __vminu2(__byte_perm(w[k], w[k + 1], sel), e2));
             mx = tmax(mx, (T)e);
+            if (wr) {
+#pragma unroll
+                for (int n = 0; n < NMAX; ++n)
+                    if (n < N)
+#pragma unroll
+                        for (int q = 0; q < G / 2; ++q) cout[(kk + 1) * CW + n * (G / 2) + q] = st16[(n * G + q) * 32];
+                cout[(kk + 1) * CW + SW] = (uint32_t)(int32_t)mx;
+            }
         }
         if constexpr (LOAD) {
             uint64_t sum = 0;
@@ -231,8 +273,13 @@ __device__ __forceinline__ T schedule_records(const SchedCtx<T> &c, const uint32
         for (int n = 0; n < NMAX; ++n)
             if (n < N)
 #pragma unroll
-                for (int i = 0; i < G; ++i) st[(n * 2 * G + i) * 32] = lane_init[n * G + i];
-        for (int kk = 0; kk < J; ++kk) {
+                for (int i = 0; i < G; ++i) {
+                    const T v = cin ? (T)(int32_t)cin[k0 * CW + n * G + i] : lane_init[n * G + i];
+                    st[(n * 2 * G + i) * 32] = v;
+                    if (wr) cout[n * G + i] = (uint32_t)(int32_t)v;
+                }
+        if (wr) cout[SW] = (uint32_t)(int32_t)mx;
+        for (int kk = k0; kk < J; ++kk) {
             const uint32_t r = rec[kk * 32];
             const int g = (int)(r & 63u) + 1;
             SAT_ASSERT(g >= 1 && g <= G && (int)((r >> 6) & 63u) < J);
@@ -269,6 +316,14 @@ __device__ __forceinline__ T schedule_records(const SchedCtx<T> &c, const uint32
 #pragma unroll
             for (int i = 0; i < G; ++i) sb[i * 32] = tmax(cur[i], tmin(s[i], be));
             mx = tmax(mx, be);
+            if (wr) {
+#pragma unroll
+                for (int n = 0; n < NMAX; ++n)
+                    if (n < N)
+#pragma unroll
+                        for (int q = 0; q < G; ++q) cout[(kk + 1) * CW + n * G + q] = (uint32_t)(int32_t)st[(n * 2 * G + q) * 32];
+                cout[(kk + 1) * CW + SW] = (uint32_t)(int32_t)mx;
+            }
         }
         if constexpr (LOAD) {
             uint64_t sum = 0;
@@ -422,8 +477,9 @@ struct LsArgs {
     uint8_t *state_out;         // [2J] final options then order of walker lo (hi == lo + 1), or null
 };
 
-__host__ __device__ inline int ls_warp_bytes(int J, int N, int G, int slot_bytes) {
-    return cand_warp_bytes(J, N, G, slot_bytes, false) + 128;        // + the walker's options / order
+// + the walker's options / order / job positions (3 x 64 bytes) + its prefix cache
+__host__ __device__ inline int ls_warp_bytes(int J, int N, int G, int slot_bytes, int cache_state_words) {
+    return cand_warp_bytes(J, N, G, slot_bytes, false) + 192 + (J + 1) * (cache_state_words + 1) * 4;
 }
 
 // neighbour of (opt, ord) under move m: source position of position k, and the option override
@@ -479,12 +535,15 @@ k_ls(LsArgs a) {
     const T *release = reinterpret_cast<const T *>(smem + h.off_release);
     const T *lane_init = reinterpret_cast<const T *>(smem + h.off_lane_init);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint8_t *wbase = smem + h.bytes + warp * ls_warp_bytes(J, N, G, cand_slot_bytes<T, L>());
+    const int SW = cache_state_words<G, L>(N);
+    uint8_t *wbase = smem + h.bytes + warp * ls_warp_bytes(J, N, G, cand_slot_bytes<T, L>(), SW);
     uint32_t *rec = reinterpret_cast<uint32_t *>(wbase) + lane;
     T *st = reinterpret_cast<T *>(wbase + J * 128) + lane;
     uint32_t *st16 = reinterpret_cast<uint32_t *>(st);
     uint8_t *wopt = wbase + cand_warp_bytes(J, N, G, cand_slot_bytes<T, L>(), false);   // [64]
     uint8_t *word = wopt + 64;                                                           // [64]
+    uint8_t *wpos = word + 64;                                                           // [64] job -> position
+    uint32_t *cache = reinterpret_cast<uint32_t *>(wpos + 64);                          // [J + 1][SW + 1]
     const T INF = SAT_INF_I32;
     if constexpr (L == kLayoutOne16 || L == kLayoutMulti16) {
         for (int n = 0; n < N; ++n)
@@ -519,10 +578,15 @@ k_ls(LsArgs a) {
             }
         }
         __syncwarp();
-        // objective of the start (every lane, identical)
+        // objective of the start (every lane, identical); lane 0 fills the prefix cache
         for (int k = 0; k < J; ++k) { const int job = word[k]; rec[k * 32] = rec_for(tb, job, wopt[job]); }
+        if (lane == 0)
+            for (int k = 0; k < J; ++k) wpos[word[k]] = (uint8_t)k;
         uint64_t load = 0;
-        T cur = schedule_records<T, G, L, true>(sc, rec, &load);
+        // the prefix cache pays off only on long orders (measured: +10 % at 64 jobs, -15 % at 16)
+        const bool use_cache = J >= 24;
+        T cur = schedule_records<T, G, L, true>(sc, rec, &load, 0, nullptr, use_cache ? cache : nullptr, lane == 0);
+        __syncwarp();
         uint64_t cur_key = ((uint64_t)(uint32_t)cur << 34) | load;
         int rounds = 0;
         for (;;) {
@@ -532,13 +596,16 @@ k_ls(LsArgs a) {
                 uint64_t key = ~0ull;
                 if (m < M) {
                     const LsMove mv = ls_decode_move(m, J, M1, M2, tb.radix, wopt);
-                    for (int k = 0; k < J; ++k) {
+                    // positions before the first changed one schedule exactly as the current
+                    // candidate: resume from the prefix cache there
+                    const int k0 = !use_cache ? 0 : (mv.kind == 1 ? (int)wpos[mv.a] : min(mv.a, mv.b));
+                    for (int k = k0; k < J; ++k) {
                         const int job = word[ls_src(mv, k)];
                         const int o = (mv.kind == 1 && job == mv.a) ? mv.b : (int)wopt[job];
                         rec[k * 32] = rec_for(tb, job, o);
                     }
                     uint64_t ld = 0;
-                    const T ms = schedule_records<T, G, L, true>(sc, rec, &ld);
+                    const T ms = schedule_records<T, G, L, true>(sc, rec, &ld, k0, use_cache ? cache : nullptr);
                     key = ((uint64_t)(uint32_t)ms << 34) | ld;
                 }
                 // warp argmin of (objective, move id)
@@ -562,8 +629,14 @@ k_ls(LsArgs a) {
                             else for (int k = mv.a; k > mv.b; --k) word[k] = word[k - 1];
                             word[mv.b] = x;
                         }
+                        for (int k = 0; k < J; ++k) wpos[word[k]] = (uint8_t)k;
                     }
                     __syncwarp();
+                    if (use_cache) {   // refresh the prefix cache for the new current candidate
+                        for (int k = 0; k < J; ++k) { const int job = word[k]; rec[k * 32] = rec_for(tb, job, wopt[job]); }
+                        schedule_records<T, G, L, false>(sc, rec, nullptr, 0, nullptr, cache, lane == 0);
+                        __syncwarp();
+                    }
                     cur_key = bk;
                     cur = (T)(bk >> 34);
                     improved = true;
