@@ -363,6 +363,9 @@ class Engine:
         t0 = time.perf_counter()
         mode, n_idx = self.plan_search(prob, opts)
         rank, world = _rank_world(group)
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record()                       # device time covers every launch of the solve
         use_bnb = (mode == "exhaustive" and opts.kernel in ("auto", "bnb") and self._tree_ok(prob))
         seed_ms = None
         if use_bnb:
@@ -380,9 +383,6 @@ class Engine:
         best = self.reset_best()
         job_steps = 0
         stats, bnb_ws = None, None
-        ev0 = torch.cuda.Event(enable_timing=True)
-        ev1 = torch.cuda.Event(enable_timing=True)
-        ev0.record()
         if mode == "exhaustive":
             src = SRC_INDEX
             use_tree = opts.kernel in ("auto", "tree", "bnb") and self._tree_ok(prob)

@@ -26,7 +26,7 @@ import numpy as np
 
 from . import domain as D
 from . import errors as E
-from .engine import SRC_EXPLICIT, SRC_INDEX, SRC_SEED, SRC_SUBSTREAM, Engine, NativeProblem, SearchResult
+from .engine import SRC_EXPLICIT, SRC_INDEX, SRC_SEED, Engine, NativeProblem, SearchResult
 from .problem import TIME_GRID, SearchProblem, SolveOptions, build_problem
 
 _ENGINES: dict = {}
