@@ -194,8 +194,29 @@ def node_eligible(job, technique, g: int, node) -> bool:
     return node.gpu_count >= g and memory_feasible(job, technique, g, node.gpu_memory)
 
 
+_CONFIGS_MEMO: dict = {}
+
+
 def feasible_configs(job, cluster, techniques: Iterable) -> list:
-    """(technique, g) runnable on some node; registration order then ascending g (core.py:165-182)."""
+    """(technique, g) runnable on some node; registration order then ascending g (core.py:165-182).
+
+    A pure function of immutable inputs (frozen dataclasses / frozen pydantic models), memoised
+    by value: re-solves and repeated solves of the same workload skip the enumeration."""
+    techniques = tuple(techniques)
+    try:
+        key = (job, cluster, techniques)
+        hit = _CONFIGS_MEMO.get(key)
+    except TypeError:                   # unhashable inputs: compute every time
+        return _feasible_configs(job, cluster, techniques)
+    if hit is None:
+        hit = tuple(_feasible_configs(job, cluster, techniques))
+        if len(_CONFIGS_MEMO) > 1 << 16:
+            _CONFIGS_MEMO.clear()
+        _CONFIGS_MEMO[key] = hit
+    return list(hit)
+
+
+def _feasible_configs(job, cluster, techniques) -> list:
     top = cluster.max_gpus_per_node
     found = []
     for tech in techniques:
