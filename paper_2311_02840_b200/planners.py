@@ -259,12 +259,31 @@ def _best_runtime_by_g(prob: SearchProblem, j: int) -> dict:
     return out
 
 
-def optimus_marginal_gain(prob: SearchProblem, j: int, g: int, best=None) -> float:
-    """best_runtime(g) - best_runtime(g+1), clamped at 0; 0 if g+1 is infeasible."""
+def _problem_gain(prob: SearchProblem, j: int, g: int, best=None) -> float:
+    """Marginal gain on a marshalled problem (runtimes already include remaining batches)."""
     best = best if best is not None else _best_runtime_by_g(prob, j)
     if g not in best or (g + 1) not in best:
         return 0.0
     return max(0.0, best[g][0] - best[g + 1][0])
+
+
+def optimus_marginal_gain(table, job, g: int, remaining_batches: int | None = None) -> float:
+    """SPEC.md:303-311: best_runtime(job, g) - best_runtime(job, g+1), best_runtime = least
+    (latency x remaining batches) over the techniques profiled at that g; 0 if g+1 (or g) has no
+    finite entry, and never negative (a harmful GPU has no gain)."""
+    import math
+
+    rem = int(job.total_batches if remaining_batches is None else remaining_batches)
+
+    def best_rt(k):
+        lats = [lat for (jid, _tech, gg), lat in table.entries.items() if jid == job.id and gg == k
+                and math.isfinite(lat)]
+        return min(lats) * rem if lats else None
+
+    a, b = best_rt(g), best_rt(g + 1)
+    if a is None or b is None:
+        return 0.0
+    return max(0.0, a - b)
 
 
 def optimus_allocation(prob: SearchProblem) -> tuple:
@@ -298,7 +317,7 @@ def optimus_allocation(prob: SearchProblem) -> tuple:
             for k in wave:
                 if alloc[k] + 1 > node_max:
                     continue
-                gain = optimus_marginal_gain(prob, k, alloc[k], best[k])
+                gain = _problem_gain(prob, k, alloc[k], best[k])
                 if gain > pick_gain:
                     pick, pick_gain = k, gain
             if pick < 0:

@@ -143,3 +143,19 @@ def test_lower_bound_never_exceeds_the_optimum():
             op.init_free = [[rng.randint(0, 3) for _ in range(n)] for n in nodes]
         ms, _ = C.CProblem(op).search()
         assert to_search_problem(op).lower_bound() <= ms, trial
+
+
+def test_optimus_marginal_gain_spec_examples():
+    """latency halving g=1 -> 2, 1000 batches, base 1 s -> 500 s; g at the node
+    maximum -> 0; a slower g+1 -> clamped to 0."""
+    from paper_2311_02840_b200 import planners as PL
+    from paper_2311_02840_b200.profiling import ProfileTable
+
+    job = D.JobSpec("a", 1000, 1.0, 1.0)
+    t = ProfileTable({("a", "t", 1): 1.0, ("a", "t", 2): 0.5, ("a", "u", 2): 0.6, ("a", "t", 3): 0.55,
+                      ("a", "t", 4): float("inf")}, "x")
+    assert PL.optimus_marginal_gain(t, job, 1, 1000) == 500.0
+    assert PL.optimus_marginal_gain(t, job, 1) == 500.0                 # default: total batches
+    assert PL.optimus_marginal_gain(t, job, 2, 1000) == 0.0              # 0.55 > 0.5: harmful GPU
+    assert PL.optimus_marginal_gain(t, job, 3, 1000) == 0.0              # g+1 infeasible
+    assert PL.optimus_marginal_gain(t, job, 8, 1000) == 0.0              # beyond the table
