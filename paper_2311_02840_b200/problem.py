@@ -46,7 +46,7 @@ class SolveOptions:
     delta: float | None = None          # explicit interval length (seconds)
     prune: bool | None = None           # None: on for single-node clusters
     search: str = "auto"                # auto | exhaustive | sampled | local
-    max_exhaustive: int = 1 << 38       # auto -> full scan when the space is <= this (~10 s worst case)
+    max_exhaustive: int = 1 << 36       # auto -> full scan when the space is <= this (~2 s worst case)
     max_bnb: int = 1 << 52              # auto -> exact bound-and-prune (one node, grid) up to this
     budget: int = 1 << 28               # sampled candidates when not exhaustive
     seed: int = 7                       # sampled stream: candidate i = substream(seed, i)
