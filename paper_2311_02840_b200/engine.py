@@ -415,18 +415,21 @@ class Engine:
             target = prob.lower_bound() if nprob.grid else -1.0
             off = ctypes.c_size_t()
             self._check(self.lib.sat_ls_counter_offset(nprob.ref, ctypes.byref(off)))
-            wave = max(1, min(int(opts.wave), n_idx))
-            rounds_total, walkers_done = 0, 0
-            for w0 in range(0, n_idx, wave):
+            # geometric waves (wave, 4 x wave, 16 x wave, ...): a small first wave keeps easy
+            # problems cheap, larger later waves keep the GPU full when the bound is not met
+            wave = max(1, int(opts.wave))
+            rounds_total, walkers_done, waves = 0, 0, 0
+            w0 = 0
+            while w0 < n_idx:
                 w1 = min(n_idx, w0 + wave)
                 a, b = _shard(w1 - w0, rank, world)
                 self.local_search(nprob, src, seed_used, w0 + a, w0 + b, opts.max_rounds, best)
                 rounds_total += int(self._ws[off.value:off.value + 8].view(torch.int64).item())
-                walkers_done = w1
+                walkers_done, waves, w0, wave = w1, waves + 1, w1, wave * 4
                 k = int(_combine(best, True, group, world)[0])
                 if k != INT64_MAX and (k >> idx_bits) <= target:
                     break
-            stats = {"walkers": walkers_done, "waves": (walkers_done + wave - 1) // wave, "rounds": rounds_total,
+            stats = {"walkers": walkers_done, "waves": waves, "rounds": rounds_total,
                      "moves_scheduled_max": rounds_total * 32, "lower_bound": target}
             kernel, evaluated = "local", walkers_done
         else:

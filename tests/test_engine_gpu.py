@@ -322,8 +322,9 @@ def test_edge_cases(eng):
 
 
 # --------------------------------------------------------------------------- local search
-@pytest.mark.parametrize("name", ["cfg1", "cfg3", "small4_2x2", "cfg4", "hetero6", "cfg5"])
-def test_local_search_walkers_match_oracle(eng, name):
+@pytest.mark.parametrize("name,seed", [("cfg1", 7), ("cfg3", 7), ("cfg3", 11), ("small4_2x2", 7), ("cfg4", 7),
+                                       ("cfg4", 2**63 + 5), ("hetero6", 7), ("cfg5", 7)])
+def test_local_search_walkers_match_oracle(eng, name, seed):
     """Every walker's whole descent (start = stream candidate, moves, tie-breaks, stop rule)
     equals the oracle's restatement: same final candidate and makespan; and the search key
     over a walker range equals the oracle's."""
@@ -334,14 +335,14 @@ def test_local_search_walkers_match_oracle(eng, name):
     bits, _ = prob.key_bits(1 << 20)
     nprob = EN.NativeProblem(prob, bits)
     for walker in range(0, W, max(1, W // 6)):
-        ms, o, r, _ = cp.local_search(walker, "substream", 7, rounds)
-        go, gr = eng.local_search_state(nprob, EN.SRC_SUBSTREAM, 7, walker, rounds)
+        ms, o, r, _ = cp.local_search(walker, "substream", seed, rounds)
+        go, gr = eng.local_search_state(nprob, EN.SRC_SUBSTREAM, seed, walker, rounds)
         assert (go, gr) == (o, r), (name, walker)
         assert cp.eval(go, gr)[0] == ms
     best = eng.reset_best()
-    eng.local_search(nprob, EN.SRC_SUBSTREAM, 7, 0, W, rounds, best)
+    eng.local_search(nprob, EN.SRC_SUBSTREAM, seed, 0, W, rounds, best)
     k = int(best.cpu().numpy().view(np.uint64)[0])
-    assert (float(k >> bits), k & ((1 << bits) - 1)) == cp.ls_search("substream", 7, 0, W, rounds)
+    assert (float(k >> bits), k & ((1 << bits) - 1)) == cp.ls_search("substream", seed, 0, W, rounds)
 
 
 def test_local_search_seed_source_and_release(eng):
