@@ -201,3 +201,23 @@ def test_bnb_beyond_the_worst_case_key_width():
     local = PL.solve(t, w)                                  # default: local search for this size
     assert exact.makespan <= local.makespan
     assert exact.lower_bound == exact.makespan
+
+
+@pytest.mark.parametrize("shape", [(1, [1]), (1, [8]), (2, [2]), (3, [8, 4, 2]), (5, [8, 4, 2]),
+                                   (4, [1, 1, 1, 1]), (3, [32]), (6, [4, 4])])
+def test_public_api_edge_shapes(shape):
+    """plan_saturn on unusual shapes (single job, single GPU nodes, mixed node sizes, a 32-GPU
+    node): a valid plan whose makespan is the oracle's exhaustive optimum."""
+    from paper_2311_02840_b200.workloads import TECHNIQUES_4
+
+    n_jobs, sizes = shape
+    jobs = tuple(D.JobSpec(f"j{j}", 100 * (1 + j), 1.0 + 0.3 * j, 10.0 + 25.0 * (j % 2), 2.0) for j in range(n_jobs))
+    nodes = tuple(D.NodeSpec(f"n{i}", g, 40.0) for i, g in enumerate(sizes))
+    w = D.Workload(jobs, D.ClusterSpec(nodes), TECHNIQUES_4)
+    t = build_profile_table(w, SyntheticExecutor(w.cluster))
+    sol = PL.solve(t, w)
+    D.check_plan(sol.plan, w, sol.runtimes)
+    op = O.build(t.entries, w)
+    if op.space <= 3_000_000:
+        assert sol.makespan == C.CProblem(op).search()[0], (shape, sol.search.kernel)
+    assert sol.lower_bound <= sol.makespan
