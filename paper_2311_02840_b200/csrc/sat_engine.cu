@@ -15,17 +15,20 @@
 // which is the sorted merge of a[g..] with g copies of e (proof in DESIGN.md).
 // Every slot update is one min and one max, with no data-dependent branches.
 //
-// Three kernel families:
-//   k_tree<G>  (sat_tree.cuh) prefix-shared exhaustive walk for one node in grid time:
+// Kernel families:
+//   k_tree<G, BNB>  (sat_tree.cuh) prefix-shared exhaustive walk for one node in grid time:
 //       each lane owns a distinct prefix (first P jobs of the order + their options)
 //       and the warp walks the remaining J-P jobs' orders x options in lock step, so
 //       the job sequence and gang sizes are warp-uniform and only free times differ
-//       per lane.  Every candidate still gets its full makespan computed.
-//   k_cand<T, SRC, G, MULTI>  (sat_cand.cuh) one candidate per thread: decoded on the
+//       per lane.  Every candidate still gets its full makespan computed.  BNB = the
+//       bound-and-prune variant (same result key, subtrees above the best skipped).
+//   k_cand<T, SRC, G, L>  (sat_cand.cuh) one candidate per thread: decoded on the
 //       device from an index (mixed radix + Lehmer, odometer-advanced) or a SplitMix64
 //       stream, list-scheduled with its sorted free times in registers / its own
 //       shared-memory column.  Multi-node, releases, int32 grid or fp64 time.  The
 //       search kernel for everything k_tree does not cover (sampled configs).
+//   k_ls<SRC, G, L>  (sat_cand.cuh) local search: a walker per warp, a move per lane,
+//       each move scheduled by the same list scheduler as k_cand.
 //   k_generic<T, SRC, RECORD=true>  one candidate per W-lane warp segment (lane = GPU
 //       slot); records each placement (option, node, start) of a few given candidates
 //       -- sat_schedule, i.e. decode_plan of the winner and fixed-plan evaluation.
