@@ -238,7 +238,7 @@ class Engine:
                 return P
         return 0
 
-    def seed_bound(self, prob: SearchProblem, budget: int = 1 << 16, seed: int = 7) -> int:
+    def seed_bound(self, prob: SearchProblem, budget: int = 1 << 20, seed: int = 7) -> int:
         """Best makespan of a quick sampled search: an achievable upper bound (grid intervals).
         Seeding *best with (U << idx_bits | max index) lets any real candidate with makespan <= U
         replace it while the bound prunes from the start."""
