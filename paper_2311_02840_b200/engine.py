@@ -248,7 +248,14 @@ class Engine:
         tmp = self.reset_best(torch.empty(2, dtype=torch.int64, device=self.device))
         self.search_sampled(sprob, SRC_SUBSTREAM, seed, 0, budget, tmp)
         k = int(tmp[0].item()) & ((1 << 64) - 1)
-        return k >> s_bits
+        bound = k >> s_bits
+        if prob.J >= 10 and prob.time_mode == TIME_GRID:
+            # long orders: a local-search wave (~ms) usually reaches the optimum value, which
+            # makes the exact search prune far more (seconds saved at 10-12 jobs)
+            self.reset_best(tmp)
+            self.local_search(sprob, SRC_SUBSTREAM, seed, 0, 4096, 4096, tmp)
+            bound = min(bound, (int(tmp[0].item()) & ((1 << 64) - 1)) >> s_bits)
+        return bound
 
     def seed_upper_bound(self, prob: SearchProblem, nprob: NativeProblem, best, budget: int = 1 << 16,
                          seed: int = 7):
