@@ -279,7 +279,7 @@ class DeviceSolve:
         if self.use_tree:
             # per rank ~22 warp tasks per resident warp at least (dynamic cursor balance)
             self.info = eng.tree_plan(self.nprob, eng.tree_prefix(self.nprob, (1 << 17) * world) if world > 1 else 0)
-            self.a, self.b = EN._shard(self.info.n_tasks, rank, world)
+            self.a, self.b = eng.tree_shard(self.nprob, self.info.prefix_len, rank, world)   # work-balanced
             self.n_cand = self.info.n_candidates
             merges = self.info.n_job_steps - self.info.n_candidates
             # algorithmic INT32 work of the prefix-shared walk:

@@ -128,6 +128,12 @@ int sat_search_tree(const sat_problem_t *p, int32_t prefix_len,
                     uint64_t task_lo, uint64_t task_hi,
                     sat_best_t *d_best, void *d_ws, size_t ws_bytes, void *stream);
 
+/* Rank `rank` of `world`'s share of the layout's warp tasks: a contiguous range whose
+ * full-scan work (placements) is 1/world of the total, so ranks finish together (task costs
+ * differ by set; an even split of the task count leaves up to ~25 % imbalance at 8 ranks). */
+int sat_tree_shard(const sat_problem_t *p, int32_t prefix_len, int32_t world, int32_t rank,
+                   uint64_t *task_lo, uint64_t *task_hi);
+
 /* Bound-and-prune over the same layout (replaces branch_and_bound):
  * subtrees whose makespan lower bound exceeds the best makespan found so far are
  * skipped; every candidate that could tie or beat the best is still scheduled, so the

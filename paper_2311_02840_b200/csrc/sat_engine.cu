@@ -743,6 +743,45 @@ static int search_tree_impl(const sat_problem_t *p, int32_t prefix_len, uint64_t
 
 size_t sat_tree_param_bytes(void) { return sizeof(TreeParams); }
 
+int sat_tree_shard(const sat_problem_t *p, int32_t prefix_len, int32_t world, int32_t rank, uint64_t *task_lo,
+                   uint64_t *task_hi) {
+    int st = validate(p);
+    if (st) return st;
+    if (world < 1 || rank < 0 || rank >= world || !task_lo || !task_hi) return SAT_ERR_INVALID;
+    TreeLayout lay;
+    st = tree_layout(p, prefix_len, lay);
+    if (st) return st;
+    const int J = p->J;
+    const uint32_t full = (1u << J) - 1u;
+    std::vector<int64_t> memo((size_t)1 << J, -1);
+    // per-task work of set s: 32 lanes x (P prefix placements + the suffix walk)
+    std::vector<long double> per_task(lay.sets.size());
+    long double total = 0;
+    for (size_t s = 0; s < lay.sets.size(); ++s) {
+        per_task[s] = 32.0L * ((long double)lay.P + (long double)walk_nodes(p->radix, full & ~lay.sets[s], memo, full));
+        total += per_task[s] * (long double)(lay.cum[s + 1] - lay.cum[s]);
+    }
+    auto boundary = [&](int32_t r) -> uint64_t {      // first task whose prefix work >= total * r / world
+        if (r <= 0) return 0;
+        if (r >= world) return lay.n_tasks;
+        const long double target = total * (long double)r / (long double)world;
+        long double acc = 0;
+        for (size_t s = 0; s < lay.sets.size(); ++s) {
+            const uint64_t nt = lay.cum[s + 1] - lay.cum[s];
+            const long double c = per_task[s] * (long double)nt;
+            if (acc + c >= target) {
+                const uint64_t k = (uint64_t)((target - acc) / per_task[s]);
+                return lay.cum[s] + std::min<uint64_t>(k, nt);
+            }
+            acc += c;
+        }
+        return lay.n_tasks;
+    };
+    *task_lo = boundary(rank);
+    *task_hi = boundary(rank + 1);
+    return SAT_OK;
+}
+
 int sat_ls_counter_offset(const sat_problem_t *p, size_t *offset) {
     int st = validate(p);
     if (st) return st;

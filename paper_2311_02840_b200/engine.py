@@ -65,6 +65,7 @@ _SIGS = {
     "sat_tree_param_bytes": ([], ctypes.c_size_t),
     "sat_local_search": ([_vp, _i32, _u64, _u64, _u64, _i32, _vp, _vp, _vp, ctypes.c_size_t, _vp], _i32),
     "sat_ls_counter_offset": ([_vp, _vp], _i32),
+    "sat_tree_shard": ([_vp, _i32, _i32, _i32, _vp, _vp], _i32),
 }
 
 _LIB = None
@@ -222,6 +223,16 @@ class Engine:
                                             _vp(ws), wsb, _vp(self.stream())), what="sat_search_bnb")
         self.launches += 1
         return self._ws
+
+    def tree_shard(self, nprob, prefix_len: int, rank: int, world: int) -> tuple:
+        """Work-balanced contiguous task range of this rank (sat_tree_shard)."""
+        if world == 1:
+            info = self.tree_plan(nprob, prefix_len)
+            return 0, info.n_tasks
+        lo, hi = ctypes.c_uint64(), ctypes.c_uint64()
+        self._check(self.lib.sat_tree_shard(nprob.ref, prefix_len, world, rank, ctypes.byref(lo), ctypes.byref(hi)),
+                    what="sat_tree_shard")
+        return lo.value, hi.value
 
     def tree_prefix(self, nprob, min_tasks: int) -> int:
         """Shortest lane prefix with at least `min_tasks` warp tasks (0 = the library's choice)."""
@@ -398,14 +409,14 @@ class Engine:
             if use_bnb:
                 P = self.bnb_prefix(nprob, (1 << 15) * world)       # enough tasks on every rank
                 info = self.tree_plan(nprob, P)
-                a, b = _shard(info.n_tasks, rank, world)
+                a, b = self.tree_shard(nprob, info.prefix_len, rank, world)
                 best[0:1].fill_((seed_ms << idx_bits) | ((1 << idx_bits) - 1))
                 bnb_ws = self.search_bnb(nprob, info.prefix_len, a, b, best)
                 stats = {"prefix_len": info.prefix_len, "tasks": b - a}
                 kernel, evaluated = "bnb", info.n_candidates
             elif use_tree:
                 info = self.tree_plan(nprob, self.tree_prefix(nprob, (1 << 17) * world) if world > 1 else 0)
-                a, b = _shard(info.n_tasks, rank, world)
+                a, b = self.tree_shard(nprob, info.prefix_len, rank, world)
                 self.search_tree(nprob, info.prefix_len, a, b, best)
                 kernel, evaluated, job_steps = "tree", info.n_candidates, info.n_job_steps
             else:

@@ -82,3 +82,44 @@ def test_validation_codes(lib):
     t4 = build_profile_table(w4, SyntheticExecutor(w4.cluster))
     p4 = EN.NativeProblem(build_problem(t4, w4), 20)
     assert lib.sat_tree_plan(p4.ref, 0, ctypes.byref(info)) == EN.SAT_ERR_UNSUPPORTED
+
+
+def test_tree_shard_partitions_and_balances_work(lib):
+    """sat_tree_shard: contiguous ranges covering every warp task once, each with ~1/world of
+    the full-scan work (host-only entry point)."""
+    w, _ = golden_workload("cfg1")
+    t = build_profile_table(w, SyntheticExecutor(w.cluster))
+    prob = build_problem(t, w)
+    bits, _ = prob.key_bits(prob.space)
+    nprob = EN.NativeProblem(prob, bits)
+    info = EN.SatTreeInfo()
+    assert lib.sat_tree_plan(nprob.ref, 5, ctypes.byref(info)) == 0
+    radix, J, P = [int(r) for r in prob.radix], prob.J, 5
+    memo = {}
+
+    def walk(rem):
+        if rem == 0:
+            return 0
+        if rem not in memo:
+            memo[rem] = sum(radix[j] * (1 + walk(rem & ~(1 << j))) for j in range(J) if rem >> j & 1)
+        return memo[rem]
+
+    per_task = []       # cost of every warp task, in layout order (sets in mask order)
+    for S in range(1 << J):
+        if bin(S).count("1") != P:
+            continue
+        npref = math.factorial(P) * math.prod(radix[j] for j in range(J) if S >> j & 1)
+        per_task += [P + walk(((1 << J) - 1) & ~S)] * ((npref + 31) // 32)
+    assert len(per_task) == info.n_tasks
+    total = sum(per_task)
+    for world in (2, 3, 8):
+        prev = 0
+        for r in range(world):
+            lo, hi = ctypes.c_uint64(), ctypes.c_uint64()
+            assert lib.sat_tree_shard(nprob.ref, 5, world, r, ctypes.byref(lo), ctypes.byref(hi)) == 0
+            assert lo.value == prev
+            prev = hi.value
+            share = sum(per_task[lo.value:hi.value]) / (total / world)
+            assert 0.98 < share < 1.02, (world, r, share)
+        assert prev == info.n_tasks
+    assert lib.sat_tree_shard(nprob.ref, 5, 2, 2, ctypes.byref(lo), ctypes.byref(hi)) == EN.SAT_ERR_INVALID
