@@ -327,6 +327,12 @@ k_tree(const __grid_constant__ TreeParams p) {
             walk_fixed<G, BNB, 1>(p, wbase, lane, 0, Q, unplaced, base, lane_ok, Bbuf, sdg, lb, U, n_pairs);
         } else if (Q == 4) {
             walk_fixed<G, BNB, 2>(p, wbase, lane, 0, Q, unplaced, base, lane_ok, Bbuf, sdg, lb, U, n_pairs);
+        } else if (BNB && Q == 5) {
+            walk_fixed<G, BNB, 3>(p, wbase, lane, 0, Q, unplaced, base, lane_ok, Bbuf, sdg, lb, U, n_pairs);
+        } else if (BNB && Q == 6) {
+            walk_fixed<G, BNB, 4>(p, wbase, lane, 0, Q, unplaced, base, lane_ok, Bbuf, sdg, lb, U, n_pairs);
+        } else if (BNB && Q == 7) {
+            walk_fixed<G, BNB, 5>(p, wbase, lane, 0, Q, unplaced, base, lane_ok, Bbuf, sdg, lb, U, n_pairs);
         } else {
             uint32_t rem_st[kTreeMaxJ];
             uint64_t acc_st[kTreeMaxJ];

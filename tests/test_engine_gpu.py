@@ -360,3 +360,16 @@ def test_local_search_seed_source_and_release(eng):
         for walker in (0, 3, 11):
             ms, o, r, _ = cp.local_search(walker, "seed", 5, 4096)
             assert eng.local_search_state(nprob, EN.SRC_SEED, 5, walker, 4096) == (o, r), (trial, walker)
+
+
+def test_bnb_fixed_depth_walkers_equal_full_scan(eng):
+    """Suffixes of 5-7 jobs (fixed-depth walkers D = 3..5) on a 9-job one-node problem: the
+    bound-and-prune key equals the full scan's for every prefix length."""
+    from paper_2311_02840_b200.workloads import synthetic_workload
+
+    w = synthetic_workload(9, 1, 8)
+    t = build_profile_table(w, SyntheticExecutor(w.cluster))
+    prob = build_problem(t, w)
+    want = gpu_key(eng, prob, "tree")
+    for prefix in (2, 3, 4, 5, 6):
+        assert bnb_key(eng, prob, prefix=prefix) == want, prefix
