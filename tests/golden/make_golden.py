@@ -184,9 +184,10 @@ def plan_verdicts(w, table):
 
 
 def milp_small():
-    """HiGHS optimum (intervals) of the oracle problems of the small workloads."""
+    """HiGHS optimum (intervals) of the oracle problems of the small workloads and of config 3
+    (whose optimum the local search reaches but the simple lower bound cannot prove)."""
     out = {}
-    for name in ("cfg1", "small5_1x4", "small4_2x2", "hetero6", "tiny3_1x3"):
+    for name in ("cfg1", "cfg3", "small5_1x4", "small4_2x2", "hetero6", "tiny3_1x3"):
         spec = WORKLOADS[name]
         w = recipe(**spec)
         table = profiling.build_profile_table(w, profiling.SyntheticExecutor(w.cluster))

@@ -52,6 +52,19 @@ def test_golden_milp_values_match_oracle_search():
         assert ms == g[name]["optimum_intervals"], name
 
 
+def test_cfg3_optimum_certificate():
+    """Config 3 (16 jobs, space 3e23): the recorded HiGHS optimum is 30 intervals, one above
+    the area / longest-job bound; the MILP admits every gang schedule, so infeasibility at
+    horizon 29 proves no list schedule reaches 29 (tools/cfg3_milp_bound.py)."""
+    g = golden()["milp"]["cfg3"]
+    w, _ = golden_workload("cfg3")
+    t = build_profile_table(w, SyntheticExecutor(w.cluster))
+    prob = O.build(t.entries, w)
+    assert prob.radix == g["radix"] and g["optimum_intervals"] == 30
+    with pytest.raises(RuntimeError, match="nfeasible"):
+        O.milp_optimum(prob, horizon=29, time_limit=120.0)
+
+
 def test_single_node_random_vs_highs():
     rng = random.Random(11)
     for _ in range(40):
