@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define SAT_ABI_VERSION 2
+#define SAT_ABI_VERSION 3
 
 /* status codes (mapped to reference errors.py classes by the host layer) */
 #define SAT_OK              0
@@ -94,6 +94,8 @@ typedef struct sat_tree_info {
     uint64_t n_tasks;       /* warp tasks (32 prefixes of one set each)                      */
     uint64_t n_candidates;  /* = prod(radix) * J!                                            */
     uint64_t n_job_steps;   /* list-scheduling placements the prefix-shared walk performs    */
+    int32_t  pair_packed;   /* 1: the last-two-jobs pass runs on 16-bit pairs (ABI v3)       */
+    int32_t  reserved;
 } sat_tree_info_t;
 
 int         sat_abi_version(void);
@@ -180,6 +182,11 @@ size_t sat_tree_param_bytes(void);
  * dependent-chain IMNMX iterations on every SM; *d_ops_out = lane-ops done. */
 int sat_alu_probe(int32_t blocks, int32_t threads, int32_t iters,
                   uint64_t *d_ops_out, int32_t *d_sink, void *stream);
+
+/* The same probe on two 16-bit lanes per register (min/max .u16x2, VIMNMX.U16x2): the
+ * denominator for k_tree launches whose pair pass is packed; counts 2 ops per lane-op. */
+int sat_alu_probe16(int32_t blocks, int32_t threads, int32_t iters,
+                    uint64_t *d_ops_out, int32_t *d_sink, void *stream);
 
 #ifdef __cplusplus
 }

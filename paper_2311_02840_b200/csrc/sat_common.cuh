@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -76,8 +77,16 @@ constexpr int kTreeMaxJ = 20;
 constexpr int kTreeMaxOpt = 384;
 constexpr int kTreeMaxSets = 768;
 
+// Packed pair pass (k_tree, G <= kTreePackMaxG): two 16-bit free times per word when every
+// time the walk can produce stays below kTreePackLimit (host-checked); missing gangs and
+// padding slots hold kTreeInf16, so a slot sum b + D2 <= 0x7FFF + 0x7FFF never carries.
+constexpr uint32_t kTreeInf16 = 0x7FFFu;
+constexpr int32_t kTreePackLimit = 0x7000;
+constexpr int kTreePackMaxG = 16;
+
 struct TreeParams {
-    int32_t J, P, Q, Gr, n_sets, idx_bits, init_max, pad;
+    int32_t J, P, Q, Gr, n_sets, idx_bits, init_max;
+    int32_t packed;                   // 1: pair pass on 16-bit pairs (dgp valid)
     int32_t radix[kTreeMaxJ];
     int32_t optbase[kTreeMaxJ];
     uint64_t wJ[kTreeMaxJ];           // option-digit weight in the index: W_j * J!
@@ -87,6 +96,7 @@ struct TreeParams {
     int32_t optoff[kTreeMaxOpt];      // (g - 1) * 32: smem word offset of slot g-1
     int32_t optd[kTreeMaxOpt];
     int32_t dg[kTreeMaxJ][32];        // per job and gang size g: min duration over its options (INF: none)
+    uint32_t dgp[kTreeMaxJ][kTreePackMaxG / 2];   // dg as 16-bit pairs (gangs 2w+1, 2w+2; kTreeInf16: none)
     uint32_t set_mask[kTreeMaxSets];
     uint64_t set_cum[kTreeMaxSets + 1];  // cumulative warp tasks
     uint64_t set_prod[kTreeMaxSets];     // prod of radix over the set

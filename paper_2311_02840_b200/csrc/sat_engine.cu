@@ -228,6 +228,28 @@ __global__ void k_alu_probe(int iters, unsigned long long *ops, int32_t *sink) {
         *ops = (unsigned long long)gridDim.x * blockDim.x * (unsigned long long)iters * 32ull;
 }
 
+// the same chains on two 16-bit lanes per register (min/max .u16x2 -> VIMNMX.U16x2): the
+// peak of k_tree's packed pair pass, counted as 2 ops per lane per instruction
+__global__ void k_alu_probe16(int iters, unsigned long long *ops, int32_t *sink) {
+    uint32_t v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = (uint32_t)threadIdx.x * 0x10001u + (uint32_t)i;
+    const uint32_t lo = (blockIdx.x & 7u) * 0x10001u, hi = (blockIdx.x | 1024u) * 0x10001u;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            asm volatile("min.u16x2 %0, %0, %1;" : "+r"(v[i]) : "r"(hi));
+            asm volatile("max.u16x2 %0, %0, %1;" : "+r"(v[i]) : "r"(lo));
+        }
+    }
+    uint32_t r = 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) r ^= v[i];
+    if (r == 0x7fffffffu) sink[0] = (int32_t)r;
+    if (threadIdx.x == 0 && blockIdx.x == 0)
+        *ops = (unsigned long long)gridDim.x * blockDim.x * (unsigned long long)iters * 64ull;
+}
+
 // ---------------------------------------------------------------------------
 // host side: validation, packing, launch sizing
 // ---------------------------------------------------------------------------
@@ -648,6 +670,25 @@ int sat_schedule(const sat_problem_t *p, int32_t source, uint64_t seed, const ui
     }
 }
 
+// k_tree's pair pass runs on 16-bit pairs when every free time a schedule can reach (the
+// latest initial free time + the sum of every job's longest option) stays below
+// kTreePackLimit, on nodes of <= kTreePackMaxG GPUs (SATURN_TREE_PACKED=0 forces the
+// 32-bit pass, for A/B checks)
+static bool tree_pair_packed(const sat_problem_t *p) {
+    const int G = p->node_gpus[0];
+    if (G < 2 || G > kTreePackMaxG) return false;
+    const char *env = std::getenv("SATURN_TREE_PACKED");
+    if (env && env[0] == '0') return false;
+    int64_t horizon = 0;
+    for (int i = 0; i < G; ++i) horizon = std::max<int64_t>(horizon, p->init_free_i32 ? p->init_free_i32[i] : 0);
+    for (int j = 0; j < p->J; ++j) {
+        int32_t dmax = 0;
+        for (int o = 0; o < p->radix[j]; ++o) dmax = std::max(dmax, p->dur_i32[j * p->Cmax + o]);
+        horizon += dmax;
+    }
+    return horizon < kTreePackLimit;
+}
+
 int sat_tree_plan(const sat_problem_t *p, int32_t prefix_len, sat_tree_info_t *info) {
     int st = validate(p);
     if (st) return st;
@@ -660,6 +701,8 @@ int sat_tree_plan(const sat_problem_t *p, int32_t prefix_len, sat_tree_info_t *i
     info->n_tasks = lay.n_tasks;
     info->n_candidates = lay.n_cand;
     info->n_job_steps = lay.n_steps;
+    info->pair_packed = tree_pair_packed(p) ? 1 : 0;
+    info->reserved = 0;
     return SAT_OK;
 }
 
@@ -711,6 +754,14 @@ static int search_tree_impl(const sat_problem_t *p, int32_t prefix_len, uint64_t
         if (real) imax = std::max(imax, v);
     }
     tp.init_max = imax;
+    tp.packed = tree_pair_packed(p) ? 1 : 0;
+    for (int j = 0; j < J; ++j)
+        for (int w = 0; w < kTreePackMaxG / 2; ++w) {
+            uint32_t lo = kTreeInf16, hi = kTreeInf16;
+            if (2 * w < tp.Gr && tp.dg[j][2 * w] < SAT_INF_I32) lo = (uint32_t)tp.dg[j][2 * w];
+            if (2 * w + 1 < tp.Gr && tp.dg[j][2 * w + 1] < SAT_INF_I32) hi = (uint32_t)tp.dg[j][2 * w + 1];
+            tp.dgp[j][w] = tp.packed ? (lo | (hi << 16)) : 0u;
+        }
     for (size_t s = 0; s < lay.sets.size(); ++s) {
         tp.set_mask[s] = lay.sets[s];
         tp.set_cum[s] = lay.cum[s];
@@ -826,6 +877,13 @@ int sat_alu_probe(int32_t blocks, int32_t threads, int32_t iters, uint64_t *d_op
                   void *stream) {
     if (blocks < 1 || threads < 32 || iters < 1 || !d_ops_out || !d_sink) return SAT_ERR_INVALID;
     k_alu_probe<<<blocks, threads, 0, (cudaStream_t)stream>>>(iters, (unsigned long long *)d_ops_out, d_sink);
+    return cudaGetLastError() == cudaSuccess ? SAT_OK : SAT_ERR_CUDA;
+}
+
+int sat_alu_probe16(int32_t blocks, int32_t threads, int32_t iters, uint64_t *d_ops_out, int32_t *d_sink,
+                    void *stream) {
+    if (blocks < 1 || threads < 32 || iters < 1 || !d_ops_out || !d_sink) return SAT_ERR_INVALID;
+    k_alu_probe16<<<blocks, threads, 0, (cudaStream_t)stream>>>(iters, (unsigned long long *)d_ops_out, d_sink);
     return cudaGetLastError() == cudaSuccess ? SAT_OK : SAT_ERR_CUDA;
 }
 

@@ -65,11 +65,58 @@ __device__ __forceinline__ void side_fold(const int32_t (&A)[G], const int32_t (
     }
 }
 
+// ---- packed pair pass: the same value on two 16-bit slots per word ----
+// P0[w] = (A[2w], A[2w+1]), P1[w] = (A[2w+1], A[2w+2]) (slots >= G: kTreeInf16), so the
+// shift by a compile-time g is a register choice (P0 for even g, P1 for odd g); per word
+// VIMNMX.U16x2 min + max and one VIADDMNMX.U16x2 cover two slots.  The group's makespan
+// max(B[G-1], min_k(B[k] + D2[k])) distributes over the two halves of the running min:
+// max(bl, min(h0, h1)) = min(max(bl, h0), max(bl, h1)), so halves are folded once per node.
+template <int G>
+struct Pk { static constexpr int W = (G + 1) / 2; };
+
+template <int G, int g>
+__device__ __forceinline__ uint32_t group_value16(const uint32_t (&P0)[Pk<G>::W], const uint32_t (&P1)[Pk<G>::W],
+                                                  const int32_t (&A)[G], uint32_t d2,
+                                                  const uint32_t (&D2)[Pk<G>::W]) {
+    constexpr int W = Pk<G>::W;
+    const uint32_t e2 = (uint32_t)A[g - 1] * 0x10001u + d2;      // e in both halves (no carry: e < 2^15)
+    uint32_t m2 = 0xFFFFFFFFu, bl2 = 0u;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+        const int src = 2 * w + g;                                // shifted slot of the low half
+        uint32_t b;
+        if (src >= G) {
+            b = e2;                                               // min(INF, e)
+        } else {
+            const uint32_t s = (g & 1) ? P1[(src - 1) / 2 < W ? (src - 1) / 2 : 0] : P0[src / 2 < W ? src / 2 : 0];
+            b = __vminu2(s, e2);
+        }
+        if (2 * w + 1 >= g) b = __vmaxu2(P0[w], b);               // slots k >= g keep max(A[k], .)
+        m2 = __viaddmin_u16x2(b, D2[w], m2);
+        if (w == (G - 1) / 2) bl2 = __byte_perm(b, 0u, ((G - 1) & 1) ? 0x3232u : 0x1010u);
+    }
+    return __vmaxu2(m2, bl2);
+}
+
+template <int G, int g>
+__device__ __forceinline__ void side_fold16(const uint32_t (&P0)[Pk<G>::W], const uint32_t (&P1)[Pk<G>::W],
+                                            const int32_t (&A)[G], const int32_t *D1,
+                                            const uint32_t (&D2)[Pk<G>::W], uint32_t &v2) {
+    if constexpr (g <= G) {
+        const int32_t d = D1[g - 1];                               // uniform (parameter block)
+        if (d < SAT_INF_I32) v2 = __vminu2(v2, group_value16<G, g>(P0, P1, A, (uint32_t)d * 0x10001u, D2));
+        side_fold16<G, g + 1>(P0, P1, A, D1, D2, v2);
+    }
+}
+
 // Exact pass over a pair node: per (first job, option) group, the makespan and the lowest
 // option of the last job reaching it, with the full candidate index for the tie-break.
 template <int G>
-__device__ __noinline__ void tree_pair_exact(const TreeParams &p, const int32_t (&A)[G], int32_t *B, int ja,
+__device__ __noinline__ void tree_pair_exact(const TreeParams &p, const int32_t *U, int32_t *B, int ja,
                                              int jb, uint64_t base, LaneBest &lb) {
+    int32_t A[G];                                    // reloaded from the column: no spill of A per node
+#pragma unroll
+    for (int i = 0; i < G; ++i) A[i] = U[i * 32];
 #pragma unroll 1
     for (int side = 0; side < 2; ++side) {
         const int j1 = side ? jb : ja;
@@ -97,6 +144,19 @@ __device__ __noinline__ void tree_pair_exact(const TreeParams &p, const int32_t 
     }
 }
 
+// A pair node's candidates have indices >= base and makespans >= v: it can only matter
+// when (v, base) ties or beats the lane's best and the best any warp has published so far
+// (keys order by makespan, then index; an unset index is ~0, so ties with a seed bound
+// pass).  The published key is read only for nodes that pass the lane test.
+__device__ __forceinline__ bool pair_needs_exact(const TreeParams &p, int32_t v, uint64_t base,
+                                                 const LaneBest &lb) {
+    if (!(v < lb.ms || (v == lb.ms && base <= lb.ix))) return false;
+    const unsigned long long hi = *reinterpret_cast<volatile unsigned long long *>(&p.best->hi);
+    if (hi == ~0ull) return true;
+    const int32_t pms = (int32_t)(hi >> p.idx_bits);
+    return v < pms || (v == pms && base <= (hi & ((1ull << p.idx_bits) - 1ull)));
+}
+
 // Two jobs left (a < b): both orders x all options of the first x all options of the
 // second.  Fast value pass in registers (per-gang minimum durations are exact for the
 // value: a shorter first job never hurts, a shorter last job never hurts); the exact pass
@@ -105,19 +165,43 @@ template <int G>
 __device__ __forceinline__ void tree_pair(const TreeParams &p, const int32_t *U, int32_t *B,
                                           const int32_t *sdg, uint32_t rem, uint64_t base, bool valid,
                                           LaneBest &lb) {
-    int32_t A[G], Da[G], Db[G];
+    int32_t A[G];
     const int ja = __ffs(rem) - 1;
     const int jb = 31 - __clz(rem);
 #pragma unroll
+    for (int i = 0; i < G; ++i) A[i] = U[i * 32];
+    int32_t v = SAT_INF_I32;
+    if constexpr (G <= kTreePackMaxG && G >= 2) {
+        if (p.packed) {
+            constexpr int W = Pk<G>::W;
+            uint32_t P0[W], P1[W], Pa[W], Pb[W];
+#pragma unroll
+            for (int w = 0; w < W; ++w) {
+                const uint32_t a0 = (uint32_t)A[2 * w];
+                const uint32_t a1 = 2 * w + 1 < G ? (uint32_t)A[2 * w + 1 < G ? 2 * w + 1 : 0] : kTreeInf16;
+                const uint32_t a2 = 2 * w + 2 < G ? (uint32_t)A[2 * w + 2 < G ? 2 * w + 2 : 0] : kTreeInf16;
+                P0[w] = __byte_perm(a0, a1, 0x5410u);
+                P1[w] = __byte_perm(a1, a2, 0x5410u);
+                Pa[w] = p.dgp[ja][w];
+                Pb[w] = p.dgp[jb][w];
+            }
+            uint32_t v2 = 0xFFFFFFFFu;
+            side_fold16<G, 1>(P0, P1, A, sdg + ja * 32, Pb, v2);
+            side_fold16<G, 1>(P0, P1, A, sdg + jb * 32, Pa, v2);
+            v = (int32_t)min(v2 & 0xFFFFu, v2 >> 16);
+            if (valid && pair_needs_exact(p, v, base, lb)) tree_pair_exact<G>(p, U, B, ja, jb, base, lb);
+            return;
+        }
+    }
+    int32_t Da[G], Db[G];
+#pragma unroll
     for (int i = 0; i < G; ++i) {
-        A[i] = U[i * 32];
         Da[i] = sdg[ja * 32 + i];
         Db[i] = sdg[jb * 32 + i];
     }
-    int32_t v = SAT_INF_I32;
     side_fold<G, 1>(A, Da, Db, v);
     side_fold<G, 1>(A, Db, Da, v);
-    if (valid && v <= lb.ms) tree_pair_exact<G>(p, A, B, ja, jb, base, lb);
+    if (valid && pair_needs_exact(p, v, base, lb)) tree_pair_exact<G>(p, U, B, ja, jb, base, lb);
 }
 
 // Upper-level merge with a warp-uniform runtime gang size, smem column to smem column.
@@ -384,8 +468,9 @@ k_tree(const __grid_constant__ TreeParams p) {
             }
         }
         __syncwarp();
-        if constexpr (BNB) {
-            // publish an improvement right away so every warp prunes against it
+        {
+            // publish an improvement right away: every warp prunes (bnb) and skips exact
+            // pair passes (both modes) against it
             uint64_t key = (lb.ix != ~0ull) ? (((uint64_t)(uint32_t)lb.ms << p.idx_bits) | lb.ix) : ~0ull;
             for (int x = 16; x >= 1; x >>= 1) {
                 const uint64_t o = shfl_u64(key, lane ^ x);

@@ -43,7 +43,7 @@ class SatProblem(ctypes.Structure):
 
 class SatTreeInfo(ctypes.Structure):
     _fields_ = [("prefix_len", _i32), ("n_sets", _i32), ("n_tasks", _u64),
-                ("n_candidates", _u64), ("n_job_steps", _u64)]
+                ("n_candidates", _u64), ("n_job_steps", _u64), ("pair_packed", _i32), ("reserved", _i32)]
 
 
 # exported symbols and their signatures (the header is the source of truth;
@@ -62,6 +62,7 @@ _SIGS = {
     "sat_schedule": ([_vp, _i32, _u64, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                       ctypes.c_size_t, _vp], _i32),
     "sat_alu_probe": ([_i32, _i32, _i32, _vp, _vp, _vp], _i32),
+    "sat_alu_probe16": ([_i32, _i32, _i32, _vp, _vp, _vp], _i32),
     "sat_tree_param_bytes": ([], ctypes.c_size_t),
     "sat_local_search": ([_vp, _i32, _u64, _u64, _u64, _i32, _vp, _vp, _vp, ctypes.c_size_t, _vp], _i32),
     "sat_ls_counter_offset": ([_vp, _vp], _i32),
@@ -84,7 +85,7 @@ def load_library(path: str = LIB_PATH):
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res
-    if lib.sat_abi_version() != 2:
+    if lib.sat_abi_version() != 3:
         raise E.PlanFailure("libsaturn_b200.so ABI version mismatch")
     _LIB = lib
     return lib

@@ -39,7 +39,7 @@ def test_header_declarations_bound(lib):
 
 
 def test_host_only_entry_points(lib):
-    assert lib.sat_abi_version() == 2
+    assert lib.sat_abi_version() == 3
     for st in range(6):
         assert lib.sat_error_string(st)
 
@@ -65,6 +65,27 @@ def test_tree_plan_layout_host_only(lib):
         assert lib.sat_tree_plan(nprob.ref, P, ctypes.byref(info)) == 0
         assert info.prefix_len == P and info.n_candidates == prob.space
     assert lib.sat_tree_plan(nprob.ref, 7, ctypes.byref(info)) == EN.SAT_ERR_INVALID
+
+
+def test_tree_plan_reports_packed_pair_pass(lib, monkeypatch):
+    """The pair pass packs two 16-bit free times per word when every reachable free time
+    (latest initial free time + each job's longest option) is below 0x7000."""
+    w, _ = golden_workload("cfg1")
+    t = build_profile_table(w, SyntheticExecutor(w.cluster))
+    prob = build_problem(t, w)
+    nprob = EN.NativeProblem(prob, 35)
+    info = EN.SatTreeInfo()
+    assert ctypes.sizeof(info) == 40
+    assert lib.sat_tree_plan(nprob.ref, 0, ctypes.byref(info)) == 0
+    assert info.pair_packed == 1
+    monkeypatch.setenv("SATURN_TREE_PACKED", "0")
+    assert lib.sat_tree_plan(nprob.ref, 0, ctypes.byref(info)) == 0
+    assert info.pair_packed == 0
+    monkeypatch.delenv("SATURN_TREE_PACKED")
+    horizon = sum(int(max(nprob.dur[j, :prob.radix[j], 0])) for j in range(prob.J))
+    nprob.dur[:] *= 0x7000 // horizon + 1                      # past the limit (same buffer)
+    assert lib.sat_tree_plan(nprob.ref, 0, ctypes.byref(info)) == 0
+    assert info.pair_packed == 0
 
 
 def test_validation_codes(lib):

@@ -184,6 +184,33 @@ def test_wide_times_use_32bit_slots(eng):
         assert got == C.CProblem(op).search("substream", trial, 0, 3000), trial
 
 
+def test_tree_packed_pair_pass_and_32bit_pass(eng, monkeypatch):
+    """k_tree's pair pass runs on 16-bit pairs when every reachable free time is below 0x7000
+    (node sizes <= 16) and on 32-bit slots otherwise: both equal the oracle, including
+    horizons on both sides of the packing limit and the forced 32-bit pass."""
+    rng = random.Random(505)
+    for trial in range(24):
+        gsz = [2, 3, 5, 8, 11, 16][trial % 6]
+        J = [3, 4, 5][trial % 3]
+        op = random_problem(rng, J, [gsz], max_opts=4, max_d=9)
+        if trial % 4 == 1:                       # horizon = sum of each job's longest option
+            horizon = sum(max(max(r) for r in job) for job in op.dur)
+            scale = (0x7000 + rng.choice([-1, 0, 1, 40])) // horizon
+            op.dur = [[[d * scale for d in row] for row in job] for job in op.dur]
+            op.runtime = [[list(r) for r in job] for job in op.dur]
+        if trial % 3 == 0:
+            op.init_free = [sorted(rng.randint(0, 5) for _ in range(gsz))]
+        prob = to_search_problem(op)
+        want = C.CProblem(op).search()
+        monkeypatch.delenv("SATURN_TREE_PACKED", raising=False)
+        assert gpu_key(eng, prob, "tree") == want, trial
+        assert bnb_key(eng, prob) == want, trial
+        monkeypatch.setenv("SATURN_TREE_PACKED", "0")
+        assert gpu_key(eng, prob, "tree") == want, trial
+        assert bnb_key(eng, prob) == want, trial
+    monkeypatch.delenv("SATURN_TREE_PACKED", raising=False)
+
+
 # --------------------------------------------------------------------------- bound-and-prune
 def bnb_key(eng, prob, prefix=None, seed_bound=True, shards=1):
     idx_bits, _ = prob.key_bits(prob.space)
