@@ -74,13 +74,18 @@ __device__ __forceinline__ void side_fold(const int32_t (&A)[G], const int32_t (
 template <int G>
 struct Pk { static constexpr int W = (G + 1) / 2; };
 
+// slot k of a packed vector, replicated into both halves
+template <int k>
+__device__ __forceinline__ uint32_t rep16(const uint32_t *P0) {
+    return __byte_perm(P0[k / 2], 0u, (k & 1) ? 0x3232u : 0x1010u);
+}
+
+// B = the state after a (g, e) placement, as 16-bit pairs: word w holds slots 2w, 2w+1 of
+// max(A[k], min(A[k+g], e)) (slots k < g: min(A[k+g], e); A[k+g] = INF past the node)
 template <int G, int g>
-__device__ __forceinline__ uint32_t group_value16(const uint32_t (&P0)[Pk<G>::W], const uint32_t (&P1)[Pk<G>::W],
-                                                  const int32_t (&A)[G], uint32_t d2,
-                                                  const uint32_t (&D2)[Pk<G>::W]) {
+__device__ __forceinline__ void merge16(const uint32_t (&P0)[Pk<G>::W], const uint32_t (&P1)[Pk<G>::W],
+                                        uint32_t e2, uint32_t (&B)[Pk<G>::W]) {
     constexpr int W = Pk<G>::W;
-    const uint32_t e2 = (uint32_t)A[g - 1] * 0x10001u + d2;      // e in both halves (no carry: e < 2^15)
-    uint32_t m2 = 0xFFFFFFFFu, bl2 = 0u;
 #pragma unroll
     for (int w = 0; w < W; ++w) {
         const int src = 2 * w + g;                                // shifted slot of the low half
@@ -88,25 +93,54 @@ __device__ __forceinline__ uint32_t group_value16(const uint32_t (&P0)[Pk<G>::W]
         if (src >= G) {
             b = e2;                                               // min(INF, e)
         } else {
-            const uint32_t s = (g & 1) ? P1[(src - 1) / 2 < W ? (src - 1) / 2 : 0] : P0[src / 2 < W ? src / 2 : 0];
-            b = __vminu2(s, e2);
+            const uint32_t sh = (g & 1) ? P1[(src - 1) / 2 < W ? (src - 1) / 2 : 0] : P0[src / 2 < W ? src / 2 : 0];
+            b = __vminu2(sh, e2);
         }
         if (2 * w + 1 >= g) b = __vmaxu2(P0[w], b);               // slots k >= g keep max(A[k], .)
-        m2 = __viaddmin_u16x2(b, D2[w], m2);
-        if (w == (G - 1) / 2) bl2 = __byte_perm(b, 0u, ((G - 1) & 1) ? 0x3232u : 0x1010u);
+        B[w] = b;
     }
-    return __vmaxu2(m2, bl2);
+}
+
+// P1 (slots 2w+1, 2w+2) of a packed vector from its P0
+template <int G>
+__device__ __forceinline__ void odd_pairs(const uint32_t (&P0)[Pk<G>::W], uint32_t (&P1)[Pk<G>::W]) {
+    constexpr int W = Pk<G>::W;
+#pragma unroll
+    for (int w = 0; w < W; ++w) P1[w] = __byte_perm(P0[w], w + 1 < W ? P0[w + 1 < W ? w + 1 : 0] : kTreeInf16, 0x5432u);
+}
+
+template <int G, int g>
+__device__ __forceinline__ uint32_t group_value16(const uint32_t (&P0)[Pk<G>::W], const uint32_t (&P1)[Pk<G>::W],
+                                                  uint32_t d2, const uint32_t (&D2)[Pk<G>::W]) {
+    constexpr int W = Pk<G>::W;
+    const uint32_t e2 = rep16<g - 1>(P0) + d2;                   // e in both halves (no carry: e < 2^15)
+    uint32_t B[W];
+    merge16<G, g>(P0, P1, e2, B);
+    uint32_t m2 = 0xFFFFFFFFu;
+#pragma unroll
+    for (int w = 0; w < W; ++w) m2 = __viaddmin_u16x2(B[w], D2[w], m2);
+    return __vmaxu2(m2, rep16<G - 1>(B));
 }
 
 template <int G, int g>
 __device__ __forceinline__ void side_fold16(const uint32_t (&P0)[Pk<G>::W], const uint32_t (&P1)[Pk<G>::W],
-                                            const int32_t (&A)[G], const int32_t *D1,
-                                            const uint32_t (&D2)[Pk<G>::W], uint32_t &v2) {
+                                            const int32_t *D1, const uint32_t (&D2)[Pk<G>::W], uint32_t &v2) {
     if constexpr (g <= G) {
         const int32_t d = D1[g - 1];                               // uniform (parameter block)
-        if (d < SAT_INF_I32) v2 = __vminu2(v2, group_value16<G, g>(P0, P1, A, (uint32_t)d * 0x10001u, D2));
-        side_fold16<G, g + 1>(P0, P1, A, D1, D2, v2);
+        if (d < SAT_INF_I32) v2 = __vminu2(v2, group_value16<G, g>(P0, P1, (uint32_t)d * 0x10001u, D2));
+        side_fold16<G, g + 1>(P0, P1, D1, D2, v2);
     }
+}
+
+// value of a pair node from its packed state: min over both orders of the two jobs
+template <int G>
+__device__ __forceinline__ int32_t pair_value16(const uint32_t (&P0)[Pk<G>::W], const uint32_t (&P1)[Pk<G>::W],
+                                                const int32_t *sdg, int ja, int jb,
+                                                const uint32_t (&Pa)[Pk<G>::W], const uint32_t (&Pb)[Pk<G>::W]) {
+    uint32_t v2 = 0xFFFFFFFFu;
+    side_fold16<G, 1>(P0, P1, sdg + ja * 32, Pb, v2);
+    side_fold16<G, 1>(P0, P1, sdg + jb * 32, Pa, v2);
+    return (int32_t)min(v2 & 0xFFFFu, v2 >> 16);
 }
 
 // Exact pass over a pair node: per (first job, option) group, the makespan and the lowest
@@ -179,16 +213,12 @@ __device__ __forceinline__ void tree_pair(const TreeParams &p, const int32_t *U,
             for (int w = 0; w < W; ++w) {
                 const uint32_t a0 = (uint32_t)A[2 * w];
                 const uint32_t a1 = 2 * w + 1 < G ? (uint32_t)A[2 * w + 1 < G ? 2 * w + 1 : 0] : kTreeInf16;
-                const uint32_t a2 = 2 * w + 2 < G ? (uint32_t)A[2 * w + 2 < G ? 2 * w + 2 : 0] : kTreeInf16;
                 P0[w] = __byte_perm(a0, a1, 0x5410u);
-                P1[w] = __byte_perm(a1, a2, 0x5410u);
                 Pa[w] = p.dgp[ja][w];
                 Pb[w] = p.dgp[jb][w];
             }
-            uint32_t v2 = 0xFFFFFFFFu;
-            side_fold16<G, 1>(P0, P1, A, sdg + ja * 32, Pb, v2);
-            side_fold16<G, 1>(P0, P1, A, sdg + jb * 32, Pa, v2);
-            v = (int32_t)min(v2 & 0xFFFFu, v2 >> 16);
+            odd_pairs<G>(P0, P1);
+            v = pair_value16<G>(P0, P1, sdg, ja, jb, Pa, Pb);
             if (valid && pair_needs_exact(p, v, base, lb)) tree_pair_exact<G>(p, U, B, ja, jb, base, lb);
             return;
         }
@@ -202,6 +232,68 @@ __device__ __forceinline__ void tree_pair(const TreeParams &p, const int32_t *U,
     side_fold<G, 1>(A, Da, Db, v);
     side_fold<G, 1>(A, Db, Da, v);
     if (valid && pair_needs_exact(p, v, base, lb)) tree_pair_exact<G>(p, U, B, ja, jb, base, lb);
+}
+
+// Packed merge with a warp-uniform runtime gang size (one uniform branch to the compile-time
+// shift)
+template <int G>
+__device__ __forceinline__ void merge_dispatch16(int g, const uint32_t (&P0)[Pk<G>::W], const uint32_t (&P1)[Pk<G>::W],
+                                                 uint32_t d2, uint32_t (&C)[Pk<G>::W]) {
+    switch (g) {
+#define SAT_CASE16(K) \
+    case K: if constexpr (K <= G) merge16<G, (K <= G ? K : 1)>(P0, P1, rep16<(K <= G ? K : 1) - 1>(P0) + d2, C); break;
+        SAT_CASE16(1) SAT_CASE16(2) SAT_CASE16(3) SAT_CASE16(4) SAT_CASE16(5) SAT_CASE16(6) SAT_CASE16(7)
+        SAT_CASE16(8) SAT_CASE16(9) SAT_CASE16(10) SAT_CASE16(11) SAT_CASE16(12) SAT_CASE16(13)
+        SAT_CASE16(14) SAT_CASE16(15) SAT_CASE16(16)
+#undef SAT_CASE16
+        default: break;
+    }
+}
+
+// Three jobs left, full scan, packed pair pass: the level-1 state (after the first of the
+// three) stays in registers as 16-bit pairs -- no shared-memory round trip per pair node; it
+// is written to the level-1 column only when a pair node needs its exact pass.
+template <int G>
+__device__ __forceinline__ void walk_q3_16(const TreeParams &p, const int32_t *L0, int32_t *dst, int32_t *Bbuf,
+                                           const int32_t *sdg, uint32_t rem, uint64_t acc_in, bool ok,
+                                           LaneBest &lb) {
+    constexpr int W = Pk<G>::W;
+    uint32_t P0[W], P1[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+        const uint32_t a0 = (uint32_t)L0[2 * w * 32];
+        const uint32_t a1 = 2 * w + 1 < G ? (uint32_t)L0[(2 * w + 1 < G ? 2 * w + 1 : 0) * 32] : kTreeInf16;
+        P0[w] = __byte_perm(a0, a1, 0x5410u);
+    }
+    odd_pairs<G>(P0, P1);
+    const uint64_t fq = p.fact[2];                    // Lehmer weight of the first of three positions
+    for (uint32_t m = rem; m; m &= m - 1) {
+        const int j = __ffs(m) - 1;
+        const uint32_t rem2 = rem & ~(1u << j);
+        const int ja = __ffs(rem2) - 1;
+        const int jb = 31 - __clz(rem2);
+        uint32_t Pa[W], Pb[W];
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            Pa[w] = p.dgp[ja][w];
+            Pb[w] = p.dgp[jb][w];
+        }
+        const uint64_t acc_j = acc_in + (uint64_t)__popc(rem & ((1u << j) - 1u)) * fq;
+        const int r = p.radix[j], ob = p.optbase[j];
+        const uint64_t wj = p.wJ[j];
+        for (int o = 0; o < r; ++o) {
+            uint32_t C0[W], C1[W];
+            merge_dispatch16<G>(p.optg[ob + o], P0, P1, (uint32_t)p.optd[ob + o] * 0x10001u, C0);
+            odd_pairs<G>(C0, C1);
+            const int32_t v = pair_value16<G>(C0, C1, sdg, ja, jb, Pa, Pb);
+            const uint64_t acc = acc_j + (uint64_t)o * wj;
+            if (ok && pair_needs_exact(p, v, acc, lb)) {
+#pragma unroll
+                for (int i = 0; i < G; ++i) dst[i * 32] = (int32_t)((C0[i / 2] >> (16 * (i & 1))) & 0xFFFFu);
+                tree_pair_exact<G>(p, dst, Bbuf, ja, jb, acc, lb);
+            }
+        }
+    }
 }
 
 // Upper-level merge with a warp-uniform runtime gang size, smem column to smem column.
@@ -297,7 +389,7 @@ __device__ __forceinline__ void walk_fixed(const TreeParams &p, int32_t *wbase, 
 // BNB = bound-and-prune: subtrees whose bound exceeds the best makespan found so far (by
 // any warp: published after every task) are skipped; the key found is the exhaustive one.
 template <int G, bool BNB>
-__global__ void __launch_bounds__(kTreeThreads, G <= 8 ? 12 : (G <= 16 ? 8 : 4))
+__global__ void __launch_bounds__(kTreeThreads, G <= 8 ? 10 : (G <= 16 ? 8 : 4))
 k_tree(const __grid_constant__ TreeParams p) {
     extern __shared__ __align__(16) int32_t tsm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -408,7 +500,14 @@ k_tree(const __grid_constant__ TreeParams p) {
             if (BNB && lane == 0) ++n_pairs;
             tree_pair<G>(p, L0, Bbuf, sdg, unplaced, base, lane_ok, lb);
         } else if (Q == 3) {
-            walk_fixed<G, BNB, 1>(p, wbase, lane, 0, Q, unplaced, base, lane_ok, Bbuf, sdg, lb, U, n_pairs);
+            bool done = false;
+            if constexpr (!BNB && G >= 2 && G <= kTreePackMaxG) {
+                if (p.packed) {
+                    walk_q3_16<G>(p, L0, wbase + col_words + lane, Bbuf, sdg, unplaced, base, lane_ok, lb);
+                    done = true;
+                }
+            }
+            if (!done) walk_fixed<G, BNB, 1>(p, wbase, lane, 0, Q, unplaced, base, lane_ok, Bbuf, sdg, lb, U, n_pairs);
         } else if (Q == 4) {
             walk_fixed<G, BNB, 2>(p, wbase, lane, 0, Q, unplaced, base, lane_ok, Bbuf, sdg, lb, U, n_pairs);
         } else if (BNB && Q == 5) {
