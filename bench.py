@@ -286,10 +286,13 @@ class DeviceSolve:
             self.info = eng.tree_plan(self.nprob, eng.tree_prefix(self.nprob, (1 << 17) * world) if world > 1 else 0)
             self.a, self.b = eng.tree_shard(self.nprob, self.info.prefix_len, rank, world)   # work-balanced
             self.n_cand = self.info.n_candidates
-            merges = self.info.n_job_steps - self.info.n_candidates
-            # algorithmic INT32 work of the prefix-shared walk:
+            # algorithmic INT32 work of the prefix-shared walk, counted on
+            # the minimal enumeration tree (every (ordered job prefix, options) node placed once:
+            # the 1-job-prefix layout), so lanes re-placing their prefix earn nothing:
             #   internal placement: node pick (N) + 2G slot min/max + add + makespan max = N + 2G + 2
             #   leaf placement (last job, no state update): node pick + add + max = N + 2
+            mini = eng.tree_plan(self.nprob, 1)
+            merges = mini.n_job_steps - mini.n_candidates
             self.ops = (merges // world) * (N + 2 * G + 2) + (self.n_cand // world) * (N + 2)
             self.kernel = "k_tree"
         else:

@@ -486,6 +486,31 @@ uint64_t walk_nodes(const int32_t *radix, uint32_t rem, std::vector<int64_t> &me
     return tot;
 }
 
+// Relative device cost of one warp walking the suffix set `rem` (shard balancing): a pair node
+// costs a fixed part plus one group per gang of each of its two jobs (the pair pass folds the
+// last job's options into per-gang minima, so its cost is r_a + r_b groups, not r_a * r_b
+// leaves); every upper-level node one merge.  Constants: warp instructions per unit in the
+// ncu source view of k_tree<8> (r01e: pair fixed ~110, group ~14, merge ~25, task ~250).
+constexpr double kCostPair = 110.0, kCostGroup = 14.0, kCostMerge = 25.0, kCostTask = 250.0;
+
+double walk_cost(const int32_t *radix, uint32_t rem, std::vector<double> &memo) {
+    const int n = __builtin_popcount(rem);
+    if (n < 2) return 0.0;
+    if (memo[rem] >= 0) return memo[rem];
+    double tot = 0;
+    if (n == 2) {
+        const int a = __builtin_ctz(rem), b = 31 - __builtin_clz(rem);
+        tot = kCostPair + kCostGroup * (double)(radix[a] + radix[b]);
+    } else {
+        for (uint32_t m = rem; m; m &= m - 1) {
+            const int j = __builtin_ctz(m);
+            tot += (double)radix[j] * (kCostMerge + walk_cost(radix, rem & ~(1u << j), memo));
+        }
+    }
+    memo[rem] = tot;
+    return tot;
+}
+
 int tree_layout(const sat_problem_t *p, int prefix_len, TreeLayout &lay) {
     const int J = p->J;
     if (p->N != 1 || p->time_mode != SAT_TIME_GRID_I32) return SAT_ERR_UNSUPPORTED;
@@ -517,12 +542,23 @@ int tree_layout(const sat_problem_t *p, int prefix_len, TreeLayout &lay) {
     };
     int P = prefix_len;
     if (P <= 0) {
-        // smallest prefix giving enough warp tasks to fill 8 GPUs several times over
-        P = J - 2;
-        for (int cand = 1; cand <= J - 2; ++cand) {
+        // smallest prefix giving enough warp tasks for one GPU's dynamic cursor (2^15, ~5 per
+        // resident warp) whose suffix the fixed-depth walkers cover (<= 4 jobs; deeper suffixes
+        // take the generic local-memory walk).  cfg1: P = 4, 8.2 ms against 8.6 ms at P = 5
+        // (profiles/r01e_shard_emulation.txt).  Sharded callers pass a longer prefix.
+        P = 0;
+        for (int cand = std::max(1, J - 4); cand <= J - 2; ++cand) {
             TreeLayout t;
-            if (!build(cand, t)) break;
-            if (t.n_tasks >= (1ull << 17)) { P = cand; break; }
+            if (!build(cand, t) || t.n_tasks >= (1ull << 31)) break;
+            if (t.n_tasks >= (1ull << 15)) { P = cand; break; }
+        }
+        if (P == 0) {   // large problems: the shortest prefix with 2^17 tasks (generic walk below)
+            P = J - 2;
+            for (int cand = 1; cand <= J - 2; ++cand) {
+                TreeLayout t;
+                if (!build(cand, t)) break;
+                if (t.n_tasks >= (1ull << 17)) { P = cand; break; }
+            }
         }
     }
     if (P < 1 || P > J - 2) return SAT_ERR_INVALID;
@@ -804,12 +840,12 @@ int sat_tree_shard(const sat_problem_t *p, int32_t prefix_len, int32_t world, in
     if (st) return st;
     const int J = p->J;
     const uint32_t full = (1u << J) - 1u;
-    std::vector<int64_t> memo((size_t)1 << J, -1);
-    // per-task work of set s: 32 lanes x (P prefix placements + the suffix walk)
+    std::vector<double> memo((size_t)1 << J, -1.0);
+    // per-task device cost of set s: the prefix decode + the warp's suffix walk (walk_cost)
     std::vector<long double> per_task(lay.sets.size());
     long double total = 0;
     for (size_t s = 0; s < lay.sets.size(); ++s) {
-        per_task[s] = 32.0L * ((long double)lay.P + (long double)walk_nodes(p->radix, full & ~lay.sets[s], memo, full));
+        per_task[s] = (long double)(kCostTask + walk_cost(p->radix, full & ~lay.sets[s], memo));
         total += per_task[s] * (long double)(lay.cum[s + 1] - lay.cum[s]);
     }
     auto boundary = [&](int32_t r) -> uint64_t {      // first task whose prefix work >= total * r / world

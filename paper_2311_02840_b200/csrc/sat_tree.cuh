@@ -379,7 +379,15 @@ __device__ __forceinline__ void walk_fixed(const TreeParams &p, int32_t *wbase, 
                 if (BNB && lane == 0) ++n_pairs;
                 tree_pair<G>(p, dst, Bbuf, sdg, rem2, acc, child_ok, lb);
             } else {
-                walk_fixed<G, BNB, D - 1>(p, wbase, lane, L + 1, Q, rem2, acc, child_ok, Bbuf, sdg, lb, U, n_pairs);
+                bool done = false;
+                if constexpr (!BNB && D == 2 && G >= 2 && G <= kTreePackMaxG) {
+                    if (p.packed) {     // three jobs left: the register-resident packed walk
+                        walk_q3_16<G>(p, dst, wbase + (L + 2) * col_words + lane, Bbuf, sdg, rem2, acc, child_ok, lb);
+                        done = true;
+                    }
+                }
+                if (!done)
+                    walk_fixed<G, BNB, D - 1>(p, wbase, lane, L + 1, Q, rem2, acc, child_ok, Bbuf, sdg, lb, U, n_pairs);
             }
         }
     }

@@ -408,7 +408,9 @@ class Engine:
             if opts.kernel in ("tree", "bnb") and not use_tree:
                 raise err.TooLarge("tree / bnb kernels need one node, grid time, 3..20 jobs")
             if use_bnb:
-                P = self.bnb_prefix(nprob, (1 << 15) * world)       # enough tasks on every rank
+                # pruning makes task costs uneven but cheap: a short prefix (2^15 tasks over all
+                # ranks) beats a longer one at every world size (profiles/r01e_shard_emulation.txt)
+                P = self.bnb_prefix(nprob, 1 << 15)
                 info = self.tree_plan(nprob, P)
                 a, b = self.tree_shard(nprob, info.prefix_len, rank, world)
                 best[0:1].fill_((seed_ms << idx_bits) | ((1 << idx_bits) - 1))

@@ -57,8 +57,8 @@ def test_tree_plan_layout_host_only(lib):
     info = EN.SatTreeInfo()
     assert lib.sat_tree_plan(nprob.ref, 0, ctypes.byref(info)) == 0
     assert info.n_candidates == prob.space == 32514048000
-    assert info.prefix_len == 5 and info.n_sets == math.comb(8, 5)
-    assert info.n_tasks >= 1 << 17
+    assert info.prefix_len == 4 and info.n_sets == math.comb(8, 4)
+    assert info.n_tasks >= 1 << 15
     # placements of the prefix-shared walk are far fewer than J per candidate
     assert prob.space < info.n_job_steps < 2 * prob.space
     for P in (1, 3, 6):
@@ -107,7 +107,9 @@ def test_validation_codes(lib):
 
 def test_tree_shard_partitions_and_balances_work(lib):
     """sat_tree_shard: contiguous ranges covering every warp task once, each with ~1/world of
-    the full-scan work (host-only entry point)."""
+    the full-scan device cost (host-only entry point).  Cost model: a pair node = a fixed part
+    + one group per gang of each of its two jobs; an upper-level node = one merge; a task = the
+    prefix decode (constants from the k_tree source profile)."""
     w, _ = golden_workload("cfg1")
     t = build_profile_table(w, SyntheticExecutor(w.cluster))
     prob = build_problem(t, w)
@@ -119,10 +121,14 @@ def test_tree_shard_partitions_and_balances_work(lib):
     memo = {}
 
     def walk(rem):
-        if rem == 0:
-            return 0
+        jobs = [j for j in range(J) if rem >> j & 1]
+        if len(jobs) < 2:
+            return 0.0
         if rem not in memo:
-            memo[rem] = sum(radix[j] * (1 + walk(rem & ~(1 << j))) for j in range(J) if rem >> j & 1)
+            if len(jobs) == 2:
+                memo[rem] = 110.0 + 14.0 * (radix[jobs[0]] + radix[jobs[1]])
+            else:
+                memo[rem] = sum(radix[j] * (25.0 + walk(rem & ~(1 << j))) for j in jobs)
         return memo[rem]
 
     per_task = []       # cost of every warp task, in layout order (sets in mask order)
@@ -130,7 +136,7 @@ def test_tree_shard_partitions_and_balances_work(lib):
         if bin(S).count("1") != P:
             continue
         npref = math.factorial(P) * math.prod(radix[j] for j in range(J) if S >> j & 1)
-        per_task += [P + walk(((1 << J) - 1) & ~S)] * ((npref + 31) // 32)
+        per_task += [250.0 + walk(((1 << J) - 1) & ~S)] * ((npref + 31) // 32)
     assert len(per_task) == info.n_tasks
     total = sum(per_task)
     for world in (2, 3, 8):
