@@ -152,14 +152,18 @@ int sat_search_bnb(const sat_problem_t *p, int32_t prefix_len,
  * `source` (SAT_SRC_SUBSTREAM / SAT_SRC_SEED) and descends over swap / option / insertion
  * moves on (makespan, total GPU load) until no move improves or max_rounds rounds of 32
  * moves were scanned.  Result: (makespan << idx_bits) | walker.
- * d_state_out (device, 2J bytes: options then order) receives the final candidate of walker
- * lo when hi == lo + 1 -- the replay that decodes a winning walker.  The number of rounds
+ * d_state_out (device, (hi - lo) x 2J bytes, or null) receives the final candidate of every
+ * walker w (options then order, at (w - lo) * 2J) -- the winner's plan without a replay;
+ * entries of abandoned walkers (below) are left untouched.  The number of rounds
  * scanned (each = up to 32 candidates scheduled) is left in the workspace as the uint64 word
  * after the walker cursor, which follows the problem blob at offset
- * sat_ls_counter_offset(p). */
+ * sat_ls_counter_offset(p).  stop_ms >= 0 (the problem's lower bound): a walker ends as
+ * soon as its makespan is <= stop_ms (its final state is the candidate at that point), and a
+ * walker whose id is above that of a key already in *d_best with makespan <= stop_ms is
+ * abandoned; neither changes the result.  stop_ms < 0: walks run to their local optimum. */
 int sat_ls_counter_offset(const sat_problem_t *p, size_t *offset);
 int sat_local_search(const sat_problem_t *p, int32_t source, uint64_t seed, uint64_t lo, uint64_t hi,
-                     int32_t max_rounds, sat_best_t *d_best, uint8_t *d_state_out,
+                     int32_t max_rounds, int32_t stop_ms, sat_best_t *d_best, uint8_t *d_state_out,
                      void *d_ws, size_t ws_bytes, void *stream);
 
 /* Schedule n candidates and record the plan of each.

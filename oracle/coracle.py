@@ -54,10 +54,10 @@ def lib():
         _lib.oracle_eval.restype = ctypes.c_double
         _lib.oracle_decode.argtypes = [_vp, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, _vp, _vp]
         _lib.oracle_local_search.argtypes = [_vp, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int,
-                                             _vp, _vp, _vp]
+                                             ctypes.c_int, _vp, _vp, _vp]
         _lib.oracle_local_search.restype = ctypes.c_double
         _lib.oracle_ls_search.argtypes = [_vp, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
-                                          ctypes.c_int, ctypes.c_int, _vp, _vp]
+                                          ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, _vp]
     return _lib
 
 
@@ -114,20 +114,22 @@ class CProblem:
                             opt.ctypes.data, ordr.ctypes.data)
         return opt.tolist(), ordr.tolist()
 
-    def local_search(self, walker, source="substream", seed=0, max_rounds=4096):
-        """(makespan, options, order, rounds) of one local-search walker (oracle.c semantics)."""
+    def local_search(self, walker, source="substream", seed=0, max_rounds=4096, stop_ms=-1):
+        """(makespan, options, order, rounds) of one local-search walker (oracle.c semantics;
+        stop_ms >= 0 ends the walk once its makespan is <= stop_ms)."""
         opt = np.zeros(self.J, dtype=np.int32)
         ordr = np.zeros(self.J, dtype=np.int32)
         rounds = ctypes.c_int()
         ms = lib().oracle_local_search(ctypes.byref(self.s), SOURCES[source], seed & ((1 << 64) - 1), walker,
-                                       max_rounds, opt.ctypes.data, ordr.ctypes.data, ctypes.byref(rounds))
+                                       max_rounds, int(stop_ms), opt.ctypes.data, ordr.ctypes.data,
+                                       ctypes.byref(rounds))
         return ms, opt.tolist(), ordr.tolist(), rounds.value
 
-    def ls_search(self, source="substream", seed=0, lo=0, hi=1, max_rounds=4096, threads=0):
+    def ls_search(self, source="substream", seed=0, lo=0, hi=1, max_rounds=4096, threads=0, stop_ms=-1):
         ms = ctypes.c_double()
         ident = ctypes.c_uint64()
         lib().oracle_ls_search(ctypes.byref(self.s), SOURCES[source], seed & ((1 << 64) - 1), lo, hi, max_rounds,
-                               threads, ctypes.byref(ms), ctypes.byref(ident))
+                               int(stop_ms), threads, ctypes.byref(ms), ctypes.byref(ident))
         return ms.value, ident.value
 
     def eval(self, opts, order):

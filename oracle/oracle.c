@@ -232,7 +232,8 @@ int oracle_decode(const oproblem *p, int source, uint64_t seed, uint64_t id, int
  *   a round = 32 consecutive move ids; rounds are scanned from move 0; the first round
  *   holding a move with objective < current applies its best move (lowest objective, then
  *   lowest id) and the scan restarts at 0; a scan without improvement, or max_rounds
- *   rounds in total, ends the walk. */
+ *   rounds in total, ends the walk; with stop_ms >= 0 (the problem's lower bound) the walk
+ *   also ends as soon as the current makespan is <= stop_ms. */
 static int ls_counts(const oproblem *p, int *M1, int *M2) {
     int J = p->J, m2 = 0;
     for (int j = 0; j < J; ++j) m2 += p->radix[j] - 1;
@@ -267,7 +268,7 @@ static void ls_neighbor(const oproblem *p, int m, int M1, int M2, const int *opt
 }
 
 double oracle_local_search(const oproblem *p, int source, uint64_t seed, uint64_t walker, int max_rounds,
-                           int *opt, int *ord, int *rounds_out) {
+                           int stop_ms, int *opt, int *ord, int *rounds_out) {
     int M1, M2;
     int M = ls_counts(p, &M1, &M2);
     if (source == 1) decode_stream(p, mix((seed ^ walker) + GOLD), opt, ord);
@@ -276,6 +277,7 @@ double oracle_local_search(const oproblem *p, int source, uint64_t seed, uint64_
     double cur = eval_full(p, opt, ord, NULL, NULL, &cur_load);
     int rounds = 0, nopt[OMAX_J], nord[OMAX_J];
     for (;;) {
+        if (stop_ms >= 0 && cur <= (double)stop_ms) break;   /* at the bound: the walk ends */
         int improved = 0;
         for (int r0 = 0; r0 < M && rounds < max_rounds; r0 += 32, ++rounds) {
             double bms = INFINITY, bload = INFINITY;
@@ -304,14 +306,14 @@ double oracle_local_search(const oproblem *p, int source, uint64_t seed, uint64_
 }
 
 int oracle_ls_search(const oproblem *p, int source, uint64_t seed, uint64_t lo, uint64_t hi, int max_rounds,
-                     int threads, double *best_ms, uint64_t *best_id) {
+                     int stop_ms, int threads, double *best_ms, uint64_t *best_id) {
     double gms = INFINITY;
     uint64_t gid = UINT64_MAX;
     if (threads < 1) threads = omp_get_max_threads();
 #pragma omp parallel for schedule(dynamic, 1) num_threads(threads)
     for (long long w = (long long)lo; w < (long long)hi; ++w) {
         int opt[OMAX_J], ord[OMAX_J];
-        double ms = oracle_local_search(p, source, seed, (uint64_t)w, max_rounds, opt, ord, NULL);
+        double ms = oracle_local_search(p, source, seed, (uint64_t)w, max_rounds, stop_ms, opt, ord, NULL);
 #pragma omp critical
         {
             if (ms < gms || (ms == gms && (uint64_t)w < gid)) { gms = ms; gid = (uint64_t)w; }

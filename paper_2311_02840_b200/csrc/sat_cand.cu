@@ -105,7 +105,7 @@ static int launch_ls_g(const sat_problem_t *p, LsArgs a, const std::vector<uint8
     const size_t blob_bytes = blob.size();
     const int N = (L == kLayoutMulti || L == kLayoutMulti16) ? p->N : 1;
     const int smem = (int)blob_bytes +
-                     kCandWarps * ls_warp_bytes(p->J, N, G, cand_slot_bytes<int32_t, L>(), cache_state_words<G, L>(N));
+                     ls_block_bytes(p->J, N, G, cand_slot_bytes<int32_t, L>(), cache_state_words<G, L>(N));
     if (smem > 220 * 1024) return SAT_ERR_TOO_LARGE;
     auto kern = k_ls<SRC, G, L>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
@@ -115,7 +115,17 @@ static int launch_ls_g(const sat_problem_t *p, LsArgs a, const std::vector<uint8
         per_sm < 1)
         per_sm = 1;
     uint64_t blocks = (uint64_t)device_sms() * (uint64_t)per_sm;
-    const uint64_t need = (a.hi - a.lo + kCandWarps - 1) / kCandWarps;
+    // warps per walker: long orders scan long (J = 32: ~72 rounds per scan), so evaluating a
+    // block's 4 rounds at once shortens the walk's critical path ~3.5x at ~6 % extra work; short
+    // orders keep a walker per warp (more walkers in flight).  SATURN_LS_GROUP = 1 / 2 / 4
+    // overrides (A/B checks).
+    int K = p->J >= 24 ? kCandWarps : 1;
+    if (const char *env = std::getenv("SATURN_LS_GROUP")) {
+        const int k = std::atoi(env);
+        if (k == 1 || k == 2 || k == kCandWarps) K = k;
+    }
+    a.group_warps = K;
+    const uint64_t need = ((a.hi - a.lo) * (uint64_t)K + kCandWarps - 1) / kCandWarps;
     if (blocks > need) blocks = std::max<uint64_t>(1, need);
     const size_t cur_off = (blob_bytes + 255) & ~(size_t)255;
     if (!d_ws || ws_bytes < cur_off + 2 * sizeof(unsigned long long)) return SAT_ERR_INVALID;

@@ -471,15 +471,22 @@ struct LsArgs {
     uint64_t seed;
     int32_t max_rounds;
     int32_t rec_d;
+    int32_t stop_ms;            // a walker ends once its makespan is <= stop_ms (-1: never)
+    int32_t idx_bits;
+    int32_t group_warps;        // warps per walker (1, 2 or kCandWarps): rounds evaluated at once
     sat_best_t *best;
     unsigned long long *cursor;
     unsigned long long *rounds; // rounds of 32 moves executed, summed over walkers (zeroed before)
-    uint8_t *state_out;         // [2J] final options then order of walker lo (hi == lo + 1), or null
+    uint8_t *state_out;         // [hi - lo][2J] final options then order of every walker (abandoned: untouched), or null
 };
 
-// + the walker's options / order / job positions (3 x 64 bytes) + its prefix cache
-__host__ __device__ inline int ls_warp_bytes(int J, int N, int G, int slot_bytes, int cache_state_words) {
-    return cand_warp_bytes(J, N, G, slot_bytes, false) + 192 + (J + 1) * (cache_state_words + 1) * 4;
+// bytes of one block's region: every warp's records / free-time columns, then the walker's
+// options / order / job positions (3 x 64 bytes) and its prefix cache
+__host__ __device__ inline int ls_walker_bytes(int J, int cache_state_words) {
+    return 192 + (J + 1) * (cache_state_words + 1) * 4;
+}
+__host__ __device__ inline int ls_block_bytes(int J, int N, int G, int slot_bytes, int cache_state_words) {
+    return kCandWarps * (cand_warp_bytes(J, N, G, slot_bytes, false) + ls_walker_bytes(J, cache_state_words));
 }
 
 // neighbour of (opt, ord) under move m: source position of position k, and the option override
@@ -514,6 +521,13 @@ __device__ __forceinline__ int ls_src(const LsMove &mv, int k) {
     return (k < mv.b || k > mv.a) ? k : (k == mv.b ? mv.a : k - 1);
 }
 
+// One walker per group of K = group_warps warps (K = 1: a walker per warp; K = kCandWarps: a
+// walker per block).  The group's warps evaluate consecutive rounds of the current scan at
+// once (warp w of the group: round q + w); the first of them, in scan order, holding an
+// improvement is the round the sequential walk would have applied, so the walk -- moves,
+// tie-breaks, round count -- is exactly the one-round-at-a-time walk (oracle.c restates
+// that), in ~1/K of the sequential steps when scans are long (the critical path of a wave is
+// its longest walk); K = 1 keeps the most walkers in flight when throughput matters.
 template <int SRC, int G, int L>
 __global__ void __launch_bounds__(kCandThreads)
 k_ls(LsArgs a) {
@@ -535,15 +549,31 @@ k_ls(LsArgs a) {
     const T *release = reinterpret_cast<const T *>(smem + h.off_release);
     const T *lane_init = reinterpret_cast<const T *>(smem + h.off_lane_init);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int K = a.group_warps;
+    const int grp = warp / K, gw = warp - grp * K;                 // walker group, warp within it
+    const bool leader = gw == 0 && lane == 0;
     const int SW = cache_state_words<G, L>(N);
-    uint8_t *wbase = smem + h.bytes + warp * ls_warp_bytes(J, N, G, cand_slot_bytes<T, L>(), SW);
+    const int wbytes = cand_warp_bytes(J, N, G, cand_slot_bytes<T, L>(), false);
+    uint8_t *wbase = smem + h.bytes + warp * wbytes;
     uint32_t *rec = reinterpret_cast<uint32_t *>(wbase) + lane;
     T *st = reinterpret_cast<T *>(wbase + J * 128) + lane;
     uint32_t *st16 = reinterpret_cast<uint32_t *>(st);
-    uint8_t *wopt = wbase + cand_warp_bytes(J, N, G, cand_slot_bytes<T, L>(), false);   // [64]
+    uint8_t *wopt = smem + h.bytes + kCandWarps * wbytes + grp * ls_walker_bytes(J, SW);   // [64] walker state
     uint8_t *word = wopt + 64;                                                           // [64]
     uint8_t *wpos = word + 64;                                                           // [64] job -> position
     uint32_t *cache = reinterpret_cast<uint32_t *>(wpos + 64);                          // [J + 1][SW + 1]
+    __shared__ uint64_t s_key[kCandWarps];             // per warp: its round's best (objective, move)
+    __shared__ int s_move[kCandWarps];
+    __shared__ unsigned long long s_walker[kCandWarps];  // per group
+    __shared__ uint64_t s_cur_key[kCandWarps];
+    __shared__ int s_beaten[kCandWarps];
+    uint64_t *g_key = s_key + grp * K;
+    int *g_move = s_move + grp * K;
+    // group barrier: the warp itself (K = 1) or a named barrier over the group's K warps
+    auto gsync = [&]() {
+        if (K == 1) __syncwarp();
+        else asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(K * 32) : "memory");
+    };
     const T INF = SAT_INF_I32;
     if constexpr (L == kLayoutOne16 || L == kLayoutMulti16) {
         for (int n = 0; n < N; ++n)
@@ -557,18 +587,19 @@ k_ls(LsArgs a) {
     int M2 = 0;
     for (int j = 0; j < J; ++j) M2 += tb.radix[j] - 1;
     const int M1 = J * (J - 1) / 2, M = M1 + M2 + J * (J - 1);
+    // the prefix cache pays off only on long orders (measured: +10 % at 64 jobs, -15 % at 16)
+    const bool use_cache = J >= 24;
 
-    T best_ms = INF;
+    T best_ms = INF;                       // group leader: the group's best (makespan, walker)
     uint64_t best_ix = ~0ull;
     const uint64_t total = a.hi - a.lo;
-    auto next_walker = [&]() -> uint64_t {
-        unsigned long long v = 0;
-        if (lane == 0) v = atomicAdd(a.cursor, 1ull);
-        return __shfl_sync(0xffffffffu, v, 0);
-    };
-    for (uint64_t wk = next_walker(); wk < total; wk = next_walker()) {
+    for (;;) {
+        if (leader) s_walker[grp] = atomicAdd(a.cursor, 1ull);
+        gsync();
+        const uint64_t wk = s_walker[grp];
+        if (wk >= total) break;
         const uint64_t id = a.lo + wk;
-        if (lane == 0) {       // the walker's start: candidate id of the stream (plan_random's draw order)
+        if (leader) {              // the walker's start: candidate id of the stream (plan_random's draw order)
             Stream s{SRC == SAT_SRC_SUBSTREAM ? mix64((a.seed ^ id) + kGolden) : a.seed + id};
             for (int j = 0; j < J; ++j) wopt[j] = (uint8_t)s.below((uint32_t)tb.radix[j], tb.mods);
             for (int k = 0; k < J; ++k) word[k] = (uint8_t)k;
@@ -576,49 +607,90 @@ k_ls(LsArgs a) {
                 const int k = (int)s.below((uint32_t)(i + 1), tb.mods);
                 const uint8_t t = word[i]; word[i] = word[k]; word[k] = t;
             }
-        }
-        __syncwarp();
-        // objective of the start (every lane, identical); lane 0 fills the prefix cache
-        for (int k = 0; k < J; ++k) { const int job = word[k]; rec[k * 32] = rec_for(tb, job, wopt[job]); }
-        if (lane == 0)
             for (int k = 0; k < J; ++k) wpos[word[k]] = (uint8_t)k;
-        uint64_t load = 0;
-        // the prefix cache pays off only on long orders (measured: +10 % at 64 jobs, -15 % at 16)
-        const bool use_cache = J >= 24;
-        T cur = schedule_records<T, G, L, true>(sc, rec, &load, 0, nullptr, use_cache ? cache : nullptr, lane == 0);
-        __syncwarp();
-        uint64_t cur_key = ((uint64_t)(uint32_t)cur << 34) | load;
+        }
+        gsync();
+        if (gw == 0) {             // objective of the start; lane 0 fills the prefix cache
+            for (int k = 0; k < J; ++k) { const int job = word[k]; rec[k * 32] = rec_for(tb, job, wopt[job]); }
+            uint64_t load = 0;
+            const T c0 = schedule_records<T, G, L, true>(sc, rec, &load, 0, nullptr, use_cache ? cache : nullptr,
+                                                        lane == 0);
+            if (lane == 0) s_cur_key[grp] = ((uint64_t)(uint32_t)c0 << 34) | load;
+        }
+        gsync();
+        uint64_t cur_key = s_cur_key[grp];
+        T cur = (T)(cur_key >> 34);
         int rounds = 0;
+        // Early stop (stop_ms = the problem's lower bound): the makespan never rises along a
+        // walk, so a walker at stop_ms has its final key (stop_ms, id) and ends there; a walker
+        // whose id is above that of a published key at <= stop_ms cannot win and is abandoned.
+        // Neither changes the search result.
+        bool abandoned = false;
         for (;;) {
+            if (cur <= a.stop_ms) break;
+            if (a.stop_ms >= 0) {
+                if (leader) {
+                    const unsigned long long k = *reinterpret_cast<volatile unsigned long long *>(&a.best->hi);
+                    s_beaten[grp] = k != ~0ull && (int64_t)(k >> a.idx_bits) <= (int64_t)a.stop_ms &&
+                                    (k & ((1ull << a.idx_bits) - 1ull)) < id;
+                }
+                gsync();
+                const bool beaten = s_beaten[grp] != 0;
+                gsync();
+                if (beaten) { abandoned = true; break; }
+            }
             bool improved = false;
-            for (int r0 = 0; r0 < M && rounds < a.max_rounds; r0 += 32, ++rounds) {
-                const int m = r0 + lane;
-                uint64_t key = ~0ull;
-                if (m < M) {
-                    const LsMove mv = ls_decode_move(m, J, M1, M2, tb.radix, wopt);
-                    // positions before the first changed one schedule exactly as the current
-                    // candidate: resume from the prefix cache there
-                    const int k0 = !use_cache ? 0 : (mv.kind == 1 ? (int)wpos[mv.a] : min(mv.a, mv.b));
-                    for (int k = k0; k < J; ++k) {
-                        const int job = word[ls_src(mv, k)];
-                        const int o = (mv.kind == 1 && job == mv.a) ? mv.b : (int)wopt[job];
-                        rec[k * 32] = rec_for(tb, job, o);
+            for (int q = 0;; q += K) {      // rounds q .. q+K-1 of this scan, one per warp
+                const int r0 = (q + gw) * 32;
+                const bool valid = r0 < M && rounds + gw < a.max_rounds;
+                uint64_t bk = ~0ull;
+                int bm = 0x7fffffff;
+                if (valid) {
+                    const int m = r0 + lane;
+                    if (m < M) {
+                        const LsMove mv = ls_decode_move(m, J, M1, M2, tb.radix, wopt);
+                        // positions before the first changed one schedule exactly as the current
+                        // candidate: resume from the prefix cache there
+                        const int k0 = !use_cache ? 0 : (mv.kind == 1 ? (int)wpos[mv.a] : min(mv.a, mv.b));
+                        for (int k = k0; k < J; ++k) {
+                            const int job = word[ls_src(mv, k)];
+                            const int o = (mv.kind == 1 && job == mv.a) ? mv.b : (int)wopt[job];
+                            rec[k * 32] = rec_for(tb, job, o);
+                        }
+                        uint64_t ld = 0;
+                        const T ms = schedule_records<T, G, L, true>(sc, rec, &ld, k0, use_cache ? cache : nullptr);
+                        bk = ((uint64_t)(uint32_t)ms << 34) | ld;
+                        bm = m;
                     }
-                    uint64_t ld = 0;
-                    const T ms = schedule_records<T, G, L, true>(sc, rec, &ld, k0, use_cache ? cache : nullptr);
-                    key = ((uint64_t)(uint32_t)ms << 34) | ld;
+                    // warp argmin of (objective, move id)
+                    for (int x = 16; x >= 1; x >>= 1) {
+                        const uint64_t ok = shfl_u64(bk, lane ^ x);
+                        const int om = __shfl_xor_sync(0xffffffffu, bm, x);
+                        if (ok < bk || (ok == bk && om < bm)) { bk = ok; bm = om; }
+                    }
                 }
-                // warp argmin of (objective, move id)
-                uint64_t bk = key;
-                int bm = m;
-                for (int x = 16; x >= 1; x >>= 1) {
-                    const uint64_t ok = shfl_u64(bk, lane ^ x);
-                    const int om = __shfl_xor_sync(0xffffffffu, bm, x);
-                    if (ok < bk || (ok == bk && om < bm)) { bk = ok; bm = om; }
+                // every thread takes the same decision: the first valid round (scan order) with
+                // an improvement, else all valid rounds were scanned without one
+                int first = -1, nvalid = 0;
+                uint64_t nk = bk;
+                int nm = bm;
+                if (K == 1) {                         // the warp's own round (all lanes hold it)
+                    nvalid = valid ? 1 : 0;
+                    if (valid && bk < cur_key) first = 0;
+                } else {
+                    if (lane == 0) { g_key[gw] = bk; g_move[gw] = bm; }
+                    gsync();
+                    for (int w = 0; w < K; ++w) {
+                        if (!((q + w) * 32 < M && rounds + w < a.max_rounds)) break;
+                        ++nvalid;
+                        if (g_key[w] < cur_key) { first = w; break; }
+                    }
+                    if (first >= 0) { nk = g_key[first]; nm = g_move[first]; }
                 }
-                if (bk < cur_key) {
-                    if (lane == 0) {
-                        const LsMove mv = ls_decode_move(bm, J, M1, M2, tb.radix, wopt);
+                if (first >= 0) {
+                    gsync();                          // every thread has read the slots
+                    if (leader) {
+                        const LsMove mv = ls_decode_move(nm, J, M1, M2, tb.radix, wopt);
                         if (mv.kind == 0) {
                             const uint8_t t = word[mv.a]; word[mv.a] = word[mv.b]; word[mv.b] = t;
                         } else if (mv.kind == 1) {
@@ -631,41 +703,44 @@ k_ls(LsArgs a) {
                         }
                         for (int k = 0; k < J; ++k) wpos[word[k]] = (uint8_t)k;
                     }
-                    __syncwarp();
-                    if (use_cache) {   // refresh the prefix cache for the new current candidate
+                    gsync();
+                    if (use_cache && gw == 0) {     // refresh the prefix cache for the new current candidate
                         for (int k = 0; k < J; ++k) { const int job = word[k]; rec[k * 32] = rec_for(tb, job, wopt[job]); }
                         schedule_records<T, G, L, false>(sc, rec, nullptr, 0, nullptr, cache, lane == 0);
-                        __syncwarp();
                     }
-                    cur_key = bk;
-                    cur = (T)(bk >> 34);
+                    gsync();
+                    cur_key = nk;
+                    cur = (T)(nk >> 34);
+                    rounds += first + 1;
                     improved = true;
-                    ++rounds;
                     break;
                 }
+                rounds += nvalid;
+                if (K > 1) gsync();                   // slots are rewritten by the next rounds
+                if (nvalid < K) break;                // scan exhausted or round budget spent
             }
             if (!improved || rounds >= a.max_rounds) break;
         }
-        if (lane == 0 && key_less(cur, id, best_ms, best_ix)) { best_ms = cur; best_ix = id; }
-        if (lane == 0) atomicAdd(a.rounds, (unsigned long long)rounds + 1ull);   // + the start's round
-        if (a.state_out && total == 1 && lane == 0) {
-            for (int j = 0; j < J; ++j) a.state_out[j] = wopt[j];
-            for (int k = 0; k < J; ++k) a.state_out[J + k] = word[k];
+        if (leader) {
+            if (!abandoned && key_less(cur, id, best_ms, best_ix)) {
+                best_ms = cur;
+                best_ix = id;
+                if (cur <= a.stop_ms)      // publish now: later walkers above this id are abandoned
+                    atomicMin(reinterpret_cast<unsigned long long *>(&a.best->hi),
+                              ((unsigned long long)(uint32_t)cur << a.idx_bits) | id);
+            }
+            atomicAdd(a.rounds, (unsigned long long)rounds + 1ull);   // + the start's round
+            if (a.state_out && !abandoned) {      // walker wk's final candidate
+                uint8_t *so = a.state_out + wk * (uint64_t)(2 * J);
+                for (int j = 0; j < J; ++j) so[j] = wopt[j];
+                for (int k = 0; k < J; ++k) so[J + k] = word[k];
+            }
         }
-        __syncwarp();
+        gsync();
     }
-    // ---- warp -> block -> grid argmin (lane 0 holds each warp's best) ----
-    __shared__ T s_ms[kCandWarps];
-    __shared__ uint64_t s_ix[kCandWarps];
-    if (lane == 0) { s_ms[warp] = best_ms; s_ix[warp] = best_ix; }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int w = 1; w < kCandWarps; ++w)
-            if (key_less(s_ms[w], s_ix[w], best_ms, best_ix)) { best_ms = s_ms[w]; best_ix = s_ix[w]; }
-        if (best_ms < INF) {
-            const uint64_t key = ((uint64_t)(uint32_t)best_ms << h.idx_bits) | best_ix;
-            atomicMin(reinterpret_cast<unsigned long long *>(&a.best->hi), (unsigned long long)key);
-        }
+    if (leader && best_ms < INF) {
+        const uint64_t key = ((uint64_t)(uint32_t)best_ms << h.idx_bits) | best_ix;
+        atomicMin(reinterpret_cast<unsigned long long *>(&a.best->hi), (unsigned long long)key);
     }
 }
 

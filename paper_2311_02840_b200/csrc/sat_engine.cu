@@ -881,7 +881,8 @@ int sat_ls_counter_offset(const sat_problem_t *p, size_t *offset) {
 }
 
 int sat_local_search(const sat_problem_t *p, int32_t source, uint64_t seed, uint64_t lo, uint64_t hi,
-                     int32_t max_rounds, sat_best_t *d_best, uint8_t *d_state_out, void *d_ws, size_t ws_bytes,
+                     int32_t max_rounds, int32_t stop_ms, sat_best_t *d_best, uint8_t *d_state_out, void *d_ws,
+                     size_t ws_bytes,
                      void *stream) {
     int st = validate(p);
     if (st) return st;
@@ -890,10 +891,10 @@ int sat_local_search(const sat_problem_t *p, int32_t source, uint64_t seed, uint
     if (p->time_mode != SAT_TIME_GRID_I32) return SAT_ERR_UNSUPPORTED;
     if (p->J < 2) return SAT_ERR_UNSUPPORTED;
     if (hi > 0 && ((hi - 1) >> p->idx_bits)) return SAT_ERR_TOO_LARGE;
-    if (d_state_out && hi - lo != 1) return SAT_ERR_INVALID;
     if (hi == lo) return SAT_OK;
     LsArgs a{};
     a.lo = lo; a.hi = hi; a.seed = seed; a.max_rounds = max_rounds; a.best = d_best; a.state_out = d_state_out;
+    a.stop_ms = stop_ms < 0 ? -1 : stop_ms; a.idx_bits = p->idx_bits;
     cudaStream_t s = (cudaStream_t)stream;
     if (source == SAT_SRC_SUBSTREAM) return launch_ls<SAT_SRC_SUBSTREAM>(p, a, d_ws, ws_bytes, s);
     return launch_ls<SAT_SRC_SEED>(p, a, d_ws, ws_bytes, s);

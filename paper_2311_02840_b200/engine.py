@@ -64,7 +64,7 @@ _SIGS = {
     "sat_alu_probe": ([_i32, _i32, _i32, _vp, _vp, _vp], _i32),
     "sat_alu_probe16": ([_i32, _i32, _i32, _vp, _vp, _vp], _i32),
     "sat_tree_param_bytes": ([], ctypes.c_size_t),
-    "sat_local_search": ([_vp, _i32, _u64, _u64, _u64, _i32, _vp, _vp, _vp, ctypes.c_size_t, _vp], _i32),
+    "sat_local_search": ([_vp, _i32, _u64, _u64, _u64, _i32, _i32, _vp, _vp, _vp, ctypes.c_size_t, _vp], _i32),
     "sat_ls_counter_offset": ([_vp, _vp], _i32),
     "sat_tree_shard": ([_vp, _i32, _i32, _i32, _vp, _vp], _i32),
 }
@@ -153,6 +153,7 @@ class SearchResult:
     wall_seconds: float = 0.0
     stats: dict | None = None  # bound-and-prune / local-search counters (this rank)
     idx_bits: int = 0          # bits of the packed key holding the candidate id
+    state: tuple | None = None  # local search: the winning walker's final (options, order)
 
 
 class Engine:
@@ -265,7 +266,7 @@ class Engine:
             # long orders: a local-search wave (~ms) usually reaches the optimum value, which
             # makes the exact search prune far more (seconds saved at 10-12 jobs)
             self.reset_best(tmp)
-            self.local_search(sprob, SRC_SUBSTREAM, seed, 0, 4096, 4096, tmp)
+            self.local_search(sprob, SRC_SUBSTREAM, seed, 0, 4096, 4096, tmp, stop_ms=int(prob.lower_bound()))
             bound = min(bound, (int(tmp[0].item()) & ((1 << 64) - 1)) >> s_bits)
         return bound
 
@@ -278,24 +279,26 @@ class Engine:
         if cur == -1 or key < cur:
             best[0:1].fill_(key)
 
-    def local_search(self, nprob, source, seed, lo, hi, max_rounds: int = 4096, best=None, state_out=None):
+    def local_search(self, nprob, source, seed, lo, hi, max_rounds: int = 4096, best=None, state_out=None,
+                     stop_ms: int = -1):
         """Walkers [lo, hi) of the local search; state_out (uint8 device tensor, 2J) receives the
-        final (options, order) of walker lo when hi == lo + 1."""
+        final (options, order) of walker lo when hi == lo + 1.  stop_ms >= 0 (the problem's lower
+        bound) ends a walk at that makespan and abandons walkers that can no longer win."""
         best = self._best if best is None else best
         ws, wsb = self.workspace(nprob)
         self._check(self.lib.sat_local_search(nprob.ref, source, seed & ((1 << 64) - 1), lo, hi, max_rounds,
-                                              _vp(best.data_ptr()),
+                                              int(stop_ms), _vp(best.data_ptr()),
                                               _vp(state_out.data_ptr()) if state_out is not None else None,
                                               _vp(ws), wsb, _vp(self.stream())), what="sat_local_search")
         self.launches += 1
 
-    def local_search_state(self, nprob, source, seed, walker, max_rounds: int = 4096):
-        """Replay one walker: its final (options, order) as lists."""
+    def local_search_state(self, nprob, source, seed, walker, max_rounds: int = 4096, stop_ms: int = -1):
+        """Replay one walker (same stop_ms as its search): its final (options, order) as lists."""
         torch = self.torch
         J = nprob.struct.J
         out = torch.zeros(2 * J, dtype=torch.uint8, device=self.device)
         tmp = self.reset_best(torch.empty(2, dtype=torch.int64, device=self.device))
-        self.local_search(nprob, source, seed, walker, walker + 1, max_rounds, tmp, out)
+        self.local_search(nprob, source, seed, walker, walker + 1, max_rounds, tmp, out, stop_ms=stop_ms)
         v = out.cpu().tolist()
         return v[:J], v[J:]
 
@@ -402,6 +405,7 @@ class Engine:
         best = self.reset_best()
         job_steps = 0
         stats, bnb_ws = None, None
+        ls_state = None
         if mode == "exhaustive":
             src = SRC_INDEX
             use_tree = opts.kernel in ("auto", "tree", "bnb") and self._tree_ok(prob)
@@ -434,6 +438,7 @@ class Engine:
             src = SRC_SUBSTREAM if source is None else source
             seed_used = opts.seed if seed is None else seed
             target = prob.lower_bound() if nprob.grid else -1.0
+            stop_ms = int(target) if (nprob.grid and opts.ls_stop) else -1
             off = ctypes.c_size_t()
             self._check(self.lib.sat_ls_counter_offset(nprob.ref, ctypes.byref(off)))
             # geometric waves (wave, 4 x wave, 16 x wave, ...): a small first wave keeps easy
@@ -441,17 +446,21 @@ class Engine:
             wave = max(1, int(opts.wave))
             rounds_total, walkers_done, waves = 0, 0, 0
             w0 = 0
+            ls_states = []          # (first walker, [walkers][2J] final states) per wave on this rank
             while w0 < n_idx:
                 w1 = min(n_idx, w0 + wave)
                 a, b = _shard(w1 - w0, rank, world)
-                self.local_search(nprob, src, seed_used, w0 + a, w0 + b, opts.max_rounds, best)
+                st_buf = torch.empty(max(1, b - a) * 2 * prob.J, dtype=torch.uint8, device=self.device)
+                ls_states.append((w0 + a, w0 + b, st_buf))
+                self.local_search(nprob, src, seed_used, w0 + a, w0 + b, opts.max_rounds, best, state_out=st_buf,
+                                  stop_ms=stop_ms)
                 rounds_total += int(self._ws[off.value:off.value + 8].view(torch.int64).item())
                 walkers_done, waves, w0, wave = w1, waves + 1, w1, wave * 4
                 k = int(_combine(best, True, group, world)[0])
                 if k != INT64_MAX and (k >> idx_bits) <= target:
                     break
             stats = {"walkers": walkers_done, "waves": waves, "rounds": rounds_total,
-                     "moves_scheduled_max": rounds_total * 32, "lower_bound": target}
+                     "moves_scheduled_max": rounds_total * 32, "lower_bound": target, "stop_ms": stop_ms}
             kernel, evaluated = "local", walkers_done
         else:
             src = SRC_SUBSTREAM if source is None else source
@@ -474,6 +483,8 @@ class Engine:
                 raise err.PlanFailure("search produced no candidate")
             makespan = float(k >> idx_bits)
             index = k & ((1 << idx_bits) - 1)
+            if mode == "local":
+                ls_state = self._walker_state(ls_states, index, prob.J, group, world)
         else:
             hi_bits, index = int(key[0]), int(key[1])
             if hi_bits == INT64_MAX:
@@ -483,7 +494,22 @@ class Engine:
                             kernel=kernel, exhaustive=mode == "exhaustive",
                             launches=self.launches - launches0, job_steps=job_steps,
                             device_seconds=dev_s, wall_seconds=time.perf_counter() - t0,
-                            stats=stats, idx_bits=idx_bits)
+                            stats=stats, idx_bits=idx_bits, state=ls_state)
+
+    def _walker_state(self, ls_states, index: int, J: int, group, world: int):
+        """The winning walker's final (options, order), recorded by its search launch (on the
+        rank that ran it; other ranks receive it through an all-reduce MAX of zeros)."""
+        torch = self.torch
+        v = torch.zeros(2 * J, dtype=torch.int32, device=self.device)
+        for lo, hi, buf in ls_states:
+            if lo <= index < hi:
+                v = buf[(index - lo) * 2 * J:(index - lo + 1) * 2 * J].to(torch.int32)
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.all_reduce(v, op=dist.ReduceOp.MAX, group=group)
+        out = v.cpu().tolist()
+        return out[:J], out[J:]
 
     @staticmethod
     def _tree_ok(prob: SearchProblem) -> bool:

@@ -143,7 +143,11 @@ def solve_problem(prob: SearchProblem, workload, opts: SolveOptions, running_con
         nprob = NativeProblem(prob, res.idx_bits)
         if res.kernel == "local":
             # replay the winning walker to get its final candidate, then schedule it explicitly
-            o_, r_ = eng.local_search_state(nprob, res.source, res.seed, res.index, opts.max_rounds)
+            if res.state is not None:          # recorded by the search launch
+                o_, r_ = res.state
+            else:
+                o_, r_ = eng.local_search_state(nprob, res.source, res.seed, res.index, opts.max_rounds,
+                                                stop_ms=res.stats.get("stop_ms", -1))
             explicit = np.array(list(o_) + list(r_), dtype=np.uint8)
             plan, options, ms, runtimes = _decode(eng, prob, NativeProblem(prob, 62), workload, SRC_EXPLICIT, 0,
                                                   explicit=explicit)

@@ -53,6 +53,7 @@ class SolveOptions:
     walkers: int = 1 << 16              # local search: walkers at most (walker w starts at candidate w)
     wave: int = 1 << 12                 # local search: first wave (then x4 per wave); stops at the bound
     max_rounds: int = 4096              # local search: rounds of 32 moves per walker
+    ls_stop: bool = True                # local search: a walk ends at the lower bound (same result)
     kernel: str = "auto"                # auto (bnb when it applies) | tree | index | bnb
 
 
@@ -116,28 +117,39 @@ class SearchProblem:
     def lower_bound(self) -> float:
         """A makespan lower bound of every candidate (grid intervals or seconds): the latest
         committed free time, each job's earliest possible end, and the area bound
-        (total GPU time >= initial commitments + every job's least g * d)."""
+        (total GPU time >= initial commitments + every job's least g * d).  Computed once per
+        problem (the arrays are not modified after build_problem)."""
+        hit = self.extra.get("_lower_bound")
+        if hit is not None:
+            return hit
         grid = self.time_mode == TIME_GRID
-        d = self.dur_i32 if grid else self.runtime
+        d = np.asarray(self.dur_i32 if grid else self.runtime, dtype=np.float64)
         init = self.init_free_i32 if grid else self.init_free_f64
-        rel = self.release_i32 if grid else self.release_f64
-        real = [float(init[n, i]) for n in range(self.N) for i in range(int(self.node_gpus[n]))]
+        rel = np.asarray(self.release_i32 if grid else self.release_f64, dtype=np.float64)
+        ng = [int(x) for x in self.node_gpus]
+        srt = [sorted(float(init[n, i]) for i in range(ng[n])) for n in range(self.N)]
+        real = [float(init[n, i]) for n in range(self.N) for i in range(ng[n])]
         lb = max(real) if real else 0.0
         area = sum(real)
+        # g-th smallest initial free time of each node, per option gang size: [J, C, N]
+        kth = np.full((self.N, max(max(ng), int(self.gpus.max())) + 1), np.inf)
+        for n in range(self.N):
+            kth[n, 1:ng[n] + 1] = srt[n]
+        g = np.asarray(self.gpus, dtype=np.int64)
+        C = g.shape[1]
+        valid = (np.arange(C)[None, :] < np.asarray(self.radix)[:, None])[:, :, None] & (
+            ((np.asarray(self.node_mask, dtype=np.int64)[:, :, None] >> np.arange(self.N)[None, None, :]) & 1) == 1)
+        start = np.maximum(rel[:, None, None], kth[np.arange(self.N)[None, None, :], g[:, :, None]])
+        ends = np.where(valid, start + d, np.inf).reshape(self.J, -1).min(axis=1)
+        areas = np.where(valid, g[:, :, None] * d, np.inf).reshape(self.J, -1).min(axis=1)
         for j in range(self.J):
-            ends, areas = [], []
-            for o in range(int(self.radix[j])):
-                g = int(self.gpus[j, o])
-                for n in range(self.N):
-                    if (int(self.node_mask[j, o]) >> n) & 1:
-                        start = max(float(rel[j]), sorted(float(init[n, i]) for i in range(int(self.node_gpus[n])))[g - 1])
-                        ends.append(start + float(d[j, o, n]))
-                        areas.append(g * float(d[j, o, n]))
-            lb = max(lb, min(ends))
-            area += min(areas)
-        total = float(sum(int(x) for x in self.node_gpus))
+            lb = max(lb, float(ends[j]))
+            area += float(areas[j])
+        total = float(sum(ng))
         lb = max(lb, area / total)
-        return float(math.ceil(lb - 1e-9)) if grid else lb
+        out = float(math.ceil(lb - 1e-9)) if grid else lb
+        self.extra["_lower_bound"] = out
+        return out
 
     def key_bits(self, n_indices: int) -> tuple:
         """(idx_bits, ms_bits) for packing (makespan << idx_bits) | index into 63 bits."""

@@ -372,6 +372,59 @@ def test_local_search_walkers_match_oracle(eng, name, seed):
     assert (float(k >> bits), k & ((1 << bits) - 1)) == cp.ls_search("substream", seed, 0, W, rounds)
 
 
+@pytest.mark.parametrize("name", ["cfg3", "cfg4", "cfg5", "hetero6"])
+def test_local_search_stop_at_bound(eng, name):
+    """stop_ms = the lower bound: each walker's walk ends at its first candidate with that
+    makespan (same final state as the oracle's restatement with the same rule), later walkers
+    are abandoned once a lower-id walker reached the bound, and the search key over a walker
+    range equals the oracle's full-walk key."""
+    w, t, prob, op = workload_problem(name)
+    cp = C.CProblem(op)
+    lb = int(prob.lower_bound())
+    rounds = 256 if name == "cfg5" else 4096
+    W = 8 if name == "cfg5" else 64
+    bits, _ = prob.key_bits(1 << 20)
+    nprob = EN.NativeProblem(prob, bits)
+    for stop in (lb, lb + 2):
+        for walker in range(0, W, max(1, W // 4)):
+            ms, o, r, _ = cp.local_search(walker, "substream", 7, rounds, stop_ms=stop)
+            assert eng.local_search_state(nprob, EN.SRC_SUBSTREAM, 7, walker, rounds, stop_ms=stop) == (o, r)
+            full = cp.local_search(walker, "substream", 7, rounds)[0]
+            assert ms == full or (ms <= stop and full <= ms), (name, walker, ms, full)
+        best = eng.reset_best()
+        eng.local_search(nprob, EN.SRC_SUBSTREAM, 7, 0, W, rounds, best, stop_ms=stop)
+        k = int(best.cpu().numpy().view(np.uint64)[0])
+        got = (float(k >> bits), k & ((1 << bits) - 1))
+        assert got == cp.ls_search("substream", 7, 0, W, rounds, stop_ms=stop)
+        full_key = cp.ls_search("substream", 7, 0, W, rounds)
+        if full_key[0] > stop:                         # the bound was not reached: same key as the full walks
+            assert got == full_key
+
+
+@pytest.mark.parametrize("name,stop", [("cfg3", -1), ("cfg4", 8), ("hetero6", -1)])
+def test_local_search_records_every_walker_state(eng, name, stop):
+    """One launch over a walker range records every walker's final candidate (the winner's
+    plan needs no replay): each equals the oracle's walk, and the engine's search result
+    carries the winner's."""
+    import torch
+
+    w, t, prob, op = workload_problem(name)
+    cp = C.CProblem(op)
+    bits, _ = prob.key_bits(1 << 20)
+    nprob = EN.NativeProblem(prob, bits)
+    W, lo = 24, 5
+    buf = torch.zeros(W * 2 * prob.J, dtype=torch.uint8, device="cuda")
+    eng.local_search(nprob, EN.SRC_SUBSTREAM, 7, lo, lo + W, 4096, eng.reset_best(), state_out=buf, stop_ms=stop)
+    got = buf.cpu().numpy().reshape(W, 2 * prob.J)
+    for i in range(W):
+        _, o, r, _ = cp.local_search(lo + i, "substream", 7, 4096, stop_ms=stop)
+        assert got[i].tolist() == o + r, (name, i)
+    res = eng.search(prob, SolveOptions(search="local", walkers=64, wave=64, seed=7))
+    assert res.state is not None
+    _, o, r, _ = cp.local_search(res.index, "substream", 7, 4096, stop_ms=res.stats["stop_ms"])
+    assert (list(res.state[0]), list(res.state[1])) == (o, r)
+
+
 def test_local_search_seed_source_and_release(eng):
     rng = random.Random(9)
     for trial in range(6):
