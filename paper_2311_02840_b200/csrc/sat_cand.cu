@@ -99,15 +99,15 @@ template int launch_cand<SAT_CAND_T, SAT_CAND_SRC>(const sat_problem_t *, CandAr
                                                    cudaStream_t);
 
 // ---------------------------------------------------------------- local search
-template <int SRC, int G, int L>
-static int launch_ls_g(const sat_problem_t *p, LsArgs a, const std::vector<uint8_t> &blob, void *d_ws,
+template <int SRC, int G, int L, int K>
+static int launch_ls_k(const sat_problem_t *p, LsArgs a, const std::vector<uint8_t> &blob, void *d_ws,
                        size_t ws_bytes, cudaStream_t stream) {
     const size_t blob_bytes = blob.size();
     const int N = (L == kLayoutMulti || L == kLayoutMulti16) ? p->N : 1;
     const int smem = (int)blob_bytes +
                      ls_block_bytes(p->J, N, G, cand_slot_bytes<int32_t, L>(), cache_state_words<G, L>(N));
     if (smem > 220 * 1024) return SAT_ERR_TOO_LARGE;
-    auto kern = k_ls<SRC, G, L>;
+    auto kern = k_ls<SRC, G, L, K>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
         return SAT_ERR_CUDA;
     int per_sm = 0;
@@ -115,15 +115,6 @@ static int launch_ls_g(const sat_problem_t *p, LsArgs a, const std::vector<uint8
         per_sm < 1)
         per_sm = 1;
     uint64_t blocks = (uint64_t)device_sms() * (uint64_t)per_sm;
-    // warps per walker: long orders scan long (J = 32: ~72 rounds per scan), so evaluating a
-    // block's 4 rounds at once shortens the walk's critical path ~3.5x at ~6 % extra work; short
-    // orders keep a walker per warp (more walkers in flight).  SATURN_LS_GROUP = 1 / 2 / 4
-    // overrides (A/B checks).
-    int K = p->J >= 24 ? kCandWarps : 1;
-    if (const char *env = std::getenv("SATURN_LS_GROUP")) {
-        const int k = std::atoi(env);
-        if (k == 1 || k == 2 || k == kCandWarps) K = k;
-    }
     a.group_warps = K;
     const uint64_t need = ((a.hi - a.lo) * (uint64_t)K + kCandWarps - 1) / kCandWarps;
     if (blocks > need) blocks = std::max<uint64_t>(1, need);
@@ -138,6 +129,22 @@ static int launch_ls_g(const sat_problem_t *p, LsArgs a, const std::vector<uint8
     a.rounds = a.cursor + 1;
     kern<<<(unsigned)blocks, kCandThreads, smem, stream>>>(a);
     return cudaGetLastError() == cudaSuccess ? SAT_OK : SAT_ERR_CUDA;
+}
+
+// warps per walker: long orders scan long (J = 32: ~72 rounds of 32 moves per scan), so a
+// block evaluating 4 rounds at once shortens the walk's critical path ~3.5x at ~6 % extra
+// work; short orders keep a walker per warp (more walkers in flight, no block barriers).
+// SATURN_LS_GROUP = 1 / 4 overrides (A/B checks).
+template <int SRC, int G, int L>
+static int launch_ls_g(const sat_problem_t *p, LsArgs a, const std::vector<uint8_t> &blob, void *d_ws,
+                       size_t ws_bytes, cudaStream_t stream) {
+    int K = p->J >= 24 ? kCandWarps : 1;
+    if (const char *env = std::getenv("SATURN_LS_GROUP")) {
+        const int k = std::atoi(env);
+        if (k == 1 || k == kCandWarps) K = k;
+    }
+    return K == 1 ? launch_ls_k<SRC, G, L, 1>(p, a, blob, d_ws, ws_bytes, stream)
+                  : launch_ls_k<SRC, G, L, kCandWarps>(p, a, blob, d_ws, ws_bytes, stream);
 }
 
 template <int SRC>

@@ -473,7 +473,7 @@ struct LsArgs {
     int32_t rec_d;
     int32_t stop_ms;            // a walker ends once its makespan is <= stop_ms (-1: never)
     int32_t idx_bits;
-    int32_t group_warps;        // warps per walker (1, 2 or kCandWarps): rounds evaluated at once
+    int32_t group_warps;        // warps per walker (1, 2 or kCandWarps; the kernel's K): rounds evaluated at once
     sat_best_t *best;
     unsigned long long *cursor;
     unsigned long long *rounds; // rounds of 32 moves executed, summed over walkers (zeroed before)
@@ -528,10 +528,11 @@ __device__ __forceinline__ int ls_src(const LsMove &mv, int k) {
 // tie-breaks, round count -- is exactly the one-round-at-a-time walk (oracle.c restates
 // that), in ~1/K of the sequential steps when scans are long (the critical path of a wave is
 // its longest walk); K = 1 keeps the most walkers in flight when throughput matters.
-template <int SRC, int G, int L>
+template <int SRC, int G, int L, int K>
 __global__ void __launch_bounds__(kCandThreads)
 k_ls(LsArgs a) {
     using T = int32_t;
+    static_assert(K == 1 || K == 2 || K == kCandWarps, "warps per walker");
     extern __shared__ __align__(16) uint8_t smem[];
     {
         const int nwords = (*reinterpret_cast<const BlobHeader *>(a.blob)).bytes / 16;
@@ -549,7 +550,6 @@ k_ls(LsArgs a) {
     const T *release = reinterpret_cast<const T *>(smem + h.off_release);
     const T *lane_init = reinterpret_cast<const T *>(smem + h.off_lane_init);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int K = a.group_warps;
     const int grp = warp / K, gw = warp - grp * K;                 // walker group, warp within it
     const bool leader = gw == 0 && lane == 0;
     const int SW = cache_state_words<G, L>(N);
@@ -571,7 +571,8 @@ k_ls(LsArgs a) {
     int *g_move = s_move + grp * K;
     // group barrier: the warp itself (K = 1) or a named barrier over the group's K warps
     auto gsync = [&]() {
-        if (K == 1) __syncwarp();
+        if constexpr (K == 1) __syncwarp();
+        else if constexpr (K == kCandWarps) __syncthreads();
         else asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(K * 32) : "memory");
     };
     const T INF = SAT_INF_I32;
@@ -674,7 +675,7 @@ k_ls(LsArgs a) {
                 int first = -1, nvalid = 0;
                 uint64_t nk = bk;
                 int nm = bm;
-                if (K == 1) {                         // the warp's own round (all lanes hold it)
+                if constexpr (K == 1) {               // the warp's own round (all lanes hold it)
                     nvalid = valid ? 1 : 0;
                     if (valid && bk < cur_key) first = 0;
                 } else {
@@ -716,7 +717,7 @@ k_ls(LsArgs a) {
                     break;
                 }
                 rounds += nvalid;
-                if (K > 1) gsync();                   // slots are rewritten by the next rounds
+                if constexpr (K > 1) gsync();         // slots are rewritten by the next rounds
                 if (nvalid < K) break;                // scan exhausted or round budget spent
             }
             if (!improved || rounds >= a.max_rounds) break;
