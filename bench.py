@@ -282,8 +282,8 @@ class DeviceSolve:
         self.use_tree = self.mode == "exhaustive" and eng._tree_ok(prob)
         G, N, J = prob.G, prob.N, prob.J
         if self.use_tree:
-            # per rank ~22 warp tasks per resident warp at least (dynamic cursor balance)
-            self.info = eng.tree_plan(self.nprob, eng.tree_prefix(self.nprob, (1 << 17) * world) if world > 1 else 0)
+            # per rank ~4 warp tasks per resident warp at least (dynamic cursor balance)
+            self.info = eng.tree_plan(self.nprob, eng.full_scan_prefix(self.nprob, world))
             self.a, self.b = eng.tree_shard(self.nprob, self.info.prefix_len, rank, world)   # work-balanced
             self.n_cand = self.info.n_candidates
             # algorithmic INT32 work of the prefix-shared walk, counted on

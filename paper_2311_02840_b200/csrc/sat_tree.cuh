@@ -345,6 +345,22 @@ __device__ __forceinline__ int32_t published_ms(const TreeParams &p) {
     return hi == ~0ull ? SAT_INF_I32 : (int32_t)(hi >> p.idx_bits);
 }
 
+// Word offset of level buffer L in a warp's region.  Level buffers hold 2G rows (rows G..2G-1
+// = INF, read by the shifted merge).  In the compact layout (full scan, packed pair pass,
+// suffixes of 3-4 jobs) only level 0 is merged from with a shift: deeper levels are the
+// register walk's input / the exact pass's input and hold G rows.
+template <int G>
+__host__ __device__ __forceinline__ int tree_level_off(int L, bool compact) {
+    return compact ? (L == 0 ? 0 : (2 * G + (L - 1) * G) * 32) : L * 2 * G * 32;
+}
+template <int G>
+__host__ __device__ __forceinline__ int tree_warp_words(int Q, bool compact) {
+    return tree_level_off<G>(Q - 1, compact) + G * 32;      // level buffers 0..Q-2, then Bbuf
+}
+__host__ __device__ __forceinline__ bool tree_compact(bool bnb, bool packed, int G, int Q) {
+    return !bnb && packed && G >= 2 && G <= kTreePackMaxG && (Q == 3 || Q == 4);
+}
+
 // Suffix walk with a compile-time number D of upper levels (Q = D + 2 jobs left): the
 // level state (remaining set, index accumulator, cursor) stays in registers instead of the
 // local-memory stack of the generic walk.  Level L's free times are the lane's column in
@@ -354,9 +370,9 @@ __device__ __forceinline__ void walk_fixed(const TreeParams &p, int32_t *wbase, 
                                            uint32_t rem, uint64_t acc_in, bool ok, int32_t *Bbuf,
                                            const int32_t *sdg, LaneBest &lb, int32_t &U,
                                            unsigned long long &n_pairs) {
-    constexpr int col_words = 2 * G * 32;
-    const int32_t *src = wbase + L * col_words + lane;
-    int32_t *dst = wbase + (L + 1) * col_words + lane;
+    const bool compact = tree_compact(BNB, p.packed != 0, G, Q);
+    const int32_t *src = wbase + tree_level_off<G>(L, compact) + lane;
+    int32_t *dst = wbase + tree_level_off<G>(L + 1, compact) + lane;
     const uint64_t fq = p.fact[Q - 1 - L];
     for (uint32_t m = rem; m; m &= m - 1) {
         const int j = __ffs(m) - 1;
@@ -382,7 +398,8 @@ __device__ __forceinline__ void walk_fixed(const TreeParams &p, int32_t *wbase, 
                 bool done = false;
                 if constexpr (!BNB && D == 2 && G >= 2 && G <= kTreePackMaxG) {
                     if (p.packed) {     // three jobs left: the register-resident packed walk
-                        walk_q3_16<G>(p, dst, wbase + (L + 2) * col_words + lane, Bbuf, sdg, rem2, acc, child_ok, lb);
+                        walk_q3_16<G>(p, dst, wbase + tree_level_off<G>(L + 2, compact) + lane, Bbuf, sdg, rem2, acc,
+                                      child_ok, lb);
                         done = true;
                     }
                 }
@@ -403,16 +420,16 @@ k_tree(const __grid_constant__ TreeParams p) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int Q = p.Q, P = p.P, J = p.J;
     const int upper = Q - 1;                         // level buffers 0..Q-2 (padded)
-    const int col_words = 2 * G * 32;
-    int32_t *wbase = tsm + warp * (upper * col_words + G * 32);
-    int32_t *Bbuf = wbase + upper * col_words + lane;
+    const bool compact = tree_compact(BNB, p.packed != 0, G, Q);
+    int32_t *wbase = tsm + warp * tree_warp_words<G>(Q, compact);
+    int32_t *Bbuf = wbase + tree_level_off<G>(upper, compact) + lane;
     // per (job, gang) least durations, shared by the block (broadcast loads in the pair pass)
     // per (job, gang) least durations, read straight from the parameter block: the job index
     // is warp-uniform, so these are uniform constant loads and the gang branches uniform
     const int32_t *sdg = &p.dg[0][0];
     // padding rows of every level buffer = INF (never rewritten)
-    for (int L = 0; L < upper; ++L)
-        for (int i = G; i < 2 * G; ++i) wbase[L * col_words + i * 32 + lane] = SAT_INF_I32;
+    for (int L = 0; L < (compact ? 1 : upper); ++L)
+        for (int i = G; i < 2 * G; ++i) wbase[tree_level_off<G>(L, compact) + i * 32 + lane] = SAT_INF_I32;
 
     // bound-and-prune records only candidates at or below the seed bound (the key's makespan
     // field is sized for it); the full scan records everything
@@ -511,7 +528,8 @@ k_tree(const __grid_constant__ TreeParams p) {
             bool done = false;
             if constexpr (!BNB && G >= 2 && G <= kTreePackMaxG) {
                 if (p.packed) {
-                    walk_q3_16<G>(p, L0, wbase + col_words + lane, Bbuf, sdg, unplaced, base, lane_ok, lb);
+                    walk_q3_16<G>(p, L0, wbase + tree_level_off<G>(1, compact) + lane, Bbuf, sdg, unplaced, base,
+                                  lane_ok, lb);
                     done = true;
                 }
             }
@@ -545,8 +563,8 @@ k_tree(const __grid_constant__ TreeParams p) {
                 }
                 cj[L] = j;
                 co[L] = o;
-                const int32_t *src = wbase + L * col_words + lane;
-                int32_t *dst = wbase + (L + 1) * col_words + lane;
+                const int32_t *src = wbase + tree_level_off<G>(L, compact) + lane;
+                int32_t *dst = wbase + tree_level_off<G>(L + 1, compact) + lane;
                 const int q2 = p.optbase[j] + o;
                 merge_cols<G>(src, dst, p.optg[q2], p.optd[q2]);
                 const uint32_t rem = rem_st[L];
@@ -606,8 +624,7 @@ k_tree(const __grid_constant__ TreeParams p) {
 
 template <int G, bool BNB>
 int launch_tree_k(const TreeParams &tp, int Q, cudaStream_t stream) {
-    const int upper = Q - 1;
-    const int smem = kTreeWarps * (upper * 2 * G * 32 + G * 32) * 4;
+    const int smem = kTreeWarps * tree_warp_words<G>(Q, tree_compact(BNB, tp.packed != 0, G, Q)) * 4;
     if (smem > 200 * 1024) return SAT_ERR_UNSUPPORTED;
     auto kern = k_tree<G, BNB>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)

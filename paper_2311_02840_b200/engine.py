@@ -236,6 +236,12 @@ class Engine:
                     what="sat_tree_shard")
         return lo.value, hi.value
 
+    def full_scan_prefix(self, nprob, world: int) -> int:
+        """Lane-prefix length of a sharded full scan: the shortest with ~4 warp tasks per
+        resident warp on every rank (40 warps per SM; profiles/r01e_shard_emulation.txt: cfg1
+        P = 4 up to 2 ranks, P = 5 from 4).  One rank: the library's choice (0)."""
+        return self.tree_prefix(nprob, 160 * self.sm_count * world) if world > 1 else 0
+
     def tree_prefix(self, nprob, min_tasks: int) -> int:
         """Shortest lane prefix with at least `min_tasks` warp tasks (0 = the library's choice)."""
         return self.bnb_prefix(nprob, min_tasks)
@@ -422,7 +428,7 @@ class Engine:
                 stats = {"prefix_len": info.prefix_len, "tasks": b - a}
                 kernel, evaluated = "bnb", info.n_candidates
             elif use_tree:
-                info = self.tree_plan(nprob, self.tree_prefix(nprob, (1 << 17) * world) if world > 1 else 0)
+                info = self.tree_plan(nprob, self.full_scan_prefix(nprob, world))
                 a, b = self.tree_shard(nprob, info.prefix_len, rank, world)
                 self.search_tree(nprob, info.prefix_len, a, b, best)
                 kernel, evaluated, job_steps = "tree", info.n_candidates, info.n_job_steps

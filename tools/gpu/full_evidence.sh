@@ -18,4 +18,8 @@ summ tree_cfg1 ${R}_ncu_full_k_tree_cfg1.json "$R: k_tree<8> full scan, config 1
 for c in 3 4 5; do python bench.py --config $c --budget 16777216 --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/plain$c.log 2>&1 && timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_cand -s 1 -c 1 -o gpurun_out/cand_cfg$c python bench.py --config $c --budget 16777216 --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_cand$c.log 2>&1; summ cand_cfg$c ${R}_ncu_full_k_cand_cfg$c.json "$R: k_cand sampled 2^24, config $c"; done
 python tools/ls_seed_check.py > gpurun_out/plain_ls.log 2>&1 && timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_ls -c 1 -o gpurun_out/ls_cfg3 python tools/ls_seed_check.py > gpurun_out/ncu_ls3.log 2>&1
 summ ls_cfg3 ${R}_ncu_full_k_ls_cfg3.json "$R: k_ls local search, config 3, one 4096-walker wave"
+python tools/ls_one_walker.py 5 4096 > gpurun_out/plain_ls5.log 2>&1 && timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_ls -c 1 -o gpurun_out/ls_cfg5 python tools/ls_one_walker.py 5 4096 > gpurun_out/ncu_ls5.log 2>&1
+summ ls_cfg5 ${R}_ncu_full_k_ls_cfg5.json "$R: k_ls local search, config 5, one 4096-walker wave (4 warps per walker, stop at the bound)"
+timeout 600 python tools/shard_emulation.py tree bnb > gpurun_out/${R}_shard_emulation.txt 2>&1
+bash tools/ls_group_sweep.sh > gpurun_out/${R}_ls_group_sweep.txt 2>&1
 du -sh gpurun_out; ls -la gpurun_out

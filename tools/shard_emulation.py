@@ -39,8 +39,10 @@ keys = set()
 modes = sys.argv[1:] or ["tree"]
 for mode in modes:
     for world in (1, 2, 4, 8):
-        default = eng.tree_prefix(nprob, (1 << 17) * world) if (mode == "tree" and world > 1) else (
-            eng.bnb_prefix(nprob, (1 << 15) * world) if mode == "bnb" else eng.tree_plan(nprob).prefix_len)
+        if mode == "tree":
+            default = eng.full_scan_prefix(nprob, world) or eng.tree_plan(nprob).prefix_len
+        else:
+            default = eng.bnb_prefix(nprob, 1 << 15)
         for P in sorted({4, 5, 6, default}):
             info = eng.tree_plan(nprob, P)
             ms = []
