@@ -261,27 +261,34 @@ def build_problem(table, workload, opts: SolveOptions | None = None, running_con
         raise err.TooLarge(f"{N} nodes x {G} padded GPUs exceed one warp ({MAX_LANES} lanes)")
 
     # per job: canonical option list with per-node runtimes
+    from .profiling import feasible_entries  # local: avoid a cycle at import time
     rows = []
     for job in pool:
-        from .profiling import feasible_entries  # local: avoid a cycle at import time
         entries = feasible_entries(table, job, workload)
         if not entries:
             raise err.NoFeasibleConfig(job.id)
         rem = remaining[job.id]
         cur = current.get(job.id)
+        cur = tuple(cur) if cur is not None else None
         row = []
-        for cfg, lat in entries:
-            tech = tech_by_name[cfg.technique]
-            per_node = []
-            for n in nodes:
-                if not node_eligible(job, tech, cfg.gpus, n):
-                    per_node.append(INFEASIBLE)
-                    continue
-                t = rem * lat                                     # profiling.py:151
-                if cur is not None and (cfg.technique, cfg.gpus, n.id) != tuple(cur):
-                    t = t + rho
-                per_node.append(t)
-            row.append((cfg, lat, per_node))
+        if N == 1 and cur is None:
+            # one node: every feasible (technique, g) runs on it (core.py:165-182 keeps only
+            # configs some node hosts), so the runtime is the plain estimate (profiling.py:151)
+            rows.append([(cfg, lat, [rem * lat]) for cfg, lat in entries])     # all finite
+            continue
+        else:
+            for cfg, lat in entries:
+                tech = tech_by_name[cfg.technique]
+                per_node = []
+                for n in nodes:
+                    if not node_eligible(job, tech, cfg.gpus, n):
+                        per_node.append(INFEASIBLE)
+                        continue
+                    t = rem * lat                                 # profiling.py:151
+                    if cur is not None and (cfg.technique, cfg.gpus, n.id) != cur:
+                        t = t + rho
+                    per_node.append(t)
+                row.append((cfg, lat, per_node))
         if all(math.isinf(t) for _, _, pn in row for t in pn):
             raise err.NoFeasibleConfig(job.id)
         rows.append(row)

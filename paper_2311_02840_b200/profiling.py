@@ -127,12 +127,9 @@ def estimate_runtime(table, job, config, remaining_batches: int) -> float:
 
 def feasible_entries(table, job, workload) -> list:
     """[(RunConfig, latency)] with finite latency, canonical order (profiling.py:154-161)."""
-    out = []
-    for cfg in feasible_configs(job, workload.cluster, workload.techniques):
-        lat = table.entries.get((job.id, cfg.technique, cfg.gpus), INFEASIBLE)
-        if math.isfinite(lat):
-            out.append((cfg, lat))
-    return out
+    get, jid, finite = table.entries.get, job.id, math.isfinite
+    return [(cfg, lat) for cfg in feasible_configs(job, workload.cluster, workload.techniques)
+            for lat in (get((jid, cfg.technique, cfg.gpus), INFEASIBLE),) if finite(lat)]
 
 
 def ensure_complete(table, workload) -> None:
