@@ -17,7 +17,7 @@ for cfg in [int(x) for x in (sys.argv[1:] or ["3", "4", "5"])]:
     J, N, G, T = SHAPES[cfg]
     w = synthetic_workload(J, N, G, T)
     t = build_profile_table(w, SyntheticExecutor(w.cluster))
-    for wave in (256, 1024, 4096, 16384):
+    for wave in [int(x) for x in os.environ.get("WAVES", "256,1024,4096,16384").split(",")]:
         opts = SolveOptions(wave=wave)
         PL.solve(t, w, None, opts)
         eng = PL.get_engine(None)
