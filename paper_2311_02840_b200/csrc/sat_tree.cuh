@@ -179,12 +179,16 @@ __device__ __noinline__ void tree_pair_exact(const TreeParams &p, const int32_t 
 }
 
 // A pair node's candidates have indices >= base and makespans >= v: it can only matter
-// when (v, base) ties or beats the lane's best and the best any warp has published so far
-// (keys order by makespan, then index; an unset index is ~0, so ties with a seed bound
-// pass).  The published key is read only for nodes that pass the lane test.
+// when (v, base) ties or beats the lane's best and, in the full scan, the best any warp has
+// published so far (keys order by makespan, then index; an unset index is ~0, so ties with
+// a seed bound pass).  The published key is read only for nodes that pass the lane test;
+// bound-and-prune skips that read (its subtrees were already cut against the published
+// bound, and most of its pair nodes pass the lane test).
+template <bool PUB>
 __device__ __forceinline__ bool pair_needs_exact(const TreeParams &p, int32_t v, uint64_t base,
                                                  const LaneBest &lb) {
     if (!(v < lb.ms || (v == lb.ms && base <= lb.ix))) return false;
+    if constexpr (!PUB) return true;
     const unsigned long long hi = *reinterpret_cast<volatile unsigned long long *>(&p.best->hi);
     if (hi == ~0ull) return true;
     const int32_t pms = (int32_t)(hi >> p.idx_bits);
@@ -195,7 +199,7 @@ __device__ __forceinline__ bool pair_needs_exact(const TreeParams &p, int32_t v,
 // second.  Fast value pass in registers (per-gang minimum durations are exact for the
 // value: a shorter first job never hurts, a shorter last job never hurts); the exact pass
 // only runs when this pair node can tie or beat the lane's best.
-template <int G>
+template <int G, bool BNB>
 __device__ __forceinline__ void tree_pair(const TreeParams &p, const int32_t *U, int32_t *B,
                                           const int32_t *sdg, uint32_t rem, uint64_t base, bool valid,
                                           LaneBest &lb) {
@@ -219,7 +223,7 @@ __device__ __forceinline__ void tree_pair(const TreeParams &p, const int32_t *U,
             }
             odd_pairs<G>(P0, P1);
             v = pair_value16<G>(P0, P1, sdg, ja, jb, Pa, Pb);
-            if (valid && pair_needs_exact(p, v, base, lb)) tree_pair_exact<G>(p, U, B, ja, jb, base, lb);
+            if (valid && pair_needs_exact<!BNB>(p, v, base, lb)) tree_pair_exact<G>(p, U, B, ja, jb, base, lb);
             return;
         }
     }
@@ -231,7 +235,7 @@ __device__ __forceinline__ void tree_pair(const TreeParams &p, const int32_t *U,
     }
     side_fold<G, 1>(A, Da, Db, v);
     side_fold<G, 1>(A, Db, Da, v);
-    if (valid && pair_needs_exact(p, v, base, lb)) tree_pair_exact<G>(p, U, B, ja, jb, base, lb);
+    if (valid && pair_needs_exact<!BNB>(p, v, base, lb)) tree_pair_exact<G>(p, U, B, ja, jb, base, lb);
 }
 
 // Packed merge with a warp-uniform runtime gang size (one uniform branch to the compile-time
@@ -287,7 +291,7 @@ __device__ __forceinline__ void walk_q3_16(const TreeParams &p, const int32_t *L
             odd_pairs<G>(C0, C1);
             const int32_t v = pair_value16<G>(C0, C1, sdg, ja, jb, Pa, Pb);
             const uint64_t acc = acc_j + (uint64_t)o * wj;
-            if (ok && pair_needs_exact(p, v, acc, lb)) {
+            if (ok && pair_needs_exact<true>(p, v, acc, lb)) {
 #pragma unroll
                 for (int i = 0; i < G; ++i) dst[i * 32] = (int32_t)((C0[i / 2] >> (16 * (i & 1))) & 0xFFFFu);
                 tree_pair_exact<G>(p, dst, Bbuf, ja, jb, acc, lb);
@@ -393,7 +397,7 @@ __device__ __forceinline__ void walk_fixed(const TreeParams &p, int32_t *wbase, 
             }
             if constexpr (D == 1) {
                 if (BNB && lane == 0) ++n_pairs;
-                tree_pair<G>(p, dst, Bbuf, sdg, rem2, acc, child_ok, lb);
+                tree_pair<G, BNB>(p, dst, Bbuf, sdg, rem2, acc, child_ok, lb);
             } else {
                 bool done = false;
                 if constexpr (!BNB && D == 2 && G >= 2 && G <= kTreePackMaxG) {
@@ -523,7 +527,7 @@ k_tree(const __grid_constant__ TreeParams p) {
         // ---- warp-uniform walk over the suffix (jobs in `unplaced`) ----
         if (Q == 2) {
             if (BNB && lane == 0) ++n_pairs;
-            tree_pair<G>(p, L0, Bbuf, sdg, unplaced, base, lane_ok, lb);
+            tree_pair<G, BNB>(p, L0, Bbuf, sdg, unplaced, base, lane_ok, lb);
         } else if (Q == 3) {
             bool done = false;
             if constexpr (!BNB && G >= 2 && G <= kTreePackMaxG) {
@@ -581,7 +585,7 @@ k_tree(const __grid_constant__ TreeParams p) {
                 }
                 if (L + 1 == Q - 2) {
                     if (BNB && lane == 0) ++n_pairs;
-                    tree_pair<G>(p, dst, Bbuf, sdg, rem2, acc, child_ok, lb);
+                    tree_pair<G, BNB>(p, dst, Bbuf, sdg, rem2, acc, child_ok, lb);
                 } else {
                     ++L;
                     rem_st[L] = rem2;
