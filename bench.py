@@ -533,6 +533,10 @@ def run_ours(args):
                                  "candidates_per_solve": [s.n_cand for s in solves]}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(1 if args.config == 2 else args.config, args.cpu_seconds, w, t, opts)
+        if head.mode == "exhaustive" and line["cpu_baseline"].get("value"):
+            # the CPU full scan's time to the best plan, extrapolated from the
+            # bounded sample's rate (the port scans candidates at a uniform cost)
+            line["cpu_baseline"]["full_scan_s_extrapolated"] = head.n_cand / line["cpu_baseline"]["value"]
         line["cpu_baseline_python"] = python_baseline(1 if args.config == 2 else args.config, w, t, opts)
         if args.config in (1, 3):
             try:
