@@ -105,18 +105,19 @@ static int launch_ls_k(const sat_problem_t *p, LsArgs a, const std::vector<uint8
     const size_t blob_bytes = blob.size();
     const int N = (L == kLayoutMulti || L == kLayoutMulti16) ? p->N : 1;
     const int smem = (int)blob_bytes +
-                     ls_block_bytes(p->J, N, G, cand_slot_bytes<int32_t, L>(), cache_state_words<G, L>(N));
+                     ls_block_bytes(p->J, N, G, cand_slot_bytes<int32_t, L>(), cache_state_words<G, L>(N), K);
     if (smem > 220 * 1024) return SAT_ERR_TOO_LARGE;
     auto kern = k_ls<SRC, G, L, K>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
         return SAT_ERR_CUDA;
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kCandThreads, smem) != cudaSuccess ||
+    constexpr int BW = ls_block_warps(K);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BW * 32, smem) != cudaSuccess ||
         per_sm < 1)
         per_sm = 1;
     uint64_t blocks = (uint64_t)device_sms() * (uint64_t)per_sm;
     a.group_warps = K;
-    const uint64_t need = ((a.hi - a.lo) * (uint64_t)K + kCandWarps - 1) / kCandWarps;
+    const uint64_t need = ((a.hi - a.lo) * (uint64_t)K + BW - 1) / BW;
     if (blocks > need) blocks = std::max<uint64_t>(1, need);
     const size_t cur_off = (blob_bytes + 255) & ~(size_t)255;
     if (!d_ws || ws_bytes < cur_off + 2 * sizeof(unsigned long long)) return SAT_ERR_INVALID;
@@ -127,24 +128,26 @@ static int launch_ls_k(const sat_problem_t *p, LsArgs a, const std::vector<uint8
     a.blob = ws;
     a.cursor = reinterpret_cast<unsigned long long *>(ws + cur_off);
     a.rounds = a.cursor + 1;
-    kern<<<(unsigned)blocks, kCandThreads, smem, stream>>>(a);
+    kern<<<(unsigned)blocks, BW * 32, smem, stream>>>(a);
     return cudaGetLastError() == cudaSuccess ? SAT_OK : SAT_ERR_CUDA;
 }
 
 // warps per walker: long orders scan long (J = 32: ~72 rounds of 32 moves per scan), so a
-// block evaluating 4 rounds at once shortens the walk's critical path ~3.5x at ~6 % extra
-// work; short orders keep a walker per warp (more walkers in flight, no block barriers).
-// SATURN_LS_GROUP = 1 / 4 overrides (A/B checks).
+// 256-thread block evaluating 8 rounds at once shortens the walk's critical path (sequential
+// steps / 6.9 on cfg5, instrumented oracle; measured cfg4 / cfg5 time to the bound: K = 1
+// 17.5 / 35 ms, K = 4 7.5 / 14.5 ms, K = 8 5.7 / 13.2 ms); short orders keep a walker per
+// warp (more walkers in flight, no block barriers).  SATURN_LS_GROUP = 1 / 4 / 8 overrides.
 template <int SRC, int G, int L>
 static int launch_ls_g(const sat_problem_t *p, LsArgs a, const std::vector<uint8_t> &blob, void *d_ws,
                        size_t ws_bytes, cudaStream_t stream) {
-    int K = p->J >= 24 ? kCandWarps : 1;
+    int K = p->J >= 24 ? 8 : 1;
     if (const char *env = std::getenv("SATURN_LS_GROUP")) {
         const int k = std::atoi(env);
-        if (k == 1 || k == kCandWarps) K = k;
+        if (k == 1 || k == kCandWarps || k == 8) K = k;
     }
-    return K == 1 ? launch_ls_k<SRC, G, L, 1>(p, a, blob, d_ws, ws_bytes, stream)
-                  : launch_ls_k<SRC, G, L, kCandWarps>(p, a, blob, d_ws, ws_bytes, stream);
+    if (K == 1) return launch_ls_k<SRC, G, L, 1>(p, a, blob, d_ws, ws_bytes, stream);
+    if (K == 8) return launch_ls_k<SRC, G, L, 8>(p, a, blob, d_ws, ws_bytes, stream);
+    return launch_ls_k<SRC, G, L, kCandWarps>(p, a, blob, d_ws, ws_bytes, stream);
 }
 
 template <int SRC>

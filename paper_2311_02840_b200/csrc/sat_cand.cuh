@@ -473,7 +473,7 @@ struct LsArgs {
     int32_t rec_d;
     int32_t stop_ms;            // a walker ends once its makespan is <= stop_ms (-1: never)
     int32_t idx_bits;
-    int32_t group_warps;        // warps per walker (1, 2 or kCandWarps; the kernel's K): rounds evaluated at once
+    int32_t group_warps;        // warps per walker (the kernel's K: 1, 4 or 8): rounds evaluated at once
     sat_best_t *best;
     unsigned long long *cursor;
     unsigned long long *rounds; // rounds of 32 moves executed, summed over walkers (zeroed before)
@@ -485,8 +485,11 @@ struct LsArgs {
 __host__ __device__ inline int ls_walker_bytes(int J, int cache_state_words) {
     return 192 + (J + 1) * (cache_state_words + 1) * 4;
 }
-__host__ __device__ inline int ls_block_bytes(int J, int N, int G, int slot_bytes, int cache_state_words) {
-    return kCandWarps * (cand_warp_bytes(J, N, G, slot_bytes, false) + ls_walker_bytes(J, cache_state_words));
+// warps per k_ls block: 4, or 8 when one walker takes 8 warps
+__host__ __device__ constexpr int ls_block_warps(int K) { return K > kCandWarps ? K : kCandWarps; }
+__host__ __device__ inline int ls_block_bytes(int J, int N, int G, int slot_bytes, int cache_state_words, int K) {
+    return ls_block_warps(K) * cand_warp_bytes(J, N, G, slot_bytes, false) +
+           (ls_block_warps(K) / K) * ls_walker_bytes(J, cache_state_words);
 }
 
 // neighbour of (opt, ord) under move m: source position of position k, and the option override
@@ -529,10 +532,11 @@ __device__ __forceinline__ int ls_src(const LsMove &mv, int k) {
 // that), in ~1/K of the sequential steps when scans are long (the critical path of a wave is
 // its longest walk); K = 1 keeps the most walkers in flight when throughput matters.
 template <int SRC, int G, int L, int K>
-__global__ void __launch_bounds__(kCandThreads)
+__global__ void __launch_bounds__(ls_block_warps(K) * 32)
 k_ls(LsArgs a) {
     using T = int32_t;
-    static_assert(K == 1 || K == 2 || K == kCandWarps, "warps per walker");
+    static_assert(K == 1 || K == 2 || K == kCandWarps || K == 8, "warps per walker");
+    constexpr int BW = ls_block_warps(K);                // warps per block
     extern __shared__ __align__(16) uint8_t smem[];
     {
         const int nwords = (*reinterpret_cast<const BlobHeader *>(a.blob)).bytes / 16;
@@ -558,21 +562,21 @@ k_ls(LsArgs a) {
     uint32_t *rec = reinterpret_cast<uint32_t *>(wbase) + lane;
     T *st = reinterpret_cast<T *>(wbase + J * 128) + lane;
     uint32_t *st16 = reinterpret_cast<uint32_t *>(st);
-    uint8_t *wopt = smem + h.bytes + kCandWarps * wbytes + grp * ls_walker_bytes(J, SW);   // [64] walker state
+    uint8_t *wopt = smem + h.bytes + BW * wbytes + grp * ls_walker_bytes(J, SW);   // [64] walker state
     uint8_t *word = wopt + 64;                                                           // [64]
     uint8_t *wpos = word + 64;                                                           // [64] job -> position
     uint32_t *cache = reinterpret_cast<uint32_t *>(wpos + 64);                          // [J + 1][SW + 1]
-    __shared__ uint64_t s_key[kCandWarps];             // per warp: its round's best (objective, move)
-    __shared__ int s_move[kCandWarps];
-    __shared__ unsigned long long s_walker[kCandWarps];  // per group
-    __shared__ uint64_t s_cur_key[kCandWarps];
-    __shared__ int s_beaten[kCandWarps];
+    __shared__ uint64_t s_key[BW];                     // per warp: its round's best (objective, move)
+    __shared__ int s_move[BW];
+    __shared__ unsigned long long s_walker[BW];        // per group
+    __shared__ uint64_t s_cur_key[BW];
+    __shared__ int s_beaten[BW];
     uint64_t *g_key = s_key + grp * K;
     int *g_move = s_move + grp * K;
     // group barrier: the warp itself (K = 1) or a named barrier over the group's K warps
     auto gsync = [&]() {
         if constexpr (K == 1) __syncwarp();
-        else if constexpr (K == kCandWarps) __syncthreads();
+        else if constexpr (K == BW) __syncthreads();
         else asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(K * 32) : "memory");
     };
     const T INF = SAT_INF_I32;
