@@ -145,6 +145,54 @@ def test_lower_bound_never_exceeds_the_optimum():
         assert to_search_problem(op).lower_bound() <= ms, trial
 
 
+def _lower_bound_literal(p):
+    """The bound of SearchProblem.lower_bound restated as plain loops (committed free time,
+    each job's earliest end over its options and eligible nodes, area over all GPUs)."""
+    import math
+
+    grid = p.time_mode == "grid"
+    d = p.dur_i32 if grid else p.runtime
+    init = p.init_free_i32 if grid else p.init_free_f64
+    rel = p.release_i32 if grid else p.release_f64
+    real = [float(init[n, i]) for n in range(p.N) for i in range(int(p.node_gpus[n]))]
+    lb, area = (max(real) if real else 0.0), sum(real)
+    for j in range(p.J):
+        ends, areas = [], []
+        for o in range(int(p.radix[j])):
+            g = int(p.gpus[j, o])
+            for n in range(p.N):
+                if (int(p.node_mask[j, o]) >> n) & 1:
+                    kth = sorted(float(init[n, i]) for i in range(int(p.node_gpus[n])))[g - 1]
+                    ends.append(max(float(rel[j]), kth) + float(d[j, o, n]))
+                    areas.append(g * float(d[j, o, n]))
+        lb = max(lb, min(ends))
+        area += min(areas)
+    lb = max(lb, area / float(sum(int(x) for x in p.node_gpus)))
+    return float(math.ceil(lb - 1e-9)) if grid else lb
+
+
+def test_lower_bound_equals_literal_restatement():
+    """The vectorised, memoised lower_bound equals the loop restatement bit for bit (grid and
+    float time, releases, initial free times, heterogeneous eligibility)."""
+    import random
+
+    from test_engine_gpu import to_search_problem
+    from test_oracle import random_problem
+
+    rng = random.Random(43)
+    for trial in range(60):
+        nodes = [[rng.randint(1, 8)], [rng.randint(1, 4), rng.randint(1, 4)], [2, 3, 1]][trial % 3]
+        op = random_problem(rng, rng.randint(1, 6), nodes, max_opts=4, max_d=20, hetero=trial % 2 == 0)
+        op.grid = trial % 5 != 0
+        if trial % 4 == 1:
+            op.release = [rng.randint(0, 6) for _ in range(op.J)]
+            op.init_free = [[rng.randint(0, 5) for _ in range(n)] for n in nodes]
+        p = to_search_problem(op)
+        want = _lower_bound_literal(p)
+        assert p.lower_bound() == want, trial
+        assert p.lower_bound() == want, trial            # memoised value
+
+
 def test_optimus_marginal_gain_spec_examples():
     """latency halving g=1 -> 2, 1000 batches, base 1 s -> 500 s; g at the node
     maximum -> 0; a slower g+1 -> clamped to 0."""
