@@ -341,6 +341,119 @@ __device__ __forceinline__ T schedule_records(const SchedCtx<T> &c, const uint32
     return mx;
 }
 
+// One placement of a (g, d) job on the register-resident packed state (One16 layout) with a
+// compile-time gang size: the shift by g is a register choice, no shared-memory round trip.
+// Words are updated in ascending order: word w reads old words >= w only.
+template <int G, int g>
+__device__ __forceinline__ void place16_reg(uint32_t (&av)[G / 2], int32_t rel, bool has_release, int32_t d,
+                                            int32_t &mx) {
+    constexpr int W = G / 2;
+    int32_t t = (int32_t)((av[(g - 1) / 2] >> (16 * ((g - 1) & 1))) & 0xFFFFu);
+    if (has_release) t = max(t, rel);
+    const int32_t e = t + d;
+    const uint32_t e2 = (uint32_t)e * 0x10001u;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+        const int s0 = w + g / 2;                               // word holding slot 2w + g (g even)
+        uint32_t sh;
+        if constexpr (g % 2 == 0) {
+            sh = s0 < W ? av[s0 < W ? s0 : 0] : 0xFFFFFFFFu;
+        } else {
+            const uint32_t lo = s0 < W ? av[s0 < W ? s0 : 0] : 0xFFFFFFFFu;
+            const uint32_t hi = s0 + 1 < W ? av[s0 + 1 < W ? s0 + 1 : 0] : 0xFFFFFFFFu;
+            sh = __byte_perm(lo, hi, 0x5432u);                  // slots 2w+g, 2w+g+1
+        }
+        av[w] = __vmaxu2(av[w], __vminu2(sh, e2));
+    }
+    mx = max(mx, e);
+}
+
+// k_ls move evaluation on the One16 layout.  The participating lanes walk positions in step
+// (from the smallest resume point k0 in the warp; a lane joins at its own k0 with the cached
+// state), so where every active lane places a job of the same gang size -- the positions a
+// move leaves in place, typically most of them -- the placement runs on registers with a
+// compile-time shift (one uniform branch); otherwise the generic shared-memory shift of
+// schedule_records.  Same arithmetic, same result.
+template <int G>
+__device__ __forceinline__ int32_t schedule_eval16(const SchedCtx<int32_t> &c, const uint32_t *rec, uint64_t *load,
+                                                   int k0, const uint32_t *cin) {
+    constexpr int W = G / 2;
+    const int J = c.J;
+    const int SW = W, CW = SW + 1;
+    uint32_t *st16 = c.st16;
+    const unsigned act = __activemask();
+    const int kmin = (int)__reduce_min_sync(act, (unsigned)k0);
+    uint32_t av[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) av[w] = 0u;
+    int32_t mx = 0;
+    bool dirty = true;                 // column st16 does not hold av
+    for (int kk = kmin; kk < J; ++kk) {
+        const bool on = kk >= k0;
+        if (kk == k0) {                // join: the cached state before position k0
+#pragma unroll
+            for (int w = 0; w < W; ++w) av[w] = cin ? cin[k0 * CW + w]
+                                                    : (uint32_t)(uint16_t)c.lane_init[2 * w] |
+                                                          ((uint32_t)(uint16_t)c.lane_init[2 * w + 1] << 16);
+            mx = cin ? (int32_t)cin[k0 * CW + SW] : (int32_t)c.init_max;
+        }
+        const uint32_t r = on ? rec[kk * 32] : 0u;
+        const int g = (int)(r & 63u) + 1;
+        SAT_ASSERT(!on || (g >= 1 && g <= G && (int)((r >> 6) & 63u) < J));
+        const unsigned onm = __ballot_sync(act, on);
+        const int g0 = __shfl_sync(act, g, __ffs(onm) - 1);
+        const bool uni = __all_sync(act, !on || g == g0);
+        const int32_t rel = (on && c.has_release) ? (int32_t)c.release[(r >> 6) & 63u] : 0;
+        const int32_t d = (int32_t)(r >> 12);
+        if (uni) {
+            if (on) {
+                switch (g0) {
+#define SAT_P16(K) case K: if constexpr (K <= G) place16_reg<G, (K <= G ? K : 1)>(av, rel, c.has_release, d, mx); break;
+                    SAT_P16(1) SAT_P16(2) SAT_P16(3) SAT_P16(4) SAT_P16(5) SAT_P16(6) SAT_P16(7) SAT_P16(8)
+                    SAT_P16(9) SAT_P16(10) SAT_P16(11) SAT_P16(12) SAT_P16(13) SAT_P16(14) SAT_P16(15) SAT_P16(16)
+                    SAT_P16(17) SAT_P16(18) SAT_P16(19) SAT_P16(20) SAT_P16(21) SAT_P16(22) SAT_P16(23) SAT_P16(24)
+                    SAT_P16(25) SAT_P16(26) SAT_P16(27) SAT_P16(28) SAT_P16(29) SAT_P16(30) SAT_P16(31) SAT_P16(32)
+#undef SAT_P16
+                    default: break;
+                }
+                dirty = true;
+            }
+        } else if (on) {
+            if (dirty) {
+#pragma unroll
+                for (int w = 0; w < W; ++w) st16[w * 32] = av[w];
+                dirty = false;
+            }
+            const int gm = g - 1;
+            const uint32_t selt = 0x4410u + (uint32_t)(gm & 1) * 0x22u;
+            int32_t t = (int32_t)__byte_perm(st16[(gm >> 1) * 32], 0u, selt);
+            if (c.has_release) t = max(t, rel);
+            const int32_t e = t + d;
+            const uint32_t e2 = (uint32_t)e * 0x10001u;
+            const uint32_t sel = (g & 1) ? 0x5432u : 0x3210u;
+            const uint32_t *src = st16 + (g >> 1) * 32;
+            uint32_t wv[W + 1];
+#pragma unroll
+            for (int k = 0; k <= W; ++k) wv[k] = src[k * 32];
+#pragma unroll
+            for (int k = 0; k < W; ++k) {
+                const uint32_t sh = __byte_perm(wv[k], wv[k + 1], sel);
+                av[k] = __vmaxu2(av[k], __vminu2(sh, e2));
+                st16[k * 32] = av[k];
+            }
+            mx = max(mx, e);
+        }
+    }
+    uint64_t sum = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+        const uint32_t lo = av[w] & 0xffffu, hi = av[w] >> 16;
+        sum += (lo != 0xffffu ? lo : 0u) + (hi != 0xffffu ? hi : 0u);
+    }
+    *load = sum;
+    return mx;
+}
+
 template <typename T, int SRC, int G, int L>
 __global__ void __launch_bounds__(kCandThreads, SRC == SAT_SRC_INDEX ? 8 : (G <= 8 ? 12 : (G <= 16 ? 10 : 8)))
 k_cand(CandArgs a) {
@@ -663,7 +776,13 @@ k_ls(LsArgs a) {
                             rec[k * 32] = rec_for(tb, job, o);
                         }
                         uint64_t ld = 0;
-                        const T ms = schedule_records<T, G, L, true>(sc, rec, &ld, k0, use_cache ? cache : nullptr);
+                        T ms;
+                        // register shifts pay off on wide nodes (G = 32: ~110 instructions per
+                        // shared-memory placement); at G = 8 the warp votes cost more than they save
+                        if constexpr (L == kLayoutOne16 && G >= 16)
+                            ms = schedule_eval16<G>(sc, rec, &ld, k0, use_cache ? cache : nullptr);
+                        else
+                            ms = schedule_records<T, G, L, true>(sc, rec, &ld, k0, use_cache ? cache : nullptr);
                         bk = ((uint64_t)(uint32_t)ms << 34) | ld;
                         bm = m;
                     }

@@ -425,6 +425,30 @@ def test_local_search_records_every_walker_state(eng, name, stop):
     assert (list(res.state[0]), list(res.state[1])) == (o, r)
 
 
+def test_local_search_wide_nodes_register_path(eng):
+    """Nodes of 9-32 GPUs (padded 16 / 32: the move evaluation shifts in registers when the
+    warp's lanes place equal gang sizes, in shared memory otherwise), with releases and initial
+    free times: every walker's final candidate equals the oracle's."""
+    rng = random.Random(17)
+    for trial in range(8):
+        nodes = [[16], [12], [32], [24]][trial % 4]
+        op = random_problem(rng, rng.randint(4, 8), nodes, max_opts=4, max_d=9)
+        if trial % 2:
+            op.release = [rng.randint(0, 4) for _ in range(op.J)]
+            op.init_free = [[rng.randint(0, 3) for _ in range(n)] for n in nodes]
+        prob = to_search_problem(op)
+        bits, _ = prob.key_bits(1 << 10)
+        nprob = EN.NativeProblem(prob, bits)
+        cp = C.CProblem(op)
+        for walker in (0, 5, 9):
+            ms, o, r, _ = cp.local_search(walker, "substream", 3, 4096)
+            assert eng.local_search_state(nprob, EN.SRC_SUBSTREAM, 3, walker, 4096) == (o, r), (trial, walker)
+        best = eng.reset_best()
+        eng.local_search(nprob, EN.SRC_SUBSTREAM, 3, 0, 32, 4096, best)
+        k = int(best.cpu().numpy().view(np.uint64)[0])
+        assert (float(k >> bits), k & ((1 << bits) - 1)) == cp.ls_search("substream", 3, 0, 32, 4096), trial
+
+
 def test_local_search_seed_source_and_release(eng):
     rng = random.Random(9)
     for trial in range(6):
