@@ -262,6 +262,12 @@ def build_problem(table, workload, opts: SolveOptions | None = None, running_con
 
     # per job: canonical option list with per-node runtimes
     from .profiling import feasible_entries  # local: avoid a cycle at import time
+    shapes = {}                         # (gpu_count, gpu_memory) -> shape index
+    node_shape = [shapes.setdefault((n.gpu_count, n.gpu_memory), len(shapes)) for n in nodes]
+    shape_rep = [None] * len(shapes)
+    for n, sh in zip(nodes, node_shape):
+        if shape_rep[sh] is None:
+            shape_rep[sh] = n
     rows = []
     for job in pool:
         entries = feasible_entries(table, job, workload)
@@ -279,12 +285,15 @@ def build_problem(table, workload, opts: SolveOptions | None = None, running_con
         else:
             for cfg, lat in entries:
                 tech = tech_by_name[cfg.technique]
+                # eligibility depends on the node only through its shape: once per shape
+                elig = [node_eligible(job, tech, cfg.gpus, rep) for rep in shape_rep]
+                t0 = rem * lat                                    # profiling.py:151
                 per_node = []
-                for n in nodes:
-                    if not node_eligible(job, tech, cfg.gpus, n):
+                for n, sh in zip(nodes, node_shape):
+                    if not elig[sh]:
                         per_node.append(INFEASIBLE)
                         continue
-                    t = rem * lat                                 # profiling.py:151
+                    t = t0
                     if cur is not None and (cfg.technique, cfg.gpus, n.id) != cur:
                         t = t + rho
                     per_node.append(t)
@@ -325,22 +334,20 @@ def build_problem(table, workload, opts: SolveOptions | None = None, running_con
 
     Cmax = max(len(r) for r in kept_rows)
     radix = np.array([len(r) for r in kept_rows], dtype=np.int32)
-    gpus = np.zeros((J, Cmax), dtype=np.int32)
-    mask = np.zeros((J, Cmax), dtype=np.uint32)
-    runtime = np.zeros((J, Cmax, N), dtype=np.float64)
-    dur = np.zeros((J, Cmax, N), dtype=np.int32)
-    for j, row in enumerate(kept_rows):
-        for o, (cfg, _lat, per_node) in enumerate(row):
-            gpus[j, o] = cfg.gpus
-            for n, t in enumerate(per_node):
-                if math.isinf(t):
-                    continue
-                mask[j, o] |= np.uint32(1 << n)
-                runtime[j, o, n] = t
-                d = math.ceil(t / delta)
-                if d >= INF_I32 // 4:
-                    raise err.TooLarge(f"duration {d} intervals overflows the device time type")
-                dur[j, o, n] = d
+    # dense tables in one pass: rows padded to Cmax with infeasible options
+    pad_rt = [INFEASIBLE] * N
+    rt_all = np.array([[pn for _, _, pn in row] + [pad_rt] * (Cmax - len(row)) for row in kept_rows],
+                      dtype=np.float64).reshape(J, Cmax, N)
+    gpus = np.array([[cfg.gpus for cfg, _, _ in row] + [0] * (Cmax - len(row)) for row in kept_rows],
+                    dtype=np.int32).reshape(J, Cmax)
+    ok = np.isfinite(rt_all)
+    mask = (ok.astype(np.uint32) << np.arange(N, dtype=np.uint32)[None, None, :]).sum(axis=2, dtype=np.uint32)
+    runtime = np.where(ok, rt_all, 0.0)
+    with np.errstate(invalid="ignore"):
+        dq = np.ceil(np.where(ok, rt_all, 0.0) / delta)         # SPEC.md:183, same IEEE ops as math.ceil(t / delta)
+    if (dq >= INF_I32 // 4).any():
+        raise err.TooLarge(f"duration {int(dq.max())} intervals overflows the device time type")
+    dur = dq.astype(np.int32)
 
     init_i = np.full((N, G), INF_I32, dtype=np.int32)
     init_f = np.full((N, G), np.inf, dtype=np.float64)
