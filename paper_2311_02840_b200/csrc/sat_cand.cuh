@@ -778,8 +778,10 @@ k_ls(LsArgs a) {
                         uint64_t ld = 0;
                         T ms;
                         // register shifts pay off on wide nodes (G = 32: ~110 instructions per
-                        // shared-memory placement); at G = 8 the warp votes cost more than they save
-                        if constexpr (L == kLayoutOne16 && G >= 16)
+                        // shared-memory placement) in the 8-warp walker (cfg5 13.2 -> 11.7 ms); with
+                        // 1 or 4 warps per walker, or at G = 8, the warp votes cost more than they save
+                        // (profiles/r01g_ls_group_sweep.txt)
+                        if constexpr (L == kLayoutOne16 && G >= 16 && K == 8)
                             ms = schedule_eval16<G>(sc, rec, &ld, k0, use_cache ? cache : nullptr);
                         else
                             ms = schedule_records<T, G, L, true>(sc, rec, &ld, k0, use_cache ? cache : nullptr);

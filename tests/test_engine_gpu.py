@@ -425,10 +425,12 @@ def test_local_search_records_every_walker_state(eng, name, stop):
     assert (list(res.state[0]), list(res.state[1])) == (o, r)
 
 
-def test_local_search_wide_nodes_register_path(eng):
-    """Nodes of 9-32 GPUs (padded 16 / 32: the move evaluation shifts in registers when the
-    warp's lanes place equal gang sizes, in shared memory otherwise), with releases and initial
-    free times: every walker's final candidate equals the oracle's."""
+@pytest.mark.parametrize("group", ["1", "8"])
+def test_local_search_wide_nodes_register_path(eng, group, monkeypatch):
+    """Nodes of 9-32 GPUs (padded 16 / 32; with 8 warps per walker the move evaluation shifts
+    in registers when the warp's lanes place equal gang sizes, in shared memory otherwise), with
+    releases and initial free times: every walker's final candidate equals the oracle's."""
+    monkeypatch.setenv("SATURN_LS_GROUP", group)
     rng = random.Random(17)
     for trial in range(8):
         nodes = [[16], [12], [32], [24]][trial % 4]
