@@ -357,9 +357,11 @@ template <int G>
 __host__ __device__ __forceinline__ int tree_level_off(int L, bool compact) {
     return compact ? (L == 0 ? 0 : (2 * G + (L - 1) * G) * 32) : L * 2 * G * 32;
 }
+// Compact: the last level (the register walk's exact-pass input) shares the exact pass's
+// scratch column Bbuf (the exact pass reads its input into registers before writing).
 template <int G>
 __host__ __device__ __forceinline__ int tree_warp_words(int Q, bool compact) {
-    return tree_level_off<G>(Q - 1, compact) + G * 32;      // level buffers 0..Q-2, then Bbuf
+    return tree_level_off<G>(compact ? Q - 2 : Q - 1, compact) + G * 32;   // level buffers, then Bbuf
 }
 __host__ __device__ __forceinline__ bool tree_compact(bool bnb, bool packed, int G, int Q) {
     return !bnb && packed && G >= 2 && G <= kTreePackMaxG && (Q == 3 || Q == 4);
@@ -402,8 +404,7 @@ __device__ __forceinline__ void walk_fixed(const TreeParams &p, int32_t *wbase, 
                 bool done = false;
                 if constexpr (!BNB && D == 2 && G >= 2 && G <= kTreePackMaxG) {
                     if (p.packed) {     // three jobs left: the register-resident packed walk
-                        walk_q3_16<G>(p, dst, wbase + tree_level_off<G>(L + 2, compact) + lane, Bbuf, sdg, rem2, acc,
-                                      child_ok, lb);
+                        walk_q3_16<G>(p, dst, Bbuf, Bbuf, sdg, rem2, acc, child_ok, lb);
                         done = true;
                     }
                 }
@@ -426,7 +427,7 @@ k_tree(const __grid_constant__ TreeParams p) {
     const int upper = Q - 1;                         // level buffers 0..Q-2 (padded)
     const bool compact = tree_compact(BNB, p.packed != 0, G, Q);
     int32_t *wbase = tsm + warp * tree_warp_words<G>(Q, compact);
-    int32_t *Bbuf = wbase + tree_level_off<G>(upper, compact) + lane;
+    int32_t *Bbuf = wbase + tree_level_off<G>(compact ? upper - 1 : upper, compact) + lane;
     // per (job, gang) least durations, shared by the block (broadcast loads in the pair pass)
     // per (job, gang) least durations, read straight from the parameter block: the job index
     // is warp-uniform, so these are uniform constant loads and the gang branches uniform
@@ -532,8 +533,7 @@ k_tree(const __grid_constant__ TreeParams p) {
             bool done = false;
             if constexpr (!BNB && G >= 2 && G <= kTreePackMaxG) {
                 if (p.packed) {
-                    walk_q3_16<G>(p, L0, wbase + tree_level_off<G>(1, compact) + lane, Bbuf, sdg, unplaced, base,
-                                  lane_ok, lb);
+                    walk_q3_16<G>(p, L0, Bbuf, Bbuf, sdg, unplaced, base, lane_ok, lb);
                     done = true;
                 }
             }
