@@ -305,7 +305,7 @@ def build_problem(table, workload, opts: SolveOptions | None = None, running_con
     J = len(pool)
     if J == 0:
         raise err.InvariantViolation("jobs", "nothing to plan")
-    min_rt = [min(t for _, _, pn in row for t in pn) for row in rows]
+    min_rt = [min(min(pn) for _, _, pn in row) for row in rows]
     if opts.delta is not None:
         delta = float(opts.delta)
         if not delta > 0:
@@ -324,9 +324,9 @@ def build_problem(table, workload, opts: SolveOptions | None = None, running_con
     kept_rows, kept_src = [], []
     for row in rows:
         if prune:
-            def cost(t):
-                return math.ceil(t / delta) if grid else t
-            keep = _dominance_prune([(i, cfg.gpus, cost(pn[0])) for i, (cfg, _, pn) in enumerate(row)])
+            ceil = math.ceil
+            keep = _dominance_prune([(i, cfg.gpus, ceil(pn[0] / delta)) for i, (cfg, _, pn) in enumerate(row)]
+                                    if grid else [(i, cfg.gpus, pn[0]) for i, (cfg, _, pn) in enumerate(row)])
         else:
             keep = list(range(len(row)))
         kept_rows.append([row[i] for i in keep])
