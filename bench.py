@@ -439,6 +439,10 @@ def run_ours(args):
                "device_s": max_over_ranks(statistics.median(dev[1:]), world) if dev else None,
                "stats": stats,
                "api": api.replace("(plan_saturn)", "(plan_saturn, default options)")}
+        if ttb["device_s"]:
+            # candidates covered (scheduled or cut by a bound) per second,
+            # reported apart from the full scan's evaluated/s
+            ttb["covered_per_s"] = head.n_cand / ttb["device_s"]
     else:
         # spaces beyond exact search: the default solve is local search from sampled starts;
         # report the plan it reaches, the lower bound and the time (next to the sampled sweep)
