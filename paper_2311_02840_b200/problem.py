@@ -22,12 +22,13 @@ Everything here runs once per solve; the per-candidate work is on the device.
 from __future__ import annotations
 
 import math
+from itertools import repeat
 from dataclasses import dataclass, field
 
 import numpy as np
 
 from . import errors as E
-from .domain import RunConfig, node_eligible
+from .domain import RunConfig, feasible_configs, node_eligible
 from .profiling import INFEASIBLE
 
 TIME_GRID = "grid"
@@ -221,6 +222,55 @@ def _dominance_prune(cost_rows: list) -> list:
     return sorted(kept)
 
 
+class _OneNodeRow:
+    """One-node option row before the prune: the job's feasible configs `cfgs`, the indices
+    `sel` of those with a finite latency `lat`, runtimes t = rem x lat and gang sizes g."""
+    __slots__ = ("cfgs", "sel", "lat", "t", "g")
+
+    def __init__(self, cfgs, sel, lat, t, g):
+        self.cfgs, self.sel, self.lat, self.t, self.g = cfgs, sel.tolist(), lat, t, g
+
+
+_ONE_NODE_MEMO: dict = {}
+
+
+def _one_node_options(job, workload):
+    """(configs, profile-table keys, gang sizes) of `feasible_configs` (core.py:165-182), a pure
+    function of immutable inputs memoised by value like `feasible_configs` itself."""
+    techniques = tuple(workload.techniques)
+    try:
+        key = (job, workload.cluster, techniques)
+        hit = _ONE_NODE_MEMO.get(key)
+    except TypeError:                   # unhashable inputs: compute every time
+        key, hit = None, None
+    if hit is None:
+        cfgs = tuple(feasible_configs(job, workload.cluster, techniques))
+        keys = tuple((job.id, c.technique, c.gpus) for c in cfgs)
+        hit = (cfgs, keys, np.array([c.gpus for c in cfgs], dtype=np.int64))
+        if key is not None:
+            if len(_ONE_NODE_MEMO) > 1 << 16:
+                _ONE_NODE_MEMO.clear()
+            _ONE_NODE_MEMO[key] = hit
+    return hit
+
+
+def _dominance_prune_arrays(g: np.ndarray, cost: np.ndarray) -> list:
+    """`_dominance_prune` over arrays (same result): per g the cheapest option, earliest on
+    ties (lexsort by g, cost, index; first of each g), then g kept while the cost strictly
+    decreases.  Costs are exact integers (grid) or the runtimes themselves (float)."""
+    n = len(g)
+    order = np.lexsort((np.arange(n), cost, g))
+    gs = g[order]
+    first = order[np.r_[True, gs[1:] != gs[:-1]]]          # best option per g, ascending g
+    kept, last = [], None
+    for idx, c in zip(first.tolist(), cost[first].tolist()):
+        if last is None or c < last:
+            kept.append(idx)
+            last = c
+    kept.sort()
+    return kept
+
+
 def choose_delta(min_runtimes: list, k_max: int = K_MAX_DEFAULT) -> float:
     """delta = max(sequential-best total / K_max, shortest job / 4).
     Summation is left to right in job-id order (fixed so oracle and engine agree)."""
@@ -269,35 +319,43 @@ def build_problem(table, workload, opts: SolveOptions | None = None, running_con
         if shape_rep[sh] is None:
             shape_rep[sh] = n
     rows = []
+    get = table.entries.get
     for job in pool:
-        entries = feasible_entries(table, job, workload)
-        if not entries:
-            raise err.NoFeasibleConfig(job.id)
         rem = remaining[job.id]
         cur = current.get(job.id)
         cur = tuple(cur) if cur is not None else None
-        row = []
         if N == 1 and cur is None:
             # one node: every feasible (technique, g) runs on it (core.py:165-182 keeps only
-            # configs some node hosts), so the runtime is the plain estimate (profiling.py:151)
-            rows.append([(cfg, lat, [rem * lat]) for cfg, lat in entries])     # all finite
+            # configs some node hosts), so the runtime is the plain estimate (profiling.py:151).
+            # feasible_entries (profiling.py:154-161) as arrays: rem * lat elementwise is the
+            # same IEEE product; per-option tuples are built only for the prune's survivors.
+            cfgs, keys, g_all = _one_node_options(job, workload)
+            lat_all = np.fromiter(map(get, keys, repeat(INFEASIBLE)), dtype=np.float64, count=len(keys))
+            sel = np.flatnonzero(np.isfinite(lat_all))
+            if not len(sel):
+                raise err.NoFeasibleConfig(job.id)
+            lat = lat_all[sel]
+            rows.append(_OneNodeRow(cfgs, sel, lat, rem * lat, g_all[sel]))
             continue
-        else:
-            for cfg, lat in entries:
-                tech = tech_by_name[cfg.technique]
-                # eligibility depends on the node only through its shape: once per shape
-                elig = [node_eligible(job, tech, cfg.gpus, rep) for rep in shape_rep]
-                t0 = rem * lat                                    # profiling.py:151
-                per_node = []
-                for n, sh in zip(nodes, node_shape):
-                    if not elig[sh]:
-                        per_node.append(INFEASIBLE)
-                        continue
-                    t = t0
-                    if cur is not None and (cfg.technique, cfg.gpus, n.id) != cur:
-                        t = t + rho
-                    per_node.append(t)
-                row.append((cfg, lat, per_node))
+        entries = feasible_entries(table, job, workload)
+        if not entries:
+            raise err.NoFeasibleConfig(job.id)
+        row = []
+        for cfg, lat in entries:
+            tech = tech_by_name[cfg.technique]
+            # eligibility depends on the node only through its shape: once per shape
+            elig = [node_eligible(job, tech, cfg.gpus, rep) for rep in shape_rep]
+            t0 = rem * lat                                    # profiling.py:151
+            per_node = []
+            for n, sh in zip(nodes, node_shape):
+                if not elig[sh]:
+                    per_node.append(INFEASIBLE)
+                    continue
+                t = t0
+                if cur is not None and (cfg.technique, cfg.gpus, n.id) != cur:
+                    t = t + rho
+                per_node.append(t)
+            row.append((cfg, lat, per_node))
         if all(math.isinf(t) for _, _, pn in row for t in pn):
             raise err.NoFeasibleConfig(job.id)
         rows.append(row)
@@ -305,7 +363,8 @@ def build_problem(table, workload, opts: SolveOptions | None = None, running_con
     J = len(pool)
     if J == 0:
         raise err.InvariantViolation("jobs", "nothing to plan")
-    min_rt = [min(min(pn) for _, _, pn in row) for row in rows]
+    min_rt = [row.t.min().item() if type(row) is _OneNodeRow else min(min(pn) for _, _, pn in row)
+              for row in rows]
     if opts.delta is not None:
         delta = float(opts.delta)
         if not delta > 0:
@@ -323,6 +382,14 @@ def build_problem(table, workload, opts: SolveOptions | None = None, running_con
 
     kept_rows, kept_src = [], []
     for row in rows:
+        if type(row) is _OneNodeRow:
+            if prune:
+                keep = _dominance_prune_arrays(row.g, np.ceil(row.t / delta) if grid else row.t)
+            else:
+                keep = range(len(row.t))
+            kept_rows.append([(row.cfgs[row.sel[i]], row.lat[i].item(), [row.t[i].item()]) for i in keep])
+            kept_src.append(list(keep))
+            continue
         if prune:
             ceil = math.ceil
             keep = _dominance_prune([(i, cfg.gpus, ceil(pn[0] / delta)) for i, (cfg, _, pn) in enumerate(row)]

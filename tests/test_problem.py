@@ -207,3 +207,38 @@ def test_optimus_marginal_gain_spec_examples():
     assert PL.optimus_marginal_gain(t, job, 2, 1000) == 0.0              # 0.55 > 0.5: harmful GPU
     assert PL.optimus_marginal_gain(t, job, 3, 1000) == 0.0              # g+1 infeasible
     assert PL.optimus_marginal_gain(t, job, 8, 1000) == 0.0              # beyond the table
+
+
+@pytest.mark.parametrize("mode", ["grid", "float"])
+def test_one_node_array_marshalling_matches_oracle(mode):
+    """The one-node fast path (profile rows as arrays, prune on arrays) against the oracle's
+    build on random one-node workloads, one table entry made infeasible and one dropped."""
+    from paper_2311_02840_b200.workloads import random_workload
+
+    for seed in range(40):
+        w = random_workload(seed, n_nodes=1)
+        t = build_profile_table(w, SyntheticExecutor(w.cluster))
+        keys = sorted(t.entries)
+        if seed % 3 == 1 and len(keys) > 2:
+            t.entries[keys[seed % len(keys)]] = math.inf
+        if seed % 3 == 2 and len(keys) > 2:
+            del t.entries[keys[(7 * seed) % len(keys)]]
+        try:
+            oprob = O.build(t.entries, w, grid=mode == "grid")
+        except Exception as exc:  # noqa: BLE001 -- both sides must refuse the same way
+            with pytest.raises(type(exc)):
+                build_problem(t, w, SolveOptions(time_mode=mode))
+            continue
+        compare(build_problem(t, w, SolveOptions(time_mode=mode)), oprob)
+
+
+def test_dominance_prune_arrays_equals_list_prune():
+    from paper_2311_02840_b200.problem import _dominance_prune, _dominance_prune_arrays
+
+    rng = np.random.default_rng(5)
+    for _ in range(500):
+        n = int(rng.integers(1, 40))
+        g = rng.integers(1, 9, n)
+        cost = rng.integers(1, 12, n).astype(np.float64)      # many ties
+        want = _dominance_prune([(i, int(g[i]), float(cost[i])) for i in range(n)])
+        assert _dominance_prune_arrays(g, cost) == want
