@@ -339,26 +339,32 @@ class Engine:
             ids_t = torch.as_tensor(np.asarray(ids, dtype=np.uint64).view(np.int64)).to(self.device)
             n = ids_t.numel()
             ex = None
-        opt = torch.empty((n, J), dtype=torch.int32, device=self.device)
-        node = torch.empty((n, J), dtype=torch.int32, device=self.device)
-        if nprob.grid:
-            start = torch.empty((n, J), dtype=torch.int32, device=self.device)
-            ms = torch.empty(n, dtype=torch.int64, device=self.device)
-        else:
-            start = torch.empty((n, J), dtype=torch.float64, device=self.device)
-            ms = torch.empty(n, dtype=torch.float64, device=self.device)
+        # one device buffer for the four outputs -> one device-to-host read after the launch
+        # layout: opt [n, J] i32 | node [n, J] i32 | start [n, J] i32/f64 | makespan [n] i64/f64
+        st_dt, ms_dt = (np.int32, np.int64) if nprob.grid else (np.float64, np.float64)
+        a8 = lambda b: (b + 7) & ~7                                              # noqa: E731
+        o_node = a8(4 * n * J)
+        o_start = o_node + a8(4 * n * J)
+        o_ms = o_start + a8(np.dtype(st_dt).itemsize * n * J)
+        out = torch.empty(o_ms + 8 * n, dtype=torch.uint8, device=self.device)
+        base = out.data_ptr()
+        opt_p, node_p, start_p, ms_p = base, base + o_node, base + o_start, base + o_ms
         ws, wsb = self.workspace(nprob)
         g = nprob.grid
         self._check(self.lib.sat_schedule(
             nprob.ref, source, seed & ((1 << 64) - 1),
             _vp(ids_t.data_ptr()) if ids_t is not None else None,
             _vp(ex.data_ptr()) if ex is not None else None, n,
-            _vp(opt.data_ptr()), _vp(node.data_ptr()),
-            _vp(start.data_ptr()) if g else None, None if g else _vp(start.data_ptr()),
-            _vp(ms.data_ptr()) if g else None, None if g else _vp(ms.data_ptr()),
+            _vp(opt_p), _vp(node_p),
+            _vp(start_p) if g else None, None if g else _vp(start_p),
+            _vp(ms_p) if g else None, None if g else _vp(ms_p),
             _vp(ws), wsb, _vp(self.stream())), what="sat_schedule")
         self.launches += 1
-        return opt.cpu().numpy(), node.cpu().numpy(), start.cpu().numpy(), ms.cpu().numpy()
+        h = out.cpu().numpy()
+        return (h[:4 * n * J].view(np.int32).reshape(n, J),
+                h[o_node:o_node + 4 * n * J].view(np.int32).reshape(n, J),
+                h[o_start:o_start + np.dtype(st_dt).itemsize * n * J].view(st_dt).reshape(n, J),
+                h[o_ms:o_ms + 8 * n].view(ms_dt))
 
     # ---- orchestration ---------------------------------------------------------
     def plan_search(self, prob: SearchProblem, opts: SolveOptions, group=None) -> tuple:

@@ -104,24 +104,32 @@ class Solution:
 
 def _decode(engine: Engine, prob: SearchProblem, nprob: NativeProblem, workload, source: int, seed: int,
             ident=None, explicit=None):
-    """Replay one candidate on the device; build the Plan."""
-    opt, node, start, ms = engine.schedule(nprob, source, seed,
-                                           ids=None if ident is None else [ident],
-                                           explicit=None if explicit is None else explicit[None, :])
+    """Replay candidates on the device (one launch, one read-back); build their Plans.
+    One candidate (``ident`` or a 1-D ``explicit`` row) -> one tuple; a 2-D ``explicit``
+    batch -> a list of tuples, row by row."""
+    batch = explicit is not None and np.ndim(explicit) == 2
+    schedule = engine.schedule(nprob, source, seed, ids=None if ident is None else [ident],
+                               explicit=None if explicit is None else np.atleast_2d(explicit))
+    out = [_plan_of(prob, workload, schedule, r) for r in range(len(schedule[3]))]
+    return out if batch else out[0]
+
+
+def _plan_of(prob: SearchProblem, workload, schedule, r: int):
+    opt, node, start, ms = schedule
     Plan, PlanEntry, RunConfig = _types_for(workload)
     grid = prob.time_mode == TIME_GRID
     scale = prob.delta if grid else 1.0
     entries, runtimes = {}, {}
     for j, job_id in enumerate(prob.job_ids):
-        o, n = int(opt[0, j]), int(node[0, j])
+        o, n = int(opt[r, j]), int(node[r, j])
         cfg = prob.options[j][o][0]
-        s = float(start[0, j]) * scale
+        s = float(start[r, j]) * scale
         entries[job_id] = PlanEntry(config=RunConfig(technique=cfg.technique, gpus=cfg.gpus),
                                     node=prob.node_ids[n], start_time=s)
         runtimes[job_id] = float(prob.runtime[j, o, n])
-    predicted = float(ms[0]) * scale
+    predicted = float(ms[r]) * scale
     plan = Plan(entries=entries, predicted_makespan=predicted)
-    return plan, [int(x) for x in opt[0]], float(ms[0]), runtimes
+    return plan, [int(x) for x in opt[r]], float(ms[r]), runtimes
 
 
 def solve(table, jobs, cluster=None, delta_opts=None, running_context=None, *, techniques=None,
@@ -149,22 +157,29 @@ def solve_problem(prob: SearchProblem, workload, opts: SolveOptions, running_con
                 o_, r_ = eng.local_search_state(nprob, res.source, res.seed, res.index, opts.max_rounds,
                                                 stop_ms=res.stats.get("stop_ms", -1))
             explicit = np.array(list(o_) + list(r_), dtype=np.uint8)
-            plan, options, ms, runtimes = _decode(eng, prob, NativeProblem(prob, 62), workload, SRC_EXPLICIT, 0,
-                                                  explicit=explicit)
-        else:
-            src = SRC_INDEX if res.exhaustive else res.source
-            plan, options, ms, runtimes = _decode(eng, prob, nprob, workload, src, res.seed, ident=res.index)
-        incumbent = None
+        incumbent, baselines = None, []
         if not res.exhaustive:
             # heuristic searches also weigh the greedy baselines as incumbents (the B&B's
             # "initial incumbent from rounding"): the plan is never worse than them
-            nexp = NativeProblem(prob, 62)
             for builder in (optimus_allocation, current_practice_allocation):
                 b_opts, b_order = builder(prob)
-                ex = np.array(list(b_opts) + list(b_order), dtype=np.uint8)
-                cand = _decode(eng, prob, nexp, workload, SRC_EXPLICIT, 0, explicit=ex)
-                if cand[2] < ms and (incumbent is None or cand[2] < incumbent[0][2]):
-                    incumbent = (cand, list(b_order), builder.__name__)
+                baselines.append((np.array(list(b_opts) + list(b_order), dtype=np.uint8), list(b_order),
+                                  builder.__name__))
+        nexp = NativeProblem(prob, 62) if (baselines or res.kernel == "local") else None
+        if res.kernel == "local":
+            # the winner's final candidate and the baselines: one explicit batch, one launch
+            cands = _decode(eng, prob, nexp, workload, SRC_EXPLICIT, 0,
+                            explicit=np.stack([explicit] + [b[0] for b in baselines]))
+            plan, options, ms, runtimes = cands[0]
+            cands = cands[1:]
+        else:
+            src = SRC_INDEX if res.exhaustive else res.source
+            plan, options, ms, runtimes = _decode(eng, prob, nprob, workload, src, res.seed, ident=res.index)
+            cands = _decode(eng, prob, nexp, workload, SRC_EXPLICIT, 0,
+                            explicit=np.stack([b[0] for b in baselines])) if baselines else []
+        for cand, (_, b_order, name) in zip(cands, baselines):
+            if cand[2] < ms and (incumbent is None or cand[2] < incumbent[0][2]):
+                incumbent = (cand, b_order, name)
     except E.SchedulerError:
         raise
     except Exception as exc:  # CUDA / NCCL trouble -> PlanFailure (ReplanFailure on re-solve)

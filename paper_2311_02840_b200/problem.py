@@ -232,6 +232,7 @@ class _OneNodeRow:
 
 
 _ONE_NODE_MEMO: dict = {}
+_ARRAY_ROW_MIN = 48          # one-node rows with at least this many configs go through arrays
 
 
 def _one_node_options(job, workload):
@@ -330,6 +331,13 @@ def build_problem(table, workload, opts: SolveOptions | None = None, running_con
             # feasible_entries (profiling.py:154-161) as arrays: rem * lat elementwise is the
             # same IEEE product; per-option tuples are built only for the prune's survivors.
             cfgs, keys, g_all = _one_node_options(job, workload)
+            if len(keys) < _ARRAY_ROW_MIN:      # short rows: plain tuples beat numpy call overhead
+                lats = list(map(get, keys, repeat(INFEASIBLE)))
+                row = [(c, lat, [rem * lat]) for c, lat in zip(cfgs, lats) if math.isfinite(lat)]
+                if not row:
+                    raise err.NoFeasibleConfig(job.id)
+                rows.append(row)
+                continue
             lat_all = np.fromiter(map(get, keys, repeat(INFEASIBLE)), dtype=np.float64, count=len(keys))
             sel = np.flatnonzero(np.isfinite(lat_all))
             if not len(sel):

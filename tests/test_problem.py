@@ -209,11 +209,16 @@ def test_optimus_marginal_gain_spec_examples():
     assert PL.optimus_marginal_gain(t, job, 8, 1000) == 0.0              # beyond the table
 
 
+@pytest.mark.parametrize("row_min", [0, 1 << 30])
 @pytest.mark.parametrize("mode", ["grid", "float"])
-def test_one_node_array_marshalling_matches_oracle(mode):
-    """The one-node fast path (profile rows as arrays, prune on arrays) against the oracle's
-    build on random one-node workloads, one table entry made infeasible and one dropped."""
+def test_one_node_array_marshalling_matches_oracle(mode, row_min, monkeypatch):
+    """Both one-node marshalling paths (rows as arrays with the array prune; short rows as
+    tuples) against the oracle's build on random one-node workloads, one table entry made
+    infeasible and one dropped."""
+    from paper_2311_02840_b200 import problem as P
     from paper_2311_02840_b200.workloads import random_workload
+
+    monkeypatch.setattr(P, "_ARRAY_ROW_MIN", row_min)
 
     for seed in range(40):
         w = random_workload(seed, n_nodes=1)
