@@ -265,17 +265,30 @@ def plan_random_best(table, jobs, cluster=None, seed0: int = 0, n_seeds: int = 1
 # Optimus -- host allocator, device schedule
 # --------------------------------------------------------------------------
 
+def _best_runtime_all(prob: SearchProblem) -> list:
+    """Per job: g -> (runtime seconds, option) minimising runtime over techniques at that g
+    (earliest option on ties); runtime on the job's fastest eligible node.  One array pass
+    over the problem's [J, Cmax, N] tables, then a short loop per job over its options."""
+    N = prob.N
+    elig = ((prob.node_mask[:, :, None] >> np.arange(N, dtype=np.uint32)) & 1).astype(bool)
+    rt_all = np.where(elig, prob.runtime, np.inf).min(axis=2).tolist()
+    any_all = elig.any(axis=2).tolist()
+    gpus_all = prob.gpus.tolist()
+    out_all = []
+    for j, R in enumerate(prob.radix.tolist()):
+        if not all(any_all[j][:R]):
+            raise ValueError("min() arg is an empty sequence")  # an option no node can run
+        out: dict = {}
+        for o, (g, r) in enumerate(zip(gpus_all[j][:R], rt_all[j][:R])):
+            if g not in out or r < out[g][0]:
+                out[g] = (r, o)
+        out_all.append(out)
+    return out_all
+
+
 def _best_runtime_by_g(prob: SearchProblem, j: int) -> dict:
-    """g -> (runtime seconds, option) minimising runtime over techniques at that g
-    (earliest option on ties); runtime on the job's fastest eligible node."""
-    out: dict = {}
-    for o in range(int(prob.radix[j])):
-        g = int(prob.gpus[j, o])
-        rts = [prob.runtime[j, o, n] for n in range(prob.N) if (int(prob.node_mask[j, o]) >> n) & 1]
-        rt = min(rts)
-        if g not in out or rt < out[g][0]:
-            out[g] = (rt, o)
-    return out
+    """`_best_runtime_all` for one job."""
+    return _best_runtime_all(prob)[j]
 
 
 def _problem_gain(prob: SearchProblem, j: int, g: int, best=None) -> float:
@@ -315,7 +328,7 @@ def optimus_allocation(prob: SearchProblem) -> tuple:
     J = prob.J
     total = int(prob.node_gpus.sum())
     node_max = int(prob.node_gpus.max())
-    best = [_best_runtime_by_g(prob, j) for j in range(J)]
+    best = _best_runtime_all(prob)
     gmin = [min(b) for b in best]
     alloc = [0] * J
     waves = []
@@ -374,8 +387,7 @@ def current_practice_allocation(prob: SearchProblem) -> tuple:
     technique at that g; jobs in id order, each on the earliest-free node."""
     node_max = int(prob.node_gpus.max())
     options = []
-    for j in range(prob.J):
-        best = _best_runtime_by_g(prob, j)
+    for best in _best_runtime_all(prob):
         g = node_max if node_max in best else max(best)
         options.append(best[g][1])
     return options, list(range(prob.J))
