@@ -236,8 +236,9 @@ _ARRAY_ROW_MIN = 48          # one-node rows with at least this many configs go 
 
 
 def _one_node_options(job, workload):
-    """(configs, profile-table keys, gang sizes) of `feasible_configs` (core.py:165-182), a pure
-    function of immutable inputs memoised by value like `feasible_configs` itself."""
+    """(configs, profile-table keys, gang sizes, per-node eligibility) of `feasible_configs`
+    (core.py:165-182) for one job, a pure function of immutable inputs memoised by value like
+    `feasible_configs` itself.  Eligibility depends on a node only through its shape."""
     techniques = tuple(workload.techniques)
     try:
         key = (job, workload.cluster, techniques)
@@ -247,7 +248,19 @@ def _one_node_options(job, workload):
     if hit is None:
         cfgs = tuple(feasible_configs(job, workload.cluster, techniques))
         keys = tuple((job.id, c.technique, c.gpus) for c in cfgs)
-        hit = (cfgs, keys, np.array([c.gpus for c in cfgs], dtype=np.int64))
+        tech_by_name = {t.name: t for t in techniques}
+        shape_elig: dict = {}
+        elig = []
+        for c in cfgs:
+            row = []
+            for n in workload.cluster.nodes:
+                k = (c.technique, c.gpus, n.gpu_count, n.gpu_memory)
+                e = shape_elig.get(k)
+                if e is None:
+                    e = shape_elig[k] = node_eligible(job, tech_by_name[c.technique], c.gpus, n)
+                row.append(e)
+            elig.append(tuple(row))
+        hit = (cfgs, keys, np.array([c.gpus for c in cfgs], dtype=np.int64), tuple(elig))
         if key is not None:
             if len(_ONE_NODE_MEMO) > 1 << 16:
                 _ONE_NODE_MEMO.clear()
@@ -330,7 +343,7 @@ def build_problem(table, workload, opts: SolveOptions | None = None, running_con
             # configs some node hosts), so the runtime is the plain estimate (profiling.py:151).
             # feasible_entries (profiling.py:154-161) as arrays: rem * lat elementwise is the
             # same IEEE product; per-option tuples are built only for the prune's survivors.
-            cfgs, keys, g_all = _one_node_options(job, workload)
+            cfgs, keys, g_all, _ = _one_node_options(job, workload)
             if len(keys) < _ARRAY_ROW_MIN:      # short rows: plain tuples beat numpy call overhead
                 lats = list(map(get, keys, repeat(INFEASIBLE)))
                 row = [(c, lat, [rem * lat]) for c, lat in zip(cfgs, lats) if math.isfinite(lat)]
@@ -344,6 +357,19 @@ def build_problem(table, workload, opts: SolveOptions | None = None, running_con
                 raise err.NoFeasibleConfig(job.id)
             lat = lat_all[sel]
             rows.append(_OneNodeRow(cfgs, sel, lat, rem * lat, g_all[sel]))
+            continue
+        if cur is None and techniques is workload.techniques:
+            # several nodes, no running config: runtime = plain estimate on every eligible node
+            # (profiling.py:151), eligibility per (config, node) from the memo
+            cfgs, keys, _, elig = _one_node_options(job, workload)
+            row = []
+            for c, lat, el in zip(cfgs, map(get, keys, repeat(INFEASIBLE)), elig):
+                if math.isfinite(lat):
+                    t0 = rem * lat
+                    row.append((c, lat, [t0 if e else INFEASIBLE for e in el]))
+            if not row or all(math.isinf(t) for _, _, pn in row for t in pn):
+                raise err.NoFeasibleConfig(job.id)
+            rows.append(row)
             continue
         entries = feasible_entries(table, job, workload)
         if not entries:
