@@ -334,6 +334,7 @@ def build_problem(table, workload, opts: SolveOptions | None = None, running_con
             shape_rep[sh] = n
     rows = []
     get = table.entries.get
+    node_id_list = [n.id for n in nodes]
     for job in pool:
         rem = remaining[job.id]
         cur = current.get(job.id)
@@ -358,15 +359,20 @@ def build_problem(table, workload, opts: SolveOptions | None = None, running_con
             lat = lat_all[sel]
             rows.append(_OneNodeRow(cfgs, sel, lat, rem * lat, g_all[sel]))
             continue
-        if cur is None and techniques is workload.techniques:
-            # several nodes, no running config: runtime = plain estimate on every eligible node
-            # (profiling.py:151), eligibility per (config, node) from the memo
+        if techniques is workload.techniques:
+            # several nodes or a running config: runtime = plain estimate on every eligible node
+            # (profiling.py:151), + rho off the job's running (technique, g, node);
+            # eligibility per (config, node) from the memo
             cfgs, keys, _, elig = _one_node_options(job, workload)
             row = []
             for c, lat, el in zip(cfgs, map(get, keys, repeat(INFEASIBLE)), elig):
                 if math.isfinite(lat):
                     t0 = rem * lat
-                    row.append((c, lat, [t0 if e else INFEASIBLE for e in el]))
+                    if cur is None:
+                        row.append((c, lat, [t0 if e else INFEASIBLE for e in el]))
+                    else:
+                        row.append((c, lat, [(t0 if (c.technique, c.gpus, nid) == cur else t0 + rho)
+                                             if e else INFEASIBLE for e, nid in zip(el, node_id_list)]))
             if not row or all(math.isinf(t) for _, _, pn in row for t in pn):
                 raise err.NoFeasibleConfig(job.id)
             rows.append(row)

@@ -247,3 +247,35 @@ def test_dominance_prune_arrays_equals_list_prune():
         cost = rng.integers(1, 12, n).astype(np.float64)      # many ties
         want = _dominance_prune([(i, int(g[i]), float(cost[i])) for i in range(n)])
         assert _dominance_prune_arrays(g, cost) == want
+
+
+def test_resolve_random_contexts_match_oracle():
+    """Re-solve marshalling on random workloads and random running contexts (some jobs done,
+    some running on a random feasible (technique, g, node), rho 0 / 30) against the oracle."""
+    from paper_2311_02840_b200.profiling import feasible_entries
+    from paper_2311_02840_b200.workloads import random_workload
+
+    for seed in range(30):
+        w = random_workload(seed)
+        t = build_profile_table(w, SyntheticExecutor(w.cluster))
+        rng = np.random.default_rng(seed)
+        remaining, current = {}, {}
+        for job in w.jobs:
+            remaining[job.id] = int(rng.integers(0, job.total_batches + 1)) if rng.random() < 0.8 else 0
+            ents = feasible_entries(t, job, w)
+            if remaining[job.id] and ents and rng.random() < 0.6:
+                cfg, _ = ents[int(rng.integers(len(ents)))]
+                node = w.cluster.nodes[int(rng.integers(len(w.cluster.nodes)))]
+                current[job.id] = (cfg.technique, cfg.gpus, node.id)
+        if not any(remaining.values()):
+            continue
+        rho = 30.0 if seed % 2 else 0.0
+        ctx = D.RunningContext(remaining=remaining, current=current, checkpoint_cost=rho)
+        for mode in ("grid", "float"):
+            try:
+                oprob = O.build(t.entries, w, grid=mode == "grid", context=(remaining, current, rho))
+            except Exception as exc:  # noqa: BLE001 -- both sides must refuse the same way
+                with pytest.raises(type(exc)):
+                    build_problem(t, w, SolveOptions(time_mode=mode), running_context=ctx)
+                continue
+            compare(build_problem(t, w, SolveOptions(time_mode=mode), running_context=ctx), oprob)
