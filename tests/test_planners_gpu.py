@@ -222,3 +222,32 @@ def test_public_api_edge_shapes(shape):
     if op.space <= 3_000_000:
         assert sol.makespan == C.CProblem(op).search()[0], (shape, sol.search.kernel)
     assert sol.lower_bound <= sol.makespan
+
+
+@pytest.mark.parametrize("cfg", [3, 4])
+def test_batched_replay_equals_single_replays(cfg):
+    """The winner and the Optimus / current-practice incumbents replay in one sat_schedule
+    launch: each row of the batch equals its own single-candidate replay and the oracle's
+    evaluation of the same (options, order)."""
+    from paper_2311_02840_b200.engine import SRC_EXPLICIT, NativeProblem
+    from paper_2311_02840_b200.problem import build_problem
+    from paper_2311_02840_b200.workloads import config_workload
+
+    w, t, _ = config_workload(cfg)
+    prob = build_problem(t, w, SolveOptions())
+    sol = PL.solve_problem(prob, w, SolveOptions())
+    eng = PL.get_engine()
+    nexp = NativeProblem(prob, 62)
+    rows = [np.array(list(sol.options) + list(sol.order), dtype=np.uint8)]
+    for builder in (PL.optimus_allocation, PL.current_practice_allocation):
+        o, r = builder(prob)
+        rows.append(np.array(list(o) + list(r), dtype=np.uint8))
+    batch = PL._decode(eng, prob, nexp, w, SRC_EXPLICIT, 0, explicit=np.stack(rows))
+    op = O.build(t.entries, w)
+    cp = C.CProblem(op)
+    for row, got in zip(rows, batch):
+        single = PL._decode(eng, prob, nexp, w, SRC_EXPLICIT, 0, explicit=row)
+        assert got[0] == single[0] and got[1:] == single[1:]
+        ms, _, _ = cp.eval([int(x) for x in row[:prob.J]], [int(x) for x in row[prob.J:]])
+        assert got[2] == ms
+    assert batch[0][2] == sol.makespan
