@@ -332,7 +332,7 @@ def build_problem(table, workload, opts: SolveOptions | None = None, running_con
     for n, sh in zip(nodes, node_shape):
         if shape_rep[sh] is None:
             shape_rep[sh] = n
-    rows = []
+    rows, row_min = [], []         # row_min[j]: the job's least runtime (None: take it from the row)
     get = table.entries.get
     node_id_list = [n.id for n in nodes]
     for job in pool:
@@ -346,11 +346,12 @@ def build_problem(table, workload, opts: SolveOptions | None = None, running_con
             # same IEEE product; per-option tuples are built only for the prune's survivors.
             cfgs, keys, g_all, _ = _one_node_options(job, workload)
             if len(keys) < _ARRAY_ROW_MIN:      # short rows: plain tuples beat numpy call overhead
-                lats = list(map(get, keys, repeat(INFEASIBLE)))
-                row = [(c, lat, [rem * lat]) for c, lat in zip(cfgs, lats) if math.isfinite(lat)]
-                if not row:
+                fin = [(c, lat) for c, lat in zip(cfgs, map(get, keys, repeat(INFEASIBLE))) if math.isfinite(lat)]
+                if not fin:
                     raise err.NoFeasibleConfig(job.id)
-                rows.append(row)
+                ts = [rem * lat for _, lat in fin]
+                rows.append([(c, lat, [t]) for (c, lat), t in zip(fin, ts)])
+                row_min.append(min(ts))
                 continue
             lat_all = np.fromiter(map(get, keys, repeat(INFEASIBLE)), dtype=np.float64, count=len(keys))
             sel = np.flatnonzero(np.isfinite(lat_all))
@@ -358,6 +359,7 @@ def build_problem(table, workload, opts: SolveOptions | None = None, running_con
                 raise err.NoFeasibleConfig(job.id)
             lat = lat_all[sel]
             rows.append(_OneNodeRow(cfgs, sel, lat, rem * lat, g_all[sel]))
+            row_min.append(rows[-1].t.min().item())
             continue
         if techniques is workload.techniques:
             # several nodes or a running config: runtime = plain estimate on every eligible node
@@ -376,6 +378,7 @@ def build_problem(table, workload, opts: SolveOptions | None = None, running_con
             if not row or all(math.isinf(t) for _, _, pn in row for t in pn):
                 raise err.NoFeasibleConfig(job.id)
             rows.append(row)
+            row_min.append(None)
             continue
         entries = feasible_entries(table, job, workload)
         if not entries:
@@ -399,12 +402,12 @@ def build_problem(table, workload, opts: SolveOptions | None = None, running_con
         if all(math.isinf(t) for _, _, pn in row for t in pn):
             raise err.NoFeasibleConfig(job.id)
         rows.append(row)
+        row_min.append(None)
 
     J = len(pool)
     if J == 0:
         raise err.InvariantViolation("jobs", "nothing to plan")
-    min_rt = [row.t.min().item() if type(row) is _OneNodeRow else min(min(pn) for _, _, pn in row)
-              for row in rows]
+    min_rt = [m if m is not None else min(min(pn) for _, _, pn in row) for m, row in zip(row_min, rows)]
     if opts.delta is not None:
         delta = float(opts.delta)
         if not delta > 0:
