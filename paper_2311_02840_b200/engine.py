@@ -154,6 +154,8 @@ class SearchResult:
     stats: dict | None = None  # bound-and-prune / local-search counters (this rank)
     idx_bits: int = 0          # bits of the packed key holding the candidate id
     state: tuple | None = None  # local search: the winning walker's final (options, order)
+    replay: tuple | None = None  # the winner's schedule (option, node, start, makespan), queued
+                                 # behind the search when search(replay=True)
 
 
 class Engine:
@@ -323,11 +325,15 @@ class Engine:
                     what="sat_search_sampled")
         self.launches += 1 if nprob.grid else 2
 
-    def schedule(self, nprob: NativeProblem, source: int, seed: int = 0, ids=None, explicit=None):
-        """Per-candidate (option, node, start) [n, J] and makespan [n], as numpy arrays."""
+    def schedule(self, nprob: NativeProblem, source: int, seed: int = 0, ids=None, explicit=None, ids_dev=None):
+        """Per-candidate (option, node, start) [n, J] and makespan [n], as numpy arrays.
+        ``ids_dev``: candidate ids already on the device (int64 tensor, e.g. the masked winner key)."""
         torch = self.torch
         J = nprob.struct.J
-        if source == SRC_EXPLICIT:
+        if ids_dev is not None:
+            ids_t, ex = ids_dev, None
+            n = ids_t.numel()
+        elif source == SRC_EXPLICIT:
             arr = np.ascontiguousarray(explicit, dtype=np.int64).reshape(-1, 2 * J)
             for row in arr:
                 if (row[:J] < 0).any() or (row[:J] >= nprob.radix).any() or sorted(row[J:]) != list(range(J)):
@@ -390,8 +396,12 @@ class Engine:
         return mode, int(opts.budget)
 
     def search(self, prob: SearchProblem, opts: SolveOptions, group=None, source: int | None = None,
-               seed: int | None = None, lo: int | None = None, hi: int | None = None) -> SearchResult:
-        """Run one solve's search on this rank's shard and combine across ranks (NCCL MIN)."""
+               seed: int | None = None, lo: int | None = None, hi: int | None = None,
+               replay: bool = False) -> SearchResult:
+        """Run one solve's search on this rank's shard and combine across ranks (NCCL MIN).
+        replay=True (grid time, full-scan / index / sampled searches): the winner's schedule is
+        launched on the stream right behind the search, reading its id from the combined
+        device key, so the host reads the key and the plan after one wait."""
         torch = self.torch
         err = E.errors_for(prob.jobs[0]) if prob.jobs else E
         t0 = time.perf_counter()
@@ -483,7 +493,17 @@ class Engine:
             self.search_sampled(nprob, src, seed_used, base_lo + a, base_lo + b, best)
             kernel, evaluated = "sampled", base_hi - base_lo
         ev1.record()
-        key = _combine(best, nprob.grid, group, world)
+        key_dev = _combine_dev(best, nprob.grid, group, world)
+        replay_out = None
+        if replay and nprob.grid and bnb_ws is None and mode in ("exhaustive", "sampled"):
+            kk = key_dev[:1]
+            idx = kk & ((1 << idx_bits) - 1)
+            bad = kk == INT64_MAX
+            if mode == "exhaustive":
+                bad = bad | (idx >= n_idx)
+            ids_dev = torch.where(bad, torch.zeros_like(idx), idx)     # an id the decode can take
+            replay_out = self.schedule(nprob, src, seed_used, ids_dev=ids_dev)
+        key = key_dev.cpu().tolist()
         ev1.synchronize()
         dev_s = ev0.elapsed_time(ev1) / 1e3
         if bnb_ws is not None:
@@ -506,7 +526,7 @@ class Engine:
                             kernel=kernel, exhaustive=mode == "exhaustive",
                             launches=self.launches - launches0, job_steps=job_steps,
                             device_seconds=dev_s, wall_seconds=time.perf_counter() - t0,
-                            stats=stats, idx_bits=idx_bits, state=ls_state)
+                            stats=stats, idx_bits=idx_bits, state=ls_state, replay=replay_out)
 
     def _walker_state(self, ls_states, index: int, J: int, group, world: int):
         """The winning walker's final (options, order), recorded by its search launch (on the
@@ -546,6 +566,11 @@ def _shard(n: int, rank: int, world: int) -> tuple:
 
 def _combine(best, grid: bool, group, world: int):
     """All-reduce MIN of the packed key (grid) or of (makespan bits, then index) (float)."""
+    return _combine_dev(best, grid, group, world).cpu().tolist()
+
+
+def _combine_dev(best, grid: bool, group, world: int):
+    """`_combine` left on the device (the reduced key tensor)."""
     import torch
 
     key = best.clone()
@@ -562,4 +587,4 @@ def _combine(best, grid: bool, group, world: int):
             idx = torch.where(key[:1] == ms, key[1:], torch.full_like(key[1:], INT64_MAX))
             dist.all_reduce(idx, op=dist.ReduceOp.MIN, group=group)
             key = torch.cat([ms, idx])
-    return key.cpu().tolist()
+    return key

@@ -147,7 +147,7 @@ def solve_problem(prob: SearchProblem, workload, opts: SolveOptions, running_con
     err = E.errors_for(workload.jobs[0] if workload.jobs else workload)
     eng = get_engine(device)
     try:
-        res = eng.search(prob, opts, group=group)
+        res = eng.search(prob, opts, group=group, replay=True)
         nprob = NativeProblem(prob, res.idx_bits)
         if res.kernel == "local":
             # replay the winning walker to get its final candidate, then schedule it explicitly
@@ -173,8 +173,11 @@ def solve_problem(prob: SearchProblem, workload, opts: SolveOptions, running_con
             plan, options, ms, runtimes = cands[0]
             cands = cands[1:]
         else:
-            src = SRC_INDEX if res.exhaustive else res.source
-            plan, options, ms, runtimes = _decode(eng, prob, nprob, workload, src, res.seed, ident=res.index)
+            if res.replay is not None:          # replayed on the device behind the search
+                plan, options, ms, runtimes = _plan_of(prob, workload, res.replay, 0)
+            else:
+                src = SRC_INDEX if res.exhaustive else res.source
+                plan, options, ms, runtimes = _decode(eng, prob, nprob, workload, src, res.seed, ident=res.index)
             cands = _decode(eng, prob, nexp, workload, SRC_EXPLICIT, 0,
                             explicit=np.stack([b[0] for b in baselines])) if baselines else []
         for cand, (_, b_order, name) in zip(cands, baselines):

@@ -251,3 +251,26 @@ def test_batched_replay_equals_single_replays(cfg):
         ms, _, _ = cp.eval([int(x) for x in row[:prob.J]], [int(x) for x in row[prob.J:]])
         assert got[2] == ms
     assert batch[0][2] == sol.makespan
+
+
+@pytest.mark.parametrize("name,opts", [("cfg1", SolveOptions(kernel="tree")),
+                                       ("small5_1x4", SolveOptions(kernel="index")),
+                                       ("cfg1", SolveOptions(search="sampled", budget=1 << 16, seed=3))])
+def test_device_replay_equals_host_decode(name, opts):
+    """search(replay=True) schedules the winner from the device-side key; the result equals the
+    replay of the host-read index (the path it replaces) and the solve's plan."""
+    from paper_2311_02840_b200.engine import SRC_INDEX, NativeProblem
+    from paper_2311_02840_b200.problem import build_problem
+
+    w, t = setup(name)
+    prob = build_problem(t, w, opts)
+    eng = PL.get_engine()
+    res = eng.search(prob, opts, replay=True)
+    assert res.replay is not None
+    src = SRC_INDEX if res.exhaustive else res.source
+    host = eng.schedule(NativeProblem(prob, res.idx_bits), src, res.seed, ids=[res.index])
+    for a, b in zip(res.replay, host):
+        assert a.dtype == b.dtype and np.array_equal(a, b)
+    assert float(res.replay[3][0]) == res.makespan
+    sol = PL.solve(t, w, None, opts)
+    assert sol.makespan == res.makespan and sol.options == [int(x) for x in host[0][0]]
