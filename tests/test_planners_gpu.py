@@ -274,3 +274,33 @@ def test_device_replay_equals_host_decode(name, opts):
     assert float(res.replay[3][0]) == res.makespan
     sol = PL.solve(t, w, None, opts)
     assert sol.makespan == res.makespan and sol.options == [int(x) for x in host[0][0]]
+
+
+@pytest.mark.parametrize("kernel", ["auto", "index"])
+def test_random_workloads_plan_equals_oracle_optimum(kernel):
+    """plan_saturn on random 4-6-job workloads (1-2 nodes): the winning index, makespan and
+    every job's (option, node, start) equal the C oracle's exhaustive search and replay.
+    kernel=auto takes bound-and-prune on one node (host-index replay) and the index kernel on
+    two; kernel=index takes the full scan with the device-queued replay."""
+    from paper_2311_02840_b200.workloads import random_workload
+
+    checked = 0
+    for seed in range(60):
+        w = random_workload(1000 + seed, n_jobs=4 + seed % 3)
+        t = build_profile_table(w, SyntheticExecutor(w.cluster))
+        op = O.build(t.entries, w)
+        if math.prod(op.radix) * math.factorial(op.J) > 3e7:      # keep the CPU search short
+            continue
+        checked += 1
+        cp = C.CProblem(op)
+        ms, ident = cp.search()
+        sol = PL.solve(t, w, None, SolveOptions(search="exhaustive", kernel=kernel))
+        assert sol.status == "Optimal" and sol.makespan == ms and sol.search.index == ident
+        opts, order = cp.decode(ident)
+        ms2, starts, nodes = cp.eval(opts, order)
+        assert ms2 == ms and sol.options == opts
+        for j, jid in enumerate(op.job_ids):
+            e = sol.plan.entries[jid]
+            assert e.start_time == starts[j] * sol.problem.delta
+            assert e.node == sol.problem.node_ids[nodes[j]]
+    assert checked >= 30
