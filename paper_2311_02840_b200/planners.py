@@ -148,7 +148,7 @@ def solve_problem(prob: SearchProblem, workload, opts: SolveOptions, running_con
     eng = get_engine(device)
     try:
         res = eng.search(prob, opts, group=group, replay=True)
-        nprob = NativeProblem(prob, res.idx_bits)
+        nprob = NativeProblem(prob, res.idx_bits) if res.replay is None else None
         if res.kernel == "local":
             # replay the winning walker to get its final candidate, then schedule it explicitly
             if res.state is not None:          # recorded by the search launch
