@@ -203,7 +203,12 @@ def solve_problem(prob: SearchProblem, workload, opts: SolveOptions, running_con
     if validate and running_context is None:
         D.check_plan(plan, workload, runtimes)
     status = "Optimal" if res.exhaustive else ("Local" if res.kernel == "local" else "Sampled")
-    lb = makespan if res.exhaustive else prob.lower_bound()
+    if res.exhaustive:
+        lb = makespan
+    elif res.kernel == "local" and prob.time_mode == TIME_GRID:
+        lb = res.stats["lower_bound"]   # prob.lower_bound(), computed once by the search (its stop target)
+    else:
+        lb = prob.lower_bound()
     if not res.exhaustive and makespan <= lb:
         status = "Optimal"          # a heuristic plan meeting the lower bound is optimal (bound proof)
     return Solution(plan=plan, status=status, makespan=makespan, lower_bound=lb,
