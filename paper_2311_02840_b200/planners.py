@@ -273,17 +273,19 @@ def plan_random_best(table, jobs, cluster=None, seed0: int = 0, n_seeds: int = 1
 # Optimus -- host allocator, device schedule
 # --------------------------------------------------------------------------
 
-def _best_runtime_all(prob: SearchProblem) -> list:
+def _best_runtime_all(prob: SearchProblem, jobs=None) -> list:
     """Per job: g -> (runtime seconds, option) minimising runtime over techniques at that g
     (earliest option on ties); runtime on the job's fastest eligible node.  One array pass
-    over the problem's [J, Cmax, N] tables, then a short loop per job over its options."""
+    over the problem's [J, Cmax, N] tables (or the rows of ``jobs``), then a short loop per job
+    over its options."""
+    sel = slice(None) if jobs is None else list(jobs)
     N = prob.N
-    elig = ((prob.node_mask[:, :, None] >> np.arange(N, dtype=np.uint32)) & 1).astype(bool)
-    rt_all = np.where(elig, prob.runtime, np.inf).min(axis=2).tolist()
+    elig = ((prob.node_mask[sel, :, None] >> np.arange(N, dtype=np.uint32)) & 1).astype(bool)
+    rt_all = np.where(elig, prob.runtime[sel], np.inf).min(axis=2).tolist()
     any_all = elig.any(axis=2).tolist()
-    gpus_all = prob.gpus.tolist()
+    gpus_all = prob.gpus[sel].tolist()
     out_all = []
-    for j, R in enumerate(prob.radix.tolist()):
+    for j, R in enumerate(prob.radix[sel].tolist()):
         if not all(any_all[j][:R]):
             raise ValueError("min() arg is an empty sequence")  # an option no node can run
         out: dict = {}
@@ -296,7 +298,7 @@ def _best_runtime_all(prob: SearchProblem) -> list:
 
 def _best_runtime_by_g(prob: SearchProblem, j: int) -> dict:
     """`_best_runtime_all` for one job."""
-    return _best_runtime_all(prob)[j]
+    return _best_runtime_all(prob, [j])[0]
 
 
 def _problem_gain(prob: SearchProblem, j: int, g: int, best=None) -> float:
