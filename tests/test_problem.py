@@ -279,3 +279,32 @@ def test_resolve_random_contexts_match_oracle():
                     build_problem(t, w, SolveOptions(time_mode=mode), running_context=ctx)
                 continue
             compare(build_problem(t, w, SolveOptions(time_mode=mode), running_context=ctx), oprob)
+
+
+def test_best_runtime_by_g_equals_loop_restatement():
+    """The incumbents' per-g best runtime (one array pass) equals its per-option loop: least
+    runtime over eligible nodes, then least over techniques at each g, earliest option on ties."""
+    from paper_2311_02840_b200 import planners as PL
+    from paper_2311_02840_b200.workloads import config_workload, random_workload
+
+    def loop(prob, j):
+        out = {}
+        for o in range(int(prob.radix[j])):
+            g = int(prob.gpus[j, o])
+            rt = min(prob.runtime[j, o, n] for n in range(prob.N) if (int(prob.node_mask[j, o]) >> n) & 1)
+            if g not in out or rt < out[g][0]:
+                out[g] = (rt, o)
+        return out
+
+    probs = [build_problem(t, w) for w, t, _ in (config_workload(k) for k in (1, 4))]
+    for seed in range(40):
+        w = random_workload(seed)
+        t = build_profile_table(w, SyntheticExecutor(w.cluster))
+        probs.append(build_problem(t, w, SolveOptions(time_mode="float" if seed % 2 else "grid")))
+    for prob in probs:
+        got = PL._best_runtime_all(prob)
+        for j in range(prob.J):
+            want = loop(prob, j)
+            assert got[j].keys() == want.keys() == PL._best_runtime_by_g(prob, j).keys()
+            for g in want:
+                assert got[j][g][1] == want[g][1] and float(got[j][g][0]).hex() == float(want[g][0]).hex()
