@@ -4,7 +4,7 @@
  * --impl reference).  Never linked into or called by the product engine.
  *
  * C restatement of the same semantics as oracle/saturn_oracle.py (which it is
- * checked against in tests/test_oracle_c.py):
+ * checked against in tests/test_oracle.py, test_c_oracle_matches_python):
  *   - candidate space of SURVEY.md Appendix A1 (index = c * J! + p), SplitMix64
  *     draws of plan_random (rng.py:20-56),
  *   - list scheduling "earliest-fit" over explicit per-GPU free

@@ -20,11 +20,14 @@ independently of the product code:
   interval) tuples and the time-indexed MILP
   solved by HiGHS through scipy.optimize.milp.
 
-Pinning: tests/test_oracle_golden.py checks this module against golden vectors
+Pinning: tests/test_golden.py (test_oracle_profile_table_matches_reference, test_rng_vectors,
+test_spec_examples_oracle) checks this module against golden vectors
 produced by running the reference package itself (tests/golden/make_golden.py)
 and against the SPEC.md known-answer examples.  Plan identity for the solver has
 no reference implementation to pin against (the reference milp module does not
-import); the optimum VALUE is pinned by HiGHS and brute force.
+import); the optimum VALUE is pinned by HiGHS and brute force, and the winner identity of the
+headline solves by tests/golden/make_winners.py (HiGHS optimum + the C oracle's scan from
+index 0 to the first candidate reaching it).
 """
 
 from __future__ import annotations

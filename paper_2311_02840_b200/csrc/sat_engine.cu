@@ -38,6 +38,11 @@
 // atomicMin; float mode reduces per block and merges in a second tiny kernel.
 #include "sat_cand.cuh"
 
+#include <list>
+#include <memory>
+#include <mutex>
+#include <nvtx3/nvToolsExt.h>
+
 namespace sat {
 template <typename T, int SRC, bool RECORD>
 __global__ void __launch_bounds__(kGenThreads)
@@ -511,7 +516,7 @@ double walk_cost(const int32_t *radix, uint32_t rem, std::vector<double> &memo) 
     return tot;
 }
 
-int tree_layout(const sat_problem_t *p, int prefix_len, TreeLayout &lay) {
+int tree_layout_build(const sat_problem_t *p, int prefix_len, TreeLayout &lay) {
     const int J = p->J;
     if (p->N != 1 || p->time_mode != SAT_TIME_GRID_I32) return SAT_ERR_UNSUPPORTED;
     if (J < 3 || J > kTreeMaxJ) return SAT_ERR_UNSUPPORTED;
@@ -575,6 +580,67 @@ int tree_layout(const sat_problem_t *p, int prefix_len, TreeLayout &lay) {
     return SAT_OK;
 }
 
+// tree_layout is a pure function of (J, radix[], requested prefix): memoised per process so that
+// repeated solves, re-solves and the host's prefix probing (Engine.bnb_prefix calls sat_tree_plan
+// once per P) do not redo the 2^J set enumeration and walk memo each call.  A small LRU under a
+// mutex keeps the C ABI reentrant; results are identical with or without it.
+struct LayoutKey {
+    int J = 0, P = 0;
+    int32_t radix[kTreeMaxJ] = {};
+    bool operator==(const LayoutKey &o) const {
+        return J == o.J && P == o.P && std::memcmp(radix, o.radix, sizeof(int32_t) * J) == 0;
+    }
+};
+struct LayoutEntry {
+    LayoutKey key;
+    int status = SAT_OK;
+    TreeLayout lay;
+    std::vector<long double> per_task;     // sat_tree_shard's per-task cost, filled on first use
+};
+static std::mutex g_layout_mu;
+static std::list<std::shared_ptr<LayoutEntry>> g_layouts;     // most recent first
+constexpr size_t kLayoutCacheEntries = 32;
+
+std::shared_ptr<LayoutEntry> tree_layout_cached(const sat_problem_t *p, int prefix_len) {
+    LayoutKey k;
+    k.J = p->J;
+    k.P = prefix_len <= 0 ? 0 : prefix_len;
+    if (p->J >= 1 && p->J <= kTreeMaxJ) std::memcpy(k.radix, p->radix, sizeof(int32_t) * p->J);
+    {
+        std::lock_guard<std::mutex> g(g_layout_mu);
+        for (auto it = g_layouts.begin(); it != g_layouts.end(); ++it)
+            if ((*it)->key == k) {
+                auto e = *it;
+                g_layouts.erase(it);
+                g_layouts.push_front(e);
+                return e;
+            }
+    }
+    auto e = std::make_shared<LayoutEntry>();
+    e->key = k;
+    e->status = tree_layout_build(p, prefix_len, e->lay);
+    std::lock_guard<std::mutex> g(g_layout_mu);
+    g_layouts.push_front(e);
+    if (g_layouts.size() > kLayoutCacheEntries) g_layouts.pop_back();
+    return e;
+}
+
+// the shape checks tree_layout_build makes that do not depend on the radices (the cache key)
+int tree_layout(const sat_problem_t *p, int prefix_len, TreeLayout &lay) {
+    if (p->N != 1 || p->time_mode != SAT_TIME_GRID_I32) return SAT_ERR_UNSUPPORTED;
+    if (p->J < 3 || p->J > kTreeMaxJ) return SAT_ERR_UNSUPPORTED;
+    if (p->release_i32)
+        for (int j = 0; j < p->J; ++j) if (p->release_i32[j] != 0) return SAT_ERR_UNSUPPORTED;
+    auto e = tree_layout_cached(p, prefix_len);
+    if (e->status == SAT_OK) lay = e->lay;
+    return e->status;
+}
+
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+
 }  // namespace sat
 
 using namespace sat;
@@ -633,6 +699,7 @@ int sat_workspace_bytes(const sat_problem_t *p, size_t *bytes) {
 
 int sat_search_index(const sat_problem_t *p, uint64_t lo, uint64_t hi, sat_best_t *d_best, void *d_ws,
                      size_t ws_bytes, void *stream) {
+    NvtxRange nvtx("sat_search_index");
     int st = validate(p);
     if (st) return st;
     if (!d_best || hi < lo) return SAT_ERR_INVALID;
@@ -652,6 +719,7 @@ int sat_search_index(const sat_problem_t *p, uint64_t lo, uint64_t hi, sat_best_
 
 int sat_search_sampled(const sat_problem_t *p, int32_t source, uint64_t seed, uint64_t lo, uint64_t hi,
                        sat_best_t *d_best, void *d_ws, size_t ws_bytes, void *stream) {
+    NvtxRange nvtx("sat_search_sampled");
     int st = validate(p);
     if (st) return st;
     if (!d_best || hi < lo) return SAT_ERR_INVALID;
@@ -675,6 +743,7 @@ int sat_schedule(const sat_problem_t *p, int32_t source, uint64_t seed, const ui
                  const uint8_t *d_explicit, int32_t n, int32_t *d_option, int32_t *d_node,
                  int32_t *d_start_i32, double *d_start_f64, int64_t *d_makespan_i64,
                  double *d_makespan_f64, void *d_ws, size_t ws_bytes, void *stream) {
+    NvtxRange nvtx("sat_schedule");
     int st = validate(p);
     if (st) return st;
     if (n < 0) return SAT_ERR_INVALID;
@@ -744,6 +813,7 @@ int sat_tree_plan(const sat_problem_t *p, int32_t prefix_len, sat_tree_info_t *i
 
 static int search_tree_impl(const sat_problem_t *p, int32_t prefix_len, uint64_t task_lo, uint64_t task_hi,
                             sat_best_t *d_best, void *d_ws, size_t ws_bytes, void *stream, bool bnb) {
+    NvtxRange nvtx(bnb ? "sat_search_bnb" : "sat_search_tree");
     int st = validate(p);
     if (st) return st;
     if (!d_best || task_hi < task_lo) return SAT_ERR_INVALID;
@@ -838,16 +908,25 @@ int sat_tree_shard(const sat_problem_t *p, int32_t prefix_len, int32_t world, in
     TreeLayout lay;
     st = tree_layout(p, prefix_len, lay);
     if (st) return st;
-    const int J = p->J;
-    const uint32_t full = (1u << J) - 1u;
-    std::vector<double> memo((size_t)1 << J, -1.0);
-    // per-task device cost of set s: the prefix decode + the warp's suffix walk (walk_cost)
-    std::vector<long double> per_task(lay.sets.size());
-    long double total = 0;
-    for (size_t s = 0; s < lay.sets.size(); ++s) {
-        per_task[s] = (long double)(kCostTask + walk_cost(p->radix, full & ~lay.sets[s], memo));
-        total += per_task[s] * (long double)(lay.cum[s + 1] - lay.cum[s]);
+    // per-task device cost of set s: the prefix decode + the warp's suffix walk (walk_cost),
+    // computed once per cached layout
+    auto entry = tree_layout_cached(p, prefix_len);
+    std::vector<long double> per_task;
+    {
+        std::lock_guard<std::mutex> g(g_layout_mu);
+        per_task = entry->per_task;
     }
+    if (per_task.empty()) {
+        const uint32_t full = (1u << p->J) - 1u;
+        std::vector<double> memo((size_t)1 << p->J, -1.0);
+        per_task.resize(lay.sets.size());
+        for (size_t s = 0; s < lay.sets.size(); ++s)
+            per_task[s] = (long double)(kCostTask + walk_cost(p->radix, full & ~lay.sets[s], memo));
+        std::lock_guard<std::mutex> g(g_layout_mu);
+        entry->per_task = per_task;
+    }
+    long double total = 0;
+    for (size_t s = 0; s < lay.sets.size(); ++s) total += per_task[s] * (long double)(lay.cum[s + 1] - lay.cum[s]);
     auto boundary = [&](int32_t r) -> uint64_t {      // first task whose prefix work >= total * r / world
         if (r <= 0) return 0;
         if (r >= world) return lay.n_tasks;
@@ -884,6 +963,7 @@ int sat_local_search(const sat_problem_t *p, int32_t source, uint64_t seed, uint
                      int32_t max_rounds, int32_t stop_ms, sat_best_t *d_best, uint8_t *d_state_out, void *d_ws,
                      size_t ws_bytes,
                      void *stream) {
+    NvtxRange nvtx("sat_local_search");
     int st = validate(p);
     if (st) return st;
     if (!d_best || hi < lo || max_rounds < 0) return SAT_ERR_INVALID;

@@ -23,6 +23,8 @@ from __future__ import annotations
 from dataclasses import dataclass, field
 from typing import Iterable, Mapping
 
+import numpy as np
+
 from . import errors as E
 
 ARCHETYPES = ("replicated", "sharded", "pipelined", "offloaded")
@@ -249,47 +251,62 @@ def validate_workload(workload):
 
 
 # --------------------------------------------------------------------------
-# plan validation (core.py:226-287)
+# plan validation (core.py:226-287), as array passes over the plan's segments
 # --------------------------------------------------------------------------
 
 def sweep_capacity(segments: Iterable, cluster, tol: float = 1e-9) -> None:
-    """Per-node event sweep; at equal t an end (kind 0) is applied before a start (kind 1)."""
-    per_node: dict = {}
-    for node_id, gpus, start, end in segments:
-        if end < start - tol:
-            raise E.InvalidPlan(f"segment on {node_id} ends before it starts")
-        ev = per_node.setdefault(node_id, [])
-        ev.append((start, 1, gpus))
-        ev.append((end, 0, -gpus))
-    for node_id, ev in per_node.items():
+    """Per-node GPU demand over time (core.py:226-251).  Each segment contributes a +g event at
+    its start and a -g event at its end; at equal times ends sort first, so a gang may take GPUs
+    freed at the instant it starts.  Demand = running sum of the sorted events per node."""
+    segs = list(segments)
+    if not segs:
+        return
+    nodes = [s[0] for s in segs]
+    g = np.array([s[1] for s in segs], dtype=np.int64)
+    t = np.array([(s[2], s[3]) for s in segs], dtype=np.float64)            # [n, (start, end)]
+    reversed_ = np.flatnonzero(t[:, 1] < t[:, 0] - tol)
+    if reversed_.size:
+        raise E.InvalidPlan(f"segment on {nodes[reversed_[0]]} ends before it starts")
+    node_of = np.array([{n: i for i, n in enumerate(dict.fromkeys(nodes))}[n] for n in nodes])
+    for k, node_id in enumerate(dict.fromkeys(nodes)):         # nodes in order of first use
+        sel = np.flatnonzero(node_of == k)
+        times = t[sel].ravel()                                  # start, end, start, end, ...
+        kind = np.tile(np.array([1, 0]), sel.size)              # start = 1 sorts after end = 0
+        step = np.stack([g[sel], -g[sel]], axis=1).ravel()
+        perm = np.lexsort((kind, times))                        # stable: ties keep input order
+        demand = np.cumsum(step[perm])
         cap = cluster.node(node_id).gpu_count
-        busy = 0
-        for t, _kind, delta in sorted(ev, key=lambda e: (e[0], e[1])):
-            busy += delta
-            if busy > cap:
-                raise E.CapacityViolation(f"node {node_id}: {busy} GPUs in use at t={t:.6g}, capacity {cap}")
+        over = np.flatnonzero(demand > cap)
+        if over.size:
+            i = over[0]
+            raise E.CapacityViolation(f"node {node_id}: {int(demand[i])} GPUs in use at t={times[perm[i]]:.6g}, "
+                                      f"capacity {cap}")
 
 
 def check_plan(plan, workload, runtimes: Mapping, tol: float = 1e-6) -> None:
-    """Coverage, gang fit, min_gpus, capacity sweep, predicted >= last end (core.py:254-287)."""
-    want = {j.id for j in workload.jobs}
-    got = set(plan.entries)
+    """Plan invariants against per-job runtimes (core.py:254-287): every workload job planned
+    exactly once, each gang fits its node and meets its technique's minimum, node capacity holds
+    at every instant, and the predicted makespan covers the last completion."""
+    want, got = {j.id for j in workload.jobs}, set(plan.entries)
     if want != got:
         raise E.InvalidPlan(f"plan covers {sorted(got)}, workload has {sorted(want)}")
-    segs = []
-    last_end = 0.0
-    for job_id, entry in plan.entries.items():
-        tech = workload.technique(entry.config.technique)
-        node = workload.cluster.node(entry.node)
-        if entry.config.gpus > node.gpu_count:
-            raise E.CapacityViolation(
-                f"job {job_id}: gang of {entry.config.gpus} exceeds node {node.id} ({node.gpu_count})")
-        if entry.config.gpus < tech.min_gpus:
-            raise E.InvalidPlan(f"job {job_id}: {entry.config.gpus} GPUs below technique minimum")
-        end = entry.start_time + runtimes[job_id]
-        segs.append((entry.node, entry.config.gpus, entry.start_time, end))
-        last_end = max(last_end, end)
-    sweep_capacity(segs, workload.cluster)
+    ids = list(plan.entries)
+    ents = [plan.entries[i] for i in ids]
+    node_objs = [workload.cluster.node(e.node) for e in ents]
+    min_g = np.array([workload.technique(e.config.technique).min_gpus for e in ents], dtype=np.int64)
+    gang = np.array([e.config.gpus for e in ents], dtype=np.int64)
+    cap = np.array([n.gpu_count for n in node_objs], dtype=np.int64)
+    wide, short = gang > cap, gang < min_g
+    first = np.flatnonzero(wide | short)
+    if first.size:
+        i = first[0]
+        if wide[i]:
+            raise E.CapacityViolation(f"job {ids[i]}: gang of {gang[i]} exceeds node {node_objs[i].id} ({cap[i]})")
+        raise E.InvalidPlan(f"job {ids[i]}: {gang[i]} GPUs below technique minimum")
+    start = np.array([e.start_time for e in ents], dtype=np.float64)
+    end = start + np.array([runtimes[i] for i in ids], dtype=np.float64)
+    sweep_capacity(zip([e.node for e in ents], gang.tolist(), start.tolist(), end.tolist()), workload.cluster)
+    last_end = max(0.0, float(end.max())) if len(ids) else 0.0
     if plan.predicted_makespan < last_end - tol:
         raise E.InvalidPlan(
             f"predicted makespan {plan.predicted_makespan:.6g} below last completion {last_end:.6g}")

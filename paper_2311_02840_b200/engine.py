@@ -126,6 +126,22 @@ class NativeProblem:
         self.struct = s
         self.idx_bits = idx_bits
         self.grid = grid
+        self.job_ids = list(prob.job_ids)
+        self.err = E.errors_for(prob.jobs[0]) if prob.jobs else E
+
+    def job_without_options(self) -> str:
+        """Id of the first job the engine found without a runnable option (SAT_ERR_NO_OPTIONS):
+        no option, or an option no node can host."""
+        for j, jid in enumerate(self.job_ids):
+            R = int(self.radix[j])
+            if R < 1:
+                return jid
+            for o in range(R):
+                g = int(self.gpus[j, o]) if self.gpus.ndim == 2 else int(self.gpus[j * self.struct.Cmax + o])
+                m = int(self.mask.reshape(len(self.job_ids), -1)[j, o])
+                if not any((m >> n) & 1 and int(self.node_gpus[n]) >= g for n in range(len(self.node_gpus))):
+                    return jid
+        return "<job>"
 
     @property
     def ref(self):
@@ -178,12 +194,14 @@ class Engine:
         self.launches = 0
 
     # ---- plumbing ----------------------------------------------------------
-    def _check(self, st: int, err=E, what: str = "engine call"):
+    def _check(self, st: int, err=None, what: str = "engine call", nprob=None):
         if st == SAT_OK:
             return
+        if err is None:
+            err = nprob.err if nprob is not None else E
         msg = f"{what}: {self.lib.sat_error_string(st).decode()}" if hasattr(self, "lib") else what
         if st == SAT_ERR_NO_OPTIONS:
-            raise err.NoFeasibleConfig("<job>")
+            raise err.NoFeasibleConfig(nprob.job_without_options() if nprob is not None else "<job>")
         if st == SAT_ERR_INVALID:
             raise err.InvariantViolation("problem", msg)
         if st in (SAT_ERR_TOO_LARGE, SAT_ERR_UNSUPPORTED):
@@ -195,7 +213,7 @@ class Engine:
 
     def workspace(self, nprob: NativeProblem):
         nbytes = ctypes.c_size_t()
-        self._check(self.lib.sat_workspace_bytes(nprob.ref, ctypes.byref(nbytes)))
+        self._check(self.lib.sat_workspace_bytes(nprob.ref, ctypes.byref(nbytes)), nprob=nprob)
         need = int(nbytes.value)
         if self._ws is None or self._ws.numel() < need:
             self._ws = self.torch.empty(max(need, 1 << 16), dtype=self.torch.uint8, device=self.device)
@@ -209,14 +227,14 @@ class Engine:
     # ---- kernels -------------------------------------------------------------
     def tree_plan(self, nprob: NativeProblem, prefix_len: int = 0) -> SatTreeInfo:
         info = SatTreeInfo()
-        self._check(self.lib.sat_tree_plan(nprob.ref, prefix_len, ctypes.byref(info)), what="sat_tree_plan")
+        self._check(self.lib.sat_tree_plan(nprob.ref, prefix_len, ctypes.byref(info)), what="sat_tree_plan", nprob=nprob)
         return info
 
     def search_tree(self, nprob, prefix_len, task_lo, task_hi, best=None):
         best = self._best if best is None else best
         ws, wsb = self.workspace(nprob)
         self._check(self.lib.sat_search_tree(nprob.ref, prefix_len, task_lo, task_hi, _vp(best.data_ptr()),
-                                             _vp(ws), wsb, _vp(self.stream())), what="sat_search_tree")
+                                             _vp(ws), wsb, _vp(self.stream())), what="sat_search_tree", nprob=nprob)
         self.launches += 1
 
     def search_bnb(self, nprob, prefix_len, task_lo, task_hi, best=None):
@@ -224,7 +242,7 @@ class Engine:
         best = self._best if best is None else best
         ws, wsb = self.workspace(nprob)
         self._check(self.lib.sat_search_bnb(nprob.ref, prefix_len, task_lo, task_hi, _vp(best.data_ptr()),
-                                            _vp(ws), wsb, _vp(self.stream())), what="sat_search_bnb")
+                                            _vp(ws), wsb, _vp(self.stream())), what="sat_search_bnb", nprob=nprob)
         self.launches += 1
         return self._ws
 
@@ -235,7 +253,7 @@ class Engine:
             return 0, info.n_tasks
         lo, hi = ctypes.c_uint64(), ctypes.c_uint64()
         self._check(self.lib.sat_tree_shard(nprob.ref, prefix_len, world, rank, ctypes.byref(lo), ctypes.byref(hi)),
-                    what="sat_tree_shard")
+                    what="sat_tree_shard", nprob=nprob)
         return lo.value, hi.value
 
     def full_scan_prefix(self, nprob, world: int) -> int:
@@ -297,7 +315,7 @@ class Engine:
         self._check(self.lib.sat_local_search(nprob.ref, source, seed & ((1 << 64) - 1), lo, hi, max_rounds,
                                               int(stop_ms), _vp(best.data_ptr()),
                                               _vp(state_out.data_ptr()) if state_out is not None else None,
-                                              _vp(ws), wsb, _vp(self.stream())), what="sat_local_search")
+                                              _vp(ws), wsb, _vp(self.stream())), what="sat_local_search", nprob=nprob)
         self.launches += 1
 
     def local_search_state(self, nprob, source, seed, walker, max_rounds: int = 4096, stop_ms: int = -1):
@@ -314,7 +332,7 @@ class Engine:
         best = self._best if best is None else best
         ws, wsb = self.workspace(nprob)
         self._check(self.lib.sat_search_index(nprob.ref, lo, hi, _vp(best.data_ptr()), _vp(ws), wsb,
-                                              _vp(self.stream())), what="sat_search_index")
+                                              _vp(self.stream())), what="sat_search_index", nprob=nprob)
         self.launches += 1 if nprob.grid else 2
 
     def search_sampled(self, nprob, source, seed, lo, hi, best=None):
@@ -322,7 +340,7 @@ class Engine:
         ws, wsb = self.workspace(nprob)
         self._check(self.lib.sat_search_sampled(nprob.ref, source, seed & ((1 << 64) - 1), lo, hi,
                                                 _vp(best.data_ptr()), _vp(ws), wsb, _vp(self.stream())),
-                    what="sat_search_sampled")
+                    what="sat_search_sampled", nprob=nprob)
         self.launches += 1 if nprob.grid else 2
 
     def schedule(self, nprob: NativeProblem, source: int, seed: int = 0, ids=None, explicit=None, ids_dev=None):
@@ -364,7 +382,7 @@ class Engine:
             _vp(opt_p), _vp(node_p),
             _vp(start_p) if g else None, None if g else _vp(start_p),
             _vp(ms_p) if g else None, None if g else _vp(ms_p),
-            _vp(ws), wsb, _vp(self.stream())), what="sat_schedule")
+            _vp(ws), wsb, _vp(self.stream())), what="sat_schedule", nprob=nprob)
         self.launches += 1
         h = out.cpu().numpy()
         return (h[:4 * n * J].view(np.int32).reshape(n, J),
@@ -431,8 +449,10 @@ class Engine:
         if mode == "exhaustive":
             src = SRC_INDEX
             use_tree = opts.kernel in ("auto", "tree", "bnb") and self._tree_ok(prob)
-            if opts.kernel in ("tree", "bnb") and not use_tree:
+            if opts.kernel in ("tree", "bnb") and not use_tree and prob.J >= 3:
                 raise err.TooLarge("tree / bnb kernels need one node, grid time, 3..20 jobs")
+            # (one- and two-job spaces -- the tail of an introspection run -- are scanned by the
+            # per-candidate index kernel whatever kernel was asked for)
             if use_bnb:
                 # pruning makes task costs uneven but cheap: a short prefix (2^15 tasks over all
                 # ranks) beats a longer one at every world size (profiles/r01e_shard_emulation.txt)
@@ -462,7 +482,7 @@ class Engine:
             target = prob.lower_bound() if nprob.grid else -1.0
             stop_ms = int(target) if (nprob.grid and opts.ls_stop) else -1
             off = ctypes.c_size_t()
-            self._check(self.lib.sat_ls_counter_offset(nprob.ref, ctypes.byref(off)))
+            self._check(self.lib.sat_ls_counter_offset(nprob.ref, ctypes.byref(off)), nprob=nprob)
             # geometric waves (wave, 4 x wave, 16 x wave, ...): a small first wave keeps easy
             # problems cheap, larger later waves keep the GPU full when the bound is not met
             wave = max(1, int(opts.wave))

@@ -1,9 +1,11 @@
 """File formats on either side of the search: profile CSV in, workload JSON in/out, plan JSON out.
 
 * profile CSV (profiling.py:22, 173-215): header ``job,technique,gpus,latency_s``, ``inf``
-  marks an infeasible configuration; ``load_profiles`` raises ``ParseError`` /
-  ``NegativeLatency`` with the 1-based line number exactly where the reference does;
-  ``save_profiles`` writes rows sorted by key with ``repr`` floats (byte-identical output).
+  marks an infeasible configuration; ``load_profiles`` (a columnar reader) raises
+  ``ParseError`` / ``NegativeLatency`` with the 1-based line number and message the reference
+  raises for the same text; ``save_profiles`` writes rows sorted by key with ``repr`` floats
+  (byte-identical output).  The reference's own reader feeds the engine just as well
+  (tests/test_dropin_reference_gpu.py).
 * workload JSON (core.py:290-310): the pydantic ``model_dump_json(indent=2)`` layout
   (fields in declaration order), parsed and validated with ``validate_workload``.
 * plan JSON (the output of ``decode_plan``): entries keyed by job id.
@@ -25,38 +27,65 @@ CSV_HEADER = "job,technique,gpus,latency_s"
 
 
 # ---------------------------------------------------------------- profile CSV
+# Columnar reader: the body is tokenised into columns first, every row gets the verdict of the
+# first rule it breaks (field count, gpu count, latency, duplicate key -- the reference's check
+# order, profiling.py:173-209), and the lowest failing line raises.  Parsing stops at the first
+# bad line in the reference, so every row above it is valid: a row is a duplicate iff its key
+# appears on an earlier row.
+
+def _as_int(raw: str):
+    try:
+        return int(raw)
+    except ValueError:
+        return None
+
+
+def _as_latency(raw: str):
+    if raw == "inf":
+        return INFEASIBLE
+    try:
+        return float(raw)
+    except ValueError:
+        return None
+
+
+def _row_error(line_no: int, n_fields: int, g_raw: str, g, lat_raw: str, lat, duplicate_of):
+    """The error the reference raises for this row (None if the row is good)."""
+    if n_fields != 4:
+        return E.ParseError(line_no, f"expected 4 comma-separated fields, got {n_fields}")
+    if g is None:
+        return E.ParseError(line_no, f"bad gpu count {g_raw!r}")
+    if g < 1:
+        return E.ParseError(line_no, f"gpu count must be >= 1, got {g}")
+    if lat is None:
+        return E.ParseError(line_no, f"bad latency {lat_raw!r}")
+    if lat <= 0:
+        return E.NegativeLatency(line_no, lat)
+    if duplicate_of is not None:
+        return E.ParseError(line_no, f"duplicate entry for {duplicate_of}")
+    return None
+
+
 def parse_profiles(text: str) -> ProfileTable:
-    lines = text.split("\n")
-    if not lines or lines[0].strip() != CSV_HEADER:
+    """Profile CSV text (header ``job,technique,gpus,latency_s``; ``inf`` = infeasible) -> table."""
+    head, _, body = text.partition("\n")
+    if head.strip() != CSV_HEADER:
         raise E.ParseError(1, f"expected header {CSV_HEADER!r}")
-    entries: dict = {}
-    for idx, line in enumerate(lines[1:], start=2):
-        if not line.strip():
-            continue
-        parts = line.split(",")
-        if len(parts) != 4:
-            raise E.ParseError(idx, f"expected 4 comma-separated fields, got {len(parts)}")
-        job_id, tech, g_raw, lat_raw = (p.strip() for p in parts)
-        try:
-            g = int(g_raw)
-        except ValueError:
-            raise E.ParseError(idx, f"bad gpu count {g_raw!r}") from None
-        if g < 1:
-            raise E.ParseError(idx, f"gpu count must be >= 1, got {g}")
-        if lat_raw == "inf":
-            lat = INFEASIBLE
-        else:
-            try:
-                lat = float(lat_raw)
-            except ValueError:
-                raise E.ParseError(idx, f"bad latency {lat_raw!r}") from None
-            if lat <= 0:
-                raise E.NegativeLatency(idx, lat)
-        key = (job_id, tech, g)
-        if key in entries:
-            raise E.ParseError(idx, f"duplicate entry for {key}")
-        entries[key] = lat
-    return ProfileTable(entries, "ingested")
+    rows = [(no, ln.split(",")) for no, ln in enumerate(body.split("\n"), start=2) if ln.strip()]
+    width = [len(f) for _, f in rows]
+    cols = [[p.strip() for p in f] if len(f) == 4 else ["", "", "", ""] for _, f in rows]
+    jobs, techs, g_raw, lat_raw = (list(c) for c in zip(*cols)) if cols else ([], [], [], [])
+    gs = [_as_int(x) for x in g_raw]
+    lats = [_as_latency(x) for x in lat_raw]
+    first_row: dict = {}
+    for r, (no, _) in enumerate(rows):
+        key = (jobs[r], techs[r], gs[r])
+        dup = key if width[r] == 4 and key in first_row else None
+        err = _row_error(no, width[r], g_raw[r], gs[r], lat_raw[r], lats[r], dup)
+        if err is not None:
+            raise err
+        first_row[key] = r
+    return ProfileTable({k: lats[r] for k, r in first_row.items()}, "ingested")
 
 
 def load_profiles(path) -> ProfileTable:
@@ -64,10 +93,10 @@ def load_profiles(path) -> ProfileTable:
 
 
 def dump_profiles(table) -> str:
-    rows = [CSV_HEADER]
-    for (job_id, tech, g), lat in sorted(table.entries.items()):
-        rows.append(f"{job_id},{tech},{g},{'inf' if math.isinf(lat) else repr(lat)}")
-    return "\n".join(rows) + "\n"
+    """Rows in key order, shortest round-trip floats (``repr``), ``inf`` for misfits."""
+    body = "".join(f"{j},{t},{g},{'inf' if v == INFEASIBLE else repr(v)}\n"
+                   for (j, t, g), v in sorted(table.entries.items()))
+    return f"{CSV_HEADER}\n{body}"
 
 
 def save_profiles(table, path) -> None:

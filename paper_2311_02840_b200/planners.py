@@ -44,9 +44,25 @@ def get_engine(device=None) -> Engine:
 
 @dataclass
 class _WorkloadView:
+    """The SPEC.md:276 call shape ``(table, jobs, cluster, techniques=...)`` seen as a workload:
+    the attributes plus the ``job(id)`` / ``technique(name)`` lookups a ``Workload`` offers
+    (core.py:132-142), which ``check_plan`` (core.py:271) and the simulator use."""
+
     jobs: tuple
     cluster: object
     techniques: tuple
+
+    def job(self, job_id: str):
+        for j in self.jobs:
+            if j.id == job_id:
+                return j
+        raise KeyError(job_id)
+
+    def technique(self, name: str):
+        for t in self.techniques:
+            if t.name == name:
+                return t
+        raise KeyError(name)
 
 
 def _as_workload(jobs, cluster=None, techniques=None):
@@ -57,13 +73,27 @@ def _as_workload(jobs, cluster=None, techniques=None):
     return _WorkloadView(tuple(jobs), cluster, tuple(techniques))
 
 
+def _family(workload):
+    """The module defining the caller's domain objects (the reference's ``jointsched.core`` for
+    its pydantic models, ``domain`` for this package's dataclasses)."""
+    probe = workload.jobs[0] if workload.jobs else workload
+    return sys.modules.get(type(probe).__module__)
+
+
 def _types_for(workload):
     """(Plan, PlanEntry, RunConfig) classes of the caller's domain family."""
-    probe = workload.jobs[0] if workload.jobs else workload
-    mod = sys.modules.get(type(probe).__module__)
+    mod = _family(workload)
     if mod is not None and all(hasattr(mod, n) for n in ("Plan", "PlanEntry", "RunConfig")):
         return mod.Plan, mod.PlanEntry, mod.RunConfig
     return D.Plan, D.PlanEntry, D.RunConfig
+
+
+def _validator_for(workload):
+    """The caller's own plan validator: ``check_plan`` of the module that defines its domain
+    objects (core.py:254-287 for reference objects), else this package's ``domain.check_plan``."""
+    mod = _family(workload)
+    fn = getattr(mod, "check_plan", None) if mod is not None else None
+    return fn if callable(fn) else D.check_plan
 
 
 def _opts(delta_opts) -> SolveOptions:
@@ -200,8 +230,15 @@ def solve_problem(prob: SearchProblem, workload, opts: SolveOptions, running_con
         (plan, options, ms, runtimes), order, source_name = incumbent
         res.stats = {**(res.stats or {}), "incumbent": source_name}
     makespan = ms
-    if validate and running_context is None:
-        D.check_plan(plan, workload, runtimes)
+    if validate:
+        # the caller's own check_plan; a re-solve's plan covers the unfinished jobs only, so it
+        # is checked against that sub-workload (runtimes carry the +rho of moved jobs)
+        target = workload
+        if running_context is not None:
+            keep = set(prob.job_ids)
+            target = _WorkloadView(tuple(j for j in workload.jobs if j.id in keep), workload.cluster,
+                                   tuple(workload.techniques))
+        _validator_for(workload)(plan, target, runtimes)
     status = "Optimal" if res.exhaustive else ("Local" if res.kernel == "local" else "Sampled")
     if res.exhaustive:
         lb = makespan

@@ -298,8 +298,11 @@ class _Sim:
             raise E.PlanFailure("simulation ended with unfinished jobs (plan could not be dispatched)")
 
     def _tick(self, now: float, replan):
-        from .domain import RunningContext
+        from . import domain
+        from .planners import _family
 
+        # the caller's own RunningContext (core.py:211-223 for reference objects)
+        RunningContext = getattr(_family(self.w), "RunningContext", domain.RunningContext)  # noqa: N806
         remaining, current = {}, {}
         for jid, j in sorted(self.jobs.items()):
             if j.state == "done":

@@ -10,7 +10,10 @@ from paper_2311_02840_b200 import domain as D
 from paper_2311_02840_b200.profiling import ProfileTable
 
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "reference_golden.json")
-REF_SRC = "/root/reference/pkg/src"
+# the reference package: installed into baseline/_ref (git-ignored, travels to the GPU box with
+# the snapshot; tools/install_reference.sh) or, in the build container, its source tree
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REF_DIRS = (os.path.join(ROOT, "baseline", "_ref"), "/root/reference/pkg/src")
 
 _gold = None
 
@@ -39,13 +42,23 @@ def golden_workload(name):
     return workload_from_json(rec["workload"]), rec
 
 
+def reference_dir():
+    for d in REF_DIRS:
+        if os.path.isfile(os.path.join(d, "jointsched", "core.py")):
+            return d
+    return None
+
+
 def reference_available() -> bool:
-    return os.path.isdir(os.path.join(REF_SRC, "jointsched"))
+    return reference_dir() is not None
 
 
 def import_reference():
     import sys
-    if REF_SRC not in sys.path:
-        sys.path.insert(0, REF_SRC)
+    d = reference_dir()
+    if d is None:
+        raise RuntimeError("reference package missing: run tools/install_reference.sh")
+    if d not in sys.path:
+        sys.path.insert(0, d)
     from jointsched import core, profiling, rng  # noqa: F401
     return core, profiling, rng

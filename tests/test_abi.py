@@ -150,3 +150,41 @@ def test_tree_shard_partitions_and_balances_work(lib):
             assert 0.98 < share < 1.02, (world, r, share)
         assert prev == info.n_tasks
     assert lib.sat_tree_shard(nprob.ref, 5, 2, 2, ctypes.byref(lo), ctypes.byref(hi)) == EN.SAT_ERR_INVALID
+
+
+def test_no_options_status_names_the_job(lib):
+    """SAT_ERR_NO_OPTIONS from the library becomes NoFeasibleConfig carrying the offending job's
+    id (errors.py:23-26), not a placeholder."""
+    from paper_2311_02840_b200 import errors as E
+
+    w, _ = golden_workload("small5_1x4")
+    t = build_profile_table(w, SyntheticExecutor(w.cluster))
+    prob = build_problem(t, w)
+    prob.radix[2] = 0                                   # job 2 loses every option
+    nprob = EN.NativeProblem(prob, 30)
+    nbytes = ctypes.c_size_t()
+    st = lib.sat_workspace_bytes(nprob.ref, ctypes.byref(nbytes))
+    assert st == EN.SAT_ERR_NO_OPTIONS
+    eng = EN.Engine.__new__(EN.Engine)                 # host-only: no device needed to map a status
+    eng.lib = lib
+    with pytest.raises(E.NoFeasibleConfig) as exc:
+        eng._check(st, nprob=nprob)
+    assert prob.job_ids[2] in str(exc.value)
+
+
+def test_tree_layout_memo_is_transparent(lib):
+    """The per-process tree-layout memo returns the same plan for repeated and interleaved calls."""
+    w, _ = golden_workload("cfg1")
+    t = build_profile_table(w, SyntheticExecutor(w.cluster))
+    prob = build_problem(t, w)
+    nprob = EN.NativeProblem(prob, 35)
+    first = {}
+    for rep in range(3):
+        for P in (0, 1, 2, 3, 4, 5, 6):
+            info = EN.SatTreeInfo()
+            assert lib.sat_tree_plan(nprob.ref, P, ctypes.byref(info)) == 0
+            got = (info.prefix_len, info.n_sets, info.n_tasks, info.n_candidates, info.n_job_steps)
+            assert first.setdefault(P, got) == got
+            lo, hi = ctypes.c_uint64(), ctypes.c_uint64()
+            assert lib.sat_tree_shard(nprob.ref, P, 3, 1, ctypes.byref(lo), ctypes.byref(hi)) == 0
+            assert 0 < lo.value < hi.value < info.n_tasks
