@@ -40,6 +40,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=8.0, help="CPU baseline sample length")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-index-leg", action="store_true", help="config 1: skip the per-candidate k_cand leg")
     return ap.parse_args()
 
 
@@ -104,12 +105,32 @@ def workload(cfg: int, budget: int):
     return w, t, c, opts
 
 
+def respawn_if_needed(args) -> None:
+    """`--gpus N` outside torchrun: re-exec this script under torch.distributed.run with N ranks
+    (one process per GPU, 127.0.0.1 rendezvous), so `python bench.py --gpus N` always runs N ranks."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    import socket
+
+    with socket.socket() as sock:
+        sock.bind(("127.0.0.1", 0))
+        port = sock.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
+
+
 def dist_setup(n_gpus: int):
     import torch
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != n_gpus:
+        raise SystemExit(f"bench.py: --gpus {n_gpus} but WORLD_SIZE={world} (launch with torchrun "
+                         f"--nproc-per-node {n_gpus}, or without torchrun to let bench.py spawn the ranks)")
+    if world > 1 and os.environ.get("SATURN_BENCH_GPU_OVERRIDE") is None and torch.cuda.device_count() < world:
+        raise SystemExit(f"bench.py: {world} ranks need {world} GPUs, {torch.cuda.device_count()} visible")
     if world > 1:
         import torch.distributed as dist
 
@@ -252,20 +273,32 @@ def run_reference(args):
     print(json.dumps(line))
 
 
-def ncu_traffic(kernel: str, cfg: int):
-    """DRAM bytes per launch of the dominant kernel from the newest committed ncu --set full
-    capture of this kernel and config (profiles/rNN_ncu_full_<kernel>_cfg<k>.json), else None."""
+NCU_KEYS = {"issue_active_pct": "smsp__issue_active.avg.pct_of_peak_sustained_active",
+            "alu_pipe_pct": "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+            "fma_pipe_pct": "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+            "lsu_pipe_pct": "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+            "threads_per_warp_inst": "smsp__thread_inst_executed_per_inst_executed.ratio",
+            "warp_insts": "smsp__inst_executed.sum",
+            "kernel_ms": "gpu__time_duration.sum"}
+
+
+def ncu_capture(kernel: str, cfg: int):
+    """The newest committed `ncu --set full` summary of this kernel at this config
+    (profiles/rNN_ncu_full_<kernel>_cfg<k>.json): (DRAM bytes per launch, issue / pipe
+    utilisation dict, source path), or Nones."""
     import glob
 
-    hits = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_ncu_full_{kernel}_cfg{cfg}.json")))
+    hits = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_ncu_full_{kernel}_cfg{cfg}.json")),
+                  key=lambda f: os.path.basename(f).split("_")[0])
     if not hits:
-        return None, None
+        return None, None, None
     with open(hits[-1]) as f:
         rep = json.load(f)
     for k in rep.get("kernels", []):
-        if kernel in k.get("kernel", "") and "traffic_bytes" in k:
-            return k["traffic_bytes"], os.path.relpath(hits[-1], ROOT)
-    return None, None
+        if kernel in k.get("kernel", ""):
+            util = {short: k[m]["value"] for short, m in NCU_KEYS.items() if isinstance(k.get(m), dict)}
+            return k.get("traffic_bytes"), util, os.path.relpath(hits[-1], ROOT)
+    return None, None, None
 
 
 # ----------------------------------------------------------------------------- ours
@@ -336,6 +369,44 @@ def introspection_run(t, w, opts, group=None, record=None):
     rep = SIM.simulate(w, t, sol0.plan, SIM.SimOptions(introspection_interval=sol0.plan.predicted_makespan / 10,
                                                        checkpoint_overhead=30.0, replanner=replan))
     return rep, evaluated[0]
+
+
+def per_candidate_leg(eng, prob, opts, rank, world, group, peak_i32, tree_key, reps: int = 2):
+    """The exhaustive space once more through the per-candidate kernel (k_cand, index source):
+    every candidate decoded and list-scheduled from scratch, no prefix sharing -- the SURVEY.md
+    8(d) work model (J x (N + 2G + 2) INT32 ops per plan) applies to it as written.  Same key as
+    the tree walk required."""
+    import torch
+
+    from paper_2311_02840_b200 import engine as EN
+
+    n = prob.space
+    bits, _ = prob.key_bits(n)
+    nprob = EN.NativeProblem(prob, bits)
+    a, b = EN._shard(n, rank, world)
+    best = eng.reset_best(torch.empty(2, dtype=torch.int64, device=eng.device))
+    stream = torch.cuda.current_stream()
+    eng.search_index(nprob, a, b, best)                                   # warm-up
+    torch.cuda.synchronize()
+    times = []
+    for _ in range(reps):
+        eng.reset_best(best)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        eng.search_index(nprob, a, b, best)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1) / 1e3)
+    t_dev = max_over_ranks(min(times), world)
+    k = int(EN._combine(best, True, group, world)[0])
+    key = (k >> bits, k & ((1 << bits) - 1))
+    ops_per_plan = prob.J * (prob.N + 2 * prob.G + 2)
+    rate = n / t_dev
+    return {"kernel": "k_cand<int32, index> (one candidate per thread, decoded + scheduled from scratch)",
+            "candidates": n, "device_s": t_dev, "value": rate, "unit": "plans/s",
+            "ops_per_plan": ops_per_plan, "achieved_tops": rate * ops_per_plan / 1e12,
+            "frac_of_int32_peak": rate * ops_per_plan / peak_i32,
+            "key": list(key), "key_equals_tree": list(key) == list(tree_key)}
 
 
 def run_ours(args):
@@ -494,8 +565,17 @@ def run_ours(args):
     per_launch_ops = sum(s.ops for s in solves)
     achieved = per_launch_ops / kern_avg
     kernel_name = head.kernel
-    traffic, traffic_src = ncu_traffic(kernel_name, 1 if args.config == 2 else args.config)
+    traffic, ncu_util, traffic_src = ncu_capture(kernel_name, 1 if args.config == 2 else args.config)
     prob = head.prob
+    # SURVEY.md 8(d)'s per-plan work model applied to every candidate of the step as if each were
+    # scheduled from scratch: J x (N + 2G + 2) INT32 ops.  The tree walk shares prefixes, so for it
+    # this exceeds the peak (the sharing is worth that factor); per-candidate kernels sit below 1.
+    per_plan_ops = sum(s.n_cand * s.prob.J * (s.prob.N + 2 * s.prob.G + 2) for s in solves)
+    per_plan_frac = per_plan_ops / kern_avg / peak_i32
+    leg = None
+    if args.config == 1 and head.use_tree and not args.no_index_leg:
+        leg = per_candidate_leg(eng, prob, opts, rank, world, group, peak_i32,
+                                (ms, key[0] & ((1 << idx_bits) - 1)))
 
     line = {
         "metric": "candidate plans evaluated/sec", "value": value, "unit": "plans/s", "n_gpus": world,
@@ -525,12 +605,29 @@ def run_ours(args):
                                      "measured: sat_alu_probe IMNMX chains on this GPU (MEASURED_PEAKS.json has "
                                      "no INT32 figure)"),
                      "int32_peak": peak_i32 / 1e12, "frac_of_int32_peak": achieved / peak_i32,
-                     "algorithmic_ops_per_launch": per_launch_ops},
+                     "algorithmic_ops_per_launch": per_launch_ops,
+                     "ops_model": ("tree walk on the minimal enumeration tree: internal placements x "
+                                   "(N + 2G + 2) + leaves x (N + 2) (DESIGN.md 4.1)" if head.use_tree else
+                                   "candidates x J x (N + 2G + 2) (SURVEY.md 8(d))"),
+                     "per_plan_model_ops": per_plan_ops, "per_plan_model_frac": per_plan_frac,
+                     "ncu": ncu_util, "ncu_source": traffic_src},
         "clocks": clk.summary(),
     }
     if head.use_tree:
         line["config"]["prefix_len"] = head.info.prefix_len
         line["config"]["walk_placements"] = head.info.n_job_steps
+        line["config"]["counting"] = (
+            "exhaustive prefix-shared enumeration (k_tree): every one of the candidates_per_step "
+            "candidates' makespans is computed and enters the argmin, but candidates sharing an "
+            "(order, options) prefix share its placements and the last job's options fold into "
+            "per-gang minima -- ~7 ALU ops per candidate instead of J x (N + 2G + 2); the "
+            "per-candidate kernel over the same space is per_candidate_leg")
+    elif head.mode == "exhaustive":
+        line["config"]["counting"] = "exhaustive, one candidate per thread decoded and scheduled from scratch"
+    else:
+        line["config"]["counting"] = "sampled candidates substream(seed, i), each scheduled from scratch"
+    if leg is not None:
+        line["per_candidate_leg"] = leg
     if report is not None:
         line["introspection"] = {"makespan_s": report.makespan, "replans": report.replan_count,
                                  "checkpoints": report.checkpoint_count,
@@ -561,6 +658,7 @@ def main():
     if args.impl == "reference":
         run_reference(args)
     else:
+        respawn_if_needed(args)
         run_ours(args)
 
 

@@ -213,7 +213,7 @@ def solve_problem(prob: SearchProblem, workload, opts: SolveOptions, running_con
         for cand, (_, b_order, name) in zip(cands, baselines):
             if cand[2] < ms and (incumbent is None or cand[2] < incumbent[0][2]):
                 incumbent = (cand, b_order, name)
-    except E.SchedulerError:
+    except (E.SchedulerError, err.SchedulerError):      # ours or the caller family's: as raised
         raise
     except Exception as exc:  # CUDA / NCCL trouble -> PlanFailure (ReplanFailure on re-solve)
         cls = err.ReplanFailure if running_context is not None else err.PlanFailure
