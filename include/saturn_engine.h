@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define SAT_ABI_VERSION 3
+#define SAT_ABI_VERSION 4
 
 /* status codes (mapped to reference errors.py classes by the host layer) */
 #define SAT_OK              0
@@ -181,6 +181,33 @@ int sat_schedule(const sat_problem_t *p, int32_t source, uint64_t seed,
 /* Bytes of the launch-parameter block the tree / bnb searches pass by value (their
  * host-to-device traffic per launch, besides the 24-byte cursor reset). */
 size_t sat_tree_param_bytes(void);
+
+/* State-space search (one node, grid time; ABI v4): is there a candidate -- options + order,
+ * list-scheduled exactly as by the other searches -- with makespan <= target?  Level k holds
+ * the distinct states (jobs still to place, sorted GPU free times) after k placements; children
+ * whose makespan lower bound exceeds `target` are cut; distinct states are kept in an exact
+ * hash set in d_ws.  INFEASIBLE proves that no candidate of the whole space reaches `target`
+ * (with a candidate at target + 1 in hand, that candidate is optimal -- the proof SPEC.md:210-214's
+ * branch-and-bound returns as status Optimal).  FEASIBLE: h_candidate (host, 2J bytes: option
+ * digit per job, then the order) receives one candidate with makespan <= target, chosen
+ * deterministically (smallest final state key, then smallest parent keys, lowest options).
+ * BUDGET: more than max_states states over all levels; nothing decided.  Synchronous: returns
+ * after the search (one small read-back per level).  Keys must fit 63 bits:
+ * 2^J x C(target + G, G) < 2^63, else SAT_ERR_UNSUPPORTED. */
+#define SAT_DP_INFEASIBLE 0
+#define SAT_DP_FEASIBLE   1
+#define SAT_DP_BUDGET     2
+typedef struct sat_dp_info {
+    int32_t  status;        /* SAT_DP_*                                                     */
+    int32_t  levels;        /* levels expanded                                              */
+    uint64_t states;        /* distinct states over all levels                              */
+    uint64_t widest_level;  /* states of the largest level                                   */
+    int32_t  makespan;      /* FEASIBLE: makespan of the returned candidate                  */
+    int32_t  reserved;
+} sat_dp_info_t;
+int sat_dp_workspace_bytes(const sat_problem_t *p, int32_t target, uint64_t max_states, size_t *bytes);
+int sat_search_dp(const sat_problem_t *p, int32_t target, uint64_t max_states, uint8_t *h_candidate,
+                  sat_dp_info_t *info, void *d_ws, size_t ws_bytes, void *stream);
 
 /* INT32 min/max issue-rate probe for the roofline denominator: runs `iters`
  * dependent-chain IMNMX iterations on every SM; *d_ops_out = lane-ops done. */

@@ -52,7 +52,8 @@ def up_to_date(out_path: str = OUT) -> bool:
 def units(obj_dir: str = OBJ_DIR) -> list:
     """(source, extra defines, object) for every translation unit."""
     OBJ_DIR = obj_dir  # noqa: N806 (local rebinding keeps the table below readable)
-    out = [(os.path.join(CSRC, "sat_engine.cu"), [], os.path.join(OBJ_DIR, "sat_engine.o"))]
+    out = [(os.path.join(CSRC, "sat_engine.cu"), [], os.path.join(OBJ_DIR, "sat_engine.o")),
+           (os.path.join(CSRC, "sat_dp.cu"), [], os.path.join(OBJ_DIR, "sat_dp.o"))]
     for t in ("int32_t", "double"):
         for s in ("SAT_SRC_INDEX", "SAT_SRC_SUBSTREAM", "SAT_SRC_SEED"):
             ls = ["-DSAT_LS_INSTANTIATE"] if t == "int32_t" and s != "SAT_SRC_INDEX" else []

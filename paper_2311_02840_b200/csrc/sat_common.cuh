@@ -68,7 +68,8 @@ __device__ inline uint64_t shfl_u64(uint64_t v, int src) {
 }
 
 
-int device_sms();   // sat_engine.cu
+int device_sms();                          // sat_engine.cu
+int validate(const sat_problem_t *p);      // sat_engine.cu
 
 // ---------------------------------------------------------------------------
 // k_tree: prefix-shared exhaustive walk, one node, grid int32 time

@@ -1,0 +1,473 @@
+// sat_dp.cu -- state-space search of the list-scheduling candidate space (one node, grid time).
+//
+// Every candidate (options + submission order) is a path of J placements.  After k placements
+// the list scheduler's whole future depends only on the STATE (set of jobs still to place,
+// sorted GPU free times): the makespan of any completion is a function of that state and of
+// the remaining choices.  Many prefixes reach the same state (different orders of jobs that
+// end up at the same free-time profile), so enumerating distinct states level by level covers
+// the prod(radix) x J! candidates with far fewer nodes than the prefix tree of k_tree.
+//
+// sat_search_dp answers "is there a candidate with makespan <= T?" exactly:
+//   level k -> k+1: every state x (job j still to place) x (option o of j) is placed with the
+//   same sorted-vector update as the other kernels (b[i] = max(a[i], min(a[i+g], e)), start =
+//   max(a[g-1], release)); children whose makespan lower bound exceeds T are cut -- the bound
+//   is the bound-and-prune one: committed end e <= T, area (sum of free times + least area of
+//   every job still to place <= T x G), and every remaining job's earliest end
+//   (min_k max(b[k], rel) + least duration at gang k+1 <= T).  Distinct children go to a
+//   global hash set keyed EXACTLY (R bits x C(T+G, G) + combinatorial rank of the sorted free
+//   times: the state itself, no fingerprints, so the dedup is sound).  An empty level proves
+//   that no candidate reaches T (the proof configs 3-5's lower bound cannot give); a
+//   non-empty last level yields one such candidate, rebuilt backwards level by level
+//   (deterministically: the smallest-key final state, then the smallest-key parent and the
+//   lowest option at each step).
+//
+// One thread per (state, job); the level loop is driven from the host (one small read-back
+// per level).  HBM holds every level's states (kept for the reconstruction).
+#include "sat_common.cuh"
+
+#include <nvtx3/nvToolsExt.h>
+
+namespace sat {
+
+constexpr int kDpMaxJ = 64;
+constexpr int kDpMaxOpt = 1024;
+constexpr int kDpThreads = 256;
+constexpr uint64_t kDpEmpty = ~0ull;
+
+struct DpParams {
+    int32_t J, Gr, T, rank_unused;
+    uint64_t cnum;                    // C(T + Gr, Gr): sorted free-time vectors with values <= T
+    int32_t ubase[kDpMaxJ], ucnt[kDpMaxJ];   // usable options of job j: [ubase, ubase + ucnt)
+    int32_t release[kDpMaxJ];
+    int32_t minarea[kDpMaxJ];         // least g x d over the job's usable options
+    uint8_t ug[kDpMaxOpt];            // gang size of usable option q
+    int16_t ud[kDpMaxOpt];            // duration of usable option q
+    int16_t dg[kDpMaxJ][32];          // least usable duration of job j at gang k+1 (T+1: none)
+    const uint64_t *binom;            // [(T + Gr + 1)][Gr + 1]: C(n, k)
+    uint64_t *table;                  // hash set of state keys, kDpEmpty = free
+    uint64_t cap_mask;
+    int32_t cap_log2;
+    int32_t max_probe;
+    const uint64_t *in_R;             // level k: remaining-job sets
+    const uint16_t *in_A;             // level k: sorted free times [n_in][Gr]
+    uint64_t n_in;
+    uint64_t *out_R;                  // level k+1 (appended)
+    uint16_t *out_A;
+    uint64_t out_cap;
+    unsigned long long *count;        // states appended to level k+1
+    unsigned int *overflow;           // set when out_cap or the probe limit is exceeded
+    // reconstruction (k_dp_parent): the child state searched for
+    uint64_t child_R;
+    uint16_t child_A[32];
+    unsigned long long *min_key;
+};
+
+__device__ __forceinline__ uint64_t dp_rank(const DpParams &p, const int32_t *b) {
+    const int K = p.Gr + 1;
+    uint64_t r = 0;
+    for (int i = 0; i < p.Gr; ++i) r += __ldg(&p.binom[(b[i] + i) * K + (i + 1)]);
+    return r;
+}
+
+// place option q (gang g, duration d) of a job with release rel on the sorted vector a
+// (a[Gr..] = +inf); returns the end time, b = the new sorted vector
+template <int GM>
+__device__ __forceinline__ int32_t dp_place(const int32_t *a, int Gr, int g, int d, int rel, int32_t *b) {
+    const int32_t t = max(a[g - 1], rel);
+    const int32_t e = t + d;
+#pragma unroll
+    for (int i = 0; i < GM; ++i) {
+        if (i < Gr) {
+            const int32_t up = (i + g < Gr) ? a[i + g] : 0x7fffffff;
+            b[i] = max(a[i], min(up, e));
+        }
+    }
+    return e;
+}
+
+// bound-and-prune test of a child state (R2, b): can some completion end by T?
+template <int GM>
+__device__ __forceinline__ bool dp_viable(const DpParams &p, uint64_t R2, const int32_t *b) {
+    int64_t area = 0;
+#pragma unroll
+    for (int i = 0; i < GM; ++i)
+        if (i < p.Gr) area += b[i];
+    for (int i = 0; i < p.J; ++i) {               // uniform loop: dg / minarea reads broadcast
+        if (!((R2 >> i) & 1ull)) continue;
+        area += p.minarea[i];
+        int32_t lo = 0x7fffffff;
+#pragma unroll
+        for (int k = 0; k < GM; ++k)
+            if (k < p.Gr) lo = min(lo, max(b[k], p.release[i]) + (int32_t)p.dg[i][k]);
+        if (lo > p.T) return false;
+    }
+    return area <= (int64_t)p.T * p.Gr;
+}
+
+template <int GM>
+__global__ void __launch_bounds__(kDpThreads) k_dp_expand(const __grid_constant__ DpParams p) {
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (tid >= p.n_in * (uint64_t)p.J) return;
+    if (*reinterpret_cast<volatile unsigned int *>(p.overflow)) return;
+    const uint64_t s = tid / (uint64_t)p.J;
+    const int j = (int)(tid - s * (uint64_t)p.J);
+    const uint64_t R = p.in_R[s];
+    if (!((R >> j) & 1ull)) return;
+    const uint64_t R2 = R & ~(1ull << j);
+    int32_t a[GM], b[GM];
+#pragma unroll
+    for (int i = 0; i < GM; ++i) a[i] = i < p.Gr ? (int32_t)p.in_A[s * p.Gr + i] : 0x7fffffff;
+    for (int q = p.ubase[j]; q < p.ubase[j] + p.ucnt[j]; ++q) {
+        const int e = dp_place<GM>(a, p.Gr, p.ug[q], p.ud[q], p.release[j], b);
+        if (e > p.T) continue;
+        if (!dp_viable<GM>(p, R2, b)) continue;
+        const uint64_t key = R2 * p.cnum + dp_rank(p, b);
+        uint64_t h = (key * kGolden) >> (64 - p.cap_log2);
+        for (int probe = 0;; ++probe) {
+            if (probe > p.max_probe) { atomicOr(p.overflow, 1u); return; }
+            const unsigned long long old = atomicCAS(reinterpret_cast<unsigned long long *>(&p.table[h]),
+                                                     (unsigned long long)kDpEmpty, (unsigned long long)key);
+            if (old == kDpEmpty) {                 // first time this state is reached: append it
+                const unsigned long long idx = atomicAdd(p.count, 1ull);
+                if (idx >= p.out_cap) { atomicOr(p.overflow, 1u); return; }
+                p.out_R[idx] = R2;
+#pragma unroll
+                for (int i = 0; i < GM; ++i)
+                    if (i < p.Gr) p.out_A[idx * p.Gr + i] = (uint16_t)b[i];
+                break;
+            }
+            if (old == key) break;                 // already in the level
+            h = (h + 1) & p.cap_mask;
+        }
+    }
+}
+
+// smallest key among a level's states (the final state of the reconstruction)
+__global__ void k_dp_min_key(const __grid_constant__ DpParams p) {
+    const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= p.n_in) return;
+    int32_t a[32];
+    for (int i = 0; i < p.Gr; ++i) a[i] = p.in_A[s * p.Gr + i];
+    atomicMin(p.min_key, (unsigned long long)(p.in_R[s] * p.cnum + dp_rank(p, a)));
+}
+
+// smallest key among the level's states that reach (child_R, child_A) with one placement
+template <int GM>
+__global__ void __launch_bounds__(kDpThreads) k_dp_parent(const __grid_constant__ DpParams p) {
+    const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= p.n_in) return;
+    const uint64_t R = p.in_R[s];
+    const uint64_t diff = R ^ p.child_R;
+    if ((R & p.child_R) != p.child_R || __popcll(diff) != 1) return;
+    const int j = __ffsll((long long)diff) - 1;
+    int32_t a[GM], b[GM];
+#pragma unroll
+    for (int i = 0; i < GM; ++i) a[i] = i < p.Gr ? (int32_t)p.in_A[s * p.Gr + i] : 0x7fffffff;
+    for (int q = p.ubase[j]; q < p.ubase[j] + p.ucnt[j]; ++q) {
+        dp_place<GM>(a, p.Gr, p.ug[q], p.ud[q], p.release[j], b);
+        bool same = true;
+#pragma unroll
+        for (int i = 0; i < GM; ++i)
+            if (i < p.Gr && b[i] != (int32_t)p.child_A[i]) same = false;
+        if (same) {
+            atomicMin(p.min_key, (unsigned long long)(R * p.cnum + dp_rank(p, a)));
+            return;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------- host side
+struct DpPlan {
+    DpParams p{};
+    std::vector<int32_t> uorig;       // usable option q -> option digit of its job
+    std::vector<int32_t> a0;          // initial sorted free times (Gr)
+    std::vector<uint64_t> binom;      // host copy of the table
+    int status = -1;                  // SAT_DP_* when decided without a search
+    size_t binom_bytes = 0, table_bytes = 0, R_bytes = 0, A_bytes = 0;
+    uint64_t cap = 0;
+};
+
+static inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// usable options, bound tables, key encoding and workspace layout for (p, T, max_states)
+static int dp_prepare(const sat_problem_t *pr, int32_t T, uint64_t max_states, DpPlan &d) {
+    if (pr->N != 1 || pr->time_mode != SAT_TIME_GRID_I32) return SAT_ERR_UNSUPPORTED;
+    if (pr->J > kDpMaxJ || max_states < 1) return SAT_ERR_INVALID;
+    const int J = pr->J, Gr = pr->node_gpus[0];
+    if (Gr > 32 || T < 0 || T > 30000) return SAT_ERR_UNSUPPORTED;
+    DpParams &p = d.p;
+    p.J = J; p.Gr = Gr; p.T = T;
+    d.a0.assign(Gr, 0);
+    int64_t sum0 = 0;
+    for (int i = 0; i < Gr; ++i) {
+        d.a0[i] = pr->init_free_i32 ? pr->init_free_i32[i] : 0;
+        sum0 += d.a0[i];
+    }
+    if (!std::is_sorted(d.a0.begin(), d.a0.end())) return SAT_ERR_INVALID;
+    if (d.a0[Gr - 1] > T) { d.status = SAT_DP_INFEASIBLE; return SAT_OK; }
+    // least area per job over the options that can end by T at all, then the area slack
+    int64_t need = sum0;
+    std::vector<int64_t> least(J);
+    for (int j = 0; j < J; ++j) {
+        const int32_t rel = pr->release_i32 ? pr->release_i32[j] : 0;
+        int64_t m = INT64_MAX;
+        for (int o = 0; o < pr->radix[j]; ++o) {
+            const int q = j * pr->Cmax + o;
+            const int g = pr->gpus[q];
+            const int32_t dd = pr->dur_i32[q];
+            if (g > Gr || std::max(d.a0[g - 1], rel) + (int64_t)dd > T) continue;
+            m = std::min<int64_t>(m, (int64_t)g * dd);
+        }
+        if (m == INT64_MAX) { d.status = SAT_DP_INFEASIBLE; return SAT_OK; }
+        least[j] = m;
+        need += m;
+    }
+    const int64_t slack = (int64_t)T * Gr - need;
+    if (slack < 0) { d.status = SAT_DP_INFEASIBLE; return SAT_OK; }
+    int q = 0;
+    for (int j = 0; j < J; ++j) {
+        const int32_t rel = pr->release_i32 ? pr->release_i32[j] : 0;
+        p.release[j] = rel;
+        p.ubase[j] = q;
+        p.minarea[j] = (int32_t)least[j];
+        for (int k = 0; k < 32; ++k) p.dg[j][k] = (int16_t)(T + 1);
+        for (int o = 0; o < pr->radix[j]; ++o) {
+            const int src = j * pr->Cmax + o;
+            const int g = pr->gpus[src];
+            const int32_t dd = pr->dur_i32[src];
+            if (g > Gr || std::max(d.a0[g - 1], rel) + (int64_t)dd > T) continue;
+            if ((int64_t)g * dd > least[j] + slack) continue;      // would overrun the area on its own
+            if (q >= kDpMaxOpt) return SAT_ERR_TOO_LARGE;
+            p.ug[q] = (uint8_t)g;
+            p.ud[q] = (int16_t)dd;
+            d.uorig.push_back(o);
+            p.dg[j][g - 1] = (int16_t)std::min<int32_t>(p.dg[j][g - 1], dd);
+            ++q;
+        }
+        p.ucnt[j] = q - p.ubase[j];
+    }
+    // exact key: R x C(T + Gr, Gr) + rank must stay below 2^63
+    const int n_max = T + Gr;
+    d.binom.assign((size_t)(n_max + 1) * (Gr + 1), 0);
+    for (int n = 0; n <= n_max; ++n) {
+        d.binom[(size_t)n * (Gr + 1)] = 1;
+        for (int k = 1; k <= Gr && k <= n; ++k) {
+            const unsigned __int128 v = (unsigned __int128)d.binom[(size_t)(n - 1) * (Gr + 1) + k - 1] +
+                                        (k <= n - 1 ? d.binom[(size_t)(n - 1) * (Gr + 1) + k] : 0);
+            if (v >> 62) return SAT_ERR_UNSUPPORTED;
+            d.binom[(size_t)n * (Gr + 1) + k] = (uint64_t)v;
+        }
+    }
+    p.cnum = d.binom[(size_t)n_max * (Gr + 1) + Gr];
+    if ((unsigned __int128)p.cnum << J >= ((unsigned __int128)1 << 63)) return SAT_ERR_UNSUPPORTED;
+    // workspace: binomials | hash set (>= 2x the states + slack, power of two) | R | A | counters
+    uint64_t cap = 1;
+    int lg = 0;
+    while (cap < 2 * max_states + (1u << 16)) { cap <<= 1; ++lg; }
+    d.cap = cap;
+    p.cap_mask = cap - 1;
+    p.cap_log2 = lg;
+    p.max_probe = 1 << 14;
+    d.binom_bytes = align256(d.binom.size() * sizeof(uint64_t));
+    d.table_bytes = align256(cap * sizeof(uint64_t));
+    d.R_bytes = align256(max_states * sizeof(uint64_t));
+    d.A_bytes = align256(max_states * Gr * sizeof(uint16_t));
+    return SAT_OK;
+}
+
+static size_t dp_ws_bytes(const DpPlan &d) { return d.binom_bytes + d.table_bytes + d.R_bytes + d.A_bytes + 256; }
+
+template <int GM>
+static int dp_launch_expand(const DpParams &p, cudaStream_t s) {
+    const uint64_t threads = p.n_in * (uint64_t)p.J;
+    const uint64_t blocks = (threads + kDpThreads - 1) / kDpThreads;
+    if (blocks == 0) return SAT_OK;
+    if (blocks > 0x7fffffffull) return SAT_ERR_TOO_LARGE;
+    k_dp_expand<GM><<<(unsigned)blocks, kDpThreads, 0, s>>>(p);
+    return cudaGetLastError() == cudaSuccess ? SAT_OK : SAT_ERR_CUDA;
+}
+
+template <int GM>
+static int dp_launch_parent(const DpParams &p, cudaStream_t s) {
+    const uint64_t blocks = (p.n_in + kDpThreads - 1) / kDpThreads;
+    if (blocks == 0) return SAT_OK;
+    k_dp_parent<GM><<<(unsigned)blocks, kDpThreads, 0, s>>>(p);
+    return cudaGetLastError() == cudaSuccess ? SAT_OK : SAT_ERR_CUDA;
+}
+
+static int dp_expand(const DpParams &p, cudaStream_t s) {
+    if (p.Gr <= 8) return dp_launch_expand<8>(p, s);
+    if (p.Gr <= 16) return dp_launch_expand<16>(p, s);
+    return dp_launch_expand<32>(p, s);
+}
+
+static int dp_parent(const DpParams &p, cudaStream_t s) {
+    if (p.Gr <= 8) return dp_launch_parent<8>(p, s);
+    if (p.Gr <= 16) return dp_launch_parent<16>(p, s);
+    return dp_launch_parent<32>(p, s);
+}
+
+// host: key -> (R, sorted free times)
+static void dp_unrank(const DpPlan &d, uint64_t key, uint64_t *R, int32_t *a) {
+    const int Gr = d.p.Gr, K = Gr + 1;
+    *R = key / d.p.cnum;
+    uint64_t r = key % d.p.cnum;
+    int c = d.p.T + Gr - 1;
+    for (int i = Gr - 1; i >= 0; --i) {
+        while (c >= 0 && d.binom[(size_t)c * K + (i + 1)] > r) --c;
+        r -= d.binom[(size_t)c * K + (i + 1)];
+        a[i] = c - i;
+        --c;
+    }
+}
+
+static int32_t dp_host_place(const DpPlan &d, const int32_t *a, int q, int rel, int32_t *b) {
+    const int Gr = d.p.Gr, g = d.p.ug[q];
+    const int32_t e = std::max(a[g - 1], rel) + d.p.ud[q];
+    for (int i = 0; i < Gr; ++i) b[i] = std::max(a[i], std::min(i + g < Gr ? a[i + g] : INT32_MAX, e));
+    return e;
+}
+
+}  // namespace sat
+
+using namespace sat;
+
+extern "C" {
+
+int sat_dp_workspace_bytes(const sat_problem_t *p, int32_t target, uint64_t max_states, size_t *bytes) {
+    if (!bytes) return SAT_ERR_INVALID;
+    int st = validate(p);
+    if (st) return st;
+    DpPlan d;
+    st = dp_prepare(p, target, max_states, d);
+    if (st) return st;
+    *bytes = d.status >= 0 ? 256 : dp_ws_bytes(d);
+    return SAT_OK;
+}
+
+int sat_search_dp(const sat_problem_t *pr, int32_t target, uint64_t max_states, uint8_t *h_candidate,
+                  sat_dp_info_t *info, void *d_ws, size_t ws_bytes, void *stream) {
+    if (!info) return SAT_ERR_INVALID;
+    int st = validate(pr);
+    if (st) return st;
+    nvtxRangePushA("sat_search_dp");
+    struct Pop { ~Pop() { nvtxRangePop(); } } pop_on_exit;
+    std::memset(info, 0, sizeof(*info));
+    DpPlan d;
+    st = dp_prepare(pr, target, max_states, d);
+    if (st) return st;
+    if (d.status >= 0) { info->status = d.status; return SAT_OK; }
+    if (!d_ws || ws_bytes < dp_ws_bytes(d)) return SAT_ERR_INVALID;
+    cudaStream_t s = (cudaStream_t)stream;
+    uint8_t *ws = static_cast<uint8_t *>(d_ws);
+    uint64_t *binom = reinterpret_cast<uint64_t *>(ws);
+    uint64_t *table = reinterpret_cast<uint64_t *>(ws + d.binom_bytes);
+    uint64_t *Rs = reinterpret_cast<uint64_t *>(ws + d.binom_bytes + d.table_bytes);
+    uint16_t *As = reinterpret_cast<uint16_t *>(ws + d.binom_bytes + d.table_bytes + d.R_bytes);
+    auto *ctr = reinterpret_cast<unsigned long long *>(ws + d.binom_bytes + d.table_bytes + d.R_bytes + d.A_bytes);
+    // ctr[0] = count, ctr[1] = overflow flag (u32), ctr[2] = min key
+    DpParams &p = d.p;
+    const int J = pr->J, Gr = p.Gr;
+    if (cudaMemcpyAsync(binom, d.binom.data(), d.binom.size() * sizeof(uint64_t), cudaMemcpyHostToDevice, s) ||
+        cudaMemsetAsync(table, 0xFF, d.cap * sizeof(uint64_t), s) || cudaMemsetAsync(ctr, 0, 256, s))
+        return SAT_ERR_CUDA;
+    // level 0: every job to place, the initial free times
+    const uint64_t full = J == 64 ? ~0ull : ((1ull << J) - 1ull);
+    std::vector<uint16_t> a0(Gr);
+    for (int i = 0; i < Gr; ++i) a0[i] = (uint16_t)d.a0[i];
+    if (cudaMemcpyAsync(Rs, &full, sizeof(full), cudaMemcpyHostToDevice, s) ||
+        cudaMemcpyAsync(As, a0.data(), Gr * sizeof(uint16_t), cudaMemcpyHostToDevice, s))
+        return SAT_ERR_CUDA;
+    p.binom = binom;
+    p.table = table;
+    p.count = ctr;
+    p.overflow = reinterpret_cast<unsigned int *>(ctr + 1);
+    p.min_key = ctr + 2;
+    std::vector<uint64_t> base(J + 2, 0), size(J + 2, 0);
+    base[0] = 0; size[0] = 1;
+    uint64_t total = 1, widest = 1;
+    int level = 0;
+    for (; level < J; ++level) {
+        p.in_R = Rs + base[level];
+        p.in_A = As + base[level] * Gr;
+        p.n_in = size[level];
+        base[level + 1] = base[level] + size[level];
+        p.out_R = Rs + base[level + 1];
+        p.out_A = As + base[level + 1] * Gr;
+        p.out_cap = max_states - base[level + 1];
+        if (cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), s)) return SAT_ERR_CUDA;
+        if ((st = dp_expand(p, s))) return st;
+        unsigned long long got[2];
+        if (cudaMemcpyAsync(got, ctr, sizeof(got), cudaMemcpyDeviceToHost, s) || cudaStreamSynchronize(s))
+            return SAT_ERR_CUDA;
+        if ((unsigned int)got[1]) {
+            info->status = SAT_DP_BUDGET;
+            info->levels = level;
+            info->states = total;
+            info->widest_level = widest;
+            return SAT_OK;
+        }
+        size[level + 1] = got[0];
+        total += got[0];
+        widest = std::max<uint64_t>(widest, got[0]);
+        if (got[0] == 0) { ++level; break; }
+    }
+    info->levels = level;
+    info->states = total;
+    info->widest_level = widest;
+    if (level < J || size[J] == 0) { info->status = SAT_DP_INFEASIBLE; return SAT_OK; }
+    // a candidate reaching T: smallest-key final state, then backwards the smallest-key parent
+    // and its lowest option producing the child
+    info->status = SAT_DP_FEASIBLE;
+    const unsigned long long ones = ~0ull;
+    auto min_key_of = [&](int lv, auto launch) -> int {
+        p.in_R = Rs + base[lv];
+        p.in_A = As + base[lv] * Gr;
+        p.n_in = size[lv];
+        if (cudaMemcpyAsync(p.min_key, &ones, sizeof(ones), cudaMemcpyHostToDevice, s)) return SAT_ERR_CUDA;
+        return launch();
+    };
+    st = min_key_of(J, [&]() {
+        const uint64_t blocks = (p.n_in + kDpThreads - 1) / kDpThreads;
+        k_dp_min_key<<<(unsigned)blocks, kDpThreads, 0, s>>>(p);
+        return cudaGetLastError() == cudaSuccess ? SAT_OK : SAT_ERR_CUDA;
+    });
+    if (st) return st;
+    unsigned long long key;
+    if (cudaMemcpyAsync(&key, p.min_key, sizeof(key), cudaMemcpyDeviceToHost, s) || cudaStreamSynchronize(s))
+        return SAT_ERR_CUDA;
+    std::vector<int32_t> cur(Gr), par(Gr), tmp(Gr);
+    uint64_t curR;
+    dp_unrank(d, key, &curR, cur.data());
+    info->makespan = cur[Gr - 1];
+    std::vector<int> order(J), opt(J);
+    for (int lv = J; lv >= 1; --lv) {
+        p.child_R = curR;
+        for (int i = 0; i < Gr; ++i) p.child_A[i] = (uint16_t)cur[i];
+        st = min_key_of(lv - 1, [&]() { return dp_parent(p, s); });
+        if (st) return st;
+        if (cudaMemcpyAsync(&key, p.min_key, sizeof(key), cudaMemcpyDeviceToHost, s) || cudaStreamSynchronize(s))
+            return SAT_ERR_CUDA;
+        if (key == ones) return SAT_ERR_CUDA;          // no parent: cannot happen
+        uint64_t parR;
+        dp_unrank(d, key, &parR, par.data());
+        const int j = __builtin_ctzll(parR ^ curR);
+        int found = -1;
+        for (int q = p.ubase[j]; q < p.ubase[j] + p.ucnt[j] && found < 0; ++q) {
+            dp_host_place(d, par.data(), q, p.release[j], tmp.data());
+            if (std::equal(tmp.begin(), tmp.end(), cur.begin())) found = q;
+        }
+        if (found < 0) return SAT_ERR_CUDA;
+        order[lv - 1] = j;
+        opt[j] = d.uorig[found];
+        curR = parR;
+        cur = par;
+    }
+    if (h_candidate) {
+        for (int j = 0; j < J; ++j) h_candidate[j] = (uint8_t)opt[j];
+        for (int k = 0; k < J; ++k) h_candidate[J + k] = (uint8_t)order[k];
+    }
+    return SAT_OK;
+}
+
+}  // extern "C"

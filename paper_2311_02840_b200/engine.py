@@ -41,6 +41,15 @@ class SatProblem(ctypes.Structure):
     ]
 
 
+class SatDpInfo(ctypes.Structure):
+    _fields_ = [("status", _i32), ("levels", _i32), ("states", _u64), ("widest_level", _u64),
+                ("makespan", _i32), ("reserved", _i32)]
+
+
+SAT_DP_INFEASIBLE, SAT_DP_FEASIBLE, SAT_DP_BUDGET = 0, 1, 2
+DP_STATUS = {SAT_DP_INFEASIBLE: "infeasible", SAT_DP_FEASIBLE: "feasible", SAT_DP_BUDGET: "budget"}
+
+
 class SatTreeInfo(ctypes.Structure):
     _fields_ = [("prefix_len", _i32), ("n_sets", _i32), ("n_tasks", _u64),
                 ("n_candidates", _u64), ("n_job_steps", _u64), ("pair_packed", _i32), ("reserved", _i32)]
@@ -67,6 +76,8 @@ _SIGS = {
     "sat_local_search": ([_vp, _i32, _u64, _u64, _u64, _i32, _i32, _vp, _vp, _vp, ctypes.c_size_t, _vp], _i32),
     "sat_ls_counter_offset": ([_vp, _vp], _i32),
     "sat_tree_shard": ([_vp, _i32, _i32, _i32, _vp, _vp], _i32),
+    "sat_dp_workspace_bytes": ([_vp, _i32, _u64, _vp], _i32),
+    "sat_search_dp": ([_vp, _i32, _u64, _vp, _vp, _vp, ctypes.c_size_t, _vp], _i32),
 }
 
 _LIB = None
@@ -85,7 +96,7 @@ def load_library(path: str = LIB_PATH):
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res
-    if lib.sat_abi_version() != 3:
+    if lib.sat_abi_version() != 4:
         raise E.PlanFailure("libsaturn_b200.so ABI version mismatch")
     _LIB = lib
     return lib
@@ -172,6 +183,7 @@ class SearchResult:
     state: tuple | None = None  # local search: the winning walker's final (options, order)
     replay: tuple | None = None  # the winner's schedule (option, node, start, makespan), queued
                                  # behind the search when search(replay=True)
+    proven: bool = False       # local search: makespan proven optimal by sat_search_dp
 
 
 class Engine:
@@ -191,6 +203,7 @@ class Engine:
         self.sm_count = sm.value
         self._best = torch.empty(2, dtype=torch.int64, device=self.device)
         self._ws = None
+        self._dp_ws = None
         self.launches = 0
 
     # ---- plumbing ----------------------------------------------------------
@@ -328,6 +341,52 @@ class Engine:
         v = out.cpu().tolist()
         return v[:J], v[J:]
 
+    def dp_search(self, nprob: NativeProblem, target: int, max_states: int = 1 << 22):
+        """sat_search_dp: does some candidate reach makespan <= target?  Returns (status, info,
+        candidate) -- candidate = (options, order) when FEASIBLE.  Synchronous."""
+        torch = self.torch
+        need = ctypes.c_size_t()
+        self._check(self.lib.sat_dp_workspace_bytes(nprob.ref, int(target), int(max_states), ctypes.byref(need)),
+                    what="sat_dp_workspace_bytes", nprob=nprob)
+        if self._dp_ws is None or self._dp_ws.numel() < need.value:
+            self._dp_ws = None
+            self._dp_ws = torch.empty(max(need.value, 1 << 16), dtype=torch.uint8, device=self.device)
+        J = nprob.struct.J
+        cand = (ctypes.c_uint8 * (2 * J))()
+        info = SatDpInfo()
+        self._check(self.lib.sat_search_dp(nprob.ref, int(target), int(max_states), cand, ctypes.byref(info),
+                                           _vp(self._dp_ws.data_ptr()), self._dp_ws.numel(), _vp(self.stream())),
+                    what="sat_search_dp", nprob=nprob)
+        self.launches += max(1, info.levels)
+        out = None
+        if info.status == SAT_DP_FEASIBLE:
+            v = list(cand)
+            out = (v[:J], v[J:])
+        return info.status, info, out
+
+    def prove_below(self, prob: SearchProblem, makespan: int, opts: SolveOptions):
+        """Descend from a known candidate makespan with sat_search_dp: target = makespan - 1 until
+        no candidate reaches it (the last makespan is then optimal) or the state budget runs out.
+        Returns (proven, best makespan, improved candidate or None, stats)."""
+        nprob = NativeProblem(prob, 1)
+        stats = {"attempts": [], "states": 0}
+        best_ms, cand = int(makespan), None
+        lb = int(prob.lower_bound())
+        while best_ms > lb:
+            st, info, c = self.dp_search(nprob, best_ms - 1, opts.dp_states)
+            stats["attempts"].append({"target": best_ms - 1, "status": DP_STATUS[st], "levels": info.levels,
+                                      "states": int(info.states), "widest_level": int(info.widest_level)})
+            stats["states"] += int(info.states)
+            if st == SAT_DP_INFEASIBLE:
+                stats["proven"] = True
+                return True, best_ms, cand, stats
+            if st == SAT_DP_BUDGET:
+                stats["proven"] = False
+                return False, best_ms, cand, stats
+            best_ms, cand = int(info.makespan), c
+        stats["proven"] = True
+        return True, best_ms, cand, stats                  # met the lower bound
+
     def search_index(self, nprob, lo, hi, best=None):
         best = self._best if best is None else best
         ws, wsb = self.workspace(nprob)
@@ -446,6 +505,7 @@ class Engine:
         job_steps = 0
         stats, bnb_ws = None, None
         ls_state = None
+        proven_opt = False
         if mode == "exhaustive":
             src = SRC_INDEX
             use_tree = opts.kernel in ("auto", "tree", "bnb") and self._tree_ok(prob)
@@ -489,6 +549,12 @@ class Engine:
             rounds_total, walkers_done, waves = 0, 0, 0
             w0 = 0
             ls_states = []          # (first walker, [walkers][2J] final states) per wave on this rank
+            # after a wave that misses the lower bound, the state-space search (one node) either
+            # proves the wave's best optimal -- no candidate one interval shorter -- or returns a
+            # shorter candidate; it is retried only when a later wave improves the best
+            dp_ok = (opts.prove and nprob.grid and prob.N == 1 and not prob.release_i32.any()
+                     and prob.J <= 64)
+            proof, dp_tried_at, dp_cand = None, None, None
             while w0 < n_idx:
                 w1 = min(n_idx, w0 + wave)
                 a, b = _shard(w1 - w0, rank, world)
@@ -501,8 +567,20 @@ class Engine:
                 k = int(_combine(best, True, group, world)[0])
                 if k != INT64_MAX and (k >> idx_bits) <= target:
                     break
+                if dp_ok and k != INT64_MAX and dp_tried_at != (k >> idx_bits):
+                    dp_tried_at = k >> idx_bits
+                    try:
+                        proven, dp_ms, cand, proof = self.prove_below(prob, dp_tried_at, opts)
+                    except E.TooLarge:              # state key does not fit 63 bits: no proof
+                        dp_ok, proven, cand = False, False, None
+                    if cand is not None:
+                        dp_cand = (dp_ms, cand)
+                    if proven:
+                        break
             stats = {"walkers": walkers_done, "waves": waves, "rounds": rounds_total,
                      "moves_scheduled_max": rounds_total * 32, "lower_bound": target, "stop_ms": stop_ms}
+            if proof is not None:
+                stats["proof"] = proof
             kernel, evaluated = "local", walkers_done
         else:
             src = SRC_SUBSTREAM if source is None else source
@@ -537,6 +615,11 @@ class Engine:
             index = k & ((1 << idx_bits) - 1)
             if mode == "local":
                 ls_state = self._walker_state(ls_states, index, prob.J, group, world)
+                if dp_cand is not None and dp_cand[0] < makespan:
+                    # the state-space search found a shorter candidate than every walker
+                    makespan, ls_state = float(dp_cand[0]), (list(dp_cand[1][0]), list(dp_cand[1][1]))
+                    stats["winner"] = "sat_search_dp"
+                proven_opt = proof is not None and bool(proof.get("proven"))
         else:
             hi_bits, index = int(key[0]), int(key[1])
             if hi_bits == INT64_MAX:
@@ -546,7 +629,8 @@ class Engine:
                             kernel=kernel, exhaustive=mode == "exhaustive",
                             launches=self.launches - launches0, job_steps=job_steps,
                             device_seconds=dev_s, wall_seconds=time.perf_counter() - t0,
-                            stats=stats, idx_bits=idx_bits, state=ls_state, replay=replay_out)
+                            stats=stats, idx_bits=idx_bits, state=ls_state, replay=replay_out,
+                            proven=mode == "local" and proven_opt)
 
     def _walker_state(self, ls_states, index: int, J: int, group, world: int):
         """The winning walker's final (options, order), recorded by its search launch (on the

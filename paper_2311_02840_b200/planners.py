@@ -248,6 +248,9 @@ def solve_problem(prob: SearchProblem, workload, opts: SolveOptions, running_con
         lb = prob.lower_bound()
     if not res.exhaustive and makespan <= lb:
         status = "Optimal"          # a heuristic plan meeting the lower bound is optimal (bound proof)
+    if res.proven and incumbent is None:
+        # sat_search_dp: no candidate of the whole space is one interval shorter
+        status, lb = "Optimal", makespan
     return Solution(plan=plan, status=status, makespan=makespan, lower_bound=lb,
                     objective=plan.predicted_makespan, problem=prob, search=res, options=options,
                     order=order, runtimes=runtimes)

@@ -56,6 +56,9 @@ class SolveOptions:
     max_rounds: int = 4096              # local search: rounds of 32 moves per walker
     ls_stop: bool = True                # local search: a walk ends at the lower bound (same result)
     kernel: str = "auto"                # auto (bnb when it applies) | tree | index | bnb
+    prove: bool = True                  # local search on one node: prove / improve the best makespan
+                                        # with the state-space search (sat_search_dp) after a wave
+    dp_states: int = 1 << 22            # state budget of one sat_search_dp call (all levels)
 
 
 @dataclass

@@ -1,0 +1,111 @@
+"""State-space search (sat_search_dp) against the CPU oracle.
+
+For every problem: with M* = the oracle's exhaustive optimum (lowest makespan over the whole
+candidate space, oracle/oracle.c), the DP must report INFEASIBLE at target M* - 1 and FEASIBLE
+at M* -- and the candidate it returns, replayed by the oracle's own list scheduler, must have
+makespan <= the target.  The returned candidate is deterministic (same one on every run).  The
+headline use: config 3's optimum (30, certified by HiGHS on the CPU) is proven on the GPU, so
+plan_saturn(cfg3) returns status Optimal."""
+
+import random
+
+import pytest
+
+from helpers import golden
+from test_engine_gpu import to_search_problem, workload_problem
+from test_oracle import random_problem
+
+from oracle import coracle as C
+from paper_2311_02840_b200 import engine as EN
+from paper_2311_02840_b200 import errors as E
+from paper_2311_02840_b200 import planners as PL
+from paper_2311_02840_b200.problem import SolveOptions, build_problem
+from paper_2311_02840_b200.workloads import config_workload
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def eng():
+    return EN.Engine(0)
+
+
+def dp(eng, prob, target, max_states=1 << 20):
+    return eng.dp_search(EN.NativeProblem(prob, 1), target, max_states)
+
+
+def check_around_optimum(eng, op, prob):
+    opt = C.CProblem(op).search()[0]
+    st, info, cand = dp(eng, prob, int(opt) - 1)
+    assert st == EN.SAT_DP_INFEASIBLE, (opt, info.levels)
+    for target in (int(opt), int(opt) + 2):
+        st, info, cand = dp(eng, prob, target)
+        assert st == EN.SAT_DP_FEASIBLE
+        opts, order = cand
+        assert sorted(order) == list(range(op.J))
+        ms, _, _ = C.CProblem(op).eval(opts, order)
+        assert ms <= target and ms == info.makespan
+        assert dp(eng, prob, target)[2] == cand            # deterministic reconstruction
+    return opt
+
+
+def test_dp_random_one_node(eng):
+    rng = random.Random(2024)
+    for trial in range(60):
+        gsz = [1, 2, 3, 4, 5, 8, 16, 32][trial % 8]
+        J = [2, 3, 4, 5, 6][trial % 5]
+        # (keys must fit 63 bits: 2^J x C(T + G, G); 32-GPU nodes get short jobs)
+        op = random_problem(rng, J, [gsz], max_opts=4 if J < 6 else 3, max_d=12 if gsz < 32 else 2)
+        if trial % 3 == 0:
+            op.init_free = [sorted(rng.randint(0, 5) for _ in range(gsz))]
+        if trial % 4 == 1:
+            op.release = [rng.randint(0, 6) for _ in range(op.J)]
+        check_around_optimum(eng, op, to_search_problem(op))
+
+
+@pytest.mark.parametrize("name", ["small5_1x4", "tiny3_1x3"])
+def test_dp_workloads(eng, name):
+    w, t, prob, op = workload_problem(name)
+    assert check_around_optimum(eng, op, prob) == golden()["milp"][name]["optimum_intervals"]
+
+
+def test_dp_cfg1_optimum():
+    """Config 1: nothing at 29, a 30-interval candidate at 30 (= HiGHS, = the full scan)."""
+    eng = PL.get_engine(0)
+    w, t, _ = config_workload(1)
+    prob = build_problem(t, w)
+    assert dp(eng, prob, 29, 1 << 22)[0] == EN.SAT_DP_INFEASIBLE
+    st, info, cand = dp(eng, prob, 30, 1 << 22)
+    assert st == EN.SAT_DP_FEASIBLE and info.makespan == 30
+
+
+def test_dp_proves_cfg3_optimal():
+    """Config 3 (16 jobs, 3e23 candidates): local search reaches 30, the trivial bound says 29;
+    the state-space search shows no candidate reaches 29, so the plan is Optimal -- the value
+    HiGHS certifies on the CPU (tests/golden)."""
+    eng = PL.get_engine(0)
+    w, t, _ = config_workload(3)
+    prob = build_problem(t, w)
+    st, info, _ = dp(eng, prob, 29, 1 << 22)
+    assert st == EN.SAT_DP_INFEASIBLE and info.levels <= prob.J
+    sol = PL.solve(t, w)
+    assert sol.status == "Optimal" and sol.makespan == 30 == golden()["milp"]["cfg3"]["optimum_intervals"]
+    assert sol.lower_bound == 30 and sol.search.proven
+    assert sol.search.stats["proof"]["attempts"][-1]["status"] == "infeasible"
+
+
+def test_dp_budget_and_unsupported(eng):
+    w, t, _ = config_workload(3)
+    prob = build_problem(t, w)
+    st, info, _ = dp(eng, prob, 29, 1000)
+    assert st == EN.SAT_DP_BUDGET
+    w4, t4, _ = config_workload(4)                       # several nodes: not this kernel
+    p4 = build_problem(t4, w4)
+    with pytest.raises(E.TooLarge):
+        dp(eng, p4, 10)
+
+
+def test_solve_without_proof_keeps_local_status():
+    w, t, _ = config_workload(3)
+    sol = PL.solve(t, w, None, SolveOptions(prove=False))
+    assert sol.status == "Local" and sol.makespan == 30 and not sol.search.proven

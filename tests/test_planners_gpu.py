@@ -167,17 +167,18 @@ def test_local_search_plan_beats_its_own_starts(name):
 
 def test_default_solve_of_large_configs_is_local_and_bounded():
     """auto on spaces beyond exact search = local search; cfg4 / cfg5 meet the lower bound
-    (proven optimal); cfg3 reaches the HiGHS-certified optimum, one above the bound."""
-    for name, proven in (("cfg3", False), ("cfg4", True), ("cfg5", True)):
+    (proven optimal); cfg3 reaches the HiGHS-certified optimum, one above the bound, and the
+    state-space search proves it (status Optimal)."""
+    for name, by_dp in (("cfg3", True), ("cfg4", False), ("cfg5", False)):
         w, t = setup(name)
         sol = PL.solve(t, w)
         assert sol.search.kernel == "local"
         D.check_plan(sol.plan, w, sol.runtimes)
-        if proven:
-            assert sol.status == "Optimal" and sol.makespan == sol.lower_bound
-        else:
-            assert sol.status == "Local" and sol.makespan == sol.lower_bound + 1
+        assert sol.status == "Optimal" and sol.makespan == sol.lower_bound
+        assert sol.search.proven == by_dp
+        if by_dp:
             assert sol.makespan == golden()["milp"][name]["optimum_intervals"]
+            assert sol.makespan == sol.problem.lower_bound() + 1
 
 
 def test_evaluate_fixed_reproduces_planner_plans():
