@@ -84,8 +84,17 @@ __host__ __device__ constexpr int cache_state_words(int N) {
     return (L == kLayoutOne16 || L == kLayoutMulti16) ? N * (G / 2) : N * G;
 }
 
-template <typename T, int G, int L, bool LOAD = false>
-__device__ __forceinline__ T schedule_records(const SchedCtx<T> &c, const uint32_t *rec,
+// Record providers: schedule_records reads the record of position k through `rec(k)`.
+//   RecCol   -- the lane's materialised record column (k_cand: decoded candidates);
+//   RecMove  -- k_ls: the walker's current records (one shared copy per walker) seen through
+//               a move, computed per position (no per-move record column to build or hold).
+struct RecCol {
+    const uint32_t *p;                           // lane's column, stride 32
+    __device__ __forceinline__ uint32_t operator()(int k) const { return p[k * 32]; }
+};
+
+template <typename T, int G, int L, bool LOAD = false, typename RecF = RecCol>
+__device__ __forceinline__ T schedule_records(const SchedCtx<T> &c, const RecF rec,
                                              uint64_t *load = nullptr, int k0 = 0,
                                              const uint32_t *cin = nullptr, uint32_t *cout = nullptr,
                                              bool writer = false) {
@@ -120,7 +129,7 @@ __device__ __forceinline__ T schedule_records(const SchedCtx<T> &c, const uint32
         }
         if (wr) cout[SW] = (uint32_t)(int32_t)mx;
         for (int kk = k0; kk < J; ++kk) {
-            const uint32_t r = rec[kk * 32];
+            const uint32_t r = rec(kk);
             const int g = (int)(r & 63u) + 1;
             SAT_ASSERT(g >= 1 && g <= G && (int)((r >> 6) & 63u) < J);
             SAT_ASSERT(rec_d || (int)(r >> 12) < c.n_opt);
@@ -168,7 +177,7 @@ __device__ __forceinline__ T schedule_records(const SchedCtx<T> &c, const uint32
         }
         if (wr) cout[SW] = (uint32_t)(int32_t)mx;
         for (int kk = k0; kk < J; ++kk) {
-            const uint32_t r = rec[kk * 32];
+            const uint32_t r = rec(kk);
             const int g = (int)(r & 63u) + 1;
             SAT_ASSERT(g >= 1 && g <= G && (int)((r >> 6) & 63u) < J);
             SAT_ASSERT(rec_d || (int)(r >> 12) < c.n_opt);
@@ -214,7 +223,7 @@ __device__ __forceinline__ T schedule_records(const SchedCtx<T> &c, const uint32
                 }
         if (wr) cout[SW] = (uint32_t)(int32_t)mx;
         for (int kk = k0; kk < J; ++kk) {
-            const uint32_t r = rec[kk * 32];
+            const uint32_t r = rec(kk);
             const int g = (int)(r & 63u) + 1;
             SAT_ASSERT(g >= 1 && g <= G && (int)((r >> 6) & 63u) < J);
             SAT_ASSERT(rec_d || (int)(r >> 12) < c.n_opt);
@@ -280,7 +289,7 @@ __device__ __forceinline__ T schedule_records(const SchedCtx<T> &c, const uint32
                 }
         if (wr) cout[SW] = (uint32_t)(int32_t)mx;
         for (int kk = k0; kk < J; ++kk) {
-            const uint32_t r = rec[kk * 32];
+            const uint32_t r = rec(kk);
             const int g = (int)(r & 63u) + 1;
             SAT_ASSERT(g >= 1 && g <= G && (int)((r >> 6) & 63u) < J);
             SAT_ASSERT(rec_d || (int)(r >> 12) < c.n_opt);
@@ -374,8 +383,8 @@ __device__ __forceinline__ void place16_reg(uint32_t (&av)[G / 2], int32_t rel, 
 // move leaves in place, typically most of them -- the placement runs on registers with a
 // compile-time shift (one uniform branch); otherwise the generic shared-memory shift of
 // schedule_records.  Same arithmetic, same result.
-template <int G>
-__device__ __forceinline__ int32_t schedule_eval16(const SchedCtx<int32_t> &c, const uint32_t *rec, uint64_t *load,
+template <int G, typename RecF>
+__device__ __forceinline__ int32_t schedule_eval16(const SchedCtx<int32_t> &c, const RecF rec, uint64_t *load,
                                                    int k0, const uint32_t *cin) {
     constexpr int W = G / 2;
     const int J = c.J;
@@ -397,7 +406,7 @@ __device__ __forceinline__ int32_t schedule_eval16(const SchedCtx<int32_t> &c, c
                                                           ((uint32_t)(uint16_t)c.lane_init[2 * w + 1] << 16);
             mx = cin ? (int32_t)cin[k0 * CW + SW] : (int32_t)c.init_max;
         }
-        const uint32_t r = on ? rec[kk * 32] : 0u;
+        const uint32_t r = on ? rec(kk) : 0u;
         const int g = (int)(r & 63u) + 1;
         SAT_ASSERT(!on || (g >= 1 && g <= G && (int)((r >> 6) & 63u) < J));
         const unsigned onm = __ballot_sync(act, on);
@@ -534,7 +543,7 @@ k_cand(CandArgs a) {
             } else {
                 decode_stream(a.seed + id, tb, rec);
             }
-            const T mx = schedule_records<T, G, L>(sc, rec);
+            const T mx = schedule_records<T, G, L>(sc, RecCol{rec});
             if (key_less(mx, id, best_ms, best_ix)) {
                 best_ms = mx;
                 best_ix = id;
@@ -593,15 +602,19 @@ struct LsArgs {
     uint8_t *state_out;         // [hi - lo][2J] final options then order of every walker (abandoned: untouched), or null
 };
 
-// bytes of one block's region: every warp's records / free-time columns, then the walker's
-// options / order / job positions (3 x 64 bytes) and its prefix cache
+// bytes of one block's region: every warp's free-time columns (a move's records are computed
+// per position from the walker's, no per-warp record column), then per walker its options /
+// order / job positions (3 x 64 bytes), its current records (64 words) and its prefix cache
 __host__ __device__ inline int ls_walker_bytes(int J, int cache_state_words) {
-    return 192 + (J + 1) * (cache_state_words + 1) * 4;
+    return 192 + 256 + (J + 1) * (cache_state_words + 1) * 4;
+}
+__host__ __device__ inline int ls_warp_bytes(int J, int N, int G, int slot_bytes) {
+    return cand_warp_bytes(J, N, G, slot_bytes, false) - J * 128;
 }
 // warps per k_ls block: 4, or 8 when one walker takes 8 warps
 __host__ __device__ constexpr int ls_block_warps(int K) { return K > kCandWarps ? K : kCandWarps; }
 __host__ __device__ inline int ls_block_bytes(int J, int N, int G, int slot_bytes, int cache_state_words, int K) {
-    return ls_block_warps(K) * cand_warp_bytes(J, N, G, slot_bytes, false) +
+    return ls_block_warps(K) * ls_warp_bytes(J, N, G, slot_bytes) +
            (ls_block_warps(K) / K) * ls_walker_bytes(J, cache_state_words);
 }
 
@@ -637,6 +650,23 @@ __device__ __forceinline__ int ls_src(const LsMove &mv, int k) {
     return (k < mv.b || k > mv.a) ? k : (k == mv.b ? mv.a : k - 1);
 }
 
+// the neighbour's record at position k: the walker's record at the source position, or (option
+// move) the moved job's record with its new option at the job's own position
+struct RecMove {
+    const uint32_t *crec;                        // walker's current records [J] (shared by its warps)
+    LsMove mv;
+    int spk;                                     // option move: the job's position (-1: none)
+    uint32_t sprec;
+    __device__ __forceinline__ uint32_t operator()(int k) const {
+        return k == spk ? sprec : crec[ls_src(mv, k)];
+    }
+};
+
+struct RecWalker {
+    const uint32_t *crec;
+    __device__ __forceinline__ uint32_t operator()(int k) const { return crec[k]; }
+};
+
 // One walker per group of K = group_warps warps (K = 1: a walker per warp; K = kCandWarps: a
 // walker per block).  The group's warps evaluate consecutive rounds of the current scan at
 // once (warp w of the group: round q + w); the first of them, in scan order, holding an
@@ -670,15 +700,15 @@ k_ls(LsArgs a) {
     const int grp = warp / K, gw = warp - grp * K;                 // walker group, warp within it
     const bool leader = gw == 0 && lane == 0;
     const int SW = cache_state_words<G, L>(N);
-    const int wbytes = cand_warp_bytes(J, N, G, cand_slot_bytes<T, L>(), false);
+    const int wbytes = ls_warp_bytes(J, N, G, cand_slot_bytes<T, L>());
     uint8_t *wbase = smem + h.bytes + warp * wbytes;
-    uint32_t *rec = reinterpret_cast<uint32_t *>(wbase) + lane;
-    T *st = reinterpret_cast<T *>(wbase + J * 128) + lane;
+    T *st = reinterpret_cast<T *>(wbase) + lane;
     uint32_t *st16 = reinterpret_cast<uint32_t *>(st);
     uint8_t *wopt = smem + h.bytes + BW * wbytes + grp * ls_walker_bytes(J, SW);   // [64] walker state
     uint8_t *word = wopt + 64;                                                           // [64]
     uint8_t *wpos = word + 64;                                                           // [64] job -> position
-    uint32_t *cache = reinterpret_cast<uint32_t *>(wpos + 64);                          // [J + 1][SW + 1]
+    uint32_t *crec = reinterpret_cast<uint32_t *>(wpos + 64);                           // [64] records by position
+    uint32_t *cache = crec + 64;                                                         // [J + 1][SW + 1]
     __shared__ uint64_t s_key[BW];                     // per warp: its round's best (objective, move)
     __shared__ int s_move[BW];
     __shared__ unsigned long long s_walker[BW];        // per group
@@ -728,11 +758,15 @@ k_ls(LsArgs a) {
             for (int k = 0; k < J; ++k) wpos[word[k]] = (uint8_t)k;
         }
         gsync();
+        if (gw == 0) {
+            for (int k = lane; k < J; k += 32) { const int job = word[k]; crec[k] = rec_for(tb, job, wopt[job]); }
+            __syncwarp();
+        }
+        gsync();
         if (gw == 0) {             // objective of the start; lane 0 fills the prefix cache
-            for (int k = 0; k < J; ++k) { const int job = word[k]; rec[k * 32] = rec_for(tb, job, wopt[job]); }
             uint64_t load = 0;
-            const T c0 = schedule_records<T, G, L, true>(sc, rec, &load, 0, nullptr, use_cache ? cache : nullptr,
-                                                        lane == 0);
+            const T c0 = schedule_records<T, G, L, true>(sc, RecWalker{crec}, &load, 0, nullptr,
+                                                        use_cache ? cache : nullptr, lane == 0);
             if (lane == 0) s_cur_key[grp] = ((uint64_t)(uint32_t)c0 << 34) | load;
         }
         gsync();
@@ -769,12 +803,9 @@ k_ls(LsArgs a) {
                         const LsMove mv = ls_decode_move(m, J, M1, M2, tb.radix, wopt);
                         // positions before the first changed one schedule exactly as the current
                         // candidate: resume from the prefix cache there
-                        const int k0 = !use_cache ? 0 : (mv.kind == 1 ? (int)wpos[mv.a] : min(mv.a, mv.b));
-                        for (int k = k0; k < J; ++k) {
-                            const int job = word[ls_src(mv, k)];
-                            const int o = (mv.kind == 1 && job == mv.a) ? mv.b : (int)wopt[job];
-                            rec[k * 32] = rec_for(tb, job, o);
-                        }
+                        const int kpos = mv.kind == 1 ? (int)wpos[mv.a] : -1;
+                        const int k0 = !use_cache ? 0 : (mv.kind == 1 ? kpos : min(mv.a, mv.b));
+                        const RecMove rec{crec, mv, kpos, mv.kind == 1 ? rec_for(tb, mv.a, mv.b) : 0u};
                         uint64_t ld = 0;
                         T ms;
                         // register shifts pay off on wide nodes (G = 32: ~110 instructions per
@@ -830,9 +861,11 @@ k_ls(LsArgs a) {
                         for (int k = 0; k < J; ++k) wpos[word[k]] = (uint8_t)k;
                     }
                     gsync();
-                    if (use_cache && gw == 0) {     // refresh the prefix cache for the new current candidate
-                        for (int k = 0; k < J; ++k) { const int job = word[k]; rec[k * 32] = rec_for(tb, job, wopt[job]); }
-                        schedule_records<T, G, L, false>(sc, rec, nullptr, 0, nullptr, cache, lane == 0);
+                    if (gw == 0) {                  // the new current candidate's records (and prefix cache)
+                        for (int k = lane; k < J; k += 32) { const int job = word[k]; crec[k] = rec_for(tb, job, wopt[job]); }
+                        __syncwarp();
+                        if (use_cache)
+                            schedule_records<T, G, L, false>(sc, RecWalker{crec}, nullptr, 0, nullptr, cache, lane == 0);
                     }
                     gsync();
                     cur_key = nk;
