@@ -675,7 +675,7 @@ struct RecWalker {
 // that), in ~1/K of the sequential steps when scans are long (the critical path of a wave is
 // its longest walk); K = 1 keeps the most walkers in flight when throughput matters.
 template <int SRC, int G, int L, int K>
-__global__ void __launch_bounds__(ls_block_warps(K) * 32)
+__global__ void __launch_bounds__(ls_block_warps(K) * 32, K == 8 ? 4 : 1)
 k_ls(LsArgs a) {
     using T = int32_t;
     static_assert(K == 1 || K == 2 || K == kCandWarps || K == 8, "warps per walker");
@@ -714,6 +714,7 @@ k_ls(LsArgs a) {
     __shared__ unsigned long long s_walker[BW];        // per group
     __shared__ uint64_t s_cur_key[BW];
     __shared__ int s_beaten[BW];
+    __shared__ uint64_t s_mkey[K > 1 ? BW * 32 : 1];   // K > 1: objective of every move of a step
     uint64_t *g_key = s_key + grp * K;
     int *g_move = s_move + grp * K;
     // group barrier: the warp itself (K = 1) or a named barrier over the group's K warps
@@ -792,34 +793,47 @@ k_ls(LsArgs a) {
                 if (beaten) { abandoned = true; break; }
             }
             bool improved = false;
-            for (int q = 0;; q += K) {      // rounds q .. q+K-1 of this scan, one per warp
-                const int r0 = (q + gw) * 32;
-                const bool valid = r0 < M && rounds + gw < a.max_rounds;
-                uint64_t bk = ~0ull;
-                int bm = 0x7fffffff;
+            for (int q = 0;; q += K) {      // rounds q .. q+K-1 of this scan
+                // a move's cost grows with how early it changes the order (it resumes there), and
+                // neighbouring moves change the same positions: the group's warps take chunks of 8
+                // consecutive moves in turn (warp gw: chunks gw, gw + K, ...) so every warp gets a
+                // share of each round of the step and reaches the barrier at about the same time;
+                // warp gw then reduces round q + gw from the shared results.  K = 1: lane = move.
+                const int mloc = ((lane >> 3) * K + gw) * 8 + (lane & 7);
+                const int m = q * 32 + mloc;
+                const int rl = mloc >> 5;
+                const bool lvalid = m < M && rounds + rl < a.max_rounds;
+                uint64_t lk = ~0ull;
+                if (lvalid) {
+                    const LsMove mv = ls_decode_move(m, J, M1, M2, tb.radix, wopt);
+                    // positions before the first changed one schedule exactly as the current
+                    // candidate: resume from the prefix cache there
+                    const int kpos = mv.kind == 1 ? (int)wpos[mv.a] : -1;
+                    const int k0 = !use_cache ? 0 : (mv.kind == 1 ? kpos : min(mv.a, mv.b));
+                    const RecMove rec{crec, mv, kpos, mv.kind == 1 ? rec_for(tb, mv.a, mv.b) : 0u};
+                    uint64_t ld = 0;
+                    T ms;
+                    // register shifts pay off on wide nodes (G = 32: ~110 instructions per
+                    // shared-memory placement) in the 8-warp walker (cfg5 13.2 -> 11.7 ms); with
+                    // 1 or 4 warps per walker, or at G = 8, the warp votes cost more than they save
+                    // (profiles/r01g_ls_group_sweep.txt)
+                    if constexpr (L == kLayoutOne16 && G >= 16 && K == 8)
+                        ms = schedule_eval16<G>(sc, rec, &ld, k0, use_cache ? cache : nullptr);
+                    else
+                        ms = schedule_records<T, G, L, true>(sc, rec, &ld, k0, use_cache ? cache : nullptr);
+                    lk = ((uint64_t)(uint32_t)ms << 34) | ld;
+                }
+                const bool valid = (q + gw) * 32 < M && rounds + gw < a.max_rounds;
+                uint64_t bk = lk;
+                int bm = lk != ~0ull ? m : 0x7fffffff;
+                if constexpr (K > 1) {
+                    s_mkey[grp * K * 32 + mloc] = lk;
+                    gsync();
+                    bk = s_mkey[grp * K * 32 + gw * 32 + lane];
+                    bm = bk != ~0ull ? q * 32 + gw * 32 + lane : 0x7fffffff;
+                }
                 if (valid) {
-                    const int m = r0 + lane;
-                    if (m < M) {
-                        const LsMove mv = ls_decode_move(m, J, M1, M2, tb.radix, wopt);
-                        // positions before the first changed one schedule exactly as the current
-                        // candidate: resume from the prefix cache there
-                        const int kpos = mv.kind == 1 ? (int)wpos[mv.a] : -1;
-                        const int k0 = !use_cache ? 0 : (mv.kind == 1 ? kpos : min(mv.a, mv.b));
-                        const RecMove rec{crec, mv, kpos, mv.kind == 1 ? rec_for(tb, mv.a, mv.b) : 0u};
-                        uint64_t ld = 0;
-                        T ms;
-                        // register shifts pay off on wide nodes (G = 32: ~110 instructions per
-                        // shared-memory placement) in the 8-warp walker (cfg5 13.2 -> 11.7 ms); with
-                        // 1 or 4 warps per walker, or at G = 8, the warp votes cost more than they save
-                        // (profiles/r01g_ls_group_sweep.txt)
-                        if constexpr (L == kLayoutOne16 && G >= 16 && K == 8)
-                            ms = schedule_eval16<G>(sc, rec, &ld, k0, use_cache ? cache : nullptr);
-                        else
-                            ms = schedule_records<T, G, L, true>(sc, rec, &ld, k0, use_cache ? cache : nullptr);
-                        bk = ((uint64_t)(uint32_t)ms << 34) | ld;
-                        bm = m;
-                    }
-                    // warp argmin of (objective, move id)
+                    // warp argmin of (objective, move id) over round q + gw
                     for (int x = 16; x >= 1; x >>= 1) {
                         const uint64_t ok = shfl_u64(bk, lane ^ x);
                         const int om = __shfl_xor_sync(0xffffffffu, bm, x);
