@@ -125,9 +125,9 @@ __device__ __forceinline__ T schedule_records(const SchedCtx<T> &c, const RecF r
             av[w] = cin ? cin[k0 * CW + w]
                         : (uint32_t)(uint16_t)lane_init[2 * w] | ((uint32_t)(uint16_t)lane_init[2 * w + 1] << 16);
             st16[w * 32] = av[w];
-            if (wr) cout[w] = av[w];
+            if (wr) cout[k0 * CW + w] = av[w];
         }
-        if (wr) cout[SW] = (uint32_t)(int32_t)mx;
+        if (wr) cout[k0 * CW + SW] = (uint32_t)(int32_t)mx;
         for (int kk = k0; kk < J; ++kk) {
             const uint32_t r = rec(kk);
             const int g = (int)(r & 63u) + 1;
@@ -173,9 +173,9 @@ __device__ __forceinline__ T schedule_records(const SchedCtx<T> &c, const RecF r
         for (int i = 0; i < G; ++i) {
             av[i] = cin ? (T)(int32_t)cin[k0 * CW + i] : lane_init[i];
             st[i * 32] = av[i];
-            if (wr) cout[i] = (uint32_t)(int32_t)av[i];
+            if (wr) cout[k0 * CW + i] = (uint32_t)(int32_t)av[i];
         }
-        if (wr) cout[SW] = (uint32_t)(int32_t)mx;
+        if (wr) cout[k0 * CW + SW] = (uint32_t)(int32_t)mx;
         for (int kk = k0; kk < J; ++kk) {
             const uint32_t r = rec(kk);
             const int g = (int)(r & 63u) + 1;
@@ -219,9 +219,9 @@ __device__ __forceinline__ T schedule_records(const SchedCtx<T> &c, const RecF r
                                            : (uint32_t)(uint16_t)lane_init[n * G + 2 * w] |
                                                  ((uint32_t)(uint16_t)lane_init[n * G + 2 * w + 1] << 16);
                     st16[(n * G + w) * 32] = v;
-                    if (wr) cout[n * (G / 2) + w] = v;
+                    if (wr) cout[k0 * CW + n * (G / 2) + w] = v;
                 }
-        if (wr) cout[SW] = (uint32_t)(int32_t)mx;
+        if (wr) cout[k0 * CW + SW] = (uint32_t)(int32_t)mx;
         for (int kk = k0; kk < J; ++kk) {
             const uint32_t r = rec(kk);
             const int g = (int)(r & 63u) + 1;
@@ -285,9 +285,9 @@ __device__ __forceinline__ T schedule_records(const SchedCtx<T> &c, const RecF r
                 for (int i = 0; i < G; ++i) {
                     const T v = cin ? (T)(int32_t)cin[k0 * CW + n * G + i] : lane_init[n * G + i];
                     st[(n * 2 * G + i) * 32] = v;
-                    if (wr) cout[n * G + i] = (uint32_t)(int32_t)v;
+                    if (wr) cout[k0 * CW + n * G + i] = (uint32_t)(int32_t)v;
                 }
-        if (wr) cout[SW] = (uint32_t)(int32_t)mx;
+        if (wr) cout[k0 * CW + SW] = (uint32_t)(int32_t)mx;
         for (int kk = k0; kk < J; ++kk) {
             const uint32_t r = rec(kk);
             const int g = (int)(r & 63u) + 1;
@@ -714,7 +714,6 @@ k_ls(LsArgs a) {
     __shared__ unsigned long long s_walker[BW];        // per group
     __shared__ uint64_t s_cur_key[BW];
     __shared__ int s_beaten[BW];
-    __shared__ uint64_t s_mkey[K > 1 ? BW * 32 : 1];   // K > 1: objective of every move of a step
     uint64_t *g_key = s_key + grp * K;
     int *g_move = s_move + grp * K;
     // group barrier: the warp itself (K = 1) or a named barrier over the group's K warps
@@ -781,59 +780,35 @@ k_ls(LsArgs a) {
         bool abandoned = false;
         for (;;) {
             if (cur <= a.stop_ms) break;
-            if (a.stop_ms >= 0) {
-                if (leader) {
-                    const unsigned long long k = *reinterpret_cast<volatile unsigned long long *>(&a.best->hi);
-                    s_beaten[grp] = k != ~0ull && (int64_t)(k >> a.idx_bits) <= (int64_t)a.stop_ms &&
-                                    (k & ((1ull << a.idx_bits) - 1ull)) < id;
-                }
-                gsync();
-                const bool beaten = s_beaten[grp] != 0;
-                gsync();
-                if (beaten) { abandoned = true; break; }
-            }
             bool improved = false;
-            for (int q = 0;; q += K) {      // rounds q .. q+K-1 of this scan
-                // a move's cost grows with how early it changes the order (it resumes there), and
-                // neighbouring moves change the same positions: the group's warps take chunks of 8
-                // consecutive moves in turn (warp gw: chunks gw, gw + K, ...) so every warp gets a
-                // share of each round of the step and reaches the barrier at about the same time;
-                // warp gw then reduces round q + gw from the shared results.  K = 1: lane = move.
-                const int mloc = ((lane >> 3) * K + gw) * 8 + (lane & 7);
-                const int m = q * 32 + mloc;
-                const int rl = mloc >> 5;
-                const bool lvalid = m < M && rounds + rl < a.max_rounds;
-                uint64_t lk = ~0ull;
-                if (lvalid) {
-                    const LsMove mv = ls_decode_move(m, J, M1, M2, tb.radix, wopt);
-                    // positions before the first changed one schedule exactly as the current
-                    // candidate: resume from the prefix cache there
-                    const int kpos = mv.kind == 1 ? (int)wpos[mv.a] : -1;
-                    const int k0 = !use_cache ? 0 : (mv.kind == 1 ? kpos : min(mv.a, mv.b));
-                    const RecMove rec{crec, mv, kpos, mv.kind == 1 ? rec_for(tb, mv.a, mv.b) : 0u};
-                    uint64_t ld = 0;
-                    T ms;
-                    // register shifts pay off on wide nodes (G = 32: ~110 instructions per
-                    // shared-memory placement) in the 8-warp walker (cfg5 13.2 -> 11.7 ms); with
-                    // 1 or 4 warps per walker, or at G = 8, the warp votes cost more than they save
-                    // (profiles/r01g_ls_group_sweep.txt)
-                    if constexpr (L == kLayoutOne16 && G >= 16 && K == 8)
-                        ms = schedule_eval16<G>(sc, rec, &ld, k0, use_cache ? cache : nullptr);
-                    else
-                        ms = schedule_records<T, G, L, true>(sc, rec, &ld, k0, use_cache ? cache : nullptr);
-                    lk = ((uint64_t)(uint32_t)ms << 34) | ld;
-                }
-                const bool valid = (q + gw) * 32 < M && rounds + gw < a.max_rounds;
-                uint64_t bk = lk;
-                int bm = lk != ~0ull ? m : 0x7fffffff;
-                if constexpr (K > 1) {
-                    s_mkey[grp * K * 32 + mloc] = lk;
-                    gsync();
-                    bk = s_mkey[grp * K * 32 + gw * 32 + lane];
-                    bm = bk != ~0ull ? q * 32 + gw * 32 + lane : 0x7fffffff;
-                }
+            for (int q = 0;; q += K) {      // rounds q .. q+K-1 of this scan, one per warp
+                const int r0 = (q + gw) * 32;
+                const bool valid = r0 < M && rounds + gw < a.max_rounds;
+                uint64_t bk = ~0ull;
+                int bm = 0x7fffffff;
                 if (valid) {
-                    // warp argmin of (objective, move id) over round q + gw
+                    const int m = r0 + lane;
+                    if (m < M) {
+                        const LsMove mv = ls_decode_move(m, J, M1, M2, tb.radix, wopt);
+                        // positions before the first changed one schedule exactly as the current
+                        // candidate: resume from the prefix cache there
+                        const int kpos = mv.kind == 1 ? (int)wpos[mv.a] : -1;
+                        const int k0 = !use_cache ? 0 : (mv.kind == 1 ? kpos : min(mv.a, mv.b));
+                        const RecMove rec{crec, mv, kpos, mv.kind == 1 ? rec_for(tb, mv.a, mv.b) : 0u};
+                        uint64_t ld = 0;
+                        T ms;
+                        // register shifts pay off on wide nodes (G = 32: ~110 instructions per
+                        // shared-memory placement) in the 8-warp walker (cfg5 13.2 -> 11.7 ms); with
+                        // 1 or 4 warps per walker, or at G = 8, the warp votes cost more than they save
+                        // (profiles/r01g_ls_group_sweep.txt)
+                        if constexpr (L == kLayoutOne16 && G >= 16 && K == 8)
+                            ms = schedule_eval16<G>(sc, rec, &ld, k0, use_cache ? cache : nullptr);
+                        else
+                            ms = schedule_records<T, G, L, true>(sc, rec, &ld, k0, use_cache ? cache : nullptr);
+                        bk = ((uint64_t)(uint32_t)ms << 34) | ld;
+                        bm = m;
+                    }
+                    // warp argmin of (objective, move id)
                     for (int x = 16; x >= 1; x >>= 1) {
                         const uint64_t ok = shfl_u64(bk, lane ^ x);
                         const int om = __shfl_xor_sync(0xffffffffu, bm, x);
@@ -859,9 +834,22 @@ k_ls(LsArgs a) {
                     if (first >= 0) { nk = g_key[first]; nm = g_move[first]; }
                 }
                 if (first >= 0) {
+                    // positions before the first one the move changes keep their records and
+                    // their prefix-cache entries (decoded before the leader rewrites the walker)
+                    const LsMove amv = ls_decode_move(nm, J, M1, M2, tb.radix, wopt);
+                    const int kc = amv.kind == 1 ? (int)wpos[amv.a] : min(amv.a, amv.b);
                     gsync();                          // every thread has read the slots
                     if (leader) {
-                        const LsMove mv = ls_decode_move(nm, J, M1, M2, tb.radix, wopt);
+                        const LsMove &mv = amv;
+                        // a walker whose id is above a published key at <= stop_ms cannot win:
+                        // it is abandoned (checked once per applied move)
+                        if (a.stop_ms >= 0) {
+                            const unsigned long long k = *reinterpret_cast<volatile unsigned long long *>(&a.best->hi);
+                            s_beaten[grp] = k != ~0ull && (int64_t)(k >> a.idx_bits) <= (int64_t)a.stop_ms &&
+                                            (k & ((1ull << a.idx_bits) - 1ull)) < id;
+                        } else {
+                            s_beaten[grp] = 0;
+                        }
                         if (mv.kind == 0) {
                             const uint8_t t = word[mv.a]; word[mv.a] = word[mv.b]; word[mv.b] = t;
                         } else if (mv.kind == 1) {
@@ -876,12 +864,13 @@ k_ls(LsArgs a) {
                     }
                     gsync();
                     if (gw == 0) {                  // the new current candidate's records (and prefix cache)
-                        for (int k = lane; k < J; k += 32) { const int job = word[k]; crec[k] = rec_for(tb, job, wopt[job]); }
+                        for (int k = kc + lane; k < J; k += 32) { const int job = word[k]; crec[k] = rec_for(tb, job, wopt[job]); }
                         __syncwarp();
                         if (use_cache)
-                            schedule_records<T, G, L, false>(sc, RecWalker{crec}, nullptr, 0, nullptr, cache, lane == 0);
+                            schedule_records<T, G, L, false>(sc, RecWalker{crec}, nullptr, kc, cache, cache, lane == 0);
                     }
                     gsync();
+                    if (s_beaten[grp]) { abandoned = true; break; }
                     cur_key = nk;
                     cur = (T)(nk >> 34);
                     rounds += first + 1;
