@@ -93,11 +93,19 @@ struct RecCol {
     __device__ __forceinline__ uint32_t operator()(int k) const { return p[k * 32]; }
 };
 
-template <typename T, int G, int L, bool LOAD = false, typename RecF = RecCol>
+// Early exit (CUT, k_ls move evaluation): a move is only of interest if it IMPROVES the current
+// candidate's (makespan, load).  List scheduling is monotone -- a placement's new vector is
+// non-decreasing in the old one -- so the evaluation stops, returning makespan cut + 1 (an
+// objective above the current one), as soon as (a) the running makespan exceeds `cut` (the
+// current makespan), or (b) past the last position the move changes (klast) the free-time
+// state dominates the current candidate's state at the same position (cin = the walker's
+// prefix cache): every later state, the makespan and the load can then only be >= the current
+// ones.  Improving moves are scheduled to the end, so the walk is unchanged.
+template <typename T, int G, int L, bool LOAD = false, typename RecF = RecCol, bool CUT = false>
 __device__ __forceinline__ T schedule_records(const SchedCtx<T> &c, const RecF rec,
                                              uint64_t *load = nullptr, int k0 = 0,
                                              const uint32_t *cin = nullptr, uint32_t *cout = nullptr,
-                                             bool writer = false) {
+                                             bool writer = false, int cut = 0, int klast = 0) {
     constexpr bool P16 = L == kLayoutOne16;
     constexpr bool M16 = L == kLayoutMulti16;
     constexpr int NMAX = (L == kLayoutMulti || M16) ? (32 / G) : 1;
@@ -152,6 +160,22 @@ __device__ __forceinline__ T schedule_records(const SchedCtx<T> &c, const RecF r
                 st16[k * 32] = av[k];
             }
             mx = tmax(mx, (T)e);
+            if constexpr (CUT) {
+                bool worse = mx > (T)cut;
+                if (!worse && cin && kk >= klast) {
+                    uint32_t diff = 0;
+#pragma unroll
+                    for (int k = 0; k < G / 2; ++k) {
+                        const uint32_t cw = cin[(kk + 1) * CW + k];
+                        diff |= __vmaxu2(av[k], cw) ^ av[k];
+                    }
+                    worse = diff == 0;
+                }
+                if (worse) {
+                    if constexpr (LOAD) *load = 0;
+                    return (T)(cut + 1);
+                }
+            }
             if (wr) {
 #pragma unroll
                 for (int w = 0; w < G / 2; ++w) cout[(kk + 1) * CW + w] = av[w];
@@ -194,6 +218,19 @@ __device__ __forceinline__ T schedule_records(const SchedCtx<T> &c, const RecF r
                 st[i * 32] = av[i];
             }
             mx = tmax(mx, e);
+            if constexpr (CUT) {
+                bool worse = mx > (T)cut;
+                if (!worse && cin && kk >= klast) {
+                    bool dom = true;
+#pragma unroll
+                    for (int i = 0; i < G; ++i) dom &= av[i] >= (T)(int32_t)cin[(kk + 1) * CW + i];
+                    worse = dom;
+                }
+                if (worse) {
+                    if constexpr (LOAD) *load = 0;
+                    return (T)(cut + 1);
+                }
+            }
             if (wr) {
 #pragma unroll
                 for (int i = 0; i < G; ++i) cout[(kk + 1) * CW + i] = (uint32_t)(int32_t)av[i];
@@ -385,7 +422,7 @@ __device__ __forceinline__ void place16_reg(uint32_t (&av)[G / 2], int32_t rel, 
 // schedule_records.  Same arithmetic, same result.
 template <int G, typename RecF>
 __device__ __forceinline__ int32_t schedule_eval16(const SchedCtx<int32_t> &c, const RecF rec, uint64_t *load,
-                                                   int k0, const uint32_t *cin) {
+                                                   int k0, const uint32_t *cin, int cut, int klast) {
     constexpr int W = G / 2;
     const int J = c.J;
     const int SW = W, CW = SW + 1;
@@ -397,8 +434,10 @@ __device__ __forceinline__ int32_t schedule_eval16(const SchedCtx<int32_t> &c, c
     for (int w = 0; w < W; ++w) av[w] = 0u;
     int32_t mx = 0;
     bool dirty = true;                 // column st16 does not hold av
+    bool live = true;                  // false once the move is known not to improve (early exit)
     for (int kk = kmin; kk < J; ++kk) {
-        const bool on = kk >= k0;
+        if (!__any_sync(act, live)) break;
+        const bool on = kk >= k0 && live;
         if (kk == k0) {                // join: the cached state before position k0
 #pragma unroll
             for (int w = 0; w < W; ++w) av[w] = cin ? cin[k0 * CW + w]
@@ -452,6 +491,20 @@ __device__ __forceinline__ int32_t schedule_eval16(const SchedCtx<int32_t> &c, c
             }
             mx = max(mx, e);
         }
+        if (on) {                      // early exit (see schedule_records, CUT)
+            bool worse = mx > cut;
+            if (!worse && cin && kk >= klast) {
+                uint32_t diff = 0;
+#pragma unroll
+                for (int k = 0; k < W; ++k) diff |= __vmaxu2(av[k], cin[(kk + 1) * CW + k]) ^ av[k];
+                worse = diff == 0;
+            }
+            if (worse) live = false;
+        }
+    }
+    if (!live) {
+        *load = 0;
+        return cut + 1;
     }
     uint64_t sum = 0;
 #pragma unroll
@@ -675,7 +728,7 @@ struct RecWalker {
 // that), in ~1/K of the sequential steps when scans are long (the critical path of a wave is
 // its longest walk); K = 1 keeps the most walkers in flight when throughput matters.
 template <int SRC, int G, int L, int K>
-__global__ void __launch_bounds__(ls_block_warps(K) * 32, K == 8 ? 4 : 1)
+__global__ void __launch_bounds__(ls_block_warps(K) * 32, K == 8 ? 4 : 8)
 k_ls(LsArgs a) {
     using T = int32_t;
     static_assert(K == 1 || K == 2 || K == kCandWarps || K == 8, "warps per walker");
@@ -801,8 +854,14 @@ k_ls(LsArgs a) {
                         // shared-memory placement) in the 8-warp walker (cfg5 13.2 -> 11.7 ms); with
                         // 1 or 4 warps per walker, or at G = 8, the warp votes cost more than they save
                         // (profiles/r01g_ls_group_sweep.txt)
+                        // last position the move changes: past it, the records are the current
+                        // candidate's (the dominance exit applies)
+                        const int klast = mv.kind == 1 ? kpos : max(mv.a, mv.b);
                         if constexpr (L == kLayoutOne16 && G >= 16 && K == 8)
-                            ms = schedule_eval16<G>(sc, rec, &ld, k0, use_cache ? cache : nullptr);
+                            ms = schedule_eval16<G>(sc, rec, &ld, k0, use_cache ? cache : nullptr, cur, klast);
+                        else if constexpr (L == kLayoutOne16 || L == kLayoutOne)
+                            ms = schedule_records<T, G, L, true, RecMove, true>(
+                                sc, rec, &ld, k0, use_cache ? cache : nullptr, nullptr, false, cur, klast);
                         else
                             ms = schedule_records<T, G, L, true>(sc, rec, &ld, k0, use_cache ? cache : nullptr);
                         bk = ((uint64_t)(uint32_t)ms << 34) | ld;
