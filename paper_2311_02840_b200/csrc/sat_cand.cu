@@ -143,10 +143,12 @@ static int launch_ls_g(const sat_problem_t *p, LsArgs a, const std::vector<uint8
     int K = p->J >= 24 ? 8 : 1;
     if (const char *env = std::getenv("SATURN_LS_GROUP")) {
         const int k = std::atoi(env);
-        if (k == 1 || k == kCandWarps || k == 8) K = k;
+        if (k == 1 || k == kCandWarps || k == 8 || k == 16 || k == 32) K = k;
     }
     if (K == 1) return launch_ls_k<SRC, G, L, 1>(p, a, blob, d_ws, ws_bytes, stream);
     if (K == 8) return launch_ls_k<SRC, G, L, 8>(p, a, blob, d_ws, ws_bytes, stream);
+    if (K == 16) return launch_ls_k<SRC, G, L, 16>(p, a, blob, d_ws, ws_bytes, stream);
+    if (K == 32) return launch_ls_k<SRC, G, L, 32>(p, a, blob, d_ws, ws_bytes, stream);
     return launch_ls_k<SRC, G, L, kCandWarps>(p, a, blob, d_ws, ws_bytes, stream);
 }
 

@@ -101,6 +101,14 @@ struct RecCol {
 // state dominates the current candidate's state at the same position (cin = the walker's
 // prefix cache): every later state, the makespan and the load can then only be >= the current
 // ones.  Improving moves are scheduled to the end, so the walk is unchanged.
+#ifndef SAT_LS_CUT
+#define SAT_LS_CUT 1     // 0: no early exit, 1: running makespan only, 2: + dominance (measured:
+                         // cfg5 11.5 / 12.3 / 15.4 ms, cfg3 5.2 / 5.0 / 5.2 ms -- the dominance test
+                         // costs more than it saves)
+#endif
+#ifndef SAT_LS_CUT_REG
+#define SAT_LS_CUT_REG 0 // the same exits in the register-shift evaluation (schedule_eval16)
+#endif
 template <typename T, int G, int L, bool LOAD = false, typename RecF = RecCol, bool CUT = false>
 __device__ __forceinline__ T schedule_records(const SchedCtx<T> &c, const RecF rec,
                                              uint64_t *load = nullptr, int k0 = 0,
@@ -160,9 +168,9 @@ __device__ __forceinline__ T schedule_records(const SchedCtx<T> &c, const RecF r
                 st16[k * 32] = av[k];
             }
             mx = tmax(mx, (T)e);
-            if constexpr (CUT) {
+            if constexpr (CUT && SAT_LS_CUT > 0) {
                 bool worse = mx > (T)cut;
-                if (!worse && cin && kk >= klast) {
+                if (SAT_LS_CUT > 1 && !worse && cin && kk >= klast) {
                     uint32_t diff = 0;
 #pragma unroll
                     for (int k = 0; k < G / 2; ++k) {
@@ -218,9 +226,9 @@ __device__ __forceinline__ T schedule_records(const SchedCtx<T> &c, const RecF r
                 st[i * 32] = av[i];
             }
             mx = tmax(mx, e);
-            if constexpr (CUT) {
+            if constexpr (CUT && SAT_LS_CUT > 0) {
                 bool worse = mx > (T)cut;
-                if (!worse && cin && kk >= klast) {
+                if (SAT_LS_CUT > 1 && !worse && cin && kk >= klast) {
                     bool dom = true;
 #pragma unroll
                     for (int i = 0; i < G; ++i) dom &= av[i] >= (T)(int32_t)cin[(kk + 1) * CW + i];
@@ -436,7 +444,7 @@ __device__ __forceinline__ int32_t schedule_eval16(const SchedCtx<int32_t> &c, c
     bool dirty = true;                 // column st16 does not hold av
     bool live = true;                  // false once the move is known not to improve (early exit)
     for (int kk = kmin; kk < J; ++kk) {
-        if (!__any_sync(act, live)) break;
+        if (SAT_LS_CUT_REG > 0 && !__any_sync(act, live)) break;
         const bool on = kk >= k0 && live;
         if (kk == k0) {                // join: the cached state before position k0
 #pragma unroll
@@ -491,9 +499,9 @@ __device__ __forceinline__ int32_t schedule_eval16(const SchedCtx<int32_t> &c, c
             }
             mx = max(mx, e);
         }
-        if (on) {                      // early exit (see schedule_records, CUT)
+        if (SAT_LS_CUT_REG > 0 && on) {    // early exit (see schedule_records, CUT)
             bool worse = mx > cut;
-            if (!worse && cin && kk >= klast) {
+            if (SAT_LS_CUT_REG > 1 && !worse && cin && kk >= klast) {
                 uint32_t diff = 0;
 #pragma unroll
                 for (int k = 0; k < W; ++k) diff |= __vmaxu2(av[k], cin[(kk + 1) * CW + k]) ^ av[k];
@@ -728,10 +736,10 @@ struct RecWalker {
 // that), in ~1/K of the sequential steps when scans are long (the critical path of a wave is
 // its longest walk); K = 1 keeps the most walkers in flight when throughput matters.
 template <int SRC, int G, int L, int K>
-__global__ void __launch_bounds__(ls_block_warps(K) * 32, K == 8 ? 4 : 8)
+__global__ void __launch_bounds__(ls_block_warps(K) * 32, K >= 8 ? 32 / K : 8)   // <= 64 registers
 k_ls(LsArgs a) {
     using T = int32_t;
-    static_assert(K == 1 || K == 2 || K == kCandWarps || K == 8, "warps per walker");
+    static_assert(K == 1 || K == 2 || K == kCandWarps || K == 8 || K == 16 || K == 32, "warps per walker");
     constexpr int BW = ls_block_warps(K);                // warps per block
     extern __shared__ __align__(16) uint8_t smem[];
     {
@@ -857,7 +865,7 @@ k_ls(LsArgs a) {
                         // last position the move changes: past it, the records are the current
                         // candidate's (the dominance exit applies)
                         const int klast = mv.kind == 1 ? kpos : max(mv.a, mv.b);
-                        if constexpr (L == kLayoutOne16 && G >= 16 && K == 8)
+                        if constexpr (L == kLayoutOne16 && G >= 16 && K >= 8)
                             ms = schedule_eval16<G>(sc, rec, &ld, k0, use_cache ? cache : nullptr, cur, klast);
                         else if constexpr (L == kLayoutOne16 || L == kLayoutOne)
                             ms = schedule_records<T, G, L, true, RecMove, true>(
