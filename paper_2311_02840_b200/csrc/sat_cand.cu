@@ -124,7 +124,13 @@ static int launch_ls_k(const sat_problem_t *p, LsArgs a, const std::vector<uint8
     uint8_t *ws = static_cast<uint8_t *>(d_ws);
     if (cudaMemcpyAsync(ws, blob.data(), blob_bytes, cudaMemcpyHostToDevice, stream) != cudaSuccess)
         return SAT_ERR_CUDA;
-    if (cudaMemsetAsync(ws + cur_off, 0, 2 * sizeof(unsigned long long), stream) != cudaSuccess) return SAT_ERR_CUDA;
+#ifdef SAT_LS_PROFILE
+    constexpr int kCounters = 8;       // cursor, rounds, 5 profile counters
+#else
+    constexpr int kCounters = 2;       // cursor, rounds
+#endif
+    if (cudaMemsetAsync(ws + cur_off, 0, kCounters * sizeof(unsigned long long), stream) != cudaSuccess)
+        return SAT_ERR_CUDA;
     a.blob = ws;
     a.cursor = reinterpret_cast<unsigned long long *>(ws + cur_off);
     a.rounds = a.cursor + 1;
@@ -140,7 +146,7 @@ static int launch_ls_k(const sat_problem_t *p, LsArgs a, const std::vector<uint8
 template <int SRC, int G, int L>
 static int launch_ls_g(const sat_problem_t *p, LsArgs a, const std::vector<uint8_t> &blob, void *d_ws,
                        size_t ws_bytes, cudaStream_t stream) {
-    int K = p->J >= 24 ? 8 : 1;
+    int K = p->J >= 24 ? 16 : 1;
     if (const char *env = std::getenv("SATURN_LS_GROUP")) {
         const int k = std::atoi(env);
         if (k == 1 || k == kCandWarps || k == 8 || k == 16 || k == 32) K = k;

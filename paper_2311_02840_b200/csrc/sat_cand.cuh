@@ -802,6 +802,11 @@ k_ls(LsArgs a) {
     T best_ms = INF;                       // group leader: the group's best (makespan, walker)
     uint64_t best_ix = ~0ull;
     const uint64_t total = a.hi - a.lo;
+#ifdef SAT_LS_PROFILE
+    // steps, improving steps, cycles evaluating (+ barrier wait), cycles applying, sum of the
+    // improving round's position in its step -- summed over walkers (a.rounds[1..5])
+    long long prof[5] = {0, 0, 0, 0, 0};
+#endif
     for (;;) {
         if (leader) s_walker[grp] = atomicAdd(a.cursor, 1ull);
         gsync();
@@ -843,6 +848,9 @@ k_ls(LsArgs a) {
             if (cur <= a.stop_ms) break;
             bool improved = false;
             for (int q = 0;; q += K) {      // rounds q .. q+K-1 of this scan, one per warp
+#ifdef SAT_LS_PROFILE
+                const long long prof_t0 = clock64();
+#endif
                 const int r0 = (q + gw) * 32;
                 const bool valid = r0 < M && rounds + gw < a.max_rounds;
                 uint64_t bk = ~0ull;
@@ -900,6 +908,10 @@ k_ls(LsArgs a) {
                     }
                     if (first >= 0) { nk = g_key[first]; nm = g_move[first]; }
                 }
+#ifdef SAT_LS_PROFILE
+                const long long prof_t1 = clock64();
+                if (leader) { prof[0] += 1; prof[2] += prof_t1 - prof_t0; }
+#endif
                 if (first >= 0) {
                     // positions before the first one the move changes keep their records and
                     // their prefix-cache entries (decoded before the leader rewrites the walker)
@@ -937,6 +949,9 @@ k_ls(LsArgs a) {
                             schedule_records<T, G, L, false>(sc, RecWalker{crec}, nullptr, kc, cache, cache, lane == 0);
                     }
                     gsync();
+#ifdef SAT_LS_PROFILE
+                    if (leader) { prof[1] += 1; prof[3] += clock64() - prof_t1; prof[4] += first; }
+#endif
                     if (s_beaten[grp]) { abandoned = true; break; }
                     cur_key = nk;
                     cur = (T)(nk >> 34);
@@ -959,6 +974,9 @@ k_ls(LsArgs a) {
                               ((unsigned long long)(uint32_t)cur << a.idx_bits) | id);
             }
             atomicAdd(a.rounds, (unsigned long long)rounds + 1ull);   // + the start's round
+#ifdef SAT_LS_PROFILE
+            for (int i = 0; i < 5; ++i) { atomicAdd(a.rounds + 1 + i, (unsigned long long)prof[i]); prof[i] = 0; }
+#endif
             if (a.state_out && !abandoned) {      // walker wk's final candidate
                 uint8_t *so = a.state_out + wk * (uint64_t)(2 * J);
                 for (int j = 0; j < J; ++j) so[j] = wopt[j];

@@ -545,7 +545,7 @@ class Engine:
             self._check(self.lib.sat_ls_counter_offset(nprob.ref, ctypes.byref(off)), nprob=nprob)
             # geometric waves (wave, 4 x wave, 16 x wave, ...): a small first wave keeps easy
             # problems cheap, larger later waves keep the GPU full when the bound is not met
-            wave = max(1, int(opts.wave))
+            wave = max(1, int(opts.wave)) if opts.wave else (8192 if prob.J < 24 else 1024)
             rounds_total, walkers_done, waves = 0, 0, 0
             w0 = 0
             ls_states = []          # (first walker, [walkers][2J] final states) per wave on this rank

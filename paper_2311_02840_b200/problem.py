@@ -52,7 +52,9 @@ class SolveOptions:
     budget: int = 1 << 28               # sampled candidates when not exhaustive
     seed: int = 7                       # sampled stream: candidate i = substream(seed, i)
     walkers: int = 1 << 16              # local search: walkers at most (walker w starts at candidate w)
-    wave: int = 1 << 14                 # local search: first wave (then x4 per wave); stops at the bound
+    wave: int | None = None             # local search: first wave (then x4 per wave); stops at the bound.
+                                        # None: 8192 walkers of one warp (< 24 jobs), 1024 walkers of 16
+                                        # warps (>= 24 jobs) -- walkers past the winner only slow it down
     max_rounds: int = 4096              # local search: rounds of 32 moves per walker
     ls_stop: bool = True                # local search: a walk ends at the lower bound (same result)
     kernel: str = "auto"                # auto (bnb when it applies) | tree | index | bnb
