@@ -90,7 +90,6 @@ __host__ __device__ constexpr int cache_state_words(int N) {
 //               a move, computed per position (no per-move record column to build or hold).
 struct RecCol {
     const uint32_t *p;                           // lane's column, stride 32
-    static constexpr int lo = 0, hi = 1 << 30;   // every position may differ between lanes
     __device__ __forceinline__ uint32_t operator()(int k) const { return p[k * 32]; }
 };
 
@@ -444,10 +443,6 @@ __device__ __forceinline__ int32_t schedule_eval16(const SchedCtx<int32_t> &c, c
     int32_t mx = 0;
     bool dirty = true;                 // column st16 does not hold av
     bool live = true;                  // false once the move is known not to improve (early exit)
-    // positions outside every lane's changed range carry the same record for all lanes: the
-    // gang size is warp-uniform there without a vote
-    const int ulo = (int)__reduce_min_sync(act, (unsigned)rec.lo);
-    const int uhi = (int)__reduce_max_sync(act, (unsigned)min(rec.hi, J));
     for (int kk = kmin; kk < J; ++kk) {
         if (SAT_LS_CUT_REG > 0 && !__any_sync(act, live)) break;
         const bool on = kk >= k0 && live;
@@ -461,16 +456,9 @@ __device__ __forceinline__ int32_t schedule_eval16(const SchedCtx<int32_t> &c, c
         const uint32_t r = on ? rec(kk) : 0u;
         const int g = (int)(r & 63u) + 1;
         SAT_ASSERT(!on || (g >= 1 && g <= G && (int)((r >> 6) & 63u) < J));
-        int g0;
-        bool uni;
-        if (kk < ulo || kk > uhi) {    // warp-uniform branch
-            g0 = (int)(rec.crec[kk] & 63u) + 1;
-            uni = true;
-        } else {
-            const unsigned onm = __ballot_sync(act, on);
-            g0 = __shfl_sync(act, g, __ffs(onm) - 1);
-            uni = __all_sync(act, !on || g == g0);
-        }
+        const unsigned onm = __ballot_sync(act, on);
+        const int g0 = __shfl_sync(act, g, __ffs(onm) - 1);
+        const bool uni = __all_sync(act, !on || g == g0);
         const int32_t rel = (on && c.has_release) ? (int32_t)c.release[(r >> 6) & 63u] : 0;
         const int32_t d = (int32_t)(r >> 12);
         if (uni) {
@@ -725,39 +713,18 @@ __device__ __forceinline__ int ls_src(const LsMove &mv, int k) {
 
 // the neighbour's record at position k: the walker's record at the source position, or (option
 // move) the moved job's record with its new option at the job's own position
-// Branch-free form of ls_src: positions in [lo, hi] read k + sh (insertions shift the block
-// between a and b by one; swaps keep it), then two endpoint overrides (e1k -> e1s: position b
-// takes the job from a, for swaps and insertions; e2k -> e2s: swaps also put b's job at a), and
-// the option move's own record at its position.  Outside [lo, hi] a move reads the walker's
-// record unchanged (the same for every move: warp-uniform).
 struct RecMove {
     const uint32_t *crec;                        // walker's current records [J] (shared by its warps)
-    int lo, hi, sh, e1k, e1s, e2k, e2s;
+    LsMove mv;
     int spk;                                     // option move: the job's position (-1: none)
     uint32_t sprec;
-    __device__ __forceinline__ RecMove(const uint32_t *c, const LsMove &mv, int kpos, uint32_t srec)
-        : crec(c), spk(kpos), sprec(srec) {
-        if (mv.kind == 1) {
-            lo = hi = kpos; sh = 0; e1k = e2k = -1; e1s = e2s = 0;
-        } else {
-            lo = min(mv.a, mv.b); hi = max(mv.a, mv.b);
-            sh = mv.kind == 0 ? 0 : (mv.a < mv.b ? 1 : -1);
-            e1k = mv.b; e1s = mv.a;
-            e2k = mv.kind == 0 ? mv.a : -1; e2s = mv.b;
-        }
-    }
     __device__ __forceinline__ uint32_t operator()(int k) const {
-        int src = (k >= lo && k <= hi) ? k + sh : k;
-        src = k == e1k ? e1s : src;
-        src = k == e2k ? e2s : src;
-        const uint32_t r = crec[src];
-        return k == spk ? sprec : r;
+        return k == spk ? sprec : crec[ls_src(mv, k)];
     }
 };
 
 struct RecWalker {
     const uint32_t *crec;
-    static constexpr int lo = 0, hi = 1 << 30;
     __device__ __forceinline__ uint32_t operator()(int k) const { return crec[k]; }
 };
 
