@@ -209,6 +209,23 @@ int sat_dp_workspace_bytes(const sat_problem_t *p, int32_t target, uint64_t max_
 int sat_search_dp(const sat_problem_t *p, int32_t target, uint64_t max_states, uint8_t *h_candidate,
                   sat_dp_info_t *info, void *d_ws, size_t ws_bytes, void *stream);
 
+/* Cross-rank shared incumbent (ABI v4).  With several ranks (one process per GPU), every rank's
+ * search kernels can atomicMin into -- and prune against -- ONE sat_best_t cell in the owner
+ * rank's HBM, reached over NVLink peer memory: the MIN combine of SURVEY.md 8(e) happens inside
+ * the searches tile by tile, so bound-and-prune and the local search's abandonment see the best
+ * key of ALL ranks while they run.  The owner allocates the cell (two sat_best_t, all ones) and
+ * exports a CUDA IPC handle (SAT_IPC_HANDLE_BYTES); the others open it (peer access enabled
+ * lazily).  sat_peer_atomics reports whether two devices support native peer atomics (NVLink;
+ * same device: yes).  sat_best_set writes a key (seeding), sat_best_copy reads one cell into
+ * another (e.g. into a rank-local buffer after the searches). */
+#define SAT_IPC_HANDLE_BYTES 64
+int sat_best_set(sat_best_t *d_best, uint64_t hi, uint64_t lo, void *stream);
+int sat_best_copy(sat_best_t *d_dst, const sat_best_t *d_src, void *stream);
+int sat_shared_best_alloc(sat_best_t **d_cell, uint8_t *handle_out);
+int sat_shared_best_open(const uint8_t *handle, sat_best_t **d_cell);
+int sat_shared_best_close(sat_best_t *d_cell, int32_t owner);
+int sat_peer_atomics(int32_t dev_a, int32_t dev_b, int32_t *supported);
+
 /* INT32 min/max issue-rate probe for the roofline denominator: runs `iters`
  * dependent-chain IMNMX iterations on every SM; *d_ops_out = lane-ops done. */
 int sat_alu_probe(int32_t blocks, int32_t threads, int32_t iters,

@@ -686,6 +686,58 @@ int sat_best_reset(sat_best_t *d_best, void *stream) {
     return check_cuda(cudaMemsetAsync(d_best, 0xFF, sizeof(sat_best_t), (cudaStream_t)stream));
 }
 
+// ---- cross-rank shared incumbent (NVLink peer memory) ----
+int sat_best_set(sat_best_t *d_best, uint64_t hi, uint64_t lo, void *stream) {
+    if (!d_best) return SAT_ERR_INVALID;
+    // a kernel-free 16-byte write: cudaMemcpyAsync from pageable host memory completes the
+    // host-side copy before returning, so a stack value is safe
+    const sat_best_t v{hi, lo};
+    return check_cuda(cudaMemcpyAsync(d_best, &v, sizeof(v), cudaMemcpyHostToDevice, (cudaStream_t)stream));
+}
+
+int sat_best_copy(sat_best_t *d_dst, const sat_best_t *d_src, void *stream) {
+    if (!d_dst || !d_src) return SAT_ERR_INVALID;
+    return check_cuda(cudaMemcpyAsync(d_dst, d_src, sizeof(sat_best_t), cudaMemcpyDefault, (cudaStream_t)stream));
+}
+
+int sat_shared_best_alloc(sat_best_t **d_cell, uint8_t *handle_out) {
+    if (!d_cell || !handle_out) return SAT_ERR_INVALID;
+    static_assert(sizeof(cudaIpcMemHandle_t) == SAT_IPC_HANDLE_BYTES, "IPC handle size");
+    void *p = nullptr;
+    if (cudaMalloc(&p, 2 * sizeof(sat_best_t)) != cudaSuccess) return SAT_ERR_CUDA;
+    cudaIpcMemHandle_t h;
+    if (cudaIpcGetMemHandle(&h, p) != cudaSuccess) { cudaFree(p); return SAT_ERR_CUDA; }
+    std::memcpy(handle_out, &h, sizeof(h));
+    if (cudaMemset(p, 0xFF, 2 * sizeof(sat_best_t)) != cudaSuccess) { cudaFree(p); return SAT_ERR_CUDA; }
+    *d_cell = static_cast<sat_best_t *>(p);
+    return SAT_OK;
+}
+
+int sat_shared_best_open(const uint8_t *handle, sat_best_t **d_cell) {
+    if (!d_cell || !handle) return SAT_ERR_INVALID;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    void *p = nullptr;
+    if (cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) return SAT_ERR_CUDA;
+    *d_cell = static_cast<sat_best_t *>(p);
+    return SAT_OK;
+}
+
+int sat_shared_best_close(sat_best_t *d_cell, int32_t owner) {
+    if (!d_cell) return SAT_ERR_INVALID;
+    return check_cuda(owner ? cudaFree(d_cell) : cudaIpcCloseMemHandle(d_cell));
+}
+
+int sat_peer_atomics(int32_t dev_a, int32_t dev_b, int32_t *supported) {
+    if (!supported) return SAT_ERR_INVALID;
+    if (dev_a == dev_b) { *supported = 1; return SAT_OK; }
+    int v = 0;
+    if (cudaDeviceGetP2PAttribute(&v, cudaDevP2PAttrNativeAtomicSupported, dev_a, dev_b) != cudaSuccess)
+        return SAT_ERR_CUDA;
+    *supported = v;
+    return SAT_OK;
+}
+
 int sat_workspace_bytes(const sat_problem_t *p, size_t *bytes) {
     int st = validate(p);
     if (st) return st;

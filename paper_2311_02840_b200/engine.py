@@ -77,6 +77,12 @@ _SIGS = {
     "sat_ls_counter_offset": ([_vp, _vp], _i32),
     "sat_tree_shard": ([_vp, _i32, _i32, _i32, _vp, _vp], _i32),
     "sat_dp_workspace_bytes": ([_vp, _i32, _u64, _vp], _i32),
+    "sat_best_set": ([_vp, _u64, _u64, _vp], _i32),
+    "sat_best_copy": ([_vp, _vp, _vp], _i32),
+    "sat_shared_best_alloc": ([_vp, _vp], _i32),
+    "sat_shared_best_open": ([_vp, _vp], _i32),
+    "sat_shared_best_close": ([_vp, _i32], _i32),
+    "sat_peer_atomics": ([_i32, _i32, _vp], _i32),
     "sat_search_dp": ([_vp, _i32, _u64, _vp, _vp, _vp, ctypes.c_size_t, _vp], _i32),
 }
 
@@ -165,6 +171,90 @@ class NativeProblem:
                                       self.release, self.init))
 
 
+class _Cell:
+    """A raw device pointer where the search methods expect a best tensor (data_ptr only)."""
+
+    def __init__(self, ptr: int):
+        self.ptr = ptr
+
+    def data_ptr(self) -> int:
+        return self.ptr
+
+
+class SharedIncumbent:
+    """The cross-rank incumbent: one sat_best_t in rank 0's HBM that every rank's search kernels
+    atomicMin into and prune against while they run, reached over NVLink peer memory through a
+    CUDA IPC handle (include/saturn_engine.h, sat_shared_best_*).  Bound-and-prune then cuts with
+    the best key of ALL ranks, and a local-search walker is abandoned as soon as ANY rank has a
+    lower-id walker at the bound -- N-rank pruning matches one rank's.
+
+    Protocol per search: rank 0 resets (or seeds) the cell, every rank waits at a barrier, the
+    kernels run, then each rank drains its stream, meets the others at a barrier (all kernels of
+    all ranks done: the cell is final) and copies the cell into its local key buffer; the usual
+    all-reduce MIN of those copies follows, which also fences the cell's next reset.
+    Enabled only when every rank can reach the owner's memory with native peer atomics (NVLink /
+    NVSwitch, or the same device); otherwise every rank keeps its own key and the all-reduce
+    alone combines them."""
+
+    def __init__(self, eng: "Engine", group):
+        import torch.distributed as dist
+
+        self.eng, self.group = eng, group
+        rank, world = _rank_world(group)
+        self.owner = rank == 0
+        self.ptr = ctypes.c_void_p()
+        lib = eng.lib
+        payload = [None]
+        if self.owner:
+            handle = (ctypes.c_uint8 * 64)()
+            st = lib.sat_shared_best_alloc(ctypes.byref(self.ptr), handle)
+            payload = [(st, bytes(handle), eng.device.index)]
+        src = dist.get_global_rank(group, 0) if group is not None else 0
+        dist.broadcast_object_list(payload, src=src, group=group)
+        st, hb, owner_dev = payload[0]
+        ok = st == SAT_OK
+        if ok and not self.owner:
+            sup = ctypes.c_int32()
+            ok = (lib.sat_peer_atomics(eng.device.index, owner_dev, ctypes.byref(sup)) == SAT_OK and sup.value == 1
+                  and lib.sat_shared_best_open((ctypes.c_uint8 * 64).from_buffer_copy(hb), ctypes.byref(self.ptr))
+                  == SAT_OK)
+        flag = eng.torch.tensor([1 if ok else 0], dtype=eng.torch.int32, device=eng.device)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+        self.enabled = bool(flag.item())
+        if not self.enabled and ok and self.ptr.value:
+            lib.sat_shared_best_close(self.ptr, 1 if self.owner else 0)
+            self.ptr = ctypes.c_void_p()
+
+    @property
+    def cell(self) -> _Cell:
+        return _Cell(self.ptr.value)
+
+    def begin(self, seed_key: int | None = None):
+        """Rank 0 resets (or seeds) the cell; all ranks start their kernels after a barrier."""
+        import torch.distributed as dist
+
+        eng = self.eng
+        if self.owner:
+            if seed_key is None:
+                eng._check(eng.lib.sat_best_reset(self.ptr, _vp(eng.stream())))
+            else:
+                eng._check(eng.lib.sat_best_set(self.ptr, seed_key & ((1 << 64) - 1), (1 << 64) - 1,
+                                                _vp(eng.stream())))
+        eng.torch.cuda.current_stream(eng.device).synchronize()
+        dist.barrier(group=self.group)
+        return self.cell
+
+    def collect(self, best):
+        """All ranks' kernels done -> the cell is final: copy it into this rank's key buffer."""
+        import torch.distributed as dist
+
+        eng = self.eng
+        eng.torch.cuda.current_stream(eng.device).synchronize()
+        dist.barrier(group=self.group)
+        eng._check(eng.lib.sat_best_copy(_vp(best.data_ptr()), self.ptr, _vp(eng.stream())))
+        return best
+
+
 @dataclass
 class SearchResult:
     makespan: float            # grid intervals (grid mode) or seconds (float mode)
@@ -204,6 +294,7 @@ class Engine:
         self._best = torch.empty(2, dtype=torch.int64, device=self.device)
         self._ws = None
         self._dp_ws = None
+        self._shared = {}
         self.launches = 0
 
     # ---- plumbing ----------------------------------------------------------
@@ -236,6 +327,15 @@ class Engine:
         best = self._best if best is None else best
         self._check(self.lib.sat_best_reset(_vp(best.data_ptr()), _vp(self.stream())))
         return best
+
+    def shared_incumbent(self, group):
+        """The group's SharedIncumbent (created on first use, collectively), or None when peer
+        atomics are not available on every rank."""
+        key = id(group) if group is not None else 0
+        sh = self._shared.get(key)
+        if sh is None:
+            sh = self._shared[key] = SharedIncumbent(self, group)
+        return sh if sh.enabled else None
 
     # ---- kernels -------------------------------------------------------------
     def tree_plan(self, nprob: NativeProblem, prefix_len: int = 0) -> SatTreeInfo:
@@ -502,6 +602,17 @@ class Engine:
         nprob = NativeProblem(prob, idx_bits)
         launches0 = self.launches
         best = self.reset_best()
+        # several ranks, grid keys, searches that prune (bound-and-prune) or abandon (local
+        # search) on the incumbent: the kernels of every rank share one incumbent cell over
+        # NVLink.  Full scans / sampled sweeps gain nothing from it and keep rank-local keys.
+        shared = (self.shared_incumbent(group)
+                  if world > 1 and nprob.grid and opts.share_incumbent and (use_bnb or mode == "local")
+                  else None)
+        if shared is not None:
+            seed_key = (seed_ms << idx_bits) | ((1 << idx_bits) - 1) if use_bnb else None
+            kbest = shared.begin(seed_key)
+        else:
+            kbest = best
         job_steps = 0
         stats, bnb_ws = None, None
         ls_state = None
@@ -519,18 +630,19 @@ class Engine:
                 P = self.bnb_prefix(nprob, 1 << 15)
                 info = self.tree_plan(nprob, P)
                 a, b = self.tree_shard(nprob, info.prefix_len, rank, world)
-                best[0:1].fill_((seed_ms << idx_bits) | ((1 << idx_bits) - 1))
-                bnb_ws = self.search_bnb(nprob, info.prefix_len, a, b, best)
+                if shared is None:
+                    best[0:1].fill_((seed_ms << idx_bits) | ((1 << idx_bits) - 1))
+                bnb_ws = self.search_bnb(nprob, info.prefix_len, a, b, kbest)
                 stats = {"prefix_len": info.prefix_len, "tasks": b - a}
                 kernel, evaluated = "bnb", info.n_candidates
             elif use_tree:
                 info = self.tree_plan(nprob, self.full_scan_prefix(nprob, world))
                 a, b = self.tree_shard(nprob, info.prefix_len, rank, world)
-                self.search_tree(nprob, info.prefix_len, a, b, best)
+                self.search_tree(nprob, info.prefix_len, a, b, kbest)
                 kernel, evaluated, job_steps = "tree", info.n_candidates, info.n_job_steps
             else:
                 a, b = _shard(n_idx, rank, world)
-                self.search_index(nprob, a, b, best)
+                self.search_index(nprob, a, b, kbest)
                 kernel, evaluated = "index", n_idx
             seed_used = 0
         elif mode == "local":
@@ -560,10 +672,12 @@ class Engine:
                 a, b = _shard(w1 - w0, rank, world)
                 st_buf = torch.empty(max(1, b - a) * 2 * prob.J, dtype=torch.uint8, device=self.device)
                 ls_states.append((w0 + a, w0 + b, st_buf))
-                self.local_search(nprob, src, seed_used, w0 + a, w0 + b, opts.max_rounds, best, state_out=st_buf,
+                self.local_search(nprob, src, seed_used, w0 + a, w0 + b, opts.max_rounds, kbest, state_out=st_buf,
                                   stop_ms=stop_ms)
                 rounds_total += int(self._ws[off.value:off.value + 8].view(torch.int64).item())
                 walkers_done, waves, w0, wave = w1, waves + 1, w1, wave * 4
+                if shared is not None:
+                    shared.collect(best)
                 k = int(_combine(best, True, group, world)[0])
                 if k != INT64_MAX and (k >> idx_bits) <= target:
                     break
@@ -588,9 +702,11 @@ class Engine:
             base_lo = 0 if lo is None else lo
             base_hi = n_idx if hi is None else hi
             a, b = _shard(base_hi - base_lo, rank, world)
-            self.search_sampled(nprob, src, seed_used, base_lo + a, base_lo + b, best)
+            self.search_sampled(nprob, src, seed_used, base_lo + a, base_lo + b, kbest)
             kernel, evaluated = "sampled", base_hi - base_lo
         ev1.record()
+        if shared is not None:
+            shared.collect(best)
         key_dev = _combine_dev(best, nprob.grid, group, world)
         replay_out = None
         if replay and nprob.grid and bnb_ws is None and mode in ("exhaustive", "sampled"):
@@ -607,6 +723,8 @@ class Engine:
         if bnb_ws is not None:
             cnt = bnb_ws[:24].view(torch.int64).cpu().tolist()
             stats.update(pruned_tasks=cnt[1], pair_nodes=cnt[2])
+        if shared is not None:
+            stats = {**(stats or {}), "shared_incumbent": True}
         if nprob.grid:
             k = int(key[0])
             if k == INT64_MAX:

@@ -61,6 +61,7 @@ class SolveOptions:
     prove: bool = True                  # local search on one node: prove / improve the best makespan
                                         # with the state-space search (sat_search_dp) after a wave
     dp_states: int = 1 << 22            # state budget of one sat_search_dp call (all levels)
+    share_incumbent: bool = True        # several ranks: one incumbent cell over NVLink peer memory
 
 
 @dataclass

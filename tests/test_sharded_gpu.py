@@ -6,7 +6,9 @@ each other; only the host-side combine meets).  Every search mode is covered: th
 scan (work-balanced task ranges from sat_tree_shard), bound-and-prune (per-rank task ranges,
 seeded bound), the per-candidate index kernel, sampled search, local-search waves (walker
 ranges, per-wave combine, winner state broadcast) and float time (two-stage MIN).  Each must
-return the single-rank key AND the single-rank plan."""
+return the single-rank key AND the single-rank plan.  Bound-and-prune and local search run with
+the cross-rank shared incumbent (one key cell every rank's kernels atomicMin into, opened
+through CUDA IPC -- NVLink peer memory across GPUs, the same device here)."""
 
 import os
 import socket
@@ -55,7 +57,7 @@ def run_cases(world: int, rank: int):
         entries = sorted((j, e.config.technique, e.config.gpus, e.node, e.start_time)
                          for j, e in sol.plan.entries.items())
         out.append((name, sol.search.kernel, sol.status, sol.makespan, sol.search.index, entries,
-                    sol.search.evaluated))
+                    sol.search.evaluated, bool((sol.search.stats or {}).get("shared_incumbent"))))
     return out
 
 
@@ -104,3 +106,5 @@ def test_sharded_equals_single_rank(world, single):
         for a, b in zip(got[rank], single):
             assert a[:6] == b[:6], (world, rank, a[:5], b[:5])
             assert a[6] == b[6]              # candidates / walkers evaluated over all ranks
+            # bound-and-prune and local search share one incumbent cell (CUDA IPC peer memory)
+            assert a[7] == (a[1] in ("bnb", "local")) and not b[7], (a[1], a[7])
