@@ -25,3 +25,4 @@ def test_integration_ctypes_example_runs():
     # two side by side on one GPU each (10), then the third on both (4) -> 14 (2 GPUs each: 16)
     assert 0 <= scope["index"] < 2 * 2 * 1 * 6
     assert scope["makespan"] == 14
+    assert scope["dp_status"] == 0                      # nothing reaches 13: 14 is optimal
