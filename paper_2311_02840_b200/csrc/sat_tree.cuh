@@ -418,8 +418,14 @@ __device__ __forceinline__ void walk_fixed(const TreeParams &p, int32_t *wbase, 
 // occupancy target per node size: 12 blocks (40 regs) up to 8 GPUs, fewer for larger nodes.
 // BNB = bound-and-prune: subtrees whose bound exceeds the best makespan found so far (by
 // any warp: published after every task) are skipped; the key found is the exhaustive one.
-template <int G, bool BNB>
-__global__ void __launch_bounds__(kTreeThreads, G <= 8 ? 10 : (G <= 16 ? 8 : 4))
+// DEEP = the generic walk (suffixes beyond the fixed-depth walkers) and prefixes of more than 8
+// jobs: their per-lane stacks live in local memory, so they get their own instantiation and
+// the common kernel (config 1: 4-job prefix, 4-job suffix) keeps no stack frame at all.
+#ifndef SAT_TREE_MINB8
+#define SAT_TREE_MINB8 10    // blocks per SM the register budget targets for nodes of <= 8 GPUs
+#endif
+template <int G, bool BNB, bool DEEP>
+__global__ void __launch_bounds__(kTreeThreads, G <= 8 ? SAT_TREE_MINB8 : (G <= 16 ? 8 : 4))
 k_tree(const __grid_constant__ TreeParams p) {
     extern __shared__ __align__(16) int32_t tsm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -475,7 +481,7 @@ k_tree(const __grid_constant__ TreeParams p) {
         // options of S's jobs: mixed radix, highest job id least significant; kept as 8-bit
         // fields indexed by the job's rank within S (P <= 8: one u64 register; else local)
         uint64_t popt_lo = 0;
-        uint8_t popt_hi[kTreeMaxJ];
+        uint8_t popt_hi[DEEP ? kTreeMaxJ : 1];
         {
             uint32_t m = S;
             int rank = P;
@@ -487,7 +493,7 @@ k_tree(const __grid_constant__ TreeParams p) {
                 const uint64_t qd = code / r;
                 const uint64_t dig = code - qd * r;
                 if (rank < 8) popt_lo |= dig << (8 * rank);
-                else popt_hi[rank] = (uint8_t)dig;
+                else if constexpr (DEEP) popt_hi[rank] = (uint8_t)dig;
                 code = qd;
             }
         }
@@ -503,7 +509,8 @@ k_tree(const __grid_constant__ TreeParams p) {
             const int j = __ffs(m) - 1;
             avail &= ~(1u << j);
             const int rk = __popc(S & ((1u << j) - 1u));
-            const int o = rk < 8 ? (int)((popt_lo >> (8 * rk)) & 0xffu) : (int)popt_hi[rk];
+            int o = (int)((popt_lo >> (8 * (rk & 7))) & 0xffu);
+            if constexpr (DEEP) if (rk >= 8) o = (int)popt_hi[rk];
             base += (uint64_t)__popc(unpl & ((1u << j) - 1u)) * p.fact[J - 1 - k] + (uint64_t)o * p.wJ[j];
             unpl &= ~(1u << j);
             // per-lane gang size: in-place merge on the lane's column
@@ -546,7 +553,7 @@ k_tree(const __grid_constant__ TreeParams p) {
             walk_fixed<G, BNB, 4>(p, wbase, lane, 0, Q, unplaced, base, lane_ok, Bbuf, sdg, lb, U, n_pairs);
         } else if (BNB && Q == 7) {
             walk_fixed<G, BNB, 5>(p, wbase, lane, 0, Q, unplaced, base, lane_ok, Bbuf, sdg, lb, U, n_pairs);
-        } else {
+        } else if constexpr (DEEP) {
             uint32_t rem_st[kTreeMaxJ];
             uint64_t acc_st[kTreeMaxJ];
             int cj[kTreeMaxJ], co[kTreeMaxJ];
@@ -630,7 +637,10 @@ template <int G, bool BNB>
 int launch_tree_k(const TreeParams &tp, int Q, cudaStream_t stream) {
     const int smem = kTreeWarps * tree_warp_words<G>(Q, tree_compact(BNB, tp.packed != 0, G, Q)) * 4;
     if (smem > 200 * 1024) return SAT_ERR_UNSUPPORTED;
-    auto kern = k_tree<G, BNB>;
+    // the fixed-depth walkers cover Q <= 4 (full scan) / Q <= 7 (bound-and-prune) with prefixes
+    // of <= 8 jobs; anything else takes the DEEP instantiation
+    const bool deep = tp.P > 8 || Q > (BNB ? 7 : 4);
+    auto kern = deep ? k_tree<G, BNB, true> : k_tree<G, BNB, false>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
         return SAT_ERR_CUDA;
     int per_sm = 0;
