@@ -162,13 +162,40 @@ def _plan_of(prob: SearchProblem, workload, schedule, r: int):
     return plan, [int(x) for x in opt[r]], float(ms[r]), runtimes
 
 
+class _nvtx:
+    """NVTX range around a host stage of a solve (visible in Nsight timelines next to the
+    library's own sat_* ranges); a no-op where torch's NVTX binding is unavailable."""
+
+    def __init__(self, name: str):
+        self.name = name
+
+    def __enter__(self):
+        try:
+            import torch
+
+            torch.cuda.nvtx.range_push(self.name)
+            self.on = True
+        except Exception:  # noqa: BLE001
+            self.on = False
+        return self
+
+    def __exit__(self, *exc):
+        if self.on:
+            import torch
+
+            torch.cuda.nvtx.range_pop()
+
+
 def solve(table, jobs, cluster=None, delta_opts=None, running_context=None, *, techniques=None,
           group=None, device=None, validate: bool = True) -> Solution:
     """Solver.solve / re-solve on the engine (build -> search -> decode -> check)."""
     workload = _as_workload(jobs, cluster, techniques)
     opts = _opts(delta_opts)
-    prob = build_problem(table, workload, opts, running_context)
-    return solve_problem(prob, workload, opts, running_context, group=group, device=device, validate=validate)
+    with _nvtx("saturn.build_problem"):
+        prob = build_problem(table, workload, opts, running_context)
+    with _nvtx("saturn.solve_problem"):
+        return solve_problem(prob, workload, opts, running_context, group=group, device=device,
+                             validate=validate)
 
 
 def solve_problem(prob: SearchProblem, workload, opts: SolveOptions, running_context=None, *, group=None,
@@ -177,7 +204,8 @@ def solve_problem(prob: SearchProblem, workload, opts: SolveOptions, running_con
     err = E.errors_for(workload.jobs[0] if workload.jobs else workload)
     eng = get_engine(device)
     try:
-        res = eng.search(prob, opts, group=group, replay=True)
+        with _nvtx("saturn.search"):
+            res = eng.search(prob, opts, group=group, replay=True)
         nprob = NativeProblem(prob, res.idx_bits) if res.replay is None else None
         if res.kernel == "local":
             # replay the winning walker to get its final candidate, then schedule it explicitly
@@ -238,7 +266,8 @@ def solve_problem(prob: SearchProblem, workload, opts: SolveOptions, running_con
             keep = set(prob.job_ids)
             target = _WorkloadView(tuple(j for j in workload.jobs if j.id in keep), workload.cluster,
                                    tuple(workload.techniques))
-        _validator_for(workload)(plan, target, runtimes)
+        with _nvtx("saturn.check_plan"):
+            _validator_for(workload)(plan, target, runtimes)
     status = "Optimal" if res.exhaustive else ("Local" if res.kernel == "local" else "Sampled")
     if res.exhaustive:
         lb = makespan

@@ -425,7 +425,7 @@ def test_local_search_records_every_walker_state(eng, name, stop):
     assert (list(res.state[0]), list(res.state[1])) == (o, r)
 
 
-@pytest.mark.parametrize("group", ["1", "8"])
+@pytest.mark.parametrize("group", ["1", "4", "8", "16", "32"])
 def test_local_search_wide_nodes_register_path(eng, group, monkeypatch):
     """Nodes of 9-32 GPUs (padded 16 / 32; with 8 warps per walker the move evaluation shifts
     in registers when the warp's lanes place equal gang sizes, in shared memory otherwise), with
