@@ -192,8 +192,12 @@ size_t sat_tree_param_bytes(void);
  * digit per job, then the order) receives one candidate with makespan <= target, chosen
  * deterministically (smallest final state key, then smallest parent keys, lowest options).
  * BUDGET: more than max_states states over all levels; nothing decided.  Synchronous: returns
- * after the search (one small read-back per level).  Keys must fit 63 bits:
- * 2^J x C(target + G, G) < 2^63, else SAT_ERR_UNSUPPORTED. */
+ * after the search (one small read-back per level).  One node with 2^J x C(target + G, G) < 2^63:
+ * exact states, 63-bit keys, candidate rebuilt.  Otherwise (several nodes, up to 8 and 32 GPUs
+ * in all, or wider keys: 2^J x prod_n C(target + G_n, G_n) < 2^126) a PROVER on 128-bit keys:
+ * interchangeable nodes are canonicalised and ties between nodes expanded both ways, so an
+ * INFEASIBLE answer is still a proof, but FEASIBLE carries no candidate (info->makespan = -1);
+ * shapes beyond that: SAT_ERR_UNSUPPORTED. */
 #define SAT_DP_INFEASIBLE 0
 #define SAT_DP_FEASIBLE   1
 #define SAT_DP_BUDGET     2

@@ -27,6 +27,8 @@
 
 #include <nvtx3/nvToolsExt.h>
 
+#include <cmath>
+
 namespace sat {
 
 constexpr int kDpMaxJ = 64;
@@ -328,6 +330,382 @@ static int32_t dp_host_place(const DpPlan &d, const int32_t *a, int q, int rel, 
     return e;
 }
 
+// ------------------------------------------------------------------------------------------
+// Wide states (several nodes, or keys beyond 63 bits): a PROVER.  The state is R plus every
+// node's sorted free-time vector; the key R x prod_n C(T + G_n, G_n) + ranks is exact in 128
+// bits, kept in a hash set of 16-byte slots claimed with a 128-bit atomicCAS
+// (ATOMG.E.CAS.128).  Interchangeable nodes (same GPU count and memory, same option
+// eligibility and durations) are canonicalised -- their vectors sorted by rank -- and a job
+// whose earliest finish ties on several nodes is placed on EACH of them: the list scheduler
+// picks the lowest label among tied nodes, and labels are what canonicalisation forgets, so
+// the level sets cover (a superset of) every candidate's states.  An empty level therefore
+// still proves that no candidate reaches T; a non-empty last level proves nothing (no
+// candidate is rebuilt: status FEASIBLE, makespan -1).
+// ------------------------------------------------------------------------------------------
+constexpr int kDpWideMaxN = 8;
+constexpr int kDpWideSlots = 32;
+
+struct DpWideParams {
+    int32_t J, N, T, Gtot;
+    int32_t node_off[kDpWideMaxN], node_g[kDpWideMaxN], node_grp[kDpWideMaxN];
+    uint64_t cnum[kDpWideMaxN];             // C(T + G_n, G_n)
+    int32_t ubase[kDpMaxJ], ucnt[kDpMaxJ], release[kDpMaxJ], minarea[kDpMaxJ];
+    int32_t Kb;                             // binomial table row width (max G_n + 1)
+    const uint64_t *binom;                  // [(T + maxG + 1)][Kb]
+    const uint8_t *ug;                      // [n_usable] gang size
+    const uint8_t *um;                      // [n_usable] node eligibility bits
+    const int16_t *ud;                      // [n_usable][N] duration per node
+    const int16_t *dg;                      // [J][N][32] least usable duration at gang k+1 (T+1: none)
+    unsigned __int128 *table;
+    uint64_t cap_mask;
+    int32_t cap_log2, max_probe;
+    const uint64_t *in_R;
+    const uint16_t *in_A;                   // [n_in][Gtot]
+    uint64_t n_in;
+    uint64_t *out_R;
+    uint16_t *out_A;
+    uint64_t out_cap;
+    unsigned long long *count;
+    unsigned int *overflow;
+};
+
+__device__ __forceinline__ unsigned __int128 cas128(unsigned __int128 *addr, unsigned __int128 cmp,
+                                                    unsigned __int128 val) {
+    uint64_t o0, o1;
+    const uint64_t c0 = (uint64_t)cmp, c1 = (uint64_t)(cmp >> 64);
+    const uint64_t v0 = (uint64_t)val, v1 = (uint64_t)(val >> 64);
+    asm volatile("{\n\t.reg .b128 c, v, d;\n\t"
+                 "mov.b128 c, {%2, %3};\n\t"
+                 "mov.b128 v, {%4, %5};\n\t"
+                 "atom.global.cas.b128 d, [%6], c, v;\n\t"
+                 "mov.b128 {%0, %1}, d;\n\t}"
+                 : "=l"(o0), "=l"(o1)
+                 : "l"(c0), "l"(c1), "l"(v0), "l"(v1), "l"(addr)
+                 : "memory");
+    return ((unsigned __int128)o1 << 64) | o0;
+}
+
+__device__ __forceinline__ uint64_t dpw_rank(const DpWideParams &p, const int32_t *v, int g) {
+    uint64_t r = 0;
+    for (int i = 0; i < g; ++i) r += __ldg(&p.binom[(v[i] + i) * p.Kb + (i + 1)]);
+    return r;
+}
+
+// canonical key of a full state (vectors are permuted in place into canonical node order)
+__device__ __forceinline__ unsigned __int128 dpw_key(const DpWideParams &p, uint64_t R, int32_t *a) {
+    uint64_t rk[kDpWideMaxN];
+    for (int n = 0; n < p.N; ++n) rk[n] = dpw_rank(p, a + p.node_off[n], p.node_g[n]);
+    // sort interchangeable nodes by rank (insertion sort over the <= 8 nodes, within groups)
+    for (int n = 1; n < p.N; ++n)
+        for (int m = n; m > 0 && p.node_grp[m - 1] == p.node_grp[m] && rk[m - 1] > rk[m]; --m) {
+            const uint64_t t = rk[m]; rk[m] = rk[m - 1]; rk[m - 1] = t;
+            int32_t *x = a + p.node_off[m - 1], *y = a + p.node_off[m];
+            for (int i = 0; i < p.node_g[m]; ++i) { const int32_t z = x[i]; x[i] = y[i]; y[i] = z; }
+        }
+    unsigned __int128 key = R;
+    for (int n = 0; n < p.N; ++n) key = key * p.cnum[n] + rk[n];
+    return key;
+}
+
+__device__ __forceinline__ bool dpw_viable(const DpWideParams &p, uint64_t R2, const int32_t *b) {
+    int64_t area = 0;
+    for (int i = 0; i < p.Gtot; ++i) area += b[i];
+    for (int i = 0; i < p.J; ++i) {
+        if (!((R2 >> i) & 1ull)) continue;
+        area += p.minarea[i];
+        int32_t lo = 0x7fffffff;
+        for (int n = 0; n < p.N; ++n) {
+            const int16_t *dgn = p.dg + ((size_t)i * p.N + n) * 32;
+            const int32_t *bn = b + p.node_off[n];
+            for (int k = 0; k < p.node_g[n]; ++k) lo = min(lo, max(bn[k], p.release[i]) + (int32_t)__ldg(&dgn[k]));
+        }
+        if (lo > p.T) return false;
+    }
+    return area <= (int64_t)p.T * p.Gtot;
+}
+
+__global__ void __launch_bounds__(kDpThreads) k_dp_expand_wide(const __grid_constant__ DpWideParams p) {
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (tid >= p.n_in * (uint64_t)p.J) return;
+    if (*reinterpret_cast<volatile unsigned int *>(p.overflow)) return;
+    const uint64_t s = tid / (uint64_t)p.J;
+    const int j = (int)(tid - s * (uint64_t)p.J);
+    const uint64_t R = p.in_R[s];
+    if (!((R >> j) & 1ull)) return;
+    const uint64_t R2 = R & ~(1ull << j);
+    int32_t a[kDpWideSlots], b[kDpWideSlots];
+    for (int i = 0; i < p.Gtot; ++i) a[i] = p.in_A[s * p.Gtot + i];
+    for (int q = p.ubase[j]; q < p.ubase[j] + p.ucnt[j]; ++q) {
+        const int g = p.ug[q];
+        const uint32_t mask = p.um[q];
+        int32_t best = 0x7fffffff;
+        for (int n = 0; n < p.N; ++n)
+            if ((mask >> n) & 1u && g <= p.node_g[n])
+                best = min(best, max(a[p.node_off[n] + g - 1], p.release[j]) + (int32_t)p.ud[q * p.N + n]);
+        if (best > p.T) continue;
+        for (int n = 0; n < p.N; ++n) {                    // every node tying for the earliest finish
+            if (!((mask >> n) & 1u) || g > p.node_g[n]) continue;
+            const int32_t *an = a + p.node_off[n];
+            if (max(an[g - 1], p.release[j]) + (int32_t)p.ud[q * p.N + n] != best) continue;
+            for (int i = 0; i < p.Gtot; ++i) b[i] = a[i];
+            int32_t *bn = b + p.node_off[n];
+            const int G = p.node_g[n];
+            for (int i = 0; i < G; ++i) bn[i] = max(an[i], min(i + g < G ? an[i + g] : 0x7fffffff, best));
+            if (!dpw_viable(p, R2, b)) continue;
+            const unsigned __int128 key = dpw_key(p, R2, b);
+            const uint64_t hh = ((uint64_t)key ^ (uint64_t)(key >> 64) * 0xBF58476D1CE4E5B9ull) * kGolden;
+            uint64_t h = hh >> (64 - p.cap_log2);
+            const unsigned __int128 EMPTY = ~(unsigned __int128)0;
+            for (int probe = 0;; ++probe) {
+                if (probe > p.max_probe) { atomicOr(p.overflow, 1u); return; }
+                const unsigned __int128 old = cas128(&p.table[h], EMPTY, key);
+                if (old == EMPTY) {
+                    const unsigned long long idx = atomicAdd(p.count, 1ull);
+                    if (idx >= p.out_cap) { atomicOr(p.overflow, 1u); return; }
+                    p.out_R[idx] = R2;
+                    for (int i = 0; i < p.Gtot; ++i) p.out_A[idx * p.Gtot + i] = (uint16_t)b[i];
+                    break;
+                }
+                if (old == key) break;
+                h = (h + 1) & p.cap_mask;
+            }
+        }
+    }
+}
+
+struct DpWidePlan {
+    DpWideParams p{};
+    std::vector<uint8_t> ug, um;
+    std::vector<int16_t> ud, dg;
+    std::vector<uint64_t> binom;
+    std::vector<uint16_t> a0;
+    int status = -1;
+    size_t binom_bytes = 0, aux_bytes = 0, table_bytes = 0, R_bytes = 0, A_bytes = 0;
+    uint64_t cap = 0;
+};
+
+static int dpw_prepare(const sat_problem_t *pr, int32_t T, uint64_t max_states, DpWidePlan &d) {
+    if (pr->time_mode != SAT_TIME_GRID_I32) return SAT_ERR_UNSUPPORTED;
+    if (pr->J > kDpMaxJ || max_states < 1) return SAT_ERR_INVALID;
+    const int J = pr->J, N = pr->N;
+    if (N > kDpWideMaxN || T < 0 || T > 30000) return SAT_ERR_UNSUPPORTED;
+    DpWideParams &p = d.p;
+    p.J = J; p.N = N; p.T = T;
+    int off = 0, gmax = 1;
+    for (int n = 0; n < N; ++n) {
+        p.node_off[n] = off;
+        p.node_g[n] = pr->node_gpus[n];
+        off += pr->node_gpus[n];
+        gmax = std::max(gmax, (int)pr->node_gpus[n]);
+    }
+    if (off > kDpWideSlots) return SAT_ERR_UNSUPPORTED;
+    p.Gtot = off;
+    // initial state: each node's initial free times (ascending per node)
+    d.a0.assign(off, 0);
+    int64_t sum0 = 0;
+    for (int n = 0; n < N; ++n)
+        for (int i = 0; i < p.node_g[n]; ++i) {
+            const int32_t v = pr->init_free_i32 ? pr->init_free_i32[n * pr->G + i] : 0;
+            if (v > T) { d.status = SAT_DP_INFEASIBLE; return SAT_OK; }
+            if (i > 0 && v < (int32_t)d.a0[p.node_off[n] + i - 1]) return SAT_ERR_INVALID;
+            d.a0[p.node_off[n] + i] = (uint16_t)v;
+            sum0 += v;
+        }
+    const uint32_t all = N >= 32 ? ~0u : ((1u << N) - 1u);
+    auto dur = [&](int j, int o, int n) { return pr->dur_i32[(j * pr->Cmax + o) * N + n]; };
+    auto elig = [&](int j, int o, int n) {
+        const uint32_t m = pr->node_mask ? pr->node_mask[j * pr->Cmax + o] & all : all;
+        return ((m >> n) & 1u) && pr->gpus[j * pr->Cmax + o] <= p.node_g[n];
+    };
+    auto can_end = [&](int j, int o, int n, int32_t rel) {
+        const int g = pr->gpus[j * pr->Cmax + o];
+        return elig(j, o, n) && std::max<int64_t>(d.a0[p.node_off[n] + g - 1], rel) + dur(j, o, n) <= T;
+    };
+    int64_t need = sum0;
+    std::vector<int64_t> least(J);
+    for (int j = 0; j < J; ++j) {
+        const int32_t rel = pr->release_i32 ? pr->release_i32[j] : 0;
+        int64_t m = INT64_MAX;
+        for (int o = 0; o < pr->radix[j]; ++o)
+            for (int n = 0; n < N; ++n)
+                if (can_end(j, o, n, rel)) m = std::min<int64_t>(m, (int64_t)pr->gpus[j * pr->Cmax + o] * dur(j, o, n));
+        if (m == INT64_MAX) { d.status = SAT_DP_INFEASIBLE; return SAT_OK; }
+        least[j] = m;
+        need += m;
+    }
+    const int64_t slack = (int64_t)T * off - need;
+    if (slack < 0) { d.status = SAT_DP_INFEASIBLE; return SAT_OK; }
+    d.dg.assign((size_t)J * N * 32, (int16_t)(T + 1));
+    int q = 0;
+    for (int j = 0; j < J; ++j) {
+        const int32_t rel = pr->release_i32 ? pr->release_i32[j] : 0;
+        p.release[j] = rel;
+        p.minarea[j] = (int32_t)least[j];
+        p.ubase[j] = q;
+        for (int o = 0; o < pr->radix[j]; ++o) {
+            const int g = pr->gpus[j * pr->Cmax + o];
+            uint8_t m = 0;
+            for (int n = 0; n < N; ++n)
+                if (can_end(j, o, n, rel) && (int64_t)g * dur(j, o, n) <= least[j] + slack) m |= (uint8_t)(1u << n);
+            if (!m) continue;
+            d.ug.push_back((uint8_t)g);
+            d.um.push_back(m);
+            for (int n = 0; n < N; ++n) {
+                const int32_t dd = ((m >> n) & 1u) ? dur(j, o, n) : T + 1;
+                d.ud.push_back((int16_t)dd);
+                if ((m >> n) & 1u) {
+                    int16_t &slot = d.dg[((size_t)j * N + n) * 32 + g - 1];
+                    slot = (int16_t)std::min<int32_t>(slot, dd);
+                }
+            }
+            ++q;
+        }
+        p.ucnt[j] = q - p.ubase[j];
+    }
+    // interchangeable nodes: same size and, for every usable option, the same eligibility
+    // and duration
+    for (int n = 0; n < N; ++n) {
+        p.node_grp[n] = n;
+        for (int m = 0; m < n; ++m) {
+            if (p.node_grp[m] != m || p.node_g[m] != p.node_g[n]) continue;
+            bool same = true;
+            for (int qq = 0; qq < q && same; ++qq)
+                same = ((d.um[qq] >> m) & 1u) == ((d.um[qq] >> n) & 1u) && d.ud[qq * N + m] == d.ud[qq * N + n];
+            if (same) { p.node_grp[n] = m; break; }
+        }
+    }
+    // canonical node order: group members adjacent (stable by first member); rebuild the
+    // per-node tables in that order
+    std::vector<int> ord(N);
+    for (int n = 0; n < N; ++n) ord[n] = n;
+    std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return p.node_grp[x] < p.node_grp[y]; });
+    {
+        DpWideParams p2 = p;
+        std::vector<uint8_t> um2(d.um.size());
+        std::vector<int16_t> ud2(d.ud.size()), dg2(d.dg.size());
+        std::vector<uint16_t> a02(off);
+        int o2 = 0;
+        for (int k = 0; k < N; ++k) {
+            const int n = ord[k];
+            p2.node_g[k] = p.node_g[n];
+            p2.node_grp[k] = p.node_grp[n];
+            p2.node_off[k] = o2;
+            for (int i = 0; i < p.node_g[n]; ++i) a02[o2 + i] = d.a0[p.node_off[n] + i];
+            o2 += p.node_g[n];
+        }
+        for (size_t qq = 0; qq < d.um.size(); ++qq) {
+            uint8_t m2 = 0;
+            for (int k = 0; k < N; ++k) {
+                if ((d.um[qq] >> ord[k]) & 1u) m2 |= (uint8_t)(1u << k);
+                ud2[qq * N + k] = d.ud[qq * N + ord[k]];
+            }
+            um2[qq] = m2;
+        }
+        for (int j = 0; j < J; ++j)
+            for (int k = 0; k < N; ++k)
+                for (int g = 0; g < 32; ++g) dg2[((size_t)j * N + k) * 32 + g] = d.dg[((size_t)j * N + ord[k]) * 32 + g];
+        p = p2; d.um = um2; d.ud = ud2; d.dg = dg2; d.a0 = a02;
+    }
+    // key width: 2^J x prod C(T + G_n, G_n) < 2^127
+    const int n_max = T + gmax;
+    p.Kb = gmax + 1;
+    d.binom.assign((size_t)(n_max + 1) * p.Kb, 0);
+    for (int n = 0; n <= n_max; ++n) {
+        d.binom[(size_t)n * p.Kb] = 1;
+        for (int k = 1; k <= gmax && k <= n; ++k) {
+            const unsigned __int128 v = (unsigned __int128)d.binom[(size_t)(n - 1) * p.Kb + k - 1] +
+                                        (k <= n - 1 ? d.binom[(size_t)(n - 1) * p.Kb + k] : 0);
+            if (v >> 62) return SAT_ERR_UNSUPPORTED;
+            d.binom[(size_t)n * p.Kb + k] = (uint64_t)v;
+        }
+    }
+    double bits = J;
+    for (int n = 0; n < N; ++n) {
+        p.cnum[n] = d.binom[(size_t)(T + p.node_g[n]) * p.Kb + p.node_g[n]];
+        bits += std::log2((double)p.cnum[n]);
+    }
+    if (bits > 126.0) return SAT_ERR_UNSUPPORTED;
+    uint64_t cap = 1;
+    int lg = 0;
+    while (cap < 2 * max_states + (1u << 16)) { cap <<= 1; ++lg; }
+    d.cap = cap;
+    p.cap_mask = cap - 1;
+    p.cap_log2 = lg;
+    p.max_probe = 1 << 14;
+    d.binom_bytes = align256(d.binom.size() * sizeof(uint64_t));
+    d.aux_bytes = align256(d.ug.size() + 16) + align256(d.um.size() + 16) + align256(d.ud.size() * 2 + 16) +
+                  align256(d.dg.size() * 2);
+    d.table_bytes = align256(cap * 16);
+    d.R_bytes = align256(max_states * sizeof(uint64_t));
+    d.A_bytes = align256(max_states * off * sizeof(uint16_t));
+    return SAT_OK;
+}
+
+static size_t dpw_ws_bytes(const DpWidePlan &d) {
+    return d.binom_bytes + d.aux_bytes + d.table_bytes + d.R_bytes + d.A_bytes + 256;
+}
+
+static int dpw_run(const sat_problem_t *pr, uint64_t max_states, sat_dp_info_t *info, void *d_ws, size_t ws_bytes,
+                   cudaStream_t s, DpWidePlan &d) {
+    if (!d_ws || ws_bytes < dpw_ws_bytes(d)) return SAT_ERR_INVALID;
+    DpWideParams &p = d.p;
+    uint8_t *ws = static_cast<uint8_t *>(d_ws);
+    size_t o = 0;
+    auto take = [&](size_t bytes) { uint8_t *r = ws + o; o += bytes; return r; };
+    uint64_t *binom = reinterpret_cast<uint64_t *>(take(d.binom_bytes));
+    uint8_t *ug = take(align256(d.ug.size() + 16));
+    uint8_t *um = take(align256(d.um.size() + 16));
+    int16_t *ud = reinterpret_cast<int16_t *>(take(align256(d.ud.size() * 2 + 16)));
+    int16_t *dg = reinterpret_cast<int16_t *>(take(align256(d.dg.size() * 2)));
+    auto *table = reinterpret_cast<unsigned __int128 *>(take(d.table_bytes));
+    uint64_t *Rs = reinterpret_cast<uint64_t *>(take(d.R_bytes));
+    uint16_t *As = reinterpret_cast<uint16_t *>(take(d.A_bytes));
+    auto *ctr = reinterpret_cast<unsigned long long *>(take(256));
+    const int J = pr->J, Gt = p.Gtot;
+    if (cudaMemcpyAsync(binom, d.binom.data(), d.binom.size() * 8, cudaMemcpyHostToDevice, s) ||
+        (d.ug.size() && cudaMemcpyAsync(ug, d.ug.data(), d.ug.size(), cudaMemcpyHostToDevice, s)) ||
+        (d.um.size() && cudaMemcpyAsync(um, d.um.data(), d.um.size(), cudaMemcpyHostToDevice, s)) ||
+        (d.ud.size() && cudaMemcpyAsync(ud, d.ud.data(), d.ud.size() * 2, cudaMemcpyHostToDevice, s)) ||
+        cudaMemcpyAsync(dg, d.dg.data(), d.dg.size() * 2, cudaMemcpyHostToDevice, s) ||
+        cudaMemsetAsync(table, 0xFF, d.cap * 16, s) || cudaMemsetAsync(ctr, 0, 256, s))
+        return SAT_ERR_CUDA;
+    const uint64_t full = J == 64 ? ~0ull : ((1ull << J) - 1ull);
+    if (cudaMemcpyAsync(Rs, &full, 8, cudaMemcpyHostToDevice, s) ||
+        cudaMemcpyAsync(As, d.a0.data(), Gt * 2, cudaMemcpyHostToDevice, s))
+        return SAT_ERR_CUDA;
+    p.binom = binom; p.ug = ug; p.um = um; p.ud = ud; p.dg = dg; p.table = table;
+    p.count = ctr;
+    p.overflow = reinterpret_cast<unsigned int *>(ctr + 1);
+    uint64_t base = 0, size = 1, total = 1, widest = 1;
+    int level = 0;
+    for (; level < J; ++level) {
+        p.in_R = Rs + base; p.in_A = As + base * Gt; p.n_in = size;
+        const uint64_t nb = base + size;
+        p.out_R = Rs + nb; p.out_A = As + nb * Gt; p.out_cap = max_states - nb;
+        if (cudaMemsetAsync(ctr, 0, 8, s)) return SAT_ERR_CUDA;
+        const uint64_t blocks = (p.n_in * (uint64_t)J + kDpThreads - 1) / kDpThreads;
+        if (blocks > 0x7fffffffull) return SAT_ERR_TOO_LARGE;
+        k_dp_expand_wide<<<(unsigned)blocks, kDpThreads, 0, s>>>(p);
+        if (cudaGetLastError() != cudaSuccess) return SAT_ERR_CUDA;
+        unsigned long long got[2];
+        if (cudaMemcpyAsync(got, ctr, sizeof(got), cudaMemcpyDeviceToHost, s) || cudaStreamSynchronize(s))
+            return SAT_ERR_CUDA;
+        if ((unsigned int)got[1]) {
+            info->status = SAT_DP_BUDGET;
+            info->levels = level; info->states = total; info->widest_level = widest;
+            return SAT_OK;
+        }
+        base = nb; size = got[0];
+        total += size;
+        widest = std::max(widest, size);
+        if (size == 0) { ++level; break; }
+    }
+    info->levels = level; info->states = total; info->widest_level = widest;
+    info->status = (level < J || size == 0) ? SAT_DP_INFEASIBLE : SAT_DP_FEASIBLE;
+    info->makespan = -1;                      // the prover rebuilds no candidate
+    return SAT_OK;
+}
+
 }  // namespace sat
 
 using namespace sat;
@@ -340,8 +718,15 @@ int sat_dp_workspace_bytes(const sat_problem_t *p, int32_t target, uint64_t max_
     if (st) return st;
     DpPlan d;
     st = dp_prepare(p, target, max_states, d);
+    if (st == SAT_OK) {
+        *bytes = d.status >= 0 ? 256 : dp_ws_bytes(d);
+        return SAT_OK;
+    }
+    if (st != SAT_ERR_UNSUPPORTED) return st;
+    DpWidePlan w;                                    // several nodes / wide keys: the prover
+    st = dpw_prepare(p, target, max_states, w);
     if (st) return st;
-    *bytes = d.status >= 0 ? 256 : dp_ws_bytes(d);
+    *bytes = w.status >= 0 ? 256 : dpw_ws_bytes(w);
     return SAT_OK;
 }
 
@@ -355,6 +740,13 @@ int sat_search_dp(const sat_problem_t *pr, int32_t target, uint64_t max_states, 
     std::memset(info, 0, sizeof(*info));
     DpPlan d;
     st = dp_prepare(pr, target, max_states, d);
+    if (st == SAT_ERR_UNSUPPORTED) {                 // several nodes / wide keys: the prover
+        DpWidePlan w;
+        st = dpw_prepare(pr, target, max_states, w);
+        if (st) return st;
+        if (w.status >= 0) { info->status = w.status; info->makespan = -1; return SAT_OK; }
+        return dpw_run(pr, max_states, info, d_ws, ws_bytes, (cudaStream_t)stream, w);
+    }
     if (st) return st;
     if (d.status >= 0) { info->status = d.status; return SAT_OK; }
     if (!d_ws || ws_bytes < dp_ws_bytes(d)) return SAT_ERR_INVALID;

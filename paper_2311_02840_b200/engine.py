@@ -480,7 +480,9 @@ class Engine:
             if st == SAT_DP_INFEASIBLE:
                 stats["proven"] = True
                 return True, best_ms, cand, stats
-            if st == SAT_DP_BUDGET:
+            if st == SAT_DP_BUDGET or c is None:
+                # out of budget, or the multi-node prover found its (superset) level non-empty:
+                # nothing proven, no shorter candidate in hand
                 stats["proven"] = False
                 return False, best_ms, cand, stats
             best_ms, cand = int(info.makespan), c
@@ -664,8 +666,7 @@ class Engine:
             # after a wave that misses the lower bound, the state-space search (one node) either
             # proves the wave's best optimal -- no candidate one interval shorter -- or returns a
             # shorter candidate; it is retried only when a later wave improves the best
-            dp_ok = (opts.prove and nprob.grid and prob.N == 1 and not prob.release_i32.any()
-                     and prob.J <= 64)
+            dp_ok = opts.prove and nprob.grid and prob.J <= 64 and prob.N <= 8
             proof, dp_tried_at, dp_cand = None, None, None
             while w0 < n_idx:
                 w1 = min(n_idx, w0 + wave)

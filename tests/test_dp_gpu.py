@@ -109,3 +109,46 @@ def test_solve_without_proof_keeps_local_status():
     w, t, _ = config_workload(3)
     sol = PL.solve(t, w, None, SolveOptions(prove=False))
     assert sol.status == "Local" and sol.makespan == 30 and not sol.search.proven
+
+
+def test_dp_multinode_prover_is_sound():
+    """Several nodes (heterogeneous, interchangeable, releases, initial free times): the wide
+    prover never calls a reachable target infeasible -- every INFEASIBLE at T has the oracle's
+    exhaustive optimum above T -- and it is FEASIBLE from the optimum up.  It proves the optimum
+    (INFEASIBLE at M* - 1) on most problems."""
+    eng = EN.Engine(0)
+    rng = random.Random(31)
+    proven = total = 0
+    for trial in range(40):
+        nodes = [[2, 2], [4, 4], [3, 2], [2, 2, 2], [4, 2, 1], [8, 8]][trial % 6]
+        op = random_problem(rng, rng.randint(2, 5), nodes, max_opts=3, max_d=8, hetero=trial % 3 == 0)
+        if trial % 4 == 1:
+            op.release = [rng.randint(0, 4) for _ in range(op.J)]
+        if trial % 5 == 2:
+            op.init_free = [sorted(rng.randint(0, 3) for _ in range(n)) for n in nodes]
+        prob = to_search_problem(op)
+        opt = int(C.CProblem(op).search()[0])
+        for target in range(max(0, opt - 3), opt + 2):
+            st, info, cand = dp(eng, prob, target)
+            assert cand is None and st != EN.SAT_DP_BUDGET
+            if st == EN.SAT_DP_INFEASIBLE:
+                assert target < opt, (trial, target, opt)
+            if target >= opt:
+                assert st == EN.SAT_DP_FEASIBLE, (trial, target, opt)
+        total += 1
+        proven += dp(eng, prob, opt - 1)[0] == EN.SAT_DP_INFEASIBLE
+    assert proven >= total * 3 // 4, (proven, total)
+
+
+def test_hetero6_local_plan_proven_or_improved():
+    """hetero6 (6 jobs, 8 + 4 GPU nodes, 2.3e11 candidates): the default solve is the local
+    search; its makespan must equal the exhaustive optimum (index kernel over the whole space)
+    and, when the prover closes the gap, carry status Optimal."""
+    w, t, prob, op = workload_problem("hetero6")
+    sol = PL.solve(t, w)
+    full = PL.solve(t, w, None, SolveOptions(search="exhaustive", kernel="index", max_exhaustive=1 << 40))
+    assert full.status == "Optimal"
+    assert sol.makespan == full.makespan
+    proof = (sol.search.stats or {}).get("proof")
+    assert proof is not None
+    assert sol.status == ("Optimal" if proof["proven"] else "Local")
