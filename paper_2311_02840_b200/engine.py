@@ -459,7 +459,7 @@ class Engine:
                     what="sat_search_dp", nprob=nprob)
         self.launches += max(1, info.levels)
         out = None
-        if info.status == SAT_DP_FEASIBLE:
+        if info.status == SAT_DP_FEASIBLE and info.makespan >= 0:      # (the prover rebuilds none)
             v = list(cand)
             out = (v[:J], v[J:])
         return info.status, info, out

@@ -99,10 +99,13 @@ def test_dp_budget_and_unsupported(eng):
     prob = build_problem(t, w)
     st, info, _ = dp(eng, prob, 29, 1000)
     assert st == EN.SAT_DP_BUDGET
-    w4, t4, _ = config_workload(4)                       # several nodes: not this kernel
+    w4, t4, _ = config_workload(4)                       # several nodes: the prover (no candidate)
     p4 = build_problem(t4, w4)
+    assert dp(eng, p4, 7)[0] == EN.SAT_DP_INFEASIBLE     # below the area bound: decided on the host
+    rng = random.Random(5)                               # > 8 nodes: beyond the prover
+    op = random_problem(rng, 3, [1] * 9, max_opts=2, max_d=4)
     with pytest.raises(E.TooLarge):
-        dp(eng, p4, 10)
+        dp(eng, to_search_problem(op), 3)
 
 
 def test_solve_without_proof_keeps_local_status():
