@@ -1,8 +1,10 @@
 """Extended parity sweep on one GPU (beyond the pytest suite's fixed trials): random one-node
 problems through the tree kernel (packed and 32-bit pair pass, every lane-prefix length) and
 bound-and-prune, random 1-4-node problems through the index kernel and the sampled stream,
-and local-search walkers (1 / 4 / 8 warps per walker) -- every key compared bit for bit with
-the CPU oracle.  Prints one summary line per family; any mismatch raises."""
+local-search walkers (1 / 4 / 8 / 16 / 32 warps per walker), and the state-space search (one node:
+INFEASIBLE at the oracle optimum - 1, FEASIBLE at it with a candidate the oracle replays within the
+target; several nodes: the prover never calls a reachable target infeasible) -- every key compared
+with the CPU oracle.  Prints one summary line per family; any mismatch raises."""
 import os
 import random
 import sys
@@ -73,7 +75,7 @@ for trial in range(max(8, N_TRIALS // 5)):
     nprob = EN.NativeProblem(prob, bits)
     cp = C.CProblem(op)
     stop = int(prob.lower_bound()) if trial % 2 else -1
-    for group in ("1", "4", "8"):
+    for group in ("1", "4", "8", "16", "32"):
         os.environ["SATURN_LS_GROUP"] = group
         for walker in (0, 7):
             _, o, r, _ = cp.local_search(walker, "substream", trial, 4096, stop_ms=stop)
@@ -81,5 +83,42 @@ for trial in range(max(8, N_TRIALS // 5)):
             assert got == (o, r), ("ls", trial, group, walker)
             checks += 1
 os.environ.pop("SATURN_LS_GROUP", None)
-print(f"local search: {checks} walks (1 / 4 / 8 warps per walker, with and without the stop) equal the oracle "
+print(f"local search: {checks} walks (1 / 4 / 8 / 16 / 32 warps per walker, with and without the stop) equal the oracle "
       f"({time.time() - t0:.0f} s)", flush=True)
+
+t0, checks, proven = time.time(), 0, 0
+for trial in range(N_TRIALS):
+    if trial % 2 == 0:
+        gsz = rng.choice([1, 2, 3, 4, 6, 8, 12, 16])
+        op = random_problem(rng, rng.randint(2, 6), [gsz], max_opts=3, max_d=rng.choice([6, 12]))
+        if trial % 3 == 0:
+            op.init_free = [sorted(rng.randint(0, 5) for _ in range(gsz))]
+        if trial % 5 == 1:
+            op.release = [rng.randint(0, 6) for _ in range(op.J)]
+        prob = to_search_problem(op)
+        cp = C.CProblem(op)
+        opt = int(cp.search()[0])
+        nprob = EN.NativeProblem(prob, 1)
+        st, _, _ = eng.dp_search(nprob, opt - 1, 1 << 20)
+        assert st == EN.SAT_DP_INFEASIBLE, ("dp", trial, opt)
+        st, info, cand = eng.dp_search(nprob, opt, 1 << 20)
+        assert st == EN.SAT_DP_FEASIBLE and cand is not None, ("dp", trial, opt)
+        assert cp.eval(*cand)[0] <= opt, ("dp replay", trial)
+        checks += 2
+    else:
+        nodes = [[2, 2], [4, 4], [3, 2], [2, 2, 2], [4, 2, 1]][trial % 5]
+        op = random_problem(rng, rng.randint(2, 5), nodes, max_opts=3, max_d=8, hetero=trial % 3 == 0)
+        if trial % 4 == 1:
+            op.release = [rng.randint(0, 4) for _ in range(op.J)]
+        prob = to_search_problem(op)
+        opt = int(C.CProblem(op).search()[0])
+        nprob = EN.NativeProblem(prob, 1)
+        for target in (opt - 1, opt):
+            st, _, _ = eng.dp_search(nprob, target, 1 << 20)
+            assert st != EN.SAT_DP_BUDGET
+            assert st == EN.SAT_DP_FEASIBLE or target < opt, ("prover", trial, target, opt)
+            checks += 1
+            proven += target == opt - 1 and st == EN.SAT_DP_INFEASIBLE
+print(f"state-space search: {N_TRIALS} random problems (1-16-GPU nodes and 2-3-node clusters, releases, initial "
+      f"free times), {checks} answers consistent with the oracle optimum; multi-node optimum proven on "
+      f"{proven} of {N_TRIALS // 2} ({time.time() - t0:.0f} s)", flush=True)

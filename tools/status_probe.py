@@ -1,3 +1,5 @@
+"""Status and time of the default solve on the small golden workloads and the SPEC.md:428-436
+mirror presets (1 and 2 nodes): python tools/status_probe.py"""
 import sys, os, time
 sys.path.insert(0, os.getcwd()); sys.path.insert(0, os.path.join(os.getcwd(), "tests"))
 import torch
@@ -11,7 +13,7 @@ for n in ["small5_1x4", "small4_2x2", "hetero6", "tiny3_1x3"]:
 for name in dir(WL):
     pass
 try:
-    for ds in ("wikitext", "imagenet"):
+    for ds in ("wikitext_mirror", "imagenet_mirror"):
         for nodes in (1, 2):
             w = WL.generate_workload(ds, nodes, seed=7) if hasattr(WL, "generate_workload") else None
             if w is not None: cases.append((f"{ds}_{nodes}n", w))
