@@ -123,6 +123,7 @@ class Solution:
     order: list                 # submission order (job axis indices)
     runtimes: dict = field(default_factory=dict)   # job id -> seconds of the chosen option/node
     lower_bound: float | None = None               # makespan lower bound (same unit as makespan)
+    cursor: object = None                          # resumable solves: the search cursor (resume.py)
 
     @property
     def gap(self) -> float:
@@ -187,15 +188,71 @@ class _nvtx:
 
 
 def solve(table, jobs, cluster=None, delta_opts=None, running_context=None, *, techniques=None,
-          group=None, device=None, validate: bool = True) -> Solution:
-    """Solver.solve / re-solve on the engine (build -> search -> decode -> check)."""
+          group=None, device=None, validate: bool = True, checkpoint=None,
+          time_budget_s: float | None = None) -> Solution:
+    """Solver.solve / re-solve on the engine (build -> search -> decode -> check).
+
+    ``checkpoint`` (a file path) and/or ``time_budget_s``: run the exact search resumably
+    (resume.py) -- when the budget runs out the search state is saved to ``checkpoint`` and the
+    Solution has status "Suspended" (the best plan found so far, or plan None); calling again
+    with the same checkpoint continues where it stopped."""
     workload = _as_workload(jobs, cluster, techniques)
     opts = _opts(delta_opts)
     with _nvtx("saturn.build_problem"):
         prob = build_problem(table, workload, opts, running_context)
+    if checkpoint is not None or time_budget_s is not None:
+        return _solve_resumable(prob, workload, opts, running_context, checkpoint, time_budget_s, device,
+                                validate)
     with _nvtx("saturn.solve_problem"):
         return solve_problem(prob, workload, opts, running_context, group=group, device=device,
                              validate=validate)
+
+
+def _solve_resumable(prob, workload, opts, running_context, checkpoint, time_budget_s, device, validate):
+    import os
+
+    from . import resume as R
+
+    eng = get_engine(device)
+    cur = None
+    if checkpoint is not None and os.path.exists(checkpoint):
+        cur = R.SearchCursor.load(checkpoint)
+        if cur.digest != R.problem_digest(prob):
+            cur = None                                  # a stale checkpoint of another problem
+    if cur is None:
+        cur = R.start_cursor(eng, prob, opts)
+    with _nvtx("saturn.search_resumable"):
+        R.run_cursor(eng, prob, cur, time_budget_s)
+    found = R.cursor_result(prob, cur)
+    plan, options, runtimes, ms = None, [], {}, float("inf")
+    if found is not None:
+        ms, index = found
+        nprob = NativeProblem(prob, cur.idx_bits)
+        plan, options, ms2, runtimes = _decode(eng, prob, nprob, workload, SRC_INDEX, 0, ident=index)
+        if ms2 != ms:
+            raise E.errors_for(workload.jobs[0]).PlanFailure(f"replay makespan {ms2} != search makespan {ms}")
+    if cur.done:
+        if checkpoint is not None and os.path.exists(checkpoint):
+            os.remove(checkpoint)
+        if plan is None:
+            raise E.errors_for(workload.jobs[0]).PlanFailure("search produced no candidate")
+        if validate:
+            target = workload
+            if running_context is not None:
+                keep = set(prob.job_ids)
+                target = _WorkloadView(tuple(j for j in workload.jobs if j.id in keep), workload.cluster,
+                                       tuple(workload.techniques))
+            _validator_for(workload)(plan, target, runtimes)
+        status, lb = "Optimal", ms
+    else:
+        if checkpoint is not None:
+            cur.save(checkpoint)
+        status, lb = "Suspended", prob.lower_bound()
+    order = prob.decode_index(found[1])[1] if found is not None else []
+    return Solution(plan=plan, status=status, makespan=ms, lower_bound=lb,
+                    objective=plan.predicted_makespan if plan is not None else float("inf"), problem=prob,
+                    search=None, options=options, order=order, runtimes=runtimes,
+                    cursor=cur)
 
 
 def solve_problem(prob: SearchProblem, workload, opts: SolveOptions, running_context=None, *, group=None,
