@@ -97,9 +97,10 @@ def start_cursor(eng, prob: SearchProblem, opts: SolveOptions) -> SearchCursor:
 
 
 def run_cursor(eng, prob: SearchProblem, cur: SearchCursor, time_budget_s: float | None = None,
-               chunk: int | None = None) -> SearchCursor:
-    """Advance the cursor chunk by chunk until the range is done or the time budget is spent.
-    Chunks grow geometrically from 1/256 of the range, each sized to ~1/8 of the budget."""
+               chunk: int | None = None, max_chunks: int | None = None) -> SearchCursor:
+    """Advance the cursor chunk by chunk until the range is done, the time budget is spent or
+    max_chunks chunks ran.  Chunks grow geometrically from 1/256 of the range, each sized to
+    ~1/8 of the budget."""
     torch = eng.torch
     if cur.digest != problem_digest(prob):
         raise E.errors_for(prob.jobs[0] if prob.jobs else prob).InvariantViolation(
@@ -108,7 +109,9 @@ def run_cursor(eng, prob: SearchProblem, cur: SearchCursor, time_budget_s: float
     best = torch.empty(2, dtype=torch.int64, device=eng.device)
     t_start = time.perf_counter()
     size = chunk or max(1, (cur.end - cur.next) // 256)
-    while not cur.done:
+    ran = 0
+    while not cur.done and (max_chunks is None or ran < max_chunks):
+        ran += 1
         lo, hi = cur.next, min(cur.end, cur.next + size)
         st = eng.lib.sat_best_set(_vp(best.data_ptr()), cur.key & ((1 << 64) - 1), (1 << 64) - 1,
                                   _vp(eng.stream()))
