@@ -113,8 +113,9 @@ def run_cursor(eng, prob: SearchProblem, cur: SearchCursor, time_budget_s: float
     while not cur.done and (max_chunks is None or ran < max_chunks):
         ran += 1
         lo, hi = cur.next, min(cur.end, cur.next + size)
-        st = eng.lib.sat_best_set(_vp(best.data_ptr()), cur.key & ((1 << 64) - 1), (1 << 64) - 1,
-                                  _vp(eng.stream()))
+        # the device cell's "nothing yet" is all ones (the kernels test for it), not INT64_MAX
+        cell = (1 << 64) - 1 if cur.key == INT64_MAX else cur.key
+        st = eng.lib.sat_best_set(_vp(best.data_ptr()), cell, (1 << 64) - 1, _vp(eng.stream()))
         eng._check(st, nprob=nprob)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
