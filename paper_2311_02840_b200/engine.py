@@ -686,7 +686,9 @@ class Engine:
                     dp_tried_at = k >> idx_bits
                     try:
                         proven, dp_ms, cand, proof = self.prove_below(prob, dp_tried_at, opts)
-                    except E.TooLarge:              # state key does not fit 63 bits: no proof
+                    except (E.TooLarge, err.TooLarge, E.InvariantViolation, err.InvariantViolation):
+                        # a shape the state-space search does not take (key width, > 8 nodes):
+                        # no proof, the local search's result stands
                         dp_ok, proven, cand = False, False, None
                     if cand is not None:
                         dp_cand = (dp_ms, cand)

@@ -182,3 +182,19 @@ def test_simulate_with_reference_objects_equals_mirror():
     assert seen and all(c is core.RunningContext for c in seen)
     assert rep.replan_count == mrep.replan_count > 0
     assert rep.to_json() == mrep.to_json()
+
+
+def test_local_search_beyond_the_prover_reference_objects():
+    """A reference workload whose shape the state-space prover does not take (9 nodes): the
+    default solve falls back to the local search's result (the prover's TooLarge is the caller's
+    own error class and must not escape)."""
+    core, profiling, _ = import_reference()
+    w, _ = golden_workload("small5_1x4")
+    rw = ref_workload(core, w)
+    nodes = [core.NodeSpec(id=f"m{i}", gpu_count=1, gpu_memory=80.0) for i in range(9)]
+    jobs = [rw.jobs[0].model_copy(update={"id": f"k{i:02d}", "model_memory": 10.0}) for i in range(14)]
+    big = core.Workload(jobs=jobs, cluster=core.ClusterSpec(nodes=nodes), techniques=rw.techniques)
+    rt = profiling.build_profile_table(big, profiling.SyntheticExecutor(big.cluster))
+    sol = PL.solve(rt, big)
+    assert sol.search.kernel == "local" and sol.status in ("Local", "Optimal")
+    core.check_plan(sol.plan, big, ref_runtimes(profiling, rt, big, sol.plan))
