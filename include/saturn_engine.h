@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define SAT_ABI_VERSION 4
+#define SAT_ABI_VERSION 5
 
 /* status codes (mapped to reference errors.py classes by the host layer) */
 #define SAT_OK              0
@@ -151,7 +151,10 @@ int sat_search_bnb(const sat_problem_t *p, int32_t prefix_len,
 /* Local search from sampled starting points (grid time): walker w starts at candidate w of
  * `source` (SAT_SRC_SUBSTREAM / SAT_SRC_SEED) and descends over swap / option / insertion
  * moves on (makespan, total GPU load) until no move improves or max_rounds rounds of 32
- * moves were scanned.  Result: (makespan << idx_bits) | walker.
+ * moves were scanned.  Result (ABI v5): the lowest
+ * (makespan, rounds scanned, walker) as (makespan << (idx_bits + SAT_LS_ROUND_BITS)) |
+ * (rounds << idx_bits) | walker -- among walkers ending at the same makespan, the one that got
+ * there in the fewest rounds, then the lowest id (max_rounds < 2^SAT_LS_ROUND_BITS).
  * d_state_out (device, (hi - lo) x 2J bytes, or null) receives the final candidate of every
  * walker w (options then order, at (w - lo) * 2J) -- the winner's plan without a replay;
  * entries of abandoned walkers (below) are left untouched.  The number of rounds
@@ -159,8 +162,10 @@ int sat_search_bnb(const sat_problem_t *p, int32_t prefix_len,
  * after the walker cursor, which follows the problem blob at offset
  * sat_ls_counter_offset(p).  stop_ms >= 0 (the problem's lower bound): a walker ends as
  * soon as its makespan is <= stop_ms (its final state is the candidate at that point), and a
- * walker whose id is above that of a key already in *d_best with makespan <= stop_ms is
- * abandoned; neither changes the result.  stop_ms < 0: walks run to their local optimum. */
+ * still-running walker that has scanned at least as many rounds as a key already in *d_best
+ * with makespan <= stop_ms is abandoned; neither changes the result.  stop_ms < 0: walks run
+ * to their local optimum. */
+#define SAT_LS_ROUND_BITS 13
 int sat_ls_counter_offset(const sat_problem_t *p, size_t *offset);
 int sat_local_search(const sat_problem_t *p, int32_t source, uint64_t seed, uint64_t lo, uint64_t hi,
                      int32_t max_rounds, int32_t stop_ms, sat_best_t *d_best, uint8_t *d_state_out,

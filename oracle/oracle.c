@@ -233,7 +233,8 @@ int oracle_decode(const oproblem *p, int source, uint64_t seed, uint64_t id, int
  *   holding a move with objective < current applies its best move (lowest objective, then
  *   lowest id) and the scan restarts at 0; a scan without improvement, or max_rounds
  *   rounds in total, ends the walk; with stop_ms >= 0 (the problem's lower bound) the walk
- *   also ends as soon as the current makespan is <= stop_ms. */
+ *   also ends as soon as the current makespan is <= stop_ms.
+ *   search over walkers: the lowest (makespan, rounds scanned, walker). */
 static int ls_counts(const oproblem *p, int *M1, int *M2) {
     int J = p->J, m2 = 0;
     for (int j = 0; j < J; ++j) m2 += p->radix[j] - 1;
@@ -310,13 +311,17 @@ int oracle_ls_search(const oproblem *p, int source, uint64_t seed, uint64_t lo, 
     double gms = INFINITY;
     uint64_t gid = UINT64_MAX;
     if (threads < 1) threads = omp_get_max_threads();
+    int grounds = INT32_MAX;
 #pragma omp parallel for schedule(dynamic, 1) num_threads(threads)
     for (long long w = (long long)lo; w < (long long)hi; ++w) {
-        int opt[OMAX_J], ord[OMAX_J];
-        double ms = oracle_local_search(p, source, seed, (uint64_t)w, max_rounds, stop_ms, opt, ord, NULL);
+        int opt[OMAX_J], ord[OMAX_J], rounds = 0;
+        double ms = oracle_local_search(p, source, seed, (uint64_t)w, max_rounds, stop_ms, opt, ord, &rounds);
 #pragma omp critical
         {
-            if (ms < gms || (ms == gms && (uint64_t)w < gid)) { gms = ms; gid = (uint64_t)w; }
+            /* (makespan, rounds scanned, walker) lexicographic: the engine's local-search key */
+            if (ms < gms || (ms == gms && (rounds < grounds || (rounds == grounds && (uint64_t)w < gid)))) {
+                gms = ms; grounds = rounds; gid = (uint64_t)w;
+            }
         }
     }
     *best_ms = gms;

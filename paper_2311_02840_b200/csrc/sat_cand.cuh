@@ -799,8 +799,25 @@ k_ls(LsArgs a) {
     // the prefix cache pays off only on long orders (measured: +10 % at 64 jobs, -15 % at 16)
     const bool use_cache = J >= 24;
 
-    T best_ms = INF;                       // group leader: the group's best (makespan, walker)
-    uint64_t best_ix = ~0ull;
+    // keys: (makespan, rounds the walk scanned, walker) lexicographic -- among walkers ending at
+    // the same makespan the one that got there in the fewest rounds wins (then the lowest id), so
+    // a running walker that has already scanned as many rounds as a published key at the bound
+    // can no longer win and is abandoned (the wave ends when its fastest walker reaches the bound
+    // plus the rounds every other walker needs to fall behind it)
+    constexpr int RB = SAT_LS_ROUND_BITS;
+    const int ib = a.idx_bits;
+    auto walker_key = [&](T ms, int r, uint64_t w) -> uint64_t {
+        const uint64_t rr = (uint64_t)min(r, (1 << RB) - 1);
+        return ((uint64_t)(uint32_t)ms << (ib + RB)) | (rr << ib) | w;
+    };
+    // published key at <= stop_ms with at most `r` rounds: a still-running walker (its final
+    // round count will exceed r) cannot beat it
+    auto beaten_at = [&](int r) -> bool {
+        const unsigned long long k = *reinterpret_cast<volatile unsigned long long *>(&a.best->hi);
+        return k != ~0ull && (int64_t)(k >> (ib + RB)) <= (int64_t)a.stop_ms &&
+               (int64_t)((k >> ib) & ((1ull << RB) - 1ull)) <= (int64_t)r;
+    };
+    uint64_t best_key = ~0ull;             // group leader: the group's best walker key
     const uint64_t total = a.hi - a.lo;
 #ifdef SAT_LS_PROFILE
     // steps, improving steps, cycles evaluating (+ barrier wait), cycles applying, sum of the
@@ -840,9 +857,9 @@ k_ls(LsArgs a) {
         T cur = (T)(cur_key >> 34);
         int rounds = 0;
         // Early stop (stop_ms = the problem's lower bound): the makespan never rises along a
-        // walk, so a walker at stop_ms has its final key (stop_ms, id) and ends there; a walker
-        // whose id is above that of a published key at <= stop_ms cannot win and is abandoned.
-        // Neither changes the search result.
+        // walk, so a walker at stop_ms has its final key (stop_ms, rounds, id) and ends there; a
+        // still-running walker that has scanned at least as many rounds as a published key at
+        // <= stop_ms cannot win and is abandoned.  Neither changes the search result.
         bool abandoned = false;
         for (;;) {
             if (cur <= a.stop_ms) break;
@@ -920,15 +937,9 @@ k_ls(LsArgs a) {
                     gsync();                          // every thread has read the slots
                     if (leader) {
                         const LsMove &mv = amv;
-                        // a walker whose id is above a published key at <= stop_ms cannot win:
-                        // it is abandoned (checked once per applied move)
-                        if (a.stop_ms >= 0) {
-                            const unsigned long long k = *reinterpret_cast<volatile unsigned long long *>(&a.best->hi);
-                            s_beaten[grp] = k != ~0ull && (int64_t)(k >> a.idx_bits) <= (int64_t)a.stop_ms &&
-                                            (k & ((1ull << a.idx_bits) - 1ull)) < id;
-                        } else {
-                            s_beaten[grp] = 0;
-                        }
+                        // still running after this move (not yet at stop_ms) and already behind a
+                        // published key at the bound: abandoned
+                        s_beaten[grp] = a.stop_ms >= 0 && (T)(nk >> 34) > a.stop_ms && beaten_at(rounds + first + 1);
                         if (mv.kind == 0) {
                             const uint8_t t = word[mv.a]; word[mv.a] = word[mv.b]; word[mv.b] = t;
                         } else if (mv.kind == 1) {
@@ -960,18 +971,25 @@ k_ls(LsArgs a) {
                     break;
                 }
                 rounds += nvalid;
-                if constexpr (K > 1) gsync();         // slots are rewritten by the next rounds
+                if (a.stop_ms >= 0) {                 // fallen behind a published key at the bound?
+                    if (leader) s_beaten[grp] = beaten_at(rounds);
+                    gsync();                          // (also: slots are rewritten by the next rounds)
+                    const bool beaten = s_beaten[grp] != 0;
+                    gsync();
+                    if (beaten) { abandoned = true; break; }
+                } else if constexpr (K > 1) {
+                    gsync();                          // slots are rewritten by the next rounds
+                }
                 if (nvalid < K) break;                // scan exhausted or round budget spent
             }
             if (!improved || rounds >= a.max_rounds) break;
         }
         if (leader) {
-            if (!abandoned && key_less(cur, id, best_ms, best_ix)) {
-                best_ms = cur;
-                best_ix = id;
-                if (cur <= a.stop_ms)      // publish now: later walkers above this id are abandoned
-                    atomicMin(reinterpret_cast<unsigned long long *>(&a.best->hi),
-                              ((unsigned long long)(uint32_t)cur << a.idx_bits) | id);
+            const uint64_t wkey = walker_key(cur, rounds, id);
+            if (!abandoned && wkey < best_key) {
+                best_key = wkey;
+                if (cur <= a.stop_ms)      // publish now: walkers behind it are abandoned
+                    atomicMin(reinterpret_cast<unsigned long long *>(&a.best->hi), (unsigned long long)wkey);
             }
             atomicAdd(a.rounds, (unsigned long long)rounds + 1ull);   // + the start's round
 #ifdef SAT_LS_PROFILE
@@ -985,10 +1003,8 @@ k_ls(LsArgs a) {
         }
         gsync();
     }
-    if (leader && best_ms < INF) {
-        const uint64_t key = ((uint64_t)(uint32_t)best_ms << h.idx_bits) | best_ix;
-        atomicMin(reinterpret_cast<unsigned long long *>(&a.best->hi), (unsigned long long)key);
-    }
+    if (leader && best_key != ~0ull)
+        atomicMin(reinterpret_cast<unsigned long long *>(&a.best->hi), (unsigned long long)best_key);
 }
 
 template <int SRC>

@@ -1018,11 +1018,12 @@ int sat_local_search(const sat_problem_t *p, int32_t source, uint64_t seed, uint
     NvtxRange nvtx("sat_local_search");
     int st = validate(p);
     if (st) return st;
-    if (!d_best || hi < lo || max_rounds < 0) return SAT_ERR_INVALID;
+    if (!d_best || hi < lo || max_rounds < 0 || max_rounds >= (1 << SAT_LS_ROUND_BITS)) return SAT_ERR_INVALID;
     if (source != SAT_SRC_SUBSTREAM && source != SAT_SRC_SEED) return SAT_ERR_INVALID;
     if (p->time_mode != SAT_TIME_GRID_I32) return SAT_ERR_UNSUPPORTED;
     if (p->J < 2) return SAT_ERR_UNSUPPORTED;
     if (hi > 0 && ((hi - 1) >> p->idx_bits)) return SAT_ERR_TOO_LARGE;
+    if (p->idx_bits + SAT_LS_ROUND_BITS > 56) return SAT_ERR_TOO_LARGE;     // the makespan keeps >= 7 bits
     if (hi == lo) return SAT_OK;
     LsArgs a{};
     a.lo = lo; a.hi = hi; a.seed = seed; a.max_rounds = max_rounds; a.best = d_best; a.state_out = d_state_out;

@@ -26,6 +26,13 @@ SAT_OK, SAT_ERR_INVALID, SAT_ERR_NO_OPTIONS, SAT_ERR_TOO_LARGE, SAT_ERR_UNSUPPOR
 SAT_TIME_GRID_I32, SAT_TIME_F64 = 0, 1
 SRC_INDEX, SRC_SUBSTREAM, SRC_SEED, SRC_EXPLICIT = 0, 1, 2, 3
 INT64_MAX = (1 << 63) - 1
+LS_ROUND_BITS = 13          # SAT_LS_ROUND_BITS: local-search keys are (makespan, rounds, walker)
+
+
+def ls_key_fields(key: int, idx_bits: int) -> tuple:
+    """(makespan, rounds scanned, walker) of a packed local-search key (include/saturn_engine.h)."""
+    return (key >> (idx_bits + LS_ROUND_BITS), (key >> idx_bits) & ((1 << LS_ROUND_BITS) - 1),
+            key & ((1 << idx_bits) - 1))
 
 _vp = ctypes.c_void_p
 _i32 = ctypes.c_int32
@@ -102,7 +109,7 @@ def load_library(path: str = LIB_PATH):
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res
-    if lib.sat_abi_version() != 4:
+    if lib.sat_abi_version() != 5:
         raise E.PlanFailure("libsaturn_b200.so ABI version mismatch")
     _LIB = lib
     return lib
@@ -406,7 +413,7 @@ class Engine:
             # makes the exact search prune far more (seconds saved at 10-12 jobs)
             self.reset_best(tmp)
             self.local_search(sprob, SRC_SUBSTREAM, seed, 0, 4096, 4096, tmp, stop_ms=int(prob.lower_bound()))
-            bound = min(bound, (int(tmp[0].item()) & ((1 << 64) - 1)) >> s_bits)
+            bound = min(bound, ls_key_fields(int(tmp[0].item()) & ((1 << 64) - 1), s_bits)[0])
         return bound
 
     def seed_upper_bound(self, prob: SearchProblem, nprob: NativeProblem, best, budget: int = 1 << 16,
@@ -600,7 +607,9 @@ class Engine:
                     raise err.TooLarge(f"key needs {idx_bits}+{seed_ms.bit_length()} bits > 63")
                 mode, n_idx, use_bnb = "local", int(opts.walkers), False
         if not use_bnb:
-            idx_bits, _ = prob.key_bits(n_idx)
+            idx_bits, ms_bits = prob.key_bits(n_idx)
+            if mode == "local" and idx_bits + LS_ROUND_BITS + ms_bits > 63:
+                raise err.TooLarge(f"local-search key needs {idx_bits}+{LS_ROUND_BITS}+{ms_bits} bits > 63")
         nprob = NativeProblem(prob, idx_bits)
         launches0 = self.launches
         best = self.reset_best()
@@ -680,10 +689,11 @@ class Engine:
                 if shared is not None:
                     shared.collect(best)
                 k = int(_combine(best, True, group, world)[0])
-                if k != INT64_MAX and (k >> idx_bits) <= target:
+                k_ms = ls_key_fields(k, idx_bits)[0]
+                if k != INT64_MAX and k_ms <= target:
                     break
-                if dp_ok and k != INT64_MAX and dp_tried_at != (k >> idx_bits):
-                    dp_tried_at = k >> idx_bits
+                if dp_ok and k != INT64_MAX and dp_tried_at != k_ms:
+                    dp_tried_at = k_ms
                     try:
                         proven, dp_ms, cand, proof = self.prove_below(prob, dp_tried_at, opts)
                     except (E.TooLarge, err.TooLarge, E.InvariantViolation, err.InvariantViolation):
@@ -735,6 +745,9 @@ class Engine:
             makespan = float(k >> idx_bits)
             index = k & ((1 << idx_bits) - 1)
             if mode == "local":
+                ms_, rounds_, index = ls_key_fields(k, idx_bits)
+                makespan = float(ms_)
+                stats["winner_rounds"] = rounds_
                 ls_state = self._walker_state(ls_states, index, prob.J, group, world)
                 if dp_cand is not None and dp_cand[0] < makespan:
                     # the state-space search found a shorter candidate than every walker

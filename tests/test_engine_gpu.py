@@ -369,15 +369,17 @@ def test_local_search_walkers_match_oracle(eng, name, seed):
     best = eng.reset_best()
     eng.local_search(nprob, EN.SRC_SUBSTREAM, seed, 0, W, rounds, best)
     k = int(best.cpu().numpy().view(np.uint64)[0])
-    assert (float(k >> bits), k & ((1 << bits) - 1)) == cp.ls_search("substream", seed, 0, W, rounds)
+    ms_, rr_, wk_ = EN.ls_key_fields(k, bits)          # (makespan, rounds scanned, walker)
+    assert (float(ms_), wk_) == cp.ls_search("substream", seed, 0, W, rounds)
+    assert rr_ == cp.local_search(wk_, "substream", seed, rounds)[3]
 
 
 @pytest.mark.parametrize("name", ["cfg3", "cfg4", "cfg5", "hetero6"])
 def test_local_search_stop_at_bound(eng, name):
     """stop_ms = the lower bound: each walker's walk ends at its first candidate with that
-    makespan (same final state as the oracle's restatement with the same rule), later walkers
-    are abandoned once a lower-id walker reached the bound, and the search key over a walker
-    range equals the oracle's full-walk key."""
+    makespan (same final state as the oracle's restatement with the same rule), walkers fall
+    out once they have scanned as many rounds as a published key at the bound, and the search
+    key -- lowest (makespan, rounds, walker) -- over a walker range equals the oracle's."""
     w, t, prob, op = workload_problem(name)
     cp = C.CProblem(op)
     lb = int(prob.lower_bound())
@@ -394,8 +396,10 @@ def test_local_search_stop_at_bound(eng, name):
         best = eng.reset_best()
         eng.local_search(nprob, EN.SRC_SUBSTREAM, 7, 0, W, rounds, best, stop_ms=stop)
         k = int(best.cpu().numpy().view(np.uint64)[0])
-        got = (float(k >> bits), k & ((1 << bits) - 1))
+        ms_, rr_, wk_ = EN.ls_key_fields(k, bits)
+        got = (float(ms_), wk_)
         assert got == cp.ls_search("substream", 7, 0, W, rounds, stop_ms=stop)
+        assert rr_ == cp.local_search(wk_, "substream", 7, rounds, stop_ms=stop)[3]
         full_key = cp.ls_search("substream", 7, 0, W, rounds)
         if full_key[0] > stop:                         # the bound was not reached: same key as the full walks
             assert got == full_key
@@ -448,7 +452,8 @@ def test_local_search_wide_nodes_register_path(eng, group, monkeypatch):
         best = eng.reset_best()
         eng.local_search(nprob, EN.SRC_SUBSTREAM, 3, 0, 32, 4096, best)
         k = int(best.cpu().numpy().view(np.uint64)[0])
-        assert (float(k >> bits), k & ((1 << bits) - 1)) == cp.ls_search("substream", 3, 0, 32, 4096), trial
+        ms_, _, wk_ = EN.ls_key_fields(k, bits)
+        assert (float(ms_), wk_) == cp.ls_search("substream", 3, 0, 32, 4096), trial
 
 
 def test_local_search_seed_source_and_release(eng):

@@ -26,4 +26,4 @@ e0.record()
 eng.local_search(nprob, EN.SRC_SUBSTREAM, 7, 0, walkers, 4096, best, stop_ms=int(prob.lower_bound()))
 e1.record()
 torch.cuda.synchronize()
-print(f"cfg{cfg} walkers={walkers} ms={int(best[0].item()) >> bits} dev_ms={e0.elapsed_time(e1):.2f}")
+print(f"cfg{cfg} walkers={walkers} ms={EN.ls_key_fields(int(best[0].item()), bits)[0]} dev_ms={e0.elapsed_time(e1):.2f}")

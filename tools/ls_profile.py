@@ -36,4 +36,4 @@ for cfg in [int(x) for x in (sys.argv[1:] or ["3", "4", "5"])]:
         rounds, steps, imp, ev, ap, pos = c
         print(f"cfg{cfg} walkers [{lo},{hi}) dev_ms={e0.elapsed_time(e1):.2f} rounds={rounds} steps={steps} "
               f"improving={imp} eval_cyc/step={ev / max(1, steps):.0f} apply_cyc/improving={ap / max(1, imp):.0f} "
-              f"mean_improving_round={pos / max(1, imp):.2f} best={int(best[0].item()) >> bits}", flush=True)
+              f"mean_improving_round={pos / max(1, imp):.2f} best={EN.ls_key_fields(int(best[0].item()), bits)[0]}", flush=True)

@@ -35,7 +35,7 @@ for cfg in [int(x) for x in (sys.argv[1:] or ["4", "5"])]:
         e1.record()
         torch.cuda.synchronize()
         rounds = int(eng._ws[off.value:off.value + 8].view(torch.int64).item())
-        ms = int(best[0].item()) >> bits
+        ms = EN.ls_key_fields(int(best[0].item()), bits)[0]
         rows.append((wk, ms, rounds, e0.elapsed_time(e1)))
     print(f"cfg{cfg} lb={lb} winner={res.index} ms={res.makespan} dev_ms={1e3 * res.search.device_seconds if hasattr(res, 'search') else res.device_seconds:.2f}")
     for r in rows:
