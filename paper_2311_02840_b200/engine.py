@@ -726,7 +726,9 @@ class Engine:
             shared.collect(best)
         key_dev = _combine_dev(best, nprob.grid, group, world)
         replay_out = None
-        if replay and nprob.grid and bnb_ws is None and mode in ("exhaustive", "sampled"):
+        if replay and nprob.grid and mode in ("exhaustive", "sampled"):
+            # (bound-and-prune too: its key always holds a real candidate -- the seed bound comes
+            # from a candidate of the same space, which the search itself reaches)
             kk = key_dev[:1]
             idx = kk & ((1 << idx_bits) - 1)
             bad = kk == INT64_MAX
@@ -734,12 +736,14 @@ class Engine:
                 bad = bad | (idx >= n_idx)
             ids_dev = torch.where(bad, torch.zeros_like(idx), idx)     # an id the decode can take
             replay_out = self.schedule(nprob, src, seed_used, ids_dev=ids_dev)
-        key = key_dev.cpu().tolist()
+        if bnb_ws is not None:               # key and the search's counters in one read-back
+            both = torch.cat([key_dev, bnb_ws[:24].view(torch.int64)]).cpu().tolist()
+            key, cnt = both[:2], both[2:]
+            stats.update(pruned_tasks=cnt[1], pair_nodes=cnt[2])
+        else:
+            key = key_dev.cpu().tolist()
         ev1.synchronize()
         dev_s = ev0.elapsed_time(ev1) / 1e3
-        if bnb_ws is not None:
-            cnt = bnb_ws[:24].view(torch.int64).cpu().tolist()
-            stats.update(pruned_tasks=cnt[1], pair_nodes=cnt[2])
         if shared is not None:
             stats = {**(stats or {}), "shared_incumbent": True}
         if nprob.grid:
