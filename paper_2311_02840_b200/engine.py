@@ -725,6 +725,9 @@ class Engine:
         if shared is not None:
             shared.collect(best)
         key_dev = _combine_dev(best, nprob.grid, group, world)
+        # bound-and-prune's counters sit at the start of the workspace, which the replay's
+        # launch below reuses: keep a device copy first
+        cnt_dev = bnb_ws[:24].view(torch.int64).clone() if bnb_ws is not None else None
         replay_out = None
         if replay and nprob.grid and mode in ("exhaustive", "sampled"):
             # (bound-and-prune too: its key always holds a real candidate -- the seed bound comes
@@ -737,7 +740,7 @@ class Engine:
             ids_dev = torch.where(bad, torch.zeros_like(idx), idx)     # an id the decode can take
             replay_out = self.schedule(nprob, src, seed_used, ids_dev=ids_dev)
         if bnb_ws is not None:               # key and the search's counters in one read-back
-            both = torch.cat([key_dev, bnb_ws[:24].view(torch.int64)]).cpu().tolist()
+            both = torch.cat([key_dev, cnt_dev]).cpu().tolist()
             key, cnt = both[:2], both[2:]
             stats.update(pruned_tasks=cnt[1], pair_nodes=cnt[2])
         else:
