@@ -679,7 +679,7 @@ class Engine:
             # after a wave that misses the lower bound, the state-space search (one node) either
             # proves the wave's best optimal -- no candidate one interval shorter -- or returns a
             # shorter candidate; it is retried only when a later wave improves the best
-            dp_ok = opts.prove and nprob.grid and prob.J <= 64 and prob.N <= 8
+            dp_ok = opts.prove and nprob.grid and prob.J <= min(64, opts.dp_max_jobs) and prob.N <= 8
             proof, dp_tried_at, dp_cand = None, None, None
             while w0 < n_idx:
                 w1 = min(n_idx, w0 + wave)

@@ -60,7 +60,11 @@ class SolveOptions:
     kernel: str = "auto"                # auto (bnb when it applies) | tree | index | bnb
     prove: bool = True                  # local search on one node: prove / improve the best makespan
                                         # with the state-space search (sat_search_dp) after a wave
-    dp_states: int = 1 << 22            # state budget of one sat_search_dp call (all levels)
+    dp_states: int = 1 << 21            # state budget of one sat_search_dp call (all levels)
+    dp_max_jobs: int = 20               # attempt the proof only up to this many jobs: beyond, the
+                                        # state space explodes unless the slack is tiny, and a
+                                        # failed attempt costs its whole budget (cfg4 at T = 8:
+                                        # ~80 ms to exhaust 4 M states)
     share_incumbent: bool = True        # several ranks: one incumbent cell over NVLink peer memory
 
 
