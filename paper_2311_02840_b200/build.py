@@ -49,6 +49,15 @@ def up_to_date(out_path: str = OUT) -> bool:
     return all(os.path.getmtime(f) <= t for f in sources() + [__file__])
 
 
+def _obj_fresh(src: str, obj: str) -> bool:
+    """An object is reused when it is newer than its own .cu, every header and this file."""
+    if not os.path.exists(obj):
+        return False
+    deps = [src, HDR, __file__] + glob.glob(os.path.join(CSRC, "*.cuh"))
+    t = os.path.getmtime(obj)
+    return all(os.path.getmtime(f) <= t for f in deps)
+
+
 def units(obj_dir: str = OBJ_DIR) -> list:
     """(source, extra defines, object) for every translation unit."""
     OBJ_DIR = obj_dir  # noqa: N806 (local rebinding keeps the table below readable)
@@ -74,6 +83,8 @@ def build(force: bool = False, verbose: bool = False, debug: bool = False) -> st
     cc = nvcc()
     procs = []
     for src, defs, obj in units(obj_dir):
+        if not force and _obj_fresh(src, obj):
+            continue
         cmd = [cc, *NVCC_FLAGS, *extra, *defs, "-c", "-o", obj, src]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)

@@ -45,6 +45,9 @@ struct DpParams {
     uint8_t ug[kDpMaxOpt];            // gang size of usable option q
     int16_t ud[kDpMaxOpt];            // duration of usable option q
     int16_t dg[kDpMaxJ][32];          // least usable duration of job j at gang k+1 (T+1: none)
+    uint32_t dgp[kDpMaxJ][16];        // dg as 16-bit pairs (gangs 2w+1, 2w+2), for VIADDMNMX.U16x2
+    int32_t nrem;                     // jobs still to place in the level being expanded
+    int32_t has_release;
     const uint64_t *binom;            // [(T + Gr + 1)][Gr + 1]: C(n, k)
     uint64_t *table;                  // hash set of state keys, kDpEmpty = free
     uint64_t cap_mask;
@@ -106,15 +109,50 @@ __device__ __forceinline__ bool dp_viable(const DpParams &p, uint64_t R2, const 
     return area <= (int64_t)p.T * p.Gr;
 }
 
+// the same test on 16-bit pairs: each remaining job's earliest end is GM/2 fused add-mins
+// (VIADDMNMX.U16x2) of the packed state and its packed least durations; free times and
+// durations are <= T + 1 <= 30001 and padding 0x7FFF, so no pair sum carries
+template <int GM>
+__device__ __forceinline__ bool dp_viable16(const DpParams &p, uint64_t R2, const int32_t *b) {
+    constexpr int W = GM / 2;
+    uint32_t bp[W];
+    int64_t area = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+        const uint32_t lo = 2 * w < p.Gr ? (uint32_t)b[2 * w] : 0x7FFFu;
+        const uint32_t hi = 2 * w + 1 < p.Gr ? (uint32_t)b[2 * w + 1] : 0x7FFFu;
+        bp[w] = lo | (hi << 16);
+        area += (2 * w < p.Gr ? b[2 * w] : 0) + (2 * w + 1 < p.Gr ? b[2 * w + 1] : 0);
+    }
+    for (uint64_t m = R2; m; m &= m - 1) {
+        const int i = __ffsll((long long)m) - 1;
+        area += p.minarea[i];
+        uint32_t m2 = 0xFFFFFFFFu;
+        if (p.has_release) {
+            const uint32_t r2 = (uint32_t)p.release[i] * 0x10001u;
+#pragma unroll
+            for (int w = 0; w < W; ++w) m2 = __viaddmin_u16x2(__vmaxu2(bp[w], r2), p.dgp[i][w], m2);
+        } else {
+#pragma unroll
+            for (int w = 0; w < W; ++w) m2 = __viaddmin_u16x2(bp[w], p.dgp[i][w], m2);
+        }
+        if ((int32_t)min(m2 & 0xFFFFu, m2 >> 16) > p.T) return false;
+    }
+    return area <= (int64_t)p.T * p.Gr;
+}
+
 template <int GM>
 __global__ void __launch_bounds__(kDpThreads) k_dp_expand(const __grid_constant__ DpParams p) {
+    // one thread per (state, job still to place): the level's states all have nrem such jobs
     const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (tid >= p.n_in * (uint64_t)p.J) return;
+    if (tid >= p.n_in * (uint64_t)p.nrem) return;
     if (*reinterpret_cast<volatile unsigned int *>(p.overflow)) return;
-    const uint64_t s = tid / (uint64_t)p.J;
-    const int j = (int)(tid - s * (uint64_t)p.J);
+    const uint64_t s = tid / (uint64_t)p.nrem;
+    const int kk = (int)(tid - s * (uint64_t)p.nrem);
     const uint64_t R = p.in_R[s];
-    if (!((R >> j) & 1ull)) return;
+    const uint32_t Rlo = (uint32_t)R, Rhi = (uint32_t)(R >> 32);
+    const int nlo = __popc(Rlo);
+    const int j = kk < nlo ? (int)__fns(Rlo, 0, kk + 1) : 32 + (int)__fns(Rhi, 0, kk - nlo + 1);
     const uint64_t R2 = R & ~(1ull << j);
     int32_t a[GM], b[GM];
 #pragma unroll
@@ -122,7 +160,7 @@ __global__ void __launch_bounds__(kDpThreads) k_dp_expand(const __grid_constant_
     for (int q = p.ubase[j]; q < p.ubase[j] + p.ucnt[j]; ++q) {
         const int e = dp_place<GM>(a, p.Gr, p.ug[q], p.ud[q], p.release[j], b);
         if (e > p.T) continue;
-        if (!dp_viable<GM>(p, R2, b)) continue;
+        if (!dp_viable16<GM>(p, R2, b)) continue;
         const uint64_t key = R2 * p.cnum + dp_rank(p, b);
         uint64_t h = (key * kGolden) >> (64 - p.cap_log2);
         for (int probe = 0;; ++probe) {
@@ -247,6 +285,12 @@ static int dp_prepare(const sat_problem_t *pr, int32_t T, uint64_t max_states, D
             ++q;
         }
         p.ucnt[j] = q - p.ubase[j];
+        for (int w = 0; w < 16; ++w) {
+            const uint32_t lo = 2 * w < Gr ? (uint32_t)std::min<int32_t>(p.dg[j][2 * w], 0x7FFF) : 0x7FFFu;
+            const uint32_t hi = 2 * w + 1 < Gr ? (uint32_t)std::min<int32_t>(p.dg[j][2 * w + 1], 0x7FFF) : 0x7FFFu;
+            p.dgp[j][w] = lo | (hi << 16);
+        }
+        p.has_release |= rel != 0;
     }
     // exact key: R x C(T + Gr, Gr) + rank must stay below 2^63
     const int n_max = T + Gr;
@@ -281,7 +325,7 @@ static size_t dp_ws_bytes(const DpPlan &d) { return d.binom_bytes + d.table_byte
 
 template <int GM>
 static int dp_launch_expand(const DpParams &p, cudaStream_t s) {
-    const uint64_t threads = p.n_in * (uint64_t)p.J;
+    const uint64_t threads = p.n_in * (uint64_t)p.nrem;
     const uint64_t blocks = (threads + kDpThreads - 1) / kDpThreads;
     if (blocks == 0) return SAT_OK;
     if (blocks > 0x7fffffffull) return SAT_ERR_TOO_LARGE;
@@ -351,6 +395,7 @@ struct DpWideParams {
     uint64_t cnum[kDpWideMaxN];             // C(T + G_n, G_n)
     int32_t ubase[kDpMaxJ], ucnt[kDpMaxJ], release[kDpMaxJ], minarea[kDpMaxJ];
     int32_t Kb;                             // binomial table row width (max G_n + 1)
+    int32_t nrem;                           // jobs still to place in the level being expanded
     const uint64_t *binom;                  // [(T + maxG + 1)][Kb]
     const uint8_t *ug;                      // [n_usable] gang size
     const uint8_t *um;                      // [n_usable] node eligibility bits
@@ -426,12 +471,14 @@ __device__ __forceinline__ bool dpw_viable(const DpWideParams &p, uint64_t R2, c
 
 __global__ void __launch_bounds__(kDpThreads) k_dp_expand_wide(const __grid_constant__ DpWideParams p) {
     const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (tid >= p.n_in * (uint64_t)p.J) return;
+    if (tid >= p.n_in * (uint64_t)p.nrem) return;
     if (*reinterpret_cast<volatile unsigned int *>(p.overflow)) return;
-    const uint64_t s = tid / (uint64_t)p.J;
-    const int j = (int)(tid - s * (uint64_t)p.J);
+    const uint64_t s = tid / (uint64_t)p.nrem;                  // (state, k-th job still to place)
+    const int kk = (int)(tid - s * (uint64_t)p.nrem);
     const uint64_t R = p.in_R[s];
-    if (!((R >> j) & 1ull)) return;
+    const uint32_t Rlo = (uint32_t)R, Rhi = (uint32_t)(R >> 32);
+    const int nlo = __popc(Rlo);
+    const int j = kk < nlo ? (int)__fns(Rlo, 0, kk + 1) : 32 + (int)__fns(Rhi, 0, kk - nlo + 1);
     const uint64_t R2 = R & ~(1ull << j);
     int32_t a[kDpWideSlots], b[kDpWideSlots];
     for (int i = 0; i < p.Gtot; ++i) a[i] = p.in_A[s * p.Gtot + i];
@@ -683,7 +730,8 @@ static int dpw_run(const sat_problem_t *pr, uint64_t max_states, sat_dp_info_t *
         const uint64_t nb = base + size;
         p.out_R = Rs + nb; p.out_A = As + nb * Gt; p.out_cap = max_states - nb;
         if (cudaMemsetAsync(ctr, 0, 8, s)) return SAT_ERR_CUDA;
-        const uint64_t blocks = (p.n_in * (uint64_t)J + kDpThreads - 1) / kDpThreads;
+        p.nrem = J - level;
+        const uint64_t blocks = (p.n_in * (uint64_t)p.nrem + kDpThreads - 1) / kDpThreads;
         if (blocks > 0x7fffffffull) return SAT_ERR_TOO_LARGE;
         k_dp_expand_wide<<<(unsigned)blocks, kDpThreads, 0, s>>>(p);
         if (cudaGetLastError() != cudaSuccess) return SAT_ERR_CUDA;
@@ -787,6 +835,7 @@ int sat_search_dp(const sat_problem_t *pr, int32_t target, uint64_t max_states, 
         p.out_R = Rs + base[level + 1];
         p.out_A = As + base[level + 1] * Gr;
         p.out_cap = max_states - base[level + 1];
+        p.nrem = J - level;
         if (cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), s)) return SAT_ERR_CUDA;
         if ((st = dp_expand(p, s))) return st;
         unsigned long long got[2];
