@@ -48,19 +48,22 @@ struct DpParams {
     uint32_t dgp[kDpMaxJ][16];        // dg as 16-bit pairs (gangs 2w+1, 2w+2), for VIADDMNMX.U16x2
     int32_t nrem;                     // jobs still to place in the level being expanded
     int32_t has_release;
+    int32_t umax;                     // most usable options of any job
     const uint64_t *binom;            // [(T + Gr + 1)][Gr + 1]: C(n, k)
     uint64_t *table;                  // hash set of state keys, kDpEmpty = free
     uint64_t cap_mask;
     int32_t cap_log2;
     int32_t max_probe;
-    const uint64_t *in_R;             // level k: remaining-job sets
-    const uint16_t *in_A;             // level k: sorted free times [n_in][Gr]
+    uint64_t *all_R;                  // every level's states, appended level after level:
+    uint16_t *all_A;                  //   remaining-job sets, sorted free times [][Gr]
+    uint64_t max_states;
+    unsigned long long *lvl_cnt;      // [J + 1] states of each level
+    unsigned long long *lvl_base;     // [J + 2] first state of each level
+    unsigned int *overflow;           // level + 1 whose expansion exceeded the budget or probe limit
+    // reconstruction: one level's states
+    const uint64_t *in_R;
+    const uint16_t *in_A;
     uint64_t n_in;
-    uint64_t *out_R;                  // level k+1 (appended)
-    uint16_t *out_A;
-    uint64_t out_cap;
-    unsigned long long *count;        // states appended to level k+1
-    unsigned int *overflow;           // set when out_cap or the probe limit is exceeded
     // reconstruction (k_dp_parent): the child state searched for
     uint64_t child_R;
     uint16_t child_A[32];
@@ -109,11 +112,37 @@ __device__ __forceinline__ bool dp_viable(const DpParams &p, uint64_t R2, const 
     return area <= (int64_t)p.T * p.Gr;
 }
 
+// per-block copies of the tables the expansion indexes by job / option: the threads of a warp
+// work on different jobs, and divergent indices into the kernel parameters (constant bank)
+// serialise, while shared-memory reads of distinct words do not
+template <int GM>
+struct DpShared {
+    uint32_t dgp[kDpMaxJ][GM / 2];
+    int32_t minarea[kDpMaxJ], release[kDpMaxJ], ubase[kDpMaxJ], ucnt[kDpMaxJ];
+    int16_t ud[kDpMaxOpt];
+    uint8_t ug[kDpMaxOpt];
+};
+
+template <int GM>
+__device__ __forceinline__ void dp_stage(const DpParams &p, DpShared<GM> &sh) {
+    constexpr int W = GM / 2;
+    const int nopt = p.J ? p.ubase[p.J - 1] + p.ucnt[p.J - 1] : 0;
+    for (int x = threadIdx.x; x < p.J * W; x += blockDim.x) sh.dgp[x / W][x % W] = p.dgp[x / W][x % W];
+    for (int x = threadIdx.x; x < p.J; x += blockDim.x) {
+        sh.minarea[x] = p.minarea[x];
+        sh.release[x] = p.release[x];
+        sh.ubase[x] = p.ubase[x];
+        sh.ucnt[x] = p.ucnt[x];
+    }
+    for (int x = threadIdx.x; x < nopt; x += blockDim.x) { sh.ud[x] = p.ud[x]; sh.ug[x] = p.ug[x]; }
+}
+
 // the same test on 16-bit pairs: each remaining job's earliest end is GM/2 fused add-mins
 // (VIADDMNMX.U16x2) of the packed state and its packed least durations; free times and
 // durations are <= T + 1 <= 30001 and padding 0x7FFF, so no pair sum carries
 template <int GM>
-__device__ __forceinline__ bool dp_viable16(const DpParams &p, uint64_t R2, const int32_t *b) {
+__device__ __forceinline__ bool dp_viable16(const DpParams &p, const DpShared<GM> &sh, uint64_t R2,
+                                            const int32_t *b) {
     constexpr int W = GM / 2;
     uint32_t bp[W];
     int64_t area = 0;
@@ -126,15 +155,15 @@ __device__ __forceinline__ bool dp_viable16(const DpParams &p, uint64_t R2, cons
     }
     for (uint64_t m = R2; m; m &= m - 1) {
         const int i = __ffsll((long long)m) - 1;
-        area += p.minarea[i];
+        area += sh.minarea[i];
         uint32_t m2 = 0xFFFFFFFFu;
         if (p.has_release) {
-            const uint32_t r2 = (uint32_t)p.release[i] * 0x10001u;
+            const uint32_t r2 = (uint32_t)sh.release[i] * 0x10001u;
 #pragma unroll
-            for (int w = 0; w < W; ++w) m2 = __viaddmin_u16x2(__vmaxu2(bp[w], r2), p.dgp[i][w], m2);
+            for (int w = 0; w < W; ++w) m2 = __viaddmin_u16x2(__vmaxu2(bp[w], r2), sh.dgp[i][w], m2);
         } else {
 #pragma unroll
-            for (int w = 0; w < W; ++w) m2 = __viaddmin_u16x2(bp[w], p.dgp[i][w], m2);
+            for (int w = 0; w < W; ++w) m2 = __viaddmin_u16x2(bp[w], sh.dgp[i][w], m2);
         }
         if ((int32_t)min(m2 & 0xFFFFu, m2 >> 16) > p.T) return false;
     }
@@ -142,42 +171,96 @@ __device__ __forceinline__ bool dp_viable16(const DpParams &p, uint64_t R2, cons
 }
 
 template <int GM>
-__global__ void __launch_bounds__(kDpThreads) k_dp_expand(const __grid_constant__ DpParams p) {
-    // one thread per (state, job still to place): the level's states all have nrem such jobs
-    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (tid >= p.n_in * (uint64_t)p.nrem) return;
-    if (*reinterpret_cast<volatile unsigned int *>(p.overflow)) return;
-    const uint64_t s = tid / (uint64_t)p.nrem;
-    const int kk = (int)(tid - s * (uint64_t)p.nrem);
-    const uint64_t R = p.in_R[s];
-    const uint32_t Rlo = (uint32_t)R, Rhi = (uint32_t)(R >> 32);
-    const int nlo = __popc(Rlo);
-    const int j = kk < nlo ? (int)__fns(Rlo, 0, kk + 1) : 32 + (int)__fns(Rhi, 0, kk - nlo + 1);
-    const uint64_t R2 = R & ~(1ull << j);
-    int32_t a[GM], b[GM];
+__global__ void __launch_bounds__(kDpThreads) k_dp_expand(const __grid_constant__ DpParams p, int L) {
+    // Level L -> L + 1, sized on the device: the level's state count and offset are read from
+    // lvl_cnt / lvl_base (written by the previous level's launch), so the host queues every
+    // level without a read-back in between.  A fixed grid strides over the level's
+    // (state, job still to place) pairs -- every state has J - L such jobs.  Options are taken
+    // in block-wide rounds (round r = every thread's r-th usable option) so that the states a
+    // round appends are claimed with ONE atomicAdd per block on the level's counter.
+    __shared__ uint32_t warp_new[2][kDpThreads / 32];  // double-buffered by round parity
+    __shared__ unsigned long long block_base[2];
+    __shared__ unsigned int stop;
+    __shared__ DpShared<GM> sh;
+    int par = 0;
+    if (threadIdx.x == 0) stop = *reinterpret_cast<volatile unsigned int *>(p.overflow);
+    __syncthreads();
+    if (stop) return;                                  // an earlier level ran out of budget
+    dp_stage<GM>(p, sh);
+    __syncthreads();
+    const uint64_t n_in = p.lvl_cnt[L], in_base = p.lvl_base[L];
+    const uint64_t out_base = in_base + n_in;
+    if (blockIdx.x == 0 && threadIdx.x == 0) p.lvl_base[L + 1] = out_base;
+    const uint64_t out_cap = p.max_states - out_base;
+    const uint64_t *in_R = p.all_R + in_base;
+    const uint16_t *in_A = p.all_A + in_base * p.Gr;
+    uint64_t *out_R = p.all_R + out_base;
+    uint16_t *out_A = p.all_A + out_base * p.Gr;
+    unsigned long long *count = p.lvl_cnt + L + 1;
+    const int nrem = p.J - L;
+    const uint64_t total = n_in * (uint64_t)nrem;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (uint64_t t0 = (uint64_t)blockIdx.x * kDpThreads; t0 < total; t0 += (uint64_t)gridDim.x * kDpThreads) {
+        const uint64_t tid = t0 + threadIdx.x;
+        int j = 0, nq = 0;
+        uint64_t R2 = 0;
+        int32_t a[GM], b[GM];
+        if (tid < total) {
+            const uint64_t s = tid / (uint64_t)nrem;
+            const int kk = (int)(tid - s * (uint64_t)nrem);
+            const uint64_t R = in_R[s];
+            const uint32_t Rlo = (uint32_t)R, Rhi = (uint32_t)(R >> 32);
+            const int nlo = __popc(Rlo);
+            j = kk < nlo ? (int)__fns(Rlo, 0, kk + 1) : 32 + (int)__fns(Rhi, 0, kk - nlo + 1);
+            R2 = R & ~(1ull << j);
+            nq = sh.ucnt[j];
 #pragma unroll
-    for (int i = 0; i < GM; ++i) a[i] = i < p.Gr ? (int32_t)p.in_A[s * p.Gr + i] : 0x7fffffff;
-    for (int q = p.ubase[j]; q < p.ubase[j] + p.ucnt[j]; ++q) {
-        const int e = dp_place<GM>(a, p.Gr, p.ug[q], p.ud[q], p.release[j], b);
-        if (e > p.T) continue;
-        if (!dp_viable16<GM>(p, R2, b)) continue;
-        const uint64_t key = R2 * p.cnum + dp_rank(p, b);
-        uint64_t h = (key * kGolden) >> (64 - p.cap_log2);
-        for (int probe = 0;; ++probe) {
-            if (probe > p.max_probe) { atomicOr(p.overflow, 1u); return; }
-            const unsigned long long old = atomicCAS(reinterpret_cast<unsigned long long *>(&p.table[h]),
-                                                     (unsigned long long)kDpEmpty, (unsigned long long)key);
-            if (old == kDpEmpty) {                 // first time this state is reached: append it
-                const unsigned long long idx = atomicAdd(p.count, 1ull);
-                if (idx >= p.out_cap) { atomicOr(p.overflow, 1u); return; }
-                p.out_R[idx] = R2;
-#pragma unroll
-                for (int i = 0; i < GM; ++i)
-                    if (i < p.Gr) p.out_A[idx * p.Gr + i] = (uint16_t)b[i];
-                break;
+            for (int i = 0; i < GM; ++i) a[i] = i < p.Gr ? (int32_t)in_A[s * p.Gr + i] : 0x7fffffff;
+        }
+        for (int r = 0; r < p.umax; ++r) {
+            bool fresh = false;
+            if (r < nq) {
+                const int q = sh.ubase[j] + r;
+                const int e = dp_place<GM>(a, p.Gr, sh.ug[q], sh.ud[q], sh.release[j], b);
+                if (e <= p.T && dp_viable16<GM>(p, sh, R2, b)) {
+                    const uint64_t key = R2 * p.cnum + dp_rank(p, b);
+                    uint64_t h = (key * kGolden) >> (64 - p.cap_log2);
+                    for (int probe = 0;; ++probe) {
+                        if (probe > p.max_probe) { atomicExch(p.overflow, (unsigned)L + 1u); break; }
+                        const unsigned long long old = atomicCAS(
+                            reinterpret_cast<unsigned long long *>(&p.table[h]), (unsigned long long)kDpEmpty,
+                            (unsigned long long)key);
+                        if (old == kDpEmpty) { fresh = true; break; }   // first time this state is reached
+                        if (old == key) break;                          // already in the level
+                        h = (h + 1) & p.cap_mask;
+                    }
+                }
             }
-            if (old == key) break;                 // already in the level
-            h = (h + 1) & p.cap_mask;
+            const uint32_t bal = __ballot_sync(0xffffffffu, fresh);
+            uint32_t *wn = warp_new[par];
+            if (lane == 0) wn[warp] = __popc(bal);
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                uint32_t tot = 0;
+#pragma unroll
+                for (int w = 0; w < kDpThreads / 32; ++w) { const uint32_t c = wn[w]; wn[w] = tot; tot += c; }
+                block_base[par] = tot ? atomicAdd(count, (unsigned long long)tot) : 0ull;
+            }
+            __syncthreads();
+            // (the next round writes the other buffer; the one after that only once every
+            // thread has passed the next round's first barrier, i.e. finished reading this one)
+            if (fresh) {
+                const unsigned long long idx = block_base[par] + wn[warp] + __popc(bal & ((1u << lane) - 1u));
+                if (idx >= out_cap) {
+                    atomicExch(p.overflow, (unsigned)L + 1u);
+                } else {
+                    out_R[idx] = R2;
+#pragma unroll
+                    for (int i = 0; i < GM; ++i)
+                        if (i < p.Gr) out_A[idx * p.Gr + i] = (uint16_t)b[i];
+                }
+            }
+            par ^= 1;
         }
     }
 }
@@ -291,6 +374,7 @@ static int dp_prepare(const sat_problem_t *pr, int32_t T, uint64_t max_states, D
             p.dgp[j][w] = lo | (hi << 16);
         }
         p.has_release |= rel != 0;
+        p.umax = std::max(p.umax, p.ucnt[j]);
     }
     // exact key: R x C(T + Gr, Gr) + rank must stay below 2^63
     const int n_max = T + Gr;
@@ -321,15 +405,21 @@ static int dp_prepare(const sat_problem_t *pr, int32_t T, uint64_t max_states, D
     return SAT_OK;
 }
 
-static size_t dp_ws_bytes(const DpPlan &d) { return d.binom_bytes + d.table_bytes + d.R_bytes + d.A_bytes + 256; }
+// level counters: [0, 8) scalars (min key, overflow), [8, 8 + J + 1) counts, then J + 2 bases
+constexpr size_t kDpCtrBytes = (8 + 2 * (kDpMaxJ + 2)) * sizeof(unsigned long long);
+static size_t dp_ws_bytes(const DpPlan &d) { return d.binom_bytes + d.table_bytes + d.R_bytes + d.A_bytes + kDpCtrBytes; }
 
 template <int GM>
-static int dp_launch_expand(const DpParams &p, cudaStream_t s) {
-    const uint64_t threads = p.n_in * (uint64_t)p.nrem;
-    const uint64_t blocks = (threads + kDpThreads - 1) / kDpThreads;
-    if (blocks == 0) return SAT_OK;
-    if (blocks > 0x7fffffffull) return SAT_ERR_TOO_LARGE;
-    k_dp_expand<GM><<<(unsigned)blocks, kDpThreads, 0, s>>>(p);
+static int dp_launch_expand(const DpParams &p, int L, cudaStream_t s) {
+    static int blocks = 0;                             // a full resident generation, once
+    if (!blocks) {
+        int dev = 0, sms = 0, per = 0;
+        if (cudaGetDevice(&dev) || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) ||
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_dp_expand<GM>, kDpThreads, 0))
+            return SAT_ERR_CUDA;
+        blocks = std::max(1, sms * per);
+    }
+    k_dp_expand<GM><<<blocks, kDpThreads, 0, s>>>(p, L);
     return cudaGetLastError() == cudaSuccess ? SAT_OK : SAT_ERR_CUDA;
 }
 
@@ -341,10 +431,10 @@ static int dp_launch_parent(const DpParams &p, cudaStream_t s) {
     return cudaGetLastError() == cudaSuccess ? SAT_OK : SAT_ERR_CUDA;
 }
 
-static int dp_expand(const DpParams &p, cudaStream_t s) {
-    if (p.Gr <= 8) return dp_launch_expand<8>(p, s);
-    if (p.Gr <= 16) return dp_launch_expand<16>(p, s);
-    return dp_launch_expand<32>(p, s);
+static int dp_expand(const DpParams &p, int L, cudaStream_t s) {
+    if (p.Gr <= 8) return dp_launch_expand<8>(p, L, s);
+    if (p.Gr <= 16) return dp_launch_expand<16>(p, L, s);
+    return dp_launch_expand<32>(p, L, s);
 }
 
 static int dp_parent(const DpParams &p, cudaStream_t s) {
@@ -805,13 +895,15 @@ int sat_search_dp(const sat_problem_t *pr, int32_t target, uint64_t max_states, 
     uint64_t *Rs = reinterpret_cast<uint64_t *>(ws + d.binom_bytes + d.table_bytes);
     uint16_t *As = reinterpret_cast<uint16_t *>(ws + d.binom_bytes + d.table_bytes + d.R_bytes);
     auto *ctr = reinterpret_cast<unsigned long long *>(ws + d.binom_bytes + d.table_bytes + d.R_bytes + d.A_bytes);
-    // ctr[0] = count, ctr[1] = overflow flag (u32), ctr[2] = min key
     DpParams &p = d.p;
     const int J = pr->J, Gr = p.Gr;
+    // level 0: every job to place, the initial free times; lvl_cnt[0] = 1, every other count 0
+    std::vector<unsigned long long> ctr_init(kDpCtrBytes / sizeof(unsigned long long), 0ull);
+    ctr_init[8] = 1;
     if (cudaMemcpyAsync(binom, d.binom.data(), d.binom.size() * sizeof(uint64_t), cudaMemcpyHostToDevice, s) ||
-        cudaMemsetAsync(table, 0xFF, d.cap * sizeof(uint64_t), s) || cudaMemsetAsync(ctr, 0, 256, s))
+        cudaMemsetAsync(table, 0xFF, d.cap * sizeof(uint64_t), s) ||
+        cudaMemcpyAsync(ctr, ctr_init.data(), kDpCtrBytes, cudaMemcpyHostToDevice, s))
         return SAT_ERR_CUDA;
-    // level 0: every job to place, the initial free times
     const uint64_t full = J == 64 ? ~0ull : ((1ull << J) - 1ull);
     std::vector<uint16_t> a0(Gr);
     for (int i = 0; i < Gr; ++i) a0[i] = (uint16_t)d.a0[i];
@@ -820,38 +912,38 @@ int sat_search_dp(const sat_problem_t *pr, int32_t target, uint64_t max_states, 
         return SAT_ERR_CUDA;
     p.binom = binom;
     p.table = table;
-    p.count = ctr;
+    p.min_key = ctr;
     p.overflow = reinterpret_cast<unsigned int *>(ctr + 1);
-    p.min_key = ctr + 2;
+    p.lvl_cnt = ctr + 8;
+    p.lvl_base = ctr + 8 + (kDpMaxJ + 1);
+    p.all_R = Rs;
+    p.all_A = As;
+    p.max_states = max_states;
+    // every level queued back to back; one read-back of the counts at the end
+    for (int L = 0; L < J; ++L)
+        if ((st = dp_expand(p, L, s))) return st;
+    std::vector<unsigned long long> got(kDpCtrBytes / sizeof(unsigned long long));
+    if (cudaMemcpyAsync(got.data(), ctr, kDpCtrBytes, cudaMemcpyDeviceToHost, s) || cudaStreamSynchronize(s))
+        return SAT_ERR_CUDA;
+    const unsigned int ovf = (unsigned int)got[1];
     std::vector<uint64_t> base(J + 2, 0), size(J + 2, 0);
-    base[0] = 0; size[0] = 1;
-    uint64_t total = 1, widest = 1;
+    uint64_t total = 0, widest = 0;
     int level = 0;
-    for (; level < J; ++level) {
-        p.in_R = Rs + base[level];
-        p.in_A = As + base[level] * Gr;
-        p.n_in = size[level];
-        base[level + 1] = base[level] + size[level];
-        p.out_R = Rs + base[level + 1];
-        p.out_A = As + base[level + 1] * Gr;
-        p.out_cap = max_states - base[level + 1];
-        p.nrem = J - level;
-        if (cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), s)) return SAT_ERR_CUDA;
-        if ((st = dp_expand(p, s))) return st;
-        unsigned long long got[2];
-        if (cudaMemcpyAsync(got, ctr, sizeof(got), cudaMemcpyDeviceToHost, s) || cudaStreamSynchronize(s))
-            return SAT_ERR_CUDA;
-        if ((unsigned int)got[1]) {
+    size[0] = 1;
+    for (int L = 0; L <= J; ++L) {
+        if (ovf && L == (int)ovf) {                     // level L's expansion from L - 1 overflowed
             info->status = SAT_DP_BUDGET;
-            info->levels = level;
+            info->levels = L - 1;
             info->states = total;
             info->widest_level = widest;
             return SAT_OK;
         }
-        size[level + 1] = got[0];
-        total += got[0];
-        widest = std::max<uint64_t>(widest, got[0]);
-        if (got[0] == 0) { ++level; break; }
+        size[L] = got[8 + L];
+        if (L > 0) base[L] = base[L - 1] + size[L - 1];
+        total += size[L];
+        widest = std::max<uint64_t>(widest, size[L]);
+        level = L;
+        if (size[L] == 0) break;
     }
     info->levels = level;
     info->states = total;

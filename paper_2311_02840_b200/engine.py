@@ -448,9 +448,16 @@ class Engine:
         v = out.cpu().tolist()
         return v[:J], v[J:]
 
-    def dp_search(self, nprob: NativeProblem, target: int, max_states: int = 1 << 22):
+    def side_stream(self) -> int:
+        """A second stream of this engine's device (work overlapped with the current stream's)."""
+        if getattr(self, "_side", None) is None:
+            self._side = self.torch.cuda.Stream(device=self.device)
+        return self._side.cuda_stream
+
+    def dp_search(self, nprob: NativeProblem, target: int, max_states: int = 1 << 22, stream: int | None = None):
         """sat_search_dp: does some candidate reach makespan <= target?  Returns (status, info,
-        candidate) -- candidate = (options, order) when FEASIBLE.  Synchronous."""
+        candidate) -- candidate = (options, order) when FEASIBLE.  Synchronous (on ``stream``,
+        default the current stream)."""
         torch = self.torch
         need = ctypes.c_size_t()
         self._check(self.lib.sat_dp_workspace_bytes(nprob.ref, int(target), int(max_states), ctypes.byref(need)),
@@ -462,7 +469,8 @@ class Engine:
         cand = (ctypes.c_uint8 * (2 * J))()
         info = SatDpInfo()
         self._check(self.lib.sat_search_dp(nprob.ref, int(target), int(max_states), cand, ctypes.byref(info),
-                                           _vp(self._dp_ws.data_ptr()), self._dp_ws.numel(), _vp(self.stream())),
+                                           _vp(self._dp_ws.data_ptr()), self._dp_ws.numel(),
+                                           _vp(self.stream() if stream is None else stream)),
                     what="sat_search_dp", nprob=nprob)
         self.launches += max(1, info.levels)
         out = None
@@ -471,14 +479,16 @@ class Engine:
             out = (v[:J], v[J:])
         return info.status, info, out
 
-    def prove_below(self, prob: SearchProblem, makespan: int, opts: SolveOptions):
+    def prove_below(self, prob: SearchProblem, makespan: int, opts: SolveOptions, lb: int | None = None,
+                    stats: dict | None = None):
         """Descend from a known candidate makespan with sat_search_dp: target = makespan - 1 until
         no candidate reaches it (the last makespan is then optimal) or the state budget runs out.
-        Returns (proven, best makespan, improved candidate or None, stats)."""
+        ``lb``: a proven lower bound (default the problem's).  Returns (proven, best makespan,
+        improved candidate or None, stats)."""
         nprob = NativeProblem(prob, 1)
-        stats = {"attempts": [], "states": 0}
+        stats = {"attempts": [], "states": 0} if stats is None else stats
         best_ms, cand = int(makespan), None
-        lb = int(prob.lower_bound())
+        lb = int(prob.lower_bound()) if lb is None else int(lb)
         while best_ms > lb:
             st, info, c = self.dp_search(nprob, best_ms - 1, opts.dp_states)
             stats["attempts"].append({"target": best_ms - 1, "status": DP_STATUS[st], "levels": info.levels,
@@ -681,6 +691,9 @@ class Engine:
             # shorter candidate; it is retried only when a later wave improves the best
             dp_ok = opts.prove and nprob.grid and prob.J <= min(64, opts.dp_max_jobs) and prob.N <= 8
             proof, dp_tried_at, dp_cand = None, None, None
+            lb_int = int(target) if nprob.grid else 0
+            spec_lb = dp_ok and prob.N == 1 and opts.dp_at_bound
+            dp_lb_hit = False
             while w0 < n_idx:
                 w1 = min(n_idx, w0 + wave)
                 a, b = _shard(w1 - w0, rank, world)
@@ -688,6 +701,27 @@ class Engine:
                 ls_states.append((w0 + a, w0 + b, st_buf))
                 self.local_search(nprob, src, seed_used, w0 + a, w0 + b, opts.max_rounds, kbest, state_out=st_buf,
                                   stop_ms=stop_ms)
+                if spec_lb:
+                    # one node: while the first wave runs, the state-space search asks on a side
+                    # stream whether anything reaches the lower bound itself.  "No" lifts the
+                    # proven bound by one interval, "yes" hands over an optimal candidate.
+                    spec_lb = False
+                    proof = {"attempts": [], "states": 0}
+                    try:
+                        st_lb, info_lb, c_lb = self.dp_search(NativeProblem(prob, 1), lb_int, opts.dp_states,
+                                                              stream=self.side_stream())
+                        proof["attempts"].append({"target": lb_int, "status": DP_STATUS[st_lb],
+                                                  "levels": info_lb.levels, "states": int(info_lb.states),
+                                                  "widest_level": int(info_lb.widest_level)})
+                        proof["states"] += int(info_lb.states)
+                        if st_lb == SAT_DP_INFEASIBLE:
+                            lb_int += 1
+                        elif st_lb == SAT_DP_FEASIBLE and c_lb is not None:
+                            dp_cand, dp_lb_hit = (int(info_lb.makespan), c_lb), True
+                        else:
+                            dp_ok = False            # out of budget at the bound: higher targets too
+                    except (E.TooLarge, err.TooLarge, E.InvariantViolation, err.InvariantViolation):
+                        dp_ok = False
                 rounds_total += int(self._ws[off.value:off.value + 8].view(torch.int64).item())
                 walkers_done, waves, w0, wave = w1, waves + 1, w1, wave * 4
                 if shared is not None:
@@ -696,10 +730,15 @@ class Engine:
                 k_ms = ls_key_fields(k, idx_bits)[0]
                 if k != INT64_MAX and k_ms <= target:
                     break
+                if dp_lb_hit or (k != INT64_MAX and k_ms <= lb_int):
+                    # the bound the side search proved (or a candidate at the bound) is met
+                    proof["proven"] = True
+                    break
                 if dp_ok and k != INT64_MAX and dp_tried_at != k_ms:
                     dp_tried_at = k_ms
                     try:
-                        proven, dp_ms, cand, proof = self.prove_below(prob, dp_tried_at, opts)
+                        proven, dp_ms, cand, proof = self.prove_below(prob, dp_tried_at, opts, lb=lb_int,
+                                                                      stats=proof)
                     except (E.TooLarge, err.TooLarge, E.InvariantViolation, err.InvariantViolation):
                         # a shape the state-space search does not take (key width, > 8 nodes):
                         # no proof, the local search's result stands

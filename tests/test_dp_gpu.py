@@ -155,3 +155,31 @@ def test_hetero6_local_plan_proven_or_improved():
     proof = (sol.search.stats or {}).get("proof")
     assert proof is not None
     assert sol.status == ("Optimal" if proof["proven"] else "Local")
+
+
+@pytest.mark.parametrize("at_bound", [True, False])
+def test_local_search_with_proof_random_one_node(eng, at_bound):
+    """Local search forced onto small one-node problems with a deliberately weak wave (8
+    walkers, 2 rounds): the state-space search -- at the lower bound on a side stream during
+    the first wave (dp_at_bound), then below the wave's best -- must still end at the oracle's
+    exhaustive optimum with a proof, and the returned (options, order) must replay to it."""
+    rng = random.Random(77)
+    seen = set()
+    for trial in range(30):
+        gsz = [2, 3, 4, 8][trial % 4]
+        op = random_problem(rng, rng.randint(3, 6), [gsz], max_opts=3, max_d=10)
+        if trial % 3 == 1:
+            op.release = [rng.randint(0, 5) for _ in range(op.J)]
+        prob = to_search_problem(op)
+        opt = C.CProblem(op).search()[0]
+        res = eng.search(prob, SolveOptions(search="local", walkers=64, wave=8, max_rounds=2,
+                                            dp_at_bound=at_bound))
+        assert res.proven or res.makespan <= prob.lower_bound(), (trial, res.stats)
+        assert res.makespan == opt, (trial, res.makespan, opt)
+        opts, order = res.state
+        assert C.CProblem(op).eval(opts, order)[0] == opt
+        proof = res.stats.get("proof")
+        if proof and proof["attempts"] and proof["attempts"][0]["target"] == int(prob.lower_bound()):
+            seen.add(proof["attempts"][0]["status"])
+    if at_bound:       # both outcomes of the side-stream attempt at the bound occur
+        assert {"feasible", "infeasible"} <= seen, seen
