@@ -22,7 +22,7 @@ Everything here runs once per solve; the per-candidate work is on the device.
 from __future__ import annotations
 
 import math
-from itertools import repeat
+from itertools import chain, repeat
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -272,7 +272,8 @@ def _one_node_options(job, workload):
                     e = shape_elig[k] = node_eligible(job, tech_by_name[c.technique], c.gpus, n)
                 row.append(e)
             elig.append(tuple(row))
-        hit = (cfgs, keys, np.array([c.gpus for c in cfgs], dtype=np.int64), tuple(elig))
+        elig_arr = np.array(elig, dtype=bool).reshape(len(cfgs), len(workload.cluster.nodes))
+        hit = (cfgs, keys, np.array([c.gpus for c in cfgs], dtype=np.int64), tuple(elig), elig_arr)
         if key is not None:
             if len(_ONE_NODE_MEMO) > 1 << 16:
                 _ONE_NODE_MEMO.clear()
@@ -295,6 +296,98 @@ def _dominance_prune_arrays(g: np.ndarray, cost: np.ndarray) -> list:
             last = c
     kept.sort()
     return kept
+
+
+def _batch_rows(pool, workload, remaining, get, opts, prune: bool, err):
+    """The marshalling of every job at once when no job has a running configuration: the same
+    arrays as the per-job rows in `build_problem`, built with one profile-table pass and
+    whole-problem numpy ops instead of per-job / per-option Python (config 5: 64 jobs x 172
+    configs; config 4: 32 jobs x 26 configs x 4 nodes).
+
+    Per job, in canonical order: finite-latency configs (profiling.py:154-161), runtime
+    t = rem x lat (profiling.py:151) on every node that can host the config, infinite on the
+    others; the least runtime for choose_delta; on one node the exact dominance prune of
+    `_dominance_prune` -- per (job, g) the cheapest option (earliest on ties), kept while the
+    cost strictly decreases with g; the running minimum restarts at every job by offsetting
+    integer cost ranks per job."""
+    per = [_one_node_options(job, workload) for job in pool]
+    J = len(pool)
+    counts = np.fromiter((len(p[1]) for p in per), dtype=np.int64, count=J)
+    total = int(counts.sum())
+    lat_all = np.fromiter(map(get, chain.from_iterable(p[1] for p in per), repeat(INFEASIBLE)),
+                          dtype=np.float64, count=total)
+    job_all = np.repeat(np.arange(J), counts)
+    finite = np.isfinite(lat_all)
+    nfin = np.bincount(job_all[finite], minlength=J)
+    if (nfin == 0).any():
+        raise err.NoFeasibleConfig(pool[int(np.argmax(nfin == 0))].id)
+    sel = np.flatnonzero(finite)                       # job-major, canonical order within a job
+    job = job_all[sel]
+    start_all = np.concatenate(([0], np.cumsum(counts)[:-1]))
+    start_sel = np.concatenate(([0], np.cumsum(nfin)[:-1]))
+    g = np.concatenate([p[2] for p in per])[sel]
+    elig = np.concatenate([p[4] for p in per])[sel]    # [n, N]
+    N = elig.shape[1]
+    lat = lat_all[sel]
+    rem = np.fromiter((remaining[j.id] for j in pool), dtype=np.float64, count=J)
+    t = rem[job] * lat                                 # the same IEEE product as rem * lat
+    t_node = np.where(elig, t[:, None], INFEASIBLE)    # [n, N]
+    row_min = np.minimum.reduceat(t_node.min(axis=1), start_sel)
+    if not np.isfinite(row_min).all():
+        raise err.NoFeasibleConfig(pool[int(np.argmax(~np.isfinite(row_min)))].id)
+    min_rt = row_min.tolist()
+    if opts.delta is not None:
+        delta = float(opts.delta)
+        if not delta > 0:
+            raise err.InvariantViolation("delta", "must be > 0")
+        horizon = math.ceil(sum(min_rt) / delta)
+        if horizon > opts.k_max:
+            raise err.HorizonOverflow(horizon, opts.k_max)
+    else:
+        delta = choose_delta(min_rt, opts.k_max)
+    grid = opts.time_mode == TIME_GRID
+    n = len(sel)
+    if prune:
+        cost = np.ceil(t / delta) if grid else t
+        # one stable argsort of an exact integer key (job, g, cost rank): within a (job, g)
+        # group the cheapest option first, the earliest of equal costs first
+        _, crank = np.unique(cost, return_inverse=True)
+        U = int(crank.max()) + 1
+        jg = job.astype(np.int64) * 64 + g
+        order = np.argsort(jg * U + crank, kind="stable")
+        jgo = jg[order]
+        first = order[np.r_[True, jgo[1:] != jgo[:-1]]]
+        # g kept while the cost strictly decreases: exclusive running minimum of the cost
+        # ranks, restarted per job by offsetting each job above every later one
+        v = crank[first].astype(np.int64) + (J - job[first]).astype(np.int64) * U
+        prev = np.r_[np.iinfo(np.int64).max, np.minimum.accumulate(v)[:-1]]
+        kept = np.sort(first[v < prev])
+    else:
+        kept = np.arange(n)
+    kj = job[kept]
+    radix = np.bincount(kj, minlength=J).astype(np.int32)
+    kstart = np.concatenate(([0], np.cumsum(radix)[:-1]))
+    slot = np.arange(len(kept)) - kstart[kj]
+    Cmax = int(radix.max())
+    gpus = np.zeros((J, Cmax), dtype=np.int32)
+    gpus[kj, slot] = g[kept]
+    ek = elig[kept]
+    runtime = np.zeros((J, Cmax, N), dtype=np.float64)
+    runtime[kj, slot, :] = np.where(ek, t[kept][:, None], 0.0)
+    mask = np.zeros((J, Cmax), dtype=np.uint32)
+    mask[kj, slot] = (ek.astype(np.uint32) << np.arange(N, dtype=np.uint32)[None, :]).sum(axis=1, dtype=np.uint32)
+    dq = np.ceil(runtime / delta)                      # SPEC.md:183
+    if (dq >= INF_I32 // 4).any():
+        raise err.TooLarge(f"duration {int(dq.max())} intervals overflows the device time type")
+    # per job: (config, latency) of the kept options and their index among the finite ones
+    local = (kept - start_sel[kj]).tolist()
+    cfg_idx = (sel[kept] - start_all[kj]).tolist()
+    lat_k = lat[kept].tolist()
+    options, option_src = [[] for _ in range(J)], [[] for _ in range(J)]
+    for jj, ci, li, lt in zip(kj.tolist(), cfg_idx, local, lat_k):
+        options[jj].append((per[jj][0][ci], lt))
+        option_src[jj].append(li)
+    return options, option_src, radix, gpus, mask, runtime, dq.astype(np.int32), delta
 
 
 def choose_delta(min_runtimes: list, k_max: int = K_MAX_DEFAULT) -> float:
@@ -336,6 +429,16 @@ def build_problem(table, workload, opts: SolveOptions | None = None, running_con
     if N * G > MAX_LANES:
         raise err.TooLarge(f"{N} nodes x {G} padded GPUs exceed one warp ({MAX_LANES} lanes)")
 
+    grid = opts.time_mode == TIME_GRID
+    prune = (N == 1) if opts.prune is None else bool(opts.prune)
+    if prune and N != 1:
+        raise err.InvariantViolation("prune", "the dominance prune is exact only on one node")
+    if _BATCH_ROWS and pool and techniques is workload.techniques and not any(j.id in current for j in pool):
+        options, option_src, radix, gpus, mask, runtime, dur, delta = _batch_rows(
+            pool, workload, remaining, table.entries.get, opts, prune, err)
+        return _search_problem(pool, nodes, G, W, options, option_src, radix, gpus, mask, runtime, dur,
+                               opts, delta, prune, running_context)
+
     # per job: canonical option list with per-node runtimes
     from .profiling import feasible_entries  # local: avoid a cycle at import time
     shapes = {}                         # (gpu_count, gpu_memory) -> shape index
@@ -356,7 +459,7 @@ def build_problem(table, workload, opts: SolveOptions | None = None, running_con
             # configs some node hosts), so the runtime is the plain estimate (profiling.py:151).
             # feasible_entries (profiling.py:154-161) as arrays: rem * lat elementwise is the
             # same IEEE product; per-option tuples are built only for the prune's survivors.
-            cfgs, keys, g_all, _ = _one_node_options(job, workload)
+            cfgs, keys, g_all, _, _ = _one_node_options(job, workload)
             if len(keys) < _ARRAY_ROW_MIN:      # short rows: plain tuples beat numpy call overhead
                 fin = [(c, lat) for c, lat in zip(cfgs, map(get, keys, repeat(INFEASIBLE))) if math.isfinite(lat)]
                 if not fin:
@@ -377,7 +480,7 @@ def build_problem(table, workload, opts: SolveOptions | None = None, running_con
             # several nodes or a running config: runtime = plain estimate on every eligible node
             # (profiling.py:151), + rho off the job's running (technique, g, node);
             # eligibility per (config, node) from the memo
-            cfgs, keys, _, elig = _one_node_options(job, workload)
+            cfgs, keys, _, elig, _ = _one_node_options(job, workload)
             row = []
             for c, lat, el in zip(cfgs, map(get, keys, repeat(INFEASIBLE)), elig):
                 if math.isfinite(lat):
@@ -430,11 +533,6 @@ def build_problem(table, workload, opts: SolveOptions | None = None, running_con
     else:
         delta = choose_delta(min_rt, opts.k_max)
 
-    grid = opts.time_mode == TIME_GRID
-    prune = (N == 1) if opts.prune is None else bool(opts.prune)
-    if prune and N != 1:
-        raise err.InvariantViolation("prune", "the dominance prune is exact only on one node")
-
     kept_rows, kept_src = [], []
     for row in rows:
         if type(row) is _OneNodeRow:
@@ -470,17 +568,25 @@ def build_problem(table, workload, opts: SolveOptions | None = None, running_con
     if (dq >= INF_I32 // 4).any():
         raise err.TooLarge(f"duration {int(dq.max())} intervals overflows the device time type")
     dur = dq.astype(np.int32)
+    return _search_problem(pool, nodes, G, W, [[(cfg, lat) for cfg, lat, _ in r] for r in kept_rows], kept_src,
+                           radix, gpus, mask, runtime, dur, opts, delta, prune, running_context)
 
+
+_BATCH_ROWS = True           # no running configuration: `_batch_rows`
+
+
+def _search_problem(pool, nodes, G, W, options, option_src, radix, gpus, mask, runtime, dur, opts, delta, prune,
+                    running_context) -> SearchProblem:
+    N, J = len(nodes), len(pool)
     init_i = np.full((N, G), INF_I32, dtype=np.int32)
     init_f = np.full((N, G), np.inf, dtype=np.float64)
     for n, node in enumerate(nodes):
         init_i[n, : node.gpu_count] = 0
         init_f[n, : node.gpu_count] = 0.0
-
     return SearchProblem(
         job_ids=[j.id for j in pool], jobs=pool, node_ids=[n.id for n in nodes],
         node_gpus=np.array([n.gpu_count for n in nodes], dtype=np.int32), G=G, W=W,
-        options=[[(cfg, lat) for cfg, lat, _ in r] for r in kept_rows], option_src=kept_src,
+        options=options, option_src=option_src,
         radix=radix, gpus=gpus, node_mask=mask, runtime=runtime, dur_i32=dur,
         release_i32=np.zeros(J, dtype=np.int32), release_f64=np.zeros(J, dtype=np.float64),
         init_free_i32=init_i, init_free_f64=init_f, time_mode=opts.time_mode, delta=delta,

@@ -219,6 +219,7 @@ def test_one_node_array_marshalling_matches_oracle(mode, row_min, monkeypatch):
     from paper_2311_02840_b200.workloads import random_workload
 
     monkeypatch.setattr(P, "_ARRAY_ROW_MIN", row_min)
+    monkeypatch.setattr(P, "_BATCH_ROWS", False)          # the per-job rows (batch: below)
 
     for seed in range(40):
         w = random_workload(seed, n_nodes=1)
@@ -308,3 +309,51 @@ def test_best_runtime_by_g_equals_loop_restatement():
             assert got[j].keys() == want.keys() == PL._best_runtime_by_g(prob, j).keys()
             for g in want:
                 assert got[j][g][1] == want[g][1] and float(got[j][g][0]).hex() == float(want[g][0]).hex()
+
+
+@pytest.mark.parametrize("mode", ["grid", "float"])
+def test_batch_marshalling_equals_per_job_rows(mode, monkeypatch):
+    """`_batch_rows` (whole-problem numpy; every solve without running configurations) builds
+    exactly the arrays, options and delta of the per-job rows: configs 1-5, and random 1-4-node
+    workloads with infeasible / missing table entries and re-solve contexts that only shrink
+    the remaining batches; errors are raised the same way."""
+    from paper_2311_02840_b200 import problem as P
+    from paper_2311_02840_b200.workloads import config_workload, random_workload
+
+    def build(flag, t, w, ctx=None, **kw):
+        monkeypatch.setattr(P, "_BATCH_ROWS", flag)
+        try:
+            return build_problem(t, w, SolveOptions(time_mode=mode, **kw), ctx)
+        except Exception as exc:  # noqa: BLE001
+            return type(exc)
+
+    def same(a, b):
+        if isinstance(a, type) or isinstance(b, type):
+            assert a == b
+            return
+        for f in ("radix", "gpus", "node_mask", "runtime", "dur_i32", "init_free_i32", "init_free_f64"):
+            x, y = getattr(a, f), getattr(b, f)
+            assert x.dtype == y.dtype and x.shape == y.shape and np.array_equal(x, y), f
+        assert a.delta.hex() == b.delta.hex()
+        assert (a.options, a.option_src, a.job_ids, a.pruned) == (b.options, b.option_src, b.job_ids, b.pruned)
+
+    cases = []
+    for c in (1, 2, 3, 4, 5):
+        w, t, _ = config_workload(c)
+        cases.append((t, w, None, {}))
+        cases.append((t, w, None, {"prune": False}))
+    for seed in range(40):
+        w = random_workload(seed, n_nodes=1 + seed % 4)
+        t = build_profile_table(w, SyntheticExecutor(w.cluster))
+        keys = sorted(t.entries)
+        if seed % 3 == 1 and len(keys) > 2:
+            t.entries[keys[seed % len(keys)]] = math.inf
+        if seed % 3 == 2 and len(keys) > 2:
+            del t.entries[keys[(7 * seed) % len(keys)]]
+        cases.append((t, w, None, {}))
+        if seed % 2:
+            rem = {j.id: (0 if k % 3 == 0 else max(1, int(j.total_batches) // (k + 2)))
+                   for k, j in enumerate(w.jobs)}
+            cases.append((t, w, D.RunningContext(remaining=rem, current={}, checkpoint_cost=30.0), {}))
+    for t, w, ctx, kw in cases:
+        same(build(True, t, w, ctx, **kw), build(False, t, w, ctx, **kw))
