@@ -201,6 +201,13 @@ __global__ void __launch_bounds__(kDpThreads) k_dp_expand(const __grid_constant_
     const uint64_t total = n_in * (uint64_t)nrem;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (uint64_t t0 = (uint64_t)blockIdx.x * kDpThreads; t0 < total; t0 += (uint64_t)gridDim.x * kDpThreads) {
+        // out of budget (this level or a probe limit): stop striding at once -- the hash set
+        // keeps filling with states that can no longer be appended, and probes lengthen
+        if (t0 != (uint64_t)blockIdx.x * kDpThreads) {
+            if (threadIdx.x == 0) stop = *reinterpret_cast<volatile unsigned int *>(p.overflow);
+            __syncthreads();
+            if (stop) return;
+        }
         const uint64_t tid = t0 + threadIdx.x;
         int j = 0, nq = 0;
         uint64_t R2 = 0;

@@ -108,6 +108,21 @@ def test_dp_budget_and_unsupported(eng):
         dp(eng, to_search_problem(op), 3)
 
 
+def test_dp_budget_exhaustion_stops_early(eng):
+    """Out of budget at one level, the remaining work of that level is dropped: config 3 at
+    T = 31 overflows 4 M states at level 5 in about a millisecond (it took 0.3 s while the
+    level kept inserting into the hash set after the overflow)."""
+    import time
+
+    w, t, _ = config_workload(3)
+    prob = build_problem(t, w)
+    dp(eng, prob, 31, 1 << 22)                           # warm (workspace, tables)
+    t0 = time.perf_counter()
+    st, info, _ = dp(eng, prob, 31, 1 << 22)
+    assert st == EN.SAT_DP_BUDGET and info.levels < prob.J
+    assert time.perf_counter() - t0 < 0.1
+
+
 def test_solve_without_proof_keeps_local_status():
     w, t, _ = config_workload(3)
     sol = PL.solve(t, w, None, SolveOptions(prove=False))
