@@ -593,11 +593,13 @@ class Engine:
 
     def search(self, prob: SearchProblem, opts: SolveOptions, group=None, source: int | None = None,
                seed: int | None = None, lo: int | None = None, hi: int | None = None,
-               replay: bool = False) -> SearchResult:
+               replay: bool = False, on_launched=None) -> SearchResult:
         """Run one solve's search on this rank's shard and combine across ranks (NCCL MIN).
         replay=True (grid time, full-scan / index / sampled searches): the winner's schedule is
         launched on the stream right behind the search, reading its id from the combined
-        device key, so the host reads the key and the plan after one wait."""
+        device key, so the host reads the key and the plan after one wait.
+        on_launched(mode): host work run once the first kernels are queued and before the first
+        wait on the device (it overlaps the search)."""
         torch = self.torch
         err = E.errors_for(prob.jobs[0]) if prob.jobs else E
         t0 = time.perf_counter()
@@ -701,6 +703,9 @@ class Engine:
                 ls_states.append((w0 + a, w0 + b, st_buf))
                 self.local_search(nprob, src, seed_used, w0 + a, w0 + b, opts.max_rounds, kbest, state_out=st_buf,
                                   stop_ms=stop_ms)
+                if on_launched is not None:
+                    on_launched(mode)
+                    on_launched = None
                 if spec_lb:
                     # one node: while the first wave runs, the state-space search asks on a side
                     # stream whether anything reaches the lower bound itself.  "No" lifts the
@@ -761,6 +766,8 @@ class Engine:
             self.search_sampled(nprob, src, seed_used, base_lo + a, base_lo + b, kbest)
             kernel, evaluated = "sampled", base_hi - base_lo
         ev1.record()
+        if on_launched is not None:
+            on_launched(mode)
         if shared is not None:
             shared.collect(best)
         key_dev = _combine_dev(best, nprob.grid, group, world)

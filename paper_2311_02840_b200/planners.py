@@ -260,9 +260,21 @@ def solve_problem(prob: SearchProblem, workload, opts: SolveOptions, running_con
     """Search -> decode -> check for an already marshalled problem (the milp facade's entry)."""
     err = E.errors_for(workload.jobs[0] if workload.jobs else workload)
     eng = get_engine(device)
+    baselines = []
+
+    def greedy_baselines(mode):
+        # heuristic searches also weigh the greedy baselines as incumbents (the B&B's "initial
+        # incumbent from rounding", SPEC.md:213): the plan is never worse than them.  Built on
+        # the host while the search's first kernels run.
+        if mode != "exhaustive":
+            for builder in (optimus_allocation, current_practice_allocation):
+                b_opts, b_order = builder(prob)
+                baselines.append((np.array(list(b_opts) + list(b_order), dtype=np.uint8), list(b_order),
+                                  builder.__name__))
+
     try:
         with _nvtx("saturn.search"):
-            res = eng.search(prob, opts, group=group, replay=True)
+            res = eng.search(prob, opts, group=group, replay=True, on_launched=greedy_baselines)
         nprob = NativeProblem(prob, res.idx_bits) if res.replay is None else None
         if res.kernel == "local":
             # replay the winning walker to get its final candidate, then schedule it explicitly
@@ -272,14 +284,7 @@ def solve_problem(prob: SearchProblem, workload, opts: SolveOptions, running_con
                 o_, r_ = eng.local_search_state(nprob, res.source, res.seed, res.index, opts.max_rounds,
                                                 stop_ms=res.stats.get("stop_ms", -1))
             explicit = np.array(list(o_) + list(r_), dtype=np.uint8)
-        incumbent, baselines = None, []
-        if not res.exhaustive:
-            # heuristic searches also weigh the greedy baselines as incumbents (the B&B's
-            # "initial incumbent from rounding"): the plan is never worse than them
-            for builder in (optimus_allocation, current_practice_allocation):
-                b_opts, b_order = builder(prob)
-                baselines.append((np.array(list(b_opts) + list(b_order), dtype=np.uint8), list(b_order),
-                                  builder.__name__))
+        incumbent = None
         nexp = NativeProblem(prob, 62) if (baselines or res.kernel == "local") else None
         if res.kernel == "local":
             # the winner's final candidate and the baselines: one explicit batch, one launch
