@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define SAT_ABI_VERSION 5
+#define SAT_ABI_VERSION 6
 
 /* status codes (mapped to reference errors.py classes by the host layer) */
 #define SAT_OK              0
@@ -60,6 +60,10 @@ extern "C" {
 #define SAT_SRC_SUBSTREAM 1    /* candidate i <- SplitMix64 substream(seed, i) (rng.py:51) */
 #define SAT_SRC_SEED      2    /* candidate i <- SplitMix64(seed + i): plan_random(seed+i) */
 #define SAT_SRC_EXPLICIT  3    /* candidate i <- caller arrays options[i][J], order[i][J]  */
+#define SAT_SRC_GREEDY    4    /* sat_local_search (ABI v6): walker i starts at the greedy  */
+                               /* candidate -- every job at its least-area option, jobs in */
+                               /* descending order of duration x (2^17 + u), u = the top 16 */
+                               /* bits of draw j of substream(seed, i)                     */
 
 #define SAT_MAX_JOBS   64
 #define SAT_MAX_LANES  32      /* N nodes x G padded GPUs per node must fit one warp */

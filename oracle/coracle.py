@@ -58,10 +58,12 @@ def lib():
         _lib.oracle_local_search.restype = ctypes.c_double
         _lib.oracle_ls_search.argtypes = [_vp, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
                                           ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, _vp]
+        _lib.oracle_local_search_from.argtypes = [_vp, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp]
+        _lib.oracle_local_search_from.restype = ctypes.c_double
     return _lib
 
 
-SOURCES = {"index": 0, "substream": 1, "seed": 2}
+SOURCES = {"index": 0, "substream": 1, "seed": 2, "greedy": 4}
 
 
 class CProblem:
@@ -123,6 +125,15 @@ class CProblem:
         ms = lib().oracle_local_search(ctypes.byref(self.s), SOURCES[source], seed & ((1 << 64) - 1), walker,
                                        max_rounds, int(stop_ms), opt.ctypes.data, ordr.ctypes.data,
                                        ctypes.byref(rounds))
+        return ms, opt.tolist(), ordr.tolist(), rounds.value
+
+    def local_search_from(self, opts, order, max_rounds=4096, stop_ms=-1):
+        """(makespan, options, order, rounds) of the walk started at the candidate (opts, order)."""
+        opt = np.array(opts, dtype=np.int32)
+        ordr = np.array(order, dtype=np.int32)
+        rounds = ctypes.c_int()
+        ms = lib().oracle_local_search_from(ctypes.byref(self.s), max_rounds, int(stop_ms), opt.ctypes.data,
+                                            ordr.ctypes.data, ctypes.byref(rounds))
         return ms, opt.tolist(), ordr.tolist(), rounds.value
 
     def ls_search(self, source="substream", seed=0, lo=0, hi=1, max_rounds=4096, threads=0, stop_ms=-1):

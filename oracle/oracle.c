@@ -268,12 +268,56 @@ static void ls_neighbor(const oproblem *p, int m, int M1, int M2, const int *opt
     }
 }
 
+static double ls_walk(const oproblem *p, int max_rounds, int stop_ms, int *opt, int *ord, int *rounds_out);
+
+/* greedy start (source 4; engine SAT_SRC_GREEDY): every job at its least-area option (area = g
+ * x the least duration over the nodes that can run it, lowest option on ties); jobs ordered by
+ * key = that duration x (2^17 + u_j) descending, lower job first on ties, u_j = the top 16 bits
+ * of the j-th SplitMix64 output of the walker's substream state s0 */
+static void greedy_start(const oproblem *p, uint64_t s0, int *opt, int *ord) {
+    uint64_t key[OMAX_J];
+    for (int j = 0; j < p->J; ++j) {
+        double best_area = INFINITY, best_d = 0.0;
+        int best_o = 0;
+        for (int o = 0; o < p->radix[j]; ++o) {
+            int q = j * p->Cmax + o;
+            double d = INFINITY;
+            for (int n = 0; n < p->N; ++n)
+                if (((p->mask[q] >> n) & 1u) && p->gpus[q] <= p->node_gpus[n] && p->dur[q * p->N + n] < d)
+                    d = p->dur[q * p->N + n];
+            if (isinf(d)) continue;
+            double area = (double)p->gpus[q] * d;
+            if (area < best_area) { best_area = area; best_o = o; best_d = d; }
+        }
+        opt[j] = best_o;
+        uint64_t u = mix(s0 + (uint64_t)(j + 1) * GOLD) >> 48;
+        key[j] = (uint64_t)best_d * (131072ull + u);
+    }
+    for (int k = 0; k < p->J; ++k) {                  /* insertion sort: stable, key descending */
+        int x = k, i = k;
+        while (i > 0 && key[ord[i - 1]] < key[x]) { ord[i] = ord[i - 1]; --i; }
+        ord[i] = x;
+    }
+}
+
 double oracle_local_search(const oproblem *p, int source, uint64_t seed, uint64_t walker, int max_rounds,
                            int stop_ms, int *opt, int *ord, int *rounds_out) {
+    if (source == 4) greedy_start(p, mix((seed ^ walker) + GOLD), opt, ord);
+    else if (source == 1) decode_stream(p, mix((seed ^ walker) + GOLD), opt, ord);
+    else decode_stream(p, seed + walker, opt, ord);
+    return ls_walk(p, max_rounds, stop_ms, opt, ord, rounds_out);
+}
+
+/* the same walk from a given start (opt, ord are read, then overwritten with the final
+ * candidate): walkers seeded with explicit candidates */
+double oracle_local_search_from(const oproblem *p, int max_rounds, int stop_ms, int *opt, int *ord,
+                                int *rounds_out) {
+    return ls_walk(p, max_rounds, stop_ms, opt, ord, rounds_out);
+}
+
+static double ls_walk(const oproblem *p, int max_rounds, int stop_ms, int *opt, int *ord, int *rounds_out) {
     int M1, M2;
     int M = ls_counts(p, &M1, &M2);
-    if (source == 1) decode_stream(p, mix((seed ^ walker) + GOLD), opt, ord);
-    else decode_stream(p, seed + walker, opt, ord);
     double cur_load;
     double cur = eval_full(p, opt, ord, NULL, NULL, &cur_load);
     int rounds = 0, nopt[OMAX_J], nord[OMAX_J];

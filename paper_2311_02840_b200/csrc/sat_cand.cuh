@@ -661,7 +661,19 @@ struct LsArgs {
     unsigned long long *cursor;
     unsigned long long *rounds; // rounds of 32 moves executed, summed over walkers (zeroed before)
     uint8_t *state_out;         // [hi - lo][2J] final options then order of every walker (abandoned: untouched), or null
+    // greedy starts (SAT_SRC_GREEDY): every job takes its least-area option gopt[j]; the order
+    // is by the noisy key gdur[j] x (2^17 + u_j) descending (ties: lower job first), u_j the
+    // top 16 bits of the j-th draw of the walker's stream -- longest jobs first, perturbed
+    int32_t greedy;
+    uint8_t gopt[64];
+    uint32_t gdur[64];
 };
+
+// the greedy start's order key of job j (LsArgs::greedy); s0 = the walker's stream state
+__host__ __device__ inline uint64_t ls_greedy_key(uint32_t gdur, uint64_t s0, int j) {
+    const uint64_t u = mix64(s0 + (uint64_t)(j + 1) * kGolden) >> 48;
+    return (uint64_t)gdur * (131072ull + u);
+}
 
 // bytes of one block's region: every warp's free-time columns (a move's records are computed
 // per position from the walker's, no per-warp record column), then per walker its options /
@@ -830,8 +842,23 @@ k_ls(LsArgs a) {
         const uint64_t wk = s_walker[grp];
         if (wk >= total) break;
         const uint64_t id = a.lo + wk;
-        if (leader) {              // the walker's start: candidate id of the stream (plan_random's draw order)
-            Stream s{SRC == SAT_SRC_SUBSTREAM ? mix64((a.seed ^ id) + kGolden) : a.seed + id};
+        const uint64_t s0 = SRC == SAT_SRC_SUBSTREAM ? mix64((a.seed ^ id) + kGolden) : a.seed + id;
+        if (a.greedy) {            // greedy start: least-area options, perturbed longest-first order
+            if (gw == 0) {
+                for (int j = lane; j < J; j += 32) wopt[j] = a.gopt[j];
+                const uint64_t k0 = lane < J ? ls_greedy_key(a.gdur[lane], s0, lane) : 0;
+                const uint64_t k1 = lane + 32 < J ? ls_greedy_key(a.gdur[lane + 32], s0, lane + 32) : 0;
+                int r0 = 0, r1 = 0;        // rank = jobs ahead: larger key, or equal key and lower id
+                for (int i = 0; i < J; ++i) {
+                    const uint64_t ki = __shfl_sync(0xffffffffu, i < 32 ? k0 : k1, i & 31);
+                    r0 += ki > k0 || (ki == k0 && i < lane);
+                    r1 += ki > k1 || (ki == k1 && i < lane + 32);
+                }
+                if (lane < J) { word[r0] = (uint8_t)lane; wpos[lane] = (uint8_t)r0; }
+                if (lane + 32 < J) { word[r1] = (uint8_t)(lane + 32); wpos[lane + 32] = (uint8_t)r1; }
+            }
+        } else if (leader) {       // the walker's start: candidate id of the stream (plan_random's draw order)
+            Stream s{s0};
             for (int j = 0; j < J; ++j) wopt[j] = (uint8_t)s.below((uint32_t)tb.radix[j], tb.mods);
             for (int k = 0; k < J; ++k) word[k] = (uint8_t)k;
             for (int i = J - 1; i >= 1; --i) {

@@ -1011,6 +1011,32 @@ int sat_ls_counter_offset(const sat_problem_t *p, size_t *offset) {
     return SAT_OK;
 }
 
+// greedy starts: per job the least-area usable option (area = g x its least duration over
+// the nodes that can run it; ties: lowest option) and that duration, the order key's base
+static bool ls_greedy_tables(const sat_problem_t *p, uint8_t *gopt, uint32_t *gdur) {
+    if (p->J > 64) return false;
+    const uint32_t all = p->N >= 32 ? ~0u : ((1u << p->N) - 1u);
+    for (int j = 0; j < p->J; ++j) {
+        int64_t best_area = INT64_MAX;
+        int best_o = -1;
+        int32_t best_d = 0;
+        for (int o = 0; o < p->radix[j]; ++o) {
+            const int q = j * p->Cmax + o;
+            const uint32_t m = p->node_mask ? p->node_mask[q] & all : all;
+            int32_t d = INT32_MAX;
+            for (int n = 0; n < p->N; ++n)
+                if (((m >> n) & 1u) && p->gpus[q] <= p->node_gpus[n]) d = std::min(d, p->dur_i32[q * p->N + n]);
+            if (d == INT32_MAX) continue;
+            const int64_t area = (int64_t)p->gpus[q] * d;
+            if (area < best_area) { best_area = area; best_o = o; best_d = d; }
+        }
+        if (best_o < 0) return false;
+        gopt[j] = (uint8_t)best_o;
+        gdur[j] = (uint32_t)std::max<int32_t>(best_d, 0);
+    }
+    return true;
+}
+
 int sat_local_search(const sat_problem_t *p, int32_t source, uint64_t seed, uint64_t lo, uint64_t hi,
                      int32_t max_rounds, int32_t stop_ms, sat_best_t *d_best, uint8_t *d_state_out, void *d_ws,
                      size_t ws_bytes,
@@ -1019,7 +1045,7 @@ int sat_local_search(const sat_problem_t *p, int32_t source, uint64_t seed, uint
     int st = validate(p);
     if (st) return st;
     if (!d_best || hi < lo || max_rounds < 0 || max_rounds >= (1 << SAT_LS_ROUND_BITS)) return SAT_ERR_INVALID;
-    if (source != SAT_SRC_SUBSTREAM && source != SAT_SRC_SEED) return SAT_ERR_INVALID;
+    if (source != SAT_SRC_SUBSTREAM && source != SAT_SRC_SEED && source != SAT_SRC_GREEDY) return SAT_ERR_INVALID;
     if (p->time_mode != SAT_TIME_GRID_I32) return SAT_ERR_UNSUPPORTED;
     if (p->J < 2) return SAT_ERR_UNSUPPORTED;
     if (hi > 0 && ((hi - 1) >> p->idx_bits)) return SAT_ERR_TOO_LARGE;
@@ -1029,6 +1055,11 @@ int sat_local_search(const sat_problem_t *p, int32_t source, uint64_t seed, uint
     a.lo = lo; a.hi = hi; a.seed = seed; a.max_rounds = max_rounds; a.best = d_best; a.state_out = d_state_out;
     a.stop_ms = stop_ms < 0 ? -1 : stop_ms; a.idx_bits = p->idx_bits;
     cudaStream_t s = (cudaStream_t)stream;
+    if (source == SAT_SRC_GREEDY) {
+        if (!ls_greedy_tables(p, a.gopt, a.gdur)) return SAT_ERR_NO_OPTIONS;
+        a.greedy = 1;                                  // noise from the walker's substream
+        return launch_ls<SAT_SRC_SUBSTREAM>(p, a, d_ws, ws_bytes, s);
+    }
     if (source == SAT_SRC_SUBSTREAM) return launch_ls<SAT_SRC_SUBSTREAM>(p, a, d_ws, ws_bytes, s);
     return launch_ls<SAT_SRC_SEED>(p, a, d_ws, ws_bytes, s);
 }

@@ -24,7 +24,7 @@ LIB_PATH = os.environ.get("SATURN_ENGINE_LIB") or os.path.join(os.path.dirname(o
 
 SAT_OK, SAT_ERR_INVALID, SAT_ERR_NO_OPTIONS, SAT_ERR_TOO_LARGE, SAT_ERR_UNSUPPORTED, SAT_ERR_CUDA = range(6)
 SAT_TIME_GRID_I32, SAT_TIME_F64 = 0, 1
-SRC_INDEX, SRC_SUBSTREAM, SRC_SEED, SRC_EXPLICIT = 0, 1, 2, 3
+SRC_INDEX, SRC_SUBSTREAM, SRC_SEED, SRC_EXPLICIT, SRC_GREEDY = 0, 1, 2, 3, 4
 INT64_MAX = (1 << 63) - 1
 LS_ROUND_BITS = 13          # SAT_LS_ROUND_BITS: local-search keys are (makespan, rounds, walker)
 
@@ -109,7 +109,7 @@ def load_library(path: str = LIB_PATH):
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res
-    if lib.sat_abi_version() != 5:
+    if lib.sat_abi_version() != 6:
         raise E.PlanFailure("libsaturn_b200.so ABI version mismatch")
     _LIB = lib
     return lib
@@ -672,7 +672,7 @@ class Engine:
             # waves of walkers in walker order; stop after the first wave whose best meets the
             # lower bound (proven optimal).  The stop depends only on completed waves, so the
             # result is deterministic.
-            src = SRC_SUBSTREAM if source is None else source
+            src = (SRC_GREEDY if opts.ls_start == "greedy" else SRC_SUBSTREAM) if source is None else source
             seed_used = opts.seed if seed is None else seed
             target = prob.lower_bound() if nprob.grid else -1.0
             stop_ms = int(target) if (nprob.grid and opts.ls_stop) else -1

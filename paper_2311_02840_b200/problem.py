@@ -57,6 +57,9 @@ class SolveOptions:
                                         # generation (2 x SMs) of 16-warp walkers (>= 24 jobs)
     max_rounds: int = 4096              # local search: rounds of 32 moves per walker
     ls_stop: bool = True                # local search: a walk ends at the lower bound (same result)
+    ls_start: str = "greedy"            # local search: walker w starts at the greedy candidate perturbed
+                                        # by substream(seed, w) ("greedy"), or at candidate w of the
+                                        # sampled stream ("sampled")
     kernel: str = "auto"                # auto (bnb when it applies) | tree | index | bnb
     prove: bool = True                  # local search on one node: prove / improve the best makespan
                                         # with the state-space search (sat_search_dp) after a wave

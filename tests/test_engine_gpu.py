@@ -423,10 +423,13 @@ def test_local_search_records_every_walker_state(eng, name, stop):
     for i in range(W):
         _, o, r, _ = cp.local_search(lo + i, "substream", 7, 4096, stop_ms=stop)
         assert got[i].tolist() == o + r, (name, i)
-    res = eng.search(prob, SolveOptions(search="local", walkers=64, wave=64, seed=7))
-    assert res.state is not None
-    _, o, r, _ = cp.local_search(res.index, "substream", 7, 4096, stop_ms=res.stats["stop_ms"])
-    assert (list(res.state[0]), list(res.state[1])) == (o, r)
+    for start in ("greedy", "sampled"):
+        res = eng.search(prob, SolveOptions(search="local", walkers=64, wave=64, seed=7, ls_start=start))
+        assert res.state is not None
+        assert res.source == (EN.SRC_GREEDY if start == "greedy" else EN.SRC_SUBSTREAM)
+        src = "greedy" if start == "greedy" else "substream"
+        _, o, r, _ = cp.local_search(res.index, src, 7, 4096, stop_ms=res.stats["stop_ms"])
+        assert (list(res.state[0]), list(res.state[1])) == (o, r)
 
 
 @pytest.mark.parametrize("group", ["1", "4", "8", "16", "32"])
@@ -471,6 +474,40 @@ def test_local_search_seed_source_and_release(eng):
         for walker in (0, 3, 11):
             ms, o, r, _ = cp.local_search(walker, "seed", 5, 4096)
             assert eng.local_search_state(nprob, EN.SRC_SEED, 5, walker, 4096) == (o, r), (trial, walker)
+
+
+@pytest.mark.parametrize("group", ["1", "16"])
+def test_local_search_greedy_starts(eng, group, monkeypatch):
+    """SAT_SRC_GREEDY (the default start): every job at its least-area option, jobs in the
+    perturbed longest-first order of the walker's substream -- one node, several nodes,
+    heterogeneous nodes, releases and initial free times, 1 and 16 warps per walker: each
+    walker's final candidate, and the search key over a walker range with and without the stop
+    at the bound, equal the oracle's restatement (greedy_start + the same walk)."""
+    monkeypatch.setenv("SATURN_LS_GROUP", group)
+    rng = random.Random(23)
+    cases = [workload_problem(n)[2:] for n in ("cfg3", "cfg4", "hetero6")]
+    for trial in range(8):
+        nodes = [[8], [4, 4], [16], [6, 3], [2, 2, 2]][trial % 5]
+        op = random_problem(rng, rng.randint(3, 9), nodes, max_opts=4, max_d=9, hetero=trial % 3 == 2)
+        if trial % 2:
+            op.release = [rng.randint(0, 4) for _ in range(op.J)]
+            op.init_free = [sorted(rng.randint(0, 3) for _ in range(n)) for n in nodes]
+        cases.append((to_search_problem(op), op))
+    for prob, op in cases:
+        cp = C.CProblem(op)
+        bits, _ = prob.key_bits(1 << 10)
+        nprob = EN.NativeProblem(prob, bits)
+        lb = int(prob.lower_bound())
+        for walker in (0, 1, 7):
+            ms, o, r, _ = cp.local_search(walker, "greedy", 11, 4096)
+            assert eng.local_search_state(nprob, EN.SRC_GREEDY, 11, walker, 4096) == (o, r), (prob.J, walker)
+        for stop in (-1, lb):
+            best = eng.reset_best()
+            eng.local_search(nprob, EN.SRC_GREEDY, 11, 0, 24, 4096, best, stop_ms=stop)
+            k = int(best.cpu().numpy().view(np.uint64)[0])
+            ms_, rr_, wk_ = EN.ls_key_fields(k, bits)
+            assert (float(ms_), wk_) == cp.ls_search("greedy", 11, 0, 24, 4096, stop_ms=stop)
+            assert rr_ == cp.local_search(wk_, "greedy", 11, 4096, stop_ms=stop)[3]
 
 
 def test_bnb_fixed_depth_walkers_equal_full_scan(eng):

@@ -11,6 +11,7 @@ from oracle import coracle as C
 from oracle import saturn_oracle as O
 import paper_2311_02840_b200 as S
 from paper_2311_02840_b200 import domain as D
+from paper_2311_02840_b200 import engine as EN
 from paper_2311_02840_b200 import planners as PL
 from paper_2311_02840_b200.problem import SolveOptions
 from paper_2311_02840_b200.profiling import ProfileTable, SyntheticExecutor, build_profile_table
@@ -153,11 +154,15 @@ def test_plan_saturn_bnb_equals_exhaustive():
 
 @pytest.mark.parametrize("name", ["cfg3", "cfg4"])
 def test_local_search_plan_beats_its_own_starts(name):
-    """search="local": each walker ends at or below its start, so the best walker is at least as
-    good as sampling the same candidates; the decoded plan is valid and replays to the key."""
+    """search="local" from sampled starts: each walker ends at or below its start, so the best
+    walker is at least as good as sampling the same candidates; the decoded plan is valid and
+    replays to the key.  The default greedy starts do at least as well here."""
     w, t = setup(name)
     n = 2048
-    loc = PL.solve(t, w, None, SolveOptions(search="local", walkers=n))
+    loc = PL.solve(t, w, None, SolveOptions(search="local", walkers=n, ls_start="sampled"))
+    gre = PL.solve(t, w, None, SolveOptions(search="local", walkers=n))
+    assert gre.search.source == EN.SRC_GREEDY and gre.makespan <= loc.makespan
+    D.check_plan(gre.plan, w, gre.runtimes)
     smp = PL.solve(t, w, None, SolveOptions(search="sampled", budget=n))
     assert loc.status in ("Local", "Optimal") and loc.makespan <= smp.makespan
     assert loc.lower_bound <= loc.makespan
