@@ -128,6 +128,8 @@ k_generic(GenArgs a) {
                 const int c = pass * segs + seg;
                 const uint64_t c_off = __shfl_sync(0xffffffffu, off, c);
                 const bool c_valid = __shfl_sync(0xffffffffu, (int)valid, c) != 0;
+                // every segment on a parked slot (no candidate): nothing to schedule in this pass
+                if (!__any_sync(0xffffffffu, c_valid)) continue;
                 const uint64_t c_id = shfl_u64(id, c);
                 const uint32_t *c_steps = steps + c;
                 T av = my_init;

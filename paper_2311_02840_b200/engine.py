@@ -680,11 +680,12 @@ class Engine:
             self._check(self.lib.sat_ls_counter_offset(nprob.ref, ctypes.byref(off)), nprob=nprob)
             # geometric waves (wave, 4 x wave, 16 x wave, ...): a small first wave keeps easy
             # problems cheap, larger later waves keep the GPU full when the bound is not met
-            # first wave: 8 192 one-warp walkers (< 24 jobs); for 16-warp walkers one resident
+            # first wave: 2 048 one-warp walkers (< 24 jobs); for 16-warp walkers one resident
             # generation -- two 512-thread blocks per SM (64 registers) -- since with keys
             # (makespan, rounds, walker) every walker of the wave runs until it falls behind
-            # the fastest one at the bound (profiles/r02_ls_tiebreak_wave.txt)
-            wave = max(1, int(opts.wave)) if opts.wave else (8192 if prob.J < 24 else 2 * self.sm_count)
+            # the fastest one at the bound (profiles/r02_ls_tiebreak_wave.txt; greedy starts:
+            # profiles/r02h_greedy_wave_sweep.txt)
+            wave = max(1, int(opts.wave)) if opts.wave else (2048 if prob.J < 24 else 2 * self.sm_count)
             rounds_total, walkers_done, waves = 0, 0, 0
             w0 = 0
             ls_states = []          # (first walker, [walkers][2J] final states) per wave on this rank

@@ -53,7 +53,7 @@ class SolveOptions:
     seed: int = 7                       # sampled stream: candidate i = substream(seed, i)
     walkers: int = 1 << 16              # local search: walkers at most (walker w starts at candidate w)
     wave: int | None = None             # local search: first wave (then x4 per wave); stops at the bound.
-                                        # None: 8192 walkers of one warp (< 24 jobs), one resident
+                                        # None: 2048 walkers of one warp (< 24 jobs), one resident
                                         # generation (2 x SMs) of 16-warp walkers (>= 24 jobs)
     max_rounds: int = 4096              # local search: rounds of 32 moves per walker
     ls_stop: bool = True                # local search: a walk ends at the lower bound (same result)
