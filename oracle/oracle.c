@@ -10,7 +10,9 @@
  *   - list scheduling "earliest-fit" over explicit per-GPU free
  *     times with GPU ids: node = the one finishing the job earliest (start = g-th
  *     smallest free time max release, + duration on that node), lowest node on ties; the g earliest-free GPUs (lowest id on ties) run the job,
- *   - best = lowest (makespan, id).
+ *   - best = lowest (makespan, id),
+ *   - the engine's local search (oracle_local_search: sampled or greedy starts, the same
+ *     moves, tie-breaks, rounds and stop rule as k_ls).
  * Times are doubles in both modes (grid intervals are small integers, exact).
  * OpenMP splits the id range into contiguous chunks, one per thread.
  */
