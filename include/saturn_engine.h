@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define SAT_ABI_VERSION 6
+#define SAT_ABI_VERSION 7
 
 /* status codes (mapped to reference errors.py classes by the host layer) */
 #define SAT_OK              0
@@ -238,6 +238,16 @@ int sat_shared_best_alloc(sat_best_t **d_cell, uint8_t *handle_out);
 int sat_shared_best_open(const uint8_t *handle, sat_best_t **d_cell);
 int sat_shared_best_close(sat_best_t *d_cell, int32_t owner);
 int sat_peer_atomics(int32_t dev_a, int32_t dev_b, int32_t *supported);
+
+/* Search key hand-off (ABI v7), one launch on `stream`: d_out[0..n_words) = the words of
+ * *d_best with "empty" (all ones) mapped to INT64_MAX (the MIN identity of the cross-rank
+ * all-reduce), d_out[n_words + e] = d_extra[e] for e < n_extra (e.g. bound-and-prune's counters,
+ * so key and counters come back in one read); if d_ids != NULL, d_ids[0] = the candidate id
+ * the winner replay decodes: the low idx_bits of the grid key, or 0 when the key is empty or
+ * (check_range) >= n_idx.  d_best == NULL: only d_ids, from d_out[0] (after the all-reduce). */
+int sat_key_finish(const sat_best_t *d_best, int32_t n_words, const uint64_t *d_extra, int32_t n_extra,
+                   int64_t *d_out, uint64_t *d_ids, int32_t idx_bits, uint64_t n_idx, int32_t check_range,
+                   void *stream);
 
 /* INT32 min/max issue-rate probe for the roofline denominator: runs `iters`
  * dependent-chain IMNMX iterations on every SM; *d_ops_out = lane-ops done. */

@@ -702,6 +702,37 @@ int sat_best_copy(sat_best_t *d_dst, const sat_best_t *d_src, void *stream) {
     return check_cuda(cudaMemcpyAsync(d_dst, d_src, sizeof(sat_best_t), cudaMemcpyDefault, (cudaStream_t)stream));
 }
 
+// ---- search key hand-off (ABI v7): one launch instead of the host library's elementwise ops ----
+// out[0..n_words) = the best cell's words, "empty" (all ones) -> INT64_MAX; out[n_words + e] =
+// extra[e]; ids[0] = the replay id of out[0] (grid key: low idx_bits; an empty or out-of-range
+// key -> 0, an id the decode can take).  best == NULL: ids only (after a cross-rank MIN of out).
+static __global__ void k_key_finish(const uint64_t *best, int n_words, const uint64_t *extra, int n_extra,
+                                    int64_t *out, uint64_t *ids, int idx_bits, uint64_t n_idx, int check) {
+    const int i = threadIdx.x;
+    if (best && i < n_words) {
+        const uint64_t v = best[i];
+        out[i] = v == ~0ull ? INT64_MAX : (int64_t)v;
+    }
+    if (i < n_extra) out[n_words + i] = (int64_t)extra[i];
+    if (ids && i == 0) {
+        const uint64_t v = best ? best[0] : (uint64_t)out[0];
+        const int64_t k = (best && v == ~0ull) ? INT64_MAX : (int64_t)v;
+        const uint64_t idx = (uint64_t)k & ((idx_bits >= 64) ? ~0ull : ((1ull << idx_bits) - 1ull));
+        ids[0] = (k == INT64_MAX || (check && idx >= n_idx)) ? 0ull : idx;
+    }
+}
+
+int sat_key_finish(const sat_best_t *d_best, int32_t n_words, const uint64_t *d_extra, int32_t n_extra,
+                   int64_t *d_out, uint64_t *d_ids, int32_t idx_bits, uint64_t n_idx, int32_t check_range,
+                   void *stream) {
+    if (!d_out || n_words < 1 || n_words > 2 || n_extra < 0 || n_extra > 30 || (n_extra && !d_extra) ||
+        idx_bits < 1 || idx_bits > 64)
+        return SAT_ERR_INVALID;
+    k_key_finish<<<1, 32, 0, (cudaStream_t)stream>>>(reinterpret_cast<const uint64_t *>(d_best), n_words,
+                                                    d_extra, n_extra, d_out, d_ids, idx_bits, n_idx, check_range);
+    return check_cuda(cudaGetLastError());
+}
+
 int sat_shared_best_alloc(sat_best_t **d_cell, uint8_t *handle_out) {
     if (!d_cell || !handle_out) return SAT_ERR_INVALID;
     static_assert(sizeof(cudaIpcMemHandle_t) == SAT_IPC_HANDLE_BYTES, "IPC handle size");

@@ -91,6 +91,7 @@ _SIGS = {
     "sat_shared_best_close": ([_vp, _i32], _i32),
     "sat_peer_atomics": ([_i32, _i32, _vp], _i32),
     "sat_search_dp": ([_vp, _i32, _u64, _vp, _vp, _vp, ctypes.c_size_t, _vp], _i32),
+    "sat_key_finish": ([_vp, _i32, _vp, _i32, _vp, _vp, _i32, _u64, _i32, _vp], _i32),
 }
 
 _LIB = None
@@ -109,7 +110,7 @@ def load_library(path: str = LIB_PATH):
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res
-    if lib.sat_abi_version() != 6:
+    if lib.sat_abi_version() != 7:
         raise E.PlanFailure("libsaturn_b200.so ABI version mismatch")
     _LIB = lib
     return lib
@@ -771,27 +772,21 @@ class Engine:
             on_launched(mode)
         if shared is not None:
             shared.collect(best)
-        key_dev = _combine_dev(best, nprob.grid, group, world)
-        # bound-and-prune's counters sit at the start of the workspace, which the replay's
-        # launch below reuses: keep a device copy first
-        cnt_dev = bnb_ws[:24].view(torch.int64).clone() if bnb_ws is not None else None
-        replay_out = None
-        if replay and nprob.grid and mode in ("exhaustive", "sampled"):
-            # (bound-and-prune too: its key always holds a real candidate -- the seed bound comes
-            # from a candidate of the same space, which the search itself reaches)
-            kk = key_dev[:1]
-            idx = kk & ((1 << idx_bits) - 1)
-            bad = kk == INT64_MAX
-            if mode == "exhaustive":
-                bad = bad | (idx >= n_idx)
-            ids_dev = torch.where(bad, torch.zeros_like(idx), idx)     # an id the decode can take
-            replay_out = self.schedule(nprob, src, seed_used, ids_dev=ids_dev)
-        if bnb_ws is not None:               # key and the search's counters in one read-back
-            both = torch.cat([key_dev, cnt_dev]).cpu().tolist()
-            key, cnt = both[:2], both[2:]
+        # key hand-off: the combined key, bound-and-prune's counters (they sit at the start of
+        # the workspace, which the replay's launch below reuses) and the replay id, in one
+        # launch (sat_key_finish) and later one read-back
+        do_replay = replay and nprob.grid and mode in ("exhaustive", "sampled")
+        # (bound-and-prune replays too: its key always holds a real candidate -- the seed bound
+        # comes from a candidate of the same space, which the search itself reaches)
+        key_dev, ids_dev = self._key_finish(best, nprob.grid, group, world, idx_bits, n_idx,
+                                            extra=bnb_ws, want_ids=do_replay,
+                                            check_range=mode == "exhaustive")
+        replay_out = self.schedule(nprob, src, seed_used, ids_dev=ids_dev) if do_replay else None
+        both = key_dev.cpu().tolist()
+        key = both[:2]
+        if bnb_ws is not None:
+            cnt = both[2:]
             stats.update(pruned_tasks=cnt[1], pair_nodes=cnt[2])
-        else:
-            key = key_dev.cpu().tolist()
         ev1.synchronize()
         dev_s = ev0.elapsed_time(ev1) / 1e3
         if shared is not None:
@@ -823,6 +818,35 @@ class Engine:
                             device_seconds=dev_s, wall_seconds=time.perf_counter() - t0,
                             stats=stats, idx_bits=idx_bits, state=ls_state, replay=replay_out,
                             proven=mode == "local" and proven_opt)
+
+    def _key_finish(self, best, grid: bool, group, world: int, idx_bits: int, n_idx: int, *, extra=None,
+                    want_ids: bool = False, check_range: bool = False):
+        """(key [2 (+3 counters)] int64, replay id [1] or None) on the device: `_combine_dev`
+        plus the replay id through one sat_key_finish launch (grid keys; float keys combine
+        through `_combine_dev`).  With several ranks the key is all-reduced (MIN) in between."""
+        torch = self.torch
+        if not grid:
+            return _combine_dev(best, grid, group, world), None
+        n_extra = 3 if extra is not None else 0
+        out = torch.empty(2 + n_extra, dtype=torch.int64, device=self.device)
+        ids = torch.empty(1, dtype=torch.int64, device=self.device) if want_ids else None
+        stream = _vp(self.stream())
+        one_launch = world == 1
+        self._check(self.lib.sat_key_finish(
+            _vp(best.data_ptr()), 2, _vp(extra.data_ptr()) if extra is not None else None, n_extra,
+            _vp(out.data_ptr()), _vp(ids.data_ptr()) if (ids is not None and one_launch) else None,
+            idx_bits, n_idx & ((1 << 64) - 1), int(check_range), stream), what="sat_key_finish")
+        self.launches += 1
+        if not one_launch:
+            import torch.distributed as dist
+
+            dist.all_reduce(out[:1], op=dist.ReduceOp.MIN, group=group)
+            if ids is not None:
+                self._check(self.lib.sat_key_finish(None, 2, None, 0, _vp(out.data_ptr()), _vp(ids.data_ptr()),
+                                                    idx_bits, n_idx & ((1 << 64) - 1), int(check_range), stream),
+                            what="sat_key_finish")
+                self.launches += 1
+        return out, ids
 
     def _walker_state(self, ls_states, index: int, J: int, group, world: int):
         """The winning walker's final (options, order), recorded by its search launch (on the

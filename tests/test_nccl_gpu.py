@@ -53,3 +53,33 @@ def test_max_over_ranks_over_nccl(nccl_group):
     t = torch.tensor([1.25], dtype=torch.float64, device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=nccl_group)
     assert float(t.item()) == 1.25
+
+
+def _finish(eng, best, world, group, idx_bits, n_idx, extra=None, check=True):
+    key, ids = eng._key_finish(best, True, group, world, idx_bits, n_idx, extra=extra, want_ids=True,
+                               check_range=check)
+    return key.cpu().tolist(), int(ids.cpu()[0])
+
+
+def test_key_finish_matches_combine(nccl_group):
+    """sat_key_finish (ABI v7) = `_combine_dev` + the replay-id rule it replaced: empty -> INT64_MAX,
+    id = low idx_bits (0 when empty or, for exhaustive spaces, out of range); counters appended;
+    the world > 1 path all-reduces between the two launches."""
+    from paper_2311_02840_b200 import planners as PL
+
+    eng = PL.get_engine(0)
+    bits = 35
+    key = (30 << bits) | 38747577
+    cnt = torch.tensor([7, 11, 13], dtype=torch.int64, device="cuda")
+    for world in (1, 2):
+        best = torch.tensor([key, 5], dtype=torch.int64, device="cuda")
+        out, rid = _finish(eng, best, world, nccl_group, bits, 1 << 34, extra=cnt.view(torch.uint8))
+        assert out[:2] == EN._combine(best, True, nccl_group, world)
+        assert out[2:] == [7, 11, 13] and rid == 38747577
+        empty = torch.tensor([-1, -1], dtype=torch.int64, device="cuda")
+        out, rid = _finish(eng, empty, world, nccl_group, bits, 1 << 34)
+        assert out == [EN.INT64_MAX, EN.INT64_MAX] and rid == 0
+        # an index past the space (exhaustive check) decodes as 0; without the check it stands
+        far = torch.tensor([(30 << bits) | ((1 << bits) - 1), 0], dtype=torch.int64, device="cuda")
+        assert _finish(eng, far, world, nccl_group, bits, 1000)[1] == 0
+        assert _finish(eng, far, world, nccl_group, bits, 1000, check=False)[1] == (1 << bits) - 1
