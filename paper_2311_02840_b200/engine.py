@@ -638,7 +638,7 @@ class Engine:
         else:
             kbest = best
         job_steps = 0
-        stats, bnb_ws = None, None
+        stats, bnb_ws, ls_key = None, None, None
         ls_state = None
         proven_opt = False
         if mode == "exhaustive":
@@ -729,11 +729,16 @@ class Engine:
                             dp_ok = False            # out of budget at the bound: higher targets too
                     except (E.TooLarge, err.TooLarge, E.InvariantViolation, err.InvariantViolation):
                         dp_ok = False
-                rounds_total += int(self._ws[off.value:off.value + 8].view(torch.int64).item())
                 walkers_done, waves, w0, wave = w1, waves + 1, w1, wave * 4
                 if shared is not None:
                     shared.collect(best)
-                k = int(_combine(best, True, group, world)[0])
+                # the combined key and this rank's rounds counter: one launch, one read-back
+                kw, _ = self._key_finish(best, True, group, world, idx_bits, n_idx,
+                                         extra=self._ws[off.value:off.value + 8], extra_words=1)
+                kv = kw.cpu().tolist()
+                rounds_total += int(kv[2])
+                k = int(kv[0])
+                ls_key = kv[:2]
                 k_ms = ls_key_fields(k, idx_bits)[0]
                 if k != INT64_MAX and k_ms <= target:
                     break
@@ -778,11 +783,14 @@ class Engine:
         do_replay = replay and nprob.grid and mode in ("exhaustive", "sampled")
         # (bound-and-prune replays too: its key always holds a real candidate -- the seed bound
         # comes from a candidate of the same space, which the search itself reaches)
-        key_dev, ids_dev = self._key_finish(best, nprob.grid, group, world, idx_bits, n_idx,
-                                            extra=bnb_ws, want_ids=do_replay,
-                                            check_range=mode == "exhaustive")
-        replay_out = self.schedule(nprob, src, seed_used, ids_dev=ids_dev) if do_replay else None
-        both = key_dev.cpu().tolist()
+        if mode == "local" and ls_key is not None:
+            both, replay_out = ls_key, None         # read back after the last wave already
+        else:
+            key_dev, ids_dev = self._key_finish(best, nprob.grid, group, world, idx_bits, n_idx,
+                                                extra=bnb_ws, want_ids=do_replay,
+                                                check_range=mode == "exhaustive")
+            replay_out = self.schedule(nprob, src, seed_used, ids_dev=ids_dev) if do_replay else None
+            both = key_dev.cpu().tolist()
         key = both[:2]
         if bnb_ws is not None:
             cnt = both[2:]
@@ -820,14 +828,15 @@ class Engine:
                             proven=mode == "local" and proven_opt)
 
     def _key_finish(self, best, grid: bool, group, world: int, idx_bits: int, n_idx: int, *, extra=None,
-                    want_ids: bool = False, check_range: bool = False):
-        """(key [2 (+3 counters)] int64, replay id [1] or None) on the device: `_combine_dev`
-        plus the replay id through one sat_key_finish launch (grid keys; float keys combine
-        through `_combine_dev`).  With several ranks the key is all-reduced (MIN) in between."""
+                    extra_words: int = 3, want_ids: bool = False, check_range: bool = False):
+        """(key [2 (+ extra_words counters)] int64, replay id [1] or None) on the device:
+        `_combine_dev` plus the replay id through one sat_key_finish launch (grid keys; float
+        keys combine through `_combine_dev`).  With several ranks the key is all-reduced (MIN)
+        in between (the counters stay this rank's)."""
         torch = self.torch
         if not grid:
             return _combine_dev(best, grid, group, world), None
-        n_extra = 3 if extra is not None else 0
+        n_extra = extra_words if extra is not None else 0
         out = torch.empty(2 + n_extra, dtype=torch.int64, device=self.device)
         ids = torch.empty(1, dtype=torch.int64, device=self.device) if want_ids else None
         stream = _vp(self.stream())
@@ -852,6 +861,11 @@ class Engine:
         """The winning walker's final (options, order), recorded by its search launch (on the
         rank that ran it; other ranks receive it through an all-reduce MAX of zeros)."""
         torch = self.torch
+        if world == 1:                  # one rank: the row itself, one copy (no kernels)
+            for lo, hi, buf in ls_states:
+                if lo <= index < hi:
+                    out = buf[(index - lo) * 2 * J:(index - lo + 1) * 2 * J].cpu().tolist()
+                    return out[:J], out[J:]
         v = torch.zeros(2 * J, dtype=torch.int32, device=self.device)
         for lo, hi, buf in ls_states:
             if lo <= index < hi:

@@ -286,23 +286,27 @@ def solve_problem(prob: SearchProblem, workload, opts: SolveOptions, running_con
             explicit = np.array(list(o_) + list(r_), dtype=np.uint8)
         incumbent = None
         nexp = NativeProblem(prob, 62) if (baselines or res.kernel == "local") else None
+        # device schedules (option, node, start, makespan) of the winner and the baselines; a
+        # Plan is built only for the one returned (the others are compared by makespan)
         if res.kernel == "local":
             # the winner's final candidate and the baselines: one explicit batch, one launch
-            cands = _decode(eng, prob, nexp, workload, SRC_EXPLICIT, 0,
-                            explicit=np.stack([explicit] + [b[0] for b in baselines]))
-            plan, options, ms, runtimes = cands[0]
-            cands = cands[1:]
+            sched = eng.schedule(nexp, SRC_EXPLICIT, 0, explicit=np.stack([explicit] + [b[0] for b in baselines]))
+            win, rows = (sched, 0), [(sched, 1 + i) for i in range(len(baselines))]
         else:
             if res.replay is not None:          # replayed on the device behind the search
-                plan, options, ms, runtimes = _plan_of(prob, workload, res.replay, 0)
+                win = (res.replay, 0)
             else:
                 src = SRC_INDEX if res.exhaustive else res.source
-                plan, options, ms, runtimes = _decode(eng, prob, nprob, workload, src, res.seed, ident=res.index)
-            cands = _decode(eng, prob, nexp, workload, SRC_EXPLICIT, 0,
-                            explicit=np.stack([b[0] for b in baselines])) if baselines else []
-        for cand, (_, b_order, name) in zip(cands, baselines):
-            if cand[2] < ms and (incumbent is None or cand[2] < incumbent[0][2]):
-                incumbent = (cand, b_order, name)
+                win = (eng.schedule(nprob, src, res.seed, ids=[res.index]), 0)
+            bs = eng.schedule(nexp, SRC_EXPLICIT, 0, explicit=np.stack([b[0] for b in baselines])) if baselines else None
+            rows = [(bs, i) for i in range(len(baselines))]
+        ms = float(win[0][3][win[1]])
+        for (bsch, r), (_, b_order, name) in zip(rows, baselines):
+            b_ms = float(bsch[3][r])
+            if b_ms < ms and (incumbent is None or b_ms < incumbent[0]):
+                incumbent = (b_ms, (bsch, r), b_order, name)
+        if incumbent is None:
+            plan, options, ms, runtimes = _plan_of(prob, workload, win[0], win[1])
     except (E.SchedulerError, err.SchedulerError):      # ours or the caller family's: as raised
         raise
     except Exception as exc:  # CUDA / NCCL trouble -> PlanFailure (ReplanFailure on re-solve)
@@ -315,9 +319,11 @@ def solve_problem(prob: SearchProblem, workload, opts: SolveOptions, running_con
     elif res.kernel == "local":
         order = [int(x) for x in explicit[prob.J:]]
     else:
-        order = sorted(range(prob.J), key=lambda j: (plan.entries[prob.job_ids[j]].start_time, j))
+        w_start = win[0][2][win[1]]
+        order = sorted(range(prob.J), key=lambda j: (float(w_start[j]), j))
     if incumbent is not None:
-        (plan, options, ms, runtimes), order, source_name = incumbent
+        _, (bsch, r), order, source_name = incumbent
+        plan, options, ms, runtimes = _plan_of(prob, workload, bsch, r)
         res.stats = {**(res.stats or {}), "incumbent": source_name}
     makespan = ms
     if validate:

@@ -247,6 +247,7 @@ class _OneNodeRow:
 
 
 _ONE_NODE_MEMO: dict = {}
+_ONE_NODE_FAST: dict = {}     # (id(job), id(cluster)) -> (job, cluster, techniques, memo entry)
 _ARRAY_ROW_MIN = 48          # one-node rows with at least this many configs go through arrays
 
 
@@ -254,9 +255,17 @@ def _one_node_options(job, workload):
     """(configs, profile-table keys, gang sizes, per-node eligibility) of `feasible_configs`
     (core.py:165-182) for one job, a pure function of immutable inputs memoised by value like
     `feasible_configs` itself.  Eligibility depends on a node only through its shape."""
+    cluster = workload.cluster
+    fast = _ONE_NODE_FAST.get((id(job), id(cluster)))
+    if fast is not None and fast[0] is job and fast[1] is cluster:
+        # the same (hashable, hence frozen) objects as a memoised call: skip hashing them
+        # (pydantic / dataclass hashes walk every field); techniques compared by identity
+        techs, ft = workload.techniques, fast[2]
+        if techs is ft or (len(techs) == len(ft) and all(a is b for a, b in zip(techs, ft))):
+            return fast[3]
     techniques = tuple(workload.techniques)
     try:
-        key = (job, workload.cluster, techniques)
+        key = (job, cluster, techniques)
         hit = _ONE_NODE_MEMO.get(key)
     except TypeError:                   # unhashable inputs: compute every time
         key, hit = None, None
@@ -281,6 +290,12 @@ def _one_node_options(job, workload):
             if len(_ONE_NODE_MEMO) > 1 << 16:
                 _ONE_NODE_MEMO.clear()
             _ONE_NODE_MEMO[key] = hit
+    if key is not None:
+        if len(_ONE_NODE_FAST) > 1 << 16:
+            _ONE_NODE_FAST.clear()
+        techs = workload.techniques
+        _ONE_NODE_FAST[(id(job), id(cluster))] = (job, cluster, techs if isinstance(techs, tuple) else techniques,
+                                                  hit)                    # strong refs: ids stay unique
     return hit
 
 
@@ -301,7 +316,56 @@ def _dominance_prune_arrays(g: np.ndarray, cost: np.ndarray) -> list:
     return kept
 
 
-def _batch_rows(pool, workload, remaining, get, opts, prune: bool, err):
+_TABLE_VIEWS: dict = {}      # id(entries dict) -> _TableView (a few tables at a time)
+
+
+class _TableView:
+    """A profile table's `entries` dict as arrays: its keys (insertion order), its latencies,
+    and per requested key sequence the positions of those keys.  The view is reused only while
+    the dict provably has the same content -- the same key objects in the same order (a list
+    comparison that short-circuits on identity) and bit-equal latencies (one pass over the
+    values) -- so a mutated table is re-read, never served stale.  Cheaper than one hashed
+    lookup per (job, config) key (config 5: 11 008 lookups, ~1.2 ms) once the key positions
+    of a workload are known."""
+
+    __slots__ = ("entries", "keys", "vals", "lat", "index", "pos")
+
+    def __init__(self, entries, keys, vals):
+        self.entries, self.keys, self.vals = entries, keys, vals
+        self.lat = np.array(vals, dtype=np.float64)
+        self.index = None
+        self.pos = {}
+
+    @staticmethod
+    def of(entries) -> "_TableView":
+        # content check on the Python objects themselves: list equality short-circuits on
+        # identity, so an unchanged dict costs two list copies (a changed value or key fails
+        # the check and rebuilds the view)
+        keys, vals = list(entries), list(entries.values())
+        v = _TABLE_VIEWS.get(id(entries))
+        if v is not None and v.entries is entries and v.keys == keys and v.vals == vals:
+            return v
+        if len(_TABLE_VIEWS) >= 8:
+            _TABLE_VIEWS.clear()
+        v = _TABLE_VIEWS[id(entries)] = _TableView(entries, keys, vals)
+        return v
+
+    def latencies(self, key_rows, total: int) -> np.ndarray:
+        """Latency of every key of the concatenated `key_rows` (tuples of keys; INFEASIBLE when
+        absent), i.e. the same array as one `entries.get(key, INFEASIBLE)` per key."""
+        sig = tuple(map(id, key_rows))
+        hit = self.pos.get(sig)
+        if hit is None or len(hit[0]) != len(key_rows) or any(a is not b for a, b in zip(hit[0], key_rows)):
+            if self.index is None:
+                self.index = {k: i for i, k in enumerate(self.keys)}
+            pos = np.fromiter(map(self.index.get, chain.from_iterable(key_rows), repeat(-1)), dtype=np.int64,
+                              count=total)
+            hit = self.pos[sig] = (tuple(key_rows), pos)      # the rows themselves: ids stay unique
+        pos = hit[1]
+        return np.where(pos >= 0, self.lat[pos], INFEASIBLE)
+
+
+def _batch_rows(pool, workload, remaining, get, opts, prune: bool, err, entries=None):
     """The marshalling of every job at once when no job has a running configuration: the same
     arrays as the per-job rows in `build_problem`, built with one profile-table pass and
     whole-problem numpy ops instead of per-job / per-option Python (config 5: 64 jobs x 172
@@ -317,8 +381,11 @@ def _batch_rows(pool, workload, remaining, get, opts, prune: bool, err):
     J = len(pool)
     counts = np.fromiter((len(p[1]) for p in per), dtype=np.int64, count=J)
     total = int(counts.sum())
-    lat_all = np.fromiter(map(get, chain.from_iterable(p[1] for p in per), repeat(INFEASIBLE)),
-                          dtype=np.float64, count=total)
+    if isinstance(entries, dict) and type(entries) is dict:
+        lat_all = _TableView.of(entries).latencies([p[1] for p in per], total)
+    else:
+        lat_all = np.fromiter(map(get, chain.from_iterable(p[1] for p in per), repeat(INFEASIBLE)),
+                              dtype=np.float64, count=total)
     job_all = np.repeat(np.arange(J), counts)
     finite = np.isfinite(lat_all)
     nfin = np.bincount(job_all[finite], minlength=J)
@@ -353,9 +420,15 @@ def _batch_rows(pool, workload, remaining, get, opts, prune: bool, err):
     if prune:
         cost = np.ceil(t / delta) if grid else t
         # one stable argsort of an exact integer key (job, g, cost rank): within a (job, g)
-        # group the cheapest option first, the earliest of equal costs first
-        _, crank = np.unique(cost, return_inverse=True)
-        U = int(crank.max()) + 1
+        # group the cheapest option first, the earliest of equal costs first.  Grid costs are
+        # small integers already (any order-preserving rank serves); float costs are ranked.
+        cmax = float(cost.max()) if len(cost) else 0.0
+        if grid and cmax < (1 << 24):
+            crank = cost.astype(np.int64)
+            U = int(cmax) + 1
+        else:
+            _, crank = np.unique(cost, return_inverse=True)
+            U = int(crank.max()) + 1
         jg = job.astype(np.int64) * 64 + g
         order = np.argsort(jg * U + crank, kind="stable")
         jgo = jg[order]
@@ -438,7 +511,7 @@ def build_problem(table, workload, opts: SolveOptions | None = None, running_con
         raise err.InvariantViolation("prune", "the dominance prune is exact only on one node")
     if _BATCH_ROWS and pool and techniques is workload.techniques and not any(j.id in current for j in pool):
         options, option_src, radix, gpus, mask, runtime, dur, delta = _batch_rows(
-            pool, workload, remaining, table.entries.get, opts, prune, err)
+            pool, workload, remaining, table.entries.get, opts, prune, err, entries=table.entries)
         return _search_problem(pool, nodes, G, W, options, option_src, radix, gpus, mask, runtime, dur,
                                opts, delta, prune, running_context)
 

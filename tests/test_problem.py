@@ -357,3 +357,36 @@ def test_batch_marshalling_equals_per_job_rows(mode, monkeypatch):
             cases.append((t, w, D.RunningContext(remaining=rem, current={}, checkpoint_cost=30.0), {}))
     for t, w, ctx, kw in cases:
         same(build(True, t, w, ctx, **kw), build(False, t, w, ctx, **kw))
+
+
+def test_table_view_never_serves_a_mutated_table():
+    """The array view of a profile table's entries (`_TableView`) is reused across solves only
+    while the dict's keys and latencies are provably unchanged: changing a latency, replacing
+    a key makes the next marshalling re-read the table (same arrays as a fresh copy of the
+    dict)."""
+    import copy
+
+    from paper_2311_02840_b200 import problem as P
+    from paper_2311_02840_b200.workloads import config_workload
+
+    w, t, _ = config_workload(4)
+
+    def arrays(tab):
+        p = build_problem(tab, w)
+        return p.radix.tobytes(), p.dur_i32.tobytes(), p.runtime.tobytes(), p.delta
+
+    base = arrays(t)
+    assert arrays(t) == base and id(t.entries) in P._TABLE_VIEWS
+    keys = [k for k, v in t.entries.items() if np.isfinite(v)]
+    k0, k1 = keys[3], keys[-1]
+    t.entries[k0] = t.entries[k0] * 0.5                          # a value change
+    fresh = copy.copy(t)
+    fresh.entries = dict(t.entries)
+    assert arrays(t) == arrays(fresh) != base
+    v1 = t.entries.pop(k1)                                       # delete + re-insert a key (order moves)
+    t.entries[k1] = v1 * 3.0
+    fresh.entries = dict(t.entries)
+    assert arrays(t) == arrays(fresh)
+    t.entries[k0] = 0.25                                         # a new float object, a new value
+    v = P._TableView.of(t.entries)
+    assert v.lat[v.keys.index(k0)] == 0.25 and P._TableView.of(t.entries) is v
