@@ -415,6 +415,10 @@ def _best_runtime_all(prob: SearchProblem, jobs=None) -> list:
     (earliest option on ties); runtime on the job's fastest eligible node.  One array pass
     over the problem's [J, Cmax, N] tables (or the rows of ``jobs``), then a short loop per job
     over its options."""
+    if jobs is None:            # whole problem: computed once per problem (arrays are final)
+        hit = prob.extra.get("_best_runtime_all")
+        if hit is not None:
+            return [dict(d) for d in hit]
     sel = slice(None) if jobs is None else list(jobs)
     N = prob.N
     elig = ((prob.node_mask[sel, :, None] >> np.arange(N, dtype=np.uint32)) & 1).astype(bool)
@@ -430,6 +434,8 @@ def _best_runtime_all(prob: SearchProblem, jobs=None) -> list:
             if g not in out or r < out[g][0]:
                 out[g] = (r, o)
         out_all.append(out)
+    if jobs is None:
+        prob.extra["_best_runtime_all"] = [dict(d) for d in out_all]
     return out_all
 
 
