@@ -109,6 +109,63 @@ struct RecCol {
 #ifndef SAT_LS_CUT_REG
 #define SAT_LS_CUT_REG 0 // the same exits in the register-shift evaluation (schedule_eval16)
 #endif
+// Multi16 placement loop (schedule_records, several nodes, 16-bit slots): NN = the node count
+// when every node slot of the layout is used (compile-time loops), 0 = runtime N; REL = the
+// problem has release times.
+template <typename T, int G, int NN, bool REL, typename RecF>
+__device__ __forceinline__ T m16_walk(const SchedCtx<T> &c, const RecF rec, int k0, T mx, uint32_t *cout, bool wr) {
+    constexpr int NMAX = 32 / G;
+    uint32_t *st16 = c.st16;
+    const int J = c.J, N = NN > 0 ? NN : c.N;
+    const bool rec_d = c.rec_d;
+    (void)rec_d;
+    const int SW = N * (G / 2), CW = SW + 1;
+    (void)CW;
+        for (int kk = k0; kk < J; ++kk) {
+            const uint32_t r = rec(kk);
+            const int g = (int)(r & 63u) + 1;
+            SAT_ASSERT(g >= 1 && g <= G && (int)((r >> 6) & 63u) < J);
+            SAT_ASSERT(rec_d || (int)(r >> 12) < c.n_opt);
+            const int gm = g - 1;
+            const int32_t rel = REL ? (int32_t)c.release[(r >> 6) & 63u] : 0;
+            const uint32_t selt = 0x4410u + (uint32_t)(gm & 1) * 0x22u;
+            uint32_t kb = 0xffffffffu;
+#pragma unroll
+            for (int n = 0; n < NMAX; ++n) {
+                if (NN > 0 || n < N) {
+                    int32_t t = (int32_t)__byte_perm(st16[(n * G + (gm >> 1)) * 32], 0u, selt);
+                    if (REL) t = max(t, rel);
+                    kb = min(kb, (uint32_t)t * 32u + (uint32_t)n);
+                }
+            }
+            const int bn = (int)(kb & 31u);
+            SAT_ASSERT(bn < N);
+            const int32_t e = (int32_t)(kb >> 5) + (int32_t)(r >> 12);
+            const uint32_t e2 = (uint32_t)e * 0x10001u;
+            const uint32_t sel = (g & 1) ? 0x5432u : 0x3210u;
+            uint32_t *nb = st16 + bn * G * 32;
+            const uint32_t *src = nb + (g >> 1) * 32;
+            uint32_t w[G / 2 + 1], cur[G / 2];
+#pragma unroll
+            for (int k = 0; k <= G / 2; ++k) w[k] = src[k * 32];
+#pragma unroll
+            for (int k = 0; k < G / 2; ++k) cur[k] = nb[k * 32];
+#pragma unroll
+            for (int k = 0; k < G / 2; ++k)
+                nb[k * 32] = __vmaxu2(cur[k], __vminu2(__byte_perm(w[k], w[k + 1], sel), e2));
+            mx = tmax(mx, (T)e);
+            if (wr) {
+#pragma unroll
+                for (int n = 0; n < NMAX; ++n)
+                    if (NN > 0 || n < N)
+#pragma unroll
+                        for (int q = 0; q < G / 2; ++q) cout[(kk + 1) * CW + n * (G / 2) + q] = st16[(n * G + q) * 32];
+                cout[(kk + 1) * CW + SW] = (uint32_t)(int32_t)mx;
+            }
+        }
+    return mx;
+}
+
 template <typename T, int G, int L, bool LOAD = false, typename RecF = RecCol, bool CUT = false>
 __device__ __forceinline__ T schedule_records(const SchedCtx<T> &c, const RecF rec,
                                              uint64_t *load = nullptr, int k0 = 0,
@@ -267,47 +324,14 @@ __device__ __forceinline__ T schedule_records(const SchedCtx<T> &c, const RecF r
                     if (wr) cout[k0 * CW + n * (G / 2) + w] = v;
                 }
         if (wr) cout[k0 * CW + SW] = (uint32_t)(int32_t)mx;
-        for (int kk = k0; kk < J; ++kk) {
-            const uint32_t r = rec(kk);
-            const int g = (int)(r & 63u) + 1;
-            SAT_ASSERT(g >= 1 && g <= G && (int)((r >> 6) & 63u) < J);
-            SAT_ASSERT(rec_d || (int)(r >> 12) < c.n_opt);
-            const int gm = g - 1;
-            const int32_t rel = has_release ? (int32_t)release[(r >> 6) & 63u] : 0;
-            const uint32_t selt = 0x4410u + (uint32_t)(gm & 1) * 0x22u;
-            uint32_t kb = 0xffffffffu;
-#pragma unroll
-            for (int n = 0; n < NMAX; ++n) {
-                if (n < N) {
-                    int32_t t = (int32_t)__byte_perm(st16[(n * G + (gm >> 1)) * 32], 0u, selt);
-                    t = max(t, rel);
-                    kb = min(kb, (uint32_t)t * 32u + (uint32_t)n);
-                }
-            }
-            const int bn = (int)(kb & 31u);
-            SAT_ASSERT(bn < N);
-            const int32_t e = (int32_t)(kb >> 5) + (int32_t)(r >> 12);
-            const uint32_t e2 = (uint32_t)e * 0x10001u;
-            const uint32_t sel = (g & 1) ? 0x5432u : 0x3210u;
-            uint32_t *nb = st16 + bn * G * 32;
-            const uint32_t *src = nb + (g >> 1) * 32;
-            uint32_t w[G / 2 + 1], cur[G / 2];
-#pragma unroll
-            for (int k = 0; k <= G / 2; ++k) w[k] = src[k * 32];
-#pragma unroll
-            for (int k = 0; k < G / 2; ++k) cur[k] = nb[k * 32];
-#pragma unroll
-            for (int k = 0; k < G / 2; ++k)
-                nb[k * 32] = __vmaxu2(cur[k], __vminu2(__byte_perm(w[k], w[k + 1], sel), e2));
-            mx = tmax(mx, (T)e);
-            if (wr) {
-#pragma unroll
-                for (int n = 0; n < NMAX; ++n)
-                    if (n < N)
-#pragma unroll
-                        for (int q = 0; q < G / 2; ++q) cout[(kk + 1) * CW + n * (G / 2) + q] = st16[(n * G + q) * 32];
-                cout[(kk + 1) * CW + SW] = (uint32_t)(int32_t)mx;
-            }
+        // the placement loop specialised on (every node slot used, release times present):
+        // no per-node predicates and no release max on the common sampled / local-search path
+        if (N == NMAX) {
+            mx = has_release ? m16_walk<T, G, NMAX, true>(c, rec, k0, mx, cout, wr)
+                             : m16_walk<T, G, NMAX, false>(c, rec, k0, mx, cout, wr);
+        } else {
+            mx = has_release ? m16_walk<T, G, 0, true>(c, rec, k0, mx, cout, wr)
+                             : m16_walk<T, G, 0, false>(c, rec, k0, mx, cout, wr);
         }
         if constexpr (LOAD) {
             uint64_t sum = 0;
