@@ -582,7 +582,7 @@ class Engine:
                 # the bound-and-prune key holds (makespan <= seed bound) << idx_bits | index:
                 # leave at least 7 bits for the makespan (grids of <= 127 intervals)
                 exact = (space - 1).bit_length() <= 56
-            # otherwise local search from sampled starts (grid time), else plain sampling
+            # otherwise local search from greedy starts (grid time), else plain sampling
             mode = "exhaustive" if exact else ("local" if prob.time_mode == TIME_GRID and prob.J >= 2 else "sampled")
         if mode == "exhaustive":
             if space > (1 << 62):
