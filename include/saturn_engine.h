@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define SAT_ABI_VERSION 7
+#define SAT_ABI_VERSION 8
 
 /* status codes (mapped to reference errors.py classes by the host layer) */
 #define SAT_OK              0
@@ -221,6 +221,18 @@ typedef struct sat_dp_info {
 int sat_dp_workspace_bytes(const sat_problem_t *p, int32_t target, uint64_t max_states, size_t *bytes);
 int sat_search_dp(const sat_problem_t *p, int32_t target, uint64_t max_states, uint8_t *h_candidate,
                   sat_dp_info_t *info, void *d_ws, size_t ws_bytes, void *stream);
+/* ABI v8: the same with flags.  SAT_DP_EXACT on several nodes: labelled states (no canonical
+ * node order) expanded by the list scheduler's own node choice (earliest end over every eligible
+ * node, lowest label on ties; a child is cut when that node cannot reach the target), so the
+ * levels hold exactly the candidates' states: INFEASIBLE is a proof as before, and FEASIBLE now
+ * returns a candidate (rebuilt backwards like the one-node search: smallest labelled key, lowest
+ * options).  More states than the prover where nodes are interchangeable.  One node: flags
+ * change nothing (the one-node search is exact already). */
+#define SAT_DP_EXACT 1
+int sat_dp_workspace_bytes_ex(const sat_problem_t *p, int32_t target, uint64_t max_states, int32_t flags,
+                              size_t *bytes);
+int sat_search_dp_ex(const sat_problem_t *p, int32_t target, uint64_t max_states, int32_t flags,
+                     uint8_t *h_candidate, sat_dp_info_t *info, void *d_ws, size_t ws_bytes, void *stream);
 
 /* Cross-rank shared incumbent (ABI v4).  With several ranks (one process per GPU), every rank's
  * search kernels can atomicMin into -- and prune against -- ONE sat_best_t cell in the owner

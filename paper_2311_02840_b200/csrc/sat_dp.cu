@@ -493,6 +493,9 @@ struct DpWideParams {
     int32_t ubase[kDpMaxJ], ucnt[kDpMaxJ], release[kDpMaxJ], minarea[kDpMaxJ];
     int32_t Kb;                             // binomial table row width (max G_n + 1)
     int32_t nrem;                           // jobs still to place in the level being expanded
+    int32_t exact;                          // 1: labelled nodes, the list scheduler's own node choice
+    const uint8_t *ue;                      // [n_usable] every node the option is eligible on (exact)
+    const int16_t *uf;                      // [n_usable][N] its duration there (exact)
     const uint64_t *binom;                  // [(T + maxG + 1)][Kb]
     const uint8_t *ug;                      // [n_usable] gang size
     const uint8_t *um;                      // [n_usable] node eligibility bits
@@ -509,6 +512,12 @@ struct DpWideParams {
     uint64_t out_cap;
     unsigned long long *count;
     unsigned int *overflow;
+    // exact mode, candidate rebuild (k_dpw_pick_state)
+    uint64_t child_R;
+    uint16_t child_A[kDpWideSlots];
+    unsigned long long *pick_hi, *pick_lo;
+    uint64_t *pick_R;
+    uint16_t *pick_A;
 };
 
 __device__ __forceinline__ unsigned __int128 cas128(unsigned __int128 *addr, unsigned __int128 cmp,
@@ -566,6 +575,55 @@ __device__ __forceinline__ bool dpw_viable(const DpWideParams &p, uint64_t R2, c
     return area <= (int64_t)p.T * p.Gtot;
 }
 
+// exact mode: node the list scheduler gives usable option q of job j from state a (earliest end
+// over every eligible node, lowest label on ties; -1: none)
+__device__ __forceinline__ int dpw_pick(const DpWideParams &p, const int32_t *a, int q, int j) {
+    const int g = p.ug[q];
+    const uint32_t em = p.ue[q];
+    int32_t best = 0x7fffffff;
+    int bn = -1;
+    for (int n = 0; n < p.N; ++n) {
+        if (!((em >> n) & 1u) || g > p.node_g[n]) continue;
+        const int32_t e = max(a[p.node_off[n] + g - 1], p.release[j]) + (int32_t)p.uf[q * p.N + n];
+        if (e < best) { best = e; bn = n; }
+    }
+    return bn;
+}
+
+// the state after placing usable option q of job j on node n (exact-mode durations); returns the end
+__device__ __forceinline__ int32_t dpw_place(const DpWideParams &p, const int32_t *a, int q, int j, int n,
+                                             int32_t *b) {
+    const int g = p.ug[q];
+    for (int i = 0; i < p.Gtot; ++i) b[i] = a[i];
+    const int32_t *an = a + p.node_off[n];
+    int32_t *bn = b + p.node_off[n];
+    const int G = p.node_g[n];
+    const int32_t e = max(an[g - 1], p.release[j]) + (int32_t)p.uf[q * p.N + n];
+    for (int i = 0; i < G; ++i) bn[i] = max(an[i], min(i + g < G ? an[i + g] : 0x7fffffff, e));
+    return e;
+}
+
+// claim the state's key in the hash set and append it to the level; false = out of budget
+__device__ __forceinline__ bool dpw_insert(const DpWideParams &p, uint64_t R2, int32_t *b) {
+    const unsigned __int128 key = dpw_key(p, R2, b);
+    const uint64_t hh = ((uint64_t)key ^ (uint64_t)(key >> 64) * 0xBF58476D1CE4E5B9ull) * kGolden;
+    uint64_t h = hh >> (64 - p.cap_log2);
+    const unsigned __int128 EMPTY = ~(unsigned __int128)0;
+    for (int probe = 0;; ++probe) {
+        if (probe > p.max_probe) { atomicOr(p.overflow, 1u); return false; }
+        const unsigned __int128 old = cas128(&p.table[h], EMPTY, key);
+        if (old == EMPTY) {
+            const unsigned long long idx = atomicAdd(p.count, 1ull);
+            if (idx >= p.out_cap) { atomicOr(p.overflow, 1u); return false; }
+            p.out_R[idx] = R2;
+            for (int i = 0; i < p.Gtot; ++i) p.out_A[idx * p.Gtot + i] = (uint16_t)b[i];
+            return true;
+        }
+        if (old == key) return true;
+        h = (h + 1) & p.cap_mask;
+    }
+}
+
 __global__ void __launch_bounds__(kDpThreads) k_dp_expand_wide(const __grid_constant__ DpWideParams p) {
     const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (tid >= p.n_in * (uint64_t)p.nrem) return;
@@ -582,6 +640,16 @@ __global__ void __launch_bounds__(kDpThreads) k_dp_expand_wide(const __grid_cons
     for (int q = p.ubase[j]; q < p.ubase[j] + p.ucnt[j]; ++q) {
         const int g = p.ug[q];
         const uint32_t mask = p.um[q];
+        if (p.exact) {
+            // the list scheduler's node: earliest end over EVERY eligible node, lowest label on
+            // ties; a node outside the usable set there means the candidate cannot reach T
+            const int bn = dpw_pick(p, a, q, j);
+            if (bn < 0 || !((mask >> bn) & 1u)) continue;
+            const int32_t e = dpw_place(p, a, q, j, bn, b);
+            if (e > p.T || !dpw_viable(p, R2, b)) continue;
+            if (!dpw_insert(p, R2, b)) return;
+            continue;
+        }
         int32_t best = 0x7fffffff;
         for (int n = 0; n < p.N; ++n)
             if ((mask >> n) & 1u && g <= p.node_g[n])
@@ -596,31 +664,59 @@ __global__ void __launch_bounds__(kDpThreads) k_dp_expand_wide(const __grid_cons
             const int G = p.node_g[n];
             for (int i = 0; i < G; ++i) bn[i] = max(an[i], min(i + g < G ? an[i + g] : 0x7fffffff, best));
             if (!dpw_viable(p, R2, b)) continue;
-            const unsigned __int128 key = dpw_key(p, R2, b);
-            const uint64_t hh = ((uint64_t)key ^ (uint64_t)(key >> 64) * 0xBF58476D1CE4E5B9ull) * kGolden;
-            uint64_t h = hh >> (64 - p.cap_log2);
-            const unsigned __int128 EMPTY = ~(unsigned __int128)0;
-            for (int probe = 0;; ++probe) {
-                if (probe > p.max_probe) { atomicOr(p.overflow, 1u); return; }
-                const unsigned __int128 old = cas128(&p.table[h], EMPTY, key);
-                if (old == EMPTY) {
-                    const unsigned long long idx = atomicAdd(p.count, 1ull);
-                    if (idx >= p.out_cap) { atomicOr(p.overflow, 1u); return; }
-                    p.out_R[idx] = R2;
-                    for (int i = 0; i < p.Gtot; ++i) p.out_A[idx * p.Gtot + i] = (uint16_t)b[i];
-                    break;
-                }
-                if (old == key) break;
-                h = (h + 1) & p.cap_mask;
-            }
+            if (!dpw_insert(p, R2, b)) return;
         }
+    }
+}
+
+// Exact mode, backwards: the final state (mode 0: every state of the level) or the parents of
+// (child_R, child_A) (mode 1: states of the previous level with a job j and a usable option whose
+// exact placement gives the child) -- phase 0: min of the high key words, phase 1: min of the low
+// words among those, phase 2: the state holding (min_hi, min_lo) writes itself out.  Keys are the
+// labelled (uncanonicalised) exact keys, so the choice is deterministic.
+__global__ void __launch_bounds__(kDpThreads) k_dpw_pick_state(const __grid_constant__ DpWideParams p, int mode,
+                                                                 int phase) {
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int nrem = mode == 0 ? 1 : p.nrem;
+    if (tid >= p.n_in * (uint64_t)nrem) return;
+    const uint64_t s = tid / (uint64_t)nrem;
+    const uint64_t R = p.in_R[s];
+    int32_t a[kDpWideSlots], b[kDpWideSlots];
+    for (int i = 0; i < p.Gtot; ++i) a[i] = p.in_A[s * p.Gtot + i];
+    if (mode == 1) {
+        const int kk = (int)(tid - s * (uint64_t)nrem);
+        const uint32_t Rlo = (uint32_t)R, Rhi = (uint32_t)(R >> 32);
+        const int nlo = __popc(Rlo);
+        const int j = kk < nlo ? (int)__fns(Rlo, 0, kk + 1) : 32 + (int)__fns(Rhi, 0, kk - nlo + 1);
+        if ((R & ~(1ull << j)) != p.child_R) return;
+        bool hit = false;
+        for (int q = p.ubase[j]; q < p.ubase[j] + p.ucnt[j] && !hit; ++q) {
+            const int bn = dpw_pick(p, a, q, j);
+            if (bn < 0 || !((p.um[q] >> bn) & 1u)) continue;
+            dpw_place(p, a, q, j, bn, b);
+            bool eq = true;
+            for (int i = 0; i < p.Gtot; ++i) eq &= b[i] == (int32_t)p.child_A[i];
+            hit = eq;
+        }
+        if (!hit) return;
+    }
+    const unsigned __int128 key = dpw_key(p, R, a);      // exact mode: no canonical permutation
+    const unsigned long long hi = (unsigned long long)(uint64_t)(key >> 64), lo = (unsigned long long)(uint64_t)key;
+    if (phase == 0) {
+        atomicMin(p.pick_hi, hi);
+    } else if (phase == 1) {
+        if (hi == *p.pick_hi) atomicMin(p.pick_lo, lo);
+    } else if (hi == *p.pick_hi && lo == *p.pick_lo) {
+        *p.pick_R = R;                                   // (equal states write equal values)
+        for (int i = 0; i < p.Gtot; ++i) p.pick_A[i] = (uint16_t)a[i];
     }
 }
 
 struct DpWidePlan {
     DpWideParams p{};
-    std::vector<uint8_t> ug, um;
-    std::vector<int16_t> ud, dg;
+    std::vector<uint8_t> ug, um, ue;
+    std::vector<int16_t> ud, dg, uf;
+    std::vector<int> uorig, ujob;           // original option digit / job of each usable option
     std::vector<uint64_t> binom;
     std::vector<uint16_t> a0;
     int status = -1;
@@ -628,13 +724,14 @@ struct DpWidePlan {
     uint64_t cap = 0;
 };
 
-static int dpw_prepare(const sat_problem_t *pr, int32_t T, uint64_t max_states, DpWidePlan &d) {
+static int dpw_prepare(const sat_problem_t *pr, int32_t T, uint64_t max_states, DpWidePlan &d, bool exact = false) {
     if (pr->time_mode != SAT_TIME_GRID_I32) return SAT_ERR_UNSUPPORTED;
     if (pr->J > kDpMaxJ || max_states < 1) return SAT_ERR_INVALID;
     const int J = pr->J, N = pr->N;
     if (N > kDpWideMaxN || T < 0 || T > 30000) return SAT_ERR_UNSUPPORTED;
     DpWideParams &p = d.p;
     p.J = J; p.N = N; p.T = T;
+    p.exact = exact ? 1 : 0;
     int off = 0, gmax = 1;
     for (int n = 0; n < N; ++n) {
         p.node_off[n] = off;
@@ -694,6 +791,14 @@ static int dpw_prepare(const sat_problem_t *pr, int32_t T, uint64_t max_states, 
             if (!m) continue;
             d.ug.push_back((uint8_t)g);
             d.um.push_back(m);
+            d.uorig.push_back(o);
+            d.ujob.push_back(j);
+            uint8_t em = 0;                       // exact mode: every eligible node and its duration
+            for (int n = 0; n < N; ++n) {
+                if (elig(j, o, n)) em |= (uint8_t)(1u << n);
+                d.uf.push_back((int16_t)(elig(j, o, n) ? std::min<int32_t>(dur(j, o, n), 0x7fff) : 0x7fff));
+            }
+            d.ue.push_back(em);
             for (int n = 0; n < N; ++n) {
                 const int32_t dd = ((m >> n) & 1u) ? dur(j, o, n) : T + 1;
                 d.ud.push_back((int16_t)dd);
@@ -710,6 +815,7 @@ static int dpw_prepare(const sat_problem_t *pr, int32_t T, uint64_t max_states, 
     // and duration
     for (int n = 0; n < N; ++n) {
         p.node_grp[n] = n;
+        if (exact) continue;                  // exact mode keeps node labels (no canonical order)
         for (int m = 0; m < n; ++m) {
             if (p.node_grp[m] != m || p.node_g[m] != p.node_g[n]) continue;
             bool same = true;
@@ -725,8 +831,8 @@ static int dpw_prepare(const sat_problem_t *pr, int32_t T, uint64_t max_states, 
     std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return p.node_grp[x] < p.node_grp[y]; });
     {
         DpWideParams p2 = p;
-        std::vector<uint8_t> um2(d.um.size());
-        std::vector<int16_t> ud2(d.ud.size()), dg2(d.dg.size());
+        std::vector<uint8_t> um2(d.um.size()), ue2(d.ue.size());
+        std::vector<int16_t> ud2(d.ud.size()), dg2(d.dg.size()), uf2(d.uf.size());
         std::vector<uint16_t> a02(off);
         int o2 = 0;
         for (int k = 0; k < N; ++k) {
@@ -738,17 +844,20 @@ static int dpw_prepare(const sat_problem_t *pr, int32_t T, uint64_t max_states, 
             o2 += p.node_g[n];
         }
         for (size_t qq = 0; qq < d.um.size(); ++qq) {
-            uint8_t m2 = 0;
+            uint8_t m2 = 0, e2 = 0;
             for (int k = 0; k < N; ++k) {
                 if ((d.um[qq] >> ord[k]) & 1u) m2 |= (uint8_t)(1u << k);
+                if ((d.ue[qq] >> ord[k]) & 1u) e2 |= (uint8_t)(1u << k);
                 ud2[qq * N + k] = d.ud[qq * N + ord[k]];
+                uf2[qq * N + k] = d.uf[qq * N + ord[k]];
             }
             um2[qq] = m2;
+            ue2[qq] = e2;
         }
         for (int j = 0; j < J; ++j)
             for (int k = 0; k < N; ++k)
                 for (int g = 0; g < 32; ++g) dg2[((size_t)j * N + k) * 32 + g] = d.dg[((size_t)j * N + ord[k]) * 32 + g];
-        p = p2; d.um = um2; d.ud = ud2; d.dg = dg2; d.a0 = a02;
+        p = p2; d.um = um2; d.ud = ud2; d.dg = dg2; d.a0 = a02; d.ue = ue2; d.uf = uf2;
     }
     // key width: 2^J x prod C(T + G_n, G_n) < 2^127
     const int n_max = T + gmax;
@@ -778,7 +887,7 @@ static int dpw_prepare(const sat_problem_t *pr, int32_t T, uint64_t max_states, 
     p.max_probe = 1 << 14;
     d.binom_bytes = align256(d.binom.size() * sizeof(uint64_t));
     d.aux_bytes = align256(d.ug.size() + 16) + align256(d.um.size() + 16) + align256(d.ud.size() * 2 + 16) +
-                  align256(d.dg.size() * 2);
+                  align256(d.dg.size() * 2) + align256(d.ue.size() + 16) + align256(d.uf.size() * 2 + 16);
     d.table_bytes = align256(cap * 16);
     d.R_bytes = align256(max_states * sizeof(uint64_t));
     d.A_bytes = align256(max_states * off * sizeof(uint16_t));
@@ -790,7 +899,7 @@ static size_t dpw_ws_bytes(const DpWidePlan &d) {
 }
 
 static int dpw_run(const sat_problem_t *pr, uint64_t max_states, sat_dp_info_t *info, void *d_ws, size_t ws_bytes,
-                   cudaStream_t s, DpWidePlan &d) {
+                   cudaStream_t s, DpWidePlan &d, uint8_t *h_candidate = nullptr) {
     if (!d_ws || ws_bytes < dpw_ws_bytes(d)) return SAT_ERR_INVALID;
     DpWideParams &p = d.p;
     uint8_t *ws = static_cast<uint8_t *>(d_ws);
@@ -801,6 +910,8 @@ static int dpw_run(const sat_problem_t *pr, uint64_t max_states, sat_dp_info_t *
     uint8_t *um = take(align256(d.um.size() + 16));
     int16_t *ud = reinterpret_cast<int16_t *>(take(align256(d.ud.size() * 2 + 16)));
     int16_t *dg = reinterpret_cast<int16_t *>(take(align256(d.dg.size() * 2)));
+    uint8_t *ue = take(align256(d.ue.size() + 16));
+    int16_t *uf = reinterpret_cast<int16_t *>(take(align256(d.uf.size() * 2 + 16)));
     auto *table = reinterpret_cast<unsigned __int128 *>(take(d.table_bytes));
     uint64_t *Rs = reinterpret_cast<uint64_t *>(take(d.R_bytes));
     uint16_t *As = reinterpret_cast<uint16_t *>(take(d.A_bytes));
@@ -811,6 +922,8 @@ static int dpw_run(const sat_problem_t *pr, uint64_t max_states, sat_dp_info_t *
         (d.um.size() && cudaMemcpyAsync(um, d.um.data(), d.um.size(), cudaMemcpyHostToDevice, s)) ||
         (d.ud.size() && cudaMemcpyAsync(ud, d.ud.data(), d.ud.size() * 2, cudaMemcpyHostToDevice, s)) ||
         cudaMemcpyAsync(dg, d.dg.data(), d.dg.size() * 2, cudaMemcpyHostToDevice, s) ||
+        (d.ue.size() && cudaMemcpyAsync(ue, d.ue.data(), d.ue.size(), cudaMemcpyHostToDevice, s)) ||
+        (d.uf.size() && cudaMemcpyAsync(uf, d.uf.data(), d.uf.size() * 2, cudaMemcpyHostToDevice, s)) ||
         cudaMemsetAsync(table, 0xFF, d.cap * 16, s) || cudaMemsetAsync(ctr, 0, 256, s))
         return SAT_ERR_CUDA;
     const uint64_t full = J == 64 ? ~0ull : ((1ull << J) - 1ull);
@@ -818,8 +931,15 @@ static int dpw_run(const sat_problem_t *pr, uint64_t max_states, sat_dp_info_t *
         cudaMemcpyAsync(As, d.a0.data(), Gt * 2, cudaMemcpyHostToDevice, s))
         return SAT_ERR_CUDA;
     p.binom = binom; p.ug = ug; p.um = um; p.ud = ud; p.dg = dg; p.table = table;
+    p.ue = ue; p.uf = uf;
     p.count = ctr;
     p.overflow = reinterpret_cast<unsigned int *>(ctr + 1);
+    p.pick_hi = ctr + 2;
+    p.pick_lo = ctr + 3;
+    p.pick_R = reinterpret_cast<uint64_t *>(ctr + 4);
+    p.pick_A = reinterpret_cast<uint16_t *>(ctr + 5);          // 32 x u16 = ctr[5..12]
+    std::vector<uint64_t> lv_base(J + 1, 0), lv_size(J + 1, 0);
+    lv_size[0] = 1;
     uint64_t base = 0, size = 1, total = 1, widest = 1;
     int level = 0;
     for (; level < J; ++level) {
@@ -841,6 +961,8 @@ static int dpw_run(const sat_problem_t *pr, uint64_t max_states, sat_dp_info_t *
             return SAT_OK;
         }
         base = nb; size = got[0];
+        lv_base[level + 1] = base;
+        lv_size[level + 1] = size;
         total += size;
         widest = std::max(widest, size);
         if (size == 0) { ++level; break; }
@@ -848,6 +970,71 @@ static int dpw_run(const sat_problem_t *pr, uint64_t max_states, sat_dp_info_t *
     info->levels = level; info->states = total; info->widest_level = widest;
     info->status = (level < J || size == 0) ? SAT_DP_INFEASIBLE : SAT_DP_FEASIBLE;
     info->makespan = -1;                      // the prover rebuilds no candidate
+    if (info->status != SAT_DP_FEASIBLE || !p.exact) return SAT_OK;
+    // exact mode: a candidate reaching T -- the smallest-key final state, then backwards the
+    // smallest-key parent and (on the host) its lowest usable option producing the child
+    const unsigned long long ones[2] = {~0ull, ~0ull};
+    auto pick = [&](int lv, int mode, uint64_t &R, std::vector<int32_t> &A) -> int {
+        p.in_R = Rs + lv_base[lv]; p.in_A = As + lv_base[lv] * Gt; p.n_in = lv_size[lv];
+        p.nrem = J - lv;
+        if (cudaMemcpyAsync(p.pick_hi, ones, sizeof(ones), cudaMemcpyHostToDevice, s)) return SAT_ERR_CUDA;
+        const uint64_t work = p.n_in * (uint64_t)(mode == 0 ? 1 : p.nrem);
+        const unsigned blocks = (unsigned)((work + kDpThreads - 1) / kDpThreads);
+        for (int ph = 0; ph < 3; ++ph) {
+            k_dpw_pick_state<<<blocks, kDpThreads, 0, s>>>(p, mode, ph);
+            if (cudaGetLastError() != cudaSuccess) return SAT_ERR_CUDA;
+        }
+        unsigned long long back[11];                    // hi, lo, R, A (64 bytes)
+        if (cudaMemcpyAsync(back, ctr + 2, sizeof(back), cudaMemcpyDeviceToHost, s) || cudaStreamSynchronize(s))
+            return SAT_ERR_CUDA;
+        if (back[0] == ~0ull && back[1] == ~0ull) return SAT_ERR_CUDA;   // nothing picked: cannot happen
+        R = back[2];
+        const uint16_t *a16 = reinterpret_cast<const uint16_t *>(back + 3);
+        A.assign(Gt, 0);
+        for (int i = 0; i < Gt; ++i) A[i] = a16[i];
+        return SAT_OK;
+    };
+    std::vector<int32_t> cur, par, tmp(Gt);
+    uint64_t curR = 0, parR = 0;
+    int st = pick(J, 0, curR, cur);
+    if (st) return st;
+    info->makespan = *std::max_element(cur.begin(), cur.end());
+    auto host_pick = [&](const std::vector<int32_t> &a, int q, int j) {
+        int32_t best = 0x7fffffff;
+        int bn = -1;
+        for (int n = 0; n < p.N; ++n) {
+            if (!((d.ue[q] >> n) & 1u) || d.ug[q] > p.node_g[n]) continue;
+            const int32_t e = std::max<int32_t>(a[p.node_off[n] + d.ug[q] - 1], p.release[j]) + d.uf[q * p.N + n];
+            if (e < best) { best = e; bn = n; }
+        }
+        return bn;
+    };
+    std::vector<int> order(J), opt(J);
+    for (int lv = J; lv >= 1; --lv) {
+        p.child_R = curR;
+        for (int i = 0; i < Gt; ++i) p.child_A[i] = (uint16_t)cur[i];
+        if ((st = pick(lv - 1, 1, parR, par))) return st;
+        const int j = __builtin_ctzll(parR ^ curR);
+        int found = -1;
+        for (int q = p.ubase[j]; q < p.ubase[j] + p.ucnt[j] && found < 0; ++q) {
+            const int bn = host_pick(par, q, j);
+            if (bn < 0 || !((d.um[q] >> bn) & 1u)) continue;
+            tmp = par;
+            const int g = d.ug[q], G = p.node_g[bn], off = p.node_off[bn];
+            const int32_t e = std::max<int32_t>(par[off + g - 1], p.release[j]) + d.uf[q * p.N + bn];
+            for (int i = 0; i < G; ++i) tmp[off + i] = std::max(par[off + i], std::min(i + g < G ? par[off + i + g] : 0x7fffffff, e));
+            if (tmp == cur) found = q;
+        }
+        if (found < 0) return SAT_ERR_CUDA;
+        order[lv - 1] = j;
+        opt[j] = d.uorig[found];
+        curR = parR;
+        cur = par;
+    }
+    if (h_candidate) {
+        for (int j = 0; j < J; ++j) h_candidate[j] = (uint8_t)opt[j];
+        for (int k = 0; k < J; ++k) h_candidate[J + k] = (uint8_t)order[k];
+    }
     return SAT_OK;
 }
 
@@ -857,8 +1044,9 @@ using namespace sat;
 
 extern "C" {
 
-int sat_dp_workspace_bytes(const sat_problem_t *p, int32_t target, uint64_t max_states, size_t *bytes) {
-    if (!bytes) return SAT_ERR_INVALID;
+int sat_dp_workspace_bytes_ex(const sat_problem_t *p, int32_t target, uint64_t max_states, int32_t flags,
+                              size_t *bytes) {
+    if (!bytes || (flags & ~SAT_DP_EXACT)) return SAT_ERR_INVALID;
     int st = validate(p);
     if (st) return st;
     DpPlan d;
@@ -869,15 +1057,24 @@ int sat_dp_workspace_bytes(const sat_problem_t *p, int32_t target, uint64_t max_
     }
     if (st != SAT_ERR_UNSUPPORTED) return st;
     DpWidePlan w;                                    // several nodes / wide keys: the prover
-    st = dpw_prepare(p, target, max_states, w);
+    st = dpw_prepare(p, target, max_states, w, (flags & SAT_DP_EXACT) != 0);
     if (st) return st;
     *bytes = w.status >= 0 ? 256 : dpw_ws_bytes(w);
     return SAT_OK;
 }
 
+int sat_dp_workspace_bytes(const sat_problem_t *p, int32_t target, uint64_t max_states, size_t *bytes) {
+    return sat_dp_workspace_bytes_ex(p, target, max_states, 0, bytes);
+}
+
 int sat_search_dp(const sat_problem_t *pr, int32_t target, uint64_t max_states, uint8_t *h_candidate,
                   sat_dp_info_t *info, void *d_ws, size_t ws_bytes, void *stream) {
-    if (!info) return SAT_ERR_INVALID;
+    return sat_search_dp_ex(pr, target, max_states, 0, h_candidate, info, d_ws, ws_bytes, stream);
+}
+
+int sat_search_dp_ex(const sat_problem_t *pr, int32_t target, uint64_t max_states, int32_t flags,
+                     uint8_t *h_candidate, sat_dp_info_t *info, void *d_ws, size_t ws_bytes, void *stream) {
+    if (!info || (flags & ~SAT_DP_EXACT)) return SAT_ERR_INVALID;
     int st = validate(pr);
     if (st) return st;
     nvtxRangePushA("sat_search_dp");
@@ -887,10 +1084,14 @@ int sat_search_dp(const sat_problem_t *pr, int32_t target, uint64_t max_states, 
     st = dp_prepare(pr, target, max_states, d);
     if (st == SAT_ERR_UNSUPPORTED) {                 // several nodes / wide keys: the prover
         DpWidePlan w;
-        st = dpw_prepare(pr, target, max_states, w);
+        st = dpw_prepare(pr, target, max_states, w, (flags & SAT_DP_EXACT) != 0);
         if (st) return st;
-        if (w.status >= 0) { info->status = w.status; info->makespan = -1; return SAT_OK; }
-        return dpw_run(pr, max_states, info, d_ws, ws_bytes, (cudaStream_t)stream, w);
+        if (w.status >= 0) {
+            // decided on the host (an initial free time or every option past the target):
+            // INFEASIBLE, never FEASIBLE without a search
+            info->status = w.status; info->makespan = -1; return SAT_OK;
+        }
+        return dpw_run(pr, max_states, info, d_ws, ws_bytes, (cudaStream_t)stream, w, h_candidate);
     }
     if (st) return st;
     if (d.status >= 0) { info->status = d.status; return SAT_OK; }

@@ -54,6 +54,7 @@ class SatDpInfo(ctypes.Structure):
 
 
 SAT_DP_INFEASIBLE, SAT_DP_FEASIBLE, SAT_DP_BUDGET = 0, 1, 2
+SAT_DP_EXACT = 1                # sat_search_dp_ex flag (ABI v8)
 DP_STATUS = {SAT_DP_INFEASIBLE: "infeasible", SAT_DP_FEASIBLE: "feasible", SAT_DP_BUDGET: "budget"}
 
 
@@ -92,6 +93,8 @@ _SIGS = {
     "sat_peer_atomics": ([_i32, _i32, _vp], _i32),
     "sat_search_dp": ([_vp, _i32, _u64, _vp, _vp, _vp, ctypes.c_size_t, _vp], _i32),
     "sat_key_finish": ([_vp, _i32, _vp, _i32, _vp, _vp, _i32, _u64, _i32, _vp], _i32),
+    "sat_dp_workspace_bytes_ex": ([_vp, _i32, _u64, _i32, _vp], _i32),
+    "sat_search_dp_ex": ([_vp, _i32, _u64, _i32, _vp, _vp, _vp, ctypes.c_size_t, _vp], _i32),
 }
 
 _LIB = None
@@ -110,7 +113,7 @@ def load_library(path: str = LIB_PATH):
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res
-    if lib.sat_abi_version() != 7:
+    if lib.sat_abi_version() != 8:
         raise E.PlanFailure("libsaturn_b200.so ABI version mismatch")
     _LIB = lib
     return lib
@@ -455,13 +458,17 @@ class Engine:
             self._side = self.torch.cuda.Stream(device=self.device)
         return self._side.cuda_stream
 
-    def dp_search(self, nprob: NativeProblem, target: int, max_states: int = 1 << 22, stream: int | None = None):
+    def dp_search(self, nprob: NativeProblem, target: int, max_states: int = 1 << 22, stream: int | None = None,
+                  exact: bool = False):
         """sat_search_dp: does some candidate reach makespan <= target?  Returns (status, info,
         candidate) -- candidate = (options, order) when FEASIBLE.  Synchronous (on ``stream``,
-        default the current stream)."""
+        default the current stream).  ``exact`` (several nodes): labelled states and the list
+        scheduler's own node choice, so FEASIBLE carries a candidate (SAT_DP_EXACT, ABI v8)."""
         torch = self.torch
         need = ctypes.c_size_t()
-        self._check(self.lib.sat_dp_workspace_bytes(nprob.ref, int(target), int(max_states), ctypes.byref(need)),
+        flags = SAT_DP_EXACT if exact else 0
+        self._check(self.lib.sat_dp_workspace_bytes_ex(nprob.ref, int(target), int(max_states), flags,
+                                                       ctypes.byref(need)),
                     what="sat_dp_workspace_bytes", nprob=nprob)
         if self._dp_ws is None or self._dp_ws.numel() < need.value:
             self._dp_ws = None
@@ -469,9 +476,9 @@ class Engine:
         J = nprob.struct.J
         cand = (ctypes.c_uint8 * (2 * J))()
         info = SatDpInfo()
-        self._check(self.lib.sat_search_dp(nprob.ref, int(target), int(max_states), cand, ctypes.byref(info),
-                                           _vp(self._dp_ws.data_ptr()), self._dp_ws.numel(),
-                                           _vp(self.stream() if stream is None else stream)),
+        self._check(self.lib.sat_search_dp_ex(nprob.ref, int(target), int(max_states), flags, cand,
+                                              ctypes.byref(info), _vp(self._dp_ws.data_ptr()), self._dp_ws.numel(),
+                                              _vp(self.stream() if stream is None else stream)),
                     what="sat_search_dp", nprob=nprob)
         self.launches += max(1, info.levels)
         out = None
@@ -490,17 +497,23 @@ class Engine:
         stats = {"attempts": [], "states": 0} if stats is None else stats
         best_ms, cand = int(makespan), None
         lb = int(prob.lower_bound()) if lb is None else int(lb)
+        exact = False               # several nodes: the canonical prover first, exact states on demand
         while best_ms > lb:
-            st, info, c = self.dp_search(nprob, best_ms - 1, opts.dp_states)
+            st, info, c = self.dp_search(nprob, best_ms - 1, opts.dp_states, exact=exact)
             stats["attempts"].append({"target": best_ms - 1, "status": DP_STATUS[st], "levels": info.levels,
-                                      "states": int(info.states), "widest_level": int(info.widest_level)})
+                                      "states": int(info.states), "widest_level": int(info.widest_level),
+                                      **({"exact": True} if exact else {})})
             stats["states"] += int(info.states)
             if st == SAT_DP_INFEASIBLE:
                 stats["proven"] = True
                 return True, best_ms, cand, stats
+            if st == SAT_DP_FEASIBLE and c is None and prob.N > 1 and not exact:
+                # the multi-node prover's (superset) level is non-empty: ask again on exact
+                # states, which either rule the target out or return a candidate reaching it
+                exact = True
+                continue
             if st == SAT_DP_BUDGET or c is None:
-                # out of budget, or the multi-node prover found its (superset) level non-empty:
-                # nothing proven, no shorter candidate in hand
+                # out of budget: nothing proven, no shorter candidate in hand
                 stats["proven"] = False
                 return False, best_ms, cand, stats
             best_ms, cand = int(info.makespan), c

@@ -39,7 +39,7 @@ def test_header_declarations_bound(lib):
 
 
 def test_host_only_entry_points(lib):
-    assert lib.sat_abi_version() == 7
+    assert lib.sat_abi_version() == 8
     for st in range(6):
         assert lib.sat_error_string(st)
 

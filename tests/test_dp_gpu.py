@@ -158,6 +158,53 @@ def test_dp_multinode_prover_is_sound():
     assert proven >= total * 3 // 4, (proven, total)
 
 
+def test_dp_multinode_exact_equals_oracle():
+    """SAT_DP_EXACT (ABI v8) on several nodes: labelled states expanded by the list scheduler's
+    own node choice, so the search is exact -- INFEASIBLE at M* - 1 on EVERY problem, FEASIBLE
+    at M* and above with a candidate the oracle replays to makespan <= target (= the reported
+    makespan), rebuilt deterministically.  Heterogeneous and interchangeable nodes, releases,
+    initial free times."""
+    eng = EN.Engine(0)
+    rng = random.Random(57)
+    for trial in range(40):
+        nodes = [[2, 2], [4, 4], [3, 2], [2, 2, 2], [4, 2, 1], [8, 8], [4, 4, 4, 4]][trial % 7]
+        op = random_problem(rng, rng.randint(2, 5), nodes, max_opts=3, max_d=8, hetero=trial % 3 == 0)
+        if trial % 4 == 1:
+            op.release = [rng.randint(0, 4) for _ in range(op.J)]
+        if trial % 5 == 2:
+            op.init_free = [sorted(rng.randint(0, 3) for _ in range(n)) for n in nodes]
+        prob = to_search_problem(op)
+        nprob = EN.NativeProblem(prob, 1)
+        opt = int(C.CProblem(op).search()[0])
+        st, info, cand = eng.dp_search(nprob, opt - 1, 1 << 20, exact=True)
+        assert st == EN.SAT_DP_INFEASIBLE, (trial, opt, info.levels)
+        for target in (opt, opt + 2):
+            st, info, cand = eng.dp_search(nprob, target, 1 << 20, exact=True)
+            assert st == EN.SAT_DP_FEASIBLE and cand is not None, (trial, target, opt)
+            opts, order = cand
+            assert sorted(order) == list(range(op.J))
+            ms, _, _ = C.CProblem(op).eval(opts, order)
+            assert ms <= target and ms == info.makespan, (trial, target, ms, info.makespan)
+            assert eng.dp_search(nprob, target, 1 << 20, exact=True)[2] == cand     # deterministic
+
+
+def test_prove_below_multinode_returns_the_optimum():
+    """prove_below on several nodes from a candidate above the optimum: the prover's
+    inconclusive answers hand over to exact states, and the descent ends AT the exhaustive
+    optimum with a candidate reaching it, proven (one interval less is infeasible)."""
+    eng = EN.Engine(0)
+    rng = random.Random(58)
+    for trial in range(12):
+        nodes = [[4, 4], [2, 2, 2], [8, 4]][trial % 3]
+        op = random_problem(rng, rng.randint(3, 5), nodes, max_opts=3, max_d=8, hetero=trial % 2 == 0)
+        prob = to_search_problem(op)
+        opt = int(C.CProblem(op).search()[0])
+        proven, ms, cand, stats = eng.prove_below(prob, opt + 3, SolveOptions(), lb=0)
+        assert proven and ms == opt, (trial, ms, opt, stats["attempts"])
+        opts, order = cand
+        assert C.CProblem(op).eval(opts, order)[0] == opt
+
+
 def test_hetero6_local_plan_proven_or_improved():
     """hetero6 (6 jobs, 8 + 4 GPU nodes, 2.3e11 candidates): the default solve is the local
     search; its makespan must equal the exhaustive optimum (index kernel over the whole space)

@@ -119,6 +119,14 @@ for trial in range(N_TRIALS):
             assert st == EN.SAT_DP_FEASIBLE or target < opt, ("prover", trial, target, opt)
             checks += 1
             proven += target == opt - 1 and st == EN.SAT_DP_INFEASIBLE
+        # exact states (SAT_DP_EXACT): infeasible at opt - 1, a candidate reaching opt
+        st, _, _ = eng.dp_search(nprob, opt - 1, 1 << 20, exact=True)
+        assert st == EN.SAT_DP_INFEASIBLE, ("exact", trial, opt)
+        st, info, cand = eng.dp_search(nprob, opt, 1 << 20, exact=True)
+        assert st == EN.SAT_DP_FEASIBLE and cand is not None, ("exact", trial, opt)
+        assert C.CProblem(op).eval(*cand)[0] == info.makespan <= opt, ("exact replay", trial)
+        checks += 2
 print(f"state-space search: {N_TRIALS} random problems (1-16-GPU nodes and 2-3-node clusters, releases, initial "
       f"free times), {checks} answers consistent with the oracle optimum; multi-node optimum proven on "
-      f"{proven} of {N_TRIALS // 2} ({time.time() - t0:.0f} s)", flush=True)
+      f"{proven} of {N_TRIALS // 2} by the prover and on every one by exact states, each with a candidate "
+      f"the oracle replays ({time.time() - t0:.0f} s)", flush=True)
