@@ -507,7 +507,7 @@ class Engine:
             if st == SAT_DP_INFEASIBLE:
                 stats["proven"] = True
                 return True, best_ms, cand, stats
-            if st == SAT_DP_FEASIBLE and c is None and prob.N > 1 and not exact:
+            if st == SAT_DP_FEASIBLE and c is None and prob.N > 1 and not exact and opts.dp_exact:
                 # the multi-node prover's (superset) level is non-empty: ask again on exact
                 # states, which either rule the target out or return a candidate reaching it
                 exact = True

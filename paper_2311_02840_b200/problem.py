@@ -68,6 +68,8 @@ class SolveOptions:
                                         # state space explodes unless the slack is tiny, and a
                                         # failed attempt costs its whole budget (cfg4 at T = 8:
                                         # ~80 ms to exhaust 4 M states)
+    dp_exact: bool = True               # several nodes: an inconclusive prover answer is asked again on
+                                        # exact (labelled) states, which return a candidate (ABI v8)
     dp_at_bound: bool = True            # one node: ask sat_search_dp about the lower bound itself on a
                                         # side stream while the first local-search wave runs
     share_incumbent: bool = True        # several ranks: one incumbent cell over NVLink peer memory
