@@ -492,6 +492,7 @@ struct DpWideParams {
     uint64_t cnum[kDpWideMaxN];             // C(T + G_n, G_n)
     int32_t ubase[kDpMaxJ], ucnt[kDpMaxJ], release[kDpMaxJ], minarea[kDpMaxJ];
     int32_t Kb;                             // binomial table row width (max G_n + 1)
+    int32_t binom_n;                        // entries of the binomial table
     int32_t nrem;                           // jobs still to place in the level being expanded
     int32_t exact;                          // 1: labelled nodes, the list scheduler's own node choice
     const uint8_t *ue;                      // [n_usable] every node the option is eligible on (exact)
@@ -501,6 +502,8 @@ struct DpWideParams {
     const uint8_t *um;                      // [n_usable] node eligibility bits
     const int16_t *ud;                      // [n_usable][N] duration per node
     const int16_t *dg;                      // [J][N][32] least usable duration at gang k+1 (T+1: none)
+    const uint32_t *dgp;                    // [J][16] the same per global slot (node_off[n] + k), two
+                                            // 16-bit slots per word, 0x7fff past Gtot
     unsigned __int128 *table;
     uint64_t cap_mask;
     int32_t cap_log2, max_probe;
@@ -536,16 +539,17 @@ __device__ __forceinline__ unsigned __int128 cas128(unsigned __int128 *addr, uns
     return ((unsigned __int128)o1 << 64) | o0;
 }
 
-__device__ __forceinline__ uint64_t dpw_rank(const DpWideParams &p, const int32_t *v, int g) {
+__device__ __forceinline__ uint64_t dpw_rank(const DpWideParams &p, const int32_t *v, int g, const uint64_t *bt) {
     uint64_t r = 0;
-    for (int i = 0; i < g; ++i) r += __ldg(&p.binom[(v[i] + i) * p.Kb + (i + 1)]);
+    for (int i = 0; i < g; ++i) r += bt[(v[i] + i) * p.Kb + (i + 1)];
     return r;
 }
 
 // canonical key of a full state (vectors are permuted in place into canonical node order)
-__device__ __forceinline__ unsigned __int128 dpw_key(const DpWideParams &p, uint64_t R, int32_t *a) {
+__device__ __forceinline__ unsigned __int128 dpw_key(const DpWideParams &p, uint64_t R, int32_t *a,
+                                                     const uint64_t *bt) {
     uint64_t rk[kDpWideMaxN];
-    for (int n = 0; n < p.N; ++n) rk[n] = dpw_rank(p, a + p.node_off[n], p.node_g[n]);
+    for (int n = 0; n < p.N; ++n) rk[n] = dpw_rank(p, a + p.node_off[n], p.node_g[n], bt);
     // sort interchangeable nodes by rank (insertion sort over the <= 8 nodes, within groups)
     for (int n = 1; n < p.N; ++n)
         for (int m = n; m > 0 && p.node_grp[m - 1] == p.node_grp[m] && rk[m - 1] > rk[m]; --m) {
@@ -558,21 +562,39 @@ __device__ __forceinline__ unsigned __int128 dpw_key(const DpWideParams &p, uint
     return key;
 }
 
-__device__ __forceinline__ bool dpw_viable(const DpWideParams &p, uint64_t R2, const int32_t *b) {
-    int64_t area = 0;
-    for (int i = 0; i < p.Gtot; ++i) area += b[i];
-    for (int i = 0; i < p.J; ++i) {
-        if (!((R2 >> i) & 1ull)) continue;
-        area += p.minarea[i];
-        int32_t lo = 0x7fffffff;
-        for (int n = 0; n < p.N; ++n) {
-            const int16_t *dgn = p.dg + ((size_t)i * p.N + n) * 32;
-            const int32_t *bn = b + p.node_off[n];
-            for (int k = 0; k < p.node_g[n]; ++k) lo = min(lo, max(bn[k], p.release[i]) + (int32_t)__ldg(&dgn[k]));
-        }
-        if (lo > p.T) return false;
+// Viability of a child state b (R2 = its jobs still to place): every such job must be able to end
+// by T -- min over nodes and gangs k of max(b[slot k-1], release) + least duration at gang k --
+// and the GPU time left must hold their least areas.  The per-job minimum runs on 16-bit pairs:
+// b packed once per child, 16 VIADDMNMX.U16x2 per job against its packed row `sdgp` (staged in
+// shared memory); every value is <= T + 1 <= 30 001, so sums stay below 2^16.  b holds
+// kDpWideSlots entries, zero past Gtot (the packing needs no per-slot bound test).
+__device__ __forceinline__ bool dpw_viable(const DpWideParams &p, uint64_t R2, const int32_t *b,
+                                           const uint32_t *sdgp) {
+    uint32_t area = 0;                         // <= 32 slots x 30 000
+    uint32_t bp[16];
+#pragma unroll
+    for (int w = 0; w < 16; ++w) {
+        const uint32_t lo = (uint32_t)b[2 * w], hi = (uint32_t)b[2 * w + 1];
+        area += lo + hi;
+        bp[w] = lo | (hi << 16);
     }
-    return area <= (int64_t)p.T * p.Gtot;
+    for (uint64_t m = R2; m; m &= m - 1) {
+        const int i = __ffsll((long long)m) - 1;
+        area += p.minarea[i];
+        const uint32_t *dj = sdgp + i * 16;
+        uint32_t acc = 0xFFFFFFFFu;
+        const int32_t rel = p.release[i];
+        if (rel == 0) {
+#pragma unroll
+            for (int w = 0; w < 16; ++w) acc = __viaddmin_u16x2(bp[w], dj[w], acc);
+        } else {
+            const uint32_t r2 = (uint32_t)rel * 0x10001u;
+#pragma unroll
+            for (int w = 0; w < 16; ++w) acc = __viaddmin_u16x2(__vmaxu2(bp[w], r2), dj[w], acc);
+        }
+        if ((int32_t)min(acc & 0xFFFFu, acc >> 16) > p.T) return false;
+    }
+    return (int64_t)area <= (int64_t)p.T * p.Gtot;
 }
 
 // exact mode: node the list scheduler gives usable option q of job j from state a (earliest end
@@ -604,8 +626,8 @@ __device__ __forceinline__ int32_t dpw_place(const DpWideParams &p, const int32_
 }
 
 // claim the state's key in the hash set and append it to the level; false = out of budget
-__device__ __forceinline__ bool dpw_insert(const DpWideParams &p, uint64_t R2, int32_t *b) {
-    const unsigned __int128 key = dpw_key(p, R2, b);
+__device__ __forceinline__ bool dpw_insert(const DpWideParams &p, uint64_t R2, int32_t *b, const uint64_t *bt) {
+    const unsigned __int128 key = dpw_key(p, R2, b, bt);
     const uint64_t hh = ((uint64_t)key ^ (uint64_t)(key >> 64) * 0xBF58476D1CE4E5B9ull) * kGolden;
     uint64_t h = hh >> (64 - p.cap_log2);
     const unsigned __int128 EMPTY = ~(unsigned __int128)0;
@@ -624,7 +646,11 @@ __device__ __forceinline__ bool dpw_insert(const DpWideParams &p, uint64_t R2, i
     }
 }
 
-__global__ void __launch_bounds__(kDpThreads) k_dp_expand_wide(const __grid_constant__ DpWideParams p) {
+__global__ void __launch_bounds__(kDpThreads, 6) k_dp_expand_wide(const __grid_constant__ DpWideParams p) {
+    __shared__ uint32_t sdgp[kDpMaxJ * 16];
+    for (int i = threadIdx.x; i < p.J * 16; i += blockDim.x) sdgp[i] = p.dgp[i];
+    __syncthreads();
+    const uint64_t *bt = p.binom;
     const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (tid >= p.n_in * (uint64_t)p.nrem) return;
     if (*reinterpret_cast<volatile unsigned int *>(p.overflow)) return;
@@ -636,7 +662,11 @@ __global__ void __launch_bounds__(kDpThreads) k_dp_expand_wide(const __grid_cons
     const int j = kk < nlo ? (int)__fns(Rlo, 0, kk + 1) : 32 + (int)__fns(Rhi, 0, kk - nlo + 1);
     const uint64_t R2 = R & ~(1ull << j);
     int32_t a[kDpWideSlots], b[kDpWideSlots];
-    for (int i = 0; i < p.Gtot; ++i) a[i] = p.in_A[s * p.Gtot + i];
+#pragma unroll
+    for (int i = 0; i < kDpWideSlots; ++i) {           // slots past Gtot stay 0 (dpw_viable packs all 32)
+        a[i] = i < p.Gtot ? (int32_t)p.in_A[s * p.Gtot + i] : 0;
+        b[i] = 0;
+    }
     for (int q = p.ubase[j]; q < p.ubase[j] + p.ucnt[j]; ++q) {
         const int g = p.ug[q];
         const uint32_t mask = p.um[q];
@@ -646,8 +676,8 @@ __global__ void __launch_bounds__(kDpThreads) k_dp_expand_wide(const __grid_cons
             const int bn = dpw_pick(p, a, q, j);
             if (bn < 0 || !((mask >> bn) & 1u)) continue;
             const int32_t e = dpw_place(p, a, q, j, bn, b);
-            if (e > p.T || !dpw_viable(p, R2, b)) continue;
-            if (!dpw_insert(p, R2, b)) return;
+            if (e > p.T || !dpw_viable(p, R2, b, sdgp)) continue;
+            if (!dpw_insert(p, R2, b, bt)) return;
             continue;
         }
         int32_t best = 0x7fffffff;
@@ -663,8 +693,8 @@ __global__ void __launch_bounds__(kDpThreads) k_dp_expand_wide(const __grid_cons
             int32_t *bn = b + p.node_off[n];
             const int G = p.node_g[n];
             for (int i = 0; i < G; ++i) bn[i] = max(an[i], min(i + g < G ? an[i + g] : 0x7fffffff, best));
-            if (!dpw_viable(p, R2, b)) continue;
-            if (!dpw_insert(p, R2, b)) return;
+            if (!dpw_viable(p, R2, b, sdgp)) continue;
+            if (!dpw_insert(p, R2, b, bt)) return;
         }
     }
 }
@@ -700,7 +730,7 @@ __global__ void __launch_bounds__(kDpThreads) k_dpw_pick_state(const __grid_cons
         }
         if (!hit) return;
     }
-    const unsigned __int128 key = dpw_key(p, R, a);      // exact mode: no canonical permutation
+    const unsigned __int128 key = dpw_key(p, R, a, p.binom);   // exact mode: no canonical permutation
     const unsigned long long hi = (unsigned long long)(uint64_t)(key >> 64), lo = (unsigned long long)(uint64_t)key;
     if (phase == 0) {
         atomicMin(p.pick_hi, hi);
@@ -717,6 +747,7 @@ struct DpWidePlan {
     std::vector<uint8_t> ug, um, ue;
     std::vector<int16_t> ud, dg, uf;
     std::vector<int> uorig, ujob;           // original option digit / job of each usable option
+    std::vector<uint32_t> dgp;              // [J][16] packed least durations per global slot
     std::vector<uint64_t> binom;
     std::vector<uint16_t> a0;
     int status = -1;
@@ -859,6 +890,16 @@ static int dpw_prepare(const sat_problem_t *pr, int32_t T, uint64_t max_states, 
                 for (int g = 0; g < 32; ++g) dg2[((size_t)j * N + k) * 32 + g] = d.dg[((size_t)j * N + ord[k]) * 32 + g];
         p = p2; d.um = um2; d.ud = ud2; d.dg = dg2; d.a0 = a02; d.ue = ue2; d.uf = uf2;
     }
+    // per job, the least usable durations per global slot, packed two per word (kernel viability)
+    d.dgp.assign((size_t)J * 16, 0x7FFF7FFFu);
+    for (int j = 0; j < J; ++j)
+        for (int n = 0; n < N; ++n)
+            for (int k = 0; k < p.node_g[n]; ++k) {
+                const int slot = p.node_off[n] + k;
+                const uint32_t v = (uint32_t)(uint16_t)d.dg[((size_t)j * N + n) * 32 + k];
+                uint32_t &wd = d.dgp[(size_t)j * 16 + slot / 2];
+                wd = (slot & 1) ? ((wd & 0xFFFFu) | (v << 16)) : ((wd & 0xFFFF0000u) | v);
+            }
     // key width: 2^J x prod C(T + G_n, G_n) < 2^127
     const int n_max = T + gmax;
     p.Kb = gmax + 1;
@@ -872,6 +913,7 @@ static int dpw_prepare(const sat_problem_t *pr, int32_t T, uint64_t max_states, 
             d.binom[(size_t)n * p.Kb + k] = (uint64_t)v;
         }
     }
+    p.binom_n = (int32_t)std::min<size_t>(d.binom.size(), 0x7fffffff);
     double bits = J;
     for (int n = 0; n < N; ++n) {
         p.cnum[n] = d.binom[(size_t)(T + p.node_g[n]) * p.Kb + p.node_g[n]];
@@ -887,7 +929,8 @@ static int dpw_prepare(const sat_problem_t *pr, int32_t T, uint64_t max_states, 
     p.max_probe = 1 << 14;
     d.binom_bytes = align256(d.binom.size() * sizeof(uint64_t));
     d.aux_bytes = align256(d.ug.size() + 16) + align256(d.um.size() + 16) + align256(d.ud.size() * 2 + 16) +
-                  align256(d.dg.size() * 2) + align256(d.ue.size() + 16) + align256(d.uf.size() * 2 + 16);
+                  align256(d.dg.size() * 2) + align256(d.ue.size() + 16) + align256(d.uf.size() * 2 + 16) +
+                  align256(d.dgp.size() * 4);
     d.table_bytes = align256(cap * 16);
     d.R_bytes = align256(max_states * sizeof(uint64_t));
     d.A_bytes = align256(max_states * off * sizeof(uint16_t));
@@ -912,6 +955,7 @@ static int dpw_run(const sat_problem_t *pr, uint64_t max_states, sat_dp_info_t *
     int16_t *dg = reinterpret_cast<int16_t *>(take(align256(d.dg.size() * 2)));
     uint8_t *ue = take(align256(d.ue.size() + 16));
     int16_t *uf = reinterpret_cast<int16_t *>(take(align256(d.uf.size() * 2 + 16)));
+    uint32_t *dgp = reinterpret_cast<uint32_t *>(take(align256(d.dgp.size() * 4)));
     auto *table = reinterpret_cast<unsigned __int128 *>(take(d.table_bytes));
     uint64_t *Rs = reinterpret_cast<uint64_t *>(take(d.R_bytes));
     uint16_t *As = reinterpret_cast<uint16_t *>(take(d.A_bytes));
@@ -924,6 +968,7 @@ static int dpw_run(const sat_problem_t *pr, uint64_t max_states, sat_dp_info_t *
         cudaMemcpyAsync(dg, d.dg.data(), d.dg.size() * 2, cudaMemcpyHostToDevice, s) ||
         (d.ue.size() && cudaMemcpyAsync(ue, d.ue.data(), d.ue.size(), cudaMemcpyHostToDevice, s)) ||
         (d.uf.size() && cudaMemcpyAsync(uf, d.uf.data(), d.uf.size() * 2, cudaMemcpyHostToDevice, s)) ||
+        cudaMemcpyAsync(dgp, d.dgp.data(), d.dgp.size() * 4, cudaMemcpyHostToDevice, s) ||
         cudaMemsetAsync(table, 0xFF, d.cap * 16, s) || cudaMemsetAsync(ctr, 0, 256, s))
         return SAT_ERR_CUDA;
     const uint64_t full = J == 64 ? ~0ull : ((1ull << J) - 1ull);
@@ -931,7 +976,7 @@ static int dpw_run(const sat_problem_t *pr, uint64_t max_states, sat_dp_info_t *
         cudaMemcpyAsync(As, d.a0.data(), Gt * 2, cudaMemcpyHostToDevice, s))
         return SAT_ERR_CUDA;
     p.binom = binom; p.ug = ug; p.um = um; p.ud = ud; p.dg = dg; p.table = table;
-    p.ue = ue; p.uf = uf;
+    p.ue = ue; p.uf = uf; p.dgp = dgp;
     p.count = ctr;
     p.overflow = reinterpret_cast<unsigned int *>(ctr + 1);
     p.pick_hi = ctr + 2;
