@@ -11,3 +11,6 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_dp
 ncu -i gpurun_out/dpw.ncu-rep --page source --csv > gpurun_out/dpw_source.csv 2>/dev/null
 ncu -i gpurun_out/dpw.ncu-rep --page details > gpurun_out/dpw_details.txt 2>/dev/null
 rm -f gpurun_out/dpw.ncu-rep
+timeout 300 python tools/dp_probe.py 3 29 30 > gpurun_out/dp_cfg3.txt 2>&1; cat gpurun_out/dp_cfg3.txt
+timeout 300 python bench.py --config 3 --steps 2 --warmup 3 --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads([l for l in sys.stdin if l.startswith('{')][-1]); t=d['time_to_best']; print('cfg3 ttb', t['device_s'], t['wall_s'], t['status'])"
+timeout 600 python tools/multinode_optimality.py 32 > gpurun_out/mn_opt2.txt 2>&1; tail -2 gpurun_out/mn_opt2.txt
