@@ -346,7 +346,10 @@ class DeviceSolve:
             eng.search_sampled(self.nprob, EN.SRC_SUBSTREAM, self.opts.seed, self.a, self.b, self.best)
 
     def combine(self, group):
-        return self.EN._combine(self.best, self.nprob.grid, group, self.world)
+        # the engine's key hand-off (sat_key_finish, + NCCL MIN across ranks): no library
+        # elementwise kernels inside the timed step
+        key, _ = self.eng._key_finish(self.best, self.nprob.grid, group, self.world, self.idx_bits, 0)
+        return key.cpu().tolist()[:2]
 
 
 def introspection_run(t, w, opts, group=None, record=None):
