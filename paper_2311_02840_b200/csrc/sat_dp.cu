@@ -742,6 +742,185 @@ __global__ void __launch_bounds__(kDpThreads) k_dpw_pick_state(const __grid_cons
     }
 }
 
+// ------------------------------------------------------------------------------------------
+// Wide expansion specialised on homogeneous nodes (N nodes of G GPUs, G even, N x G <= 32): the
+// state lives in registers as N x G/2 words of 16-bit pairs; the shift by a thread's own gang is
+// a read of its shared-memory column (node n at words n*G .. n*G+G/2-1, +inf words after it, one
+// pad word at the end) with one PRMT per word -- the k_cand Multi16 scheme -- so no state array
+// sits in local memory.  Same children, viability, canonical keys and appends as
+// k_dp_expand_wide (the generic kernel keeps every other shape).
+// ------------------------------------------------------------------------------------------
+template <int N, int G>
+__global__ void __launch_bounds__(kDpThreads) k_dpw_expand_h(const __grid_constant__ DpWideParams p) {
+    constexpr int H = G / 2, W = N * H, CW = N * G + 1;     // words: per node, state, column
+    __shared__ uint32_t sdgp[kDpMaxJ * 16];
+    extern __shared__ uint32_t scol[];                      // [CW][kDpThreads]
+    for (int i = threadIdx.x; i < p.J * 16; i += blockDim.x) sdgp[i] = p.dgp[i];
+    __syncthreads();
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (tid >= p.n_in * (uint64_t)p.nrem) return;
+    if (*reinterpret_cast<volatile unsigned int *>(p.overflow)) return;
+    const uint64_t s = tid / (uint64_t)p.nrem;
+    const int kk = (int)(tid - s * (uint64_t)p.nrem);
+    const uint64_t R = p.in_R[s];
+    const uint32_t Rlo = (uint32_t)R, Rhi = (uint32_t)(R >> 32);
+    const int nlo = __popc(Rlo);
+    const int j = kk < nlo ? (int)__fns(Rlo, 0, kk + 1) : 32 + (int)__fns(Rhi, 0, kk - nlo + 1);
+    const uint64_t R2 = R & ~(1ull << j);
+    uint32_t ap[W];
+    const uint32_t *inw = reinterpret_cast<const uint32_t *>(p.in_A + s * (uint64_t)(N * G));
+    uint32_t *col = scol + threadIdx.x;
+#pragma unroll
+    for (int w = 0; w < W; ++w) ap[w] = inw[w];
+#pragma unroll
+    for (int n = 0; n < N; ++n)
+#pragma unroll
+        for (int k = 0; k < H; ++k) {
+            col[(n * G + k) * kDpThreads] = ap[n * H + k];
+            col[(n * G + H + k) * kDpThreads] = 0xFFFFFFFFu;
+        }
+    col[(CW - 1) * kDpThreads] = 0xFFFFFFFFu;
+    const int32_t rel = p.release[j];
+    const int64_t cap = (int64_t)p.T * (N * G);
+    const uint64_t *bt = p.binom;
+    // child on node bn (gang g, end e) from the parent: packed, then viability, key, append
+    auto child = [&](int g, int bn, int32_t e) -> bool {
+        const uint32_t e2 = (uint32_t)e * 0x10001u;
+        const uint32_t sel = (g & 1) ? 0x5432u : 0x3210u;
+        const uint32_t *nb = col + bn * G * kDpThreads;
+        const uint32_t *src = nb + (g >> 1) * kDpThreads;
+        uint32_t nw[H];
+#pragma unroll
+        for (int k = 0; k < H; ++k)
+            nw[k] = __vmaxu2(nb[k * kDpThreads],
+                             __vminu2(__byte_perm(src[k * kDpThreads], src[(k + 1) * kDpThreads], sel), e2));
+        uint32_t bp[W];
+        uint32_t area = 0;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            bp[w] = (w / H == bn) ? nw[w % H] : ap[w];
+            area += (bp[w] & 0xFFFFu) + (bp[w] >> 16);
+        }
+        // viability: every remaining job can end by T; their least areas fit
+        for (uint64_t m = R2; m; m &= m - 1) {
+            const int i = __ffsll((long long)m) - 1;
+            area += p.minarea[i];
+            const uint32_t *dj = sdgp + i * 16;
+            uint32_t acc = 0xFFFFFFFFu;
+            const int32_t ri = p.release[i];
+            if (ri == 0) {
+#pragma unroll
+                for (int w = 0; w < W; ++w) acc = __viaddmin_u16x2(bp[w], dj[w], acc);
+            } else {
+                const uint32_t r2 = (uint32_t)ri * 0x10001u;
+#pragma unroll
+                for (int w = 0; w < W; ++w) acc = __viaddmin_u16x2(__vmaxu2(bp[w], r2), dj[w], acc);
+            }
+            if ((int32_t)min(acc & 0xFFFFu, acc >> 16) > p.T) return true;
+        }
+        if ((int64_t)area > cap) return true;
+        // canonical key: ranks per node, interchangeable nodes sorted by rank (as dpw_key)
+        uint64_t rk[N];
+#pragma unroll
+        for (int n = 0; n < N; ++n) {
+            uint64_t r = 0;
+#pragma unroll
+            for (int k = 0; k < G; ++k) {
+                const int32_t v = (int32_t)((bp[n * H + k / 2] >> (16 * (k & 1))) & 0xFFFFu);
+                r += __ldg(&bt[(v + k) * p.Kb + (k + 1)]);
+            }
+            rk[n] = r;
+        }
+#pragma unroll
+        for (int n = 1; n < N; ++n)
+#pragma unroll
+            for (int m = n; m > 0; --m) {
+                const bool sw = p.node_grp[m - 1] == p.node_grp[m] && rk[m - 1] > rk[m];
+                const uint64_t t0 = rk[m - 1], t1 = rk[m];
+                rk[m - 1] = sw ? t1 : t0;
+                rk[m] = sw ? t0 : t1;
+#pragma unroll
+                for (int k = 0; k < H; ++k) {
+                    const uint32_t x = bp[(m - 1) * H + k], y = bp[m * H + k];
+                    bp[(m - 1) * H + k] = sw ? y : x;
+                    bp[m * H + k] = sw ? x : y;
+                }
+            }
+        unsigned __int128 key = R2;
+#pragma unroll
+        for (int n = 0; n < N; ++n) key = key * p.cnum[n] + rk[n];
+        const uint64_t hh = ((uint64_t)key ^ (uint64_t)(key >> 64) * 0xBF58476D1CE4E5B9ull) * kGolden;
+        uint64_t h = hh >> (64 - p.cap_log2);
+        const unsigned __int128 EMPTY = ~(unsigned __int128)0;
+        for (int probe = 0;; ++probe) {
+            if (probe > p.max_probe) { atomicOr(p.overflow, 1u); return false; }
+            const unsigned __int128 old = cas128(&p.table[h], EMPTY, key);
+            if (old == EMPTY) {
+                const unsigned long long idx = atomicAdd(p.count, 1ull);
+                if (idx >= p.out_cap) { atomicOr(p.overflow, 1u); return false; }
+                p.out_R[idx] = R2;
+                uint32_t *ow = reinterpret_cast<uint32_t *>(p.out_A + idx * (uint64_t)(N * G));
+#pragma unroll
+                for (int w = 0; w < W; ++w) ow[w] = bp[w];
+                return true;
+            }
+            if (old == key) return true;
+            h = (h + 1) & p.cap_mask;
+        }
+    };
+    for (int q = p.ubase[j]; q < p.ubase[j] + p.ucnt[j]; ++q) {
+        const int g = p.ug[q];
+        const uint32_t mask = p.um[q];
+        const int gm = g - 1;
+        const uint32_t selt = 0x4410u + (uint32_t)(gm & 1) * 0x22u;
+        int32_t t[N];
+#pragma unroll
+        for (int n = 0; n < N; ++n)
+            t[n] = max((int32_t)__byte_perm(col[(n * G + (gm >> 1)) * kDpThreads], 0u, selt), rel);
+        if (p.exact) {
+            const uint32_t em = p.ue[q];
+            int32_t best = 0x7fffffff;
+            int bn = -1;
+#pragma unroll
+            for (int n = 0; n < N; ++n) {
+                const int32_t e = t[n] + (int32_t)p.uf[q * N + n];
+                if (((em >> n) & 1u) && e < best) { best = e; bn = n; }
+            }
+            if (bn < 0 || !((mask >> bn) & 1u) || best > p.T) continue;
+            if (!child(g, bn, best)) return;
+            continue;
+        }
+        int32_t best = 0x7fffffff;
+#pragma unroll
+        for (int n = 0; n < N; ++n)
+            if ((mask >> n) & 1u) best = min(best, t[n] + (int32_t)p.ud[q * N + n]);
+        if (best > p.T) continue;
+#pragma unroll
+        for (int n = 0; n < N; ++n) {                       // every node tying for the earliest finish
+            if (!((mask >> n) & 1u) || t[n] + (int32_t)p.ud[q * N + n] != best) continue;
+            if (!child(g, n, best)) return;
+        }
+    }
+}
+
+// launch of one wide level: the homogeneous specialisation when the shape has one
+static int dpw_launch_level(const DpWideParams &p, unsigned blocks, cudaStream_t s) {
+    bool homog = p.Gtot == p.N * p.node_g[0];
+    for (int n = 1; n < p.N; ++n) homog &= p.node_g[n] == p.node_g[0];
+    const int G = p.node_g[0];
+    const size_t smem = (size_t)(p.N * G + 1) * kDpThreads * 4;
+#define SAT_DPW(NN, GG)                                                                   \
+    if (homog && p.N == NN && G == GG) {                                                  \
+        k_dpw_expand_h<NN, GG><<<blocks, kDpThreads, smem, s>>>(p);                      \
+        return cudaGetLastError() == cudaSuccess ? SAT_OK : SAT_ERR_CUDA;                 \
+    }
+    // (3 and 4 nodes of 8 GPUs need 100+ registers here and ran no faster than the generic kernel)
+    SAT_DPW(2, 4) SAT_DPW(3, 4) SAT_DPW(4, 4) SAT_DPW(2, 8)
+#undef SAT_DPW
+    k_dp_expand_wide<<<blocks, kDpThreads, 0, s>>>(p);
+    return cudaGetLastError() == cudaSuccess ? SAT_OK : SAT_ERR_CUDA;
+}
+
 struct DpWidePlan {
     DpWideParams p{};
     std::vector<uint8_t> ug, um, ue;
@@ -995,8 +1174,7 @@ static int dpw_run(const sat_problem_t *pr, uint64_t max_states, sat_dp_info_t *
         p.nrem = J - level;
         const uint64_t blocks = (p.n_in * (uint64_t)p.nrem + kDpThreads - 1) / kDpThreads;
         if (blocks > 0x7fffffffull) return SAT_ERR_TOO_LARGE;
-        k_dp_expand_wide<<<(unsigned)blocks, kDpThreads, 0, s>>>(p);
-        if (cudaGetLastError() != cudaSuccess) return SAT_ERR_CUDA;
+        if (dpw_launch_level(p, (unsigned)blocks, s) != SAT_OK) return SAT_ERR_CUDA;
         unsigned long long got[2];
         if (cudaMemcpyAsync(got, ctr, sizeof(got), cudaMemcpyDeviceToHost, s) || cudaStreamSynchronize(s))
             return SAT_ERR_CUDA;

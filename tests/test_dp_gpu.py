@@ -130,15 +130,16 @@ def test_solve_without_proof_keeps_local_status():
 
 
 def test_dp_multinode_prover_is_sound():
-    """Several nodes (heterogeneous, interchangeable, releases, initial free times): the wide
-    prover never calls a reachable target infeasible -- every INFEASIBLE at T has the oracle's
+    """Several nodes (heterogeneous, interchangeable, releases, initial free times; the
+    homogeneous 2 x 4, 3 x 4, 4 x 4 and 2 x 8 shapes run the register-resident specialisation of
+    the wide kernel): the wide prover never calls a reachable target infeasible -- every INFEASIBLE at T has the oracle's
     exhaustive optimum above T -- and it is FEASIBLE from the optimum up.  It proves the optimum
     (INFEASIBLE at M* - 1) on most problems."""
     eng = EN.Engine(0)
     rng = random.Random(31)
     proven = total = 0
     for trial in range(40):
-        nodes = [[2, 2], [4, 4], [3, 2], [2, 2, 2], [4, 2, 1], [8, 8]][trial % 6]
+        nodes = [[2, 2], [4, 4], [3, 2], [2, 2, 2], [4, 2, 1], [8, 8], [4, 4, 4], [4, 4, 4, 4]][trial % 8]
         op = random_problem(rng, rng.randint(2, 5), nodes, max_opts=3, max_d=8, hetero=trial % 3 == 0)
         if trial % 4 == 1:
             op.release = [rng.randint(0, 4) for _ in range(op.J)]
@@ -167,7 +168,7 @@ def test_dp_multinode_exact_equals_oracle():
     eng = EN.Engine(0)
     rng = random.Random(57)
     for trial in range(40):
-        nodes = [[2, 2], [4, 4], [3, 2], [2, 2, 2], [4, 2, 1], [8, 8], [4, 4, 4, 4]][trial % 7]
+        nodes = [[2, 2], [4, 4], [3, 2], [2, 2, 2], [4, 2, 1], [8, 8], [4, 4, 4, 4], [4, 4, 4]][trial % 8]
         op = random_problem(rng, rng.randint(2, 5), nodes, max_opts=3, max_d=8, hetero=trial % 3 == 0)
         if trial % 4 == 1:
             op.release = [rng.randint(0, 4) for _ in range(op.J)]

@@ -106,7 +106,7 @@ for trial in range(N_TRIALS):
         assert cp.eval(*cand)[0] <= opt, ("dp replay", trial)
         checks += 2
     else:
-        nodes = [[2, 2], [4, 4], [3, 2], [2, 2, 2], [4, 2, 1]][trial % 5]
+        nodes = [[2, 2], [4, 4], [3, 2], [2, 2, 2], [4, 2, 1], [4, 4, 4], [4, 4, 4, 4], [8, 8]][trial % 8]
         op = random_problem(rng, rng.randint(2, 5), nodes, max_opts=3, max_d=8, hetero=trial % 3 == 0)
         if trial % 4 == 1:
             op.release = [rng.randint(0, 4) for _ in range(op.J)]
