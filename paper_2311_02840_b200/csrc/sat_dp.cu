@@ -170,6 +170,45 @@ __device__ __forceinline__ bool dp_viable16(const DpParams &p, const DpShared<GM
     return area <= (int64_t)p.T * p.Gr;
 }
 
+// dp_viable16 on an already packed child (slots >= Gr hold 0x7FFF, taken back out of the area)
+template <int GM>
+__device__ __forceinline__ bool dp_viable16p(const DpParams &p, const DpShared<GM> &sh, uint64_t R2,
+                                             const uint32_t (&bp)[GM / 2]) {
+    constexpr int W = GM / 2;
+    int64_t area = -(int64_t)(GM - p.Gr) * 0x7FFF;
+#pragma unroll
+    for (int w = 0; w < W; ++w) area += (bp[w] & 0xFFFFu) + (bp[w] >> 16);
+    for (uint64_t m = R2; m; m &= m - 1) {
+        const int i = __ffsll((long long)m) - 1;
+        area += sh.minarea[i];
+        uint32_t m2 = 0xFFFFFFFFu;
+        if (p.has_release) {
+            const uint32_t r2 = (uint32_t)sh.release[i] * 0x10001u;
+#pragma unroll
+            for (int w = 0; w < W; ++w) m2 = __viaddmin_u16x2(__vmaxu2(bp[w], r2), sh.dgp[i][w], m2);
+        } else {
+#pragma unroll
+            for (int w = 0; w < W; ++w) m2 = __viaddmin_u16x2(bp[w], sh.dgp[i][w], m2);
+        }
+        if ((int32_t)min(m2 & 0xFFFFu, m2 >> 16) > p.T) return false;
+    }
+    return area <= (int64_t)p.T * p.Gr;
+}
+
+// dp_rank of a packed state
+template <int GM>
+__device__ __forceinline__ uint64_t dp_rank16(const DpParams &p, const uint32_t (&bp)[GM / 2]) {
+    const int K = p.Gr + 1;
+    uint64_t r = 0;
+#pragma unroll
+    for (int i = 0; i < GM; ++i)
+        if (i < p.Gr) {
+            const int32_t v = (int32_t)((bp[i / 2] >> (16 * (i & 1))) & 0xFFFFu);
+            r += __ldg(&p.binom[(v + i) * K + (i + 1)]);
+        }
+    return r;
+}
+
 template <int GM>
 __global__ void __launch_bounds__(kDpThreads) k_dp_expand(const __grid_constant__ DpParams p, int L) {
     // Level L -> L + 1, sized on the device: the level's state count and offset are read from
@@ -182,6 +221,11 @@ __global__ void __launch_bounds__(kDpThreads) k_dp_expand(const __grid_constant_
     __shared__ unsigned long long block_base[2];
     __shared__ unsigned int stop;
     __shared__ DpShared<GM> sh;
+    // per thread: the parent's packed slots (GM/2 words), then GM/2 + 1 words of 0x7FFF pairs --
+    // the shift by the option's gang is one PRMT of two column words (k_cand's scheme)
+    __shared__ uint32_t scol[(GM + 1) * kDpThreads];
+    constexpr int H = GM / 2;
+    uint32_t *col = scol + threadIdx.x;
     int par = 0;
     if (threadIdx.x == 0) stop = *reinterpret_cast<volatile unsigned int *>(p.overflow);
     __syncthreads();
@@ -211,7 +255,7 @@ __global__ void __launch_bounds__(kDpThreads) k_dp_expand(const __grid_constant_
         const uint64_t tid = t0 + threadIdx.x;
         int j = 0, nq = 0;
         uint64_t R2 = 0;
-        int32_t a[GM], b[GM];
+        uint32_t ap[H], bp[H];
         if (tid < total) {
             const uint64_t s = tid / (uint64_t)nrem;
             const int kk = (int)(tid - s * (uint64_t)nrem);
@@ -222,15 +266,36 @@ __global__ void __launch_bounds__(kDpThreads) k_dp_expand(const __grid_constant_
             R2 = R & ~(1ull << j);
             nq = sh.ucnt[j];
 #pragma unroll
-            for (int i = 0; i < GM; ++i) a[i] = i < p.Gr ? (int32_t)in_A[s * p.Gr + i] : 0x7fffffff;
+            for (int w = 0; w < H; ++w) {
+                const uint32_t lo = 2 * w < p.Gr ? (uint32_t)in_A[s * p.Gr + 2 * w] : 0x7FFFu;
+                const uint32_t hi = 2 * w + 1 < p.Gr ? (uint32_t)in_A[s * p.Gr + 2 * w + 1] : 0x7FFFu;
+                ap[w] = lo | (hi << 16);
+                col[w * kDpThreads] = ap[w];
+                col[(H + w) * kDpThreads] = 0x7FFF7FFFu;
+            }
+            col[GM * kDpThreads] = 0x7FFF7FFFu;
         }
         for (int r = 0; r < p.umax; ++r) {
             bool fresh = false;
             if (r < nq) {
                 const int q = sh.ubase[j] + r;
-                const int e = dp_place<GM>(a, p.Gr, sh.ug[q], sh.ud[q], sh.release[j], b);
-                if (e <= p.T && dp_viable16<GM>(p, sh, R2, b)) {
-                    const uint64_t key = R2 * p.cnum + dp_rank(p, b);
+                const int g = sh.ug[q], gm = g - 1;
+                const uint32_t selt = 0x4410u + (uint32_t)(gm & 1) * 0x22u;
+                const int32_t t = max((int32_t)__byte_perm(col[(gm >> 1) * kDpThreads], 0u, selt), sh.release[j]);
+                const int32_t e = t + (int32_t)sh.ud[q];
+                bool ok = e <= p.T;
+                if (ok) {
+                    // b[i] = max(a[i], min(a[i + g], e)); slots past Gr stay 0x7FFF (> any e <= T)
+                    const uint32_t e2 = (uint32_t)e * 0x10001u;
+                    const uint32_t sel = (g & 1) ? 0x5432u : 0x3210u;
+                    const uint32_t *src = col + (g >> 1) * kDpThreads;
+#pragma unroll
+                    for (int k = 0; k < H; ++k)
+                        bp[k] = __vmaxu2(ap[k], __vminu2(__byte_perm(src[k * kDpThreads], src[(k + 1) * kDpThreads], sel), e2));
+                    ok = dp_viable16p<GM>(p, sh, R2, bp);
+                }
+                if (ok) {
+                    const uint64_t key = R2 * p.cnum + dp_rank16<GM>(p, bp);
                     uint64_t h = (key * kGolden) >> (64 - p.cap_log2);
                     for (int probe = 0;; ++probe) {
                         if (probe > p.max_probe) { atomicExch(p.overflow, (unsigned)L + 1u); break; }
@@ -264,7 +329,7 @@ __global__ void __launch_bounds__(kDpThreads) k_dp_expand(const __grid_constant_
                     out_R[idx] = R2;
 #pragma unroll
                     for (int i = 0; i < GM; ++i)
-                        if (i < p.Gr) out_A[idx * p.Gr + i] = (uint16_t)b[i];
+                        if (i < p.Gr) out_A[idx * p.Gr + i] = (uint16_t)(bp[i / 2] >> (16 * (i & 1)));
                 }
             }
             par ^= 1;
