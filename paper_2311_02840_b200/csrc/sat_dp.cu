@@ -818,6 +818,7 @@ __global__ void __launch_bounds__(kDpThreads) k_dpw_pick_state(const __grid_cons
 template <int N, int G>
 __global__ void __launch_bounds__(kDpThreads) k_dpw_expand_h(const __grid_constant__ DpWideParams p) {
     constexpr int H = G / 2, W = N * H, CW = N * G + 1;     // words: per node, state, column
+    constexpr bool LEAN = N * G >= 16;   // large states: the parent stays in the column only (registers)
     __shared__ uint32_t sdgp[kDpMaxJ * 16];
     extern __shared__ uint32_t scol[];                      // [CW][kDpThreads]
     for (int i = threadIdx.x; i < p.J * 16; i += blockDim.x) sdgp[i] = p.dgp[i];
@@ -832,16 +833,16 @@ __global__ void __launch_bounds__(kDpThreads) k_dpw_expand_h(const __grid_consta
     const int nlo = __popc(Rlo);
     const int j = kk < nlo ? (int)__fns(Rlo, 0, kk + 1) : 32 + (int)__fns(Rhi, 0, kk - nlo + 1);
     const uint64_t R2 = R & ~(1ull << j);
-    uint32_t ap[W];
+    uint32_t ap[LEAN ? 1 : W];
     const uint32_t *inw = reinterpret_cast<const uint32_t *>(p.in_A + s * (uint64_t)(N * G));
     uint32_t *col = scol + threadIdx.x;
-#pragma unroll
-    for (int w = 0; w < W; ++w) ap[w] = inw[w];
 #pragma unroll
     for (int n = 0; n < N; ++n)
 #pragma unroll
         for (int k = 0; k < H; ++k) {
-            col[(n * G + k) * kDpThreads] = ap[n * H + k];
+            const uint32_t v = inw[n * H + k];
+            if constexpr (!LEAN) ap[n * H + k] = v;
+            col[(n * G + k) * kDpThreads] = v;
             col[(n * G + H + k) * kDpThreads] = 0xFFFFFFFFu;
         }
     col[(CW - 1) * kDpThreads] = 0xFFFFFFFFu;
@@ -863,7 +864,10 @@ __global__ void __launch_bounds__(kDpThreads) k_dpw_expand_h(const __grid_consta
         uint32_t area = 0;
 #pragma unroll
         for (int w = 0; w < W; ++w) {
-            bp[w] = (w / H == bn) ? nw[w % H] : ap[w];
+            if constexpr (LEAN)
+                bp[w] = (w / H == bn) ? nw[w % H] : col[((w / H) * G + w % H) * kDpThreads];
+            else
+                bp[w] = (w / H == bn) ? nw[w % H] : ap[LEAN ? 0 : w];
             area += (bp[w] & 0xFFFFu) + (bp[w] >> 16);
         }
         // viability: every remaining job can end by T; their least areas fit
@@ -979,8 +983,7 @@ static int dpw_launch_level(const DpWideParams &p, unsigned blocks, cudaStream_t
         k_dpw_expand_h<NN, GG><<<blocks, kDpThreads, smem, s>>>(p);                      \
         return cudaGetLastError() == cudaSuccess ? SAT_OK : SAT_ERR_CUDA;                 \
     }
-    // (3 and 4 nodes of 8 GPUs need 100+ registers here and ran no faster than the generic kernel)
-    SAT_DPW(2, 4) SAT_DPW(3, 4) SAT_DPW(4, 4) SAT_DPW(2, 8)
+    SAT_DPW(2, 4) SAT_DPW(3, 4) SAT_DPW(4, 4) SAT_DPW(2, 8) SAT_DPW(3, 8) SAT_DPW(4, 8)
 #undef SAT_DPW
     k_dp_expand_wide<<<blocks, kDpThreads, 0, s>>>(p);
     return cudaGetLastError() == cudaSuccess ? SAT_OK : SAT_ERR_CUDA;
