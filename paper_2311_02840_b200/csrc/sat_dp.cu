@@ -93,25 +93,6 @@ __device__ __forceinline__ int32_t dp_place(const int32_t *a, int Gr, int g, int
     return e;
 }
 
-// bound-and-prune test of a child state (R2, b): can some completion end by T?
-template <int GM>
-__device__ __forceinline__ bool dp_viable(const DpParams &p, uint64_t R2, const int32_t *b) {
-    int64_t area = 0;
-#pragma unroll
-    for (int i = 0; i < GM; ++i)
-        if (i < p.Gr) area += b[i];
-    for (int i = 0; i < p.J; ++i) {               // uniform loop: dg / minarea reads broadcast
-        if (!((R2 >> i) & 1ull)) continue;
-        area += p.minarea[i];
-        int32_t lo = 0x7fffffff;
-#pragma unroll
-        for (int k = 0; k < GM; ++k)
-            if (k < p.Gr) lo = min(lo, max(b[k], p.release[i]) + (int32_t)p.dg[i][k]);
-        if (lo > p.T) return false;
-    }
-    return area <= (int64_t)p.T * p.Gr;
-}
-
 // per-block copies of the tables the expansion indexes by job / option: the threads of a warp
 // work on different jobs, and divergent indices into the kernel parameters (constant bank)
 // serialise, while shared-memory reads of distinct words do not
@@ -137,40 +118,10 @@ __device__ __forceinline__ void dp_stage(const DpParams &p, DpShared<GM> &sh) {
     for (int x = threadIdx.x; x < nopt; x += blockDim.x) { sh.ud[x] = p.ud[x]; sh.ug[x] = p.ug[x]; }
 }
 
-// the same test on 16-bit pairs: each remaining job's earliest end is GM/2 fused add-mins
-// (VIADDMNMX.U16x2) of the packed state and its packed least durations; free times and
-// durations are <= T + 1 <= 30001 and padding 0x7FFF, so no pair sum carries
-template <int GM>
-__device__ __forceinline__ bool dp_viable16(const DpParams &p, const DpShared<GM> &sh, uint64_t R2,
-                                            const int32_t *b) {
-    constexpr int W = GM / 2;
-    uint32_t bp[W];
-    int64_t area = 0;
-#pragma unroll
-    for (int w = 0; w < W; ++w) {
-        const uint32_t lo = 2 * w < p.Gr ? (uint32_t)b[2 * w] : 0x7FFFu;
-        const uint32_t hi = 2 * w + 1 < p.Gr ? (uint32_t)b[2 * w + 1] : 0x7FFFu;
-        bp[w] = lo | (hi << 16);
-        area += (2 * w < p.Gr ? b[2 * w] : 0) + (2 * w + 1 < p.Gr ? b[2 * w + 1] : 0);
-    }
-    for (uint64_t m = R2; m; m &= m - 1) {
-        const int i = __ffsll((long long)m) - 1;
-        area += sh.minarea[i];
-        uint32_t m2 = 0xFFFFFFFFu;
-        if (p.has_release) {
-            const uint32_t r2 = (uint32_t)sh.release[i] * 0x10001u;
-#pragma unroll
-            for (int w = 0; w < W; ++w) m2 = __viaddmin_u16x2(__vmaxu2(bp[w], r2), sh.dgp[i][w], m2);
-        } else {
-#pragma unroll
-            for (int w = 0; w < W; ++w) m2 = __viaddmin_u16x2(bp[w], sh.dgp[i][w], m2);
-        }
-        if ((int32_t)min(m2 & 0xFFFFu, m2 >> 16) > p.T) return false;
-    }
-    return area <= (int64_t)p.T * p.Gr;
-}
-
-// dp_viable16 on an already packed child (slots >= Gr hold 0x7FFF, taken back out of the area)
+// bound-and-prune test of a packed child state (R2, bp): can some completion end by T?  Each
+// remaining job's earliest end is GM/2 fused add-mins (VIADDMNMX.U16x2) of the packed state and
+// its packed least durations; free times and durations are <= T + 1 <= 30001 and padding 0x7FFF,
+// so no pair sum carries.  Slots >= Gr hold 0x7FFF and are taken back out of the area.
 template <int GM>
 __device__ __forceinline__ bool dp_viable16p(const DpParams &p, const DpShared<GM> &sh, uint64_t R2,
                                              const uint32_t (&bp)[GM / 2]) {
@@ -557,7 +508,6 @@ struct DpWideParams {
     uint64_t cnum[kDpWideMaxN];             // C(T + G_n, G_n)
     int32_t ubase[kDpMaxJ], ucnt[kDpMaxJ], release[kDpMaxJ], minarea[kDpMaxJ];
     int32_t Kb;                             // binomial table row width (max G_n + 1)
-    int32_t binom_n;                        // entries of the binomial table
     int32_t nrem;                           // jobs still to place in the level being expanded
     int32_t exact;                          // 1: labelled nodes, the list scheduler's own node choice
     const uint8_t *ue;                      // [n_usable] every node the option is eligible on (exact)
@@ -1160,7 +1110,6 @@ static int dpw_prepare(const sat_problem_t *pr, int32_t T, uint64_t max_states, 
             d.binom[(size_t)n * p.Kb + k] = (uint64_t)v;
         }
     }
-    p.binom_n = (int32_t)std::min<size_t>(d.binom.size(), 0x7fffffff);
     double bits = J;
     for (int n = 0; n < N; ++n) {
         p.cnum[n] = d.binom[(size_t)(T + p.node_g[n]) * p.Kb + p.node_g[n]];
