@@ -432,9 +432,21 @@ def _batch_rows(pool, workload, remaining, get, opts, prune: bool, err, entries=
             _, crank = np.unique(cost, return_inverse=True)
             U = int(crank.max()) + 1
         jg = job.astype(np.int64) * 64 + g
-        order = np.argsort(jg * U + crank, kind="stable")
-        jgo = jg[order]
-        first = order[np.r_[True, jgo[1:] != jgo[:-1]]]
+        if J * 64 <= (1 << 16):
+            # (job, g) fits 16 bits: a stable radix sort groups it (indices ascending within a
+            # group), then per group the least cost and the first index reaching it
+            order = np.argsort(jg.astype(np.uint16), kind="stable")
+            jgo = jg[order]
+            starts = np.flatnonzero(np.r_[True, jgo[1:] != jgo[:-1]])
+            co = crank[order]
+            cmin = np.minimum.reduceat(co, starts)
+            gid = np.cumsum(np.r_[False, jgo[1:] != jgo[:-1]])
+            pos = np.where(co == cmin[gid], np.arange(len(co)), len(co))
+            first = order[np.minimum.reduceat(pos, starts)]
+        else:
+            order = np.argsort(jg * U + crank, kind="stable")
+            jgo = jg[order]
+            first = order[np.r_[True, jgo[1:] != jgo[:-1]]]
         # g kept while the cost strictly decreases: exclusive running minimum of the cost
         # ranks, restarted per job by offsetting each job above every later one
         v = crank[first].astype(np.int64) + (J - job[first]).astype(np.int64) * U
