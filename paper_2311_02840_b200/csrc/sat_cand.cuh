@@ -166,7 +166,8 @@ __device__ __forceinline__ T m16_walk(const SchedCtx<T> &c, const RecF rec, int 
     return mx;
 }
 
-template <typename T, int G, int L, bool LOAD = false, typename RecF = RecCol, bool CUT = false>
+template <typename T, int G, int L, bool LOAD = false, typename RecF = RecCol, bool CUT = false,
+          bool NOREL = false>   // NOREL: the problem has no release times (no per-placement release read)
 __device__ __forceinline__ T schedule_records(const SchedCtx<T> &c, const RecF rec,
                                              uint64_t *load = nullptr, int k0 = 0,
                                              const uint32_t *cin = nullptr, uint32_t *cout = nullptr,
@@ -210,7 +211,7 @@ __device__ __forceinline__ T schedule_records(const SchedCtx<T> &c, const RecF r
             // slot g-1 = one half of word (g-1)/2 (read as the word: no type-punned loads)
             const uint32_t selt = 0x4410u + (uint32_t)(gm & 1) * 0x22u;
             int32_t t = (int32_t)__byte_perm(st16[(gm >> 1) * 32], 0u, selt);
-            if (has_release) t = max(t, (int32_t)release[(r >> 6) & 63u]);
+            if (!NOREL && has_release) t = max(t, (int32_t)release[(r >> 6) & 63u]);
             const int32_t e = t + (int32_t)(r >> 12);
             const uint32_t e2 = (uint32_t)e * 0x10001u;
             const uint32_t sel = (g & 1) ? 0x5432u : 0x3210u;
@@ -272,7 +273,7 @@ __device__ __forceinline__ T schedule_records(const SchedCtx<T> &c, const RecF r
             SAT_ASSERT(rec_d || (int)(r >> 12) < c.n_opt);
             const T d = rec_d ? (T)(int32_t)(r >> 12) : dur[r >> 12];
             T t = st[(g - 1) * 32];
-            if (has_release) t = tmax(t, release[(r >> 6) & 63u]);
+            if (!NOREL && has_release) t = tmax(t, release[(r >> 6) & 63u]);
             const T e = t + d;
             T s[G];
 #pragma unroll
@@ -363,7 +364,7 @@ __device__ __forceinline__ T schedule_records(const SchedCtx<T> &c, const RecF r
             SAT_ASSERT(g >= 1 && g <= G && (int)((r >> 6) & 63u) < J);
             SAT_ASSERT(rec_d || (int)(r >> 12) < c.n_opt);
             const uint32_t pay = r >> 12;
-            const T rel = has_release ? release[(r >> 6) & 63u] : (T)0;
+            const T rel = (!NOREL && has_release) ? release[(r >> 6) & 63u] : (T)0;
             // node finishing the job earliest, lowest node on ties
             T be = INF;
             int bn = 0;
@@ -628,7 +629,8 @@ k_cand(CandArgs a) {
             } else {
                 decode_stream(a.seed + id, tb, rec);
             }
-            const T mx = schedule_records<T, G, L>(sc, RecCol{rec});
+            const T mx = has_release ? schedule_records<T, G, L>(sc, RecCol{rec})
+                                     : schedule_records<T, G, L, false, RecCol, false, true>(sc, RecCol{rec});
             if (key_less(mx, id, best_ms, best_ix)) {
                 best_ms = mx;
                 best_ix = id;
