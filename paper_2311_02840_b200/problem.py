@@ -362,6 +362,8 @@ class _TableView:
                 self.index = {k: i for i, k in enumerate(self.keys)}
             pos = np.fromiter(map(self.index.get, chain.from_iterable(key_rows), repeat(-1)), dtype=np.int64,
                               count=total)
+            if len(self.pos) >= 256:                          # bounded: many pools of one table
+                self.pos.clear()
             hit = self.pos[sig] = (tuple(key_rows), pos)      # the rows themselves: ids stay unique
         pos = hit[1]
         return np.where(pos >= 0, self.lat[pos], INFEASIBLE)
